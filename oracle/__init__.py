@@ -1,0 +1,247 @@
+"""ORACLE -- TEST INFRASTRUCTURE ONLY.
+
+A plain, slow, obviously-correct FP64 CPU implementation of what the CUDA path computes, written from
+PAPER.md (arXiv 2204.13241).  Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` leg may import it.  It shares no code with
+``paper_2204_13241_b200`` (neither imports the other); both consume only ``xpcs_inputs``.
+
+Contents (each function cites the passage it follows):
+  * liboracle.so (oracle.c): the direct sum Eq.(7)/(8) and the pair sum Eq.(2), FP64, OpenMP over q.
+  * lattice_q       -- reciprocal-lattice q = (2 pi / L) (m0 + h ma + k mb), Algorithm 1 step 1.
+  * ewald_q         -- Ewald-sphere detector q = k (u - z), Eq.(1) + Fig. 5 (reading R4).
+  * g2              -- Eq.(14) literal estimator (reading R6).
+  * lattice_bins / radial_bins / shell_mean / structure_factor_shells -- ring average, Eq.(12).
+  * xsvs_beta       -- Eq.(15) + Eq.(17), per-snapshot then averaged.
+Every function is pinned by tests/test_oracle_pins.py (no function here is "parity unpinned").
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c (gcc -O2 -fopenmp, no fast-math)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-fno-fast-math",
+                               "-ffp-contract=off", _SRC, "-o", _LIB, "-lm"])
+    return _LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        dp = ctypes.POINTER(ctypes.c_double)
+        i64 = ctypes.c_int64
+        L.oracle_amplitude.argtypes = [dp, i64, dp, dp, i64, ctypes.c_double, dp, dp]
+        L.oracle_intensity.argtypes = [dp, i64, dp, dp, i64, i64, ctypes.c_double, dp]
+        L.oracle_pair_sum.argtypes = [dp, i64, dp, dp, i64, ctypes.c_double, dp]
+        L.oracle_max_threads.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def threads() -> int:
+    return int(lib().oracle_max_threads())
+
+
+def _d(a):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a, a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _f(f):
+    if f is None:
+        return None, None
+    return _d(f)
+
+
+# ----------------------------------------------------------------------------------------------
+# q geometry
+# ----------------------------------------------------------------------------------------------
+def lattice_q(L, h0, n_h, k0, n_k, m0=(0, 0, 0), ma=(1, 0, 0), mb=(0, 1, 0)) -> np.ndarray:
+    """Algorithm 1 step 1: q on the reciprocal lattice of the cubic box, components
+    integer multiples of 2 pi / L.  Pixel (ih, ik) -> h = h0 + ih, k = k0 + ik,
+    q = (2 pi / L) (m0 + h ma + k mb), pixel index ih * n_k + ik.  FP64."""
+    h = np.arange(h0, h0 + n_h, dtype=np.float64)[:, None, None]
+    k = np.arange(k0, k0 + n_k, dtype=np.float64)[None, :, None]
+    m = (np.asarray(m0, np.float64)[None, None, :] + h * np.asarray(ma, np.float64)[None, None, :]
+         + k * np.asarray(mb, np.float64)[None, None, :])
+    return (2.0 * np.pi / L) * m.reshape(-1, 3)
+
+
+def plane_grid(n):
+    """The configs' detector plane: h, k in [-n/2, n/2 - 1], l = 0 (reading R7)."""
+    return dict(h0=-(n // 2), n_h=n, k0=-(n // 2), n_k=n)
+
+
+def ewald_q(wavelength, npx, npy, pitch) -> np.ndarray:
+    """Detector pixels on the Ewald sphere (Eq.(1): |k_i| = |k_f| = 2 pi / lambda,
+    q = k_f - k_i; Fig. 5 'spherical slice ... to keep |k_f| = |k_i|').
+    Reading R4: k_i = k z, pixel (i, j) at lon-lat angles
+    psi_x = (i - (npx-1)/2) pitch, psi_y = (j - (npy-1)/2) pitch,
+    u = (sin psi_x cos psi_y, sin psi_y, cos psi_x cos psi_y), q = k (u - z).  FP64, index i*npy + j."""
+    k = 2.0 * np.pi / wavelength
+    px = (np.arange(npx, dtype=np.float64) - (npx - 1) / 2.0) * pitch
+    py = (np.arange(npy, dtype=np.float64) - (npy - 1) / 2.0) * pitch
+    PX, PY = np.meshgrid(px, py, indexing="ij")
+    u = np.stack([np.sin(PX) * np.cos(PY), np.sin(PY), np.cos(PX) * np.cos(PY)], -1)
+    q = k * (u - np.array([0.0, 0.0, 1.0]))
+    return q.reshape(-1, 3)
+
+
+# ----------------------------------------------------------------------------------------------
+# the direct method
+# ----------------------------------------------------------------------------------------------
+def amplitude(pos, f, q, L):
+    """Eq.(7): complex p^e(q) for one frame [N][3] (positions promoted to FP64)."""
+    pos, pp = _d(pos)
+    N = pos.shape[0]
+    f, fp = _f(f)
+    q, qp = _d(q)
+    n_q = q.shape[0]
+    re = np.zeros(n_q)
+    im = np.zeros(n_q)
+    lib().oracle_amplitude(pp, N, fp, qp, n_q, float(L), _d(re)[1], _d(im)[1])
+    return re + 1j * im
+
+
+def intensity(pos, f, q, L):
+    """Eq.(8) I(q,t) = |p^e(q,t)|^2 for positions [T][N][3] (or [N][3]); returns [T][n_q]."""
+    pos = np.asarray(pos)
+    if pos.ndim == 2:
+        pos = pos[None]
+    pos, pp = _d(pos)
+    T, N = pos.shape[0], pos.shape[1]
+    f, fp = _f(f)
+    q, qp = _d(q)
+    n_q = q.shape[0]
+    out = np.zeros((T, n_q))
+    lib().oracle_intensity(pp, N, fp, qp, n_q, T, float(L), out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    return out
+
+
+def pair_sum_intensity(pos, f, q, L):
+    """Eq.(2): I(q) by the O(N^2) double sum over atom pairs (tiny N only)."""
+    pos, pp = _d(pos)
+    N = pos.shape[0]
+    f, fp = _f(f)
+    q, qp = _d(q)
+    n_q = q.shape[0]
+    out = np.zeros(n_q)
+    lib().oracle_pair_sum(pp, N, fp, qp, n_q, float(L), out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    return out
+
+
+# ----------------------------------------------------------------------------------------------
+# speckle statistics
+# ----------------------------------------------------------------------------------------------
+def g2(I, lags):
+    """Eq.(14), literal estimator (R6):
+    num(tau) = 1/(T - tau) sum_{t=0}^{T-1-tau} I_t I_{t+tau},  den = ((1/T) sum_t I_t)^2,
+    g2 = num / den; NaN where den == 0.  I [T][n_q] -> [n_lags][n_q] FP64."""
+    I = np.asarray(I, dtype=np.float64)
+    T = I.shape[0]
+    mean = I.sum(0) / T
+    den = mean * mean
+    out = np.empty((len(lags), I.shape[1]))
+    for i, tau in enumerate(lags):
+        num = (I[: T - tau] * I[tau:]).sum(0) / (T - tau)
+        with np.errstate(divide="ignore", invalid="ignore"):
+            out[i] = np.where(den > 0, num / np.where(den > 0, den, 1.0), np.nan)
+    return out
+
+
+def lattice_bins(n, n_bins=32, h0=None, k0=None):
+    """q-ring membership q - dq/2 <= |q| < q + dq/2 on the n x n lattice plane,
+    in exact integer arithmetic (R8): radius unit w = n / (2 n_bins) pixels,
+    b = floor(sqrt(h^2 + k^2) / w) = isqrt(h^2 + k^2) // w; q = 0 and h^2 + k^2 >= (n/2)^2 excluded (-1)."""
+    h0 = -(n // 2) if h0 is None else h0
+    k0 = -(n // 2) if k0 is None else k0
+    w = n // (2 * n_bins)
+    assert w * 2 * n_bins == n
+    out = np.full(n * n, -1, dtype=np.int32)
+    lim = (n // 2) ** 2
+    for ih in range(n):
+        h = h0 + ih
+        for ik in range(n):
+            k = k0 + ik
+            r2 = h * h + k * k
+            if r2 == 0 or r2 >= lim:
+                continue
+            out[ih * n + ik] = math.isqrt(r2) // w
+    return out
+
+
+def radial_bins(q, q_max, n_bins=32):
+    """Shells of |q| for an explicit q list (config 4): b = floor(|q| / q_max * n_bins) in FP64 from the
+    (fp32) q array; |q| >= q_max and q = 0 excluded (-1)."""
+    q = np.asarray(q, dtype=np.float64)
+    r = np.sqrt((q * q).sum(1))
+    b = np.floor(r / q_max * n_bins).astype(np.int64)
+    b[(r >= q_max) | (r == 0.0)] = -1
+    return b.astype(np.int32)
+
+
+def shell_mean(values, bins, n_bins):
+    """Average over all detector pixels in each ring, per row; non-finite values
+    (e.g. g2 of a zero-mean pixel) are excluded; empty ring -> NaN.  values [rows][n_q] -> [rows][n_bins]."""
+    v = np.asarray(values, dtype=np.float64)
+    if v.ndim == 1:
+        v = v[None]
+    out = np.full((v.shape[0], n_bins), np.nan)
+    for b in range(n_bins):
+        sel = v[:, bins == b]
+        for r in range(v.shape[0]):
+            x = sel[r][np.isfinite(sel[r])]
+            if x.size:
+                out[r, b] = x.sum() / x.size
+    return out
+
+
+def structure_factor_shells(I, f, N, bins, n_bins):
+    """Eq.(12)/(13): S(q,t) = I(q,t) / sum_j f_j^2, ring-averaged per frame -> [T][n_bins]."""
+    s2 = float(N) if f is None else float(np.sum(np.asarray(f, np.float64) ** 2))
+    return shell_mean(I, bins, n_bins) / s2
+
+
+def xsvs_beta(I, bins, n_bins, windows, per_window=False):
+    """Optical contrast vs exposure (XSVS).  Eq.(15) as a discrete, unnormalised
+    sum over non-overlapping windows of W frames aligned at t = 0 (remainder dropped):
+        I_W(q, s) = sum_{t = sW}^{sW + W - 1} I(q, t),  s = 0 .. floor(T/W) - 1;
+    Eq.(17) per snapshot s and ring b with the population variance
+        beta_{W,b,s} = (<I_W^2>_b - <I_W>_b^2) / <I_W>_b^2,
+    then averaged over snapshots.  Returns [n_windows][n_bins] FP64 (NaN: empty ring)."""
+    I = np.asarray(I, dtype=np.float64)
+    T = I.shape[0]
+    out = np.full((len(windows), n_bins), np.nan)
+    detail = []
+    for wi, W in enumerate(windows):
+        S = T // W
+        IW = I[: S * W].reshape(S, W, -1).sum(1)          # [S][n_q]
+        row = []
+        for b in range(n_bins):
+            x = IW[:, bins == b]                           # [S][m0]
+            m0 = x.shape[1]
+            if m0 == 0:
+                row.append(None)
+                continue
+            m1 = x.sum(1)
+            m2 = (x * x).sum(1)
+            mean = m1 / m0
+            beta_s = (m2 / m0 - mean * mean) / (mean * mean)
+            out[wi, b] = beta_s.sum() / S
+            row.append(beta_s)
+        detail.append(row)
+    return (out, detail) if per_window else out

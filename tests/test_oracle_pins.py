@@ -1,0 +1,336 @@
+"""Pins of the FP64 oracle against what the paper and the mathematics fix (CPU only).
+
+Each test names the passage it checks.  None of them re-types the oracle's formula: they use the
+O(N^2) pair sum (Eq. 2), closed forms (single atoms, forward limit, Bragg peaks of perfect crystals,
+the ideal-gas expectation with the box shape transform, the Brownian g2 and XSVS laws), invariants
+(inversion, PBC shift, permutation) and numbers printed in the paper (tests/golden/).
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import xpcs_inputs as xi
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _gold(name):
+    with open(os.path.join(GOLD, name)) as fh:
+        return json.load(fh)
+
+
+def _hkl_q(L, hkl):
+    return (2 * np.pi / L) * np.asarray(hkl, dtype=np.float64)
+
+
+# ------------------------------------------------------------------ worked examples (golden)
+@pytest.mark.parametrize("case", ["single_atom_origin", "single_atom_half_box"])
+def test_golden_amplitude_sign(case):
+    g = _gold("spec_examples.json")[case]
+    A = oracle.amplitude(np.array(g["pos"]), np.array(g["f"]), _hkl_q(g["L"], g["hkl"]), g["L"])
+    np.testing.assert_allclose(A.real, g["amplitude_re"], atol=1e-12)
+    np.testing.assert_allclose(A.imag, g["amplitude_im"], atol=1e-12)
+
+
+@pytest.mark.parametrize("case", ["one_atom_f", "forward"])
+def test_golden_intensity(case):
+    g = _gold("spec_examples.json")[case]
+    I = oracle.intensity(np.array(g["pos"]), np.array(g["f"]), _hkl_q(g["L"], g["hkl"]), g["L"])[0]
+    np.testing.assert_allclose(I, g["intensity"], rtol=1e-12)
+
+
+def test_paper_q_point_is_a_lattice_vector():
+    """PAPER.md:414 prints q = (0, 1.481, -1.164) A^-1 for the L = 59.19 A box;
+    Algorithm 1 only allows reciprocal-lattice q: lattice_q must reproduce the printed
+    point as (2 pi / L)(0, 14, -11) to the printed 3 decimals."""
+    g = _gold("paper_parameters.json")
+    L = g["box_L_angstrom"]["value"]
+    hkl = g["q_point_fig3"]["hkl"]
+    q = oracle.lattice_q(L, h0=hkl[1], n_h=1, k0=hkl[2], n_k=1, m0=(hkl[0], 0, 0), ma=(0, 1, 0), mb=(0, 0, 1))[0]
+    np.testing.assert_allclose(q, g["q_point_fig3"]["value"], atol=6e-3)
+
+
+def test_two_atoms_closed_form():
+    """Eq.(2) with N = 2: I = f1^2 + f2^2 + 2 f1 f2 cos(q . (r1 - r2))."""
+    L = 9.0
+    pos = np.array([[1.1, 2.2, 3.3], [7.7, 0.4, 5.9]])
+    f = np.array([1.5, 0.7])
+    q = oracle.lattice_q(L, -5, 11, -5, 11, m0=(2, 0, 0), ma=(0, 1, 0), mb=(0, 0, 1))
+    d = pos[0] - pos[1]
+    expect = f[0] ** 2 + f[1] ** 2 + 2 * f[0] * f[1] * np.cos(q @ d)
+    np.testing.assert_allclose(oracle.intensity(pos, f, q, L)[0], expect, rtol=1e-12, atol=1e-12)
+
+
+# ------------------------------------------------------------------ brute force
+@pytest.mark.parametrize("N,two", [(8, False), (50, True), (100, True)])
+def test_direct_equals_pair_sum(N, two):
+    """Single sum Eq.(7)+(8) == O(N^2) pair sum Eq.(2) to 1e-10 relative on all lattice q, |q| <= 3
+    (SPEC.md:596 acceptance #1; PAPER.md:280-284 derivation)."""
+    L = 6.0
+    rng = np.random.default_rng(N)
+    pos = rng.uniform(0, L, (N, 3))
+    f = np.where(np.arange(N) % 2 == 1, 2.0, 1.0) if two else np.ones(N)
+    q = np.concatenate([oracle.lattice_q(L, -3, 7, -3, 7, m0=(l, 0, 0), ma=(0, 1, 0), mb=(0, 0, 1))
+                        for l in range(-3, 4)])
+    q = q[np.linalg.norm(q, axis=1) <= 3.0]
+    a = oracle.intensity(pos, f, q, L)[0]
+    b = oracle.pair_sum_intensity(pos, f, q, L)
+    scale = max(1.0, float(np.max(np.abs(b))))
+    assert np.max(np.abs(a - b)) <= 1e-10 * scale
+
+
+def test_forward_limit_and_inversion():
+    """I(0) = (sum f)^2; I(q) = I(-q) (conjugate symmetry of Eq. 7)."""
+    cfg = xi.scaled(xi.CONFIGS["c3"], N=600, T=1)
+    pos = xi.positions(cfg)[0]
+    f = xi.form_factors(cfg).astype(np.float64)
+    n = 16
+    q = oracle.lattice_q(cfg.L, **oracle.plane_grid(n))
+    I = oracle.intensity(pos, f, q, cfg.L)[0].reshape(n, n)
+    assert abs(I[n // 2, n // 2] - f.sum() ** 2) <= 1e-12 * f.sum() ** 2
+    inner = I[1:, 1:]                       # h, k in [-n/2+1, n/2-1] has its mirror inside the grid
+    np.testing.assert_allclose(inner, inner[::-1, ::-1], rtol=1e-12, atol=1e-9)
+
+
+def test_pbc_shift_and_permutation_invariance():
+    """Lattice q: any periodic image gives the same I -> a rigid shift of all atoms,
+    re-wrapped, leaves I unchanged; so does relabelling atoms."""
+    L = 8.0
+    rng = np.random.default_rng(7)
+    pos = rng.uniform(0, L, (300, 3))
+    f = rng.uniform(0.5, 2.0, 300)
+    q = oracle.lattice_q(L, -6, 12, -6, 12, m0=(3, 0, 0), ma=(0, 1, 0), mb=(0, 0, 1))
+    I0 = oracle.intensity(pos, f, q, L)[0]
+    shifted = pos + np.array([3.7, -12.25, 101.5])      # the oracle wraps into [0, L)
+    I1 = oracle.intensity(shifted, f, q, L)[0]
+    np.testing.assert_allclose(I1, I0, rtol=1e-9, atol=1e-9 * 300)
+    perm = rng.permutation(300)
+    I2 = oracle.intensity(pos[perm], f[perm], q, L)[0]
+    np.testing.assert_allclose(I2, I0, rtol=1e-11, atol=1e-10)
+
+
+# ------------------------------------------------------------------ Bragg peaks (closed form)
+@pytest.mark.parametrize("kind,n_cells,L,n,period,rule", [
+    ("sc", 10, 10.0, 64, 10, "all"),           # config 1's own size: SC 10^3, L = 10
+    ("fcc", 6, 12.0, 64, 12, "all"),           # FCC: h, k in 2 n_c Z (l = 0)
+    ("bcc", 8, 20.0, 64, 8, "even"),           # BCC: H + K even, H = h / n_c
+])
+def test_bragg_peaks(kind, n_cells, L, n, period, rule):
+    """Perfect crystal, f = 1: geometric lattice sums give I = N^2 on the reciprocal lattice of the
+    crystal and 0 elsewhere (Eq. 7 as a lattice sum; PAPER.md:285-288 reciprocal lattice)."""
+    pos = xi.crystal(kind, n_cells, L)
+    N = pos.shape[0]
+    q = oracle.lattice_q(L, **oracle.plane_grid(n))
+    I = oracle.intensity(pos, None, q, L)[0].reshape(n, n)
+    h = np.arange(-n // 2, n // 2)
+    H, K = np.meshgrid(h, h, indexing="ij")
+    peak = (H % period == 0) & (K % period == 0)
+    if rule == "even":
+        peak &= ((H // period + K // period) % 2 == 0)
+    assert peak.sum() > 4
+    np.testing.assert_allclose(I[peak], float(N) ** 2, rtol=1e-12)
+    assert np.max(I[~peak]) < 1e-6 * N
+
+
+# ------------------------------------------------------------------ ideal-gas statistics
+def test_random_positions_plane_mean():
+    """Uniform random positions, lattice q != 0: E[I] = sum f^2 (Eq. 12 with S = 1 for an ideal gas);
+    plane mean of I / sum f^2 = 1 +- 5/sqrt(n_q/2) (pairs +-q identical)."""
+    cfg = xi.scaled(xi.CONFIGS["c3"], N=2000, T=1)
+    pos = xi.positions(cfg)[0]
+    f = xi.form_factors(cfg).astype(np.float64)
+    n = 48
+    q = oracle.lattice_q(cfg.L, **oracle.plane_grid(n))
+    I = oracle.intensity(pos, f, q, cfg.L)[0]
+    nz = np.linalg.norm(q, axis=1) > 0
+    m = I[nz].mean() / np.sum(f ** 2)
+    assert abs(m - 1.0) < 5.0 / np.sqrt(nz.sum() / 2)
+
+
+def test_random_positions_off_lattice_expectation():
+    """Off-lattice q (R3): for iid uniform atoms in [0, L)^3,
+    E[I(q)] = S2 + (S1^2 - S2) prod_c sinc^2(q_c L / 2)  (characteristic function of U[0, L)),
+    checked at 5 sigma over independent frames, including near-forward q where the box term dominates."""
+    N, L, frames = 60, 5.0, 400
+    f = np.where(np.arange(N) % 2 == 1, 2.0, 1.0)
+    S1, S2 = f.sum(), (f ** 2).sum()
+    q = np.array([[0.3, 0.1, -0.2], [0.9, 0.0, 0.0], [1.7, -0.6, 0.4], [0.05, 0.05, 0.05], [2.5, 2.5, -1.0]])
+    Is = np.stack([oracle.intensity(xi.uniform_frame(1000 + s, N, L), f, q, L)[0] for s in range(frames)])
+    sinc2 = np.prod(np.sinc(q * L / 2 / np.pi) ** 2, axis=1)   # np.sinc(x) = sin(pi x)/(pi x)
+    expect = S2 + (S1 ** 2 - S2) * sinc2
+    sigma = Is.std(0) / np.sqrt(frames)
+    assert np.all(np.abs(Is.mean(0) - expect) < 5 * sigma + 1e-9)
+
+
+def test_contrast_of_single_snapshot():
+    """Fully coherent speckle: beta = 1, precisely beta0 = 1 - S4/S2^2 for N random
+    phasors (SPEC 8(c) 'intensity statistics'); XSVS W = 1 on one frame over large rings, 5 sigma."""
+    cfg = xi.scaled(xi.CONFIGS["c3"], N=1500, T=1)
+    pos = xi.positions(cfg)
+    f = xi.form_factors(cfg).astype(np.float64)
+    n = 64
+    q = oracle.lattice_q(cfg.L, **oracle.plane_grid(n))
+    I = oracle.intensity(pos, f, q, cfg.L)
+    bins = oracle.lattice_bins(n, n_bins=4)
+    beta = oracle.xsvs_beta(I, bins, 4, [1])[0]
+    beta0 = 1 - np.sum(f ** 4) / np.sum(f ** 2) ** 2
+    for b in (2, 3):
+        n_eff = np.sum(bins == b) / 2
+        # exponential intensities: var of the sample contrast ~ 8 / n_eff (4th moment of Exp)
+        assert abs(beta[b] - beta0 * (1 - 2 / n_eff)) < 5 * np.sqrt(8.0 / n_eff), (b, beta[b])
+
+
+# ------------------------------------------------------------------ Brownian dynamics: g2 and XSVS
+def _brownian(N, L, T, D, dt, seed):
+    cfg = xi.Config("pin", N, L, T, D, dt, 0, True, "f64", (), (), seed=seed)
+    return xi.positions(cfg), xi.form_factors(cfg).astype(np.float64)
+
+
+def test_g2_brownian_numerator_and_denominator():
+    """Siegert + diffusion (Eq. 24 + Eq. 25): for independent Brownian particles on
+    lattice q != 0, E[I_t I_{t+tau}] = S2^2 + phi^2 (S2^2 - S4), phi = exp(-D q^2 tau dt), i.e.
+    g2 - 1 = beta0 exp(-2 D q^2 tau).  The literal Eq.(14) ratio is biased at finite T (R6),
+    so the unbiased numerator (per shell, 5 sigma) and the denominator mean I / S2 = 1 are pinned."""
+    N, L, T, D, dt = 300, 7.0, 500, 0.05, 1.0
+    pos, f = _brownian(N, L, T, D, dt, seed=4242)
+    n = 16
+    q = oracle.lattice_q(L, **oracle.plane_grid(n))
+    I = oracle.intensity(pos, f, q, L)
+    S2, S4 = np.sum(f ** 2), np.sum(f ** 4)
+    beta0 = 1 - S4 / S2 ** 2
+    lags = [1, 2, 4, 8]
+    bins = oracle.lattice_bins(n, n_bins=4)
+    q2 = (q ** 2).sum(1)
+    # numerator = g2 * den  (use oracle.g2 so the function under test is exercised)
+    den = (I.mean(0)) ** 2
+    G = oracle.g2(I, lags)
+    num = G * den[None, :]
+    worst = 0.0
+    for li, tau in enumerate(lags):
+        for b in range(4):
+            sel = bins == b
+            v = num[li, sel] / S2 ** 2 - 1.0
+            pred = beta0 * np.mean(np.exp(-2 * D * q2[sel] * tau * dt))
+            sigma = v.std() / np.sqrt(sel.sum() / 2)
+            z = abs(v.mean() - pred) / sigma
+            worst = max(worst, z)
+    assert worst < 5.0, worst
+    m = I[:, bins >= 0].mean() / S2
+    assert abs(m - 1) < 5 * I[:, bins >= 0].std() / S2 / np.sqrt(T * (bins >= 0).sum() / 2 / 10)
+
+
+def test_xsvs_brownian_closed_form():
+    """XSVS contrast vs exposure (Eq. 28) in discrete form for diffusion:
+    beta_W = beta0 mean_q[(W + 2 S_W(x)) / W^2], x = exp(-2 D q^2 dt),
+    S_W(x) = x (W (1 - x) - 1 + x^W) / (1 - x)^2; literal estimator on fast rings, 5 sigma of the snapshot spread."""
+    N, L, T, D, dt = 400, 12.0, 240, 0.05, 0.1
+    pos, f = _brownian(N, L, T, D, dt, seed=777)
+    n = 48
+    q = oracle.lattice_q(L, **oracle.plane_grid(n))
+    I = oracle.intensity(pos, f, q, L)
+    nb = 4
+    bins = oracle.lattice_bins(n, n_bins=nb)
+    windows = [1, 2, 4, 8, 16]
+    beta, detail = oracle.xsvs_beta(I, bins, nb, windows, per_window=True)
+    S2, S4 = np.sum(f ** 2), np.sum(f ** 4)
+    beta0 = 1 - S4 / S2 ** 2
+    q2 = (q ** 2).sum(1)
+    for b in (2, 3):
+        sel = bins == b
+        x = np.exp(-2 * D * q2[sel] * dt)
+        assert np.min(2 * D * q2[sel] * dt * T) >= 20
+        for wi, W in enumerate(windows):
+            SW = x * (W * (1 - x) - 1 + x ** W) / (1 - x) ** 2
+            pred = beta0 * np.mean((W + 2 * SW) / W ** 2)
+            n_eff = sel.sum() / 2
+            pred *= (1 - 2 / n_eff)                    # finite-ring bias of the literal estimator
+            bs = detail[wi][b]                         # per-snapshot contrasts (S of them)
+            sigma = bs.std() / np.sqrt(len(bs)) if len(bs) > 1 else 0.1 * pred
+            assert abs(beta[wi, b] - pred) < max(5 * sigma, 0.03 * pred), (b, W, beta[wi, b], pred, sigma)
+
+
+# ------------------------------------------------------------------ reductions: invariants
+def test_g2_invariants():
+    """Eq.(14): constant series -> g2 = 1; scale invariance; time reversal symmetry of the
+    numerator; zero-mean pixel -> NaN."""
+    rng = np.random.default_rng(3)
+    I = rng.exponential(1.0, (60, 40))
+    I[:, 5] = 3.0
+    I[:, 6] = 0.0
+    lags = [0, 1, 5, 20]
+    G = oracle.g2(I, lags)
+    np.testing.assert_allclose(G[:, 5], 1.0, rtol=1e-14)
+    assert np.all(np.isnan(G[:, 6]))
+    np.testing.assert_allclose(oracle.g2(7.5 * I, lags), G, rtol=1e-13)
+    np.testing.assert_allclose(oracle.g2(I[::-1], lags), G, rtol=1e-13)
+    # tau = 0 gives beta0 + 1 = <I^2>/<I>^2 (Eq. 19)
+    m = I[:, :5].mean(0)
+    np.testing.assert_allclose(G[0, :5], (I[:, :5] ** 2).mean(0) / m ** 2, rtol=1e-13)
+
+
+def test_xsvs_invariants():
+    """Eq.(15)/(17): W = 1 on a static series equals the single-frame contrast for every W;
+    constant field -> beta = 0; Exp(1) pixels -> 1 +- 5 sigma; empty ring -> NaN."""
+    rng = np.random.default_rng(11)
+    n_q = 4000
+    bins = (np.arange(n_q) % 3).astype(np.int32)
+    bins[:10] = -1
+    frame = rng.exponential(2.0, n_q)
+    frame[bins == 2] = 5.0
+    I = np.repeat(frame[None], 16, 0)
+    beta = oracle.xsvs_beta(I, bins, 4, [1, 2, 4, 16])
+    np.testing.assert_allclose(beta[:, 0], beta[0, 0], rtol=1e-12)
+    np.testing.assert_allclose(beta[:, 2], 0.0, atol=1e-14)
+    assert np.all(np.isnan(beta[:, 3]))
+    m = np.sum(bins == 0)
+    assert abs(beta[0, 0] - 1) < 5 * np.sqrt(8.0 / m)
+
+
+def test_lattice_bins():
+    """Rings q - dq/2 <= |q| < q + dq/2: integer bins agree with a float evaluation away
+    from bin edges, are symmetric under q -> -q, and exclude q = 0 and the corners."""
+    for n in (64, 256):
+        b = oracle.lattice_bins(n)
+        h = np.arange(-n // 2, n // 2)
+        H, K = np.meshgrid(h, h, indexing="ij")
+        r = np.sqrt(H ** 2 + K ** 2).ravel()
+        w = n / 64
+        fb = np.floor(r / w)
+        ok = (r > 0) & (r < n / 2)
+        assert np.all(b[~ok] == -1)
+        assert np.all(b[ok] == fb[ok])
+        B = b.reshape(n, n)
+        np.testing.assert_array_equal(B[1:, 1:], B[1:, 1:][::-1, ::-1])
+        assert b.max() == 31
+
+
+def test_ewald_geometry():
+    """Eq.(1): elastic scattering, |k_f| = |k_i| = 2 pi / lambda, so every detector q
+    satisfies |q + k z| = k; the centre of an even detector is 4 half-pixels off the beam; the corner
+    of the config-4 detector reaches q_max = 8 pi / sigma (R4)."""
+    lam, pitch, npx = xi.EWALD_WAVELENGTH_SIGMA, xi.EWALD_PITCH_RAD, 64
+    q = oracle.ewald_q(lam, npx, npx, pitch * 16)
+    k = 2 * np.pi / lam
+    kf = q + np.array([0, 0, k])
+    np.testing.assert_allclose(np.linalg.norm(kf, axis=1), k, rtol=1e-13)
+    assert np.all(q[:, 2] <= 0)
+    qf = oracle.ewald_q(lam, 1024, 1024, pitch)
+    r = np.linalg.norm(qf, axis=1)
+    assert abs(r.max() - xi.EWALD_QMAX) / xi.EWALD_QMAX < 2e-3
+    c = r.reshape(1024, 1024)[511, 511]
+    np.testing.assert_allclose(c, 2 * k * np.sin(np.arccos(np.cos(pitch / 2) ** 2) / 2), rtol=1e-9)
+
+
+def test_shell_mean_and_structure_factor():
+    """Eq.(12)-(13): S = I / sum f^2 ring-averaged; NaNs excluded; empty ring NaN."""
+    I = np.array([[1.0, 2.0, 3.0, np.nan, 10.0], [4.0, 4.0, 4.0, 4.0, 4.0]])
+    bins = np.array([0, 0, 1, 1, -1], np.int32)
+    out = oracle.shell_mean(I, bins, 3)
+    np.testing.assert_allclose(out[:, :2], [[1.5, 3.0], [4.0, 4.0]])
+    assert np.all(np.isnan(out[:, 2]))
+    S = oracle.structure_factor_shells(I, np.array([1.0, 2.0]), 2, bins, 3)
+    np.testing.assert_allclose(S[:, :2], out[:, :2] / 5.0)
