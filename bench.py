@@ -1,0 +1,307 @@
+#!/usr/bin/env python
+"""Benchmark of the direct-method hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--engine auto|simt|tensor]
+    python bench.py --impl reference ...       # the FP64 CPU oracle on a bounded sample (the reference arm)
+
+A "step" = one pass of the whole hot path over one batch of synthetic input: frame staging, I(q,t) for every
+pixel of every frame, g2 for all lags, ring-averaged S(q,t) and g2, XSVS contrast for every exposure window.
+Default workload = BASELINE.json configs[1] ("c2": N = 32000, 100 Brownian frames, 256 x 256 lattice plane,
+g2 tau = 1..50).  Metric: atom.q pairs/s for I(q,t) (whole job, all ranks).  Multi-GPU = weak scaling: every
+rank processes its own independent trajectory (no data-path collective).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import xpcs_inputs as xi  # noqa: E402
+
+METRIC = "atom·q pairs/s for I(q,t) at 1 B200; fraction of FP32/SFU or tensor roofline"
+UNIT = "pairs/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index=0):
+        self.rows = []
+        self.proc = None
+        self.index = index
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[4:8]) if v.lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws > 1:
+        import torch.distributed as dist
+        rank = int(os.environ["RANK"])
+        local = int(os.environ.get("LOCAL_RANK", rank))
+        return ws, rank, local, dist
+    return 1, 0, 0, None
+
+
+def run_reference(args):
+    """The reference arm: the FP64 CPU oracle (as it stands) on a bounded sample of the same workload."""
+    ws, rank, _, dist = _dist()
+    if rank != 0:
+        return 0
+    import oracle
+    cfg = xi.CONFIGS[args.config]
+    pos = xi.positions(cfg, frames=1)[0]
+    f = xi.form_factors(cfg).astype(np.float64) if cfg.two_species else None
+    if cfg.n_plane:
+        q = oracle.lattice_q(cfg.L, **oracle.plane_grid(cfg.n_plane))
+    else:
+        q = oracle.ewald_q(xi.EWALD_WAVELENGTH_SIGMA, cfg.detector, cfg.detector, xi.EWALD_PITCH_RAD).astype(np.float32)
+    n_pix = min(q.shape[0], args.ref_pixels)
+    pix = xi.pixel_subset(q.shape[0], n_pix, 1234)
+    qs = q[pix].astype(np.float64)
+    oracle.intensity(pos, f, qs[:64], cfg.L)            # load + warm
+    times = []
+    for it in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        oracle.intensity(pos, f, qs, cfg.L)
+        dt = time.perf_counter() - t0
+        if it >= args.warmup:
+            times.append(dt)
+    pairs = cfg.N * n_pix
+    ms = 1e3 * float(np.mean(times))
+    val = pairs / (ms / 1e3)
+    sample = f"{args.config} frame 0, {n_pix} seeded pixels x {cfg.N} atoms = {pairs:.3g} pairs per step"
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "N": cfg.N, "n_q": int(q.shape[0]), "frames": cfg.T},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": oracle.threads(), "kind": "oracle", "sample": sample},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline(cfg, budget_s):
+    """Oracle timed on the host cores on a bounded sample (rank 0, N = 1 only)."""
+    import oracle
+    pos = xi.positions(cfg, frames=1)[0]
+    f = xi.form_factors(cfg).astype(np.float64) if cfg.two_species else None
+    if cfg.n_plane:
+        q = oracle.lattice_q(cfg.L, **oracle.plane_grid(cfg.n_plane))
+    else:
+        q = oracle.ewald_q(xi.EWALD_WAVELENGTH_SIGMA, cfg.detector, cfg.detector, xi.EWALD_PITCH_RAD).astype(np.float32)
+    qs = q.astype(np.float64)
+    # calibrate on 256 pixels, then size the sample to ~budget_s
+    t0 = time.perf_counter()
+    oracle.intensity(pos, f, qs[:256], cfg.L)
+    per_pix = (time.perf_counter() - t0) / 256
+    n_pix = int(max(256, min(q.shape[0], budget_s / max(per_pix, 1e-9))))
+    pix = xi.pixel_subset(q.shape[0], n_pix, 99)
+    t0 = time.perf_counter()
+    oracle.intensity(pos, f, qs[pix], cfg.L)
+    dt = time.perf_counter() - t0
+    pairs = cfg.N * len(pix)
+    return {"value": pairs / dt, "unit": UNIT, "cores": oracle.threads(), "kind": "oracle",
+            "sample": f"{cfg.name} frame 0, {len(pix)} seeded pixels x {cfg.N} atoms ({pairs:.3g} pairs, {dt:.1f} s)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(xi.CONFIGS))
+    ap.add_argument("--engine", default="auto", choices=["auto", "simt", "tensor"])
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--ref-pixels", type=int, default=4096)
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import paper_2204_13241_b200 as xp
+    from paper_2204_13241_b200 import pipeline
+
+    ws, rank, local, dist = _dist()
+    torch.cuda.set_device(local)
+    if dist is not None:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    cfg = xi.CONFIGS[args.config]
+    # weak scaling: each rank its own independent trajectory
+    cfg_r = xi.scaled(cfg, seed=cfg.seed + 1000 * rank) if rank else cfg
+    pos_h = xi.positions(cfg_r)
+    f_h = xi.form_factors(cfg_r) if cfg.two_species else None
+    engine = {"auto": xp.ENGINE_AUTO, "simt": xp.ENGINE_SIMT, "tensor": xp.ENGINE_TENSOR}[args.engine]
+    wl = pipeline.workload_from_config(cfg, device=dev)
+    wl.engine = engine
+    P = pipeline.Pipeline(wl, device=dev)
+    pos_d = torch.from_numpy(pos_h).to(dev)
+    f_d = torch.from_numpy(f_h).to(dev) if f_h is not None else None
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)    # 256 MB > 126 MB L2
+
+    for _ in range(args.warmup):
+        P.run(pos_d, f_d)
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    xp.profile_reset()
+    n_launch0 = xp.launch_count()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()                                   # L2 flush between timed iterations (untimed)
+            if dist is not None:
+                dist.barrier()
+            torch.cuda.synchronize()
+            ev[i][0].record(stream)
+            P.run(pos_d, f_d, profile=True)
+            ev[i][1].record(stream)
+            torch.cuda.synchronize()
+    n_launch = xp.launch_count() - n_launch0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    ms = float(np.mean(step_ms))
+    prof = xp.profile_query()
+    if dist is not None:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    pairs_step = P.pairs_per_step
+    value = ws * pairs_step / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel (intensity main kernel), CUDA events on its stream
+    main_ms, main_n = prof["intensity_main"]
+    per_launch_ms = main_ms / max(main_n, 1)
+    launches_per_step = max(main_n // args.steps, 1)
+    pairs_launch = pairs_step / launches_per_step
+    peaks, peak_src = _peaks()
+    sm_count, _ = xp.device_info()
+    used = os.environ.get("XPCS_BENCH_ENGINE_USED", "")
+    if cfg.n_plane == 0:
+        # generic q: 2 XU (MUFU) ops per pair; peak = 148 SM x 16 XU/clk x max clock
+        peak = sm_count * 16 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 2 / 1e12
+        roof = {"bound": "alu", "unit": "Tpairs/s (XU: 2 MUFU per pair)", "peak": peak,
+                "achieved": pairs_launch / (per_launch_ms / 1e3) / 1e12}
+    elif wl.in_dtype == xp.F32 and engine != xp.ENGINE_SIMT and "tensor" in used:
+        # tcgen05 split-FP16: 3 fp16 products x 4 real MAC = 24 flop per pair vs measured bf16 (= fp16) dense peak
+        peak = peaks["bf16_tflops_sustained"]
+        roof = {"bound": "tensor", "unit": "TFLOP/s", "peak": peak,
+                "achieved": 24.0 * pairs_launch / (per_launch_ms / 1e3) / 1e12}
+    else:
+        # FP32 CUDA cores: 1 complex MAC = 4 FMA = 8 flop per pair; peak = 148 x 128 FMA/clk x 2 x max clock
+        peak = sm_count * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        roof = {"bound": "alu", "unit": "TFLOP/s (FP32 FMA pipe)", "peak": peak,
+                "achieved": 8.0 * pairs_launch / (per_launch_ms / 1e3) / 1e12}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    roof["peak_source"] = peak_src if roof["bound"] == "tensor" else "derived (DESIGN.md)"
+    roof["kernel_ms"] = per_launch_ms
+    roof["kernel_share_of_step"] = main_ms / args.steps / ms if ms > 0 else None
+
+    # ---- end to end through the public API from pinned host memory
+    e2e = None
+    if not args.no_e2e:
+        P.alloc_host_io(pos_h, f_h)
+        P.run_host()
+        torch.cuda.synchronize()
+        t_e = []
+        for _ in range(max(2, args.steps)):
+            if dist is not None:
+                dist.barrier()
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            P.run_host()
+            b.record(stream)
+            torch.cuda.synchronize()
+            t_e.append(a.elapsed_time(b))
+        e_ms = float(np.mean(t_e))
+        if dist is not None:
+            t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        h2d, d2h = P.io_bytes()
+        e2e = {"value": ws * pairs_step / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, args.cpu_budget)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64" if wl.in_dtype == xp.F64 else "f32", "data": "synthetic",
+                "config": {"workload": cfg.name, "N": cfg.N, "n_q": P.n_q, "frames": cfg.T,
+                           "lags": len(cfg.lags), "windows": list(cfg.windows), "rings": cfg.n_bins,
+                           "pairs_per_step_per_gpu": pairs_step, "engine": args.engine,
+                           "l2": "flushed between timed steps (256 MB write, untimed)",
+                           "parallelism": f"weak x{ws} (independent trajectories)"},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(n_launch),
+                "clocks": clk.summary(), "step_ms_all": step_ms,
+                "kernel_ms": {k: v[0] / max(args.steps, 1) for k, v in prof.items()}}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,184 @@
+/*
+ * xpcs.h -- C ABI of libxpcs.so, the B200 (sm_100a) implementation of the direct method of
+ * S. Mohanty, C. B. Cooper, H. Wang, M. Liang, W. Cai, "Computational Approaches to Model X-ray Photon
+ * Correlation Spectroscopy from Molecular Dynamics", arXiv 2204.13241 (cited as PAPER.md:<line>).
+ *
+ * Conventions shared by every entry point
+ *  - Array pointers are DEVICE pointers owned by the caller unless marked HOST; arrays are contiguous
+ *    and row-major.  Structs passed by pointer (xpcs_opts, xpcs_qgrid) live in HOST memory.
+ *  - All work is enqueued on opts->stream (a cudaStream_t; NULL = the legacy default stream).  Calls
+ *    return as soon as the work is enqueued; outputs are valid after that stream is synchronised.
+ *  - Return value: 0 (XPCS_OK) or a positive xpcs_status.  A human-readable message for the most recent
+ *    failure of the calling thread is returned by xpcs_last_error().  No C++ exception crosses the ABI.
+ *    An asynchronous CUDA fault from earlier work is reported as XPCS_ECUDA by the next call.
+ *  - Argument validation happens before any work is enqueued: on XPCS_EINVAL nothing was launched.
+ *  - The library owns only internal scratch (cached per device, grown on demand); xpcs_release() frees it.
+ *  - There is no CPU fallback: every step runs in this library's CUDA kernels.
+ */
+#ifndef XPCS_H_
+#define XPCS_H_
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define XPCS_API __attribute__((visibility("default")))
+#else
+#define XPCS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    XPCS_OK = 0,
+    XPCS_EINVAL = 1,       /* bad argument (null pointer, size <= 0, lag >= frames, window out of range, ...) */
+    XPCS_ECUDA = 2,        /* CUDA runtime error (launch failure or an earlier asynchronous fault)        */
+    XPCS_ENOMEM = 3,       /* device scratch allocation failed                                            */
+    XPCS_EUNSUPPORTED = 4  /* valid request this build does not implement (e.g. engine not available)     */
+} xpcs_status;
+
+typedef enum { XPCS_F32 = 0, XPCS_F64 = 1 } xpcs_dtype;
+
+/* Which kernel family evaluates a lattice-grid contraction (xpcs_intensity_grid, f32 only).
+ * AUTO picks the fastest available engine; SIMT = FP32 CUDA-core factorised kernel; TENSOR = tcgen05
+ * split-precision kernel.  The generic q-list path ignores this field. */
+typedef enum { XPCS_ENGINE_AUTO = 0, XPCS_ENGINE_SIMT = 1, XPCS_ENGINE_TENSOR = 2 } xpcs_engine;
+
+typedef struct {
+    int32_t in_dtype;   /* xpcs_dtype of positions / form factors / q vectors, or of the intensity series fed to
+                           xpcs_g2, xsvs_contrast, xpcs_shell_mean                                              */
+    int32_t out_dtype;  /* xpcs_dtype of I_out (xpcs_intensity*) and g2_out (xpcs_g2)                          */
+    void*   stream;     /* cudaStream_t; NULL = legacy default stream                                           */
+    int32_t engine;     /* xpcs_engine (lattice grids only)                                                     */
+    int32_t profile;    /* nonzero: time the dominant kernels with CUDA events (see xpcs_profile_query)        */
+} xpcs_opts;
+
+/* A plane of the reciprocal lattice of a cubic periodic box of edge L (Algorithm 1 step 1,
+ * PAPER.md:295): pixel (ih, ik), 0 <= ih < n_h, 0 <= ik < n_k, has integer indices h = h0 + ih, k = k0 + ik and
+ *     q = (2 pi / L) (m0 + h * ma + k * mb),
+ * with integer 3-vectors m0, ma, mb.  Pixel index = ih * n_k + ik.  The configs' detector plane is
+ * m0 = 0, ma = (1,0,0), mb = (0,1,0), h0 = k0 = -n/2, n_h = n_k = n (xpcs_qgrid_lattice_plane). */
+typedef struct {
+    double  L;
+    int32_t m0[3];
+    int32_t ma[3];
+    int32_t mb[3];
+    int32_t pad_;
+    int64_t h0, n_h, k0, n_k;
+} xpcs_qgrid;
+
+/* ------------------------------------------------------------------------------------------------
+ * Speckle intensity by the direct method.
+ * Eq.(7):  p^e(q,t) = sum_j f_j exp(-i q . r_j(t));  Eq.(8), PAPER.md:134-138:
+ * I(q,t) = |p^e(q,t)|^2;  Algorithm 1, evaluated for every q and every frame.
+ *
+ * xpcs_intensity: an explicit list of q vectors (any q, e.g. Ewald-sphere detector pixels).
+ *   positions    [frames][N][3] in_dtype  atom positions r_j(t); wrapped into [0, box_L)^3 before use
+ *                                          (reading R3: off-lattice q sees this image choice)
+ *   N            atoms per frame (> 0)
+ *   form_factors [N] in_dtype or NULL      q-independent f_j (NULL: f_j = 1)  (R2)
+ *   q_vectors    [n_q][3] in_dtype         diffraction vectors q = k_f - k_i (Eq. 1)
+ *   n_q, frames  > 0
+ *   box_L        > 0, periodic box edge (same length unit as 1/|q|)
+ *   I_out        [frames][n_q] out_dtype
+ * Errors: EINVAL for null positions / q_vectors / I_out, N, n_q, frames <= 0, box_L <= 0 or non-finite,
+ *         unknown dtype.  Positions are read as given: NaN/Inf inputs propagate into I_out. */
+XPCS_API int xpcs_intensity(const void* positions, int64_t N, const void* form_factors,
+                   const void* q_vectors, int64_t n_q, int64_t frames, double box_L,
+                   void* I_out, const xpcs_opts* opts);
+
+/* xpcs_intensity_grid: q on a reciprocal-lattice plane (host struct *grid).  Same output as xpcs_intensity
+ * with the q list of the grid, but the library forms every phase from the exact integers (h, k, m0, ma, mb)
+ * and L (R9: q is never rounded to fp32) and evaluates the per-axis factorisation
+ *     p^e(h,k) = sum_j X_h(j) W_k(j),  X_h = e^{-2 pi i h (ma . r_j)/L},  W_k = f_j e^{-2 pi i (m0 + k mb) . r_j / L}
+ * on the engine selected by opts->engine.
+ *   I_out [frames][n_h * n_k] out_dtype.
+ * Errors: as xpcs_intensity, plus EINVAL for n_h, n_k <= 0 or |indices| too large for 32-bit turns,
+ *         EUNSUPPORTED if opts->engine = TENSOR is requested for f64 inputs. */
+XPCS_API int xpcs_intensity_grid(const void* positions, int64_t N, const void* form_factors,
+                        const xpcs_qgrid* grid, int64_t frames, void* I_out, const xpcs_opts* opts);
+
+/* ------------------------------------------------------------------------------------------------
+ * Intensity autocorrelation, Eq.(14), PAPER.md:170-174 (literal estimator, R6), per pixel:
+ *   num(tau) = 1/(T - tau) sum_{t=0}^{T-1-tau} I_t I_{t+tau},  den = ((1/T) sum_t I_t)^2,  g2 = num / den.
+ * tau = 0 gives beta0 + 1 (Eq. 19).  Products and sums in FP64.
+ *   I_series [frames][n_q] in_dtype;  lags HOST [n_lags], 0 <= lag < frames;  g2_out [n_lags][n_q] out_dtype.
+ * A pixel whose mean intensity is 0 gets g2 = NaN.
+ * Errors: EINVAL for null pointers, frames/n_q/n_lags <= 0, any lag outside [0, frames). */
+XPCS_API int xpcs_g2(const void* I_series, int64_t frames, int64_t n_q, const int32_t* lags, int64_t n_lags,
+            void* g2_out, const xpcs_opts* opts);
+
+/* ------------------------------------------------------------------------------------------------
+ * XSVS optical contrast versus exposure.  Eq.(15), as a discrete unnormalised sum over
+ * non-overlapping windows of W frames aligned at t = 0 (remainder dropped):
+ *     I_W(q, s) = sum_{t=sW}^{sW+W-1} I(q, t),   s = 0 .. floor(T/W) - 1;
+ * Eq.(17), per snapshot and q-ring b (population variance over the ring's pixels):
+ *     beta_{W,b,s} = (<I_W^2>_b - <I_W>_b^2) / <I_W>_b^2,
+ * then averaged over the snapshots s.  Moments in FP64.
+ *   I_series [frames][n_q] in_dtype;  bin_of_q DEVICE [n_q] int32 ring index in [0, n_bins) or -1 (excluded);
+ *   windows HOST [n_windows] (1 <= W <= frames);  beta_out DEVICE [n_windows][n_bins] double.
+ * An empty ring gives NaN.
+ * Errors: EINVAL for null pointers, frames/n_q/n_windows <= 0, n_bins <= 0, any window outside [1, frames]. */
+XPCS_API int xsvs_contrast(const void* I_series, int64_t frames, int64_t n_q,
+                  const int32_t* bin_of_q, int32_t n_bins,
+                  const int32_t* windows, int64_t n_windows,
+                  double* beta_out, const xpcs_opts* opts);
+
+/* Ring average of any per-pixel quantity, per row:
+ *   out[r][b] = scale * mean_{q in ring b, values finite} values[r][q]   (NaN if no finite value),
+ * e.g. the ring-averaged g2(q, tau) or, with scale = 1 / sum_j f_j^2, the structure factor
+ * S(q,t) of Eq.(12)/(13) (see xpcs_structure_factor_shells).
+ *   values [rows][n_q] in_dtype; bin_of_q DEVICE [n_q]; out DEVICE [rows][n_bins] double. */
+XPCS_API int xpcs_shell_mean(const void* values, int64_t rows, int64_t n_q, const int32_t* bin_of_q, int32_t n_bins,
+                    double scale, double* out, const xpcs_opts* opts);
+
+/* Eq.(12)-(13): ring-averaged S(q,t) = <I(q,t)>_ring / sum_j f_j^2, with sum_j f_j^2 reduced
+ * on the device from form_factors [N] (in_dtype, NULL => f = 1).  I [rows][n_q] in_dtype -> out [rows][n_bins]. */
+XPCS_API int xpcs_structure_factor_shells(const void* I, int64_t rows, int64_t n_q, const void* form_factors, int64_t N,
+                                 const int32_t* bin_of_q, int32_t n_bins, double* out, const xpcs_opts* opts);
+
+/* ------------------------------------------------------------------------------------------------
+ * q geometry helpers.
+ * xpcs_qgrid_lattice_plane (HOST only, no device work): the configs' plane h, k in [-n/2, n/2 - 1] at height l,
+ *   q = (2 pi / L)(h, k, l).  Errors: EINVAL for L <= 0, n <= 0, null out.
+ * xpcs_qgrid_ewald: detector pixels on the Ewald sphere (Eq.(1); Fig. 5, PAPER.md:445;
+ *   DESIGN.md R4): k = 2 pi / wavelength, k_i = k z, pixel (i, j) at lon-lat angles
+ *   psi_x = (i - (npx-1)/2) pitch, psi_y = (j - (npy-1)/2) pitch, u = (sin psi_x cos psi_y, sin psi_y,
+ *   cos psi_x cos psi_y), q = k (u - z); computed in FP64, stored as opts->out_dtype into q_out DEVICE
+ *   [npx * npy][3] (index i * npy + j).  Errors: EINVAL for wavelength <= 0, npx/npy <= 0, null q_out.
+ * xpcs_lattice_bins: ring index of every grid pixel in exact integer arithmetic (R8):
+ *   r2 = |m0 + h ma + k mb|^2, b = isqrt(r2) / w; excluded (-1) if r2 == 0 or r2 >= (n_bins w)^2.
+ *   bin_out DEVICE [n_h * n_k] int32.  Errors: EINVAL for null pointers, n_bins <= 0, w <= 0.
+ * xpcs_radial_bins: ring index of explicit q vectors (in_dtype): b = floor(|q| / q_max * n_bins) in FP64,
+ *   -1 for q = 0 or |q| >= q_max.  bin_out DEVICE [n_q]. */
+XPCS_API int xpcs_qgrid_lattice_plane(double L, int64_t n, int32_t l, xpcs_qgrid* out);
+XPCS_API int xpcs_qgrid_ewald(double wavelength, int64_t npx, int64_t npy, double pitch, void* q_out,
+                     const xpcs_opts* opts);
+XPCS_API int xpcs_lattice_bins(const xpcs_qgrid* grid, int32_t n_bins, int32_t w, int32_t* bin_out,
+                      const xpcs_opts* opts);
+XPCS_API int xpcs_radial_bins(const void* q_vectors, int64_t n_q, double q_max, int32_t n_bins, int32_t* bin_out,
+                     const xpcs_opts* opts);
+
+/* ------------------------------------------------------------------------------------------------
+ * Runtime.
+ * xpcs_last_error: message of the calling thread's most recent failure ("" if none); valid until the next call.
+ * xpcs_release: synchronise the device and free all cached scratch.
+ * xpcs_launch_count: number of CUDA kernels this library has launched since load (monotone).
+ * xpcs_profile_reset / xpcs_profile_query: when opts->profile != 0 the library brackets each launch of its
+ *   main kernels with CUDA events on opts->stream.  query(i) synchronises and returns, for kernel class i
+ *   (0 = intensity main kernel, 1 = staging, 2 = amplitude reduction, 3 = g2, 4 = XSVS, 5 = rings),
+ *   its name, the summed device time in ms and the number of timed launches; returns EINVAL past the end.
+ * xpcs_device_info: SM count and SM clock (kHz) of the current device (HOST outputs). */
+XPCS_API const char* xpcs_last_error(void);
+XPCS_API int xpcs_release(void);
+XPCS_API int64_t xpcs_launch_count(void);
+XPCS_API int xpcs_profile_reset(void);
+XPCS_API int xpcs_profile_query(int32_t kernel_class, const char** name, double* total_ms, int64_t* launches);
+XPCS_API int xpcs_device_info(int32_t* sm_count, int32_t* sm_clock_khz);
+XPCS_API int xpcs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* XPCS_H_ */

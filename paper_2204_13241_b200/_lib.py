@@ -1,0 +1,287 @@
+"""ctypes binding of libxpcs.so (include/xpcs.h).  Argument marshalling only: every step runs in the CUDA
+library; there is no CPU fallback -- if the shared library or a CUDA device is missing, calls raise.
+
+Names follow the C ABI.  Tensor arguments are torch CUDA tensors (device memory + the current stream are the
+only things PyTorch provides); host-side integer lists (lags, windows) are plain Python sequences.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libxpcs.so")
+
+XPCS_OK, XPCS_EINVAL, XPCS_ECUDA, XPCS_ENOMEM, XPCS_EUNSUPPORTED = 0, 1, 2, 3, 4
+F32, F64 = 0, 1
+ENGINE_AUTO, ENGINE_SIMT, ENGINE_TENSOR = 0, 1, 2
+KERNEL_CLASSES = ("intensity_main", "stage", "amplitude_reduce", "g2", "xsvs", "rings")
+
+EXPORTED = (
+    "xpcs_intensity", "xpcs_intensity_grid", "xpcs_g2", "xsvs_contrast", "xpcs_shell_mean",
+    "xpcs_structure_factor_shells", "xpcs_qgrid_lattice_plane", "xpcs_qgrid_ewald", "xpcs_lattice_bins",
+    "xpcs_radial_bins", "xpcs_last_error", "xpcs_release", "xpcs_launch_count", "xpcs_profile_reset",
+    "xpcs_profile_query", "xpcs_device_info", "xpcs_version",
+)
+
+
+class XpcsError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"xpcs status {status}: {msg}")
+        self.status = status
+
+
+class Opts(ctypes.Structure):
+    _fields_ = [("in_dtype", ctypes.c_int32), ("out_dtype", ctypes.c_int32), ("stream", ctypes.c_void_p),
+                ("engine", ctypes.c_int32), ("profile", ctypes.c_int32)]
+
+
+class QGrid(ctypes.Structure):
+    _fields_ = [("L", ctypes.c_double), ("m0", ctypes.c_int32 * 3), ("ma", ctypes.c_int32 * 3),
+                ("mb", ctypes.c_int32 * 3), ("pad_", ctypes.c_int32), ("h0", ctypes.c_int64),
+                ("n_h", ctypes.c_int64), ("k0", ctypes.c_int64), ("n_k", ctypes.c_int64)]
+
+    @property
+    def n_q(self):
+        return int(self.n_h * self.n_k)
+
+
+_lib = None
+
+
+def load():
+    """Load libxpcs.so (raises if it has not been built: run __graft_entry__.build())."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise OSError(f"{LIB_PATH} not built (run `python -c 'import __graft_entry__ as g; g.build()'`)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i64, i32, dbl = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double
+    op = ctypes.POINTER(Opts)
+    gp = ctypes.POINTER(QGrid)
+    ip32 = ctypes.POINTER(ctypes.c_int32)
+    sig = {
+        "xpcs_intensity": [vp, i64, vp, vp, i64, i64, dbl, vp, op],
+        "xpcs_intensity_grid": [vp, i64, vp, gp, i64, vp, op],
+        "xpcs_g2": [vp, i64, i64, ip32, i64, vp, op],
+        "xsvs_contrast": [vp, i64, i64, vp, i32, ip32, i64, vp, op],
+        "xpcs_shell_mean": [vp, i64, i64, vp, i32, dbl, vp, op],
+        "xpcs_structure_factor_shells": [vp, i64, i64, vp, i64, vp, i32, vp, op],
+        "xpcs_qgrid_lattice_plane": [dbl, i64, i32, gp],
+        "xpcs_qgrid_ewald": [dbl, i64, i64, dbl, vp, op],
+        "xpcs_lattice_bins": [gp, i32, i32, vp, op],
+        "xpcs_radial_bins": [vp, i64, dbl, i32, vp, op],
+        "xpcs_last_error": [],
+        "xpcs_release": [],
+        "xpcs_launch_count": [],
+        "xpcs_profile_reset": [],
+        "xpcs_profile_query": [i32, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_double),
+                               ctypes.POINTER(ctypes.c_int64)],
+        "xpcs_device_info": [ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)],
+        "xpcs_version": [],
+    }
+    for name, args in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_int
+    L.xpcs_last_error.restype = ctypes.c_char_p
+    L.xpcs_launch_count.restype = ctypes.c_int64
+    _lib = L
+    return L
+
+
+def _check(rc):
+    if rc != XPCS_OK:
+        raise XpcsError(rc, load().xpcs_last_error().decode())
+
+
+def _dtype_code(t):
+    import torch
+    if t.dtype == torch.float32:
+        return F32
+    if t.dtype == torch.float64:
+        return F64
+    raise TypeError(f"unsupported dtype {t.dtype}")
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("xpcs: tensors must live in device memory (no CPU fallback)")
+    if not t.is_contiguous():
+        raise ValueError("xpcs: tensors must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def make_opts(in_dtype=F32, out_dtype=F32, stream=None, engine=ENGINE_AUTO, profile=False):
+    return Opts(in_dtype, out_dtype, _stream(stream), engine, 1 if profile else 0)
+
+
+def _i32_array(seq):
+    a = np.ascontiguousarray(np.asarray(seq, dtype=np.int32))
+    return a, a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+
+
+# --------------------------------------------------------------------------------------------- API
+def lattice_plane(L, n, l=0) -> QGrid:
+    g = QGrid()
+    _check(load().xpcs_qgrid_lattice_plane(float(L), int(n), int(l), ctypes.byref(g)))
+    return g
+
+
+def qgrid(L, h0, n_h, k0, n_k, m0=(0, 0, 0), ma=(1, 0, 0), mb=(0, 1, 0)) -> QGrid:
+    g = QGrid()
+    g.L = float(L)
+    g.m0[:], g.ma[:], g.mb[:] = list(m0), list(ma), list(mb)
+    g.h0, g.n_h, g.k0, g.n_k = int(h0), int(n_h), int(k0), int(n_k)
+    return g
+
+
+def xpcs_intensity(positions, form_factors, q_vectors, box_L, out=None, out_dtype=None, stream=None, profile=False):
+    """Eq.(7)-(8) at an explicit q list.  positions [T][N][3], q [n_q][3] (same dtype), -> I [T][n_q]."""
+    import torch
+    if positions.dim() == 2:
+        positions = positions.unsqueeze(0)
+    T, N = positions.shape[0], positions.shape[1]
+    n_q = q_vectors.shape[0]
+    ind = _dtype_code(positions)
+    outd = ind if out_dtype is None else out_dtype
+    if out is None:
+        out = torch.empty((T, n_q), dtype=torch.float64 if outd == F64 else torch.float32, device=positions.device)
+    o = make_opts(ind, outd, stream, ENGINE_AUTO, profile)
+    _check(load().xpcs_intensity(_ptr(positions), N, _ptr(form_factors), _ptr(q_vectors), n_q, T, float(box_L),
+                                 _ptr(out), ctypes.byref(o)))
+    return out
+
+
+def xpcs_intensity_grid(positions, form_factors, grid: QGrid, out=None, out_dtype=None, engine=ENGINE_AUTO,
+                        stream=None, profile=False):
+    """Eq.(7)-(8) on a reciprocal-lattice plane (exact integer phases).  -> I [T][n_h * n_k]."""
+    import torch
+    if positions.dim() == 2:
+        positions = positions.unsqueeze(0)
+    T, N = positions.shape[0], positions.shape[1]
+    ind = _dtype_code(positions)
+    outd = ind if out_dtype is None else out_dtype
+    if out is None:
+        out = torch.empty((T, grid.n_q), dtype=torch.float64 if outd == F64 else torch.float32,
+                          device=positions.device)
+    o = make_opts(ind, outd, stream, engine, profile)
+    _check(load().xpcs_intensity_grid(_ptr(positions), N, _ptr(form_factors), ctypes.byref(grid), T, _ptr(out),
+                                      ctypes.byref(o)))
+    return out
+
+
+def xpcs_g2(I, lags, out=None, out_dtype=F64, stream=None, profile=False):
+    """Eq.(14) per pixel. I [T][n_q] -> g2 [n_lags][n_q]."""
+    import torch
+    T, n_q = I.shape
+    lag_arr, lag_p = _i32_array(lags)
+    if out is None:
+        out = torch.empty((len(lag_arr), n_q), dtype=torch.float64 if out_dtype == F64 else torch.float32,
+                          device=I.device)
+    o = make_opts(_dtype_code(I), out_dtype, stream, ENGINE_AUTO, profile)
+    _check(load().xpcs_g2(_ptr(I), T, n_q, lag_p, len(lag_arr), _ptr(out), ctypes.byref(o)))
+    return out
+
+
+def xsvs_contrast(I, bins, n_bins, windows, out=None, stream=None, profile=False):
+    """Eq.(15)+(17): beta [n_windows][n_bins] (float64)."""
+    import torch
+    T, n_q = I.shape
+    w_arr, w_p = _i32_array(windows)
+    if out is None:
+        out = torch.empty((len(w_arr), n_bins), dtype=torch.float64, device=I.device)
+    o = make_opts(_dtype_code(I), F64, stream, ENGINE_AUTO, profile)
+    _check(load().xsvs_contrast(_ptr(I), T, n_q, _ptr(bins), int(n_bins), w_p, len(w_arr), _ptr(out),
+                                ctypes.byref(o)))
+    return out
+
+
+def xpcs_shell_mean(values, bins, n_bins, scale=1.0, out=None, stream=None, profile=False):
+    import torch
+    if values.dim() == 1:
+        values = values.unsqueeze(0)
+    rows, n_q = values.shape
+    if out is None:
+        out = torch.empty((rows, n_bins), dtype=torch.float64, device=values.device)
+    o = make_opts(_dtype_code(values), F64, stream, ENGINE_AUTO, profile)
+    _check(load().xpcs_shell_mean(_ptr(values), rows, n_q, _ptr(bins), int(n_bins), float(scale), _ptr(out),
+                                  ctypes.byref(o)))
+    return out
+
+
+def xpcs_structure_factor_shells(I, form_factors, N, bins, n_bins, out=None, stream=None, profile=False):
+    import torch
+    rows, n_q = I.shape
+    if out is None:
+        out = torch.empty((rows, n_bins), dtype=torch.float64, device=I.device)
+    o = make_opts(_dtype_code(I), F64, stream, ENGINE_AUTO, profile)
+    _check(load().xpcs_structure_factor_shells(_ptr(I), rows, n_q, _ptr(form_factors), int(N), _ptr(bins),
+                                               int(n_bins), _ptr(out), ctypes.byref(o)))
+    return out
+
+
+def xpcs_qgrid_ewald(wavelength, npx, npy, pitch, out_dtype=F32, device="cuda", stream=None):
+    import torch
+    out = torch.empty((npx * npy, 3), dtype=torch.float64 if out_dtype == F64 else torch.float32, device=device)
+    o = make_opts(F32, out_dtype, stream)
+    _check(load().xpcs_qgrid_ewald(float(wavelength), int(npx), int(npy), float(pitch), _ptr(out), ctypes.byref(o)))
+    return out
+
+
+def xpcs_lattice_bins(grid: QGrid, n_bins, w, device="cuda", stream=None):
+    import torch
+    out = torch.empty(grid.n_q, dtype=torch.int32, device=device)
+    o = make_opts(stream=stream)
+    _check(load().xpcs_lattice_bins(ctypes.byref(grid), int(n_bins), int(w), _ptr(out), ctypes.byref(o)))
+    return out
+
+
+def xpcs_radial_bins(q, q_max, n_bins, stream=None):
+    import torch
+    out = torch.empty(q.shape[0], dtype=torch.int32, device=q.device)
+    o = make_opts(_dtype_code(q), F32, stream)
+    _check(load().xpcs_radial_bins(_ptr(q), q.shape[0], float(q_max), int(n_bins), _ptr(out), ctypes.byref(o)))
+    return out
+
+
+def launch_count() -> int:
+    return int(load().xpcs_launch_count())
+
+
+def profile_reset():
+    _check(load().xpcs_profile_reset())
+
+
+def profile_query():
+    """{class name: (total ms, launches)} for every kernel class (synchronises on the recorded events)."""
+    out = {}
+    for i in range(len(KERNEL_CLASSES)):
+        name = ctypes.c_char_p()
+        ms = ctypes.c_double()
+        n = ctypes.c_int64()
+        _check(load().xpcs_profile_query(i, ctypes.byref(name), ctypes.byref(ms), ctypes.byref(n)))
+        out[name.value.decode()] = (ms.value, n.value)
+    return out
+
+
+def release():
+    _check(load().xpcs_release())
+
+
+def device_info():
+    sm = ctypes.c_int32()
+    clk = ctypes.c_int32()
+    _check(load().xpcs_device_info(ctypes.byref(sm), ctypes.byref(clk)))
+    return sm.value, clk.value

@@ -1,0 +1,159 @@
+// common.cuh -- internal helpers of libxpcs.so (sm_100a).  Not part of the ABI (see include/xpcs.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstddef>
+
+namespace xpcs {
+
+// ------------------------------------------------------------------------------------------------
+// host-side runtime services (defined in runtime.cu)
+// ------------------------------------------------------------------------------------------------
+enum KernelClass { KC_MAIN = 0, KC_STAGE = 1, KC_REDUCE = 2, KC_G2 = 3, KC_XSVS = 4, KC_RINGS = 5, KC_COUNT = 6 };
+
+void set_error(const char* fmt, ...);
+void note_launch(int n = 1);
+
+// Scratch cached per (stream, slot); grown on demand (the grow synchronises the device).
+enum ScratchSlot {
+    SS_STAGE = 0, SS_PARTIAL, SS_PLAN, SS_PLAN2, SS_XSVS, SS_SMALL, SS_LAGS, SS_TC, SS_COUNT
+};
+void* scratch(cudaStream_t s, int slot, size_t bytes);   // nullptr on failure (error already set)
+void release_scratch();
+
+// Profiling: events around launches of one kernel class on a stream (opts->profile).
+struct ProfScope {
+    ProfScope(bool on, int cls, cudaStream_t s);
+    ~ProfScope();
+    bool on_;
+    int cls_;
+    cudaStream_t s_;
+    cudaEvent_t a_, b_;
+};
+
+int sm_count();
+
+// ------------------------------------------------------------------------------------------------
+// device helpers
+// ------------------------------------------------------------------------------------------------
+// Fixed-point turns: a phase of T * 2^-32 turns (T mod 2^32) -> angle in radians in [-pi, pi).
+// Bit trick: (T >> 9) ^ 0x3FC00000 is the float 1.5 + t with t = (int32)T * 2^-32 truncated to 2^-23
+// (the truncation is a constant -2^-24-turn mean offset = a global phase, invisible in |p|^2, plus
+// a zero-mean error < 2^-23 turns).  Then theta = 2 pi (f - 1.5) in one FFMA.
+__device__ __forceinline__ float turns_to_radians(uint32_t T) {
+    const float f = __uint_as_float((T >> 9) ^ 0x3FC00000u);
+    return fmaf(f, 6.28318530717958647692f, -1.5f * 6.28318530717958647692f);
+}
+
+// Accurate conversion for table generation (no truncation): signed turns in [-0.5, 0.5).
+__device__ __forceinline__ float turns_signed(uint32_t T) {
+    return (float)(int32_t)T * 2.3283064365386963e-10f;   // 2^-32
+}
+
+__device__ __forceinline__ double turns_signed64(uint64_t T) {
+    return (double)(int64_t)T * 5.421010862427522170037e-20;   // 2^-64
+}
+
+// packed FP32x2 FMA (SASS FFMA2): d = a * b + c, element-wise on (lo, hi)
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b,
+                                                    unsigned long long c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
+    return (unsigned long long)__float_as_uint(lo) | ((unsigned long long)__float_as_uint(hi) << 32);
+}
+__device__ __forceinline__ float lo2(unsigned long long v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float hi2(unsigned long long v) { return __uint_as_float((uint32_t)(v >> 32)); }
+
+// Position -> fraction of the box in [0, 1) (periodic wrap) -> 32/64-bit fixed point.
+__device__ __forceinline__ double box_fraction(double x, double L) {
+    // periodic wrap as the ABI documents it: y = x - L floor(x / L) (a result equal to L maps to 0),
+    // then the box fraction u = y / L in [0, 1)
+    double y = x - L * floor(x / L);
+    if (y >= L || y < 0.0) y = 0.0;
+    const double u = y / L;
+    return u < 1.0 ? u : 0.0;
+}
+__device__ __forceinline__ uint32_t frac_to_fixed32(double u) {
+    // round(u * 2^32) mod 2^32 ; u in [0, 1)
+    unsigned long long v = (unsigned long long)llrint(u * 4294967296.0);
+    return (uint32_t)v;
+}
+__device__ __forceinline__ uint64_t frac_to_fixed64(double u) {
+    // u has <= 53 significant bits, so u * 2^64 is an exact integer-valued real < 2^64
+    const double hi = floor(u * 4294967296.0);
+    const double lo = (u * 4294967296.0 - hi) * 4294967296.0;   // exact
+    return ((uint64_t)hi << 32) + (uint64_t)llrint(lo);
+}
+
+}  // namespace xpcs
+
+// ------------------------------------------------------------------------------------------------
+// launchers (one per kernel family; defined in the k_*.cu files).  All return cudaError_t of the launch.
+// ------------------------------------------------------------------------------------------------
+namespace xpcs {
+
+struct LatticeGeom {
+    double L;
+    int32_t m0[3], ma[3], mb[3];
+    int64_t h0, n_h, k0, n_k;
+};
+
+// staging: positions [T][N][3] (f32|f64) + f [N] (f32|f64|null) -> per-atom fixed-point turns
+cudaError_t launch_stage_lattice32(const void* pos, int pos_f64, const void* f, int f_f64, int64_t N,
+                                   int64_t frames, const LatticeGeom& g, uint4* out, cudaStream_t s);
+cudaError_t launch_stage_lattice64(const void* pos, const void* f, int64_t N, int64_t frames,
+                                   const LatticeGeom& g, ulonglong4* out, cudaStream_t s);
+cudaError_t launch_stage_generic32(const void* pos, int pos_f64, const void* f, int f_f64, int64_t N,
+                                   int64_t frames, double L, uint4* out, cudaStream_t s);
+cudaError_t launch_stage_generic64(const void* pos, const void* f, int64_t N, int64_t frames, double L,
+                                   ulonglong4* out, cudaStream_t s);
+
+// lattice contraction, FP32 CUDA cores: partial [C][Tb][n_h*n_k] float2
+cudaError_t launch_lattice_simt(const uint4* staged, int64_t N, int64_t frames, const LatticeGeom& g,
+                                int64_t chunk_atoms, int64_t n_chunks, float2* partial, cudaStream_t s);
+// lattice contraction, tcgen05 split-FP16: partial [C][Tb][n_h*n_k] float2.  Returns cudaErrorNotSupported
+// if the geometry does not fit the engine's tiling constraints.
+cudaError_t launch_lattice_tc(const uint4* staged, int64_t N, int64_t frames, const LatticeGeom& g,
+                              int64_t chunk_atoms, int64_t n_chunks, float2* partial, cudaStream_t s);
+bool lattice_tc_supported(const LatticeGeom& g);
+// lattice FP64 (direct per-pixel evaluation with 64-bit turns): writes I directly (double)
+cudaError_t launch_lattice_f64(const ulonglong4* staged, int64_t N, int64_t frames, const LatticeGeom& g,
+                               void* I_out, int out_f64, cudaStream_t s);
+// generic q list: partial [C][Tb][n_q] double2
+cudaError_t launch_generic32(const uint4* staged, int64_t N, int64_t frames, const void* q, int q_f64,
+                             int64_t n_q, double L, int64_t chunk_atoms, int64_t n_chunks, double2* partial,
+                             cudaStream_t s);
+cudaError_t launch_generic64(const ulonglong4* staged, int64_t N, int64_t frames, const void* q,
+                             int64_t n_q, double L, double2* partial, cudaStream_t s);
+// |sum_c partial|^2 -> I_out rows
+cudaError_t launch_amp_reduce_f(const float2* partial, int64_t C, int64_t frames, int64_t n_q, void* I_out,
+                                int out_f64, cudaStream_t s);
+cudaError_t launch_amp_reduce_d(const double2* partial, int64_t C, int64_t frames, int64_t n_q, void* I_out,
+                                int out_f64, cudaStream_t s);
+
+// statistics
+cudaError_t launch_g2(const void* I, int in_f64, int64_t T, int64_t n_q, const int32_t* lags_dev,
+                      int64_t n_lags, int max_lag, void* out, int out_f64, cudaStream_t s);
+struct BinPlan {
+    int32_t* perm;        // [n_valid] pixel indices sorted by (bin, pixel)
+    int32_t* offsets;     // [n_bins + 1]
+    int32_t* warp_off;    // [n_bins + 1] prefix of ceil(count_b / 32)
+};
+cudaError_t launch_binplan(const int32_t* bins, int64_t n_q, int32_t n_bins, BinPlan plan, cudaStream_t s);
+cudaError_t launch_sum_f2(const void* f, int f_f64, int64_t N, double* out, cudaStream_t s);
+cudaError_t launch_shell_mean(const void* v, int in_f64, int64_t rows, int64_t n_q, BinPlan plan,
+                              int32_t n_bins, double scale, const double* norm, double* out, cudaStream_t s);
+cudaError_t launch_xsvs(const void* I, int in_f64, int64_t T, int64_t n_q, BinPlan plan, int32_t n_bins,
+                        const int32_t* windows_host, int64_t n_windows, int64_t max_warps, double* warp_moments,
+                        int32_t* dev_windows, double* beta_out, cudaStream_t s);
+// geometry
+cudaError_t launch_ewald(double wavelength, int64_t npx, int64_t npy, double pitch, void* q, int out_f64,
+                         cudaStream_t s);
+cudaError_t launch_lattice_bins(const LatticeGeom& g, int32_t n_bins, int32_t w, int32_t* out, cudaStream_t s);
+cudaError_t launch_radial_bins(const void* q, int q_f64, int64_t n_q, double q_max, int32_t n_bins,
+                               int32_t* out, cudaStream_t s);
+
+}  // namespace xpcs

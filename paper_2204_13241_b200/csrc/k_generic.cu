@@ -1,0 +1,235 @@
+// k_generic.cu -- K1: direct structure-factor sum at an explicit list of q vectors (any q: Ewald detector pixels,
+// off-lattice points), and the FP64 kernels.  SURVEY 8(a) rows a3/a4; Eq.(7)-(8), PAPER.md:127-138;
+// Algorithm 1 step 2, PAPER.md:296 ("summing e^{-i q.r_i} over each atom").
+//
+// Phase arithmetic: the phase in turns is q . r / 2 pi = sum_c g_c u_c with
+// g_c = q_c L / 2 pi (per q, formed once in FP64) and u_c = r_c / L in [0, 1) (per atom, staged as 32-bit fixed
+// point Xi_c).  Writing g_c = n_c + Phi_c 2^-32 (integer part, 32-bit fraction):
+//     turns mod 1 = sum_c [ n_c Xi_c + hi32(Phi_c Xi_c) ] * 2^-32      (mod 2^32, 6 integer multiply-adds)
+// exact to ~3 * 2^-32 turns for any |q| and any box, with no rounded 2 pi and no large fp32 argument.
+// The angle then goes to the SFU: FFMA -> FMUL.RZ -> MUFU.SIN / MUFU.COS (2 XU ops per atom.q pair, the
+// pipe that bounds this kernel), and f_j cos / f_j sin accumulate in fp32 for at most SUB atoms before being
+// folded into FP64 registers.
+#include "common.cuh"
+
+namespace xpcs {
+
+namespace {
+constexpr int GT = 256;     // threads per CTA
+constexpr int QT = 4;       // q per thread
+constexpr int SUB = 512;    // atoms per shared-memory sub-block (also the fp32 accumulation length)
+}
+
+__device__ __forceinline__ void q_to_fixed(double qc, double L_over_2pi, uint32_t& n, uint32_t& phi) {
+    const double gq = qc * L_over_2pi;
+    const double fl = floor(gq);
+    const double fr = gq - fl;                                   // exact, in [0, 1)
+    long long ip = (long long)fl;
+    unsigned long long ph = (unsigned long long)llrint(fr * 4294967296.0);
+    if (ph >= 4294967296ull) { ph -= 4294967296ull; ip += 1; }
+    n = (uint32_t)(unsigned long long)ip;
+    phi = (uint32_t)ph;
+}
+
+template <typename Q>
+__global__ void __launch_bounds__(GT, 2)
+k_generic32(const uint4* __restrict__ staged, int64_t N, const Q* __restrict__ q, int64_t n_q, double L_over_2pi,
+            int64_t chunk_atoms, int64_t frames, double2* __restrict__ partial) {
+    __shared__ uint4 As[SUB];
+    const int64_t t = blockIdx.z;
+    const int64_t chunk = blockIdx.y;
+    const int64_t a_begin = chunk * chunk_atoms, a_end = min(N, a_begin + chunk_atoms);
+    const uint4* S = staged + t * N;
+
+    uint32_t nx[QT], ny[QT], nz[QT], px[QT], py[QT], pz[QT];
+    int64_t iq[QT];
+#pragma unroll
+    for (int i = 0; i < QT; ++i) {
+        iq[i] = (int64_t)blockIdx.x * (GT * QT) + threadIdx.x + GT * i;
+        const int64_t qq = iq[i] < n_q ? iq[i] : 0;
+        q_to_fixed((double)q[3 * qq + 0], L_over_2pi, nx[i], px[i]);
+        q_to_fixed((double)q[3 * qq + 1], L_over_2pi, ny[i], py[i]);
+        q_to_fixed((double)q[3 * qq + 2], L_over_2pi, nz[i], pz[i]);
+    }
+    double dre[QT], dim[QT];
+#pragma unroll
+    for (int i = 0; i < QT; ++i) dre[i] = dim[i] = 0.0;
+
+    for (int64_t a0 = a_begin; a0 < a_end; a0 += SUB) {
+        const int cnt = (int)min((int64_t)SUB, a_end - a0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < SUB; e += GT) As[e] = e < cnt ? S[a0 + e] : make_uint4(0, 0, 0, 0);
+        __syncthreads();
+        float re[QT], im[QT];
+#pragma unroll
+        for (int i = 0; i < QT; ++i) re[i] = im[i] = 0.f;
+#pragma unroll 4
+        for (int a = 0; a < SUB; ++a) {
+            const uint4 at = As[a];                               // broadcast
+            const float fj = __uint_as_float(at.w);               // 0 for padding atoms
+#pragma unroll
+            for (int i = 0; i < QT; ++i) {
+                uint32_t T = nx[i] * at.x;
+                T = ny[i] * at.y + T;
+                T = nz[i] * at.z + T;
+                T = __umulhi(px[i], at.x) + T;
+                T = __umulhi(py[i], at.y) + T;
+                T = __umulhi(pz[i], at.z) + T;
+                float s, c;
+                __sincosf(turns_to_radians(T), &s, &c);
+                re[i] = fmaf(fj, c, re[i]);
+                im[i] = fmaf(fj, s, im[i]);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < QT; ++i) { dre[i] += (double)re[i]; dim[i] += (double)im[i]; }
+    }
+    double2* P = partial + (chunk * frames + t) * n_q;
+#pragma unroll
+    for (int i = 0; i < QT; ++i)
+        if (iq[i] < n_q) P[iq[i]] = make_double2(dre[i], -dim[i]);     // e^{-i phase}: Im = -sum f sin
+}
+
+// ---- FP64 generic: 64-bit turns, sincospi in FP64 (config-1 class precision)
+__device__ __forceinline__ void q_to_fixed64(double qc, double L_over_2pi, uint64_t& n, uint64_t& phi) {
+    const double gq = qc * L_over_2pi;
+    const double fl = floor(gq);
+    const double fr = gq - fl;
+    n = (uint64_t)(long long)fl;
+    // fraction to 64-bit fixed point (fr has <= 53 significant bits: exact)
+    const double hi = floor(fr * 4294967296.0);
+    const double lo = (fr * 4294967296.0 - hi) * 4294967296.0;
+    phi = ((uint64_t)hi << 32) + (uint64_t)llrint(lo);
+}
+
+__global__ void __launch_bounds__(128)
+k_generic64(const ulonglong4* __restrict__ staged, int64_t N, const double* __restrict__ q, int64_t n_q,
+            double L_over_2pi, int64_t frames, double2* __restrict__ partial) {
+    __shared__ ulonglong4 As[128];
+    const int64_t t = blockIdx.y;
+    const int64_t i = (int64_t)blockIdx.x * 128 + threadIdx.x;
+    const int64_t qq = i < n_q ? i : 0;
+    uint64_t n[3], p[3];
+    for (int c = 0; c < 3; ++c) q_to_fixed64(q[3 * qq + c], L_over_2pi, n[c], p[c]);
+    const ulonglong4* S = staged + t * N;
+    double re = 0.0, im = 0.0;
+    for (int64_t a0 = 0; a0 < N; a0 += 128) {
+        __syncthreads();
+        const int64_t j = a0 + threadIdx.x;
+        As[threadIdx.x] = j < N ? S[j] : make_ulonglong4(0, 0, 0, 0);
+        __syncthreads();
+        const int cnt = (int)min((int64_t)128, N - a0);
+        for (int a = 0; a < cnt; ++a) {
+            const ulonglong4 at = As[a];
+            uint64_t T = n[0] * at.x + n[1] * at.y + n[2] * at.z;
+            T += __umul64hi(p[0], at.x) + __umul64hi(p[1], at.y) + __umul64hi(p[2], at.z);
+            double s, c;
+            sincospi(2.0 * turns_signed64(T), &s, &c);
+            const double fj = __longlong_as_double((long long)at.w);
+            re += fj * c;
+            im -= fj * s;
+        }
+    }
+    if (i < n_q) partial[t * n_q + i] = make_double2(re, im);
+}
+
+// ---- FP64 lattice: one pixel per thread, 64-bit turns (exact h*Th_a + k*Th_b + Th_0 mod 2^64)
+template <typename O>
+__global__ void __launch_bounds__(128)
+k_lattice64(const ulonglong4* __restrict__ staged, int64_t N, LatticeGeom g, O* __restrict__ I_out) {
+    __shared__ ulonglong4 As[128];
+    const int64_t t = blockIdx.y;
+    const int64_t n_q = g.n_h * g.n_k;
+    const int64_t pix = (int64_t)blockIdx.x * 128 + threadIdx.x;
+    const int64_t pp = pix < n_q ? pix : 0;
+    const uint64_t h = (uint64_t)(g.h0 + pp / g.n_k), k = (uint64_t)(g.k0 + pp % g.n_k);
+    const ulonglong4* S = staged + t * N;
+    double re = 0.0, im = 0.0;
+    for (int64_t a0 = 0; a0 < N; a0 += 128) {
+        __syncthreads();
+        const int64_t j = a0 + threadIdx.x;
+        As[threadIdx.x] = j < N ? S[j] : make_ulonglong4(0, 0, 0, 0);
+        __syncthreads();
+        const int cnt = (int)min((int64_t)128, N - a0);
+        for (int a = 0; a < cnt; ++a) {
+            const ulonglong4 at = As[a];
+            const uint64_t T = h * at.x + k * at.y + at.z;
+            double s, c;
+            sincospi(2.0 * turns_signed64(T), &s, &c);
+            const double fj = __longlong_as_double((long long)at.w);
+            re += fj * c;
+            im -= fj * s;
+        }
+    }
+    if (pix < n_q) I_out[t * n_q + pix] = (O)(re * re + im * im);
+}
+
+// ---- |sum_c P_c|^2 (FP64 fold of the atom chunks, fixed order)
+template <typename P, typename O>
+__global__ void __launch_bounds__(256)
+k_amp_reduce(const P* __restrict__ partial, int64_t C, int64_t total, O* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        double re = 0.0, im = 0.0;
+        for (int64_t c = 0; c < C; ++c) {
+            const P v = partial[c * total + i];
+            re += (double)v.x;
+            im += (double)v.y;
+        }
+        out[i] = (O)(re * re + im * im);          // Eq.(8): I = p p*
+    }
+}
+
+cudaError_t launch_generic32(const uint4* staged, int64_t N, int64_t frames, const void* q, int q_f64,
+                             int64_t n_q, double L, int64_t chunk_atoms, int64_t n_chunks, double2* partial,
+                             cudaStream_t s) {
+    dim3 grid((unsigned)((n_q + GT * QT - 1) / (GT * QT)), (unsigned)n_chunks, (unsigned)frames);
+    const double l2p = L / (2.0 * 3.14159265358979323846);
+    note_launch();
+    if (q_f64) k_generic32<double><<<grid, GT, 0, s>>>(staged, N, (const double*)q, n_q, l2p, chunk_atoms, frames, partial);
+    else k_generic32<float><<<grid, GT, 0, s>>>(staged, N, (const float*)q, n_q, l2p, chunk_atoms, frames, partial);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_generic64(const ulonglong4* staged, int64_t N, int64_t frames, const void* q,
+                             int64_t n_q, double L, double2* partial, cudaStream_t s) {
+    dim3 grid((unsigned)((n_q + 127) / 128), (unsigned)frames);
+    note_launch();
+    k_generic64<<<grid, 128, 0, s>>>(staged, N, (const double*)q, n_q, L / (2.0 * 3.14159265358979323846), frames, partial);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_lattice_f64(const ulonglong4* staged, int64_t N, int64_t frames, const LatticeGeom& g,
+                               void* I_out, int out_f64, cudaStream_t s) {
+    const int64_t n_q = g.n_h * g.n_k;
+    dim3 grid((unsigned)((n_q + 127) / 128), (unsigned)frames);
+    note_launch();
+    if (out_f64) k_lattice64<double><<<grid, 128, 0, s>>>(staged, N, g, (double*)I_out);
+    else k_lattice64<float><<<grid, 128, 0, s>>>(staged, N, g, (float*)I_out);
+    return cudaGetLastError();
+}
+
+static dim3 rgrid(int64_t total) {
+    int64_t b = (total + 255) / 256;
+    const int64_t cap = (int64_t)sm_count() * 8;
+    return dim3((unsigned)(b < cap ? (b > 0 ? b : 1) : cap));
+}
+
+cudaError_t launch_amp_reduce_f(const float2* partial, int64_t C, int64_t frames, int64_t n_q, void* I_out,
+                                int out_f64, cudaStream_t s) {
+    const int64_t total = frames * n_q;
+    note_launch();
+    if (out_f64) k_amp_reduce<float2, double><<<rgrid(total), 256, 0, s>>>(partial, C, total, (double*)I_out);
+    else k_amp_reduce<float2, float><<<rgrid(total), 256, 0, s>>>(partial, C, total, (float*)I_out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_amp_reduce_d(const double2* partial, int64_t C, int64_t frames, int64_t n_q, void* I_out,
+                                int out_f64, cudaStream_t s) {
+    const int64_t total = frames * n_q;
+    note_launch();
+    if (out_f64) k_amp_reduce<double2, double><<<rgrid(total), 256, 0, s>>>(partial, C, total, (double*)I_out);
+    else k_amp_reduce<double2, float><<<rgrid(total), 256, 0, s>>>(partial, C, total, (float*)I_out);
+    return cudaGetLastError();
+}
+
+}  // namespace xpcs

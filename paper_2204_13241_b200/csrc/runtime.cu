@@ -1,0 +1,128 @@
+// runtime.cu -- error strings, launch counting, cached device scratch and event profiling for libxpcs.so.
+#include "common.cuh"
+#include "../../include/xpcs.h"
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <map>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+namespace xpcs {
+
+static thread_local std::string g_err;
+static std::atomic<long long> g_launches{0};
+static std::mutex g_mu;
+
+void set_error(const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+}
+void clear_error() { g_err.clear(); }
+const char* last_error() { return g_err.c_str(); }
+
+void note_launch(int n) { g_launches.fetch_add(n); }
+long long launches() { return g_launches.load(); }
+
+// ---------------------------------------------------------------- scratch
+struct Buf { void* p = nullptr; size_t n = 0; };
+static std::map<std::pair<cudaStream_t, int>, Buf> g_scratch;
+
+void* scratch(cudaStream_t s, int slot, size_t bytes) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    Buf& b = g_scratch[{s, slot}];
+    if (bytes == 0) bytes = 16;
+    if (b.n >= bytes) return b.p;
+    if (b.p) {
+        cudaStreamSynchronize(s);      // the old buffer may still be in use by queued work on s
+        cudaFree(b.p);
+        b.p = nullptr;
+        b.n = 0;
+    }
+    size_t want = bytes + bytes / 8;  // grow with slack
+    cudaError_t e = cudaMalloc(&b.p, want);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        e = cudaMalloc(&b.p, bytes);
+        want = bytes;
+    }
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        b.p = nullptr;
+        set_error("xpcs: device scratch allocation of %zu bytes failed (%s)", bytes, cudaGetErrorString(e));
+        return nullptr;
+    }
+    b.n = want;
+    return b.p;
+}
+
+void release_scratch() {
+    std::lock_guard<std::mutex> lk(g_mu);
+    cudaDeviceSynchronize();
+    for (auto& kv : g_scratch)
+        if (kv.second.p) cudaFree(kv.second.p);
+    g_scratch.clear();
+}
+
+int sm_count() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+// ---------------------------------------------------------------- profiling
+static const char* kClassNames[KC_COUNT] = {"intensity_main", "stage", "amplitude_reduce", "g2", "xsvs", "rings"};
+struct ProfRec { std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev; };
+static ProfRec g_prof[KC_COUNT];
+
+ProfScope::ProfScope(bool on, int cls, cudaStream_t s) : on_(on), cls_(cls), s_(s), a_(nullptr), b_(nullptr) {
+    if (!on_) return;
+    cudaEventCreate(&a_);
+    cudaEventCreate(&b_);
+    cudaEventRecord(a_, s_);
+}
+ProfScope::~ProfScope() {
+    if (!on_) return;
+    cudaEventRecord(b_, s_);
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_prof[cls_].ev.push_back({a_, b_});
+}
+
+int profile_reset() {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (auto& r : g_prof) {
+        for (auto& p : r.ev) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
+        r.ev.clear();
+    }
+    return 0;
+}
+
+int profile_query(int cls, const char** name, double* ms, long long* n) {
+    if (cls < 0 || cls >= KC_COUNT) return XPCS_EINVAL;
+    std::lock_guard<std::mutex> lk(g_mu);
+    double tot = 0.0;
+    for (auto& p : g_prof[cls].ev) {
+        cudaEventSynchronize(p.second);
+        float t = 0.f;
+        if (cudaEventElapsedTime(&t, p.first, p.second) == cudaSuccess) tot += t;
+        else cudaGetLastError();
+    }
+    if (name) *name = kClassNames[cls];
+    if (ms) *ms = tot;
+    if (n) *n = (long long)g_prof[cls].ev.size();
+    return 0;
+}
+
+}  // namespace xpcs

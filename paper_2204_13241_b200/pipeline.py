@@ -1,0 +1,119 @@
+"""One pass of the whole hot path for a workload, through the C ABI.
+
+    I(q,t)      xpcs_intensity_grid (lattice plane) | xpcs_intensity (explicit q, e.g. Ewald detector)
+    g2(q,tau)   xpcs_g2                               Eq.(14)
+    S_b(t)      xpcs_structure_factor_shells          Eq.(12)-(13), ring average PAPER.md:192
+    g2_b(tau)   xpcs_shell_mean(g2)                   ring-averaged g2
+    beta_{W,b}  xsvs_contrast                         Eq.(15)+(17)
+
+This module is orchestration only (which ABI call, with which buffers); it contains no arithmetic of the method.
+``run_host`` is the end-to-end entry a user calls with host arrays: pinned host -> device copy of the step's
+inputs, the device pass, and the device -> host copy of its results.
+"""
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+import torch
+
+from . import _lib as X
+
+
+@dataclasses.dataclass
+class Workload:
+    name: str
+    N: int
+    L: float
+    T: int
+    n_plane: int = 0            # lattice plane n x n (0 = explicit q list)
+    q: torch.Tensor | None = None   # explicit q [n_q][3] (device) when n_plane == 0
+    q_max: float = 0.0          # ring range for explicit q
+    lags: tuple = ()
+    windows: tuple = ()
+    n_bins: int = 32
+    in_dtype: int = X.F32
+    engine: int = X.ENGINE_AUTO
+
+
+class Pipeline:
+    def __init__(self, wl: Workload, device="cuda", stream=None):
+        self.wl = wl
+        self.device = torch.device(device)
+        self.stream = stream
+        if wl.n_plane:
+            self.grid = X.lattice_plane(wl.L, wl.n_plane, 0)
+            self.n_q = self.grid.n_q
+            # ring unit w = n / (2 n_bins) pixels: rings cover the inscribed disk |h|,|k| < n/2 (R8)
+            self.bins = X.xpcs_lattice_bins(self.grid, wl.n_bins, wl.n_plane // (2 * wl.n_bins), self.device, stream)
+        else:
+            assert wl.q is not None
+            self.grid = None
+            self.n_q = wl.q.shape[0]
+            self.bins = X.xpcs_radial_bins(wl.q, wl.q_max, wl.n_bins, stream)
+        odt = torch.float64 if wl.in_dtype == X.F64 else torch.float32
+        self.I = torch.empty((wl.T, self.n_q), dtype=odt, device=self.device)
+        self.g2 = torch.empty((len(wl.lags), self.n_q), dtype=torch.float32, device=self.device) if wl.lags else None
+
+    @property
+    def pairs_per_step(self) -> int:
+        return int(self.wl.N) * int(self.n_q) * int(self.wl.T)
+
+    def run(self, positions: torch.Tensor, form_factors: torch.Tensor | None, profile=False) -> dict:
+        wl, s = self.wl, self.stream
+        if self.grid is not None:
+            X.xpcs_intensity_grid(positions, form_factors, self.grid, out=self.I, engine=wl.engine, stream=s,
+                                  profile=profile)
+        else:
+            X.xpcs_intensity(positions, form_factors, wl.q, wl.L, out=self.I, stream=s, profile=profile)
+        out = {"I": self.I}
+        out["S_rings"] = X.xpcs_structure_factor_shells(self.I, form_factors, wl.N, self.bins, wl.n_bins, stream=s,
+                                                        profile=profile)
+        if wl.lags:
+            X.xpcs_g2(self.I, wl.lags, out=self.g2, out_dtype=X.F32, stream=s, profile=profile)
+            out["g2"] = self.g2
+            out["g2_rings"] = X.xpcs_shell_mean(self.g2, self.bins, wl.n_bins, stream=s, profile=profile)
+        if wl.windows:
+            out["beta"] = X.xsvs_contrast(self.I, self.bins, wl.n_bins, wl.windows, stream=s, profile=profile)
+        return out
+
+    # ---------------------------------------------------------------- end to end from host memory
+    def alloc_host_io(self, pos_host: np.ndarray, f_host: np.ndarray | None):
+        """Pinned host copies of the inputs and pinned result buffers (allocated once, reused per step)."""
+        self.h_pos = torch.from_numpy(np.ascontiguousarray(pos_host)).pin_memory()
+        self.h_f = torch.from_numpy(np.ascontiguousarray(f_host)).pin_memory() if f_host is not None else None
+        self.d_pos = torch.empty(self.h_pos.shape, dtype=self.h_pos.dtype, device=self.device)
+        self.d_f = torch.empty(self.h_f.shape, dtype=self.h_f.dtype, device=self.device) if f_host is not None else None
+        self.h_out = {}
+
+    def run_host(self) -> dict:
+        """H2D (pinned) -> one device pass -> D2H of every result (I, S rings, g2, g2 rings, beta)."""
+        self.d_pos.copy_(self.h_pos, non_blocking=True)
+        if self.d_f is not None:
+            self.d_f.copy_(self.h_f, non_blocking=True)
+        out = self.run(self.d_pos, self.d_f)
+        for k, v in out.items():
+            if k not in self.h_out:
+                self.h_out[k] = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
+            self.h_out[k].copy_(v, non_blocking=True)
+        return self.h_out
+
+    def io_bytes(self):
+        h2d = self.h_pos.numel() * self.h_pos.element_size()
+        if self.h_f is not None:
+            h2d += self.h_f.numel() * self.h_f.element_size()
+        d2h = sum(v.numel() * v.element_size() for v in self.h_out.values())
+        return h2d, d2h
+
+
+def workload_from_config(cfg, device="cuda", stream=None) -> Workload:
+    """Map an xpcs_inputs.Config onto the pipeline (geometry computed on the device for explicit-q configs)."""
+    import xpcs_inputs as xi
+    in_dtype = X.F64 if cfg.dtype == "f64" else X.F32
+    if cfg.n_plane:
+        return Workload(cfg.name, cfg.N, cfg.L, cfg.T, n_plane=cfg.n_plane, lags=tuple(cfg.lags),
+                        windows=tuple(cfg.windows), n_bins=cfg.n_bins, in_dtype=in_dtype)
+    q = X.xpcs_qgrid_ewald(xi.EWALD_WAVELENGTH_SIGMA, cfg.detector, cfg.detector, xi.EWALD_PITCH_RAD,
+                           out_dtype=in_dtype, device=device, stream=stream)
+    return Workload(cfg.name, cfg.N, cfg.L, cfg.T, n_plane=0, q=q, q_max=xi.EWALD_QMAX, lags=tuple(cfg.lags),
+                    windows=tuple(cfg.windows), n_bins=cfg.n_bins, in_dtype=in_dtype)

@@ -1,0 +1,83 @@
+"""CPU-side checks of the boundary: the library builds for sm_100a, loads, exports every symbol that
+include/xpcs.h declares, and its host-only / validation paths behave as documented (no compute calls)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2204_13241_b200 as xp
+from paper_2204_13241_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "xpcs.h")).read()
+    return sorted(set(re.findall(r"^XPCS_API\s+(?:const\s+)?\w+\*?\s+(\w+)\(", src, re.M)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2204_13241_b200 import build
+    build.build()
+    return _lib.load()
+
+
+def test_every_declared_symbol_is_exported(lib):
+    decl = _declared()
+    assert len(decl) >= 15
+    for name in decl:
+        assert hasattr(lib, name), name
+    assert sorted(_lib.EXPORTED) == decl
+
+
+def test_sass_is_sm100a(lib):
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_lattice_plane_host_helper(lib):
+    g = xp.lattice_plane(34.2, 256, 0)
+    assert (g.h0, g.n_h, g.k0, g.n_k) == (-128, 256, -128, 256)
+    assert list(g.ma) == [1, 0, 0] and list(g.mb) == [0, 1, 0] and list(g.m0) == [0, 0, 0]
+    g = _lib.QGrid()
+    rc = lib.xpcs_qgrid_lattice_plane(-1.0, 4, 0, ctypes.byref(g))
+    assert rc == _lib.XPCS_EINVAL and b"L must" in lib.xpcs_last_error()
+
+
+def test_validation_rejects_before_any_launch(lib):
+    """EINVAL paths never touch the device (they run in this GPU-less container)."""
+    n0 = lib.xpcs_launch_count()
+    o = _lib.Opts(0, 0, None, 0, 0)
+    rc = lib.xpcs_intensity(None, 10, None, None, 5, 1, 1.0, None, ctypes.byref(o))
+    assert rc == _lib.XPCS_EINVAL and b"must not be NULL" in lib.xpcs_last_error()
+    dummy = ctypes.c_void_p(16)
+    rc = lib.xpcs_intensity(dummy, 0, None, dummy, 5, 1, 1.0, dummy, ctypes.byref(o))
+    assert rc == _lib.XPCS_EINVAL and b"N must be > 0" in lib.xpcs_last_error()
+    rc = lib.xpcs_intensity(dummy, 10, None, dummy, 5, 1, -2.0, dummy, ctypes.byref(o))
+    assert rc == _lib.XPCS_EINVAL
+    bad = _lib.Opts(7, 0, None, 0, 0)
+    rc = lib.xpcs_intensity(dummy, 10, None, dummy, 5, 1, 1.0, dummy, ctypes.byref(bad))
+    assert rc == _lib.XPCS_EINVAL and b"dtype" in lib.xpcs_last_error()
+    lags, lp = _lib._i32_array([1, 5, 9])
+    rc = lib.xpcs_g2(dummy, 9, 4, lp, 3, dummy, ctypes.byref(o))
+    assert rc == _lib.XPCS_EINVAL and b"lag 9" in lib.xpcs_last_error()
+    w, wp = _lib._i32_array([1, 0])
+    rc = lib.xsvs_contrast(dummy, 9, 4, dummy, 3, wp, 2, dummy, ctypes.byref(o))
+    assert rc == _lib.XPCS_EINVAL and b"window 0" in lib.xpcs_last_error()
+    g = xp.lattice_plane(10.0, 8)
+    g.n_h = 0
+    rc = lib.xpcs_intensity_grid(dummy, 10, None, ctypes.byref(g), 1, dummy, ctypes.byref(o))
+    assert rc == _lib.XPCS_EINVAL
+    rc = lib.xpcs_profile_query(99, None, None, None)
+    assert rc == _lib.XPCS_EINVAL
+    assert lib.xpcs_launch_count() == n0
+
+
+def test_binding_refuses_host_tensors(lib):
+    torch = pytest.importorskip("torch")
+    with pytest.raises(ValueError, match="device memory"):
+        _lib._ptr(torch.zeros(3))
