@@ -231,13 +231,14 @@ def main():
     pairs_launch = pairs_step / launches_per_step
     peaks, peak_src = _peaks()
     sm_count, _ = xp.device_info()
-    used = os.environ.get("XPCS_BENCH_ENGINE_USED", "")
+    tc_used = bool(cfg.n_plane) and wl.in_dtype == xp.F32 and engine != xp.ENGINE_SIMT and \
+        xp.engine_available(xp.ENGINE_TENSOR)
     if cfg.n_plane == 0:
         # generic q: 2 XU (MUFU) ops per pair; peak = 148 SM x 16 XU/clk x max clock
         peak = sm_count * 16 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 2 / 1e12
         roof = {"bound": "alu", "unit": "Tpairs/s (XU: 2 MUFU per pair)", "peak": peak,
                 "achieved": pairs_launch / (per_launch_ms / 1e3) / 1e12}
-    elif wl.in_dtype == xp.F32 and engine != xp.ENGINE_SIMT and "tensor" in used:
+    elif tc_used:
         # tcgen05 split-FP16: 3 fp16 products x 4 real MAC = 24 flop per pair vs measured bf16 (= fp16) dense peak
         peak = peaks["bf16_tflops_sustained"]
         roof = {"bound": "tensor", "unit": "TFLOP/s", "peak": peak,
@@ -291,6 +292,7 @@ def main():
                 "config": {"workload": cfg.name, "N": cfg.N, "n_q": P.n_q, "frames": cfg.T,
                            "lags": len(cfg.lags), "windows": list(cfg.windows), "rings": cfg.n_bins,
                            "pairs_per_step_per_gpu": pairs_step, "engine": args.engine,
+                           "engine_used": "tensor" if tc_used else ("simt" if cfg.n_plane and wl.in_dtype == xp.F32 else "generic/f64"),
                            "l2": "flushed between timed steps (256 MB write, untimed)",
                            "parallelism": f"weak x{ws} (independent trajectories)"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(n_launch),

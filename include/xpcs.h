@@ -176,6 +176,9 @@ XPCS_API int64_t xpcs_launch_count(void);
 XPCS_API int xpcs_profile_reset(void);
 XPCS_API int xpcs_profile_query(int32_t kernel_class, const char** name, double* total_ms, int64_t* launches);
 XPCS_API int xpcs_device_info(int32_t* sm_count, int32_t* sm_clock_khz);
+/* 1 if xpcs_intensity_grid can run the given xpcs_engine on the current device (AUTO resolves to TENSOR when
+ * this returns 1 for TENSOR), else 0.  Set XPCS_DISABLE_TC=1 in the environment to force the SIMT engine. */
+XPCS_API int xpcs_engine_available(int32_t engine);
 XPCS_API int xpcs_version(void);
 
 #ifdef __cplusplus

@@ -23,7 +23,7 @@ EXPORTED = (
     "xpcs_intensity", "xpcs_intensity_grid", "xpcs_g2", "xsvs_contrast", "xpcs_shell_mean",
     "xpcs_structure_factor_shells", "xpcs_qgrid_lattice_plane", "xpcs_qgrid_ewald", "xpcs_lattice_bins",
     "xpcs_radial_bins", "xpcs_last_error", "xpcs_release", "xpcs_launch_count", "xpcs_profile_reset",
-    "xpcs_profile_query", "xpcs_device_info", "xpcs_version",
+    "xpcs_profile_query", "xpcs_device_info", "xpcs_version", "xpcs_engine_available",
 )
 
 
@@ -82,6 +82,7 @@ def load():
                                ctypes.POINTER(ctypes.c_int64)],
         "xpcs_device_info": [ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)],
         "xpcs_version": [],
+        "xpcs_engine_available": [i32],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -278,6 +279,10 @@ def profile_query():
 
 def release():
     _check(load().xpcs_release())
+
+
+def engine_available(engine) -> bool:
+    return bool(load().xpcs_engine_available(int(engine)))
 
 
 def device_info():

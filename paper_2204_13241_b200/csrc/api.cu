@@ -165,6 +165,13 @@ int xpcs_device_info(int32_t* sm, int32_t* clk) {
     return XPCS_OK;
 }
 
+int xpcs_engine_available(int32_t engine) {
+    if (engine == XPCS_ENGINE_SIMT) return 1;
+    LatticeGeom g{};
+    if (engine == XPCS_ENGINE_TENSOR || engine == XPCS_ENGINE_AUTO) return lattice_tc_supported(g) ? 1 : (engine == XPCS_ENGINE_AUTO);
+    return 0;
+}
+
 // ------------------------------------------------------------------------------------------- intensity
 int xpcs_intensity(const void* positions, int64_t N, const void* form_factors, const void* q_vectors, int64_t n_q,
                    int64_t frames, double box_L, void* I_out, const xpcs_opts* opts) {
@@ -267,7 +274,18 @@ int xpcs_intensity_grid(const void* positions, int64_t N, const void* form_facto
             return XPCS_EUNSUPPORTED;
         }
     }
-    const int64_t chunk = tc ? 4096 : 4096;
+    // atom chunks (split-K over CTAs, folded in FP64 by the reduction): SIMT keeps fp32 register sums short
+    // (<= 4096 atoms); the tensor engine drains TMEM every 128 atoms into RN sums, so its chunks only balance
+    // the grid (>= ~8 waves of one CTA per SM) and stay >= 1024 atoms.
+    int64_t chunk = 4096;
+    if (tc) {
+        const int64_t tiles = ((g.n_h + 127) / 128) * ((g.n_k + 127) / 128);
+        const int64_t units = tiles * std::min<int64_t>(frames, 64);
+        int64_t C0 = std::max<int64_t>(1, (8LL * sm_count() + units - 1) / units);
+        C0 = std::min<int64_t>(C0, std::max<int64_t>(1, N / 1024));
+        chunk = ((N + C0 - 1) / C0 + 15) / 16 * 16;
+    }
+    if (const char* e = getenv("XPCS_CHUNK_ATOMS")) chunk = std::max<int64_t>(16, atoll(e));   // experiments only
     const int64_t C = (N + chunk - 1) / chunk;
     const int64_t Tb = std::max<int64_t>(1, std::min<int64_t>(frames, (int64_t)(kBatchBytes / std::max<int64_t>(16 * N, 8 * C * n_q))));
     uint4* st = (uint4*)scratch(o.s, SS_STAGE, sizeof(uint4) * (size_t)(N * Tb));

@@ -4,7 +4,7 @@
 //     p^e(h,k) = sum_j X_h(j) W_k(j),   X_h(j) = e^{-2 pi i h Th_a(j)},  W_k(j) = f_j e^{-2 pi i (Th_0(j) + k Th_b(j))}
 // with Th_v the staged 32-bit turns (k_stage.cu).  Per CTA: a TH x TK pixel tile of one frame and a chunk of
 // <= chunk_atoms atoms.  Per 16-atom sub-block the CTA generates the 16 x (TH + TK) phasors into shared memory
-// (accurate sincospif from the exact integer turns h * Th_a mod 2^32), then every thread accumulates a
+// (exact integer turns h * Th_a mod 2^32 -> SFU sin/cos, |error| < 1e-6 per phasor), then every thread accumulates a
 // RH x RK register tile of complex MACs with packed FFMA2:
 //     (re, im) += (xr, xr) * (wr, wi) ;  (re, im) += (-xi, xi) * (wi, wr)        -> 2 FFMA2 per atom.q pair
 // fp32 accumulation never spans more than chunk_atoms (<= 4096) atoms; chunks are combined in FP64 by the
@@ -52,7 +52,7 @@ k_lattice_simt(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64
             if (j < a_end) {
                 const uint4 st = S[j];
                 const uint32_t T = (uint32_t)(g.h0 + th0 + m) * st.x;       // h * Th_a mod 2^32 (exact)
-                sincospif(2.0f * turns_signed(T), &s, &c);
+                __sincosf(turns_to_radians(T), &s, &c);
             }
             // X = cos - i sin  ->  (xr, xr, -xi, xi) = (c, c, s, -s)
             Xs[a * TH + m] = make_float4(c, c, s, -s);
@@ -64,7 +64,7 @@ k_lattice_simt(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64
             if (j < a_end) {
                 const uint4 st = S[j];
                 const uint32_t T = st.z + (uint32_t)(g.k0 + tk0 + m) * st.y;  // Th_0 + k Th_b mod 2^32
-                sincospif(2.0f * turns_signed(T), &s, &c);
+                __sincosf(turns_to_radians(T), &s, &c);
                 f = __uint_as_float(st.w);
             }
             const float wr = f * c, wi = -f * s;

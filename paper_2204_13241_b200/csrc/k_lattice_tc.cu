@@ -1,13 +1,314 @@
-// k_lattice_tc.cu -- K3: lattice-plane amplitude on the tcgen05 tensor cores (placeholder until implemented).
+// k_lattice_tc.cu -- K3: lattice-plane amplitude on the 5th-generation tensor cores (tcgen05, TMEM accumulators).
+//
+// The per-axis factorisation of Eq.(7) on a reciprocal-lattice plane,
+//     p^e(h,k) = sum_j X_h(j) W_k(j),   X_h(j) = e^{-2 pi i h Th_a(j)},  W_k(j) = f_j e^{-2 pi i (Th_0(j) + k Th_b(j))},
+// is a complex matrix product with the atoms as the contraction dimension K.  Each CTA owns a 128 (h) x 128 (k)
+// pixel tile of one frame and a chunk of <= 4096 atoms (split-K; chunks are folded in FP64 by k_amp_reduce):
+//     Re = Xr Wr^T - Xi Wi^T ,   Im = Xr Wi^T + Xi Wr^T           (A-negate bit of the instruction descriptor)
+// on tcgen05.mma.cta_group::1.kind::f16, M = 128, N = 128, K = 16, FP32 accumulators in TMEM (256 columns).
+// Precision: every phasor component v is split v = hi + lo with hi = fp16(v), lo = fp16(v - hi) and each real
+// product uses three MMAs (hi.hi + hi.lo + lo.hi; the dropped lo.lo term is < 2^-22 per term), i.e. FP32-class
+// products (a single fp16/tf32 pass fails the 1e-3 N gate).
+//
+// Accumulation: the tcgen05 FP32 accumulator is not round-to-nearest (measured: the error of a TMEM accumulation
+// grows linearly with its length, SURVEY A.8 / DESIGN.md "tensor accumulator"), so no TMEM accumulator ever sums
+// more than SUB_STAGES * 16 = 128 atoms: two TMEM accumulators (2 x 256 columns) alternate, and while the MMA
+// fills one, four drain warps add the other into round-to-nearest FP32 running sums in shared memory.
+//
+// One CTA per SM (TMEM 512 columns), 21 warps: warps 0-15 generate the phasor planes of 16-atom stages into a
+// 3-stage shared-memory ring (exact integer turns -> SFU sin/cos -> fp16 hi/lo, K-major canonical no-swizzle
+// layout); warps 16-19 drain TMEM and write the tile; warp 20 allocates TMEM and one lane issues the 12 MMAs per
+// stage.  Producer -> MMA: mbarrier full[s] (16 warp arrivals after fence.proxy.async); MMA -> producer:
+// tcgen05.commit -> empty[s]; MMA -> drain: tcgen05.commit -> tfull[b]; drain -> MMA: tempty[b] (4 arrivals).
 #include "common.cuh"
+#include <cuda_fp16.h>
 
 namespace xpcs {
 
-bool lattice_tc_supported(const LatticeGeom&) { return false; }
+namespace tc {
+constexpr int TM = 128, TN = 128, KS = 16;        // tile rows (h), tile cols (k), atoms per stage
+constexpr int STAGES = 3;
+constexpr int SUB_STAGES = 8;                     // stages per TMEM accumulator (128 atoms)
+constexpr int PLANE = TM * KS * 2;                // bytes per fp16 plane (128 rows x 16 atoms)
+constexpr int STAGE_BYTES = 8 * PLANE;            // Xr_hi Xr_lo Xi_hi Xi_lo Wr_hi Wr_lo Wi_hi Wi_lo
+constexpr int NPROD_WARPS = 16, NDRAIN_WARPS = 4;
+constexpr int MMA_WARP = NPROD_WARPS + NDRAIN_WARPS;
+constexpr int NTHREADS = (MMA_WARP + 1) * 32;     // 672
+constexpr int TMEM_COLS = 512;                    // buffer b: Re cols [256b, 256b+128), Im [256b+128, 256b+256)
+constexpr int SUM_LD = 129;                       // running sums [256 cols][129] fp32 (padded: conflict-free)
+constexpr int SUM_BYTES = 256 * SUM_LD * 4;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + SUM_BYTES + 1024 + 256;
+}  // namespace tc
 
-cudaError_t launch_lattice_tc(const uint4*, int64_t, int64_t, const LatticeGeom&, int64_t, int64_t, float2*,
-                              cudaStream_t) {
-    return cudaErrorNotSupported;
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.release.cta.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// UMMA shared-memory descriptor, K-major, no swizzle: core matrix = 8 rows x 16 B contiguous (128 B);
+// LBO = byte distance between the two K-adjacent core matrices, SBO = between 8-row groups; version 1 (sm_100).
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;                      // descriptor version for tcgen05
+    return d;                                     // base offset 0, lbo mode 0, layout SWIZZLE_NONE (0)
+}
+
+// kind::f16 instruction descriptor: D fp32, A/B fp16, K-major both, N = TN, M = TM.
+__host__ __device__ constexpr uint32_t idesc_f16(bool neg_a) {
+    return (1u << 4) | (0u << 7) | (0u << 10) | ((neg_a ? 1u : 0u) << 13) | ((uint32_t)(tc::TN >> 3) << 17) |
+           ((uint32_t)(tc::TM >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+#define TMEM_LD32(taddr, r)                                                                                        \
+    asm volatile(                                                                                                  \
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18," \
+        "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                            \
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),         \
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),   \
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), \
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])  \
+        : "r"(taddr))
+
+// byte offset of element (row m, atom a) inside one plane: [m/8][a/8][m%8][a%8] fp16
+__device__ __forceinline__ uint32_t plane_off(int m, int a) {
+    return (uint32_t)((m >> 3) * 256 + (a >> 3) * 128 + (m & 7) * 16 + (a & 7) * 2);
+}
+
+// store v0 (atom a), v1 (atom a+1) as fp16 hi/lo pairs
+__device__ __forceinline__ void store_split(char* hi_plane, char* lo_plane, uint32_t off, float v0, float v1) {
+    const __half2 h = __floats2half2_rn(v0, v1);
+    const float2 hf = __half22float2(h);
+    const __half2 l = __floats2half2_rn(v0 - hf.x, v1 - hf.y);
+    *reinterpret_cast<__half2*>(hi_plane + off) = h;
+    *reinterpret_cast<__half2*>(lo_plane + off) = l;
+}
+
+__global__ void __launch_bounds__(tc::NTHREADS, 1)
+k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t chunk_atoms, int tiles_k,
+             float2* __restrict__ partial, int64_t frames, int dbg_flags) {
+    using namespace tc;
+    extern __shared__ __align__(1024) char smem_raw[];
+    char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    float* sums = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + SUM_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tile = blockIdx.x;
+    const int th0 = (tile / tiles_k) * TM, tk0 = (tile % tiles_k) * TN;
+    const int64_t chunk = blockIdx.y, t = blockIdx.z;
+    const int64_t a_begin = chunk * chunk_atoms, a_end = min(N, a_begin + chunk_atoms);
+    const int n_stages = (int)((a_end - a_begin + KS - 1) / KS);
+    const int n_sub = (n_stages + SUB_STAGES - 1) / SUB_STAGES;
+    const uint4* S = staged + t * N;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], NPROD_WARPS); mbar_init(&empty[s], 1); }
+        for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], NDRAIN_WARPS); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == MMA_WARP) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == MMA_WARP) {
+        // ================= MMA issuer (one lane) =================
+        if (lane == 0) {
+            const uint32_t id_pos = idesc_f16(false), id_neg = idesc_f16(true);
+            const uint32_t lo_on = dbg_flags & 1 ? 0u : 1u;   // experiments: bit 0 drops the hi.lo / lo.hi products
+            const uint32_t base = smem_u32(smem);
+            for (int i = 0; i < n_stages; ++i) {
+                const int s = i % STAGES;
+                const int u = i / SUB_STAGES, b = u & 1;
+                const bool sub_first = (i % SUB_STAGES) == 0;
+                if (sub_first) {   // accumulator b must have been drained (its previous use was sub-chunk u - 2)
+                    mbar_wait(&tempty[b], (uint32_t)(((u >> 1) + 1) & 1));
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                }
+                mbar_wait(&full[s], (uint32_t)((i / STAGES) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t sb = base + s * STAGE_BYTES;
+                uint64_t d[8];
+#pragma unroll
+                for (int p = 0; p < 8; ++p) d[p] = umma_desc(sb + p * PLANE, 128, 256);
+                // planes: 0 Xr_hi 1 Xr_lo 2 Xi_hi 3 Xi_lo 4 Wr_hi 5 Wr_lo 6 Wi_hi 7 Wi_lo
+                const uint32_t re = tmem + (uint32_t)(b * 256), im = re + TN;
+                const uint32_t first = sub_first ? 0u : 1u;
+                umma_f16(re, d[0], d[4], id_pos, first);     // Re += Xr Wr
+                if (lo_on) { umma_f16(re, d[0], d[5], id_pos, 1); umma_f16(re, d[1], d[4], id_pos, 1); }
+                umma_f16(re, d[2], d[6], id_neg, 1);         // Re -= Xi Wi
+                if (lo_on) { umma_f16(re, d[2], d[7], id_neg, 1); umma_f16(re, d[3], d[6], id_neg, 1); }
+                umma_f16(im, d[0], d[6], id_pos, first);     // Im += Xr Wi
+                if (lo_on) { umma_f16(im, d[0], d[7], id_pos, 1); umma_f16(im, d[1], d[6], id_pos, 1); }
+                umma_f16(im, d[2], d[4], id_pos, 1);         // Im += Xi Wr
+                if (lo_on) { umma_f16(im, d[2], d[5], id_pos, 1); umma_f16(im, d[3], d[4], id_pos, 1); }
+                umma_commit(&empty[s]);                      // frees the stage when these MMAs complete
+                if ((i % SUB_STAGES) == SUB_STAGES - 1 || i == n_stages - 1) umma_commit(&tfull[b]);
+            }
+        }
+        __syncwarp();
+    } else if (warp < NPROD_WARPS) {
+        // ================= phasor producers =================
+        // thread -> fixed atom pair (a, a+1) of every stage; per item one core matrix (8 rows x 8 atoms) of a plane
+        const int ah = warp & 1;
+        const int a_loc = ah * 8 + 2 * (lane & 3);
+        const int mrow = lane >> 2;
+        for (int i = 0; i < n_stages; ++i) {
+            const int s = i % STAGES;
+            mbar_wait(&empty[s], (uint32_t)(((i / STAGES) + 1) & 1));
+            char* st = smem + s * STAGE_BYTES;
+            const int64_t j0 = a_begin + (int64_t)i * KS + a_loc;
+            uint4 at0 = make_uint4(0, 0, 0, 0), at1 = make_uint4(0, 0, 0, 0);
+            if (j0 < a_end) at0 = __ldg(S + j0);
+            if (j0 + 1 < a_end) at1 = __ldg(S + j0 + 1);
+            const float f0 = __uint_as_float(at0.w), f1 = __uint_as_float(at1.w);   // 0 for padding atoms
+            const float x0 = (j0 < a_end) ? 1.f : 0.f, x1 = (j0 + 1 < a_end) ? 1.f : 0.f;
+#pragma unroll
+            for (int it = 0; it < 2; ++it) {
+                const int m = ((warp >> 1) + 8 * it) * 8 + mrow;          // row within the tile
+                const uint32_t off = plane_off(m, a_loc);
+                {   // X_h, h = h0 + th0 + m
+                    const uint32_t hh = (uint32_t)(g.h0 + th0 + m);
+                    float s0, c0, s1, c1;
+                    __sincosf(turns_to_radians(hh * at0.x), &s0, &c0);
+                    __sincosf(turns_to_radians(hh * at1.x), &s1, &c1);
+                    store_split(st + 0 * PLANE, st + 1 * PLANE, off, x0 * c0, x1 * c1);     // Xr =  cos
+                    store_split(st + 2 * PLANE, st + 3 * PLANE, off, -x0 * s0, -x1 * s1);   // Xi = -sin
+                }
+                {   // W_k, k = k0 + tk0 + m
+                    const uint32_t kk = (uint32_t)(g.k0 + tk0 + m);
+                    float s0, c0, s1, c1;
+                    __sincosf(turns_to_radians(at0.z + kk * at0.y), &s0, &c0);
+                    __sincosf(turns_to_radians(at1.z + kk * at1.y), &s1, &c1);
+                    store_split(st + 4 * PLANE, st + 5 * PLANE, off, f0 * c0, f1 * c1);     // Wr =  f cos
+                    store_split(st + 6 * PLANE, st + 7 * PLANE, off, -f0 * s0, -f1 * s1);   // Wi = -f sin
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> async proxy
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[s]);
+        }
+    } else {
+        // ================= drain warps: TMEM accumulator -> RN fp32 running sums (smem) -> tile =================
+        const int quarter = warp & 3;               // TMEM lanes 32*quarter .. +31 = tile rows
+        const int r = quarter * 32 + lane;
+        for (int c = 0; c < 256; ++c) sums[c * SUM_LD + r] = 0.f;
+        for (int u = 0; u < n_sub; ++u) {
+            const int b = u & 1;
+            mbar_wait(&tfull[b], (uint32_t)((u >> 1) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * 256);
+            uint32_t v[2][32];
+#pragma unroll
+            for (int blk = 0; blk < 8; blk += 2) {
+#pragma unroll
+                for (int q = 0; q < 2; ++q) TMEM_LD32(tb + (uint32_t)((blk + q) * 32), v[q]);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (blk == 6) {   // all of accumulator b has been read: hand it back to the MMA
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[b]);
+                }
+#pragma unroll
+                for (int q = 0; q < 2; ++q)
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) sums[((blk + q) * 32 + c) * SUM_LD + r] += __uint_as_float(v[q][c]);
+            }
+        }
+        // ---- write the tile: row-major partial[chunk][t][ih][ik], coalesced along k
+        __syncwarp();
+        const int64_t n_q = g.n_h * g.n_k;
+        float2* P = partial + (chunk * frames + t) * n_q;
+        for (int rr = 0; rr < 32; ++rr) {
+            const int row = quarter * 32 + rr;
+            const int64_t ih = th0 + row;
+            if (ih >= g.n_h) break;
+#pragma unroll
+            for (int j = 0; j < TN / 32; ++j) {
+                const int c = lane + 32 * j;
+                const int64_t ik = tk0 + c;
+                if (ik < g.n_k) P[ih * g.n_k + ik] = make_float2(sums[c * SUM_LD + row], sums[(TN + c) * SUM_LD + row]);
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == MMA_WARP) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+    }
+}
+
+bool lattice_tc_supported(const LatticeGeom& g) {
+    static int ok = -1;
+    if (ok < 0) {
+        int dev = 0, major = 0, minor = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+        ok = (major == 10 && minor == 0) ? 1 : 0;
+        const char* env = getenv("XPCS_DISABLE_TC");
+        if (env && env[0] == '1') ok = 0;
+    }
+    (void)g;
+    return ok == 1;
+}
+
+cudaError_t launch_lattice_tc(const uint4* staged, int64_t N, int64_t frames, const LatticeGeom& g,
+                              int64_t chunk_atoms, int64_t n_chunks, float2* partial, cudaStream_t s) {
+    using namespace tc;
+    const int tiles_h = (int)((g.n_h + TM - 1) / TM), tiles_k = (int)((g.n_k + TN - 1) / TN);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_lattice_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        attr = true;
+    }
+    dim3 grid(tiles_h * tiles_k, (unsigned)n_chunks, (unsigned)frames);
+    note_launch();
+    static int dbg = -1;
+    if (dbg < 0) { const char* e = getenv("XPCS_TC_DEBUG"); dbg = e ? atoi(e) : 0; }
+    k_lattice_tc<<<grid, NTHREADS, SMEM_BYTES, s>>>(staged, N, g, chunk_atoms, tiles_k, partial, frames, dbg);
+    return cudaGetLastError();
 }
 
 }  // namespace xpcs

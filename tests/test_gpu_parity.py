@@ -61,16 +61,17 @@ def test_config1_fp64_full():
     np.testing.assert_allclose(I, ref, rtol=1e-9, atol=1e-9 * cfg.N)
 
 
+@pytest.mark.parametrize("engine", [xp.ENGINE_SIMT, xp.ENGINE_AUTO])
 @pytest.mark.parametrize("kind,n_cells,L,n,dtype", [("sc", 10, 10.0, 64, "f64"), ("sc", 10, 10.0, 64, "f32"),
                                                      ("fcc", 20, xi.CONFIGS["c2"].L, 256, "f32"),
                                                      ("bcc", 16, 40.0, 128, "f32")])
-def test_bragg_peaks_gpu(kind, n_cells, L, n, dtype):
+def test_bragg_peaks_gpu(kind, n_cells, L, n, dtype, engine):
     """Perfect crystals: I = N^2 at the crystal's reciprocal lattice, ~0 elsewhere (closed form; the c2-size
     FCC is config 2's own N = 32000)."""
     pos = xi.crystal(kind, n_cells, L, dtype)
     N = pos.shape[0]
     g = xp.lattice_plane(L, n)
-    I = xp.xpcs_intensity_grid(_t(pos), None, g).cpu().numpy().reshape(n, n).astype(np.float64)
+    I = xp.xpcs_intensity_grid(_t(pos), None, g, engine=engine).cpu().numpy().reshape(n, n).astype(np.float64)
     h = np.arange(-n // 2, n // 2)
     H, K = np.meshgrid(h, h, indexing="ij")
     period = 2 * n_cells if kind == "fcc" else n_cells
@@ -79,6 +80,24 @@ def test_bragg_peaks_gpu(kind, n_cells, L, n, dtype):
         peak &= ((H // period + K // period) % 2 == 0)
     np.testing.assert_allclose(I[peak], float(N) ** 2, rtol=1e-5)
     assert np.max(I[~peak]) <= 1e-3 * N
+
+
+def test_tensor_engine_available():
+    """On a B200 the AUTO engine must resolve to the tcgen05 kernel (no silent SIMT fallback)."""
+    assert xp.engine_available(xp.ENGINE_TENSOR)
+
+
+@pytest.mark.parametrize("N", [16, 1000, 4096, 20000])
+def test_tensor_engine_accumulation_length(N):
+    """The tcgen05 accumulator truncates; drains every 128 atoms keep the error flat in N."""
+    cfg = xi.scaled(xi.CONFIGS["c3"], N=N, T=1)
+    pos = xi.positions(cfg)
+    f = xi.form_factors(cfg)
+    g = xp.qgrid(cfg.L, -64, 128, -64, 128)
+    I = xp.xpcs_intensity_grid(_t(pos), _t(f), g, engine=xp.ENGINE_TENSOR).cpu().numpy()
+    ref = oracle.intensity(pos, f.astype(np.float64), _grid_q(g), cfg.L)
+    ratio, worst = assert_pixels(I, ref, N, "tc accumulation")
+    assert worst < 2e-4, worst
 
 
 def test_shift_invariance_gpu():
@@ -219,6 +238,18 @@ def _sampled_parity(cfg, frames, n_pix, seed):
     ref = oracle.intensity(pos[frames], f.astype(np.float64) if cfg.two_species else None, q[pix], cfg.L)
     assert_pixels(I[frames][:, pix], ref, cfg.N, cfg.name)
     return out, I, pos
+
+
+def test_config2_simt_engine_sampled():
+    """The SIMT engine on config 2's size (first 10 frames) against the oracle."""
+    cfg = xi.scaled(xi.CONFIGS["c2"], T=10)
+    pos = xi.positions(cfg)
+    g = xp.lattice_plane(cfg.L, cfg.n_plane)
+    I = xp.xpcs_intensity_grid(_t(pos), None, g, engine=xp.ENGINE_SIMT).cpu().numpy()
+    q = oracle.lattice_q(cfg.L, **oracle.plane_grid(cfg.n_plane))
+    pix = xi.pixel_subset(q.shape[0], 256, 7)
+    ref = oracle.intensity(pos[[0, 9]], None, q[pix], cfg.L)
+    assert_pixels(I[[0, 9]][:, pix], ref, cfg.N, "c2 simt")
 
 
 def test_config2_full_size():
