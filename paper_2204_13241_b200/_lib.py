@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libxpcs.so")
+LIB_PATH = os.environ.get("XPCS_LIB", os.path.join(_HERE, "lib", "libxpcs.so"))   # XPCS_LIB: experiments only
 
 XPCS_OK, XPCS_EINVAL, XPCS_ECUDA, XPCS_ENOMEM, XPCS_EUNSUPPORTED = 0, 1, 2, 3, 4
 F32, F64 = 0, 1

@@ -6,7 +6,7 @@
 // pixel tile of one frame and a chunk of <= 4096 atoms (split-K; chunks are folded in FP64 by k_amp_reduce):
 //     Re = Xr Wr^T - Xi Wi^T ,   Im = Xr Wi^T + Xi Wr^T           (A-negate bit of the instruction descriptor)
 // on tcgen05.mma.cta_group::1.kind::f16, M = 128, N = 128, K = 16, FP32 accumulators in TMEM (256 columns).
-// Precision: every phasor component v is split v = hi + lo with hi = fp16(v), lo = fp16(v - hi) and each real
+// Precision: every phasor component v is split v = hi + lo (hi on a 2^-10 grid, exact in fp16; lo = fp16(v - hi)) and each real
 // product uses three MMAs (hi.hi + hi.lo + lo.hi; the dropped lo.lo term is < 2^-22 per term), i.e. FP32-class
 // products (a single fp16/tf32 pass fails the 1e-3 N gate).
 //
@@ -26,18 +26,25 @@
 namespace xpcs {
 
 namespace tc {
-constexpr int TM = 128, TN = 128, KS = 16;        // tile rows (h), tile cols (k), atoms per stage
+constexpr int TM = 128, TN = 128, KS = 16;        // rows (h) per CTA, tile cols (k), atoms per stage
+constexpr int PAIR_M = 2 * TM;                    // a CTA pair (cluster of 2 SMs) owns 256 h x 128 k
+constexpr int BN = TN / 2;                        // each CTA of the pair holds half of B (64 k rows)
 constexpr int STAGES = 3;
-constexpr int SUB_STAGES = 8;                     // stages per TMEM accumulator (128 atoms)
-constexpr int PLANE = TM * KS * 2;                // bytes per fp16 plane (128 rows x 16 atoms)
-constexpr int STAGE_BYTES = 8 * PLANE;            // Xr_hi Xr_lo Xi_hi Xi_lo Wr_hi Wr_lo Wi_hi Wi_lo
+#ifndef XPCS_TC_SUB_STAGES
+#define XPCS_TC_SUB_STAGES 16
+#endif
+constexpr int SUB_STAGES = XPCS_TC_SUB_STAGES;    // stages per TMEM accumulator (16 stages = 256 atoms)
+constexpr int APLANE = TM * KS * 2;               // bytes per fp16 A plane (128 rows x 16 atoms)
+constexpr int BPLANE = BN * KS * 2;               // bytes per fp16 B plane (64 rows x 16 atoms)
+constexpr int STAGE_BYTES = 4 * APLANE + 4 * BPLANE;   // Xr_hi Xr_lo Xs_hi Xs_lo | Wr_hi Wr_lo Ws_hi Ws_lo
 constexpr int NPROD_WARPS = 16, NDRAIN_WARPS = 4;
 constexpr int MMA_WARP = NPROD_WARPS + NDRAIN_WARPS;
 constexpr int NTHREADS = (MMA_WARP + 1) * 32;     // 672
-constexpr int TMEM_COLS = 512;                    // buffer b: Re cols [256b, 256b+128), Im [256b+128, 256b+256)
+constexpr int TMEM_COLS = 512;                    // buffer b: Re cols [256b, 256b+128), Im' [256b+128, 256b+256)
 constexpr int SUM_LD = 129;                       // running sums [256 cols][129] fp32 (padded: conflict-free)
 constexpr int SUM_BYTES = 256 * SUM_LD * 4;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + SUM_BYTES + 1024 + 256;
+constexpr int ASLOT_BYTES = NPROD_WARPS * 2 * 16 * 16;   // per producer warp: 2 x 16 atom records (cp.async)
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + SUM_BYTES + ASLOT_BYTES + 1024 + 256;
 }  // namespace tc
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -70,10 +77,10 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
     return d;                                     // base offset 0, lbo mode 0, layout SWIZZLE_NONE (0)
 }
 
-// kind::f16 instruction descriptor: D fp32, A/B fp16, K-major both, N = TN, M = TM.
+// kind::f16 instruction descriptor: D fp32, A/B fp16, K-major both, N = TN, M = PAIR_M (cta_group::2).
 __host__ __device__ constexpr uint32_t idesc_f16(bool neg_a) {
     return (1u << 4) | (0u << 7) | (0u << 10) | ((neg_a ? 1u : 0u) << 13) | ((uint32_t)(tc::TN >> 3) << 17) |
-           ((uint32_t)(tc::TM >> 4) << 24);
+           ((uint32_t)(tc::PAIR_M >> 4) << 24);
 }
 
 __device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
@@ -87,6 +94,54 @@ __device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t a, uint64_t b
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
+}
+
+// ---- CTA-pair (cluster of 2) helpers
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// address of the same shared variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void umma2_f16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+// commit to the barrier at the same offset in both CTAs of the pair
+__device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+            smem_u32(bar))
+        : "memory");
 }
 
 #define TMEM_LD32(taddr, r)                                                                                        \
@@ -104,31 +159,76 @@ __device__ __forceinline__ uint32_t plane_off(int m, int a) {
     return (uint32_t)((m >> 3) * 256 + (a >> 3) * 128 + (m & 7) * 16 + (a & 7) * 2);
 }
 
-// store v0 (atom a), v1 (atom a+1) as fp16 hi/lo pairs
-__device__ __forceinline__ void store_split(char* hi_plane, char* lo_plane, uint32_t off, float v0, float v1) {
-    const __half2 h = __floats2half2_rn(v0, v1);
-    const float2 hf = __half22float2(h);
-    const __half2 l = __floats2half2_rn(v0 - hf.x, v1 - hf.y);
-    *reinterpret_cast<__half2*>(hi_plane + off) = h;
-    *reinterpret_cast<__half2*>(lo_plane + off) = l;
+// ---- split-precision operand generation -------------------------------------------------------------
+// hi = v rounded to the grid 2^(e-10) with the magic constant M = 1.5 * 2^(13+e) (|v| <= 2^e: hi has <= 11
+// significant bits, so fp16(hi) is exact); lo = v - hi exactly (|lo| <= 2^(e-11)), then fp16(lo): the pair
+// represents v to ~2^(e-22).  For W = f * cos the residual comes from one FMA of the exact product f * cos.
+__device__ __forceinline__ unsigned long long fadd2(unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ unsigned long long fsub2(unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ uint32_t pack_half2(unsigned long long v) {   // (lo, hi) fp32 -> half2 bits
+    uint32_t r;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi2(v)), "f"(lo2(v)));
+    return r;
+}
+template <int OFF>
+__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.b32 [%0+%2], %1;" ::"r"(addr), "r"(v), "n"(OFF));
+}
+// v = (v0, v1) for atoms (a, a+1); M2 = (M, M); hi -> plane P, lo -> plane P + 1
+template <int OFF_HI, int OFF_LO>
+__device__ __forceinline__ void split_store(uint32_t addr, unsigned long long v, unsigned long long M2) {
+    const unsigned long long hi = fsub2(fadd2(v, M2), M2);
+    const unsigned long long lo = fsub2(v, hi);
+    sts32<OFF_HI>(addr, pack_half2(hi));
+    sts32<OFF_LO>(addr, pack_half2(lo));
+}
+// v = f * c (pairwise) with the residual taken from the exact products
+template <int OFF_HI, int OFF_LO>
+__device__ __forceinline__ void split_store_f(uint32_t addr, unsigned long long f2, unsigned long long c2,
+                                              unsigned long long M2) {
+    const unsigned long long t = ffma2(f2, c2, M2);
+    const unsigned long long hi = fsub2(t, M2);
+    const unsigned long long nhi = fsub2(M2, t);                  // -hi
+    unsigned long long lo;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(lo) : "l"(f2), "l"(c2), "l"(nhi));
+    sts32<OFF_HI>(addr, pack_half2(hi));
+    sts32<OFF_LO>(addr, pack_half2(lo));
+}
+// M = 1.5 * 2^(13 + e), e = max(0, exponent bound of |f|) so that |f| <= 2^e
+__device__ __forceinline__ float split_magic(float f) {
+    const int ef = (int)((__float_as_uint(f) >> 23) & 0xFF);
+    const int e = max(0, ef - 126);
+    return __uint_as_float(((uint32_t)(140 + e) << 23) | 0x00400000u);
 }
 
-__global__ void __launch_bounds__(tc::NTHREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::NTHREADS, 1)
 k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t chunk_atoms, int tiles_k,
              float2* __restrict__ partial, int64_t frames, int dbg_flags) {
     using namespace tc;
     extern __shared__ __align__(1024) char smem_raw[];
     char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     float* sums = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + SUM_BYTES);
+    uint4* aslot = reinterpret_cast<uint4*>(smem + STAGES * STAGE_BYTES + SUM_BYTES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + SUM_BYTES + ASLOT_BYTES);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tile = blockIdx.x;
-    const int th0 = (tile / tiles_k) * TM, tk0 = (tile % tiles_k) * TN;
+    const uint32_t rank = cluster_rank();                  // 0 = leader (issues the pair's MMAs)
+    const int ptile = blockIdx.x >> 1;                     // pair tile: 256 h x 128 k
+    const int th0 = (ptile / tiles_k) * PAIR_M + (int)rank * TM;   // this CTA's 128 h rows (A half)
+    const int tk0 = (ptile % tiles_k) * TN;                        // the pair's 128 k columns
+    const int bk0 = tk0 + (int)rank * BN;                          // this CTA's 64 k rows of B
     const int64_t chunk = blockIdx.y, t = blockIdx.z;
     const int64_t a_begin = chunk * chunk_atoms, a_end = min(N, a_begin + chunk_atoms);
     const int n_stages = (int)((a_end - a_begin + KS - 1) / KS);
@@ -136,24 +236,26 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
     const uint4* S = staged + t * N;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], NPROD_WARPS); mbar_init(&empty[s], 1); }
-        for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], NDRAIN_WARPS); }
+        // full[s]: the 16 local producer warps (+ 1 forwarded arrival from the peer in the leader); tempty[b]: the
+        // 4 drain warps of each CTA (in the leader)
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], NPROD_WARPS + (rank == 0 ? 1 : 0)); mbar_init(&empty[s], 1); }
+        for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 2 * NDRAIN_WARPS); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == MMA_WARP) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"(TMEM_COLS)
                      : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
+    cluster_sync();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
 
     if (warp == MMA_WARP) {
-        // ================= MMA issuer (one lane) =================
-        if (lane == 0) {
+        // ================= MMA issuer: one lane of the leader CTA drives the pair =================
+        if (rank == 0 && lane == 0) {
             const uint32_t id_pos = idesc_f16(false), id_neg = idesc_f16(true);
             const uint32_t lo_on = dbg_flags & 1 ? 0u : 1u;   // experiments: bit 0 drops the hi.lo / lo.hi products
             const uint32_t base = smem_u32(smem);
@@ -161,67 +263,101 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
                 const int s = i % STAGES;
                 const int u = i / SUB_STAGES, b = u & 1;
                 const bool sub_first = (i % SUB_STAGES) == 0;
-                if (sub_first) {   // accumulator b must have been drained (its previous use was sub-chunk u - 2)
-                    mbar_wait(&tempty[b], (uint32_t)(((u >> 1) + 1) & 1));
+                if (sub_first) {   // accumulator b must have been drained by both CTAs (use u - 2)
+                    mbar_wait_cluster(&tempty[b], (uint32_t)(((u >> 1) + 1) & 1));
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 }
-                mbar_wait(&full[s], (uint32_t)((i / STAGES) & 1));
+                mbar_wait_cluster(&full[s], (uint32_t)((i / STAGES) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t sb = base + s * STAGE_BYTES;
                 uint64_t d[8];
 #pragma unroll
-                for (int p = 0; p < 8; ++p) d[p] = umma_desc(sb + p * PLANE, 128, 256);
-                // planes: 0 Xr_hi 1 Xr_lo 2 Xi_hi 3 Xi_lo 4 Wr_hi 5 Wr_lo 6 Wi_hi 7 Wi_lo
+                for (int p = 0; p < 4; ++p) d[p] = umma_desc(sb + p * APLANE, 128, 256);
+#pragma unroll
+                for (int p = 0; p < 4; ++p) d[4 + p] = umma_desc(sb + 4 * APLANE + p * BPLANE, 128, 256);
+                // planes: 0 Xr_hi 1 Xr_lo 2 Xs_hi 3 Xs_lo 4 Wr_hi 5 Wr_lo 6 Ws_hi 7 Ws_lo  (Xs = sin, Ws = f sin)
+                // Re = Xr Wr - Xs Ws ;  Im' = Xr Ws + Xs Wr = -Im  (|p|^2 is unchanged; the tile holds conj(p))
                 const uint32_t re = tmem + (uint32_t)(b * 256), im = re + TN;
                 const uint32_t first = sub_first ? 0u : 1u;
-                umma_f16(re, d[0], d[4], id_pos, first);     // Re += Xr Wr
-                if (lo_on) { umma_f16(re, d[0], d[5], id_pos, 1); umma_f16(re, d[1], d[4], id_pos, 1); }
-                umma_f16(re, d[2], d[6], id_neg, 1);         // Re -= Xi Wi
-                if (lo_on) { umma_f16(re, d[2], d[7], id_neg, 1); umma_f16(re, d[3], d[6], id_neg, 1); }
-                umma_f16(im, d[0], d[6], id_pos, first);     // Im += Xr Wi
-                if (lo_on) { umma_f16(im, d[0], d[7], id_pos, 1); umma_f16(im, d[1], d[6], id_pos, 1); }
-                umma_f16(im, d[2], d[4], id_pos, 1);         // Im += Xi Wr
-                if (lo_on) { umma_f16(im, d[2], d[5], id_pos, 1); umma_f16(im, d[3], d[4], id_pos, 1); }
-                umma_commit(&empty[s]);                      // frees the stage when these MMAs complete
-                if ((i % SUB_STAGES) == SUB_STAGES - 1 || i == n_stages - 1) umma_commit(&tfull[b]);
+                if (!(dbg_flags & 4)) {   // experiments: bit 2 skips the MMAs (producer/drain cost alone)
+                    umma2_f16(re, d[0], d[4], id_pos, first);     // Re += Xr Wr
+                    if (lo_on) { umma2_f16(re, d[0], d[5], id_pos, 1); umma2_f16(re, d[1], d[4], id_pos, 1); }
+                    umma2_f16(re, d[2], d[6], id_neg, 1);         // Re -= Xs Ws
+                    if (lo_on) { umma2_f16(re, d[2], d[7], id_neg, 1); umma2_f16(re, d[3], d[6], id_neg, 1); }
+                    umma2_f16(im, d[0], d[6], id_pos, first);     // Im' += Xr Ws
+                    if (lo_on) { umma2_f16(im, d[0], d[7], id_pos, 1); umma2_f16(im, d[1], d[6], id_pos, 1); }
+                    umma2_f16(im, d[2], d[4], id_pos, 1);         // Im' += Xs Wr
+                    if (lo_on) { umma2_f16(im, d[2], d[5], id_pos, 1); umma2_f16(im, d[3], d[4], id_pos, 1); }
+                }
+                umma2_commit_both(&empty[s]);                     // frees the stage in both CTAs
+                if ((i % SUB_STAGES) == SUB_STAGES - 1 || i == n_stages - 1) umma2_commit_both(&tfull[b]);
+            }
+        } else if (rank == 1 && lane == 0) {
+            // forwarder: the peer's 16 producer warps arrive locally (CTA-scope release, cheap); one cluster-scope
+            // arrival per stage then tells the leader that this CTA's half of the operands is in shared memory
+            const uint32_t full_addr0 = mapa(smem_u32(full), 0);
+            for (int i = 0; i < n_stages; ++i) {
+                const int s = i % STAGES;
+                mbar_wait(&full[s], (uint32_t)((i / STAGES) & 1));
+                mbar_arrive_cluster(full_addr0 + (uint32_t)(s * 8));
             }
         }
         __syncwarp();
     } else if (warp < NPROD_WARPS) {
-        // ================= phasor producers =================
-        // thread -> fixed atom pair (a, a+1) of every stage; per item one core matrix (8 rows x 8 atoms) of a plane
+        // ================= phasor producers (both CTAs): own 128 A rows, own 64 B rows =================
         const int ah = warp & 1;
         const int a_loc = ah * 8 + 2 * (lane & 3);
         const int mrow = lane >> 2;
+        const int gi = warp >> 1;                            // 0..7
+        // atom records of stage i+1 are prefetched with cp.async into this warp's shared slot (the per-stage
+        // MEMBAR of the release-arrive does not wait on cp.async, unlike on register loads in flight)
+        const uint32_t slot = smem_u32(aslot) + (uint32_t)(warp * 2 * 16 * 16);
+        const uint4* aslot_w = aslot + warp * 2 * 16;
+        auto prefetch = [&](int stage_idx) {
+            if (lane < KS) {
+                const int64_t j = a_begin + (int64_t)stage_idx * KS + lane;
+                const bool ok = j < a_end;
+                cp_async16(slot + (uint32_t)(((stage_idx & 1) * 16 + lane) * 16), S + (ok ? j : 0), ok ? 16u : 0u);
+            }
+            cp_async_commit();
+        };
+        prefetch(0);
         for (int i = 0; i < n_stages; ++i) {
             const int s = i % STAGES;
+            prefetch(i + 1);
+            cp_async_wait1();                 // stage i's records have landed
+            __syncwarp();
+            const uint4 at0 = aslot_w[(i & 1) * 16 + a_loc], at1 = aslot_w[(i & 1) * 16 + a_loc + 1];
+            __syncwarp();
             mbar_wait(&empty[s], (uint32_t)(((i / STAGES) + 1) & 1));
-            char* st = smem + s * STAGE_BYTES;
-            const int64_t j0 = a_begin + (int64_t)i * KS + a_loc;
-            uint4 at0 = make_uint4(0, 0, 0, 0), at1 = make_uint4(0, 0, 0, 0);
-            if (j0 < a_end) at0 = __ldg(S + j0);
-            if (j0 + 1 < a_end) at1 = __ldg(S + j0 + 1);
-            const float f0 = __uint_as_float(at0.w), f1 = __uint_as_float(at1.w);   // 0 for padding atoms
-            const float x0 = (j0 < a_end) ? 1.f : 0.f, x1 = (j0 + 1 < a_end) ? 1.f : 0.f;
+            // padding atoms have f = 0, so W = 0 and their (finite) X values never contribute
+            const float f0 = __uint_as_float(at0.w), f1 = __uint_as_float(at1.w);
+            const unsigned long long F2 = pack2(f0, f1);
+            const float MX = 12288.0f;                                       // |X| <= 1: grid 2^-10
+            const float MW = split_magic(fmaxf(fabsf(f0), fabsf(f1)));
+            const unsigned long long MX2 = pack2(MX, MX), MW2 = pack2(MW, MW);
+            const uint32_t sbase = smem_u32(smem) + (uint32_t)(s * STAGE_BYTES);
+            if (!(dbg_flags & 2)) {   // experiments: bit 1 skips generation
 #pragma unroll
-            for (int it = 0; it < 2; ++it) {
-                const int m = ((warp >> 1) + 8 * it) * 8 + mrow;          // row within the tile
-                const uint32_t off = plane_off(m, a_loc);
-                {   // X_h, h = h0 + th0 + m
+                for (int it = 0; it < 2; ++it) {   // X rows: groups gi and gi + 8 of this CTA's 128 rows
+                    const int m = (gi + 8 * it) * 8 + mrow;
+                    const uint32_t off = sbase + plane_off(m, a_loc);
                     const uint32_t hh = (uint32_t)(g.h0 + th0 + m);
                     float s0, c0, s1, c1;
                     __sincosf(turns_to_radians(hh * at0.x), &s0, &c0);
                     __sincosf(turns_to_radians(hh * at1.x), &s1, &c1);
-                    store_split(st + 0 * PLANE, st + 1 * PLANE, off, x0 * c0, x1 * c1);     // Xr =  cos
-                    store_split(st + 2 * PLANE, st + 3 * PLANE, off, -x0 * s0, -x1 * s1);   // Xi = -sin
+                    split_store<0 * APLANE, 1 * APLANE>(off, pack2(c0, c1), MX2);     // Xr = cos
+                    split_store<2 * APLANE, 3 * APLANE>(off, pack2(s0, s1), MX2);     // Xs = sin
                 }
-                {   // W_k, k = k0 + tk0 + m
-                    const uint32_t kk = (uint32_t)(g.k0 + tk0 + m);
+                {   // W rows: group gi of this CTA's 64 B rows, k = k0 + bk0 + m
+                    const int m = gi * 8 + mrow;
+                    const uint32_t off = sbase + 4 * APLANE + plane_off(m, a_loc);
+                    const uint32_t kk = (uint32_t)(g.k0 + bk0 + m);
                     float s0, c0, s1, c1;
                     __sincosf(turns_to_radians(at0.z + kk * at0.y), &s0, &c0);
                     __sincosf(turns_to_radians(at1.z + kk * at1.y), &s1, &c1);
-                    store_split(st + 4 * PLANE, st + 5 * PLANE, off, f0 * c0, f1 * c1);     // Wr =  f cos
-                    store_split(st + 6 * PLANE, st + 7 * PLANE, off, -f0 * s0, -f1 * s1);   // Wi = -f sin
+                    split_store_f<0 * BPLANE, 1 * BPLANE>(off, F2, pack2(c0, c1), MW2);   // Wr = f cos
+                    split_store_f<2 * BPLANE, 3 * BPLANE>(off, F2, pack2(s0, s1), MW2);   // Ws = f sin
                 }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> async proxy
@@ -230,12 +366,13 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
         }
     } else {
         // ================= drain warps: TMEM accumulator -> RN fp32 running sums (smem) -> tile =================
-        const int quarter = warp & 3;               // TMEM lanes 32*quarter .. +31 = tile rows
+        const int quarter = warp & 3;               // TMEM lanes 32*quarter .. +31 = rows of this CTA's half
         const int r = quarter * 32 + lane;
+        const uint32_t tempty0 = mapa(smem_u32(tempty), 0);
         for (int c = 0; c < 256; ++c) sums[c * SUM_LD + r] = 0.f;
         for (int u = 0; u < n_sub; ++u) {
             const int b = u & 1;
-            mbar_wait(&tfull[b], (uint32_t)((u >> 1) & 1));
+            mbar_wait_cluster(&tfull[b], (uint32_t)((u >> 1) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * 256);
             uint32_t v[2][32];
@@ -244,18 +381,23 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
 #pragma unroll
                 for (int q = 0; q < 2; ++q) TMEM_LD32(tb + (uint32_t)((blk + q) * 32), v[q]);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (blk == 6) {   // all of accumulator b has been read: hand it back to the MMA
+                if (blk == 6) {   // all of accumulator b has been read: hand it back to the leader's MMA
                     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&tempty[b]);
+                    if (lane == 0) mbar_arrive_cluster(tempty0 + (uint32_t)(b * 8));
                 }
 #pragma unroll
-                for (int q = 0; q < 2; ++q)
+                for (int q = 0; q < 2; ++q) {
+                    float* col = sums + ((blk + q) * 32) * SUM_LD + r;
+                    float acc[32];
 #pragma unroll
-                    for (int c = 0; c < 32; ++c) sums[((blk + q) * 32 + c) * SUM_LD + r] += __uint_as_float(v[q][c]);
+                    for (int c = 0; c < 32; ++c) acc[c] = col[c * SUM_LD];
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) col[c * SUM_LD] = acc[c] + __uint_as_float(v[q][c]);
+                }
             }
         }
-        // ---- write the tile: row-major partial[chunk][t][ih][ik], coalesced along k
+        // ---- write this CTA's 128 x 128 half tile: row-major partial[chunk][t][ih][ik], coalesced along k
         __syncwarp();
         const int64_t n_q = g.n_h * g.n_k;
         float2* P = partial + (chunk * frames + t) * n_q;
@@ -272,10 +414,10 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
+    cluster_sync();
     if (warp == MMA_WARP) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
     }
 }
 
@@ -297,13 +439,13 @@ bool lattice_tc_supported(const LatticeGeom& g) {
 cudaError_t launch_lattice_tc(const uint4* staged, int64_t N, int64_t frames, const LatticeGeom& g,
                               int64_t chunk_atoms, int64_t n_chunks, float2* partial, cudaStream_t s) {
     using namespace tc;
-    const int tiles_h = (int)((g.n_h + TM - 1) / TM), tiles_k = (int)((g.n_k + TN - 1) / TN);
+    const int tiles_h = (int)((g.n_h + PAIR_M - 1) / PAIR_M), tiles_k = (int)((g.n_k + TN - 1) / TN);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_lattice_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
         attr = true;
     }
-    dim3 grid(tiles_h * tiles_k, (unsigned)n_chunks, (unsigned)frames);
+    dim3 grid(2 * tiles_h * tiles_k, (unsigned)n_chunks, (unsigned)frames);   // 2 CTAs (one cluster) per pair tile
     note_launch();
     static int dbg = -1;
     if (dbg < 0) { const char* e = getenv("XPCS_TC_DEBUG"); dbg = e ? atoi(e) : 0; }
