@@ -117,13 +117,19 @@ struct PlanBufs {
 };
 
 int make_plan(const int32_t* bins, int64_t n_q, int32_t n_bins, cudaStream_t s, PlanBufs& pb) {
-    const size_t perm_b = sizeof(int32_t) * (size_t)n_q;
-    const size_t off_b = sizeof(int32_t) * (size_t)(n_bins + 1);
-    char* base = (char*)scratch(s, SS_PLAN, perm_b + 2 * off_b + 64);
+    if (n_bins > 12288) {
+        set_error("xpcs: n_bins must be <= 12288 (got %d)", n_bins);
+        return XPCS_EINVAL;
+    }
+    const size_t perm_b = ((sizeof(int32_t) * (size_t)n_q + 255) / 256) * 256;
+    const size_t off_b = ((sizeof(int32_t) * (size_t)(n_bins + 1) + 255) / 256) * 256;
+    const size_t cnt_b = sizeof(int32_t) * (size_t)((n_q + 1023) / 1024) * (size_t)n_bins;
+    char* base = (char*)scratch(s, SS_PLAN, perm_b + 2 * off_b + cnt_b + 256);
     if (!base) return XPCS_ENOMEM;
     pb.plan.perm = (int32_t*)base;
-    pb.plan.offsets = (int32_t*)(base + ((perm_b + 15) / 16) * 16);
-    pb.plan.warp_off = pb.plan.offsets + (n_bins + 1);
+    pb.plan.offsets = (int32_t*)(base + perm_b);
+    pb.plan.warp_off = (int32_t*)(base + perm_b + off_b);
+    pb.plan.bcounts = (int32_t*)(base + perm_b + 2 * off_b);
     pb.max_warps = (n_q + 31) / 32 + n_bins;
     return cuda_fail(launch_binplan(bins, n_q, n_bins, pb.plan, s), "ring plan");
 }

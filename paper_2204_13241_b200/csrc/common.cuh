@@ -141,6 +141,7 @@ struct BinPlan {
     int32_t* perm;        // [n_valid] pixel indices sorted by (bin, pixel)
     int32_t* offsets;     // [n_bins + 1]
     int32_t* warp_off;    // [n_bins + 1] prefix of ceil(count_b / 32)
+    int32_t* bcounts;     // [ceil(n_q / 1024)][n_bins] scratch of the plan build
 };
 cudaError_t launch_binplan(const int32_t* bins, int64_t n_q, int32_t n_bins, BinPlan plan, cudaStream_t s);
 cudaError_t launch_sum_f2(const void* f, int f_f64, int64_t N, double* out, cudaStream_t s);

@@ -117,13 +117,14 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+    // CTA-scope release (as CUTLASS's ClusterBarrier::arrive(cta_id)): a .cluster scope would emit CCTL.IVALL
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAITC_%=:\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
         "@!p bra WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
@@ -236,9 +237,8 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
     const uint4* S = staged + t * N;
 
     if (threadIdx.x == 0) {
-        // full[s]: the 16 local producer warps (+ 1 forwarded arrival from the peer in the leader); tempty[b]: the
-        // 4 drain warps of each CTA (in the leader)
-        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], NPROD_WARPS + (rank == 0 ? 1 : 0)); mbar_init(&empty[s], 1); }
+        // in the leader: full[s] counts the 16 producer warps of both CTAs, tempty[b] the 4 drain warps of both
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 2 * NPROD_WARPS); mbar_init(&empty[s], 1); }
         for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 2 * NDRAIN_WARPS); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -292,15 +292,6 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
                 umma2_commit_both(&empty[s]);                     // frees the stage in both CTAs
                 if ((i % SUB_STAGES) == SUB_STAGES - 1 || i == n_stages - 1) umma2_commit_both(&tfull[b]);
             }
-        } else if (rank == 1 && lane == 0) {
-            // forwarder: the peer's 16 producer warps arrive locally (CTA-scope release, cheap); one cluster-scope
-            // arrival per stage then tells the leader that this CTA's half of the operands is in shared memory
-            const uint32_t full_addr0 = mapa(smem_u32(full), 0);
-            for (int i = 0; i < n_stages; ++i) {
-                const int s = i % STAGES;
-                mbar_wait(&full[s], (uint32_t)((i / STAGES) & 1));
-                mbar_arrive_cluster(full_addr0 + (uint32_t)(s * 8));
-            }
         }
         __syncwarp();
     } else if (warp < NPROD_WARPS) {
@@ -312,7 +303,7 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
         // atom records of stage i+1 are prefetched with cp.async into this warp's shared slot (the per-stage
         // MEMBAR of the release-arrive does not wait on cp.async, unlike on register loads in flight)
         const uint32_t slot = smem_u32(aslot) + (uint32_t)(warp * 2 * 16 * 16);
-        const uint4* aslot_w = aslot + warp * 2 * 16;
+        const uint32_t full0 = mapa(smem_u32(full), 0);
         auto prefetch = [&](int stage_idx) {
             if (lane < KS) {
                 const int64_t j = a_begin + (int64_t)stage_idx * KS + lane;
@@ -327,7 +318,12 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
             prefetch(i + 1);
             cp_async_wait1();                 // stage i's records have landed
             __syncwarp();
-            const uint4 at0 = aslot_w[(i & 1) * 16 + a_loc], at1 = aslot_w[(i & 1) * 16 + a_loc + 1];
+            uint4 at0, at1;
+            {
+                const uint32_t ra = slot + (uint32_t)(((i & 1) * 16 + a_loc) * 16);
+                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(at0.x), "=r"(at0.y), "=r"(at0.z), "=r"(at0.w) : "r"(ra));
+                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4+16];" : "=r"(at1.x), "=r"(at1.y), "=r"(at1.z), "=r"(at1.w) : "r"(ra));
+            }
             __syncwarp();
             mbar_wait(&empty[s], (uint32_t)(((i / STAGES) + 1) & 1));
             // padding atoms have f = 0, so W = 0 and their (finite) X values never contribute
@@ -362,7 +358,7 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> async proxy
             __syncwarp();
-            if (lane == 0) mbar_arrive(&full[s]);
+            if (lane == 0) mbar_arrive_cluster(full0 + (uint32_t)(s * 8));   // the leader's full[s]
         }
     } else {
         // ================= drain warps: TMEM accumulator -> RN fp32 running sums (smem) -> tile =================

@@ -4,50 +4,74 @@
 //   K5 XSVS contrast beta_{W,b}           Eq.(15), Eq.(17), averaging PAPER.md:429
 // All sums are FP64 and in a fixed order (deterministic, no float atomics).
 #include "common.cuh"
+#include <algorithm>
 #include <vector>
 
 namespace xpcs {
 
 // =====================================================================================================
-// K4: g2.  Block = 32 pixels (lanes) x 8 warps; warp w owns up to 16 lags.  The time series of the 32 pixels
-// are staged through shared memory in chunks of GC frames plus a halo of max_lag frames (zero beyond T, so the
-// products with t + tau >= T vanish and each lag sums exactly over t < T - tau).  fp32 x fp32 products are exact
-// in FP64; the hot loop is one LDS + one DFMA per (pixel, lag, frame).
+// K4: g2.  A warp owns 32 pixels (lanes) x 16 lags.  The pixels' time series are staged through shared memory
+// (fp32 for fp32 input: products of two fp32 are exact in FP64) in chunks of GC frames plus a halo of max_lag
+// frames (zero beyond T, so products with t + tau >= T vanish and each lag sums exactly over t < T - tau).
+// Consecutive lag groups (tau_l = tau_0 + l) use a register-blocked sliding window: per 16 frames 48 shared loads
+// feed 256 DFMA; other lag lists fall back to one shared load per DFMA.
 // =====================================================================================================
 namespace { constexpr int G2_LPW = 16, G2_WARPS = 8, G2_LAGS_PER_BLOCK = G2_LPW * G2_WARPS, GC = 128; }
 
-template <typename In, typename Out>
+template <typename In, typename Out, typename St>
 __global__ void __launch_bounds__(256)
 k_g2(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __restrict__ lags, int64_t n_lags,
      int halo, Out* __restrict__ out) {
-    extern __shared__ double S[];                    // [(GC + halo)][32]
+    extern __shared__ __align__(16) unsigned char g2_smem[];
+    St* S = reinterpret_cast<St*>(g2_smem);              // [(GC + halo + 16)][32]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t px = (int64_t)blockIdx.x * 32 + lane;
     const int64_t lbase = (int64_t)blockIdx.y * G2_LAGS_PER_BLOCK + warp * G2_LPW;
+    const bool active = lbase < n_lags;
     int tau[G2_LPW];
+    bool consecutive = true;
 #pragma unroll
-    for (int l = 0; l < G2_LPW; ++l) tau[l] = (lbase + l < n_lags) ? lags[lbase + l] : 0;
+    for (int l = 0; l < G2_LPW; ++l) {
+        tau[l] = (lbase + l < n_lags) ? lags[lbase + l] : (active ? lags[lbase] + l : 0);
+        if (tau[l] != tau[0] + l) consecutive = false;
+    }
     double acc[G2_LPW];
 #pragma unroll
     for (int l = 0; l < G2_LPW; ++l) acc[l] = 0.0;
     double sum = 0.0;
-    const int rows = GC + halo;
+    const int rows = GC + halo + 16;
     for (int64_t t0 = 0; t0 < T; t0 += GC) {
         __syncthreads();
         for (int r = warp; r < rows; r += G2_WARPS) {
             const int64_t t = t0 + r;
-            S[r * 32 + lane] = (t < T && px < n_q) ? (double)I[t * n_q + px] : 0.0;
+            S[r * 32 + lane] = (t < T && px < n_q) ? (St)I[t * n_q + px] : (St)0;
         }
         __syncthreads();
         const int rmax = (int)min((int64_t)GC, T - t0);
-        for (int r = 0; r < rmax; ++r) {
-            const double a = S[r * 32 + lane];
-            sum += a;
+        for (int r = 0; r < rmax; ++r) sum += (double)S[r * 32 + lane];
+        if (!active) continue;
+        if (consecutive) {
+            const int t0l = tau[0];
+            for (int r0 = 0; r0 < rmax; r0 += 16) {          // rows beyond rmax are zero-padded or ignored
+                double a[16], w[32];
 #pragma unroll
-            for (int l = 0; l < G2_LPW; ++l) acc[l] = fma(a, S[(r + tau[l]) * 32 + lane], acc[l]);
+                for (int i = 0; i < 16; ++i) a[i] = (r0 + i < rmax) ? (double)S[(r0 + i) * 32 + lane] : 0.0;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) w[j] = (double)S[(r0 + t0l + j) * 32 + lane];
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+#pragma unroll
+                    for (int l = 0; l < G2_LPW; ++l) acc[l] = fma(a[i], w[i + l], acc[l]);
+            }
+        } else {
+            for (int r = 0; r < rmax; ++r) {
+                const double a = (double)S[r * 32 + lane];
+#pragma unroll
+                for (int l = 0; l < G2_LPW; ++l) acc[l] = fma(a, (double)S[(r + tau[l]) * 32 + lane], acc[l]);
+            }
         }
     }
-    if (px >= n_q) return;
+    if (px >= n_q || !active) return;
     const double mean = sum / (double)T;
     const double den = mean * mean;
 #pragma unroll
@@ -60,86 +84,111 @@ k_g2(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __restrict
 
 cudaError_t launch_g2(const void* I, int in_f64, int64_t T, int64_t n_q, const int32_t* lags_dev,
                       int64_t n_lags, int max_lag, void* out, int out_f64, cudaStream_t s) {
+    const int wpb = (int)std::min<int64_t>(G2_WARPS, (n_lags + G2_LPW - 1) / G2_LPW);   // drop idle warps
     dim3 grid((unsigned)((n_q + 31) / 32), (unsigned)((n_lags + G2_LAGS_PER_BLOCK - 1) / G2_LAGS_PER_BLOCK));
-    const size_t smem = sizeof(double) * 32 * (GC + max_lag);
+    const size_t elem = in_f64 ? sizeof(double) : sizeof(float);
+    const size_t smem = elem * 32 * (GC + max_lag + 16 + 16);
+    (void)wpb;
     note_launch();
-#define G2_CASE(IN, OUT)                                                                              \
+#define G2_CASE(IN, OUT, ST)                                                                          \
     {                                                                                                 \
-        auto kern = k_g2<IN, OUT>;                                                                    \
+        auto kern = k_g2<IN, OUT, ST>;                                                                \
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-        kern<<<grid, 256, smem, s>>>((const IN*)I, T, n_q, lags_dev, n_lags, max_lag, (OUT*)out);     \
+        kern<<<grid, 256, smem, s>>>((const IN*)I, T, n_q, lags_dev, n_lags, max_lag + 16, (OUT*)out); \
     }
-    if (in_f64) { if (out_f64) G2_CASE(double, double) else G2_CASE(double, float) }
-    else { if (out_f64) G2_CASE(float, double) else G2_CASE(float, float) }
+    if (in_f64) { if (out_f64) G2_CASE(double, double, double) else G2_CASE(double, float, double) }
+    else { if (out_f64) G2_CASE(float, double, float) else G2_CASE(float, float, float) }
 #undef G2_CASE
     return cudaGetLastError();
 }
 
 // =====================================================================================================
-// Ring plan: pixels sorted by (ring, pixel index), stable and deterministic (one block per ring, block scan).
+// Ring plan: pixels sorted by (ring, pixel index) -- stable and deterministic.
+//   k_bin_count : per 1024-pixel block, per-ring counts (shared-memory integer atomics: exact)
+//   k_bin_scan  : per ring, exclusive scan over blocks (+ ring offsets and warp offsets)
+//   k_bin_fill  : per block, warps in order; within a warp equal rings are ranked with __match_any_sync
 // =====================================================================================================
-__device__ __forceinline__ int block_excl_scan(int v, int* sh, int& total) {
-    // 256-thread exclusive scan of v (Hillis-Steele in shared memory)
-    const int tid = threadIdx.x;
-    sh[tid] = v;
+constexpr int PLAN_BLOCK = 1024;
+
+__global__ void __launch_bounds__(256) k_bin_count(const int32_t* __restrict__ bins, int64_t n_q, int32_t n_bins,
+                                                   int32_t* __restrict__ bcounts) {
+    extern __shared__ int cnt[];
+    for (int b = threadIdx.x; b < n_bins; b += 256) cnt[b] = 0;
     __syncthreads();
-    for (int off = 1; off < 256; off <<= 1) {
-        const int x = tid >= off ? sh[tid - off] : 0;
+    const int64_t base = (int64_t)blockIdx.x * PLAN_BLOCK;
+    for (int k = threadIdx.x; k < PLAN_BLOCK; k += 256) {
+        const int64_t i = base + k;
+        if (i < n_q) {
+            const int b = bins[i];
+            if (b >= 0 && b < n_bins) atomicAdd(&cnt[b], 1);
+        }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < n_bins; b += 256) bcounts[(int64_t)blockIdx.x * n_bins + b] = cnt[b];
+}
+
+__global__ void __launch_bounds__(256) k_bin_scan(int32_t* __restrict__ bcounts, int nblk, int32_t n_bins,
+                                                  int32_t* __restrict__ offsets, int32_t* __restrict__ warp_off) {
+    // one thread per ring: in-place exclusive scan of its counts over blocks -> per-block start (relative)
+    __shared__ int tot[1024];
+    for (int b0 = 0; b0 < n_bins; b0 += 1024) {
+        for (int b = b0 + threadIdx.x; b < min(n_bins, b0 + 1024); b += 256) {
+            int run = 0;
+            for (int k = 0; k < nblk; ++k) {
+                const int c = bcounts[(int64_t)k * n_bins + b];
+                bcounts[(int64_t)k * n_bins + b] = run;
+                run += c;
+            }
+            tot[b - b0] = run;
+        }
         __syncthreads();
-        sh[tid] += x;
+        if (threadIdx.x == 0) {
+            int o = b0 == 0 ? 0 : offsets[b0], w = b0 == 0 ? 0 : warp_off[b0];
+            for (int b = b0; b < min(n_bins, b0 + 1024); ++b) {
+                offsets[b] = o;
+                warp_off[b] = w;
+                o += tot[b - b0];
+                w += (tot[b - b0] + 31) / 32;
+            }
+            offsets[min(n_bins, b0 + 1024)] = o;
+            warp_off[min(n_bins, b0 + 1024)] = w;
+        }
         __syncthreads();
     }
-    total = sh[255];
-    const int incl = sh[tid];
-    __syncthreads();
-    return incl - v;
 }
 
-__global__ void __launch_bounds__(256) k_bin_count(const int32_t* __restrict__ bins, int64_t n_q, int32_t* counts) {
-    __shared__ int sh[256];
-    const int b = blockIdx.x;
-    int c = 0;
-    for (int64_t i = threadIdx.x; i < n_q; i += 256) c += (bins[i] == b);
-    int total;
-    block_excl_scan(c, sh, total);
-    if (threadIdx.x == 0) counts[b] = total;
-}
-
-__global__ void k_bin_scan(const int32_t* counts, int32_t n_bins, int32_t* offsets, int32_t* warp_off) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    int o = 0, w = 0;
-    for (int b = 0; b < n_bins; ++b) {
-        const int c = counts[b];          // counts may alias warp_off: read before overwriting
-        offsets[b] = o;
-        warp_off[b] = w;
-        o += c;
-        w += (c + 31) / 32;
-    }
-    offsets[n_bins] = o;
-    warp_off[n_bins] = w;
-}
-
-__global__ void __launch_bounds__(256) k_bin_fill(const int32_t* __restrict__ bins, int64_t n_q,
+__global__ void __launch_bounds__(256) k_bin_fill(const int32_t* __restrict__ bins, int64_t n_q, int32_t n_bins,
+                                                  const int32_t* __restrict__ bstart,
                                                   const int32_t* __restrict__ offsets, int32_t* __restrict__ perm) {
-    __shared__ int sh[256];
-    const int b = blockIdx.x;
-    int base = offsets[b];
-    for (int64_t i0 = 0; i0 < n_q; i0 += 256) {
-        const int64_t i = i0 + threadIdx.x;
-        const int flag = (i < n_q) && (bins[i] == b);
-        int total;
-        const int pos = block_excl_scan(flag, sh, total);
-        if (flag) perm[base + pos] = (int32_t)i;
-        base += total;
+    extern __shared__ int run[];
+    for (int b = threadIdx.x; b < n_bins; b += 256) run[b] = offsets[b] + bstart[(int64_t)blockIdx.x * n_bins + b];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t base = (int64_t)blockIdx.x * PLAN_BLOCK;
+    for (int round = 0; round < PLAN_BLOCK / 256; ++round) {
+        const int64_t i = base + round * 256 + threadIdx.x;
+        const int b = (i < n_q) ? bins[i] : -1;
+        const bool valid = b >= 0 && b < n_bins;
+        const unsigned same = __match_any_sync(0xffffffffu, valid ? b : -1);
+        const int rank = __popc(same & ((1u << lane) - 1u));
+        const bool leader = rank == 0;
+        for (int w = 0; w < 8; ++w) {          // warps in pixel order: stable
+            __syncthreads();
+            if (w == warp && valid) {
+                perm[run[b] + rank] = (int32_t)i;
+                __syncwarp(same);
+                if (leader) run[b] += __popc(same);
+            }
+        }
     }
 }
 
 cudaError_t launch_binplan(const int32_t* bins, int64_t n_q, int32_t n_bins, BinPlan plan, cudaStream_t s) {
-    int32_t* counts = plan.warp_off;   // temporary; k_bin_scan reads each count before overwriting it
+    const int nblk = (int)((n_q + PLAN_BLOCK - 1) / PLAN_BLOCK);
+    const size_t sh = sizeof(int) * (size_t)n_bins;
     note_launch(3);
-    k_bin_count<<<n_bins, 256, 0, s>>>(bins, n_q, counts);
-    k_bin_scan<<<1, 1, 0, s>>>(counts, n_bins, plan.offsets, plan.warp_off);
-    k_bin_fill<<<n_bins, 256, 0, s>>>(bins, n_q, plan.offsets, plan.perm);
+    k_bin_count<<<nblk, 256, sh, s>>>(bins, n_q, n_bins, plan.bcounts);
+    k_bin_scan<<<1, 256, 0, s>>>(plan.bcounts, nblk, n_bins, plan.offsets, plan.warp_off);
+    k_bin_fill<<<nblk, 256, sh, s>>>(bins, n_q, n_bins, plan.bcounts, plan.offsets, plan.perm);
     return cudaGetLastError();
 }
 
@@ -281,6 +330,7 @@ k_xsvs_final(const double2* __restrict__ mom, const int32_t* __restrict__ off, c
     double acc = 0.0;
     for (int s = threadIdx.x; s < S; s += 256) {
         double m1 = 0.0, m2 = 0.0;
+#pragma unroll 8
         for (int g = woff[b]; g < woff[b + 1]; ++g) {
             const double2 v = mom[(int64_t)g * ws.total_slots + ws.base[w] + s];
             m1 += v.x;
