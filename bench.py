@@ -40,49 +40,55 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock and clock-event (throttle) reasons sampled every 10 ms through NVML during the timed region
+    (the B200_PROFILING.md clocks line; nvidia-smi's 100 ms period is too coarse for a ~100 ms region)."""
 
-    def __init__(self, index=0):
-        self.rows = []
-        self.proc = None
-        self.index = index
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index=0, period=0.01):
+        self.index, self.period = index, period
+        self.sm, self.mx, self.reasons = [], None, set()
+        self._stop = threading.Event()
+        self.ok = False
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index),
-                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+            self.ok = True
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
-        except OSError:
-            self.proc = None
+        except Exception:
+            self.ok = False
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+                r = int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(self.period)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self._stop.set()
+        if self.ok:
+            self.t.join(timeout=1)
 
     def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in self.rows for n, v in zip(names, r[4:8]) if v.lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        if not self.ok or not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.mx, "reasons": ["unavailable"]}
+        return {"sm_mhz": float(np.median(self.sm)), "sm_max_mhz": self.mx, "reasons": sorted(self.reasons),
+                "samples": len(self.sm), "source": "nvml, 10 ms"}
 
 
 def _dist():
@@ -93,6 +99,18 @@ def _dist():
         local = int(os.environ.get("LOCAL_RANK", rank))
         return ws, rank, local, dist
     return 1, 0, 0, None
+
+
+def _traffic(workload, engine, pairs_launch):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the committed ncu --set full capture
+    (profiles/traffic.json, written from the capture summary), scaled to this launch's pairs; None if absent."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            t = json.load(fh)
+        rec = t[workload][engine]
+        return rec["dram_bytes"] * pairs_launch / rec["pairs"]
+    except (OSError, KeyError, ValueError, ZeroDivisionError):
+        return None
 
 
 def run_reference(args):
@@ -160,7 +178,7 @@ def cpu_baseline(cfg, budget_s):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2", choices=sorted(xi.CONFIGS))
     ap.add_argument("--engine", default="auto", choices=["auto", "simt", "tensor"])
@@ -249,7 +267,7 @@ def main():
         roof = {"bound": "alu", "unit": "TFLOP/s (FP32 FMA pipe)", "peak": peak,
                 "achieved": 8.0 * pairs_launch / (per_launch_ms / 1e3) / 1e12}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = None
+    roof["traffic"] = _traffic(cfg.name, "tensor" if tc_used else ("simt" if cfg.n_plane else "generic"), pairs_launch)
     roof["peak_source"] = peak_src if roof["bound"] == "tensor" else "derived (DESIGN.md)"
     roof["kernel_ms"] = per_launch_ms
     roof["kernel_share_of_step"] = main_ms / args.steps / ms if ms > 0 else None

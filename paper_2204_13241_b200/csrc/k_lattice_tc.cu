@@ -43,7 +43,8 @@ constexpr int NTHREADS = (MMA_WARP + 1) * 32;     // 672
 constexpr int TMEM_COLS = 512;                    // buffer b: Re cols [256b, 256b+128), Im' [256b+128, 256b+256)
 constexpr int SUM_LD = 129;                       // running sums [256 cols][129] fp32 (padded: conflict-free)
 constexpr int SUM_BYTES = 256 * SUM_LD * 4;
-constexpr int ASLOT_BYTES = NPROD_WARPS * 2 * 16 * 16;   // per producer warp: 2 x 16 atom records (cp.async)
+constexpr int ASLOTS = 4;                         // cp.async prefetch ring depth (distance ASLOTS - 1 stages)
+constexpr int ASLOT_BYTES = NPROD_WARPS * ASLOTS * 8 * 16;   // per producer warp: its 8 atoms of ASLOTS stages
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + SUM_BYTES + ASLOT_BYTES + 1024 + 256;
 }  // namespace tc
 
@@ -115,7 +116,8 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
     // CTA-scope release (as CUTLASS's ClusterBarrier::arrive(cta_id)): a .cluster scope would emit CCTL.IVALL
     asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
@@ -263,7 +265,7 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
                 const int s = i % STAGES;
                 const int u = i / SUB_STAGES, b = u & 1;
                 const bool sub_first = (i % SUB_STAGES) == 0;
-                if (sub_first) {   // accumulator b must have been drained by both CTAs (use u - 2)
+                if (sub_first && !(dbg_flags & 8)) {   // accumulator b must have been drained by both CTAs (use u - 2)
                     mbar_wait_cluster(&tempty[b], (uint32_t)(((u >> 1) + 1) & 1));
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 }
@@ -300,27 +302,29 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
         const int a_loc = ah * 8 + 2 * (lane & 3);
         const int mrow = lane >> 2;
         const int gi = warp >> 1;                            // 0..7
-        // atom records of stage i+1 are prefetched with cp.async into this warp's shared slot (the per-stage
-        // MEMBAR of the release-arrive does not wait on cp.async, unlike on register loads in flight)
-        const uint32_t slot = smem_u32(aslot) + (uint32_t)(warp * 2 * 16 * 16);
+        // atom records are prefetched ASLOTS - 1 stages ahead with cp.async into this warp's shared ring (the warp
+        // needs atoms ah*8 .. ah*8+7 of each stage; the per-stage MEMBAR of the release-arrive does not wait on
+        // cp.async, unlike on register loads in flight)
+        const uint32_t slot = smem_u32(aslot) + (uint32_t)(warp * ASLOTS * 8 * 16);
         const uint32_t full0 = mapa(smem_u32(full), 0);
         auto prefetch = [&](int stage_idx) {
-            if (lane < KS) {
-                const int64_t j = a_begin + (int64_t)stage_idx * KS + lane;
+            if (lane < 8) {
+                const int64_t j = a_begin + (int64_t)stage_idx * KS + ah * 8 + lane;
                 const bool ok = j < a_end;
-                cp_async16(slot + (uint32_t)(((stage_idx & 1) * 16 + lane) * 16), S + (ok ? j : 0), ok ? 16u : 0u);
+                cp_async16(slot + (uint32_t)(((stage_idx % ASLOTS) * 8 + lane) * 16), S + (ok ? j : 0), ok ? 16u : 0u);
             }
             cp_async_commit();
         };
-        prefetch(0);
+#pragma unroll
+        for (int k = 0; k < ASLOTS - 1; ++k) prefetch(k);
         for (int i = 0; i < n_stages; ++i) {
             const int s = i % STAGES;
-            prefetch(i + 1);
-            cp_async_wait1();                 // stage i's records have landed
+            prefetch(i + ASLOTS - 1);
+            cp_async_wait<ASLOTS - 1>();      // stage i's records have landed
             __syncwarp();
             uint4 at0, at1;
             {
-                const uint32_t ra = slot + (uint32_t)(((i & 1) * 16 + a_loc) * 16);
+                const uint32_t ra = slot + (uint32_t)(((i % ASLOTS) * 8 + 2 * (lane & 3)) * 16);
                 asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(at0.x), "=r"(at0.y), "=r"(at0.z), "=r"(at0.w) : "r"(ra));
                 asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4+16];" : "=r"(at1.x), "=r"(at1.y), "=r"(at1.z), "=r"(at1.w) : "r"(ra));
             }
@@ -366,7 +370,7 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
         const int r = quarter * 32 + lane;
         const uint32_t tempty0 = mapa(smem_u32(tempty), 0);
         for (int c = 0; c < 256; ++c) sums[c * SUM_LD + r] = 0.f;
-        for (int u = 0; u < n_sub; ++u) {
+        for (int u = 0; u < ((dbg_flags & 8) ? 0 : n_sub); ++u) {   // experiments: bit 3 skips the drain
             const int b = u & 1;
             mbar_wait_cluster(&tfull[b], (uint32_t)((u >> 1) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
