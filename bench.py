@@ -202,7 +202,8 @@ def main():
     dev = torch.device("cuda", local)
     cfg = xi.CONFIGS[args.config]
     # weak scaling: each rank its own independent trajectory
-    cfg_r = xi.scaled(cfg, seed=cfg.seed + 1000 * rank) if rank else cfg
+    from paper_2204_13241_b200 import dist as xd
+    cfg_r = xi.scaled(cfg, seed=xd.trajectory_seed(cfg.seed, rank)) if rank else cfg
     pos_h = xi.positions(cfg_r)
     f_h = xi.form_factors(cfg_r) if cfg.two_species else None
     engine = {"auto": xp.ENGINE_AUTO, "simt": xp.ENGINE_SIMT, "tensor": xp.ENGINE_TENSOR}[args.engine]
@@ -235,10 +236,7 @@ def main():
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms = float(np.mean(step_ms))
     prof = xp.profile_query()
-    if dist is not None:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = xd.max_over_ranks(ms, dev)
     pairs_step = P.pairs_per_step
     value = ws * pairs_step / (ms / 1e3)
 
@@ -290,11 +288,7 @@ def main():
             b.record(stream)
             torch.cuda.synchronize()
             t_e.append(a.elapsed_time(b))
-        e_ms = float(np.mean(t_e))
-        if dist is not None:
-            t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = float(t.item())
+        e_ms = xd.max_over_ranks(float(np.mean(t_e)), dev)
         h2d, d2h = P.io_bytes()
         e2e = {"value": ws * pairs_step / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}

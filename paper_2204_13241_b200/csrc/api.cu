@@ -225,8 +225,8 @@ int xpcs_intensity(const void* positions, int64_t N, const void* form_factors, c
     int64_t chunk = (N + C - 1) / C;
     chunk = ((chunk + 511) / 512) * 512;
     C = (N + chunk - 1) / chunk;
-    const int64_t Tb = std::max<int64_t>(1, std::min<int64_t>(frames, (int64_t)(kBatchBytes / std::max<int64_t>(16 * N, 16 * C * n_q))));
-    uint4* st = (uint4*)scratch(o.s, SS_STAGE, sizeof(uint4) * (size_t)(N * Tb));
+    const int64_t Tb = std::max<int64_t>(1, std::min<int64_t>(frames, (int64_t)(kBatchBytes / std::max<int64_t>(32 * N, 16 * C * n_q))));
+    uint4* st = (uint4*)scratch(o.s, SS_STAGE, 2 * sizeof(uint4) * (size_t)(N * Tb));   // 32 B / atom
     double2* part = (double2*)scratch(o.s, SS_PARTIAL, sizeof(double2) * (size_t)(C * n_q * Tb));
     if (!st || !part) return XPCS_ENOMEM;
     for (int64_t t0 = 0; t0 < frames; t0 += Tb) {

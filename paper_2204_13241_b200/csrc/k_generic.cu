@@ -4,9 +4,11 @@
 //
 // Phase arithmetic: the phase in turns is q . r / 2 pi = sum_c g_c u_c with
 // g_c = q_c L / 2 pi (per q, formed once in FP64) and u_c = r_c / L in [0, 1) (per atom, staged as 32-bit fixed
-// point Xi_c).  Writing g_c = n_c + Phi_c 2^-32 (integer part, 32-bit fraction):
-//     turns mod 1 = sum_c [ n_c Xi_c + hi32(Phi_c Xi_c) ] * 2^-32      (mod 2^32, 6 integer multiply-adds)
-// exact to ~3 * 2^-32 turns for any |q| and any box, with no rounded 2 pi and no large fp32 argument.
+// point Xi_c and as fp32 xi_c).  Writing g_c = n_c + phi_c (integer part, fraction in [0, 1)):
+//     turns = [ sum_c n_c Xi_c mod 2^32 ] * 2^-32  +  sum_c phi_c xi_c
+// the first term exact in integer arithmetic (3 IMAD), the second in fp32 FFMA (|error| <~ 2e-7 turns, and the
+// per-q rounding of phi_c only moves q by < 1e-7 of a reciprocal-lattice spacing).  No rounded 2 pi ever multiplies
+// a large argument.
 // The angle then goes to the SFU: FFMA -> FMUL.RZ -> MUFU.SIN / MUFU.COS (2 XU ops per atom.q pair, the
 // pipe that bounds this kernel), and f_j cos / f_j sin accumulate in fp32 for at most SUB atoms before being
 // folded into FP64 registers.
@@ -20,36 +22,33 @@ constexpr int QT = 4;       // q per thread
 constexpr int SUB = 512;    // atoms per shared-memory sub-block (also the fp32 accumulation length)
 }
 
-__device__ __forceinline__ void q_to_fixed(double qc, double L_over_2pi, uint32_t& n, uint32_t& phi) {
+__device__ __forceinline__ void q_split(double qc, double L_over_2pi, uint32_t& n, float& two_pi_phi) {
     const double gq = qc * L_over_2pi;
     const double fl = floor(gq);
-    const double fr = gq - fl;                                   // exact, in [0, 1)
-    long long ip = (long long)fl;
-    unsigned long long ph = (unsigned long long)llrint(fr * 4294967296.0);
-    if (ph >= 4294967296ull) { ph -= 4294967296ull; ip += 1; }
-    n = (uint32_t)(unsigned long long)ip;
-    phi = (uint32_t)ph;
+    n = (uint32_t)(unsigned long long)(long long)fl;
+    two_pi_phi = (float)((gq - fl) * 6.283185307179586476925);
 }
 
 template <typename Q>
 __global__ void __launch_bounds__(GT, 2)
 k_generic32(const uint4* __restrict__ staged, int64_t N, const Q* __restrict__ q, int64_t n_q, double L_over_2pi,
             int64_t chunk_atoms, int64_t frames, double2* __restrict__ partial) {
-    __shared__ uint4 As[SUB];
+    __shared__ uint4 As[2 * SUB];
     const int64_t t = blockIdx.z;
     const int64_t chunk = blockIdx.y;
     const int64_t a_begin = chunk * chunk_atoms, a_end = min(N, a_begin + chunk_atoms);
-    const uint4* S = staged + t * N;
+    const uint4* S = staged + 2 * t * N;
 
-    uint32_t nx[QT], ny[QT], nz[QT], px[QT], py[QT], pz[QT];
+    uint32_t nx[QT], ny[QT], nz[QT];
+    float px[QT], py[QT], pz[QT];
     int64_t iq[QT];
 #pragma unroll
     for (int i = 0; i < QT; ++i) {
         iq[i] = (int64_t)blockIdx.x * (GT * QT) + threadIdx.x + GT * i;
         const int64_t qq = iq[i] < n_q ? iq[i] : 0;
-        q_to_fixed((double)q[3 * qq + 0], L_over_2pi, nx[i], px[i]);
-        q_to_fixed((double)q[3 * qq + 1], L_over_2pi, ny[i], py[i]);
-        q_to_fixed((double)q[3 * qq + 2], L_over_2pi, nz[i], pz[i]);
+        q_split((double)q[3 * qq + 0], L_over_2pi, nx[i], px[i]);
+        q_split((double)q[3 * qq + 1], L_over_2pi, ny[i], py[i]);
+        q_split((double)q[3 * qq + 2], L_over_2pi, nz[i], pz[i]);
     }
     double dre[QT], dim[QT];
 #pragma unroll
@@ -58,25 +57,28 @@ k_generic32(const uint4* __restrict__ staged, int64_t N, const Q* __restrict__ q
     for (int64_t a0 = a_begin; a0 < a_end; a0 += SUB) {
         const int cnt = (int)min((int64_t)SUB, a_end - a0);
         __syncthreads();
-        for (int e = threadIdx.x; e < SUB; e += GT) As[e] = e < cnt ? S[a0 + e] : make_uint4(0, 0, 0, 0);
+        for (int e = threadIdx.x; e < 2 * SUB; e += GT) As[e] = (e >> 1) < cnt ? S[2 * a0 + e] : make_uint4(0, 0, 0, 0);
         __syncthreads();
         float re[QT], im[QT];
 #pragma unroll
         for (int i = 0; i < QT; ++i) re[i] = im[i] = 0.f;
 #pragma unroll 4
         for (int a = 0; a < SUB; ++a) {
-            const uint4 at = As[a];                               // broadcast
+            const uint4 at = As[2 * a];                           // broadcast: exact fractions + f
+            const uint4 af = As[2 * a + 1];                       // fp32 fractions
             const float fj = __uint_as_float(at.w);               // 0 for padding atoms
+            const float xf = __uint_as_float(af.x), yf = __uint_as_float(af.y), zf = __uint_as_float(af.z);
 #pragma unroll
             for (int i = 0; i < QT; ++i) {
                 uint32_t T = nx[i] * at.x;
                 T = ny[i] * at.y + T;
                 T = nz[i] * at.z + T;
-                T = __umulhi(px[i], at.x) + T;
-                T = __umulhi(py[i], at.y) + T;
-                T = __umulhi(pz[i], at.z) + T;
+                float th = turns_to_radians(T);                   // integer part of the phase, in [-pi, pi)
+                th = fmaf(px[i], xf, th);                         // + 2 pi sum_c phi_c xi_c
+                th = fmaf(py[i], yf, th);
+                th = fmaf(pz[i], zf, th);
                 float s, c;
-                __sincosf(turns_to_radians(T), &s, &c);
+                __sincosf(th, &s, &c);
                 re[i] = fmaf(fj, c, re[i]);
                 im[i] = fmaf(fj, s, im[i]);
             }

@@ -4,11 +4,11 @@
 // (on the reciprocal lattice the image choice is irrelevant) and converted ONCE per frame into
 // exact fixed-point phase turns, so that the hot kernels never multiply a rounded q by a large coordinate
 // (R9 / "precision budget"):
-//   generic q   : Xi_c = round(frac(r_c / L) * 2^32)                       -> uint4 {Xi_x, Xi_y, Xi_z, f}
+//   generic q   : Xi_c = round(frac(r_c / L) * 2^32)   -> 2 x uint4 {Xi_x, Xi_y, Xi_z, f}{xi_x, xi_y, xi_z, 0}
 //   lattice q   : Theta_v = v . Xi (mod 2^32) for v = ma, mb, m0           -> uint4 {Th_a, Th_b, Th_0, f}
 // because q . r / 2 pi = (m . r) / L for q = (2 pi / L) m with integer m, so the phase in turns is the integer
 // combination of the box fractions, exact modulo 1.  fp64 inputs use 64-bit turns (ulonglong4).
-// HBM-bound: reads 12-24 B and writes 16-32 B per atom per frame.
+// HBM-bound: reads 12-24 B and writes 16-32 B per atom per frame (32 B for the generic fp32 record).
 #include "common.cuh"
 
 namespace xpcs {
@@ -51,17 +51,23 @@ __global__ void __launch_bounds__(256) k_stage_lattice64(const double* __restric
     }
 }
 
+// generic record (32 B): {Xi_x, Xi_y, Xi_z, f} exact 32-bit box fractions + {xi_x, xi_y, xi_z, 0} the same
+// fractions as fp32 (for the fractional part of q.r, see k_generic.cu)
 template <typename P, typename F>
 __global__ void __launch_bounds__(256) k_stage_generic32(const P* __restrict__ pos, const F* __restrict__ f,
                                                          int64_t N, int64_t total, double L,
                                                          uint4* __restrict__ out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const P* r = pos + 3 * i;
-        const uint32_t x = frac_to_fixed32(box_fraction((double)r[0], L));
-        const uint32_t y = frac_to_fixed32(box_fraction((double)r[1], L));
-        const uint32_t z = frac_to_fixed32(box_fraction((double)r[2], L));
+        const double ux = box_fraction((double)r[0], L), uy = box_fraction((double)r[1], L),
+                     uz = box_fraction((double)r[2], L);
+        const uint32_t x = frac_to_fixed32(ux), y = frac_to_fixed32(uy), z = frac_to_fixed32(uz);
         const float fj = f ? (float)f[i % N] : 1.0f;
-        out[i] = make_uint4(x, y, z, __float_as_uint(fj));
+        out[2 * i] = make_uint4(x, y, z, __float_as_uint(fj));
+        // fp32 fractions of the same fixed-point values (x * 2^-32 rounded once)
+        out[2 * i + 1] = make_uint4(__float_as_uint((float)((double)x * 2.3283064365386963e-10)),
+                                    __float_as_uint((float)((double)y * 2.3283064365386963e-10)),
+                                    __float_as_uint((float)((double)z * 2.3283064365386963e-10)), 0u);
     }
 }
 

@@ -78,24 +78,66 @@ class Pipeline:
         return out
 
     # ---------------------------------------------------------------- end to end from host memory
-    def alloc_host_io(self, pos_host: np.ndarray, f_host: np.ndarray | None):
+    def alloc_host_io(self, pos_host: np.ndarray, f_host: np.ndarray | None, batches: int = 4):
         """Pinned host copies of the inputs and pinned result buffers (allocated once, reused per step)."""
         self.h_pos = torch.from_numpy(np.ascontiguousarray(pos_host)).pin_memory()
         self.h_f = torch.from_numpy(np.ascontiguousarray(f_host)).pin_memory() if f_host is not None else None
         self.d_pos = torch.empty(self.h_pos.shape, dtype=self.h_pos.dtype, device=self.device)
         self.d_f = torch.empty(self.h_f.shape, dtype=self.h_f.dtype, device=self.device) if f_host is not None else None
         self.h_out = {}
+        T = self.wl.T
+        nb = max(1, min(int(batches), T))
+        edges = [round(i * T / nb) for i in range(nb + 1)]
+        self.batches = [(edges[i], edges[i + 1]) for i in range(nb) if edges[i + 1] > edges[i]]
+        self.s_h2d = torch.cuda.Stream(self.device)
+        self.s_d2h = torch.cuda.Stream(self.device)
 
     def run_host(self) -> dict:
-        """H2D (pinned) -> one device pass -> D2H of every result (I, S rings, g2, g2 rings, beta)."""
-        self.d_pos.copy_(self.h_pos, non_blocking=True)
+        """End to end: pinned H2D of the step's positions, I(q,t), g2, rings and XSVS, D2H of every result.
+        Frames are split into batches on three streams so that the copies of batch b+1 (H2D) and b-1 (D2H)
+        overlap the intensity kernel of batch b; the reductions follow on the compute stream."""
+        wl = self.wl
+        main = torch.cuda.current_stream(self.device)
+        if "I" not in self.h_out:
+            self.h_out["I"] = torch.empty(self.I.shape, dtype=self.I.dtype, pin_memory=True)
         if self.d_f is not None:
-            self.d_f.copy_(self.h_f, non_blocking=True)
-        out = self.run(self.d_pos, self.d_f)
+            with torch.cuda.stream(self.s_h2d):
+                self.d_f.copy_(self.h_f, non_blocking=True)
+        self.s_h2d.wait_stream(main)            # previous step's readers of d_pos are done
+        self.s_d2h.wait_stream(main)
+        ev_in = []
+        for (t0, t1) in self.batches:
+            with torch.cuda.stream(self.s_h2d):
+                self.d_pos[t0:t1].copy_(self.h_pos[t0:t1], non_blocking=True)
+                e = torch.cuda.Event()
+                e.record(self.s_h2d)
+                ev_in.append(e)
+        for bi, (t0, t1) in enumerate(self.batches):
+            main.wait_event(ev_in[bi])
+            pos_b = self.d_pos[t0:t1]
+            I_b = self.I[t0:t1]
+            if self.grid is not None:
+                X.xpcs_intensity_grid(pos_b, self.d_f, self.grid, out=I_b, engine=wl.engine, stream=main)
+            else:
+                X.xpcs_intensity(pos_b, self.d_f, wl.q, wl.L, out=I_b, stream=main)
+            e = torch.cuda.Event()
+            e.record(main)
+            self.s_d2h.wait_event(e)
+            with torch.cuda.stream(self.s_d2h):
+                self.h_out["I"][t0:t1].copy_(I_b, non_blocking=True)
+        out = {"S_rings": X.xpcs_structure_factor_shells(self.I, self.d_f, wl.N, self.bins, wl.n_bins, stream=main)}
+        if wl.lags:
+            X.xpcs_g2(self.I, wl.lags, out=self.g2, out_dtype=X.F32, stream=main)
+            out["g2"] = self.g2
+            out["g2_rings"] = X.xpcs_shell_mean(self.g2, self.bins, wl.n_bins, stream=main)
+        if wl.windows:
+            out["beta"] = X.xsvs_contrast(self.I, self.bins, wl.n_bins, wl.windows, stream=main)
         for k, v in out.items():
             if k not in self.h_out:
                 self.h_out[k] = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
             self.h_out[k].copy_(v, non_blocking=True)
+        main.wait_stream(self.s_d2h)
+        main.wait_stream(self.s_h2d)
         return self.h_out
 
     def io_bytes(self):

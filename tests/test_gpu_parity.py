@@ -266,6 +266,26 @@ def test_config2_full_size():
     assert abs(np.nanmean(S[:, 4:]) - 1) < 0.01
 
 
+def test_end_to_end_host_path_matches_device_path():
+    """pipeline.run_host (pinned H2D in frame batches on 3 streams, D2H of every result) == pipeline.run."""
+    cfg = xi.scaled(xi.CONFIGS["c3"], N=5000, T=37, lags=(1, 2, 5, 9), windows=(1, 2, 4, 8))
+    cfg = xi.Config(**{**cfg.__dict__, "n_plane": 128})
+    pos = xi.positions(cfg)
+    f = xi.form_factors(cfg)
+    wl = pipeline.workload_from_config(cfg)
+    P = pipeline.Pipeline(wl)
+    dev = P.run(_t(pos), _t(f))
+    ref = {k: v.cpu().numpy().copy() for k, v in dev.items()}
+    P.alloc_host_io(pos, f, batches=5)
+    for _ in range(2):
+        host = P.run_host()
+        torch.cuda.synchronize()
+        for k in ref:
+            np.testing.assert_array_equal(host[k].numpy(), ref[k], err_msg=k)
+    h2d, d2h = P.io_bytes()
+    assert h2d == pos.nbytes + f.nbytes and d2h > pos.shape[0] * 128 * 128 * 4
+
+
 @pytest.mark.slow
 def test_config4_full_size_sampled():
     cfg = xi.CONFIGS["c4"]
