@@ -29,20 +29,28 @@ namespace tc {
 constexpr int TM = 128, TN = 128, KS = 16;        // rows (h) per CTA, tile cols (k), atoms per stage
 constexpr int PAIR_M = 2 * TM;                    // a CTA pair (cluster of 2 SMs) owns 256 h x 128 k
 constexpr int BN = TN / 2;                        // each CTA of the pair holds half of B (64 k rows)
-constexpr int STAGES = 3;
+#ifndef XPCS_TC_STAGES
+#define XPCS_TC_STAGES 3
+#endif
+#ifndef XPCS_TC_HALFSUMS
+#define XPCS_TC_HALFSUMS 0
+#endif
+constexpr int STAGES = XPCS_TC_STAGES;
 #ifndef XPCS_TC_SUB_STAGES
 #define XPCS_TC_SUB_STAGES 16
 #endif
 constexpr int SUB_STAGES = XPCS_TC_SUB_STAGES;    // stages per TMEM accumulator (16 stages = 256 atoms)
 constexpr int APLANE = TM * KS * 2;               // bytes per fp16 A plane (128 rows x 16 atoms)
-constexpr int BPLANE = BN * KS * 2;               // bytes per fp16 B plane (64 rows x 16 atoms)
-constexpr int STAGE_BYTES = 4 * APLANE + 4 * BPLANE;   // Xr_hi Xr_lo Xs_hi Xs_lo | Wr_hi Wr_lo Ws_hi Ws_lo
+constexpr int BROWS = 3 * BN;                     // B rows of this CTA: [-Ws | Wr | Ws] for its 64 k
+constexpr int BPLANE = BROWS * KS * 2;            // bytes per fp16 B plane (192 rows x 16 atoms)
+constexpr int STAGE_BYTES = 4 * APLANE + 2 * BPLANE;   // Xr_hi Xr_lo Xs_hi Xs_lo | B_hi B_lo
+constexpr int MMA_N = 2 * TN;                     // N = 256: [Re | Im'] of 64 k per CTA half
 constexpr int NPROD_WARPS = 16, NDRAIN_WARPS = 4;
 constexpr int MMA_WARP = NPROD_WARPS + NDRAIN_WARPS;
 constexpr int NTHREADS = (MMA_WARP + 1) * 32;     // 672
-constexpr int TMEM_COLS = 512;                    // buffer b: Re cols [256b, 256b+128), Im' [256b+128, 256b+256)
+constexpr int TMEM_COLS = 512;                    // buffer b: cols [256b, 256b+256) = [Re k<64 | Im' k<64 | Re k>=64 | Im' k>=64]
 constexpr int SUM_LD = 129;                       // running sums [256 cols][129] fp32 (padded: conflict-free)
-constexpr int SUM_BYTES = 256 * SUM_LD * 4;
+constexpr int SUM_BYTES = (XPCS_TC_HALFSUMS ? 128 : 256) * SUM_LD * 4;   // HALFSUMS: timing experiments only
 constexpr int ASLOTS = 4;                         // cp.async prefetch ring depth (distance ASLOTS - 1 stages)
 constexpr int ASLOT_BYTES = NPROD_WARPS * ASLOTS * 8 * 16;   // per producer warp: its 8 atoms of ASLOTS stages
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + SUM_BYTES + ASLOT_BYTES + 1024 + 256;
@@ -78,9 +86,9 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
     return d;                                     // base offset 0, lbo mode 0, layout SWIZZLE_NONE (0)
 }
 
-// kind::f16 instruction descriptor: D fp32, A/B fp16, K-major both, N = TN, M = PAIR_M (cta_group::2).
+// kind::f16 instruction descriptor: D fp32, A/B fp16, K-major both, N = MMA_N, M = PAIR_M (cta_group::2).
 __host__ __device__ constexpr uint32_t idesc_f16(bool neg_a) {
-    return (1u << 4) | (0u << 7) | (0u << 10) | ((neg_a ? 1u : 0u) << 13) | ((uint32_t)(tc::TN >> 3) << 17) |
+    return (1u << 4) | (0u << 7) | (0u << 10) | ((neg_a ? 1u : 0u) << 13) | ((uint32_t)(tc::MMA_N >> 3) << 17) |
            ((uint32_t)(tc::PAIR_M >> 4) << 24);
 }
 
@@ -205,6 +213,17 @@ __device__ __forceinline__ void split_store_f(uint32_t addr, unsigned long long 
     sts32<OFF_HI>(addr, pack_half2(hi));
     sts32<OFF_LO>(addr, pack_half2(lo));
 }
+// value-only variant: hi / lo half2 words of f * c (residual from the exact products)
+__device__ __forceinline__ void split_vals_f(unsigned long long f2, unsigned long long c2, unsigned long long M2,
+                                             uint32_t& h, uint32_t& l) {
+    const unsigned long long t = ffma2(f2, c2, M2);
+    const unsigned long long hi = fsub2(t, M2);
+    const unsigned long long nhi = fsub2(M2, t);
+    unsigned long long lo;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(lo) : "l"(f2), "l"(c2), "l"(nhi));
+    h = pack_half2(hi);
+    l = pack_half2(lo);
+}
 // M = 1.5 * 2^(13 + e), e = max(0, exponent bound of |f|) so that |f| <= 2^e
 __device__ __forceinline__ float split_magic(float f) {
     const int ef = (int)((__float_as_uint(f) >> 23) & 0xFF);
@@ -258,7 +277,7 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
     if (warp == MMA_WARP) {
         // ================= MMA issuer: one lane of the leader CTA drives the pair =================
         if (rank == 0 && lane == 0) {
-            const uint32_t id_pos = idesc_f16(false), id_neg = idesc_f16(true);
+            const uint32_t idesc = idesc_f16(false);
             const uint32_t lo_on = dbg_flags & 1 ? 0u : 1u;   // experiments: bit 0 drops the hi.lo / lo.hi products
             const uint32_t base = smem_u32(smem);
             for (int i = 0; i < n_stages; ++i) {
@@ -272,24 +291,21 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
                 mbar_wait_cluster(&full[s], (uint32_t)((i / STAGES) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t sb = base + s * STAGE_BYTES;
-                uint64_t d[8];
-#pragma unroll
-                for (int p = 0; p < 4; ++p) d[p] = umma_desc(sb + p * APLANE, 128, 256);
-#pragma unroll
-                for (int p = 0; p < 4; ++p) d[4 + p] = umma_desc(sb + 4 * APLANE + p * BPLANE, 128, 256);
-                // planes: 0 Xr_hi 1 Xr_lo 2 Xs_hi 3 Xs_lo 4 Wr_hi 5 Wr_lo 6 Ws_hi 7 Ws_lo  (Xs = sin, Ws = f sin)
-                // Re = Xr Wr - Xs Ws ;  Im' = Xr Ws + Xs Wr = -Im  (|p|^2 is unchanged; the tile holds conj(p))
-                const uint32_t re = tmem + (uint32_t)(b * 256), im = re + TN;
+                // A planes: Xr_hi Xr_lo Xs_hi Xs_lo.  B rows of each CTA: [-Ws | Wr | Ws] (64 k each):
+                //   B1 = rows 64..191 = [Wr | Ws],  B2 = rows 0..127 = [-Ws | Wr]
+                //   Xr . B1 -> (Xr Wr, Xr Ws),  Xs . B2 -> (-Xs Ws, Xs Wr):  D = [Re | Im'] with Im' = -Im
+                const uint64_t xr_h = umma_desc(sb + 0 * APLANE, 128, 256), xr_l = umma_desc(sb + 1 * APLANE, 128, 256);
+                const uint64_t xs_h = umma_desc(sb + 2 * APLANE, 128, 256), xs_l = umma_desc(sb + 3 * APLANE, 128, 256);
+                const uint32_t bh = sb + 4 * APLANE, bl = bh + BPLANE;
+                const uint64_t b1_h = umma_desc(bh + BN * 32, 128, 256), b1_l = umma_desc(bl + BN * 32, 128, 256);
+                const uint64_t b2_h = umma_desc(bh, 128, 256), b2_l = umma_desc(bl, 128, 256);
+                const uint32_t d = tmem + (uint32_t)(b * 256);
                 const uint32_t first = sub_first ? 0u : 1u;
                 if (!(dbg_flags & 4)) {   // experiments: bit 2 skips the MMAs (producer/drain cost alone)
-                    umma2_f16(re, d[0], d[4], id_pos, first);     // Re += Xr Wr
-                    if (lo_on) { umma2_f16(re, d[0], d[5], id_pos, 1); umma2_f16(re, d[1], d[4], id_pos, 1); }
-                    umma2_f16(re, d[2], d[6], id_neg, 1);         // Re -= Xs Ws
-                    if (lo_on) { umma2_f16(re, d[2], d[7], id_neg, 1); umma2_f16(re, d[3], d[6], id_neg, 1); }
-                    umma2_f16(im, d[0], d[6], id_pos, first);     // Im' += Xr Ws
-                    if (lo_on) { umma2_f16(im, d[0], d[7], id_pos, 1); umma2_f16(im, d[1], d[6], id_pos, 1); }
-                    umma2_f16(im, d[2], d[4], id_pos, 1);         // Im' += Xs Wr
-                    if (lo_on) { umma2_f16(im, d[2], d[5], id_pos, 1); umma2_f16(im, d[3], d[4], id_pos, 1); }
+                    umma2_f16(d, xr_h, b1_h, idesc, first);
+                    if (lo_on) { umma2_f16(d, xr_h, b1_l, idesc, 1); umma2_f16(d, xr_l, b1_h, idesc, 1); }
+                    umma2_f16(d, xs_h, b2_h, idesc, 1);
+                    if (lo_on) { umma2_f16(d, xs_h, b2_l, idesc, 1); umma2_f16(d, xs_l, b2_h, idesc, 1); }
                 }
                 umma2_commit_both(&empty[s]);                     // frees the stage in both CTAs
                 if ((i % SUB_STAGES) == SUB_STAGES - 1 || i == n_stages - 1) umma2_commit_both(&tfull[b]);
@@ -349,15 +365,21 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
                     split_store<0 * APLANE, 1 * APLANE>(off, pack2(c0, c1), MX2);     // Xr = cos
                     split_store<2 * APLANE, 3 * APLANE>(off, pack2(s0, s1), MX2);     // Xs = sin
                 }
-                {   // W rows: group gi of this CTA's 64 B rows, k = k0 + bk0 + m
+                {   // W rows: group gi of this CTA's 64 k, k = k0 + bk0 + m;  B rows: -Ws at m, Wr at 64+m, Ws at 128+m
                     const int m = gi * 8 + mrow;
-                    const uint32_t off = sbase + 4 * APLANE + plane_off(m, a_loc);
                     const uint32_t kk = (uint32_t)(g.k0 + bk0 + m);
                     float s0, c0, s1, c1;
                     __sincosf(turns_to_radians(at0.z + kk * at0.y), &s0, &c0);
                     __sincosf(turns_to_radians(at1.z + kk * at1.y), &s1, &c1);
-                    split_store_f<0 * BPLANE, 1 * BPLANE>(off, F2, pack2(c0, c1), MW2);   // Wr = f cos
-                    split_store_f<2 * BPLANE, 3 * BPLANE>(off, F2, pack2(s0, s1), MW2);   // Ws = f sin
+                    uint32_t wr_h, wr_l, ws_h, ws_l;
+                    split_vals_f(F2, pack2(c0, c1), MW2, wr_h, wr_l);       // Wr = f cos
+                    split_vals_f(F2, pack2(s0, s1), MW2, ws_h, ws_l);       // Ws = f sin
+                    const uint32_t ob = sbase + 4 * APLANE;
+                    const uint32_t o_ns = ob + plane_off(m, a_loc), o_r = ob + plane_off(BN + m, a_loc),
+                                   o_s = ob + plane_off(2 * BN + m, a_loc);
+                    sts32<0>(o_r, wr_h);      sts32<BPLANE>(o_r, wr_l);
+                    sts32<0>(o_s, ws_h);      sts32<BPLANE>(o_s, ws_l);
+                    sts32<0>(o_ns, ws_h ^ 0x80008000u); sts32<BPLANE>(o_ns, ws_l ^ 0x80008000u);   // -Ws (sign bits)
                 }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> async proxy
@@ -369,7 +391,7 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
         const int quarter = warp & 3;               // TMEM lanes 32*quarter .. +31 = rows of this CTA's half
         const int r = quarter * 32 + lane;
         const uint32_t tempty0 = mapa(smem_u32(tempty), 0);
-        for (int c = 0; c < 256; ++c) sums[c * SUM_LD + r] = 0.f;
+        for (int c = 0; c < (XPCS_TC_HALFSUMS ? 128 : 256); ++c) sums[c * SUM_LD + r] = 0.f;
         for (int u = 0; u < ((dbg_flags & 8) ? 0 : n_sub); ++u) {   // experiments: bit 3 skips the drain
             const int b = u & 1;
             mbar_wait_cluster(&tfull[b], (uint32_t)((u >> 1) & 1));
@@ -378,6 +400,7 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
             uint32_t v[2][32];
 #pragma unroll
             for (int blk = 0; blk < 8; blk += 2) {
+                if (XPCS_TC_HALFSUMS && blk >= 4) { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); __syncwarp(); if (lane == 0 && blk == 6) mbar_arrive_cluster(tempty0 + (uint32_t)(b * 8)); continue; }
 #pragma unroll
                 for (int q = 0; q < 2; ++q) TMEM_LD32(tb + (uint32_t)((blk + q) * 32), v[q]);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -409,7 +432,9 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
             for (int j = 0; j < TN / 32; ++j) {
                 const int c = lane + 32 * j;
                 const int64_t ik = tk0 + c;
-                if (ik < g.n_k) P[ih * g.n_k + ik] = make_float2(sums[c * SUM_LD + row], sums[(TN + c) * SUM_LD + row]);
+                // accumulator columns: [Re k<64 | Im' k<64 | Re k>=64 | Im' k>=64]
+                const int cre = (c < BN) ? c : c + BN, cim = cre + BN;
+                if (ik < g.n_k) P[ih * g.n_k + ik] = make_float2(sums[cre * SUM_LD + row], XPCS_TC_HALFSUMS ? 0.f : sums[cim * SUM_LD + row]);
             }
         }
     }
