@@ -99,6 +99,26 @@ XPCS_API int xpcs_intensity(const void* positions, int64_t N, const void* form_f
 XPCS_API int xpcs_intensity_grid(const void* positions, int64_t N, const void* form_factors,
                         const xpcs_qgrid* grid, int64_t frames, void* I_out, const xpcs_opts* opts);
 
+/* Complex amplitude p^e(q,t) = sum_j f_j exp(-i q . r_j(t)) itself (Eq. 7, the paper's sign),
+ * for the intermediate scattering function (Eq. 22) and any analysis that needs phases.  Same arguments and
+ * engines as xpcs_intensity / xpcs_intensity_grid; A_out [frames][n_q][2] out_dtype = (Re p, Im p). */
+XPCS_API int xpcs_amplitude(const void* positions, int64_t N, const void* form_factors,
+                   const void* q_vectors, int64_t n_q, int64_t frames, double box_L,
+                   void* A_out, const xpcs_opts* opts);
+XPCS_API int xpcs_amplitude_grid(const void* positions, int64_t N, const void* form_factors,
+                        const xpcs_qgrid* grid, int64_t frames, void* A_out, const xpcs_opts* opts);
+
+/* Intermediate scattering function, Eq.(22), PAPER.md:218-223:
+ *   F(q, tau) = (1 / (T - tau)) sum_{t=0}^{T-1-tau} p(q,t) p*(q, t+tau)  /  sum_j f_j^2
+ * (time average over the T - tau available pairs; sum_j f_j^2 reduced on the device from form_factors, NULL => N).
+ * F(q,0) = S(q) (Eq. 12); the normalised F^ = F(tau)/F(0) of Eq.(23) and the Siegert relation g2 = 1 + beta0 |F^|^2
+ * (Eq. 24) are formed from these outputs.
+ *   A_series [frames][n_q][2] in_dtype;  lags HOST [n_lags] (0 <= lag < frames, <= 320);
+ *   F_out DEVICE [n_lags][n_q][2] double.
+ * Errors: EINVAL for null pointers, sizes <= 0, lags out of range; EUNSUPPORTED for lags > 320. */
+XPCS_API int xpcs_isf(const void* A_series, int64_t frames, int64_t n_q, const int32_t* lags, int64_t n_lags,
+             const void* form_factors, int64_t N, double* F_out, const xpcs_opts* opts);
+
 /* ------------------------------------------------------------------------------------------------
  * Intensity autocorrelation, Eq.(14), PAPER.md:170-174 (literal estimator, R6), per pixel:
  *   num(tau) = 1/(T - tau) sum_{t=0}^{T-1-tau} I_t I_{t+tau},  den = ((1/T) sum_t I_t)^2,  g2 = num / den.

@@ -10,6 +10,7 @@ Contents (each function cites the passage it follows):
   * lattice_q       -- reciprocal-lattice q = (2 pi / L) (m0 + h ma + k mb), Algorithm 1 step 1.
   * ewald_q         -- Ewald-sphere detector q = k (u - z), Eq.(1) + Fig. 5 (reading R4).
   * g2              -- Eq.(14) literal estimator (reading R6).
+  * amplitudes / isf -- Eq.(7) per frame, Eq.(22) intermediate scattering function.
   * lattice_bins / radial_bins / shell_mean / structure_factor_shells -- ring average, Eq.(12).
   * xsvs_beta       -- Eq.(15) + Eq.(17), per-snapshot then averaged.
 Every function is pinned by tests/test_oracle_pins.py (no function here is "parity unpinned").
@@ -129,6 +130,25 @@ def intensity(pos, f, q, L):
     n_q = q.shape[0]
     out = np.zeros((T, n_q))
     lib().oracle_intensity(pp, N, fp, qp, n_q, T, float(L), out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    return out
+
+
+def amplitudes(pos, f, q, L):
+    """Eq.(7) for every frame: complex p^e [T][n_q] (positions [T][N][3] or [N][3])."""
+    pos = np.asarray(pos)
+    if pos.ndim == 2:
+        pos = pos[None]
+    return np.stack([amplitude(p, f, q, L) for p in pos])
+
+
+def isf(A, lags, S2):
+    """Eq.(22): F(q, tau) = <p(t) p*(t + tau)>_t / sum_j f_j^2, the time average taken over the
+    T - tau available pairs.  A complex [T][n_q] -> complex [n_lags][n_q]."""
+    A = np.asarray(A, dtype=np.complex128)
+    T = A.shape[0]
+    out = np.empty((len(lags), A.shape[1]), dtype=np.complex128)
+    for i, tau in enumerate(lags):
+        out[i] = (A[: T - tau] * np.conj(A[tau:])).sum(0) / (T - tau) / S2
     return out
 
 

@@ -24,6 +24,7 @@ EXPORTED = (
     "xpcs_structure_factor_shells", "xpcs_qgrid_lattice_plane", "xpcs_qgrid_ewald", "xpcs_lattice_bins",
     "xpcs_radial_bins", "xpcs_last_error", "xpcs_release", "xpcs_launch_count", "xpcs_profile_reset",
     "xpcs_profile_query", "xpcs_device_info", "xpcs_version", "xpcs_engine_available",
+    "xpcs_amplitude", "xpcs_amplitude_grid", "xpcs_isf",
 )
 
 
@@ -83,6 +84,9 @@ def load():
         "xpcs_device_info": [ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)],
         "xpcs_version": [],
         "xpcs_engine_available": [i32],
+        "xpcs_amplitude": [vp, i64, vp, vp, i64, i64, dbl, vp, op],
+        "xpcs_amplitude_grid": [vp, i64, vp, gp, i64, vp, op],
+        "xpcs_isf": [vp, i64, i64, ip32, i64, vp, i64, vp, op],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -180,6 +184,56 @@ def xpcs_intensity_grid(positions, form_factors, grid: QGrid, out=None, out_dtyp
     o = make_opts(ind, outd, stream, engine, profile)
     _check(load().xpcs_intensity_grid(_ptr(positions), N, _ptr(form_factors), ctypes.byref(grid), T, _ptr(out),
                                       ctypes.byref(o)))
+    return out
+
+
+def xpcs_amplitude(positions, form_factors, q_vectors, box_L, out=None, out_dtype=None, stream=None):
+    """Eq.(7) complex amplitude at an explicit q list -> [T][n_q][2] (Re, Im)."""
+    import torch
+    if positions.dim() == 2:
+        positions = positions.unsqueeze(0)
+    T, N = positions.shape[0], positions.shape[1]
+    n_q = q_vectors.shape[0]
+    ind = _dtype_code(positions)
+    outd = ind if out_dtype is None else out_dtype
+    if out is None:
+        out = torch.empty((T, n_q, 2), dtype=torch.float64 if outd == F64 else torch.float32, device=positions.device)
+    o = make_opts(ind, outd, stream)
+    _check(load().xpcs_amplitude(_ptr(positions), N, _ptr(form_factors), _ptr(q_vectors), n_q, T, float(box_L),
+                                 _ptr(out), ctypes.byref(o)))
+    return out
+
+
+def xpcs_amplitude_grid(positions, form_factors, grid: QGrid, out=None, out_dtype=None, engine=ENGINE_AUTO,
+                        stream=None):
+    """Eq.(7) complex amplitude on a lattice plane -> [T][n_h * n_k][2] (Re, Im)."""
+    import torch
+    if positions.dim() == 2:
+        positions = positions.unsqueeze(0)
+    T, N = positions.shape[0], positions.shape[1]
+    ind = _dtype_code(positions)
+    outd = ind if out_dtype is None else out_dtype
+    if out is None:
+        out = torch.empty((T, grid.n_q, 2), dtype=torch.float64 if outd == F64 else torch.float32,
+                          device=positions.device)
+    o = make_opts(ind, outd, stream, engine)
+    _check(load().xpcs_amplitude_grid(_ptr(positions), N, _ptr(form_factors), ctypes.byref(grid), T, _ptr(out),
+                                      ctypes.byref(o)))
+    return out
+
+
+def xpcs_isf(A, lags, form_factors=None, N=None, out=None, stream=None):
+    """Eq.(22) intermediate scattering function from an amplitude series A [T][n_q][2] -> F [n_lags][n_q][2]."""
+    import torch
+    T, n_q = A.shape[0], A.shape[1]
+    lag_arr, lag_p = _i32_array(lags)
+    if N is None:
+        N = form_factors.shape[0] if form_factors is not None else 1
+    if out is None:
+        out = torch.empty((len(lag_arr), n_q, 2), dtype=torch.float64, device=A.device)
+    o = make_opts(_dtype_code(A), F64, stream)
+    _check(load().xpcs_isf(_ptr(A), T, n_q, lag_p, len(lag_arr), _ptr(form_factors), int(N), _ptr(out),
+                           ctypes.byref(o)))
     return out
 
 

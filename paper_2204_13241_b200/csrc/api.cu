@@ -178,9 +178,12 @@ int xpcs_engine_available(int32_t engine) {
     return 0;
 }
 
+}  // extern "C"
+
 // ------------------------------------------------------------------------------------------- intensity
-int xpcs_intensity(const void* positions, int64_t N, const void* form_factors, const void* q_vectors, int64_t n_q,
-                   int64_t frames, double box_L, void* I_out, const xpcs_opts* opts) {
+// amp = 0: I(q,t) = |p|^2 (Eq. 8) -> out [frames][n_q];  amp = 1: p(q,t) (Eq. 7) -> out [frames][n_q][2]
+static int run_direct(const void* positions, int64_t N, const void* form_factors, const void* q_vectors, int64_t n_q,
+                      int64_t frames, double box_L, void* I_out, const xpcs_opts* opts, int amp) {
     clear_error();
     Opts o;
     TRY(parse_opts(opts, o));
@@ -199,7 +202,7 @@ int xpcs_intensity(const void* positions, int64_t N, const void* form_factors, c
         return XPCS_EINVAL;
     }
     TRY(check_sticky());
-    const size_t isz = out_size(o.out_f64);
+    const size_t isz = out_size(o.out_f64) * (amp ? 2 : 1);
     const size_t psz = o.in_f64 ? 24 : 12;
     if (o.in_f64) {
         const int64_t Tb = std::max<int64_t>(1, std::min<int64_t>(frames, (int64_t)(kBatchBytes / std::max<int64_t>(1, std::max<int64_t>(32 * N, 16 * n_q)))));
@@ -213,7 +216,7 @@ int xpcs_intensity(const void* positions, int64_t N, const void* form_factors, c
             { ProfScope p(o.profile, KC_MAIN, o.s);
               TRY(cuda_fail(launch_generic64(st, N, tb, q_vectors, n_q, box_L, part, o.s), "generic64")); }
             { ProfScope p(o.profile, KC_REDUCE, o.s);
-              TRY(cuda_fail(launch_amp_reduce_d(part, 1, tb, n_q, (char*)I_out + isz * n_q * t0, o.out_f64, o.s), "reduce")); }
+              TRY(cuda_fail(launch_amp_reduce_d(part, 1, tb, n_q, (char*)I_out + isz * n_q * t0, o.out_f64, amp, o.s), "reduce")); }
         }
         return XPCS_OK;
     }
@@ -236,13 +239,13 @@ int xpcs_intensity(const void* positions, int64_t N, const void* form_factors, c
         { ProfScope p(o.profile, KC_MAIN, o.s);
           TRY(cuda_fail(launch_generic32(st, N, tb, q_vectors, 0, n_q, box_L, chunk, C, part, o.s), "generic32")); }
         { ProfScope p(o.profile, KC_REDUCE, o.s);
-          TRY(cuda_fail(launch_amp_reduce_d(part, C, tb, n_q, (char*)I_out + isz * n_q * t0, o.out_f64, o.s), "reduce")); }
+          TRY(cuda_fail(launch_amp_reduce_d(part, C, tb, n_q, (char*)I_out + isz * n_q * t0, o.out_f64, amp, o.s), "reduce")); }
     }
     return XPCS_OK;
 }
 
-int xpcs_intensity_grid(const void* positions, int64_t N, const void* form_factors, const xpcs_qgrid* grid,
-                        int64_t frames, void* I_out, const xpcs_opts* opts) {
+static int run_grid(const void* positions, int64_t N, const void* form_factors, const xpcs_qgrid* grid,
+                    int64_t frames, void* I_out, const xpcs_opts* opts, int amp) {
     clear_error();
     Opts o;
     TRY(parse_opts(opts, o));
@@ -254,7 +257,7 @@ int xpcs_intensity_grid(const void* positions, int64_t N, const void* form_facto
     TRY(check_sticky());
     const LatticeGeom g = to_geom(*grid);
     const int64_t n_q = g.n_h * g.n_k;
-    const size_t isz = out_size(o.out_f64);
+    const size_t isz = out_size(o.out_f64) * (amp ? 2 : 1);
     if (o.in_f64) {
         if (o.engine == XPCS_ENGINE_TENSOR) {
             set_error("xpcs: the tensor engine needs f32 inputs");
@@ -268,7 +271,7 @@ int xpcs_intensity_grid(const void* positions, int64_t N, const void* form_facto
             { ProfScope p(o.profile, KC_STAGE, o.s);
               TRY(cuda_fail(launch_stage_lattice64((const char*)positions + 24 * N * t0, form_factors, N, tb, g, st, o.s), "stage")); }
             { ProfScope p(o.profile, KC_MAIN, o.s);
-              TRY(cuda_fail(launch_lattice_f64(st, N, tb, g, (char*)I_out + isz * n_q * t0, o.out_f64, o.s), "lattice64")); }
+              TRY(cuda_fail(launch_lattice_f64(st, N, tb, g, (char*)I_out + isz * n_q * t0, o.out_f64, amp, o.s), "lattice64")); }
         }
         return XPCS_OK;
     }
@@ -281,7 +284,7 @@ int xpcs_intensity_grid(const void* positions, int64_t N, const void* form_facto
         }
     }
     // atom chunks (split-K over CTAs, folded in FP64 by the reduction): SIMT keeps fp32 register sums short
-    // (<= 4096 atoms); the tensor engine drains TMEM every 128 atoms into RN sums, so its chunks only balance
+    // (<= 4096 atoms); the tensor engine drains TMEM every 256 atoms into RN sums, so its chunks only balance
     // the grid (>= ~8 waves of one CTA per SM) and stay >= 1024 atoms.
     int64_t chunk = 4096;
     if (tc) {
@@ -305,9 +308,68 @@ int xpcs_intensity_grid(const void* positions, int64_t N, const void* form_facto
           if (tc) TRY(cuda_fail(launch_lattice_tc(st, N, tb, g, chunk, C, part, o.s), "lattice tcgen05"));
           else TRY(cuda_fail(launch_lattice_simt(st, N, tb, g, chunk, C, part, o.s), "lattice simt")); }
         { ProfScope p(o.profile, KC_REDUCE, o.s);
-          TRY(cuda_fail(launch_amp_reduce_f(part, C, tb, n_q, (char*)I_out + isz * n_q * t0, o.out_f64, o.s), "reduce")); }
+          // the tensor engine's partials hold conj(p) (R1)
+          TRY(cuda_fail(launch_amp_reduce_f(part, C, tb, n_q, (char*)I_out + isz * n_q * t0, o.out_f64,
+                                            amp ? (tc ? 2 : 1) : 0, o.s), "reduce")); }
     }
     return XPCS_OK;
+}
+
+extern "C" {
+
+int xpcs_intensity(const void* positions, int64_t N, const void* form_factors, const void* q_vectors, int64_t n_q,
+                   int64_t frames, double box_L, void* I_out, const xpcs_opts* opts) {
+    return run_direct(positions, N, form_factors, q_vectors, n_q, frames, box_L, I_out, opts, 0);
+}
+int xpcs_amplitude(const void* positions, int64_t N, const void* form_factors, const void* q_vectors, int64_t n_q,
+                   int64_t frames, double box_L, void* A_out, const xpcs_opts* opts) {
+    return run_direct(positions, N, form_factors, q_vectors, n_q, frames, box_L, A_out, opts, 1);
+}
+int xpcs_intensity_grid(const void* positions, int64_t N, const void* form_factors, const xpcs_qgrid* grid,
+                        int64_t frames, void* I_out, const xpcs_opts* opts) {
+    return run_grid(positions, N, form_factors, grid, frames, I_out, opts, 0);
+}
+int xpcs_amplitude_grid(const void* positions, int64_t N, const void* form_factors, const xpcs_qgrid* grid,
+                        int64_t frames, void* A_out, const xpcs_opts* opts) {
+    return run_grid(positions, N, form_factors, grid, frames, A_out, opts, 1);
+}
+
+int xpcs_isf(const void* A_series, int64_t frames, int64_t n_q, const int32_t* lags, int64_t n_lags,
+             const void* form_factors, int64_t N, double* F_out, const xpcs_opts* opts) {
+    clear_error();
+    Opts o;
+    TRY(parse_opts(opts, o));
+    NEED(A_series, "A_series");
+    NEED(lags, "lags");
+    NEED(F_out, "F_out");
+    POS(frames, "frames");
+    POS(n_q, "n_q");
+    POS(n_lags, "n_lags");
+    POS(N, "N");
+    int max_lag = 0;
+    for (int64_t i = 0; i < n_lags; ++i) {
+        if (lags[i] < 0 || lags[i] >= frames) {
+            set_error("xpcs: lag %d out of range [0, %lld)", lags[i], (long long)frames);
+            return XPCS_EINVAL;
+        }
+        max_lag = std::max(max_lag, (int)lags[i]);
+    }
+    if (max_lag > 320) {
+        set_error("xpcs: lags > 320 frames are not supported by xpcs_isf in this build");
+        return XPCS_EUNSUPPORTED;
+    }
+    TRY(check_sticky());
+    int32_t* dl = (int32_t*)scratch(o.s, SS_LAGS, sizeof(int32_t) * (size_t)n_lags);
+    if (!dl) return XPCS_ENOMEM;
+    TRY(cuda_fail(cudaMemcpyAsync(dl, lags, sizeof(int32_t) * (size_t)n_lags, cudaMemcpyHostToDevice, o.s), "lag upload"));
+    double* norm = nullptr;
+    if (form_factors) {
+        norm = (double*)scratch(o.s, SS_SMALL, 64);
+        if (!norm) return XPCS_ENOMEM;
+        TRY(cuda_fail(launch_sum_f2(form_factors, o.in_f64, N, norm, o.s), "sum f^2"));
+    }
+    ProfScope p(o.profile, KC_G2, o.s);
+    return cuda_fail(launch_isf(A_series, o.in_f64, frames, n_q, dl, n_lags, max_lag, norm, (double)N, F_out, o.s), "isf");
 }
 
 // ------------------------------------------------------------------------------------------- statistics

@@ -121,18 +121,21 @@ cudaError_t launch_lattice_tc(const uint4* staged, int64_t N, int64_t frames, co
 bool lattice_tc_supported(const LatticeGeom& g);
 // lattice FP64 (direct per-pixel evaluation with 64-bit turns): writes I directly (double)
 cudaError_t launch_lattice_f64(const ulonglong4* staged, int64_t N, int64_t frames, const LatticeGeom& g,
-                               void* I_out, int out_f64, cudaStream_t s);
+                               void* I_out, int out_f64, int mode, cudaStream_t s);
 // generic q list: partial [C][Tb][n_q] double2
 cudaError_t launch_generic32(const uint4* staged, int64_t N, int64_t frames, const void* q, int q_f64,
                              int64_t n_q, double L, int64_t chunk_atoms, int64_t n_chunks, double2* partial,
                              cudaStream_t s);
 cudaError_t launch_generic64(const ulonglong4* staged, int64_t N, int64_t frames, const void* q,
                              int64_t n_q, double L, double2* partial, cudaStream_t s);
-// |sum_c partial|^2 -> I_out rows
+// fold of the atom-chunk partials: mode 0 -> I = |p|^2, 1 -> p (re, im), 2 -> partials hold conj(p), write p
 cudaError_t launch_amp_reduce_f(const float2* partial, int64_t C, int64_t frames, int64_t n_q, void* I_out,
-                                int out_f64, cudaStream_t s);
+                                int out_f64, int mode, cudaStream_t s);
 cudaError_t launch_amp_reduce_d(const double2* partial, int64_t C, int64_t frames, int64_t n_q, void* I_out,
-                                int out_f64, cudaStream_t s);
+                                int out_f64, int mode, cudaStream_t s);
+// intermediate scattering function F(q, tau) = <p(t) p*(t + tau)>_t / norm, complex in/out
+cudaError_t launch_isf(const void* A, int in_f64, int64_t T, int64_t n_q, const int32_t* lags_dev, int64_t n_lags,
+                       int max_lag, const double* norm, double norm_const, double* F_out, cudaStream_t s);
 
 // statistics
 cudaError_t launch_g2(const void* I, int in_f64, int64_t T, int64_t n_q, const int32_t* lags_dev,

@@ -138,7 +138,7 @@ k_generic64(const ulonglong4* __restrict__ staged, int64_t N, const double* __re
 // ---- FP64 lattice: one pixel per thread, 64-bit turns (exact h*Th_a + k*Th_b + Th_0 mod 2^64)
 template <typename O>
 __global__ void __launch_bounds__(128)
-k_lattice64(const ulonglong4* __restrict__ staged, int64_t N, LatticeGeom g, O* __restrict__ I_out) {
+k_lattice64(const ulonglong4* __restrict__ staged, int64_t N, LatticeGeom g, O* __restrict__ I_out, int mode) {
     __shared__ ulonglong4 As[128];
     const int64_t t = blockIdx.y;
     const int64_t n_q = g.n_h * g.n_k;
@@ -163,13 +163,17 @@ k_lattice64(const ulonglong4* __restrict__ staged, int64_t N, LatticeGeom g, O* 
             im -= fj * s;
         }
     }
-    if (pix < n_q) I_out[t * n_q + pix] = (O)(re * re + im * im);
+    if (pix < n_q) {
+        if (mode == 0) I_out[t * n_q + pix] = (O)(re * re + im * im);          // Eq.(8)
+        else { I_out[2 * (t * n_q + pix)] = (O)re; I_out[2 * (t * n_q + pix) + 1] = (O)im; }   // Eq.(7)
+    }
 }
 
 // ---- |sum_c P_c|^2 (FP64 fold of the atom chunks, fixed order)
+// mode 0: I = |p|^2 (Eq. 8);  mode 1: p = (re, im) (Eq. 7);  mode 2: the partials hold conj(p) -> p
 template <typename P, typename O>
 __global__ void __launch_bounds__(256)
-k_amp_reduce(const P* __restrict__ partial, int64_t C, int64_t total, O* __restrict__ out) {
+k_amp_reduce(const P* __restrict__ partial, int64_t C, int64_t total, O* __restrict__ out, int mode) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         double re = 0.0, im = 0.0;
         for (int64_t c = 0; c < C; ++c) {
@@ -177,7 +181,8 @@ k_amp_reduce(const P* __restrict__ partial, int64_t C, int64_t total, O* __restr
             re += (double)v.x;
             im += (double)v.y;
         }
-        out[i] = (O)(re * re + im * im);          // Eq.(8): I = p p*
+        if (mode == 0) out[i] = (O)(re * re + im * im);          // Eq.(8): I = p p*
+        else { out[2 * i] = (O)re; out[2 * i + 1] = (O)(mode == 2 ? -im : im); }
     }
 }
 
@@ -201,12 +206,12 @@ cudaError_t launch_generic64(const ulonglong4* staged, int64_t N, int64_t frames
 }
 
 cudaError_t launch_lattice_f64(const ulonglong4* staged, int64_t N, int64_t frames, const LatticeGeom& g,
-                               void* I_out, int out_f64, cudaStream_t s) {
+                               void* I_out, int out_f64, int mode, cudaStream_t s) {
     const int64_t n_q = g.n_h * g.n_k;
     dim3 grid((unsigned)((n_q + 127) / 128), (unsigned)frames);
     note_launch();
-    if (out_f64) k_lattice64<double><<<grid, 128, 0, s>>>(staged, N, g, (double*)I_out);
-    else k_lattice64<float><<<grid, 128, 0, s>>>(staged, N, g, (float*)I_out);
+    if (out_f64) k_lattice64<double><<<grid, 128, 0, s>>>(staged, N, g, (double*)I_out, mode);
+    else k_lattice64<float><<<grid, 128, 0, s>>>(staged, N, g, (float*)I_out, mode);
     return cudaGetLastError();
 }
 
@@ -217,20 +222,20 @@ static dim3 rgrid(int64_t total) {
 }
 
 cudaError_t launch_amp_reduce_f(const float2* partial, int64_t C, int64_t frames, int64_t n_q, void* I_out,
-                                int out_f64, cudaStream_t s) {
+                                int out_f64, int mode, cudaStream_t s) {
     const int64_t total = frames * n_q;
     note_launch();
-    if (out_f64) k_amp_reduce<float2, double><<<rgrid(total), 256, 0, s>>>(partial, C, total, (double*)I_out);
-    else k_amp_reduce<float2, float><<<rgrid(total), 256, 0, s>>>(partial, C, total, (float*)I_out);
+    if (out_f64) k_amp_reduce<float2, double><<<rgrid(total), 256, 0, s>>>(partial, C, total, (double*)I_out, mode);
+    else k_amp_reduce<float2, float><<<rgrid(total), 256, 0, s>>>(partial, C, total, (float*)I_out, mode);
     return cudaGetLastError();
 }
 
 cudaError_t launch_amp_reduce_d(const double2* partial, int64_t C, int64_t frames, int64_t n_q, void* I_out,
-                                int out_f64, cudaStream_t s) {
+                                int out_f64, int mode, cudaStream_t s) {
     const int64_t total = frames * n_q;
     note_launch();
-    if (out_f64) k_amp_reduce<double2, double><<<rgrid(total), 256, 0, s>>>(partial, C, total, (double*)I_out);
-    else k_amp_reduce<double2, float><<<rgrid(total), 256, 0, s>>>(partial, C, total, (float*)I_out);
+    if (out_f64) k_amp_reduce<double2, double><<<rgrid(total), 256, 0, s>>>(partial, C, total, (double*)I_out, mode);
+    else k_amp_reduce<double2, float><<<rgrid(total), 256, 0, s>>>(partial, C, total, (float*)I_out, mode);
     return cudaGetLastError();
 }
 

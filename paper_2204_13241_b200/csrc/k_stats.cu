@@ -102,6 +102,77 @@ cudaError_t launch_g2(const void* I, int in_f64, int64_t T, int64_t n_q, const i
     return cudaGetLastError();
 }
 
+
+// =====================================================================================================
+// Intermediate scattering function, Eq.(22), PAPER.md:218-223:
+//     F(q, tau) = (1 / (T - tau)) sum_{t < T - tau} p(q, t) p*(q, t + tau)  /  sum_j f_j^2
+// from the complex amplitude series p [T][n_q] (re, im).  Same tiling as K4: a warp owns 32 pixels x 16 lags,
+// the series are staged through shared memory with a zero halo; FP64 accumulation.
+// =====================================================================================================
+template <typename In>
+__global__ void __launch_bounds__(256)
+k_isf(const In* __restrict__ A, int64_t T, int64_t n_q, const int32_t* __restrict__ lags, int64_t n_lags, int halo,
+      const double* __restrict__ norm, double norm_const, double* __restrict__ F) {
+    extern __shared__ __align__(16) unsigned char isf_smem[];
+    double2* S = reinterpret_cast<double2*>(isf_smem);   // [(GC + halo)][32]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t px = (int64_t)blockIdx.x * 32 + lane;
+    const int64_t lbase = (int64_t)blockIdx.y * G2_LAGS_PER_BLOCK + warp * G2_LPW;
+    int tau[G2_LPW];
+#pragma unroll
+    for (int l = 0; l < G2_LPW; ++l) tau[l] = (lbase + l < n_lags) ? lags[lbase + l] : 0;
+    double ar[G2_LPW], ai[G2_LPW];
+#pragma unroll
+    for (int l = 0; l < G2_LPW; ++l) ar[l] = ai[l] = 0.0;
+    const int rows = GC + halo;
+    for (int64_t t0 = 0; t0 < T; t0 += GC) {
+        __syncthreads();
+        for (int r = warp; r < rows; r += G2_WARPS) {
+            const int64_t t = t0 + r;
+            double2 v = make_double2(0.0, 0.0);
+            if (t < T && px < n_q) v = make_double2((double)A[2 * (t * n_q + px)], (double)A[2 * (t * n_q + px) + 1]);
+            S[r * 32 + lane] = v;
+        }
+        __syncthreads();
+        if (lbase >= n_lags) continue;
+        const int rmax = (int)min((int64_t)GC, T - t0);
+        for (int r = 0; r < rmax; ++r) {
+            const double2 p = S[r * 32 + lane];
+#pragma unroll
+            for (int l = 0; l < G2_LPW; ++l) {
+                const double2 q2 = S[(r + tau[l]) * 32 + lane];      // p(t) conj(p(t + tau))
+                ar[l] = fma(p.x, q2.x, fma(p.y, q2.y, ar[l]));
+                ai[l] = fma(p.y, q2.x, fma(-p.x, q2.y, ai[l]));
+            }
+        }
+    }
+    if (px >= n_q || lbase >= n_lags) return;
+    const double nrm = norm ? norm[0] : norm_const;
+#pragma unroll
+    for (int l = 0; l < G2_LPW; ++l) {
+        if (lbase + l >= n_lags) break;
+        const double w = 1.0 / ((double)(T - tau[l]) * nrm);
+        F[2 * ((lbase + l) * n_q + px)] = ar[l] * w;
+        F[2 * ((lbase + l) * n_q + px) + 1] = ai[l] * w;
+    }
+}
+
+cudaError_t launch_isf(const void* A, int in_f64, int64_t T, int64_t n_q, const int32_t* lags_dev, int64_t n_lags,
+                       int max_lag, const double* norm, double norm_const, double* F_out, cudaStream_t s) {
+    dim3 grid((unsigned)((n_q + 31) / 32), (unsigned)((n_lags + G2_LAGS_PER_BLOCK - 1) / G2_LAGS_PER_BLOCK));
+    const size_t smem = sizeof(double2) * 32 * (GC + max_lag);
+    note_launch();
+    if (in_f64) {
+        auto k = k_isf<double>;
+        if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k<<<grid, 256, smem, s>>>((const double*)A, T, n_q, lags_dev, n_lags, max_lag, norm, norm_const, F_out);
+    } else {
+        auto k = k_isf<float>;
+        if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k<<<grid, 256, smem, s>>>((const float*)A, T, n_q, lags_dev, n_lags, max_lag, norm, norm_const, F_out);
+    }
+    return cudaGetLastError();
+}
 // =====================================================================================================
 // Ring plan: pixels sorted by (ring, pixel index) -- stable and deterministic.
 //   k_bin_count : per 1024-pixel block, per-ring counts (shared-memory integer atomics: exact)

@@ -334,3 +334,38 @@ def test_shell_mean_and_structure_factor():
     assert np.all(np.isnan(out[:, 2]))
     S = oracle.structure_factor_shells(I, np.array([1.0, 2.0]), 2, bins, 3)
     np.testing.assert_allclose(S[:, :2], out[:, :2] / 5.0)
+
+
+# ------------------------------------------------------------------ intermediate scattering function (8(f) rank 1)
+def test_isf_brownian_and_siegert():
+    """Eq.(22)-(25): for independent Brownian particles on lattice q != 0, E[p(t) p*(t+tau)] / S2 =
+    exp(-D q^2 tau dt) (real); F(0) = S(q) (Eq. 12 vs Eq. 22); and the Siegert relation Eq.(24),
+    g2 - 1 = beta0 |F^|^2, holds for the unbiased g2 numerator (Fig. 4b)."""
+    N, L, T, D, dt = 300, 7.0, 500, 0.05, 1.0
+    pos, f = _brownian(N, L, T, D, dt, seed=99)
+    n = 16
+    q = oracle.lattice_q(L, **oracle.plane_grid(n))
+    A = oracle.amplitudes(pos, f, q, L)
+    S2, S4 = np.sum(f ** 2), np.sum(f ** 4)
+    lags = [0, 1, 2, 4, 8]
+    F = oracle.isf(A, lags, S2)
+    I = oracle.intensity(pos, f, q, L)
+    np.testing.assert_allclose(F[0].real, I.mean(0) / S2, rtol=1e-12)     # F(q, 0) = <S(q, t)>_t
+    np.testing.assert_allclose(F[0].imag, 0.0, atol=1e-12 * N)
+    bins = oracle.lattice_bins(n, n_bins=4)
+    q2 = (q ** 2).sum(1)
+    beta0 = 1 - S4 / S2 ** 2
+    den = I.mean(0) ** 2
+    G = oracle.g2(I, lags)
+    for li, tau in enumerate(lags[1:], start=1):
+        for b in range(4):
+            sel = bins == b
+            phi = np.exp(-D * q2[sel] * tau * dt)
+            for comp, pred in ((F[li, sel].real, phi), (F[li, sel].imag, 0 * phi)):
+                z = (comp.mean() - pred.mean()) / (comp.std() / np.sqrt(sel.sum() / 2))
+                assert abs(z) < 5, (tau, b, z)
+            # Siegert: the unbiased numerator num/S2^2 - 1 vs beta0 |F|^2 with E|F|^2 ~ phi^2 (ring level)
+            num = G[li, sel] * den[sel] / S2 ** 2 - 1
+            sieg = beta0 * phi ** 2
+            z = (num.mean() - sieg.mean()) / (num.std() / np.sqrt(sel.sum() / 2))
+            assert abs(z) < 5, (tau, b, z)
