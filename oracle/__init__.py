@@ -13,6 +13,9 @@ Contents (each function cites the passage it follows):
   * amplitudes / isf -- Eq.(7) per frame, Eq.(22) intermediate scattering function.
   * lattice_bins / radial_bins / shell_mean / structure_factor_shells -- ring average, Eq.(12).
   * xsvs_beta       -- Eq.(15) + Eq.(17), per-snapshot then averaged.
+  * lattice_volume_q -- 3-D reciprocal-lattice block (Table 1's 81^3 grid).
+  * species_intensity / pair_sum_species -- Eq.(2)/(7) with q-dependent form factors f_s(q).
+  * form_factor_gaussian -- f(q) as a sum of Gaussians.
 Every function is pinned by tests/test_oracle_pins.py (no function here is "parity unpinned").
 """
 from __future__ import annotations
@@ -48,6 +51,9 @@ def lib():
         L.oracle_amplitude.argtypes = [dp, i64, dp, dp, i64, ctypes.c_double, dp, dp]
         L.oracle_intensity.argtypes = [dp, i64, dp, dp, i64, i64, ctypes.c_double, dp]
         L.oracle_pair_sum.argtypes = [dp, i64, dp, dp, i64, ctypes.c_double, dp]
+        ip = ctypes.POINTER(ctypes.c_int32)
+        L.oracle_species.argtypes = [dp, i64, ip, dp, dp, i64, i64, ctypes.c_double, ctypes.c_int, dp]
+        L.oracle_pair_sum_species.argtypes = [dp, i64, ip, dp, dp, i64, ctypes.c_double, dp]
         L.oracle_max_threads.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -80,6 +86,26 @@ def lattice_q(L, h0, n_h, k0, n_k, m0=(0, 0, 0), ma=(1, 0, 0), mb=(0, 1, 0)) -> 
     m = (np.asarray(m0, np.float64)[None, None, :] + h * np.asarray(ma, np.float64)[None, None, :]
          + k * np.asarray(mb, np.float64)[None, None, :])
     return (2.0 * np.pi / L) * m.reshape(-1, 3)
+
+
+def lattice_volume_q(L, h0, n_h, k0, n_k, l0, n_l, m0=(0, 0, 0), ma=(1, 0, 0), mb=(0, 1, 0), mc=(0, 0, 1)):
+    """Algorithm 1 step 1 on a 3-D block of the reciprocal lattice (the 81 x 81 x 81 grid of
+    Table 1): q = (2 pi / L) (m0 + h ma + k mb + l mc), index ((il * n_h) + ih) * n_k + ik, i.e.
+    the l-planes of lattice_q stacked.  FP64."""
+    planes = [lattice_q(L, h0, n_h, k0, n_k, tuple(np.asarray(m0) + (l0 + il) * np.asarray(mc)), ma, mb)
+              for il in range(n_l)]
+    return np.concatenate(planes, 0)
+
+
+def form_factor_gaussian(q, a, b, c):
+    """Atomic form factor as a sum of Gaussians ('well parameterized by a sum of Gaussians'):
+    f(q) = c + sum_i a_i exp(-b_i s^2) with s = |q| / (4 pi) (= sin(theta) / lambda).  q [n_q][3] -> [n_q] FP64."""
+    q = np.asarray(q, dtype=np.float64)
+    s2 = (q * q).sum(1) / (4.0 * np.pi) ** 2
+    out = np.full(q.shape[0], float(c))
+    for ai, bi in zip(a, b):
+        out += float(ai) * np.exp(-float(bi) * s2)
+    return out
 
 
 def plane_grid(n):
@@ -149,6 +175,43 @@ def isf(A, lags, S2):
     out = np.empty((len(lags), A.shape[1]), dtype=np.complex128)
     for i, tau in enumerate(lags):
         out[i] = (A[: T - tau] * np.conj(A[tau:])).sum(0) / (T - tau) / S2
+    return out
+
+
+def _species_args(species, fq, n_q):
+    sp = np.ascontiguousarray(species, dtype=np.int32)
+    fq = np.ascontiguousarray(fq, dtype=np.float64)
+    assert fq.ndim == 2 and fq.shape[1] == n_q and sp.min() >= 0 and sp.max() < fq.shape[0]
+    return sp, sp.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), fq, fq.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def species_intensity(pos, species, fq, q, L, amp=False):
+    """Eq.(2)/(7)/(8) with q-dependent form factors f_{s(j)}(q): p = sum_j f_{s(j)}(q) e^{-i q.r_j},
+    I = |p|^2.  pos [T][N][3] (or [N][3]), species [N] int, fq [n_species][n_q].  Returns I [T][n_q] or, with
+    amp=True, complex p [T][n_q]."""
+    pos = np.asarray(pos)
+    if pos.ndim == 2:
+        pos = pos[None]
+    pos, pp = _d(pos)
+    T, N = pos.shape[0], pos.shape[1]
+    q, qp = _d(q)
+    n_q = q.shape[0]
+    sp, spp, fq, fqp = _species_args(species, fq, n_q)
+    out = np.zeros((T, n_q, 2) if amp else (T, n_q))
+    lib().oracle_species(pp, N, spp, fqp, qp, n_q, T, float(L), 1 if amp else 0,
+                         out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    return out[..., 0] + 1j * out[..., 1] if amp else out
+
+
+def pair_sum_species(pos, species, fq, q, L):
+    """Eq.(2) with f_i(q): the O(N^2) pair sum (tiny N only)."""
+    pos, pp = _d(pos)
+    N = pos.shape[0]
+    q, qp = _d(q)
+    n_q = q.shape[0]
+    sp, spp, fq, fqp = _species_args(species, fq, n_q)
+    out = np.zeros(n_q)
+    lib().oracle_pair_sum_species(pp, N, spp, fqp, qp, n_q, float(L), out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
     return out
 
 

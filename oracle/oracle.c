@@ -99,3 +99,56 @@ int oracle_max_threads(void) {
     return 1;
 #endif
 }
+
+/* Eq.(2) with q-dependent form factors f_i(q) via the single sum of Eq.(7):
+ *     p(q,t) = sum_j f_{s(j)}(q) exp(-i q . r_j(t)),   I(q,t) = |p|^2,
+ * for atoms of n_species kinds: species[j] in [0, n_species), fq [n_species][n_q] the form factor of each
+ * kind at each q (the paper parameterises f by a sum of Gaussians; the table is an input).
+ * pos [T][N][3]; amp != 0 writes (re, im) pairs to out [T][n_q][2], else I to out [T][n_q]. */
+void oracle_species(const double* pos, int64_t N, const int32_t* species, const double* fq, const double* q,
+                    int64_t n_q, int64_t T, double L, int amp, double* out) {
+    for (int64_t t = 0; t < T; ++t) {
+        const double* p = pos + (size_t)t * (size_t)N * 3;
+#pragma omp parallel for schedule(dynamic, 16)
+        for (int64_t iq = 0; iq < n_q; ++iq) {
+            const double qx = q[3 * iq + 0], qy = q[3 * iq + 1], qz = q[3 * iq + 2];
+            double re = 0.0, im = 0.0;
+            for (int64_t j = 0; j < N; ++j) {
+                const double x = wrap(p[3 * j + 0], L);
+                const double y = wrap(p[3 * j + 1], L);
+                const double z = wrap(p[3 * j + 2], L);
+                const double phase = qx * x + qy * y + qz * z;
+                const double fj = fq[(size_t)species[j] * (size_t)n_q + iq];
+                re += fj * cos(phase);
+                im -= fj * sin(phase);
+            }
+            if (amp) {
+                out[2 * ((size_t)t * (size_t)n_q + iq) + 0] = re;
+                out[2 * ((size_t)t * (size_t)n_q + iq) + 1] = im;
+            } else {
+                out[(size_t)t * (size_t)n_q + iq] = re * re + im * im;
+            }
+        }
+    }
+}
+
+/* Eq.(2) itself with q-dependent form factors: the O(N^2) pair sum sum_i sum_j f_i(q) f_j(q) cos(q . (r_i - r_j))
+ * (tiny N only; brute-force pin of oracle_species). */
+void oracle_pair_sum_species(const double* pos, int64_t N, const int32_t* species, const double* fq,
+                             const double* q, int64_t n_q, double L, double* I_out) {
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t iq = 0; iq < n_q; ++iq) {
+        const double qx = q[3 * iq + 0], qy = q[3 * iq + 1], qz = q[3 * iq + 2];
+        double s = 0.0;
+        for (int64_t i = 0; i < N; ++i) {
+            const double xi = wrap(pos[3 * i + 0], L), yi = wrap(pos[3 * i + 1], L), zi = wrap(pos[3 * i + 2], L);
+            const double fi = fq[(size_t)species[i] * (size_t)n_q + iq];
+            for (int64_t j = 0; j < N; ++j) {
+                const double xj = wrap(pos[3 * j + 0], L), yj = wrap(pos[3 * j + 1], L), zj = wrap(pos[3 * j + 2], L);
+                const double fj = fq[(size_t)species[j] * (size_t)n_q + iq];
+                s += fi * fj * cos(qx * (xi - xj) + qy * (yi - yj) + qz * (zi - zj));
+            }
+        }
+        I_out[iq] = s;
+    }
+}

@@ -369,3 +369,85 @@ def test_isf_brownian_and_siegert():
             sieg = beta0 * phi ** 2
             z = (num.mean() - sieg.mean()) / (num.std() / np.sqrt(sel.sum() / 2))
             assert abs(z) < 5, (tau, b, z)
+
+
+# ------------------------------------------------------------------ q-dependent form factors, 3-D q blocks
+def _two_species_fq(q, n_species=2):
+    """Synthetic Gaussian-sum form factors (PAPER.md:94-95 form; the coefficients are made up, not tabulated data)."""
+    coef = [([2.0, 1.0], [3.0, 20.0], 0.5), ([0.8, 0.3], [1.5, 9.0], 0.1), ([1.2], [6.0], 0.0)]
+    return np.stack([oracle.form_factor_gaussian(q, *coef[s]) for s in range(n_species)])
+
+
+@pytest.mark.parametrize("N,S", [(7, 2), (40, 3)])
+def test_species_direct_equals_pair_sum(N, S):
+    """Eq.(2) with f_i(q) f_j(q) as an O(N^2) pair sum == the single-sum species oracle."""
+    L = 5.5
+    rng = np.random.default_rng(100 + N)
+    pos = rng.uniform(0, L, (N, 3))
+    sp = rng.integers(0, S, N)
+    q = np.concatenate([oracle.lattice_q(L, -3, 7, -3, 7, m0=(l, 0, 0), ma=(0, 1, 0), mb=(0, 0, 1))
+                        for l in range(-2, 3)])
+    fq = _two_species_fq(q, S)
+    a = oracle.species_intensity(pos, sp, fq, q, L)[0]
+    b = oracle.pair_sum_species(pos, sp, fq, q, L)
+    np.testing.assert_allclose(a, b, rtol=1e-10, atol=1e-10 * np.max(np.abs(b)))
+
+
+def test_species_two_atoms_closed_form_and_constant_limit():
+    """Two atoms of different kinds: I = fa(q)^2 + fb(q)^2 + 2 fa fb cos(q . (ra - rb)); q-independent tables reduce
+    to the per-atom-f direct method (oracle.intensity, a separate routine)."""
+    L = 7.0
+    pos = np.array([[0.3, 1.9, 4.4], [5.1, 6.2, 0.7]])
+    q = oracle.lattice_q(L, -4, 9, -4, 9, m0=(1, 0, 0), ma=(0, 1, 0), mb=(0, 0, 1))
+    fq = _two_species_fq(q)
+    I = oracle.species_intensity(pos, [0, 1], fq, q, L)[0]
+    expect = fq[0] ** 2 + fq[1] ** 2 + 2 * fq[0] * fq[1] * np.cos(q @ (pos[0] - pos[1]))
+    np.testing.assert_allclose(I, expect, rtol=1e-12, atol=1e-12)
+    A = oracle.species_intensity(pos, [0, 1], fq, q, L, amp=True)[0]
+    np.testing.assert_allclose(A, fq[0] * np.exp(-1j * (q @ pos[0])) + fq[1] * np.exp(-1j * (q @ pos[1])), atol=1e-12)
+    rng = np.random.default_rng(3)
+    pos = rng.uniform(0, L, (200, 3))
+    sp = rng.integers(0, 3, 200)
+    c = np.array([1.0, 2.5, 0.75])
+    fq_const = np.repeat(c[:, None], q.shape[0], 1)
+    np.testing.assert_allclose(oracle.species_intensity(pos, sp, fq_const, q, L)[0],
+                               oracle.intensity(pos, c[sp], q, L)[0], rtol=1e-11, atol=1e-9)
+
+
+def test_form_factor_is_fourier_transform_of_gaussian_density():
+    """f(q) is the Fourier transform of the atom's electron density.  A density that is a sum of
+    isotropic Gaussians n_i N(0, s_i^2 I) plus a point charge c has, by radial quadrature of
+    f(q) = int 4 pi r^2 rho(r) sin(qr)/(qr) dr, the Gaussian-sum form c + sum a_i exp(-b_i (q/4pi)^2) with
+    a_i = n_i and b_i = 8 pi^2 s_i^2."""
+    from scipy.integrate import quad
+    n_i, s_i, c = [2.0, 1.0], [0.2, 0.5], 0.5
+    a = n_i
+    b = [8 * np.pi ** 2 * s * s for s in s_i]
+    for qm in [0.0, 0.7, 2.0, 5.5, 11.0]:
+        def integrand(r):
+            rho = sum(n * np.exp(-r * r / (2 * s * s)) / (2 * np.pi * s * s) ** 1.5 for n, s in zip(n_i, s_i))
+            k = 1.0 if qm == 0 else np.sin(qm * r) / (qm * r)
+            return 4 * np.pi * r * r * rho * k
+        f_num = quad(integrand, 0, 10, limit=400, epsabs=1e-13)[0] + c
+        f_or = oracle.form_factor_gaussian(np.array([[0.0, 0.0, qm]]), a, b, c)[0]
+        assert abs(f_num - f_or) < 1e-9, (qm, f_num, f_or)
+
+
+def test_volume_bragg_peaks_and_table1_grid():
+    """3-D reciprocal-lattice block (Algorithm 1 step 1; Table 1's 81^3 grid): an SC
+    crystal of n^3 atoms has I = N^2 exactly at h, k, l in n Z and 0 elsewhere -- pins the (l, h, k) index order.
+    The Table 1 grid of the L = 59.19 A box has 531441 q with |q_c| <= 40 (2 pi / L)."""
+    n_c, L = 4, 6.0
+    pos = xi.crystal("sc", n_c, L)
+    N = pos.shape[0]
+    q = oracle.lattice_volume_q(L, -5, 11, -6, 12, -4, 9)
+    I = oracle.intensity(pos, None, q, L)[0].reshape(9, 11, 12)
+    l, h, k = np.meshgrid(np.arange(-4, 5), np.arange(-5, 6), np.arange(-6, 6), indexing="ij")
+    peak = (h % n_c == 0) & (k % n_c == 0) & (l % n_c == 0)
+    np.testing.assert_allclose(I[peak], float(N) ** 2, rtol=1e-12)
+    assert np.max(I[~peak]) < 1e-8 * N
+    g = _gold("paper_parameters.json")
+    Lp = g["box_L_angstrom"]["value"]
+    qt = oracle.lattice_volume_q(Lp, -40, 81, -40, 81, -40, 81)
+    assert qt.shape == (81 ** 3, 3)
+    np.testing.assert_allclose(np.abs(qt).max(0), 40 * 2 * np.pi / Lp, rtol=1e-15)
