@@ -108,6 +108,65 @@ XPCS_API int xpcs_amplitude(const void* positions, int64_t N, const void* form_f
 XPCS_API int xpcs_amplitude_grid(const void* positions, int64_t N, const void* form_factors,
                         const xpcs_qgrid* grid, int64_t frames, void* A_out, const xpcs_opts* opts);
 
+/* ------------------------------------------------------------------------------------------------
+ * 3-D blocks of the reciprocal lattice and q-dependent atomic form factors.
+ *
+ * xpcs_qvolume: n_l stacked lattice planes (Algorithm 1 step 1; the 81 x 81 x 81 grid of Table 1,
+ * PAPER.md:459): plane il (0 <= il < n_l) is `plane` with m0 replaced by m0 + (l0 + il) mc, i.e.
+ *     q = (2 pi / L) (m0 + h ma + k mb + l mc),   l = l0 + il,
+ * output index (il * n_h + ih) * n_k + ik.  A plane is the n_l = 1 case. */
+typedef struct {
+    xpcs_qgrid plane;
+    int32_t mc[3];
+    int32_t pad_;
+    int64_t l0, n_l;
+} xpcs_qvolume;
+
+/* Atom kinds with q-dependent form factors (Eq.(2): f_i(q); f is the Fourier
+ * transform of the atom's electron density, e.g. a sum of Gaussians, see xpcs_form_factor_gaussian):
+ *     p(q,t) = sum_j f_{species[j]}(q) exp(-i q . r_j(t)).
+ *   n_species  1 .. 16
+ *   species    HOST [N] int32, each in [0, n_species): atoms are gathered per kind on the device (the permutation is
+ *              built on the host and uploaded once per call; the array may be freed when the call returns)
+ *   f_q        DEVICE [n_species][n_q_total] in_dtype: f_s at every output q (n_q_total = n_q for a q list,
+ *              n_l * n_h * n_k for a volume, same q order as the output) */
+typedef struct {
+    int32_t n_species;
+    int32_t pad_;
+    const int32_t* species;
+    const void* f_q;
+} xpcs_species;
+
+/* xpcs_intensity_volume / xpcs_amplitude_volume: I (or p, as (re, im) pairs) on a 3-D lattice block for every
+ * frame, by the same exact-turn factorised engines as xpcs_intensity_grid (each (frame, l-plane) pair is one
+ * plane contraction).  species == NULL: per-atom q-independent form_factors [N] (NULL => 1) as in
+ * xpcs_intensity_grid; species != NULL: q-dependent f_s(q) (form_factors must then be NULL).
+ *   I_out [frames][n_l][n_h][n_k] out_dtype (amplitude: [..][2]).
+ * Errors: as xpcs_intensity_grid, plus EINVAL for vol NULL, n_l <= 0, |l| too large, form_factors together with
+ *         species, n_species outside [1, 16], a species index out of range, f_q NULL. */
+XPCS_API int xpcs_intensity_volume(const void* positions, int64_t N, const void* form_factors,
+                                   const xpcs_species* species, const xpcs_qvolume* vol, int64_t frames,
+                                   void* I_out, const xpcs_opts* opts);
+XPCS_API int xpcs_amplitude_volume(const void* positions, int64_t N, const void* form_factors,
+                                   const xpcs_species* species, const xpcs_qvolume* vol, int64_t frames,
+                                   void* A_out, const xpcs_opts* opts);
+/* xpcs_intensity_species / xpcs_amplitude_species: explicit q list (as xpcs_intensity) with q-dependent
+ * form factors; species must not be NULL.  Errors: as xpcs_intensity plus the species errors above. */
+XPCS_API int xpcs_intensity_species(const void* positions, int64_t N, const xpcs_species* species,
+                                    const void* q_vectors, int64_t n_q, int64_t frames, double box_L,
+                                    void* I_out, const xpcs_opts* opts);
+XPCS_API int xpcs_amplitude_species(const void* positions, int64_t N, const xpcs_species* species,
+                                    const void* q_vectors, int64_t n_q, int64_t frames, double box_L,
+                                    void* A_out, const xpcs_opts* opts);
+/* Gaussian-sum form factor: f(q) = c + sum_{i < n_gauss} a_i exp(-b_i s^2), s = |q| / (4 pi),
+ * evaluated in FP64 at an explicit q list (q_vectors DEVICE [n_q][3] in_dtype) or, if q_vectors is NULL, at every
+ * q of the volume *vol (n_q ignored).  a, b HOST [n_gauss], 0 <= n_gauss <= 6.  f_out DEVICE [n_q] out_dtype.
+ * Errors: EINVAL for f_out NULL, both q_vectors and vol NULL, n_q <= 0 with a q list, n_gauss outside [0, 6],
+ *         a/b NULL with n_gauss > 0. */
+XPCS_API int xpcs_form_factor_gaussian(const void* q_vectors, int64_t n_q, const xpcs_qvolume* vol, int32_t n_gauss,
+                                       const double* a, const double* b, double c, void* f_out,
+                                       const xpcs_opts* opts);
+
 /* Intermediate scattering function, Eq.(22), PAPER.md:218-223:
  *   F(q, tau) = (1 / (T - tau)) sum_{t=0}^{T-1-tau} p(q,t) p*(q, t+tau)  /  sum_j f_j^2
  * (time average over the T - tau available pairs; sum_j f_j^2 reduced on the device from form_factors, NULL => N).

@@ -25,6 +25,8 @@ EXPORTED = (
     "xpcs_radial_bins", "xpcs_last_error", "xpcs_release", "xpcs_launch_count", "xpcs_profile_reset",
     "xpcs_profile_query", "xpcs_device_info", "xpcs_version", "xpcs_engine_available",
     "xpcs_amplitude", "xpcs_amplitude_grid", "xpcs_isf",
+    "xpcs_intensity_volume", "xpcs_amplitude_volume", "xpcs_intensity_species", "xpcs_amplitude_species",
+    "xpcs_form_factor_gaussian",
 )
 
 
@@ -47,6 +49,20 @@ class QGrid(ctypes.Structure):
     @property
     def n_q(self):
         return int(self.n_h * self.n_k)
+
+
+class QVolume(ctypes.Structure):
+    _fields_ = [("plane", QGrid), ("mc", ctypes.c_int32 * 3), ("pad_", ctypes.c_int32), ("l0", ctypes.c_int64),
+                ("n_l", ctypes.c_int64)]
+
+    @property
+    def n_q(self):
+        return int(self.plane.n_h * self.plane.n_k * self.n_l)
+
+
+class Species(ctypes.Structure):
+    _fields_ = [("n_species", ctypes.c_int32), ("pad_", ctypes.c_int32), ("species", ctypes.POINTER(ctypes.c_int32)),
+                ("f_q", ctypes.c_void_p)]
 
 
 _lib = None
@@ -87,6 +103,12 @@ def load():
         "xpcs_amplitude": [vp, i64, vp, vp, i64, i64, dbl, vp, op],
         "xpcs_amplitude_grid": [vp, i64, vp, gp, i64, vp, op],
         "xpcs_isf": [vp, i64, i64, ip32, i64, vp, i64, vp, op],
+        "xpcs_intensity_volume": [vp, i64, vp, ctypes.POINTER(Species), ctypes.POINTER(QVolume), i64, vp, op],
+        "xpcs_amplitude_volume": [vp, i64, vp, ctypes.POINTER(Species), ctypes.POINTER(QVolume), i64, vp, op],
+        "xpcs_intensity_species": [vp, i64, ctypes.POINTER(Species), vp, i64, i64, dbl, vp, op],
+        "xpcs_amplitude_species": [vp, i64, ctypes.POINTER(Species), vp, i64, i64, dbl, vp, op],
+        "xpcs_form_factor_gaussian": [vp, i64, ctypes.POINTER(QVolume), i32, ctypes.POINTER(ctypes.c_double),
+                                      ctypes.POINTER(ctypes.c_double), dbl, vp, op],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -150,6 +172,87 @@ def qgrid(L, h0, n_h, k0, n_k, m0=(0, 0, 0), ma=(1, 0, 0), mb=(0, 1, 0)) -> QGri
     g.m0[:], g.ma[:], g.mb[:] = list(m0), list(ma), list(mb)
     g.h0, g.n_h, g.k0, g.n_k = int(h0), int(n_h), int(k0), int(n_k)
     return g
+
+
+def qvolume(L, h0, n_h, k0, n_k, l0, n_l, m0=(0, 0, 0), ma=(1, 0, 0), mb=(0, 1, 0), mc=(0, 0, 1)) -> QVolume:
+    """3-D reciprocal-lattice block q = (2 pi / L)(m0 + h ma + k mb + l mc), output order (l, h, k)."""
+    v = QVolume()
+    v.plane = qgrid(L, h0, n_h, k0, n_k, m0, ma, mb)
+    v.mc[:] = list(mc)
+    v.l0, v.n_l = int(l0), int(n_l)
+    return v
+
+
+def species_desc(species, f_q):
+    """xpcs_species from a host int array species [N] and a device table f_q [n_species][n_q] (kept alive by the
+    returned tuple's second element)."""
+    sp = np.ascontiguousarray(np.asarray(species, dtype=np.int32))
+    d = Species()
+    d.n_species = int(f_q.shape[0])
+    d.species = sp.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+    d.f_q = _ptr(f_q)
+    return d, (sp, f_q)
+
+
+def _positions3(positions):
+    return positions.unsqueeze(0) if positions.dim() == 2 else positions
+
+
+def xpcs_intensity_volume(positions, form_factors, vol: QVolume, species=None, f_q=None, out=None, out_dtype=None,
+                          engine=ENGINE_AUTO, stream=None, profile=False, amplitude=False):
+    """Eq.(7)-(8) on a 3-D lattice block (species/f_q: q-dependent form factors) -> I [T][n_l * n_h * n_k]
+    (amplitude=True: p as [..][2])."""
+    import torch
+    positions = _positions3(positions)
+    T, N = positions.shape[0], positions.shape[1]
+    ind = _dtype_code(positions)
+    outd = ind if out_dtype is None else out_dtype
+    shape = (T, vol.n_q, 2) if amplitude else (T, vol.n_q)
+    if out is None:
+        out = torch.empty(shape, dtype=torch.float64 if outd == F64 else torch.float32, device=positions.device)
+    o = make_opts(ind, outd, stream, engine, profile)
+    sp, keep = (species_desc(species, f_q) if species is not None else (None, None))
+    fn = load().xpcs_amplitude_volume if amplitude else load().xpcs_intensity_volume
+    _check(fn(_ptr(positions), N, _ptr(form_factors), ctypes.byref(sp) if sp is not None else None,
+              ctypes.byref(vol), T, _ptr(out), ctypes.byref(o)))
+    del keep
+    return out
+
+
+def xpcs_intensity_species(positions, species, f_q, q_vectors, box_L, out=None, out_dtype=None, stream=None,
+                           profile=False, amplitude=False):
+    """Eq.(7)-(8) at an explicit q list with q-dependent form factors f_q [n_species][n_q] -> I [T][n_q]."""
+    import torch
+    positions = _positions3(positions)
+    T, N = positions.shape[0], positions.shape[1]
+    n_q = q_vectors.shape[0]
+    ind = _dtype_code(positions)
+    outd = ind if out_dtype is None else out_dtype
+    shape = (T, n_q, 2) if amplitude else (T, n_q)
+    if out is None:
+        out = torch.empty(shape, dtype=torch.float64 if outd == F64 else torch.float32, device=positions.device)
+    o = make_opts(ind, outd, stream, ENGINE_AUTO, profile)
+    sp, keep = species_desc(species, f_q)
+    fn = load().xpcs_amplitude_species if amplitude else load().xpcs_intensity_species
+    _check(fn(_ptr(positions), N, ctypes.byref(sp), _ptr(q_vectors), n_q, T, float(box_L), _ptr(out),
+              ctypes.byref(o)))
+    del keep
+    return out
+
+
+def xpcs_form_factor_gaussian(a, b, c, q_vectors=None, vol: QVolume = None, out_dtype=F32, in_dtype=F32,
+                              device="cuda", stream=None):
+    """f(q) = c + sum_i a_i exp(-b_i (|q|/4 pi)^2) at a q list or every q of a volume -> [n_q]."""
+    import torch
+    n_q = q_vectors.shape[0] if q_vectors is not None else vol.n_q
+    out = torch.empty(n_q, dtype=torch.float64 if out_dtype == F64 else torch.float32,
+                      device=q_vectors.device if q_vectors is not None else device)
+    ad = (ctypes.c_double * max(1, len(a)))(*[float(x) for x in a])
+    bd = (ctypes.c_double * max(1, len(b)))(*[float(x) for x in b])
+    o = make_opts(_dtype_code(q_vectors) if q_vectors is not None else in_dtype, out_dtype, stream)
+    _check(load().xpcs_form_factor_gaussian(_ptr(q_vectors), n_q, ctypes.byref(vol) if vol is not None else None,
+                                            len(a), ad, bd, float(c), _ptr(out), ctypes.byref(o)))
+    return out
 
 
 def xpcs_intensity(positions, form_factors, q_vectors, box_L, out=None, out_dtype=None, stream=None, profile=False):

@@ -181,9 +181,85 @@ int xpcs_engine_available(int32_t engine) {
 }  // extern "C"
 
 // ------------------------------------------------------------------------------------------- intensity
+// Atom groups of one call: without species one group (all atoms, identity map); with species one group per kind,
+// gathered through a device permutation built here (stable partition of the HOST species array).
+struct Groups {
+    int n_species = 0;                       // 0: no species
+    std::vector<int64_t> off, cnt;           // per group: offset into the permutation, atom count
+    const int32_t* d_idx = nullptr;          // device permutation (species only)
+    std::vector<int32_t> perm;               // host permutation (stable partition by kind)
+    const void* fq = nullptr;
+    int count() const { return (int)cnt.size(); }
+    const int32_t* idx(int g) const { return d_idx ? d_idx + off[g] : nullptr; }
+};
+
+// host-side validation and permutation (no device work: runs before any launch, EINVAL launches nothing)
+static int prep_groups(const xpcs_species* sp, const void* form_factors, int64_t N, Groups& G) {
+    if (!sp) {
+        G.off.assign(1, 0);
+        G.cnt.assign(1, N);
+        return XPCS_OK;
+    }
+    if (form_factors) {
+        set_error("xpcs: form_factors and species are exclusive (fold per-atom weights into f_q)");
+        return XPCS_EINVAL;
+    }
+    if (sp->n_species < 1 || sp->n_species > kMaxSpecies) {
+        set_error("xpcs: n_species must be in [1, %d] (got %d)", kMaxSpecies, sp->n_species);
+        return XPCS_EINVAL;
+    }
+    NEED(sp->species, "species->species");
+    NEED(sp->f_q, "species->f_q");
+    if (N > (int64_t(1) << 31) - 1) {
+        set_error("xpcs: species gather supports N < 2^31");
+        return XPCS_EINVAL;
+    }
+    const int S = sp->n_species;
+    G.n_species = S;
+    G.fq = sp->f_q;
+    G.cnt.assign(S, 0);
+    for (int64_t j = 0; j < N; ++j) {
+        const int32_t k = sp->species[j];
+        if (k < 0 || k >= S) {
+            set_error("xpcs: species[%lld] = %d outside [0, %d)", (long long)j, k, S);
+            return XPCS_EINVAL;
+        }
+        ++G.cnt[k];
+    }
+    G.off.assign(S, 0);
+    for (int k = 1; k < S; ++k) G.off[k] = G.off[k - 1] + G.cnt[k - 1];
+    G.perm.resize((size_t)N);
+    std::vector<int64_t> fill(G.off);
+    for (int64_t j = 0; j < N; ++j) G.perm[(size_t)fill[sp->species[j]]++] = (int32_t)j;
+    return XPCS_OK;
+}
+
+static int upload_groups(Groups& G, cudaStream_t s) {
+    if (!G.n_species) return XPCS_OK;
+    const size_t bytes = sizeof(int32_t) * G.perm.size();
+    int32_t* d = (int32_t*)scratch(s, SS_IDX, bytes);
+    if (!d) return XPCS_ENOMEM;
+    // pageable source: the copy is staged before cudaMemcpyAsync returns, so `perm` may be freed afterwards
+    TRY(cuda_fail(cudaMemcpyAsync(d, G.perm.data(), bytes, cudaMemcpyHostToDevice, s), "species upload"));
+    G.d_idx = d;
+    return XPCS_OK;
+}
+
+static StageMap stage_map(const Groups& G, int g, int64_t N, int64_t v0, int64_t n_l, int64_t l0, const int32_t* mc) {
+    StageMap m;
+    m.idx = G.idx(g);
+    m.n_src = N;
+    m.v0 = v0;
+    m.n_l = n_l;
+    m.l0 = l0;
+    for (int c = 0; c < 3; ++c) m.mc[c] = mc ? mc[c] : 0;
+    return m;
+}
+
 // amp = 0: I(q,t) = |p|^2 (Eq. 8) -> out [frames][n_q];  amp = 1: p(q,t) (Eq. 7) -> out [frames][n_q][2]
-static int run_direct(const void* positions, int64_t N, const void* form_factors, const void* q_vectors, int64_t n_q,
-                      int64_t frames, double box_L, void* I_out, const xpcs_opts* opts, int amp) {
+static int run_direct(const void* positions, int64_t N, const void* form_factors, const xpcs_species* species,
+                      const void* q_vectors, int64_t n_q, int64_t frames, double box_L, void* I_out,
+                      const xpcs_opts* opts, int amp) {
     clear_error();
     Opts o;
     TRY(parse_opts(opts, o));
@@ -201,51 +277,111 @@ static int run_direct(const void* positions, int64_t N, const void* form_factors
         set_error("xpcs: N or n_q too large");
         return XPCS_EINVAL;
     }
+    Groups G;
+    TRY(prep_groups(species, form_factors, N, G));
     TRY(check_sticky());
+    TRY(upload_groups(G, o.s));
     const size_t isz = out_size(o.out_f64) * (amp ? 2 : 1);
-    const size_t psz = o.in_f64 ? 24 : 12;
+    const int ng = G.count();
+    SpeciesParts sp{};
+    sp.n = G.n_species;
+    sp.part_f64 = 1;
     if (o.in_f64) {
-        const int64_t Tb = std::max<int64_t>(1, std::min<int64_t>(frames, (int64_t)(kBatchBytes / std::max<int64_t>(1, std::max<int64_t>(32 * N, 16 * n_q)))));
+        const int64_t per_frame = std::max<int64_t>(32 * N, 16 * n_q * ng);
+        const int64_t Tb = std::max<int64_t>(1, std::min<int64_t>(frames, (int64_t)(kBatchBytes / std::max<int64_t>(1, per_frame))));
         ulonglong4* st = (ulonglong4*)scratch(o.s, SS_STAGE, sizeof(ulonglong4) * (size_t)(N * Tb));
-        double2* part = (double2*)scratch(o.s, SS_PARTIAL, sizeof(double2) * (size_t)(n_q * Tb));
+        double2* part = (double2*)scratch(o.s, SS_PARTIAL, sizeof(double2) * (size_t)(n_q * Tb * ng));
         if (!st || !part) return XPCS_ENOMEM;
         for (int64_t t0 = 0; t0 < frames; t0 += Tb) {
             const int64_t tb = std::min(Tb, frames - t0);
-            { ProfScope p(o.profile, KC_STAGE, o.s);
-              TRY(cuda_fail(launch_stage_generic64((const char*)positions + psz * N * t0, form_factors, N, tb, box_L, st, o.s), "stage")); }
-            { ProfScope p(o.profile, KC_MAIN, o.s);
-              TRY(cuda_fail(launch_generic64(st, N, tb, q_vectors, n_q, box_L, part, o.s), "generic64")); }
-            { ProfScope p(o.profile, KC_REDUCE, o.s);
-              TRY(cuda_fail(launch_amp_reduce_d(part, 1, tb, n_q, (char*)I_out + isz * n_q * t0, o.out_f64, amp, o.s), "reduce")); }
+            int64_t stoff = 0;
+            for (int g = 0; g < ng; ++g) {
+                const int64_t Ng = G.cnt[g];
+                double2* pg = part + (size_t)g * (size_t)(n_q * tb);
+                sp.part[g] = pg;
+                sp.C[g] = Ng > 0 ? 1 : 0;
+                if (Ng == 0) continue;
+                const StageMap m = stage_map(G, g, N, t0, 1, 0, nullptr);
+                { ProfScope p(o.profile, KC_STAGE, o.s);
+                  TRY(cuda_fail(launch_stage_generic64(positions, form_factors, Ng, tb, box_L, m, st + stoff, o.s), "stage")); }
+                { ProfScope p(o.profile, KC_MAIN, o.s);
+                  TRY(cuda_fail(launch_generic64(st + stoff, Ng, tb, q_vectors, n_q, box_L, pg, o.s), "generic64")); }
+                stoff += Ng * tb;
+            }
+            void* dst = (char*)I_out + isz * n_q * t0;
+            ProfScope p(o.profile, KC_REDUCE, o.s);
+            if (G.n_species) TRY(cuda_fail(launch_species_combine(sp, tb, n_q, G.fq, 1, t0, 1, dst, o.out_f64, amp, o.s), "species combine"));
+            else TRY(cuda_fail(launch_amp_reduce_d(part, 1, tb, n_q, dst, o.out_f64, amp, o.s), "reduce"));
         }
         return XPCS_OK;
     }
     // fp32: split atoms only when (q tiles x frames) cannot fill the device
     const int64_t qtiles = (n_q + 1023) / 1024;
-    int64_t C = 1;
-    const int64_t want = 2LL * sm_count();
-    if (qtiles * frames < want) C = std::min<int64_t>((want + qtiles * frames - 1) / (qtiles * frames), (N + 511) / 512);
-    int64_t chunk = (N + C - 1) / C;
-    chunk = ((chunk + 511) / 512) * 512;
-    C = (N + chunk - 1) / chunk;
-    const int64_t Tb = std::max<int64_t>(1, std::min<int64_t>(frames, (int64_t)(kBatchBytes / std::max<int64_t>(32 * N, 16 * C * n_q))));
+    std::vector<int64_t> chunk(ng, 512), C(ng, 0);
+    int64_t sumC = 0;
+    for (int g = 0; g < ng; ++g) {
+        const int64_t Ng = G.cnt[g];
+        if (Ng == 0) continue;
+        int64_t c = 1;
+        const int64_t want = 2LL * sm_count();
+        if (qtiles * frames < want) c = std::min<int64_t>((want + qtiles * frames - 1) / (qtiles * frames), (Ng + 511) / 512);
+        int64_t ch = (Ng + c - 1) / c;
+        ch = ((ch + 511) / 512) * 512;
+        chunk[g] = ch;
+        C[g] = (Ng + ch - 1) / ch;
+        sumC += C[g];
+    }
+    const int64_t Tb = std::max<int64_t>(1, std::min<int64_t>(frames, (int64_t)(kBatchBytes / std::max<int64_t>(32 * N, 16 * sumC * n_q))));
     uint4* st = (uint4*)scratch(o.s, SS_STAGE, 2 * sizeof(uint4) * (size_t)(N * Tb));   // 32 B / atom
-    double2* part = (double2*)scratch(o.s, SS_PARTIAL, sizeof(double2) * (size_t)(C * n_q * Tb));
+    double2* part = (double2*)scratch(o.s, SS_PARTIAL, sizeof(double2) * (size_t)(sumC * n_q * Tb));
     if (!st || !part) return XPCS_ENOMEM;
     for (int64_t t0 = 0; t0 < frames; t0 += Tb) {
         const int64_t tb = std::min(Tb, frames - t0);
-        { ProfScope p(o.profile, KC_STAGE, o.s);
-          TRY(cuda_fail(launch_stage_generic32((const char*)positions + psz * N * t0, 0, form_factors, 0, N, tb, box_L, st, o.s), "stage")); }
-        { ProfScope p(o.profile, KC_MAIN, o.s);
-          TRY(cuda_fail(launch_generic32(st, N, tb, q_vectors, 0, n_q, box_L, chunk, C, part, o.s), "generic32")); }
-        { ProfScope p(o.profile, KC_REDUCE, o.s);
-          TRY(cuda_fail(launch_amp_reduce_d(part, C, tb, n_q, (char*)I_out + isz * n_q * t0, o.out_f64, amp, o.s), "reduce")); }
+        int64_t stoff = 0, poff = 0;
+        for (int g = 0; g < ng; ++g) {
+            const int64_t Ng = G.cnt[g];
+            sp.part[g] = part + poff;
+            sp.C[g] = C[g];
+            if (Ng == 0) continue;
+            const StageMap m = stage_map(G, g, N, t0, 1, 0, nullptr);
+            { ProfScope p(o.profile, KC_STAGE, o.s);
+              TRY(cuda_fail(launch_stage_generic32(positions, 0, form_factors, 0, Ng, tb, box_L, m, st + 2 * stoff, o.s), "stage")); }
+            { ProfScope p(o.profile, KC_MAIN, o.s);
+              TRY(cuda_fail(launch_generic32(st + 2 * stoff, Ng, tb, q_vectors, 0, n_q, box_L, chunk[g], C[g], part + poff, o.s), "generic32")); }
+            stoff += Ng * tb;
+            poff += C[g] * n_q * tb;
+        }
+        void* dst = (char*)I_out + isz * n_q * t0;
+        ProfScope p(o.profile, KC_REDUCE, o.s);
+        if (G.n_species) TRY(cuda_fail(launch_species_combine(sp, tb, n_q, G.fq, 0, t0, 1, dst, o.out_f64, amp, o.s), "species combine"));
+        else TRY(cuda_fail(launch_amp_reduce_d(part, C[0], tb, n_q, dst, o.out_f64, amp, o.s), "reduce"));
     }
     return XPCS_OK;
 }
 
-static int run_grid(const void* positions, int64_t N, const void* form_factors, const xpcs_qgrid* grid,
-                    int64_t frames, void* I_out, const xpcs_opts* opts, int amp) {
+static int validate_volume(const xpcs_qvolume* vol) {
+    NEED(vol, "vol");
+    TRY(validate_grid(&vol->plane));
+    POS(vol->n_l, "vol->n_l");
+    const int64_t lim = int64_t(1) << 30;
+    if (std::llabs(vol->l0) > lim || vol->n_l > lim) {
+        set_error("xpcs: vol->l0 / n_l out of range");
+        return XPCS_EINVAL;
+    }
+    for (int c = 0; c < 3; ++c) {
+        for (const int64_t l : {vol->l0, vol->l0 + vol->n_l - 1}) {
+            const int64_t m = (int64_t)vol->plane.m0[c] + l * (int64_t)vol->mc[c];
+            if (std::llabs(m) > lim) {
+                set_error("xpcs: m0 + l mc out of range for 32-bit turns");
+                return XPCS_EINVAL;
+            }
+        }
+    }
+    return XPCS_OK;
+}
+
+static int run_volume(const void* positions, int64_t N, const void* form_factors, const xpcs_species* species,
+                      const xpcs_qvolume* vol, int64_t frames, void* I_out, const xpcs_opts* opts, int amp) {
     clear_error();
     Opts o;
     TRY(parse_opts(opts, o));
@@ -253,85 +389,201 @@ static int run_grid(const void* positions, int64_t N, const void* form_factors, 
     NEED(I_out, "I_out");
     POS(N, "N");
     POS(frames, "frames");
-    TRY(validate_grid(grid));
+    TRY(validate_volume(vol));
+    if (frames > (int64_t(1) << 40) / vol->n_l) {
+        set_error("xpcs: frames x n_l too large");
+        return XPCS_EINVAL;
+    }
+    Groups G;
+    TRY(prep_groups(species, form_factors, N, G));
     TRY(check_sticky());
-    const LatticeGeom g = to_geom(*grid);
+    const LatticeGeom g = to_geom(vol->plane);
     const int64_t n_q = g.n_h * g.n_k;
+    const int64_t n_l = vol->n_l, l0 = vol->l0;
+    const int64_t V = frames * n_l;             // virtual frames: (frame, l-plane), row-major = output order
     const size_t isz = out_size(o.out_f64) * (amp ? 2 : 1);
-    if (o.in_f64) {
-        if (o.engine == XPCS_ENGINE_TENSOR) {
-            set_error("xpcs: the tensor engine needs f32 inputs");
-            return XPCS_EUNSUPPORTED;
-        }
-        const int64_t Tb = std::max<int64_t>(1, std::min<int64_t>(frames, (int64_t)(kBatchBytes / (32 * N))));
-        ulonglong4* st = (ulonglong4*)scratch(o.s, SS_STAGE, sizeof(ulonglong4) * (size_t)(N * Tb));
-        if (!st) return XPCS_ENOMEM;
-        for (int64_t t0 = 0; t0 < frames; t0 += Tb) {
-            const int64_t tb = std::min(Tb, frames - t0);
-            { ProfScope p(o.profile, KC_STAGE, o.s);
-              TRY(cuda_fail(launch_stage_lattice64((const char*)positions + 24 * N * t0, form_factors, N, tb, g, st, o.s), "stage")); }
-            { ProfScope p(o.profile, KC_MAIN, o.s);
-              TRY(cuda_fail(launch_lattice_f64(st, N, tb, g, (char*)I_out + isz * n_q * t0, o.out_f64, amp, o.s), "lattice64")); }
-        }
-        return XPCS_OK;
+    if (o.in_f64 && o.engine == XPCS_ENGINE_TENSOR) {
+        set_error("xpcs: the tensor engine needs f32 inputs");
+        return XPCS_EUNSUPPORTED;
     }
     bool tc = false;
-    if (o.engine == XPCS_ENGINE_TENSOR || o.engine == XPCS_ENGINE_AUTO) {
+    if (!o.in_f64 && (o.engine == XPCS_ENGINE_TENSOR || o.engine == XPCS_ENGINE_AUTO)) {
         tc = lattice_tc_supported(g);
         if (!tc && o.engine == XPCS_ENGINE_TENSOR) {
             set_error("xpcs: the tensor engine is not available for this grid/build");
             return XPCS_EUNSUPPORTED;
         }
     }
+    TRY(upload_groups(G, o.s));
+    const int ng = G.count();
+    SpeciesParts sp{};
+    sp.n = G.n_species;
+    if (o.in_f64) {
+        // FP64: direct per-pixel evaluation with 64-bit turns; with species each kind's amplitude goes to scratch
+        sp.part_f64 = 1;
+        const int64_t per_frame = std::max<int64_t>(32 * N, G.n_species ? 16 * n_q * ng : 0);
+        const int64_t Tb = std::max<int64_t>(1, std::min<int64_t>(V, (int64_t)(kBatchBytes / per_frame)));
+        ulonglong4* st = (ulonglong4*)scratch(o.s, SS_STAGE, sizeof(ulonglong4) * (size_t)(N * Tb));
+        double2* part = G.n_species ? (double2*)scratch(o.s, SS_PARTIAL, sizeof(double2) * (size_t)(n_q * Tb * ng)) : nullptr;
+        if (!st || (G.n_species && !part)) return XPCS_ENOMEM;
+        for (int64_t v0 = 0; v0 < V; v0 += Tb) {
+            const int64_t vb = std::min(Tb, V - v0);
+            void* dst = (char*)I_out + isz * n_q * v0;
+            int64_t stoff = 0;
+            for (int gi = 0; gi < ng; ++gi) {
+                const int64_t Ng = G.cnt[gi];
+                double2* pg = part ? part + (size_t)gi * (size_t)(n_q * vb) : nullptr;
+                sp.part[gi] = pg;
+                sp.C[gi] = Ng > 0 ? 1 : 0;
+                if (Ng == 0) continue;
+                const StageMap m = stage_map(G, gi, N, v0, n_l, l0, vol->mc);
+                { ProfScope p(o.profile, KC_STAGE, o.s);
+                  TRY(cuda_fail(launch_stage_lattice64(positions, form_factors, Ng, vb, g, m, st + stoff, o.s), "stage")); }
+                { ProfScope p(o.profile, KC_MAIN, o.s);
+                  if (G.n_species) TRY(cuda_fail(launch_lattice_f64(st + stoff, Ng, vb, g, pg, 1, 1, o.s), "lattice64"));
+                  else TRY(cuda_fail(launch_lattice_f64(st + stoff, Ng, vb, g, dst, o.out_f64, amp, o.s), "lattice64")); }
+                stoff += Ng * vb;
+            }
+            if (G.n_species) {
+                ProfScope p(o.profile, KC_REDUCE, o.s);
+                TRY(cuda_fail(launch_species_combine(sp, vb, n_q, G.fq, 1, v0, n_l, dst, o.out_f64, amp, o.s), "species combine"));
+            }
+        }
+        return XPCS_OK;
+    }
     // atom chunks (split-K over CTAs, folded in FP64 by the reduction): SIMT keeps fp32 register sums short
     // (<= 4096 atoms); the tensor engine drains TMEM every 256 atoms into RN sums, so its chunks only balance
     // the grid (>= ~8 waves of one CTA per SM) and stay >= 1024 atoms.
-    int64_t chunk = 4096;
-    if (tc) {
-        const int64_t tiles = ((g.n_h + 127) / 128) * ((g.n_k + 127) / 128);
-        const int64_t units = tiles * std::min<int64_t>(frames, 64);
-        int64_t C0 = std::max<int64_t>(1, (8LL * sm_count() + units - 1) / units);
-        C0 = std::min<int64_t>(C0, std::max<int64_t>(1, N / 1024));
-        chunk = ((N + C0 - 1) / C0 + 15) / 16 * 16;
+    std::vector<int64_t> chunk(ng, 4096), C(ng, 0);
+    int64_t sumC = 0;
+    for (int gi = 0; gi < ng; ++gi) {
+        const int64_t Ng = G.cnt[gi];
+        if (Ng == 0) continue;
+        int64_t ch = 4096;
+        if (tc) {
+            const int64_t tiles = ((g.n_h + 127) / 128) * ((g.n_k + 127) / 128);
+            const int64_t units = tiles * std::min<int64_t>(V, 64);
+            int64_t C0 = std::max<int64_t>(1, (8LL * sm_count() + units - 1) / units);
+            C0 = std::min<int64_t>(C0, std::max<int64_t>(1, Ng / 1024));
+            ch = ((Ng + C0 - 1) / C0 + 15) / 16 * 16;
+        }
+        if (const char* e = getenv("XPCS_CHUNK_ATOMS")) ch = std::max<int64_t>(16, atoll(e));   // experiments only
+        chunk[gi] = ch;
+        C[gi] = (Ng + ch - 1) / ch;
+        sumC += C[gi];
     }
-    if (const char* e = getenv("XPCS_CHUNK_ATOMS")) chunk = std::max<int64_t>(16, atoll(e));   // experiments only
-    const int64_t C = (N + chunk - 1) / chunk;
-    const int64_t Tb = std::max<int64_t>(1, std::min<int64_t>(frames, (int64_t)(kBatchBytes / std::max<int64_t>(16 * N, 8 * C * n_q))));
+    sp.part_f64 = 0;
+    const int64_t Tb = std::max<int64_t>(1, std::min<int64_t>(V, (int64_t)(kBatchBytes / std::max<int64_t>(16 * N, 8 * sumC * n_q))));
     uint4* st = (uint4*)scratch(o.s, SS_STAGE, sizeof(uint4) * (size_t)(N * Tb));
-    float2* part = (float2*)scratch(o.s, SS_PARTIAL, sizeof(float2) * (size_t)(C * n_q * Tb));
+    float2* part = (float2*)scratch(o.s, SS_PARTIAL, sizeof(float2) * (size_t)(sumC * n_q * Tb));
     if (!st || !part) return XPCS_ENOMEM;
-    for (int64_t t0 = 0; t0 < frames; t0 += Tb) {
-        const int64_t tb = std::min(Tb, frames - t0);
-        { ProfScope p(o.profile, KC_STAGE, o.s);
-          TRY(cuda_fail(launch_stage_lattice32((const char*)positions + 12 * N * t0, 0, form_factors, 0, N, tb, g, st, o.s), "stage")); }
-        { ProfScope p(o.profile, KC_MAIN, o.s);
-          if (tc) TRY(cuda_fail(launch_lattice_tc(st, N, tb, g, chunk, C, part, o.s), "lattice tcgen05"));
-          else TRY(cuda_fail(launch_lattice_simt(st, N, tb, g, chunk, C, part, o.s), "lattice simt")); }
-        { ProfScope p(o.profile, KC_REDUCE, o.s);
-          // the tensor engine's partials hold conj(p) (R1)
-          TRY(cuda_fail(launch_amp_reduce_f(part, C, tb, n_q, (char*)I_out + isz * n_q * t0, o.out_f64,
-                                            amp ? (tc ? 2 : 1) : 0, o.s), "reduce")); }
+    // the tensor engine's partials hold conj(p) (R1)
+    const int mode = amp ? (tc ? 2 : 1) : 0;
+    for (int64_t v0 = 0; v0 < V; v0 += Tb) {
+        const int64_t vb = std::min(Tb, V - v0);
+        int64_t stoff = 0, poff = 0;
+        for (int gi = 0; gi < ng; ++gi) {
+            const int64_t Ng = G.cnt[gi];
+            sp.part[gi] = part + poff;
+            sp.C[gi] = C[gi];
+            if (Ng == 0) continue;
+            const StageMap m = stage_map(G, gi, N, v0, n_l, l0, vol->mc);
+            { ProfScope p(o.profile, KC_STAGE, o.s);
+              TRY(cuda_fail(launch_stage_lattice32(positions, 0, form_factors, 0, Ng, vb, g, m, st + stoff, o.s), "stage")); }
+            { ProfScope p(o.profile, KC_MAIN, o.s);
+              if (tc) TRY(cuda_fail(launch_lattice_tc(st + stoff, Ng, vb, g, chunk[gi], C[gi], part + poff, o.s), "lattice tcgen05"));
+              else TRY(cuda_fail(launch_lattice_simt(st + stoff, Ng, vb, g, chunk[gi], C[gi], part + poff, o.s), "lattice simt")); }
+            stoff += Ng * vb;
+            poff += C[gi] * n_q * vb;
+        }
+        void* dst = (char*)I_out + isz * n_q * v0;
+        ProfScope p(o.profile, KC_REDUCE, o.s);
+        if (G.n_species) TRY(cuda_fail(launch_species_combine(sp, vb, n_q, G.fq, 0, v0, n_l, dst, o.out_f64, mode, o.s), "species combine"));
+        else TRY(cuda_fail(launch_amp_reduce_f(part, C[0], vb, n_q, dst, o.out_f64, mode, o.s), "reduce"));
     }
     return XPCS_OK;
+}
+
+static xpcs_qvolume plane_volume(const xpcs_qgrid* grid) {
+    xpcs_qvolume v;
+    std::memset(&v, 0, sizeof(v));
+    if (grid) v.plane = *grid;
+    v.l0 = 0;
+    v.n_l = 1;
+    return v;
 }
 
 extern "C" {
 
 int xpcs_intensity(const void* positions, int64_t N, const void* form_factors, const void* q_vectors, int64_t n_q,
                    int64_t frames, double box_L, void* I_out, const xpcs_opts* opts) {
-    return run_direct(positions, N, form_factors, q_vectors, n_q, frames, box_L, I_out, opts, 0);
+    return run_direct(positions, N, form_factors, nullptr, q_vectors, n_q, frames, box_L, I_out, opts, 0);
 }
 int xpcs_amplitude(const void* positions, int64_t N, const void* form_factors, const void* q_vectors, int64_t n_q,
                    int64_t frames, double box_L, void* A_out, const xpcs_opts* opts) {
-    return run_direct(positions, N, form_factors, q_vectors, n_q, frames, box_L, A_out, opts, 1);
+    return run_direct(positions, N, form_factors, nullptr, q_vectors, n_q, frames, box_L, A_out, opts, 1);
+}
+int xpcs_intensity_species(const void* positions, int64_t N, const xpcs_species* species, const void* q_vectors,
+                           int64_t n_q, int64_t frames, double box_L, void* I_out, const xpcs_opts* opts) {
+    if (!species) { clear_error(); set_error("xpcs: species must not be NULL"); return XPCS_EINVAL; }
+    return run_direct(positions, N, nullptr, species, q_vectors, n_q, frames, box_L, I_out, opts, 0);
+}
+int xpcs_amplitude_species(const void* positions, int64_t N, const xpcs_species* species, const void* q_vectors,
+                           int64_t n_q, int64_t frames, double box_L, void* A_out, const xpcs_opts* opts) {
+    if (!species) { clear_error(); set_error("xpcs: species must not be NULL"); return XPCS_EINVAL; }
+    return run_direct(positions, N, nullptr, species, q_vectors, n_q, frames, box_L, A_out, opts, 1);
 }
 int xpcs_intensity_grid(const void* positions, int64_t N, const void* form_factors, const xpcs_qgrid* grid,
                         int64_t frames, void* I_out, const xpcs_opts* opts) {
-    return run_grid(positions, N, form_factors, grid, frames, I_out, opts, 0);
+    if (!grid) { clear_error(); set_error("xpcs: grid must not be NULL"); return XPCS_EINVAL; }
+    const xpcs_qvolume v = plane_volume(grid);
+    return run_volume(positions, N, form_factors, nullptr, &v, frames, I_out, opts, 0);
 }
 int xpcs_amplitude_grid(const void* positions, int64_t N, const void* form_factors, const xpcs_qgrid* grid,
                         int64_t frames, void* A_out, const xpcs_opts* opts) {
-    return run_grid(positions, N, form_factors, grid, frames, A_out, opts, 1);
+    if (!grid) { clear_error(); set_error("xpcs: grid must not be NULL"); return XPCS_EINVAL; }
+    const xpcs_qvolume v = plane_volume(grid);
+    return run_volume(positions, N, form_factors, nullptr, &v, frames, A_out, opts, 1);
+}
+int xpcs_intensity_volume(const void* positions, int64_t N, const void* form_factors, const xpcs_species* species,
+                          const xpcs_qvolume* vol, int64_t frames, void* I_out, const xpcs_opts* opts) {
+    return run_volume(positions, N, form_factors, species, vol, frames, I_out, opts, 0);
+}
+int xpcs_amplitude_volume(const void* positions, int64_t N, const void* form_factors, const xpcs_species* species,
+                          const xpcs_qvolume* vol, int64_t frames, void* A_out, const xpcs_opts* opts) {
+    return run_volume(positions, N, form_factors, species, vol, frames, A_out, opts, 1);
+}
+
+int xpcs_form_factor_gaussian(const void* q_vectors, int64_t n_q, const xpcs_qvolume* vol, int32_t n_gauss,
+                              const double* a, const double* b, double c, void* f_out, const xpcs_opts* opts) {
+    clear_error();
+    Opts o;
+    TRY(parse_opts(opts, o));
+    NEED(f_out, "f_out");
+    if (n_gauss < 0 || n_gauss > 6) {
+        set_error("xpcs: n_gauss must be in [0, 6] (got %d)", n_gauss);
+        return XPCS_EINVAL;
+    }
+    if (n_gauss > 0) { NEED(a, "a"); NEED(b, "b"); }
+    LatticeGeom g{};
+    int64_t l0 = 0, n_l = 1;
+    const int32_t* mc = nullptr;
+    if (q_vectors) {
+        POS(n_q, "n_q");
+    } else {
+        if (!vol) {
+            set_error("xpcs: q_vectors and vol must not both be NULL");
+            return XPCS_EINVAL;
+        }
+        TRY(validate_volume(vol));
+        g = to_geom(vol->plane);
+        l0 = vol->l0;
+        n_l = vol->n_l;
+        mc = vol->mc;
+    }
+    TRY(check_sticky());
+    return cuda_fail(launch_form_factor_gaussian(q_vectors, o.in_f64, n_q, g, l0, n_l, mc, n_gauss, a, b, c, f_out,
+                                                 o.out_f64, o.s), "form factor");
 }
 
 int xpcs_isf(const void* A_series, int64_t frames, int64_t n_q, const int32_t* lags, int64_t n_lags,

@@ -16,7 +16,7 @@ void note_launch(int n = 1);
 
 // Scratch cached per (stream, slot); grown on demand (the grow synchronises the device).
 enum ScratchSlot {
-    SS_STAGE = 0, SS_PARTIAL, SS_PLAN, SS_PLAN2, SS_XSVS, SS_SMALL, SS_LAGS, SS_TC, SS_COUNT
+    SS_STAGE = 0, SS_PARTIAL, SS_PLAN, SS_PLAN2, SS_XSVS, SS_SMALL, SS_LAGS, SS_TC, SS_IDX, SS_COUNT
 };
 void* scratch(cudaStream_t s, int slot, size_t bytes);   // nullptr on failure (error already set)
 void release_scratch();
@@ -101,15 +101,41 @@ struct LatticeGeom {
     int64_t h0, n_h, k0, n_k;
 };
 
-// staging: positions [T][N][3] (f32|f64) + f [N] (f32|f64|null) -> per-atom fixed-point turns
+// Which source atoms / frames / lattice planes a staging launch reads (see k_stage.cu).
+struct StageMap {
+    const int32_t* idx;   // device [N staged atoms]: source atom index (species gather); nullptr = identity
+    int64_t n_src;        // atoms per source frame
+    int64_t v0;           // first virtual frame of the batch
+    int64_t n_l, l0;      // virtual frame v = (frame v / n_l, plane l0 + v % n_l); n_l = 1 for a plane / q list
+    int32_t mc[3];        // plane step of a 3-D q block: m0(l) = m0 + l mc
+};
+
+// staging: positions [T][n_src][3] (f32|f64) + f [n_src] (f32|f64|null) -> per-atom fixed-point turns [frames][N]
 cudaError_t launch_stage_lattice32(const void* pos, int pos_f64, const void* f, int f_f64, int64_t N,
-                                   int64_t frames, const LatticeGeom& g, uint4* out, cudaStream_t s);
+                                   int64_t frames, const LatticeGeom& g, const StageMap& m, uint4* out, cudaStream_t s);
 cudaError_t launch_stage_lattice64(const void* pos, const void* f, int64_t N, int64_t frames,
-                                   const LatticeGeom& g, ulonglong4* out, cudaStream_t s);
+                                   const LatticeGeom& g, const StageMap& m, ulonglong4* out, cudaStream_t s);
 cudaError_t launch_stage_generic32(const void* pos, int pos_f64, const void* f, int f_f64, int64_t N,
-                                   int64_t frames, double L, uint4* out, cudaStream_t s);
+                                   int64_t frames, double L, const StageMap& m, uint4* out, cudaStream_t s);
 cudaError_t launch_stage_generic64(const void* pos, const void* f, int64_t N, int64_t frames, double L,
-                                   ulonglong4* out, cudaStream_t s);
+                                   const StageMap& m, ulonglong4* out, cudaStream_t s);
+
+// species superposition (q-dependent form factors): out = |sum_s f_s(q) sum_c part_s[c]|^2 (mode 0) or the
+// amplitude (mode 1; mode 2: the partials hold conj(p)).  part_s [C_s][frames][n_q] (float2 | double2);
+// fq [n_species][n_l * n_q] (f32|f64), row of virtual frame v: plane (v0 + v) % n_l.
+constexpr int kMaxSpecies = 16;
+struct SpeciesParts {
+    const void* part[kMaxSpecies];
+    int64_t C[kMaxSpecies];
+    int n;
+    int part_f64;
+};
+cudaError_t launch_species_combine(const SpeciesParts& sp, int64_t frames, int64_t n_q, const void* fq, int fq_f64,
+                                   int64_t v0, int64_t n_l, void* out, int out_f64, int mode, cudaStream_t s);
+// f(q) = c + sum_i a_i exp(-b_i (|q| / 4 pi)^2) for an explicit q list (q != nullptr) or a 3-D lattice block
+cudaError_t launch_form_factor_gaussian(const void* q, int q_f64, int64_t n_q, const LatticeGeom& g, int64_t l0,
+                                        int64_t n_l, const int32_t* mc, int n_gauss, const double* a, const double* b,
+                                        double c, void* out, int out_f64, cudaStream_t s);
 
 // lattice contraction, FP32 CUDA cores: partial [C][Tb][n_h*n_k] float2
 cudaError_t launch_lattice_simt(const uint4* staged, int64_t N, int64_t frames, const LatticeGeom& g,

@@ -9,44 +9,65 @@
 // because q . r / 2 pi = (m . r) / L for q = (2 pi / L) m with integer m, so the phase in turns is the integer
 // combination of the box fractions, exact modulo 1.  fp64 inputs use 64-bit turns (ulonglong4).
 // HBM-bound: reads 12-24 B and writes 16-32 B per atom per frame (32 B for the generic fp32 record).
+// Staging also realises the 3-D q blocks (one virtual frame per (frame, l-plane)) and the species gather.
 #include "common.cuh"
 
 namespace xpcs {
 
+// Record i of a batch is staged atom j = i % N of virtual frame v = m.v0 + i / N; virtual frame v is source frame
+// t = v / m.n_l and reciprocal-lattice plane l = m.l0 + v % m.n_l (3-D q blocks: Th_0 = (m0 + l mc) . Xi); staged
+// atom j reads source atom m.idx[j] (species gather) or j.  Source frames hold m.n_src atoms.
+__device__ __forceinline__ int64_t stage_src(const StageMap& m, int64_t N, int64_t i, int64_t& v) {
+    v = m.v0 + i / N;
+    const int64_t j = i - (i / N) * N;
+    return m.idx ? (int64_t)m.idx[j] : j;
+}
+
 template <typename P, typename F>
 __global__ void __launch_bounds__(256) k_stage_lattice32(const P* __restrict__ pos, const F* __restrict__ f,
-                                                         int64_t N, int64_t total, LatticeGeom g,
+                                                         int64_t N, int64_t total, LatticeGeom g, StageMap m,
                                                          uint4* __restrict__ out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const P* r = pos + 3 * i;
+        int64_t v;
+        const int64_t src = stage_src(m, N, i, v);
+        const int64_t t = v / m.n_l, l = m.l0 + (v - t * m.n_l);
+        const P* r = pos + 3 * (t * m.n_src + src);
         uint32_t X[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) X[c] = frac_to_fixed32(box_fraction((double)r[c], g.L));
         uint32_t th[3];
-        const int32_t* m[3] = {g.ma, g.mb, g.m0};
+        int32_t m0[3];
 #pragma unroll
-        for (int v = 0; v < 3; ++v)
-            th[v] = (uint32_t)m[v][0] * X[0] + (uint32_t)m[v][1] * X[1] + (uint32_t)m[v][2] * X[2];
-        const float fj = f ? (float)f[i % N] : 1.0f;
+        for (int c = 0; c < 3; ++c) m0[c] = g.m0[c] + (int32_t)l * m.mc[c];
+        const int32_t* mv[3] = {g.ma, g.mb, m0};
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            th[k] = (uint32_t)mv[k][0] * X[0] + (uint32_t)mv[k][1] * X[1] + (uint32_t)mv[k][2] * X[2];
+        const float fj = f ? (float)f[src] : 1.0f;
         out[i] = make_uint4(th[0], th[1], th[2], __float_as_uint(fj));
     }
 }
 
 __global__ void __launch_bounds__(256) k_stage_lattice64(const double* __restrict__ pos, const double* __restrict__ f,
-                                                         int64_t N, int64_t total, LatticeGeom g,
+                                                         int64_t N, int64_t total, LatticeGeom g, StageMap m,
                                                          ulonglong4* __restrict__ out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const double* r = pos + 3 * i;
+        int64_t v;
+        const int64_t src = stage_src(m, N, i, v);
+        const int64_t t = v / m.n_l, l = m.l0 + (v - t * m.n_l);
+        const double* r = pos + 3 * (t * m.n_src + src);
         uint64_t X[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) X[c] = frac_to_fixed64(box_fraction(r[c], g.L));
         uint64_t th[3];
-        const int32_t* m[3] = {g.ma, g.mb, g.m0};
+        int64_t m0[3];
 #pragma unroll
-        for (int v = 0; v < 3; ++v)
-            th[v] = (uint64_t)(int64_t)m[v][0] * X[0] + (uint64_t)(int64_t)m[v][1] * X[1] +
-                    (uint64_t)(int64_t)m[v][2] * X[2];
-        const double fj = f ? f[i % N] : 1.0;
+        for (int c = 0; c < 3; ++c) m0[c] = (int64_t)g.m0[c] + l * (int64_t)m.mc[c];
+        const int64_t mv[3][3] = {{g.ma[0], g.ma[1], g.ma[2]}, {g.mb[0], g.mb[1], g.mb[2]}, {m0[0], m0[1], m0[2]}};
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            th[k] = (uint64_t)mv[k][0] * X[0] + (uint64_t)mv[k][1] * X[1] + (uint64_t)mv[k][2] * X[2];
+        const double fj = f ? f[src] : 1.0;
         out[i] = make_ulonglong4(th[0], th[1], th[2], (unsigned long long)__double_as_longlong(fj));
     }
 }
@@ -55,14 +76,16 @@ __global__ void __launch_bounds__(256) k_stage_lattice64(const double* __restric
 // fractions as fp32 (for the fractional part of q.r, see k_generic.cu)
 template <typename P, typename F>
 __global__ void __launch_bounds__(256) k_stage_generic32(const P* __restrict__ pos, const F* __restrict__ f,
-                                                         int64_t N, int64_t total, double L,
+                                                         int64_t N, int64_t total, double L, StageMap m,
                                                          uint4* __restrict__ out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const P* r = pos + 3 * i;
+        int64_t v;
+        const int64_t src = stage_src(m, N, i, v);
+        const P* r = pos + 3 * (v * m.n_src + src);
         const double ux = box_fraction((double)r[0], L), uy = box_fraction((double)r[1], L),
                      uz = box_fraction((double)r[2], L);
         const uint32_t x = frac_to_fixed32(ux), y = frac_to_fixed32(uy), z = frac_to_fixed32(uz);
-        const float fj = f ? (float)f[i % N] : 1.0f;
+        const float fj = f ? (float)f[src] : 1.0f;
         out[2 * i] = make_uint4(x, y, z, __float_as_uint(fj));
         // fp32 fractions of the same fixed-point values (x * 2^-32 rounded once)
         out[2 * i + 1] = make_uint4(__float_as_uint((float)((double)x * 2.3283064365386963e-10)),
@@ -72,11 +95,13 @@ __global__ void __launch_bounds__(256) k_stage_generic32(const P* __restrict__ p
 }
 
 __global__ void __launch_bounds__(256) k_stage_generic64(const double* __restrict__ pos, const double* __restrict__ f,
-                                                         int64_t N, int64_t total, double L,
+                                                         int64_t N, int64_t total, double L, StageMap m,
                                                          ulonglong4* __restrict__ out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const double* r = pos + 3 * i;
-        const double fj = f ? f[i % N] : 1.0;
+        int64_t v;
+        const int64_t src = stage_src(m, N, i, v);
+        const double* r = pos + 3 * (v * m.n_src + src);
+        const double fj = f ? f[src] : 1.0;
         out[i] = make_ulonglong4(frac_to_fixed64(box_fraction(r[0], L)), frac_to_fixed64(box_fraction(r[1], L)),
                                  frac_to_fixed64(box_fraction(r[2], L)),
                                  (unsigned long long)__double_as_longlong(fj));
@@ -90,46 +115,48 @@ static dim3 grid_for(int64_t total) {
 }
 
 cudaError_t launch_stage_lattice32(const void* pos, int pos_f64, const void* f, int f_f64, int64_t N,
-                                   int64_t frames, const LatticeGeom& g, uint4* out, cudaStream_t s) {
+                                   int64_t frames, const LatticeGeom& g, const StageMap& m, uint4* out, cudaStream_t s) {
     const int64_t total = N * frames;
     note_launch();
+    const dim3 gr = grid_for(total);
     if (pos_f64) {
-        if (f_f64) k_stage_lattice32<double, double><<<grid_for(total), 256, 0, s>>>((const double*)pos, (const double*)f, N, total, g, out);
-        else k_stage_lattice32<double, float><<<grid_for(total), 256, 0, s>>>((const double*)pos, (const float*)f, N, total, g, out);
+        if (f_f64) k_stage_lattice32<double, double><<<gr, 256, 0, s>>>((const double*)pos, (const double*)f, N, total, g, m, out);
+        else k_stage_lattice32<double, float><<<gr, 256, 0, s>>>((const double*)pos, (const float*)f, N, total, g, m, out);
     } else {
-        if (f_f64) k_stage_lattice32<float, double><<<grid_for(total), 256, 0, s>>>((const float*)pos, (const double*)f, N, total, g, out);
-        else k_stage_lattice32<float, float><<<grid_for(total), 256, 0, s>>>((const float*)pos, (const float*)f, N, total, g, out);
+        if (f_f64) k_stage_lattice32<float, double><<<gr, 256, 0, s>>>((const float*)pos, (const double*)f, N, total, g, m, out);
+        else k_stage_lattice32<float, float><<<gr, 256, 0, s>>>((const float*)pos, (const float*)f, N, total, g, m, out);
     }
     return cudaGetLastError();
 }
 
 cudaError_t launch_stage_lattice64(const void* pos, const void* f, int64_t N, int64_t frames,
-                                   const LatticeGeom& g, ulonglong4* out, cudaStream_t s) {
+                                   const LatticeGeom& g, const StageMap& m, ulonglong4* out, cudaStream_t s) {
     const int64_t total = N * frames;
     note_launch();
-    k_stage_lattice64<<<grid_for(total), 256, 0, s>>>((const double*)pos, (const double*)f, N, total, g, out);
+    k_stage_lattice64<<<grid_for(total), 256, 0, s>>>((const double*)pos, (const double*)f, N, total, g, m, out);
     return cudaGetLastError();
 }
 
 cudaError_t launch_stage_generic32(const void* pos, int pos_f64, const void* f, int f_f64, int64_t N,
-                                   int64_t frames, double L, uint4* out, cudaStream_t s) {
+                                   int64_t frames, double L, const StageMap& m, uint4* out, cudaStream_t s) {
     const int64_t total = N * frames;
     note_launch();
+    const dim3 gr = grid_for(total);
     if (pos_f64) {
-        if (f_f64) k_stage_generic32<double, double><<<grid_for(total), 256, 0, s>>>((const double*)pos, (const double*)f, N, total, L, out);
-        else k_stage_generic32<double, float><<<grid_for(total), 256, 0, s>>>((const double*)pos, (const float*)f, N, total, L, out);
+        if (f_f64) k_stage_generic32<double, double><<<gr, 256, 0, s>>>((const double*)pos, (const double*)f, N, total, L, m, out);
+        else k_stage_generic32<double, float><<<gr, 256, 0, s>>>((const double*)pos, (const float*)f, N, total, L, m, out);
     } else {
-        if (f_f64) k_stage_generic32<float, double><<<grid_for(total), 256, 0, s>>>((const float*)pos, (const double*)f, N, total, L, out);
-        else k_stage_generic32<float, float><<<grid_for(total), 256, 0, s>>>((const float*)pos, (const float*)f, N, total, L, out);
+        if (f_f64) k_stage_generic32<float, double><<<gr, 256, 0, s>>>((const float*)pos, (const double*)f, N, total, L, m, out);
+        else k_stage_generic32<float, float><<<gr, 256, 0, s>>>((const float*)pos, (const float*)f, N, total, L, m, out);
     }
     return cudaGetLastError();
 }
 
 cudaError_t launch_stage_generic64(const void* pos, const void* f, int64_t N, int64_t frames, double L,
-                                   ulonglong4* out, cudaStream_t s) {
+                                   const StageMap& m, ulonglong4* out, cudaStream_t s) {
     const int64_t total = N * frames;
     note_launch();
-    k_stage_generic64<<<grid_for(total), 256, 0, s>>>((const double*)pos, (const double*)f, N, total, L, out);
+    k_stage_generic64<<<grid_for(total), 256, 0, s>>>((const double*)pos, (const double*)f, N, total, L, m, out);
     return cudaGetLastError();
 }
 

@@ -81,3 +81,41 @@ def test_binding_refuses_host_tensors(lib):
     torch = pytest.importorskip("torch")
     with pytest.raises(ValueError, match="device memory"):
         _lib._ptr(torch.zeros(3))
+
+
+def test_volume_species_validation_before_launch(lib):
+    """3-D blocks / q-dependent form factors: host-side validation rejects before any launch."""
+    n0 = lib.xpcs_launch_count()
+    o = _lib.Opts(0, 0, None, 0, 0)
+    dummy = ctypes.c_void_p(16)
+    vol = xp.qvolume(10.0, -4, 8, -4, 8, -2, 5)
+    assert vol.n_q == 320
+    vol.n_l = 0
+    rc = lib.xpcs_intensity_volume(dummy, 4, None, None, ctypes.byref(vol), 1, dummy, ctypes.byref(o))
+    assert rc == _lib.XPCS_EINVAL and b"n_l" in lib.xpcs_last_error()
+    vol = xp.qvolume(10.0, -4, 8, -4, 8, -2, 5, mc=(0, 0, 1 << 30))
+    rc = lib.xpcs_intensity_volume(dummy, 4, None, None, ctypes.byref(vol), 1, dummy, ctypes.byref(o))
+    assert rc == _lib.XPCS_EINVAL and b"out of range" in lib.xpcs_last_error()
+    vol = xp.qvolume(10.0, -4, 8, -4, 8, -2, 5)
+    sp = _lib.Species()
+    arr, ap = _lib._i32_array([0, 1, 2, 1])
+    sp.species, sp.f_q, sp.n_species = ap, dummy, 2
+    rc = lib.xpcs_intensity_volume(dummy, 4, None, ctypes.byref(sp), ctypes.byref(vol), 1, dummy, ctypes.byref(o))
+    assert rc == _lib.XPCS_EINVAL and b"species[2] = 2" in lib.xpcs_last_error()
+    sp.n_species = 17
+    rc = lib.xpcs_intensity_species(dummy, 4, ctypes.byref(sp), dummy, 5, 1, 1.0, dummy, ctypes.byref(o))
+    assert rc == _lib.XPCS_EINVAL and b"n_species" in lib.xpcs_last_error()
+    sp.n_species = 3
+    rc = lib.xpcs_intensity_volume(dummy, 4, dummy, ctypes.byref(sp), ctypes.byref(vol), 1, dummy, ctypes.byref(o))
+    assert rc == _lib.XPCS_EINVAL and b"exclusive" in lib.xpcs_last_error()
+    sp.f_q = None
+    rc = lib.xpcs_intensity_species(dummy, 4, ctypes.byref(sp), dummy, 5, 1, 1.0, dummy, ctypes.byref(o))
+    assert rc == _lib.XPCS_EINVAL and b"f_q" in lib.xpcs_last_error()
+    rc = lib.xpcs_intensity_species(dummy, 4, None, dummy, 5, 1, 1.0, dummy, ctypes.byref(o))
+    assert rc == _lib.XPCS_EINVAL
+    a = (ctypes.c_double * 7)()
+    rc = lib.xpcs_form_factor_gaussian(dummy, 5, None, 7, a, a, 0.0, dummy, ctypes.byref(o))
+    assert rc == _lib.XPCS_EINVAL and b"n_gauss" in lib.xpcs_last_error()
+    rc = lib.xpcs_form_factor_gaussian(None, 5, None, 1, a, a, 0.0, dummy, ctypes.byref(o))
+    assert rc == _lib.XPCS_EINVAL
+    assert lib.xpcs_launch_count() == n0

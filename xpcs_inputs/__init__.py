@@ -146,3 +146,25 @@ def pixel_subset(n_q: int, count: int, seed: int, include=()) -> np.ndarray:
     rng = np.random.Generator(np.random.PCG64(seed))
     pick = rng.choice(n_q, size=min(count, n_q), replace=False)
     return np.unique(np.concatenate([pick, np.asarray(include, dtype=np.int64)])).astype(np.int64)
+
+
+def species_labels(N: int, n_species: int, seed: int) -> np.ndarray:
+    """Seeded atom kinds in [0, n_species) (int32), for the q-dependent form-factor path."""
+    rng = np.random.Generator(np.random.PCG64([seed, 77]))
+    return rng.integers(0, n_species, N).astype(np.int32)
+
+
+# Table 1 of the paper (PAPER.md:451-465): one liquid-Ar frame, N = 4000 atoms in a cubic box of L = 59.19 Angstrom
+# (PAPER.md:385), Algorithm 1 on an 81 x 81 x 81 reciprocal-lattice grid (PAPER.md:459), h, k, l in [-40, 40].
+# The Ar configuration itself is not available: a seeded uniform frame of the same N, L stands in for it.
+TABLE1 = dict(N=4000, L=59.19, n=81, seed=SEED_BASE + 10)
+
+
+def gaussian_form_factor_coefficients(n_species: int):
+    """Synthetic Gaussian-sum coefficients (a, b, c) per kind for f(q) = c + sum a_i exp(-b_i (q / 4 pi)^2)
+    (the PAPER.md:94-95 form; NOT tabulated element data -- values made up for testing, in sigma units)."""
+    table = [([9.0, 6.0, 2.0], [1.5, 12.0, 45.0], 1.0),
+             ([3.0, 2.0], [4.0, 25.0], 0.3),
+             ([0.5], [8.0], 0.0),
+             ([5.0, 1.0, 0.5, 0.25], [2.0, 8.0, 30.0, 90.0], 0.2)]
+    return [table[s % len(table)] for s in range(n_species)]
