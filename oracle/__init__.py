@@ -16,6 +16,7 @@ Contents (each function cites the passage it follows):
   * lattice_volume_q -- 3-D reciprocal-lattice block (Table 1's 81^3 grid).
   * species_intensity / pair_sum_species -- Eq.(2)/(7) with q-dependent form factors f_s(q).
   * form_factor_gaussian -- f(q) as a sum of Gaussians.
+  * speckle_histogram / erlang_pdf -- kappa = I_M / <I_M>_ring statistics, Eq.(37)-(38).
 Every function is pinned by tests/test_oracle_pins.py (no function here is "parity unpinned").
 """
 from __future__ import annotations
@@ -328,3 +329,45 @@ def xsvs_beta(I, bins, n_bins, windows, per_window=False):
             row.append(beta_s)
         detail.append(row)
     return (out, detail) if per_window else out
+
+
+def speckle_histogram(I, bins, n_bins, M, n_hist, kappa_max, edge_tol=1e-9):
+    """Speckle intensity statistics (PAPER.md:540-546 and Eq.(37)-(38)).  The incoherent
+    superposition of M patterns (sum over intensity) of consecutive frames,
+        I_M(q, s) = sum_{t=sM}^{sM+M-1} I(q, t),  s = 0 .. floor(T/M) - 1,
+    normalised per ring b and snapshot s, kappa(q) = I_M(q, s) / <I_M(., s)>_{q in b} (the paper's
+    kappa = I / <I>_q), is histogrammed over the ring's pixels and all snapshots into n_hist bins of width
+    kappa_max / n_hist on [0, kappa_max) (kappa >= kappa_max dropped): h = floor(kappa * n_hist / kappa_max).
+    Returns (counts int64 [n_bins][n_hist], ambiguous int64 [n_bins][n_hist + 1]) where ambiguous counts values
+    whose kappa * n_hist / kappa_max lies within edge_tol (relative) of an integer edge e (slot e), the only
+    decisions a different FP64 summation order of the ring mean could flip."""
+    I = np.asarray(I, dtype=np.float64)
+    T = I.shape[0]
+    S = T // M
+    IM = I[: S * M].reshape(S, M, -1).sum(1)                    # [S][n_q]
+    counts = np.zeros((n_bins, n_hist), dtype=np.int64)
+    amb = np.zeros((n_bins, n_hist + 1), dtype=np.int64)
+    for b in range(n_bins):
+        sel = IM[:, bins == b]                                   # [S][m0]
+        if sel.shape[1] == 0:
+            continue
+        for s in range(S):
+            x = sel[s]
+            mean = x.sum() / x.size
+            if not mean > 0:
+                continue
+            u = (x / mean) * n_hist / kappa_max
+            for v in u:
+                h = int(math.floor(v))
+                if h < n_hist:
+                    counts[b, h] += 1
+                e = int(round(v))
+                if abs(v - e) <= edge_tol * max(1.0, abs(v)) and e <= n_hist:
+                    amb[b, e] += 1
+    return counts, amb
+
+
+def erlang_pdf(kappa, M):
+    """Eq.(38): P_M(kappa) = M^M kappa^(M-1) exp(-M kappa) / (M-1)!  (M = 1: Eq.(37) exp(-kappa))."""
+    kappa = np.asarray(kappa, dtype=np.float64)
+    return M ** M * kappa ** (M - 1) * np.exp(-M * kappa) / math.factorial(M - 1)

@@ -451,3 +451,46 @@ def test_volume_bragg_peaks_and_table1_grid():
     qt = oracle.lattice_volume_q(Lp, -40, 81, -40, 81, -40, 81)
     assert qt.shape == (81 ** 3, 3)
     np.testing.assert_allclose(np.abs(qt).max(0), 40 * 2 * np.pi / Lp, rtol=1e-15)
+
+
+# ------------------------------------------------------------------ speckle statistics, Eq.(37)-(38)
+@pytest.mark.parametrize("case", ["one_ring_M1", "two_rings_M2_remainder"])
+def test_speckle_histogram_worked_examples(case):
+    g = _gold("speckle_histogram.json")[case]
+    counts, amb = oracle.speckle_histogram(np.array(g["I"]), np.array(g["bins"]), len(g["counts"]), g["M"],
+                                           g["n_hist"], g["kappa_max"])
+    np.testing.assert_array_equal(counts, g["counts"])
+
+
+def test_erlang_pdf_is_the_gamma_law():
+    """Eq.(38) is the Gamma(M, 1/M) density (sum of M iid Exp(1) normalised by M); M = 1 is
+    Eq.(37)."""
+    from scipy import stats
+    k = np.linspace(0.01, 6, 200)
+    for M in (1, 2, 5, 10, 20):
+        np.testing.assert_allclose(oracle.erlang_pdf(k, M), stats.gamma(a=M, scale=1.0 / M).pdf(k), rtol=1e-12)
+
+
+def test_speckle_histogram_follows_erlang_law():
+    """Ideal-gas independent frames on lattice q: |p|^2 is exponential (fully coherent) and the sum of
+    M independent patterns is Erlang.  The pooled histogram of kappa over rings and snapshots must
+    match the bin integrals of Eq.(38) within 5 sigma (+ a 3% allowance for normalising by the ring's sample mean)."""
+    from scipy import stats
+    N, L, T, n = 400, 8.0, 48, 40
+    pos = np.stack([xi.uniform_frame(500 + s, N, L) for s in range(T)])
+    I = oracle.intensity(pos, None, oracle.lattice_q(L, **oracle.plane_grid(n)), L)
+    bins = oracle.lattice_bins(n, n_bins=4)
+    bins[bins == 0] = -1                                   # innermost ring: too few pixels
+    for M in (1, 3, 6):
+        n_hist, kmax = 16, 4.0
+        counts, _ = oracle.speckle_histogram(I, bins, 4, M, n_hist, kmax)
+        tot = counts.sum(0)
+        n_all = int((bins >= 0).sum()) * (T // M)
+        edges = np.linspace(0, kmax, n_hist + 1)
+        cdf = stats.gamma(a=M, scale=1.0 / M).cdf(edges)
+        expect = n_all * np.diff(cdf)
+        assert np.all(np.abs(tot - expect) <= 5 * np.sqrt(expect + 1) + 0.03 * expect), (M, tot, expect)
+        # invariants: every kappa < kmax is counted once; scaling I leaves kappa unchanged
+        assert tot.sum() <= n_all
+        c2, _ = oracle.speckle_histogram(I * 3.5, bins, 4, M, n_hist, kmax)
+        np.testing.assert_array_equal(c2, counts)
