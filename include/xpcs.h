@@ -204,6 +204,20 @@ XPCS_API int xsvs_contrast(const void* I_series, int64_t frames, int64_t n_q,
                   const int32_t* windows, int64_t n_windows,
                   double* beta_out, const xpcs_opts* opts);
 
+/* Speckle intensity statistics (kappa = I / <I>_q over a q ring follows exp(-kappa), Eq.(37), for a
+ * coherent beam; the incoherent superposition of M independent patterns follows the Erlang law of
+ * Eq.(38) with contrast 1/M).  With I_M(q, s) = sum_{t=sM}^{sM+M-1} I(q, t), s = 0 .. floor(T/M) - 1 (remainder
+ * dropped) and kappa = I_M(q, s) / <I_M(., s)>_{ring b} (ring mean over the ring's pixels, FP64), counts kappa over
+ * all pixels and snapshots into n_hist bins of width kappa_max / n_hist on [0, kappa_max), bin
+ * h = floor((kappa * n_hist) / kappa_max); kappa >= kappa_max is not counted; a ring/snapshot with mean <= 0 is skipped.
+ *   I_series [frames][n_q] in_dtype; bin_of_q DEVICE [n_q] (-1 = excluded); counts_out DEVICE [n_bins][n_hist] int64.
+ * The counts are exact integers; only a kappa within ~1e-15 relative of a bin edge can land differently from a
+ * summation in another order.  Errors: EINVAL for null pointers, sizes <= 0, M outside [1, frames], n_hist outside
+ * [1, 2^20], kappa_max <= 0 or non-finite. */
+XPCS_API int xpcs_speckle_histogram(const void* I_series, int64_t frames, int64_t n_q, const int32_t* bin_of_q,
+                                    int32_t n_bins, int32_t M, int32_t n_hist, double kappa_max, int64_t* counts_out,
+                                    const xpcs_opts* opts);
+
 /* Ring average of any per-pixel quantity, per row:
  *   out[r][b] = scale * mean_{q in ring b, values finite} values[r][q]   (NaN if no finite value),
  * e.g. the ring-averaged g2(q, tau) or, with scale = 1 / sum_j f_j^2, the structure factor

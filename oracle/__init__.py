@@ -16,6 +16,7 @@ Contents (each function cites the passage it follows):
   * lattice_volume_q -- 3-D reciprocal-lattice block (Table 1's 81^3 grid).
   * species_intensity / pair_sum_species -- Eq.(2)/(7) with q-dependent form factors f_s(q).
   * form_factor_gaussian -- f(q) as a sum of Gaussians.
+  * fft_intensity / fft_block -- Algorithm 2, the FFT-based method, FP64 numpy FFT.
   * speckle_histogram / erlang_pdf -- kappa = I_M / <I_M>_ring statistics, Eq.(37)-(38).
 Every function is pinned by tests/test_oracle_pins.py (no function here is "parity unpinned").
 """
@@ -371,3 +372,56 @@ def erlang_pdf(kappa, M):
     """Eq.(38): P_M(kappa) = M^M kappa^(M-1) exp(-M kappa) / (M-1)!  (M = 1: Eq.(37) exp(-kappa))."""
     kappa = np.asarray(kappa, dtype=np.float64)
     return M ** M * kappa ** (M - 1) * np.exp(-M * kappa) / math.factorial(M - 1)
+
+
+# ----------------------------------------------------------------------------------------------
+# Algorithm 2 (FFT-based method, PAPER.md:303-372) -- SURVEY 8(f) rank 4, the paper's cross-check path
+# ----------------------------------------------------------------------------------------------
+def fft_kernel_width(L, n_grid, eta, k=0):
+    """k = 'the nearest integer greater than 10 eta' in grid spacings, made odd so the k points
+    nearest the origin are centred (reading R16); an explicit k > 0 is used as given (must be odd)."""
+    if k <= 0:
+        k = int(math.floor(10.0 * eta / (L / n_grid))) + 1
+        if k % 2 == 0:
+            k += 1
+    assert k % 2 == 1
+    return k
+
+
+def _spread(pos, L, n_grid, eta, k):
+    """Algorithm 2 steps 1-2: rho^eta on the n_grid^3 grid, each atom's Gaussian (Eq. 30) evaluated on the k x k x k
+    grid points nearest to it (periodic wrap of the indices), grid point n at r = n L / n_grid."""
+    d = L / n_grid
+    rho = np.zeros((n_grid, n_grid, n_grid))
+    c = (1.0 / (math.sqrt(2.0 * math.pi) * eta)) ** 3
+    for r in np.asarray(pos, dtype=np.float64):
+        idx = []
+        for a in range(3):
+            u = r[a] / d
+            n0 = int(math.floor(u - k / 2.0)) + 1              # the k integers nearest to u
+            idx.append(np.arange(n0, n0 + k))
+        X, Y, Z = np.meshgrid(*idx, indexing="ij")
+        r2 = (X * d - r[0]) ** 2 + (Y * d - r[1]) ** 2 + (Z * d - r[2]) ** 2
+        np.add.at(rho, (X % n_grid, Y % n_grid, Z % n_grid), c * np.exp(-r2 / (2.0 * eta * eta)))
+    return rho
+
+
+def fft_intensity(pos, L, n_grid, eta, k=0, f=1.0):
+    """Algorithm 2 for one frame [N][3]: rho^eta (steps 1-2), p^eta = FFT (step 3, with the
+    e^{-i q.r} sign of Eq. 31: numpy's forward transform), f^eta = FFT of the truncated Gaussian centred at the origin
+    (step 4), I = f^2 |p^eta|^2 / |f^eta|^2 (Eq. 35, step 5).  Returns I on the full FFT grid [n][n][n], axis index
+    m <-> frequency h = m (m < n/2) or m - n; q = (2 pi / L)(h, k, l).  FP64."""
+    k = fft_kernel_width(L, n_grid, eta, k)
+    P = np.fft.fftn(_spread(pos, L, n_grid, eta, k))
+    G = np.fft.fftn(_spread(np.zeros((1, 3)), L, n_grid, eta, k))
+    return f * f * np.abs(P) ** 2 / np.abs(G) ** 2
+
+
+def fft_block(I_full, h0, n_h, k0, n_k, l0, n_l):
+    """Block of a full FFT-grid array in (l, h, k) output order (as xpcs_qvolume / lattice_volume_q): entry
+    [il][ih][ik] = I at frequencies (h0 + ih, k0 + ik, l0 + il) on axes (x, y, z)."""
+    n = I_full.shape[0]
+    hh = (np.arange(h0, h0 + n_h)) % n
+    kk = (np.arange(k0, k0 + n_k)) % n
+    ll = (np.arange(l0, l0 + n_l)) % n
+    return I_full[np.ix_(hh, kk, ll)].transpose(2, 0, 1).reshape(-1)

@@ -26,7 +26,7 @@ EXPORTED = (
     "xpcs_profile_query", "xpcs_device_info", "xpcs_version", "xpcs_engine_available",
     "xpcs_amplitude", "xpcs_amplitude_grid", "xpcs_isf",
     "xpcs_intensity_volume", "xpcs_amplitude_volume", "xpcs_intensity_species", "xpcs_amplitude_species",
-    "xpcs_form_factor_gaussian",
+    "xpcs_form_factor_gaussian", "xpcs_speckle_histogram",
 )
 
 
@@ -107,6 +107,7 @@ def load():
         "xpcs_amplitude_volume": [vp, i64, vp, ctypes.POINTER(Species), ctypes.POINTER(QVolume), i64, vp, op],
         "xpcs_intensity_species": [vp, i64, ctypes.POINTER(Species), vp, i64, i64, dbl, vp, op],
         "xpcs_amplitude_species": [vp, i64, ctypes.POINTER(Species), vp, i64, i64, dbl, vp, op],
+        "xpcs_speckle_histogram": [vp, i64, i64, vp, i32, i32, i32, dbl, vp, op],
         "xpcs_form_factor_gaussian": [vp, i64, ctypes.POINTER(QVolume), i32, ctypes.POINTER(ctypes.c_double),
                                       ctypes.POINTER(ctypes.c_double), dbl, vp, op],
     }
@@ -363,6 +364,18 @@ def xsvs_contrast(I, bins, n_bins, windows, out=None, stream=None, profile=False
     o = make_opts(_dtype_code(I), F64, stream, ENGINE_AUTO, profile)
     _check(load().xsvs_contrast(_ptr(I), T, n_q, _ptr(bins), int(n_bins), w_p, len(w_arr), _ptr(out),
                                 ctypes.byref(o)))
+    return out
+
+
+def xpcs_speckle_histogram(I, bins, n_bins, M, n_hist, kappa_max, out=None, stream=None, profile=False):
+    """Eq.(37)-(38) statistics: counts of kappa = I_M / <I_M>_ring -> int64 [n_bins][n_hist]."""
+    import torch
+    T, n_q = I.shape
+    if out is None:
+        out = torch.empty((n_bins, n_hist), dtype=torch.int64, device=I.device)
+    o = make_opts(_dtype_code(I), F64, stream, ENGINE_AUTO, profile)
+    _check(load().xpcs_speckle_histogram(_ptr(I), T, n_q, _ptr(bins), int(n_bins), int(M), int(n_hist),
+                                         float(kappa_max), _ptr(out), ctypes.byref(o)))
     return out
 
 

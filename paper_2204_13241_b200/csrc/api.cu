@@ -452,8 +452,9 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
         return XPCS_OK;
     }
     // atom chunks (split-K over CTAs, folded in FP64 by the reduction): SIMT keeps fp32 register sums short
-    // (<= 4096 atoms); the tensor engine drains TMEM every 256 atoms into RN sums, so its chunks only balance
-    // the grid (>= ~8 waves of one CTA per SM) and stay >= 1024 atoms.
+    // (<= 4096 atoms) and splits further (>= 512 atoms per chunk) when tiles x frames cannot fill ~2 waves; the
+    // tensor engine drains TMEM every 256 atoms into RN sums, so its chunks only balance the grid (>= ~8 waves of
+    // one CTA per SM) and stay >= 1024 atoms (>= 256 when the grid is small: few tiles, few frames).
     std::vector<int64_t> chunk(ng, 4096), C(ng, 0);
     int64_t sumC = 0;
     for (int gi = 0; gi < ng; ++gi) {
@@ -464,8 +465,16 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
             const int64_t tiles = ((g.n_h + 127) / 128) * ((g.n_k + 127) / 128);
             const int64_t units = tiles * std::min<int64_t>(V, 64);
             int64_t C0 = std::max<int64_t>(1, (8LL * sm_count() + units - 1) / units);
-            C0 = std::min<int64_t>(C0, std::max<int64_t>(1, Ng / 1024));
+            const int64_t min_chunk = units >= sm_count() ? 1024 : 256;
+            C0 = std::min<int64_t>(C0, std::max<int64_t>(1, Ng / min_chunk));
             ch = ((Ng + C0 - 1) / C0 + 15) / 16 * 16;
+        } else {
+            const int64_t units = ((g.n_h + 63) / 64) * ((g.n_k + 127) / 128) * V;
+            const int64_t want = 2LL * sm_count() * 4;
+            if (units * ((Ng + 4095) / 4096) < want) {
+                const int64_t C0 = std::min<int64_t>((want + units - 1) / units, std::max<int64_t>(1, Ng / 512));
+                ch = std::min<int64_t>(4096, ((Ng + C0 - 1) / C0 + 15) / 16 * 16);
+            }
         }
         if (const char* e = getenv("XPCS_CHUNK_ATOMS")) ch = std::max<int64_t>(16, atoll(e));   // experiments only
         chunk[gi] = ch;
@@ -693,6 +702,45 @@ int xsvs_contrast(const void* I_series, int64_t frames, int64_t n_q, const int32
     if (!mom) return XPCS_ENOMEM;
     return cuda_fail(launch_xsvs(I_series, o.in_f64, frames, n_q, pb.plan, n_bins, windows, n_windows, pb.max_warps,
                                  mom, nullptr, beta_out, o.s), "xsvs");
+}
+
+int xpcs_speckle_histogram(const void* I_series, int64_t frames, int64_t n_q, const int32_t* bin_of_q, int32_t n_bins,
+                           int32_t M, int32_t n_hist, double kappa_max, int64_t* counts_out, const xpcs_opts* opts) {
+    clear_error();
+    Opts o;
+    TRY(parse_opts(opts, o));
+    NEED(I_series, "I_series");
+    NEED(bin_of_q, "bin_of_q");
+    NEED(counts_out, "counts_out");
+    POS(frames, "frames");
+    POS(n_q, "n_q");
+    POS(n_bins, "n_bins");
+    if (M < 1 || M > frames) {
+        set_error("xpcs: M = %d out of range [1, %lld]", M, (long long)frames);
+        return XPCS_EINVAL;
+    }
+    if (n_hist < 1 || n_hist > (1 << 20)) {
+        set_error("xpcs: n_hist must be in [1, 2^20] (got %d)", n_hist);
+        return XPCS_EINVAL;
+    }
+    if (!(kappa_max > 0.0) || !std::isfinite(kappa_max)) {
+        set_error("xpcs: kappa_max must be finite and > 0");
+        return XPCS_EINVAL;
+    }
+    if (n_q > (int64_t(1) << 31) - 1) {
+        set_error("xpcs: n_q too large for the ring plan");
+        return XPCS_EINVAL;
+    }
+    TRY(check_sticky());
+    ProfScope p(o.profile, KC_XSVS, o.s);
+    PlanBufs pb;
+    TRY(make_plan(bin_of_q, n_q, n_bins, o.s, pb));
+    const int64_t S = frames / M;
+    double* mom = (double*)scratch(o.s, SS_XSVS, sizeof(double2) * (size_t)(pb.max_warps * S) + sizeof(double) * (size_t)(S * n_bins));
+    if (!mom) return XPCS_ENOMEM;
+    double* means = mom + 2 * (size_t)(pb.max_warps * S);
+    return cuda_fail(launch_speckle_hist(I_series, o.in_f64, frames, n_q, pb.plan, n_bins, M, pb.max_warps, mom, means,
+                                         n_hist, kappa_max, counts_out, o.s), "speckle histogram");
 }
 
 int xpcs_shell_mean(const void* values, int64_t rows, int64_t n_q, const int32_t* bin_of_q, int32_t n_bins,

@@ -176,6 +176,9 @@ cudaError_t launch_binplan(const int32_t* bins, int64_t n_q, int32_t n_bins, Bin
 cudaError_t launch_sum_f2(const void* f, int f_f64, int64_t N, double* out, cudaStream_t s);
 cudaError_t launch_shell_mean(const void* v, int in_f64, int64_t rows, int64_t n_q, BinPlan plan,
                               int32_t n_bins, double scale, const double* norm, double* out, cudaStream_t s);
+cudaError_t launch_speckle_hist(const void* I, int in_f64, int64_t T, int64_t n_q, BinPlan plan, int32_t n_bins,
+                                int32_t M, int64_t max_warps, double* warp_moments, double* means, int32_t n_hist,
+                                double kappa_max, int64_t* counts, cudaStream_t s);
 cudaError_t launch_xsvs(const void* I, int in_f64, int64_t T, int64_t n_q, BinPlan plan, int32_t n_bins,
                         const int32_t* windows_host, int64_t n_windows, int64_t max_warps, double* warp_moments,
                         int32_t* dev_windows, double* beta_out, cudaStream_t s);

@@ -443,4 +443,80 @@ cudaError_t launch_xsvs(const void* I, int in_f64, int64_t T, int64_t n_q, BinPl
     return cudaSuccess;
 }
 
+// =====================================================================================================
+// Speckle statistics (Eq.(37)-(38) PAPER.md:560-569): histogram of kappa = I_M / <I_M>_ring over
+// the pixels of each ring and all snapshots, I_M the sum of M consecutive frames (incoherent superposition).
+// Pass 1 = the XSVS warp moments with the single window M (ring sums per snapshot); pass 2 forms the ring means in
+// fixed order; pass 3 streams the series again, bins kappa in FP64 and counts with warp-aggregated integer
+// atomics (the counts are exact and order-independent).
+// =====================================================================================================
+__global__ void __launch_bounds__(256)
+k_ring_snapshot_mean(const double2* __restrict__ mom, const int32_t* __restrict__ off, const int32_t* __restrict__ woff,
+                     int S, int total_slots, int32_t n_bins, double* __restrict__ mean) {
+    const int b = blockIdx.x;
+    const int m0 = off[b + 1] - off[b];
+    for (int s = threadIdx.x; s < S; s += 256) {
+        double m1 = 0.0;
+        for (int g = woff[b]; g < woff[b + 1]; ++g) m1 += mom[(int64_t)g * total_slots + s].x;
+        mean[(int64_t)s * n_bins + b] = m0 > 0 ? m1 / m0 : 0.0;
+    }
+}
+
+template <typename In>
+__global__ void __launch_bounds__(128)
+k_speckle_hist(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __restrict__ perm,
+               const int32_t* __restrict__ off, const int32_t* __restrict__ woff, int32_t n_bins, int64_t total_warps,
+               int M, int S, const double* __restrict__ mean, int n_hist, double kappa_max,
+               unsigned long long* __restrict__ counts) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (gw >= total_warps || gw >= woff[n_bins]) return;
+    int lo = 0, hi = n_bins;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (woff[mid] <= gw) lo = mid; else hi = mid;
+    }
+    const int b = lo;
+    const int64_t idx = off[b] + (gw - woff[b]) * 32 + lane;
+    const bool valid = idx < off[b + 1];
+    const int64_t px = valid ? perm[idx] : 0;
+    const double nh = (double)n_hist;
+    for (int s = 0; s < S; ++s) {
+        double run = 0.0;
+        for (int t = 0; t < M; ++t) run += valid ? (double)I[((int64_t)s * M + t) * n_q + px] : 0.0;
+        const double mu = mean[(int64_t)s * n_bins + b];
+        int h = -1;
+        if (valid && mu > 0.0) {
+            const double u = (run / mu) * nh / kappa_max;      // same operation order as the oracle
+            if (u < nh) h = (int)floor(u);
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, h);
+        if (h >= 0 && lane == __ffs(peers) - 1)
+            atomicAdd(&counts[(int64_t)b * n_hist + h], (unsigned long long)__popc(peers));
+    }
+}
+
+cudaError_t launch_speckle_hist(const void* I, int in_f64, int64_t T, int64_t n_q, BinPlan plan, int32_t n_bins,
+                                int32_t M, int64_t max_warps, double* warp_moments, double* means, int32_t n_hist,
+                                double kappa_max, int64_t* counts, cudaStream_t s) {
+    const int S = (int)(T / M);
+    WinSet ws{};
+    ws.n = 1;
+    ws.W[0] = M;
+    ws.S[0] = S;
+    ws.base[0] = 0;
+    ws.total_slots = S;
+    const unsigned blocks = (unsigned)((max_warps + 3) / 4);
+    cudaError_t e = cudaMemsetAsync(counts, 0, sizeof(int64_t) * (size_t)n_bins * (size_t)n_hist, s);
+    if (e != cudaSuccess) return e;
+    if (blocks == 0) return cudaSuccess;
+    note_launch(3);
+    if (in_f64) k_xsvs_warp<double><<<blocks, 128, 0, s>>>((const double*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, ws, (double2*)warp_moments);
+    else k_xsvs_warp<float><<<blocks, 128, 0, s>>>((const float*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, ws, (double2*)warp_moments);
+    k_ring_snapshot_mean<<<n_bins, 256, 0, s>>>((const double2*)warp_moments, plan.offsets, plan.warp_off, S, S, n_bins, means);
+    if (in_f64) k_speckle_hist<double><<<blocks, 128, 0, s>>>((const double*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, M, S, means, n_hist, kappa_max, (unsigned long long*)counts);
+    else k_speckle_hist<float><<<blocks, 128, 0, s>>>((const float*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, M, S, means, n_hist, kappa_max, (unsigned long long*)counts);
+    return cudaGetLastError();
+}
+
 }  // namespace xpcs

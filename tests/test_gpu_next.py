@@ -132,3 +132,49 @@ def test_beta_q_space_equals_beta_time_and_superposition():
         assert abs(beta[0, b] - beta_t[b]) < 0.1
         for wi, M in enumerate(windows):
             assert abs(beta[wi, b] * M - beta0 * (1 - 2 / n_eff)) < 0.15, (b, M, beta[wi, b])
+
+
+def _hist_close(got, counts, amb):
+    """Exact integer counts; a value within 1e-9 of a bin edge e may sit on either side (different FP64 summation
+    order of the ring mean): allow moves between bins e-1 and e bounded by ambiguous[e]."""
+    d = got.astype(np.int64) - counts
+    if not d.any():
+        return
+    carry = np.zeros(d.shape[0], dtype=np.int64)
+    for e in range(d.shape[1]):
+        carry = carry + d[:, e]
+        assert np.all(np.abs(carry) <= amb[:, e + 1]), (e, d, amb)
+
+
+@pytest.mark.parametrize("M,n_hist,kmax", [(1, 40, 8.0), (3, 25, 5.0), (7, 1000, 3.0)])
+def test_speckle_histogram_reduction_parity(M, n_hist, kmax):
+    rng = np.random.default_rng(M)
+    T, n = 45, 96
+    I = rng.exponential(1.0, (T, n * n)).astype(np.float32) * 37.0
+    bins = oracle.lattice_bins(n, n_bins=16)
+    got = xp.xpcs_speckle_histogram(_t(I), _t(bins), 16, M, n_hist, kmax).cpu().numpy()
+    counts, amb = oracle.speckle_histogram(I, bins, 16, M, n_hist, kmax)
+    _hist_close(got, counts, amb)
+
+
+def test_erlang_statistics_on_gpu_outputs():
+    """PAPER.md:560-572 (Fig. 8 analogue): M independent ideal-gas patterns superposed -> Erlang(M) intensity law
+    (Eq. 38) and contrast 1/M, all from GPU outputs (I by the tensor engine, histogram and XSVS by the library)."""
+    from scipy import stats
+    cfg = xi.scaled(xi.CONFIGS["c4"], N=2000, T=40)
+    pos = xi.positions(cfg)
+    n = 128
+    I = xp.xpcs_intensity_grid(_t(pos), None, xp.qgrid(cfg.L, -n // 2, n, -n // 2, n))
+    bins_h = oracle.lattice_bins(n, n_bins=8)
+    bins_h[bins_h < 2] = -1
+    bins = _t(bins_h)
+    n_hist, kmax = 20, 4.0
+    edges = np.linspace(0, kmax, n_hist + 1)
+    for M in (1, 5, 10, 20):
+        got = xp.xpcs_speckle_histogram(I, bins, 8, M, n_hist, kmax).cpu().numpy().sum(0)
+        n_all = int((bins_h >= 0).sum()) * (cfg.T // M)
+        expect = n_all * np.diff(stats.gamma(a=M, scale=1.0 / M).cdf(edges))
+        assert np.all(np.abs(got - expect) <= 5 * np.sqrt(expect + 1) + 0.04 * expect), (M, got, expect)
+    beta = xp.xsvs_contrast(I, bins, 8, [1, 5, 10, 20]).cpu().numpy()
+    for wi, M in enumerate((1, 5, 10, 20)):
+        assert np.all(np.abs(beta[wi, 2:] * M - 1.0) < 0.12), (M, beta[wi])
