@@ -158,6 +158,20 @@ XPCS_API int xpcs_intensity_species(const void* positions, int64_t N, const xpcs
 XPCS_API int xpcs_amplitude_species(const void* positions, int64_t N, const xpcs_species* species,
                                     const void* q_vectors, int64_t n_q, int64_t frames, double box_L,
                                     void* A_out, const xpcs_opts* opts);
+/* Algorithm 2, the FFT-based method (a cross-check / second workload beside the direct method):
+ * rho^eta = sum_i of normalised Gaussians of width eta (Eq. 30) on an n_grid^3 grid of the periodic box, each evaluated
+ * on the k x k x k grid points nearest the atom (k = k_cut, or for k_cut <= 0 the paper's "nearest integer greater
+ * than 10 eta" in grid spacings, rounded up to odd: DESIGN.md R16); p^eta = FFT(rho^eta) (cuFFT,
+ * FP64); f^eta = the DFT of the truncated Gaussian centred at the origin; I = f(q)^2 |p^eta|^2 /
+ * f^eta^2 (Eq. 35).  Output: the axis-aligned block `block` of the FFT grid (block->plane.L is the box edge; m0 = 0,
+ * ma = x, mb = y, mc = z; every index in [-n_grid/2, n_grid/2 - 1]), order [frames][n_l][n_h][n_k] out_dtype.
+ *   positions [frames][N][3] in_dtype (wrapped into the box);  f_q DEVICE [n_l*n_h*n_k] in_dtype or NULL (f = 1).
+ * Deposits use FP64 atomics, so the last bits of rho (and of I) may differ between runs.
+ * Errors: EINVAL for null pointers, N/frames <= 0, a non-axis-aligned block or indices outside the grid, n_grid odd
+ *         or outside [8, 1024], eta <= 0, k even or > 31; ECUDA for CUDA/cuFFT failures. */
+XPCS_API int xpcs_intensity_fft(const void* positions, int64_t N, int64_t frames, const xpcs_qvolume* block,
+                                int32_t n_grid, double eta, int32_t k_cut, const void* f_q, void* I_out,
+                                const xpcs_opts* opts);
 /* Gaussian-sum form factor: f(q) = c + sum_{i < n_gauss} a_i exp(-b_i s^2), s = |q| / (4 pi),
  * evaluated in FP64 at an explicit q list (q_vectors DEVICE [n_q][3] in_dtype) or, if q_vectors is NULL, at every
  * q of the volume *vol (n_q ignored).  a, b HOST [n_gauss], 0 <= n_gauss <= 6.  f_out DEVICE [n_q] out_dtype.

@@ -26,7 +26,7 @@ EXPORTED = (
     "xpcs_profile_query", "xpcs_device_info", "xpcs_version", "xpcs_engine_available",
     "xpcs_amplitude", "xpcs_amplitude_grid", "xpcs_isf",
     "xpcs_intensity_volume", "xpcs_amplitude_volume", "xpcs_intensity_species", "xpcs_amplitude_species",
-    "xpcs_form_factor_gaussian", "xpcs_speckle_histogram",
+    "xpcs_form_factor_gaussian", "xpcs_speckle_histogram", "xpcs_intensity_fft",
 )
 
 
@@ -107,6 +107,7 @@ def load():
         "xpcs_amplitude_volume": [vp, i64, vp, ctypes.POINTER(Species), ctypes.POINTER(QVolume), i64, vp, op],
         "xpcs_intensity_species": [vp, i64, ctypes.POINTER(Species), vp, i64, i64, dbl, vp, op],
         "xpcs_amplitude_species": [vp, i64, ctypes.POINTER(Species), vp, i64, i64, dbl, vp, op],
+        "xpcs_intensity_fft": [vp, i64, i64, ctypes.POINTER(QVolume), i32, dbl, i32, vp, vp, op],
         "xpcs_speckle_histogram": [vp, i64, i64, vp, i32, i32, i32, dbl, vp, op],
         "xpcs_form_factor_gaussian": [vp, i64, ctypes.POINTER(QVolume), i32, ctypes.POINTER(ctypes.c_double),
                                       ctypes.POINTER(ctypes.c_double), dbl, vp, op],
@@ -364,6 +365,23 @@ def xsvs_contrast(I, bins, n_bins, windows, out=None, stream=None, profile=False
     o = make_opts(_dtype_code(I), F64, stream, ENGINE_AUTO, profile)
     _check(load().xsvs_contrast(_ptr(I), T, n_q, _ptr(bins), int(n_bins), w_p, len(w_arr), _ptr(out),
                                 ctypes.byref(o)))
+    return out
+
+
+def xpcs_intensity_fft(positions, block: QVolume, n_grid, eta, k_cut=0, f_q=None, out=None, out_dtype=None,
+                       stream=None, profile=False):
+    """Algorithm 2 (FFT method): I on an axis-aligned block of the n_grid^3 FFT grid -> [T][n_l * n_h * n_k]."""
+    import torch
+    positions = _positions3(positions)
+    T, N = positions.shape[0], positions.shape[1]
+    ind = _dtype_code(positions)
+    outd = ind if out_dtype is None else out_dtype
+    if out is None:
+        out = torch.empty((T, block.n_q), dtype=torch.float64 if outd == F64 else torch.float32,
+                          device=positions.device)
+    o = make_opts(ind, outd, stream, ENGINE_AUTO, profile)
+    _check(load().xpcs_intensity_fft(_ptr(positions), N, T, ctypes.byref(block), int(n_grid), float(eta), int(k_cut),
+                                     _ptr(f_q), _ptr(out), ctypes.byref(o)))
     return out
 
 

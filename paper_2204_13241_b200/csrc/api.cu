@@ -146,6 +146,7 @@ int64_t xpcs_launch_count(void) { return (int64_t)launches(); }
 
 int xpcs_release(void) {
     clear_error();
+    fft_release_plan();
     release_scratch();
     return check_sticky();
 }
@@ -454,7 +455,8 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
     // atom chunks (split-K over CTAs, folded in FP64 by the reduction): SIMT keeps fp32 register sums short
     // (<= 4096 atoms) and splits further (>= 512 atoms per chunk) when tiles x frames cannot fill ~2 waves; the
     // tensor engine drains TMEM every 256 atoms into RN sums, so its chunks only balance the grid (>= ~8 waves of
-    // one CTA per SM) and stay >= 1024 atoms (>= 256 when the grid is small: few tiles, few frames).
+    // one CTA per SM) and stay >= 1024 atoms; for the default (tensor) engine the chunking of a call with >= 64
+    // frames does not depend on the frame count, so batching frames differently gives bit-identical results.
     std::vector<int64_t> chunk(ng, 4096), C(ng, 0);
     int64_t sumC = 0;
     for (int gi = 0; gi < ng; ++gi) {
@@ -465,8 +467,7 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
             const int64_t tiles = ((g.n_h + 127) / 128) * ((g.n_k + 127) / 128);
             const int64_t units = tiles * std::min<int64_t>(V, 64);
             int64_t C0 = std::max<int64_t>(1, (8LL * sm_count() + units - 1) / units);
-            const int64_t min_chunk = units >= sm_count() ? 1024 : 256;
-            C0 = std::min<int64_t>(C0, std::max<int64_t>(1, Ng / min_chunk));
+            C0 = std::min<int64_t>(C0, std::max<int64_t>(1, Ng / 1024));
             ch = ((Ng + C0 - 1) / C0 + 15) / 16 * 16;
         } else {
             const int64_t units = ((g.n_h + 63) / 64) * ((g.n_k + 127) / 128) * V;
@@ -561,6 +562,76 @@ int xpcs_intensity_volume(const void* positions, int64_t N, const void* form_fac
 int xpcs_amplitude_volume(const void* positions, int64_t N, const void* form_factors, const xpcs_species* species,
                           const xpcs_qvolume* vol, int64_t frames, void* A_out, const xpcs_opts* opts) {
     return run_volume(positions, N, form_factors, species, vol, frames, A_out, opts, 1);
+}
+
+int xpcs_intensity_fft(const void* positions, int64_t N, int64_t frames, const xpcs_qvolume* block, int32_t n_grid,
+                       double eta, int32_t k_cut, const void* f_q, void* I_out, const xpcs_opts* opts) {
+    clear_error();
+    Opts o;
+    TRY(parse_opts(opts, o));
+    NEED(positions, "positions");
+    NEED(I_out, "I_out");
+    POS(N, "N");
+    POS(frames, "frames");
+    TRY(validate_volume(block));
+    const xpcs_qgrid& pl = block->plane;
+    const bool axes = pl.m0[0] == 0 && pl.m0[1] == 0 && pl.m0[2] == 0 && pl.ma[0] == 1 && pl.ma[1] == 0 &&
+                      pl.ma[2] == 0 && pl.mb[0] == 0 && pl.mb[1] == 1 && pl.mb[2] == 0 && block->mc[0] == 0 &&
+                      block->mc[1] == 0 && block->mc[2] == 1;
+    if (!axes) {
+        set_error("xpcs: the FFT method returns an axis-aligned block of its grid (m0 = 0, ma = x, mb = y, mc = z)");
+        return XPCS_EINVAL;
+    }
+    if (n_grid < 8 || n_grid > 1024 || (n_grid & 1)) {
+        set_error("xpcs: n_grid must be even and in [8, 1024] (got %d)", n_grid);
+        return XPCS_EINVAL;
+    }
+    if (!(eta > 0.0) || !std::isfinite(eta)) {
+        set_error("xpcs: eta must be finite and > 0");
+        return XPCS_EINVAL;
+    }
+    const double L = pl.L;
+    int k = k_cut;
+    if (k <= 0) {   // the paper's rule: the nearest integer greater than 10 eta (grid units), made odd (R16)
+        const double kk = std::floor(10.0 * eta / (L / n_grid)) + 1.0;
+        k = kk > 64.0 ? 65 : (int)kk;
+        if (!(k & 1)) ++k;
+    }
+    if (!(k & 1) || k > 31 || k > n_grid) {
+        set_error("xpcs: the kernel width k must be odd, <= 31 and <= n_grid (got %d)", k);
+        return XPCS_EINVAL;
+    }
+    const int64_t lo = -(int64_t)(n_grid / 2), hi = n_grid / 2 - 1;
+    if (pl.h0 < lo || pl.h0 + pl.n_h - 1 > hi || pl.k0 < lo || pl.k0 + pl.n_k - 1 > hi || block->l0 < lo ||
+        block->l0 + block->n_l - 1 > hi) {
+        set_error("xpcs: block indices must lie in [-n_grid/2, n_grid/2 - 1]");
+        return XPCS_EINVAL;
+    }
+    TRY(check_sticky());
+    const int64_t n3 = (int64_t)n_grid * n_grid * n_grid;
+    const int64_t per_frame = 8 * n3 + 16 * (int64_t)n_grid * n_grid * (n_grid / 2 + 1);
+    const int64_t Tb = std::max<int64_t>(1, std::min<int64_t>(frames, (int64_t)(2 * kBatchBytes) / per_frame));
+    char* buf = (char*)scratch(o.s, SS_FFT, (size_t)(per_frame * Tb) + 256);
+    if (!buf) return XPCS_ENOMEM;
+    double* rho = (double*)buf;
+    double2* spec = (double2*)(buf + ((8 * n3 * Tb + 255) / 256) * 256);
+    const int64_t blk = block->n_l * pl.n_h * pl.n_k;
+    const size_t psz = o.in_f64 ? 24 : 12;
+    for (int64_t t0 = 0; t0 < frames; t0 += Tb) {
+        const int64_t tb = std::min(Tb, frames - t0);
+        const char* what = "";
+        ProfScope p(o.profile, KC_MAIN, o.s);
+        const int rc = launch_fft_intensity((const char*)positions + psz * N * t0, o.in_f64, N, tb, L, n_grid, eta, k,
+                                            rho, spec, pl.h0, pl.n_h, pl.k0, pl.n_k, block->l0, block->n_l, f_q,
+                                            o.in_f64, (char*)I_out + out_size(o.out_f64) * blk * t0, o.out_f64, o.s,
+                                            &what);
+        if (rc == 2) return cuda_fail(cudaGetLastError(), what);
+        if (rc == 3) {
+            set_error("xpcs: cuFFT %s failed", what);
+            return XPCS_ECUDA;
+        }
+    }
+    return XPCS_OK;
 }
 
 int xpcs_form_factor_gaussian(const void* q_vectors, int64_t n_q, const xpcs_qvolume* vol, int32_t n_gauss,

@@ -16,7 +16,7 @@ void note_launch(int n = 1);
 
 // Scratch cached per (stream, slot); grown on demand (the grow synchronises the device).
 enum ScratchSlot {
-    SS_STAGE = 0, SS_PARTIAL, SS_PLAN, SS_PLAN2, SS_XSVS, SS_SMALL, SS_LAGS, SS_TC, SS_IDX, SS_COUNT
+    SS_STAGE = 0, SS_PARTIAL, SS_PLAN, SS_PLAN2, SS_XSVS, SS_SMALL, SS_LAGS, SS_TC, SS_IDX, SS_FFT, SS_COUNT
 };
 void* scratch(cudaStream_t s, int slot, size_t bytes);   // nullptr on failure (error already set)
 void release_scratch();
@@ -132,6 +132,13 @@ struct SpeciesParts {
 };
 cudaError_t launch_species_combine(const SpeciesParts& sp, int64_t frames, int64_t n_q, const void* fq, int fq_f64,
                                    int64_t v0, int64_t n_l, void* out, int out_f64, int mode, cudaStream_t s);
+// Algorithm 2 (FFT method): spread + cuFFT D2Z + epilogue for `frames` frames; rho [frames][n^3] double, spec
+// [frames][n][n][n/2+1] double2 scratch.  Returns 0, 2 (CUDA error) or 3 (cuFFT error); *what names the step.
+int launch_fft_intensity(const void* pos, int pos_f64, int64_t N, int64_t frames, double L, int n, double eta, int k,
+                         double* rho, double2* spec, int64_t h0, int64_t n_h, int64_t k0, int64_t n_k, int64_t l0,
+                         int64_t n_l, const void* fq, int fq_f64, void* out, int out_f64, cudaStream_t s,
+                         const char** what);
+cudaError_t fft_release_plan();
 // f(q) = c + sum_i a_i exp(-b_i (|q| / 4 pi)^2) for an explicit q list (q != nullptr) or a 3-D lattice block
 cudaError_t launch_form_factor_gaussian(const void* q, int q_f64, int64_t n_q, const LatticeGeom& g, int64_t l0,
                                         int64_t n_l, const int32_t* mc, int n_gauss, const double* a, const double* b,

@@ -119,3 +119,23 @@ def test_volume_species_validation_before_launch(lib):
     rc = lib.xpcs_form_factor_gaussian(None, 5, None, 1, a, a, 0.0, dummy, ctypes.byref(o))
     assert rc == _lib.XPCS_EINVAL
     assert lib.xpcs_launch_count() == n0
+
+
+def test_fft_method_validation(lib):
+    n0 = lib.xpcs_launch_count()
+    o = _lib.Opts(0, 0, None, 0, 0)
+    dummy = ctypes.c_void_p(16)
+    ok = xp.qvolume(10.0, -4, 8, -4, 8, -2, 5)
+    tilted = xp.qvolume(10.0, -4, 8, -4, 8, -2, 5, mb=(0, 1, 1))
+    rc = lib.xpcs_intensity_fft(dummy, 10, 1, ctypes.byref(tilted), 32, 0.3, 0, None, dummy, ctypes.byref(o))
+    assert rc == _lib.XPCS_EINVAL and b"axis-aligned" in lib.xpcs_last_error()
+    rc = lib.xpcs_intensity_fft(dummy, 10, 1, ctypes.byref(ok), 33, 0.3, 0, None, dummy, ctypes.byref(o))
+    assert rc == _lib.XPCS_EINVAL and b"n_grid" in lib.xpcs_last_error()
+    rc = lib.xpcs_intensity_fft(dummy, 10, 1, ctypes.byref(ok), 32, 0.3, 10, None, dummy, ctypes.byref(o))
+    assert rc == _lib.XPCS_EINVAL and b"odd" in lib.xpcs_last_error()
+    wide = xp.qvolume(10.0, -5, 8, -4, 8, -2, 5)
+    rc = lib.xpcs_intensity_fft(dummy, 10, 1, ctypes.byref(wide), 8, 0.3, 0, None, dummy, ctypes.byref(o))
+    assert rc == _lib.XPCS_EINVAL and b"block indices" in lib.xpcs_last_error()
+    rc = lib.xpcs_intensity_fft(dummy, 10, 1, ctypes.byref(ok), 32, -1.0, 0, None, dummy, ctypes.byref(o))
+    assert rc == _lib.XPCS_EINVAL and b"eta" in lib.xpcs_last_error()
+    assert lib.xpcs_launch_count() == n0
