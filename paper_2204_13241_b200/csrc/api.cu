@@ -455,8 +455,8 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
     // atom chunks (split-K over CTAs, folded in FP64 by the reduction): SIMT keeps fp32 register sums short
     // (<= 4096 atoms) and splits further (>= 512 atoms per chunk) when tiles x frames cannot fill ~2 waves; the
     // tensor engine drains TMEM every 256 atoms into RN sums, so its chunks only balance the grid (>= ~8 waves of
-    // one CTA per SM) and stay >= 1024 atoms; for the default (tensor) engine the chunking of a call with >= 64
-    // frames does not depend on the frame count, so batching frames differently gives bit-identical results.
+    // one CTA per SM) and stay >= 1024 atoms.  The chunking depends on the frame count of the call only through the
+    // grid-fill rule (when the 1024-atom floor binds, splitting the frames over several calls is bit-identical).
     std::vector<int64_t> chunk(ng, 4096), C(ng, 0);
     int64_t sumC = 0;
     for (int gi = 0; gi < ng; ++gi) {
