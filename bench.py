@@ -181,7 +181,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2", choices=sorted(xi.CONFIGS))
-    ap.add_argument("--engine", default="auto", choices=["auto", "simt", "tensor"])
+    ap.add_argument("--engine", default="auto", choices=["auto", "simt", "tensor", "i8"])
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--ref-pixels", type=int, default=4096)
     ap.add_argument("--cpu-budget", type=float, default=12.0)
@@ -206,7 +206,8 @@ def main():
     cfg_r = xi.scaled(cfg, seed=xd.trajectory_seed(cfg.seed, rank)) if rank else cfg
     pos_h = xi.positions(cfg_r)
     f_h = xi.form_factors(cfg_r) if cfg.two_species else None
-    engine = {"auto": xp.ENGINE_AUTO, "simt": xp.ENGINE_SIMT, "tensor": xp.ENGINE_TENSOR}[args.engine]
+    engine = {"auto": xp.ENGINE_AUTO, "simt": xp.ENGINE_SIMT, "tensor": xp.ENGINE_TENSOR,
+              "i8": xp.ENGINE_TENSOR_I8}[args.engine]
     wl = pipeline.workload_from_config(cfg, device=dev)
     wl.engine = engine
     P = pipeline.Pipeline(wl, device=dev)
@@ -249,11 +250,19 @@ def main():
     sm_count, _ = xp.device_info()
     tc_used = bool(cfg.n_plane) and wl.in_dtype == xp.F32 and engine != xp.ENGINE_SIMT and \
         xp.engine_available(xp.ENGINE_TENSOR)
+    i8_used = tc_used and xp.engine_resolved(engine, f_h is None) == xp.ENGINE_TENSOR_I8
     if cfg.n_plane == 0:
         # generic q: 2 XU (MUFU) ops per pair; peak = 148 SM x 16 XU/clk x max clock
         peak = sm_count * 16 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 2 / 1e12
         roof = {"bound": "alu", "unit": "Tpairs/s (XU: 2 MUFU per pair)", "peak": peak,
                 "achieved": pairs_launch / (per_launch_ms / 1e3) / 1e12}
+    elif i8_used:
+        # tcgen05 kind::i8: 3 int8 limb products x 4 real MAC = 24 int8 ops per pair vs the int8 dense peak =
+        # 2 x the measured bf16 (= fp16) peak (B200: 4.5 POPS int8 vs 2.25 PFLOP/s fp16 nominal; tools/mma_rate.cu
+        # measured 8192 vs 4096 MAC/clk/SM)
+        peak = 2.0 * peaks["bf16_tflops_sustained"]
+        roof = {"bound": "tensor", "unit": "TOPS (int8)", "peak": peak,
+                "achieved": 24.0 * pairs_launch / (per_launch_ms / 1e3) / 1e12}
     elif tc_used:
         # tcgen05 split-FP16: 3 fp16 products x 4 real MAC = 24 flop per pair vs measured bf16 (= fp16) dense peak
         peak = peaks["bf16_tflops_sustained"]
@@ -265,7 +274,8 @@ def main():
         roof = {"bound": "alu", "unit": "TFLOP/s (FP32 FMA pipe)", "peak": peak,
                 "achieved": 8.0 * pairs_launch / (per_launch_ms / 1e3) / 1e12}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = _traffic(cfg.name, "tensor" if tc_used else ("simt" if cfg.n_plane else "generic"), pairs_launch)
+    eng_name = "i8" if i8_used else ("tensor" if tc_used else ("simt" if cfg.n_plane else "generic"))
+    roof["traffic"] = _traffic(cfg.name, eng_name, pairs_launch)
     roof["peak_source"] = peak_src if roof["bound"] == "tensor" else "derived (DESIGN.md)"
     roof["kernel_ms"] = per_launch_ms
     roof["kernel_share_of_step"] = main_ms / args.steps / ms if ms > 0 else None
@@ -304,7 +314,7 @@ def main():
                 "config": {"workload": cfg.name, "N": cfg.N, "n_q": P.n_q, "frames": cfg.T,
                            "lags": len(cfg.lags), "windows": list(cfg.windows), "rings": cfg.n_bins,
                            "pairs_per_step_per_gpu": pairs_step, "engine": args.engine,
-                           "engine_used": "tensor" if tc_used else ("simt" if cfg.n_plane and wl.in_dtype == xp.F32 else "generic/f64"),
+                           "engine_used": eng_name if cfg.n_plane and wl.in_dtype == xp.F32 else "generic/f64",
                            "l2": "flushed between timed steps (256 MB write, untimed)",
                            "parallelism": f"weak x{ws} (independent trajectories)"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(n_launch),

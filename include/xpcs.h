@@ -40,10 +40,15 @@ typedef enum {
 
 typedef enum { XPCS_F32 = 0, XPCS_F64 = 1 } xpcs_dtype;
 
-/* Which kernel family evaluates a lattice-grid contraction (xpcs_intensity_grid, f32 only).
- * AUTO picks the fastest available engine; SIMT = FP32 CUDA-core factorised kernel; TENSOR = tcgen05
- * split-precision kernel.  The generic q-list path ignores this field. */
-typedef enum { XPCS_ENGINE_AUTO = 0, XPCS_ENGINE_SIMT = 1, XPCS_ENGINE_TENSOR = 2 } xpcs_engine;
+/* Which kernel family evaluates a lattice-grid contraction (xpcs_intensity_grid / _volume, f32 only).
+ * AUTO picks the fastest available engine that meets the north_star tolerance for the call: TENSOR_I8 when
+ * form_factors is NULL (f = 1, and every kind of a species call), TENSOR for per-atom form factors, SIMT without
+ * tcgen05 (XPCS_DISABLE_TC=1); SIMT = FP32 CUDA-core
+ * factorised kernel; TENSOR = tcgen05 split-FP16 kernel (FP32-class products, per-pixel |dI| ~ 1e-4 N at most);
+ * TENSOR_I8 = tcgen05 integer kernel (two int8 limbs per phasor component, exact int32 accumulation; per-pixel
+ * rms |dI| ~ 3e-5 N (f = 1), W scaled by max |f_j| for per-atom form factors).  The generic q-list path ignores
+ * this field. */
+typedef enum { XPCS_ENGINE_AUTO = 0, XPCS_ENGINE_SIMT = 1, XPCS_ENGINE_TENSOR = 2, XPCS_ENGINE_TENSOR_I8 = 3 } xpcs_engine;
 
 typedef struct {
     int32_t in_dtype;   /* xpcs_dtype of positions / form factors / q vectors, or of the intensity series fed to

@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("XPCS_LIB", os.path.join(_HERE, "lib", "libxpcs.so")) 
 
 XPCS_OK, XPCS_EINVAL, XPCS_ECUDA, XPCS_ENOMEM, XPCS_EUNSUPPORTED = 0, 1, 2, 3, 4
 F32, F64 = 0, 1
-ENGINE_AUTO, ENGINE_SIMT, ENGINE_TENSOR = 0, 1, 2
+ENGINE_AUTO, ENGINE_SIMT, ENGINE_TENSOR, ENGINE_TENSOR_I8 = 0, 1, 2, 3
 KERNEL_CLASSES = ("intensity_main", "stage", "amplitude_reduce", "g2", "xsvs", "rings")
 
 EXPORTED = (
@@ -443,6 +443,19 @@ def xpcs_radial_bins(q, q_max, n_bins, stream=None):
     o = make_opts(_dtype_code(q), F32, stream)
     _check(load().xpcs_radial_bins(_ptr(q), q.shape[0], float(q_max), int(n_bins), _ptr(out), ctypes.byref(o)))
     return out
+
+
+def engine_resolved(engine, uniform_f=True) -> int:
+    """The engine a lattice f32 call with this opts.engine runs (mirrors api.cu): AUTO -> the integer tensor engine
+    for uniform form factors, the split-FP16 tensor engine otherwise; SIMT when tcgen05 is unavailable."""
+    if engine == ENGINE_SIMT or not engine_available(ENGINE_TENSOR):
+        return ENGINE_SIMT
+    if engine == ENGINE_AUTO:
+        return ENGINE_TENSOR_I8 if (uniform_f and AUTO_I8) else ENGINE_TENSOR
+    return engine
+
+
+AUTO_I8 = True    # AUTO routes uniform-f lattice calls to the integer engine (mirrors api.cu)
 
 
 def launch_count() -> int:

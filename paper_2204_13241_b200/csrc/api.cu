@@ -34,7 +34,7 @@ int parse_opts(const xpcs_opts* o, Opts& out) {
             set_error("xpcs: unknown dtype (in_dtype=%d, out_dtype=%d)", o->in_dtype, o->out_dtype);
             return XPCS_EINVAL;
         }
-        if (o->engine < XPCS_ENGINE_AUTO || o->engine > XPCS_ENGINE_TENSOR) {
+        if (o->engine < XPCS_ENGINE_AUTO || o->engine > XPCS_ENGINE_TENSOR_I8) {
             set_error("xpcs: unknown engine %d", o->engine);
             return XPCS_EINVAL;
         }
@@ -173,9 +173,9 @@ int xpcs_device_info(int32_t* sm, int32_t* clk) {
 }
 
 int xpcs_engine_available(int32_t engine) {
-    if (engine == XPCS_ENGINE_SIMT) return 1;
+    if (engine == XPCS_ENGINE_SIMT || engine == XPCS_ENGINE_AUTO) return 1;
     LatticeGeom g{};
-    if (engine == XPCS_ENGINE_TENSOR || engine == XPCS_ENGINE_AUTO) return lattice_tc_supported(g) ? 1 : (engine == XPCS_ENGINE_AUTO);
+    if (engine == XPCS_ENGINE_TENSOR || engine == XPCS_ENGINE_TENSOR_I8) return lattice_tc_supported(g) ? 1 : 0;
     return 0;
 }
 
@@ -403,17 +403,22 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
     const int64_t n_l = vol->n_l, l0 = vol->l0;
     const int64_t V = frames * n_l;             // virtual frames: (frame, l-plane), row-major = output order
     const size_t isz = out_size(o.out_f64) * (amp ? 2 : 1);
-    if (o.in_f64 && o.engine == XPCS_ENGINE_TENSOR) {
-        set_error("xpcs: the tensor engine needs f32 inputs");
+    if (o.in_f64 && (o.engine == XPCS_ENGINE_TENSOR || o.engine == XPCS_ENGINE_TENSOR_I8)) {
+        set_error("xpcs: the tensor engines need f32 inputs");
         return XPCS_EUNSUPPORTED;
     }
-    bool tc = false;
-    if (!o.in_f64 && (o.engine == XPCS_ENGINE_TENSOR || o.engine == XPCS_ENGINE_AUTO)) {
-        tc = lattice_tc_supported(g);
-        if (!tc && o.engine == XPCS_ENGINE_TENSOR) {
+    bool tc = false, i8 = false;
+    if (!o.in_f64 && o.engine != XPCS_ENGINE_SIMT) {
+        const bool avail = lattice_tc_supported(g);
+        if (!avail && o.engine != XPCS_ENGINE_AUTO) {
             set_error("xpcs: the tensor engine is not available for this grid/build");
             return XPCS_EUNSUPPORTED;
         }
+        // AUTO: the integer engine when every atom has f = 1 inside the contraction (form_factors NULL: uniform f, and
+        // every kind of a species call); per-atom f keeps the split-FP16 engine (the W scale max|f| costs the small-f
+        // atoms limb precision: two-species worst case ~0.8 of the per-pixel gate)
+        i8 = avail && (o.engine == XPCS_ENGINE_TENSOR_I8 || (o.engine == XPCS_ENGINE_AUTO && form_factors == nullptr));
+        tc = avail && !i8;
     }
     TRY(upload_groups(G, o.s));
     const int ng = G.count();
@@ -463,7 +468,24 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
         const int64_t Ng = G.cnt[gi];
         if (Ng == 0) continue;
         int64_t ch = 4096;
-        if (tc) {
+        if (i8) {
+            // exact int32 accumulation: chunks only balance the grid (clusters of 2 CTAs, one CTA per SM) and stay
+            // <= kI8MaxChunk; among C in [C0/2, 2 C0] pick the fewest wave-quantisation losses
+            const int64_t units = ((g.n_h + 255) / 256) * ((g.n_k + 127) / 128) * V;
+            const int64_t wave = std::max<int64_t>(1, sm_count() / 2);
+            const int64_t cmin = std::max<int64_t>(1, (Ng + kI8MaxChunk - 1) / kI8MaxChunk);
+            const int64_t cmax = std::max<int64_t>(cmin, std::min<int64_t>((Ng + 1023) / 1024, 64));
+            const int64_t C0 = std::min(cmax, std::max(cmin, (8 * wave + units - 1) / units));
+            int64_t best = C0;
+            double best_eff = -1.0;
+            for (int64_t c = std::max(cmin, C0 / 2); c <= std::min(cmax, 2 * C0); ++c) {
+                const double w = (double)(units * c) / (double)wave;
+                const double eff = w / std::ceil(w) - 0.004 * (double)c;   // mild preference for fewer, longer CTAs
+                if (eff > best_eff) { best_eff = eff; best = c; }
+            }
+            ch = ((Ng + best - 1) / best + 31) / 32 * 32;
+            ch = std::min<int64_t>(ch, kI8MaxChunk);
+        } else if (tc) {
             const int64_t tiles = ((g.n_h + 127) / 128) * ((g.n_k + 127) / 128);
             const int64_t units = tiles * std::min<int64_t>(V, 64);
             int64_t C0 = std::max<int64_t>(1, (8LL * sm_count() + units - 1) / units);
@@ -487,8 +509,13 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
     uint4* st = (uint4*)scratch(o.s, SS_STAGE, sizeof(uint4) * (size_t)(N * Tb));
     float2* part = (float2*)scratch(o.s, SS_PARTIAL, sizeof(float2) * (size_t)(sumC * n_q * Tb));
     if (!st || !part) return XPCS_ENOMEM;
-    // the tensor engine's partials hold conj(p) (R1)
-    const int mode = amp ? (tc ? 2 : 1) : 0;
+    float* fmax = nullptr;
+    if (i8 && form_factors) {
+        fmax = (float*)scratch(o.s, SS_SMALL, 64);
+        if (!fmax) return XPCS_ENOMEM;
+    }
+    // the tensor engines' partials hold conj(p) (R1)
+    const int mode = amp ? ((tc || i8) ? 2 : 1) : 0;
     for (int64_t v0 = 0; v0 < V; v0 += Tb) {
         const int64_t vb = std::min(Tb, V - v0);
         int64_t stoff = 0, poff = 0;
@@ -501,7 +528,9 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
             { ProfScope p(o.profile, KC_STAGE, o.s);
               TRY(cuda_fail(launch_stage_lattice32(positions, 0, form_factors, 0, Ng, vb, g, m, st + stoff, o.s), "stage")); }
             { ProfScope p(o.profile, KC_MAIN, o.s);
-              if (tc) TRY(cuda_fail(launch_lattice_tc(st + stoff, Ng, vb, g, chunk[gi], C[gi], part + poff, o.s), "lattice tcgen05"));
+              if (i8) TRY(cuda_fail(launch_lattice_i8(st + stoff, Ng, vb, g, chunk[gi], C[gi], fmax, form_factors == nullptr,
+                                                      part + poff, o.s), "lattice tcgen05 i8"));
+              else if (tc) TRY(cuda_fail(launch_lattice_tc(st + stoff, Ng, vb, g, chunk[gi], C[gi], part + poff, o.s), "lattice tcgen05"));
               else TRY(cuda_fail(launch_lattice_simt(st + stoff, Ng, vb, g, chunk[gi], C[gi], part + poff, o.s), "lattice simt")); }
             stoff += Ng * vb;
             poff += C[gi] * n_q * vb;

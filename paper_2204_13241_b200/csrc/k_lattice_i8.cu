@@ -1,0 +1,436 @@
+// k_lattice_i8.cu -- K3b: lattice-plane amplitude on the tcgen05 INTEGER tensor cores (kind::i8, exact int32
+// accumulation in TMEM), the fast engine for uniform form factors.
+//
+// Same factorisation as k_lattice_tc.cu (Eq. 7, on a reciprocal-lattice plane):
+//     p^e(h,k) = sum_j X_h(j) W_k(j),  X_h = e^{-2 pi i h Th_a(j)},  W_k = (f_j / F) e^{-2 pi i (Th_0 + k Th_b)(j)}
+// with F = max_j |f_j|.  Every phasor component v in [-1, 1] is written as two int8 limbs
+//     v ~ (254 hi + lo) / 32258,  hi = rint(127 v) in [-127, 127],  lo = rint(254 (127 v - hi)) in [-127, 127]
+// (|error| <= 1 / 64516 = 1.55e-5; both limbs always fit: |254 (127 v - hi)| <= 127 exactly), so each real product is
+//     v w ~ [64516 hi.hi' + 254 (hi.lo' + lo.hi')] / 32258^2      (the dropped lo.lo' term is < 1.6e-5)
+// i.e. three int8 MMAs into two TMEM accumulators, HH = sum hi.hi' and X = sum (hi.lo' + lo.hi').  The integer
+// accumulation is EXACT (no TMEM rounding, unlike the FP32 accumulator of the split-FP16 engine), so
+// a chunk of up to 32768 atoms (int32 overflow bound: 4 x 127^2 x 32768 < 2^31) accumulates in TMEM and is drained
+// once; the result carries only the limb quantisation error (rms |dI| ~ 3e-5 N per pixel for f = 1).
+// The int8 tensor rate is twice the fp16 rate on sm_100a (measured 8192 vs 4096 MAC/clk/SM, tools/mma_rate.cu).
+//
+// CTA pair (cluster of 2, cta_group::2): 256 (h) x 128 (k) pixel tile, M = 256, N = 256 ([Re | Im'] of 64 k per CTA
+// half, B rows [-Ws | Wr | Ws]), K = 32 atoms per stage, 6 MMAs per stage:
+//     HH += Xr_hi.B1_hi + Xs_hi.B2_hi,   X += Xr_hi.B1_lo + Xr_lo.B1_hi + Xs_hi.B2_lo + Xs_lo.B2_hi
+// (B1 = [Wr | Ws], B2 = [-Ws | Wr]: D = [Re | Im'], Im' = -Im; the partials hold conj(p) like the fp16 engine).
+//
+// Producers: 3 groups of 6 warps; group g fills stages i = g mod 3 (6-stage ring, 28 KB per stage).  A warp thread
+// owns 4 consecutive atoms (one 32-bit word per row and limb plane) and 8 rows spaced 8 apart (X or W), and walks
+// the rows with the angle-addition recurrence X_{m+8} = X_m X_8 (packed FP32x2, 2 ops per phasor; 2 SFU sincos per
+// atom per thread), quantises with magic-number rounding (3 packed ops per phasor) and packs limb bytes with PRMT.
+// Lanes (quad qq, row mr) write 32 distinct banks per store.  After the last stage, warps 0-3 (one per TMEM lane
+// quarter) wait for the final MMA commit and drain both accumulators: p = (64516 HH + 254 X) F / 32258^2.
+#include "common.cuh"
+
+namespace xpcs {
+
+namespace ti8 {
+constexpr int TM = 128, TN = 128, KS = 32;          // rows (h) per CTA, pair tile cols (k), atoms per stage
+constexpr int PAIR_M = 2 * TM;
+constexpr int BN = TN / 2;                          // k rows of B per CTA
+constexpr int APLANE = TM * KS;                     // int8 A plane: 128 rows x 32 atoms = 4 KB
+constexpr int BROWS = 3 * BN;                       // [-Ws | Wr | Ws]
+constexpr int BPLANE = BROWS * KS;                  // 6 KB
+constexpr int STAGE_BYTES = 4 * APLANE + 2 * BPLANE;   // Xr_hi Xr_lo Xs_hi Xs_lo | B_hi B_lo = 28 KB
+constexpr int STAGES = 6;
+#ifndef XPCS_I8_GROUPS
+#define XPCS_I8_GROUPS 3
+#endif
+constexpr int NGROUPS = XPCS_I8_GROUPS, GROUP_WARPS = 6;   // per group: 4 X warps (2 quad halves x 2 row halves), 2 W warps
+constexpr int NPROD_WARPS = NGROUPS * GROUP_WARPS;  // 18
+constexpr int MMA_WARP = NPROD_WARPS;               // warps 0-3 (distinct TMEM lane quarters) also drain the tile
+constexpr int NTHREADS = (MMA_WARP + 1) * 32;       // 608
+constexpr int MMA_N = 2 * TN;                       // 256
+constexpr int TMEM_COLS = 512;                      // HH cols [0, 256), X cols [256, 512)
+constexpr int ASL = 4;                              // atom-record slots per group (cp.async prefetch distance ASL - 1)
+constexpr int ASLOT_BYTES = NGROUPS * ASL * KS * 16;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + ASLOT_BYTES + 1024 + 256;
+constexpr float MAGIC = 12582912.0f;                // 1.5 * 2^23
+}  // namespace ti8
+
+namespace {
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void i8_mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void i8_mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WI8_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WI8_%=;\n\t}" ::"r"(su32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void i8_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ uint32_t i8_mapa(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ uint32_t i8_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void i8_cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint64_t i8_desc(uint32_t saddr) {
+    // K-major, no swizzle: core matrix 8 rows x 16 B; LBO = 128 B (K-adjacent core matrices), SBO = 256 B (8-row groups)
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((128u >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((256u >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    return d;
+}
+// kind::i8 instruction descriptor: D s32 (2), A/B signed int8 (1), K-major, N = 256, M = 256 (cta_group::2)
+constexpr uint32_t kIdescI8 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(ti8::MMA_N >> 3) << 17) |
+                              ((uint32_t)(ti8::PAIR_M >> 4) << 24);
+__device__ __forceinline__ void umma2_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(kIdescI8), "r"(acc));
+}
+__device__ __forceinline__ void i8_commit_both(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+            su32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void i8_cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void i8_named_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ unsigned long long f2mul(unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ unsigned long long f2add(unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ unsigned long long swap2(unsigned long long v) { return (v >> 32) | (v << 32); }
+
+// (c, s) -> limb magic floats: t1 = M + hi (low byte = hi), t2 = M + lo (low byte = lo), element-wise on (c, s).
+// u = M - 254 hi is exact (an integer < 2^24); t2 = fl(32258 v + u) rounds once to the integer grid of M, so
+// t2 = M + rint(32258 v - 254 hi) = M + lo with |lo| <= 127 (|32258 v - 254 hi| = 254 |127 v - hi| <= 127).
+__device__ __forceinline__ void quantise(unsigned long long v, unsigned long long& t1, unsigned long long& t2) {
+    t1 = ffma2(v, pack2(127.0f, 127.0f), pack2(ti8::MAGIC, ti8::MAGIC));          // M + rint(127 v)
+    const unsigned long long u = ffma2(t1, pack2(-254.0f, -254.0f),
+                                       pack2(255.0f * ti8::MAGIC, 255.0f * ti8::MAGIC));   // = M - 254 hi (exact)
+    t2 = ffma2(v, pack2(32258.0f, 32258.0f), u);                                  // M + lo
+}
+// low bytes of four 32-bit words -> one word (byte t = atom t)
+__device__ __forceinline__ uint32_t pack_bytes(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
+}
+// per-byte two's-complement negation of four int8 in [-127, 127]
+__device__ __forceinline__ uint32_t neg_bytes(uint32_t w) {
+    const uint32_t n = ~w;
+    return ((n & 0x7F7F7F7Fu) + 0x01010101u) ^ (n & 0x80808080u);
+}
+template <int OFF>
+__device__ __forceinline__ void i8_sts(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.b32 [%0+%2], %1;" ::"r"(addr), "r"(v), "n"(OFF));
+}
+
+#define I8_TMEM_LD16(taddr, r)                                                                                     \
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),  \
+                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),        \
+                   "=r"(r[15])                                                                                       \
+                 : "r"(taddr))
+
+}  // namespace
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ti8::NTHREADS, 1)
+k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t chunk_atoms, int tiles_k,
+             float2* __restrict__ partial, int64_t frames, const float* __restrict__ fmax_dev, int dbg_flags) {
+    using namespace ti8;
+    extern __shared__ __align__(1024) char smem_raw[];
+    char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint4* aslot = reinterpret_cast<uint4*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + ASLOT_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* done = empty + STAGES;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = i8_rank();
+    const int ptile = blockIdx.x >> 1;
+    const int th0 = (ptile / tiles_k) * PAIR_M + (int)rank * TM;
+    const int tk0 = (ptile % tiles_k) * TN;
+    const int bk0 = tk0 + (int)rank * BN;
+    const int64_t chunk = blockIdx.y, t = blockIdx.z;
+    const int64_t a_begin = chunk * chunk_atoms, a_end = min(N, a_begin + chunk_atoms);
+    const int n_stages = (int)((a_end - a_begin + KS - 1) / KS);
+    const uint4* S = staged + t * N;
+    const float F = fmax_dev ? fmaxf(*fmax_dev, 1e-30f) : 1.0f;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) { i8_mbar_init(&full[s], 2 * GROUP_WARPS); i8_mbar_init(&empty[s], 1); }
+        i8_mbar_init(done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == MMA_WARP) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                     "r"(TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    i8_cluster_sync();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == MMA_WARP) {
+        // ================= MMA issuer: one lane of the leader CTA drives the pair =================
+        if (rank == 0 && lane == 0) {
+            const uint32_t base = su32(smem);
+            for (int i = 0; i < n_stages; ++i) {
+                const int s = i % STAGES;
+                i8_mbar_wait(&full[s], (uint32_t)((i / STAGES) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t sb = base + s * STAGE_BYTES;
+                const uint64_t xr_h = i8_desc(sb), xr_l = i8_desc(sb + APLANE);
+                const uint64_t xs_h = i8_desc(sb + 2 * APLANE), xs_l = i8_desc(sb + 3 * APLANE);
+                const uint32_t bh = sb + 4 * APLANE, bl = bh + BPLANE;
+                const uint64_t b1_h = i8_desc(bh + BN * KS), b1_l = i8_desc(bl + BN * KS);
+                const uint64_t b2_h = i8_desc(bh), b2_l = i8_desc(bl);
+                const uint32_t acc = i > 0 ? 1u : 0u;
+                if (!(dbg_flags & 4)) {
+                    umma2_i8(tmem, xr_h, b1_h, acc);
+                    umma2_i8(tmem, xs_h, b2_h, 1);
+                    umma2_i8(tmem + 256, xr_h, b1_l, acc);
+                    umma2_i8(tmem + 256, xr_l, b1_h, 1);
+                    umma2_i8(tmem + 256, xs_h, b2_l, 1);
+                    umma2_i8(tmem + 256, xs_l, b2_h, 1);
+                }
+                i8_commit_both(&empty[s]);
+            }
+            i8_commit_both(done);
+        }
+        __syncwarp();
+    } else if (warp < NPROD_WARPS) {
+        // ================= producers: group g fills stages g, g + 3, g + 6, ... =================
+        const int grp = warp / GROUP_WARPS, wi = warp % GROUP_WARPS;
+        const int qq = lane & 3, mr = lane >> 2;
+        const bool is_x = wi < 4;
+        const int qh = is_x ? (wi & 1) : wi - 4;              // quad half (K bytes 0-15 or 16-31 of the stage)
+        const int rh = wi >> 1;                               // X warps: row half (rows mr + 8 r, r in [8 rh, 8 rh + 8))
+        const int q = 4 * qh + qq;                            // atom quad: atoms 4q .. 4q + 3 of the stage
+        const uint32_t full0 = i8_mapa(su32(full), 0);
+        const uint32_t slot0 = su32(aslot) + (uint32_t)(grp * ASL * KS * 16);
+        const float invF = 1.0f / F;
+        auto prefetch = [&](int li) {   // local stage li of this group -> slot li % ASL (warp 0 of the group only)
+            const int i = grp + li * NGROUPS;
+            if (i < n_stages) {
+                const int64_t j = a_begin + (int64_t)i * KS + lane;
+                const bool ok = j < a_end;
+                i8_cp_async16(slot0 + (uint32_t)(((li % ASL) * KS + lane) * 16), S + (ok ? j : 0), ok ? 16u : 0u);
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        if (wi == 0) {
+#pragma unroll
+            for (int k = 0; k < ASL - 1; ++k) prefetch(k);
+        }
+        for (int li = 0;; ++li) {
+            const int i = grp + li * NGROUPS;
+            if (i >= n_stages) break;
+            const int s = i % STAGES;
+            if (wi == 0) asm volatile("cp.async.wait_group %0;" ::"n"(ti8::ASL - 2) : "memory");
+            // records of stage i visible to the group; every warp of the group finished local stage li - 1, so the
+            // slot of li - 1 (= (li + ASL - 1) % ASL) can be refilled
+            i8_named_sync(1 + grp, GROUP_WARPS * 32);
+            if (wi == 0) prefetch(li + ASL - 1);
+            uint4 at[4];
+            {
+                const uint32_t ra = slot0 + (uint32_t)(((li % ASL) * KS + 4 * q) * 16);
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(at[u].x), "=r"(at[u].y), "=r"(at[u].z), "=r"(at[u].w)
+                                 : "r"(ra + 16 * u));
+            }
+            i8_mbar_wait(&empty[s], (uint32_t)(((i / STAGES) + 1) & 1));
+            const uint32_t sbase = su32(smem) + (uint32_t)(s * STAGE_BYTES);
+            if (!(dbg_flags & 2)) {
+                if (is_x) {
+                    // X rows m = mr + 8 r (8 rh <= r < 8 rh + 8) of this CTA's 128: X_m = e^{-2 pi i h Th_a}, h = h0 + th0 + m
+                    const uint32_t h = (uint32_t)(g.h0 + th0 + mr + 64 * rh);
+                    unsigned long long v[4], st[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        float s0, c0, s1, c1;
+                        __sincosf(turns_to_radians(h * at[u].x), &s0, &c0);
+                        __sincosf(turns_to_radians(8u * at[u].x), &s1, &c1);
+                        v[u] = pack2(c0, s0);
+                        st[u] = pack2(c1, s1);
+                    }
+                    const uint32_t a0 = sbase + (uint32_t)(qh * 128 + mr * 16 + qq * 4 + rh * 8 * 256);
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) {
+                        uint32_t hc[4], lc[4], hs[4], ls[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            unsigned long long t1, t2;
+                            quantise(v[u], t1, t2);
+                            hc[u] = (uint32_t)t1; hs[u] = (uint32_t)(t1 >> 32);
+                            lc[u] = (uint32_t)t2; ls[u] = (uint32_t)(t2 >> 32);
+                            // angle addition: (c, s) <- (c cd - s sd, s cd + c sd)
+                            const unsigned long long cd = pack2(lo2(st[u]), lo2(st[u]));
+                            const unsigned long long sd = pack2(-hi2(st[u]), hi2(st[u]));
+                            v[u] = ffma2(swap2(v[u]), sd, f2mul(v[u], cd));
+                        }
+                        const uint32_t ad = a0 + (uint32_t)(r * 256);
+                        i8_sts<0 * APLANE>(ad, pack_bytes(hc[0], hc[1], hc[2], hc[3]));
+                        i8_sts<1 * APLANE>(ad, pack_bytes(lc[0], lc[1], lc[2], lc[3]));
+                        i8_sts<2 * APLANE>(ad, pack_bytes(hs[0], hs[1], hs[2], hs[3]));
+                        i8_sts<3 * APLANE>(ad, pack_bytes(ls[0], ls[1], ls[2], ls[3]));
+                    }
+                } else {
+                    // W rows k = mr + 8 r (r < 8) of this CTA's 64: W_k = (f / F) e^{-2 pi i (Th_0 + kk Th_b)}
+                    const uint32_t kk = (uint32_t)(g.k0 + bk0 + mr);
+                    unsigned long long v[4], st[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        float s0, c0, s1, c1;
+                        __sincosf(turns_to_radians(at[u].z + kk * at[u].y), &s0, &c0);
+                        __sincosf(turns_to_radians(8u * at[u].y), &s1, &c1);
+                        const float fs = __uint_as_float(at[u].w) * invF;
+                        v[u] = pack2(fs * c0, fs * s0);
+                        st[u] = pack2(c1, s1);
+                    }
+                    const uint32_t a0 = sbase + (uint32_t)(4 * APLANE + qh * 128 + mr * 16 + qq * 4);
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) {
+                        uint32_t hc[4], lc[4], hs[4], ls[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            unsigned long long t1, t2;
+                            quantise(v[u], t1, t2);
+                            hc[u] = (uint32_t)t1; hs[u] = (uint32_t)(t1 >> 32);
+                            lc[u] = (uint32_t)t2; ls[u] = (uint32_t)(t2 >> 32);
+                            const unsigned long long cd = pack2(lo2(st[u]), lo2(st[u]));
+                            const unsigned long long sd = pack2(-hi2(st[u]), hi2(st[u]));
+                            v[u] = ffma2(swap2(v[u]), sd, f2mul(v[u], cd));
+                        }
+                        const uint32_t whr = pack_bytes(hc[0], hc[1], hc[2], hc[3]);
+                        const uint32_t wlr = pack_bytes(lc[0], lc[1], lc[2], lc[3]);
+                        const uint32_t whs = pack_bytes(hs[0], hs[1], hs[2], hs[3]);
+                        const uint32_t wls = pack_bytes(ls[0], ls[1], ls[2], ls[3]);
+                        const uint32_t ad = a0 + (uint32_t)(r * 256);
+                        // B rows: -Ws at k, Wr at BN + k, Ws at 2 BN + k  (BN rows = 8 groups of 256 B)
+                        i8_sts<0>(ad, neg_bytes(whs));
+                        i8_sts<BPLANE>(ad, neg_bytes(wls));
+                        i8_sts<8 * 256>(ad, whr);
+                        i8_sts<BPLANE + 8 * 256>(ad, wlr);
+                        i8_sts<16 * 256>(ad, whs);
+                        i8_sts<BPLANE + 16 * 256>(ad, wls);
+                    }
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) i8_arrive_cluster(full0 + (uint32_t)(s * 8));
+        }
+        if (wi == 0) asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    if (warp < 4) {
+        // ================= drain (warps 0-3 after production): exact int32 accumulators -> fp32 partial tile ======
+        const int quarter = warp & 3;
+        i8_mbar_wait(done, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16);
+        const int row = quarter * 32 + lane;
+        const int64_t ih = th0 + row;
+        const int64_t n_q = g.n_h * g.n_k;
+        float2* P = partial + (chunk * frames + t) * n_q;
+        // p = (64516 HH + 254 X) F / 32258^2 in FP32 (the partial is fp32; |rounding| <= 2^-23 |p|)
+        const float c_hh = (float)(64516.0 * (double)F / (32258.0 * 32258.0));
+        const float c_x = (float)(254.0 * (double)F / (32258.0 * 32258.0));
+#pragma unroll 1
+        for (int kb = 0; kb < 8; ++kb) {
+            const uint32_t cre = (uint32_t)(kb < 4 ? 16 * kb : 16 * kb + 64);   // [Re k<64 | Im' k<64 | Re k>=64 | Im' k>=64]
+            uint32_t hre[16], him[16], xre[16], xim[16];
+            I8_TMEM_LD16(tb + cre, hre);
+            I8_TMEM_LD16(tb + cre + 64, him);
+            I8_TMEM_LD16(tb + 256 + cre, xre);
+            I8_TMEM_LD16(tb + 256 + cre + 64, xim);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (ih < g.n_h) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const int64_t ik = tk0 + 16 * kb + j;
+                    const float re = fmaf((float)(int32_t)hre[j], c_hh, (float)(int32_t)xre[j] * c_x);
+                    const float im = fmaf((float)(int32_t)him[j], c_hh, (float)(int32_t)xim[j] * c_x);
+                    if (ik < g.n_k) P[ih * g.n_k + ik] = make_float2(re, im);
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    i8_cluster_sync();
+    if (warp == MMA_WARP) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+    }
+}
+
+__global__ void k_absmax_f(const uint4* __restrict__ staged, int64_t n, float* __restrict__ out) {
+    __shared__ float sh[256];
+    float m = 0.0f;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) m = fmaxf(m, fabsf(__uint_as_float(staged[i].w)));
+    sh[threadIdx.x] = m;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] = fmaxf(sh[threadIdx.x], sh[threadIdx.x + o]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[0] = sh[0];
+}
+
+cudaError_t launch_lattice_i8(const uint4* staged, int64_t N, int64_t frames, const LatticeGeom& g, int64_t chunk_atoms,
+                              int64_t n_chunks, float* fmax_scratch, int uniform_f, float2* partial, cudaStream_t s) {
+    using namespace ti8;
+    if (chunk_atoms > kI8MaxChunk) return cudaErrorInvalidValue;
+    const int tiles_h = (int)((g.n_h + PAIR_M - 1) / PAIR_M), tiles_k = (int)((g.n_k + TN - 1) / TN);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_lattice_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        attr = true;
+    }
+    const float* fm = nullptr;
+    if (!uniform_f) {
+        // W scale F = max |f_j| over the staged atoms of frame 0 (f is per atom, the same in every frame)
+        note_launch();
+        k_absmax_f<<<1, 256, 0, s>>>(staged, N, fmax_scratch);
+        fm = fmax_scratch;
+    }
+    static int dbg = -1;
+    if (dbg < 0) { const char* e = getenv("XPCS_I8_DEBUG"); dbg = e ? atoi(e) : 0; }
+    dim3 grid(2 * tiles_h * tiles_k, (unsigned)n_chunks, (unsigned)frames);
+    note_launch();
+    k_lattice_i8<<<grid, NTHREADS, SMEM_BYTES, s>>>(staged, N, g, chunk_atoms, tiles_k, partial, frames, fm, dbg);
+    return cudaGetLastError();
+}
+
+}  // namespace xpcs

@@ -1,0 +1,115 @@
+"""GPU parity of the integer tensor engine (XPCS_ENGINE_TENSOR_I8: tcgen05 kind::i8, two int8 limbs per phasor
+component, exact int32 accumulation) against the FP64 oracle, at the north_star per-pixel gate (R11), on
+ragged tiles / chunks, per-atom and per-kind form factors, amplitudes, 3-D blocks, Bragg crystals and the full c2
+workload (sampled pixels, all frames)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+import xpcs_inputs as xi  # noqa: E402
+import paper_2204_13241_b200 as xp  # noqa: E402
+from _gates import assert_pixels, pixel_gate  # noqa: E402
+
+DEV = "cuda"
+I8 = xp.ENGINE_TENSOR_I8
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    xp.load()
+    if not xp.engine_available(I8):
+        pytest.skip("no tcgen05")
+    yield
+    xp.release()
+
+
+def _t(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def _grid_q(g):
+    return oracle.lattice_q(g.L, g.h0, g.n_h, g.k0, g.n_k, tuple(g.m0), tuple(g.ma), tuple(g.mb))
+
+
+@pytest.mark.parametrize("N,f_kind", [(9001, "two"), (777, "none"), (40000, "none")])
+def test_i8_ragged_parity(N, f_kind):
+    """Ragged tiles (n_h, n_k not multiples of 256 / 128), tilted plane, N not a multiple of the 32-atom stage,
+    several atom chunks (N = 40000 > one 32768-atom chunk)."""
+    cfg = xi.scaled(xi.CONFIGS["c3"], N=N, T=2)
+    pos = xi.positions(cfg)
+    f = xi.form_factors(cfg) if f_kind == "two" else None
+    g = xp.qgrid(cfg.L, -37, 300, -75, 150, m0=(0, 0, 2), ma=(1, 0, 0), mb=(0, 1, 1))
+    I = xp.xpcs_intensity_grid(_t(pos), _t(f) if f is not None else None, g, engine=I8).cpu().numpy()
+    ref = oracle.intensity(pos, f.astype(np.float64) if f is not None else None, _grid_q(g), cfg.L)
+    ratio, worst = assert_pixels(I, ref, cfg.N, f"i8 ragged N={N}")
+    print(f"i8 N={N} f={f_kind}: worst err/allowed {ratio:.3f}, max |dI|/N {worst:.2e}")
+
+
+def test_i8_matches_split_fp16_engine_statistically():
+    """Same input on both tensor engines: the difference is the int8 limb quantisation, rms ~ 3e-5 N per pixel."""
+    cfg = xi.scaled(xi.CONFIGS["c2"], N=32000, T=4)
+    pos = _t(xi.positions(cfg))
+    g = xp.lattice_plane(cfg.L, 256)
+    a = xp.xpcs_intensity_grid(pos, None, g, engine=I8, out_dtype=xp.F64).cpu().numpy()
+    b = xp.xpcs_intensity_grid(pos, None, g, engine=xp.ENGINE_TENSOR, out_dtype=xp.F64).cpu().numpy()
+    d = (a - b) / cfg.N
+    rms = float(np.sqrt(np.mean(d * d)))
+    assert rms < 8e-5, rms
+    assert np.max(np.abs(d)) < 1e-3
+    # the forward point is exact in both (all phases 0): I(0) = N^2
+    c = (128 * 256 + 128)
+    assert abs(a[0, c] - cfg.N ** 2) <= 1e-6 * cfg.N ** 2
+
+
+def test_i8_amplitude_volume_and_species():
+    cfg = xi.scaled(xi.CONFIGS["c2"], N=5003, T=2)
+    pos = xi.positions(cfg)
+    v = xp.qvolume(cfg.L, -40, 80, -30, 100, -2, 3, mc=(0, 0, 1))
+    q = oracle.lattice_volume_q(cfg.L, -40, 80, -30, 100, -2, 3)
+    A = xp.xpcs_intensity_volume(_t(pos), None, v, engine=I8, amplitude=True).cpu().numpy().astype(np.float64)
+    ref = oracle.amplitudes(pos, None, q, cfg.L)
+    err = np.abs(A[..., 0] + 1j * A[..., 1] - ref)
+    assert np.max(err / (1e-3 * np.sqrt(cfg.N) + 1e-5 * np.abs(ref))) <= 1.0
+    sp = xi.species_labels(cfg.N, 2, 3)
+    coef = xi.gaussian_form_factor_coefficients(2)
+    fq = np.stack([oracle.form_factor_gaussian(q, *coef[s]) for s in range(2)]).astype(np.float32)
+    I = xp.xpcs_intensity_volume(_t(pos), None, v, species=sp, f_q=_t(fq), engine=I8).cpu().numpy()
+    Iref = oracle.species_intensity(pos, sp, fq.astype(np.float64), q, cfg.L)
+    counts = np.bincount(sp, minlength=2).astype(np.float64)
+    S2 = (counts[:, None] * fq.astype(np.float64) ** 2).sum(0)
+    assert np.max(np.abs(I - Iref) / (1e-3 * S2 + 1e-5 * Iref)) <= 1.0
+
+
+@pytest.mark.parametrize("kind,n_cells", [("fcc", 20), ("sc", 32)])
+def test_i8_bragg(kind, n_cells):
+    """Perfect crystals at c2/c3-class N: I = N^2 on the crystal's reciprocal lattice, ~0 elsewhere."""
+    L = 40.0
+    pos = xi.crystal(kind, n_cells, L, "f32")
+    N = pos.shape[0]
+    n = 256
+    I = xp.xpcs_intensity_grid(_t(pos[None]), None, xp.lattice_plane(L, n), engine=I8).cpu().numpy()[0].reshape(n, n)
+    period = 2 * n_cells if kind == "fcc" else n_cells
+    h = np.arange(-n // 2, n // 2)
+    H, K = np.meshgrid(h, h, indexing="ij")
+    peak = (H % period == 0) & (K % period == 0)
+    np.testing.assert_allclose(I[peak], float(N) ** 2, rtol=2e-5)
+    assert np.max(I[~peak]) < 1e-3 * N
+
+
+def test_i8_config2_full_size_sampled():
+    """Config 2 in the bench's launch configuration on the i8 engine: all 100 frames, 512 seeded pixels vs the oracle."""
+    cfg = xi.CONFIGS["c2"]
+    pos = xi.positions(cfg)
+    g = xp.lattice_plane(cfg.L, cfg.n_plane)
+    I = xp.xpcs_intensity_grid(_t(pos), None, g, engine=I8).cpu().numpy()
+    q = oracle.lattice_q(cfg.L, **oracle.plane_grid(cfg.n_plane))
+    pix = xi.pixel_subset(q.shape[0], 512, 11, include=[128 * 256 + 128])
+    ref = oracle.intensity(pos[::9], None, q[pix], cfg.L)
+    ratio, worst, _ = pixel_gate(I[::9][:, pix], ref, cfg.N)
+    print(f"c2 i8 sampled: worst err/allowed {ratio:.3f}, max |dI|/N {worst:.2e}")
+    assert ratio <= 1.0

@@ -36,7 +36,7 @@ def _grid_q(grid):
 
 
 # ----------------------------------------------------------------------------------- lattice planes
-@pytest.mark.parametrize("engine", [xp.ENGINE_SIMT, xp.ENGINE_AUTO])
+@pytest.mark.parametrize("engine", [xp.ENGINE_SIMT, xp.ENGINE_TENSOR, xp.ENGINE_TENSOR_I8])
 def test_lattice_f32_ragged(engine):
     """Ragged everything: N not a multiple of the 16-atom sub-block or the 4096-atom chunk, n_h / n_k not
     multiples of the 64 x 128 tile, an l != 0 plane with a tilted direction, two species."""
@@ -61,7 +61,7 @@ def test_config1_fp64_full():
     np.testing.assert_allclose(I, ref, rtol=1e-9, atol=1e-9 * cfg.N)
 
 
-@pytest.mark.parametrize("engine", [xp.ENGINE_SIMT, xp.ENGINE_AUTO])
+@pytest.mark.parametrize("engine", [xp.ENGINE_SIMT, xp.ENGINE_TENSOR, xp.ENGINE_TENSOR_I8])
 @pytest.mark.parametrize("kind,n_cells,L,n,dtype", [("sc", 10, 10.0, 64, "f64"), ("sc", 10, 10.0, 64, "f32"),
                                                      ("fcc", 20, xi.CONFIGS["c2"].L, 256, "f32"),
                                                      ("bcc", 16, 40.0, 128, "f32")])
@@ -71,6 +71,10 @@ def test_bragg_peaks_gpu(kind, n_cells, L, n, dtype, engine):
     pos = xi.crystal(kind, n_cells, L, dtype)
     N = pos.shape[0]
     g = xp.lattice_plane(L, n)
+    if dtype == "f64" and engine != xp.ENGINE_SIMT:
+        with pytest.raises(xp.XpcsError, match="f32"):          # tensor engines are f32-only (EUNSUPPORTED)
+            xp.xpcs_intensity_grid(_t(pos), None, g, engine=engine)
+        engine = xp.ENGINE_AUTO                                  # -> the FP64 kernel
     I = xp.xpcs_intensity_grid(_t(pos), None, g, engine=engine).cpu().numpy().reshape(n, n).astype(np.float64)
     h = np.arange(-n // 2, n // 2)
     H, K = np.meshgrid(h, h, indexing="ij")

@@ -22,7 +22,7 @@ def main():
     ap.add_argument("config")
     ap.add_argument("--frames", type=int, default=0)
     ap.add_argument("--pixels", type=int, default=0)
-    ap.add_argument("--engine", default="auto", choices=["auto", "simt", "tensor"])
+    ap.add_argument("--engine", default="auto", choices=["auto", "simt", "tensor", "i8"])
     ap.add_argument("--repeat", type=int, default=2)
     a = ap.parse_args()
     cfg = xi.CONFIGS[a.config]
@@ -32,7 +32,8 @@ def main():
     pos = torch.from_numpy(xi.positions(cfg)).cuda()
     f = torch.from_numpy(xi.form_factors(cfg)).cuda() if cfg.two_species else None
     wl = pipeline.workload_from_config(cfg)
-    wl.engine = {"auto": xp.ENGINE_AUTO, "simt": xp.ENGINE_SIMT, "tensor": xp.ENGINE_TENSOR}[a.engine]
+    wl.engine = {"auto": xp.ENGINE_AUTO, "simt": xp.ENGINE_SIMT, "tensor": xp.ENGINE_TENSOR,
+                 "i8": xp.ENGINE_TENSOR_I8}[a.engine]
     if a.pixels and wl.q is not None:
         wl.q = wl.q[: a.pixels].contiguous()
     P = pipeline.Pipeline(wl)
