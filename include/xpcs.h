@@ -237,6 +237,17 @@ XPCS_API int xpcs_speckle_histogram(const void* I_series, int64_t frames, int64_
                                     int32_t n_bins, int32_t M, int32_t n_hist, double kappa_max, int64_t* counts_out,
                                     const xpcs_opts* opts);
 
+/* Ring plans.  Every ring reduction (xsvs_contrast, xpcs_shell_mean, xpcs_structure_factor_shells,
+ * xpcs_speckle_histogram) first groups the detector pixels by ring (a deterministic counting sort of bin_of_q, three
+ * small kernels).  xpcs_rings_register builds that plan once for a DEVICE bin_of_q array (n_q entries, n_bins rings)
+ * and keeps it (device memory owned by the library); later reductions that pass the same pointer with the same
+ * (n_q, n_bins) on the same device reuse it.  The caller must not modify the array while it is registered.
+ * xpcs_rings_unregister synchronises the device and frees the plan; xpcs_release frees all plans.
+ * Errors: EINVAL for null bin_of_q, n_q <= 0, n_bins outside [1, 12288], an unregistered pointer (unregister);
+ *         ENOMEM/ECUDA from the allocation or the build. */
+XPCS_API int xpcs_rings_register(const int32_t* bin_of_q, int64_t n_q, int32_t n_bins, const xpcs_opts* opts);
+XPCS_API int xpcs_rings_unregister(const int32_t* bin_of_q);
+
 /* Ring average of any per-pixel quantity, per row:
  *   out[r][b] = scale * mean_{q in ring b, values finite} values[r][q]   (NaN if no finite value),
  * e.g. the ring-averaged g2(q, tau) or, with scale = 1 / sum_j f_j^2, the structure factor

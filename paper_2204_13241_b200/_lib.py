@@ -26,7 +26,8 @@ EXPORTED = (
     "xpcs_profile_query", "xpcs_device_info", "xpcs_version", "xpcs_engine_available",
     "xpcs_amplitude", "xpcs_amplitude_grid", "xpcs_isf",
     "xpcs_intensity_volume", "xpcs_amplitude_volume", "xpcs_intensity_species", "xpcs_amplitude_species",
-    "xpcs_form_factor_gaussian", "xpcs_speckle_histogram", "xpcs_intensity_fft",
+    "xpcs_form_factor_gaussian", "xpcs_speckle_histogram", "xpcs_intensity_fft", "xpcs_rings_register",
+    "xpcs_rings_unregister",
 )
 
 
@@ -107,6 +108,8 @@ def load():
         "xpcs_amplitude_volume": [vp, i64, vp, ctypes.POINTER(Species), ctypes.POINTER(QVolume), i64, vp, op],
         "xpcs_intensity_species": [vp, i64, ctypes.POINTER(Species), vp, i64, i64, dbl, vp, op],
         "xpcs_amplitude_species": [vp, i64, ctypes.POINTER(Species), vp, i64, i64, dbl, vp, op],
+        "xpcs_rings_register": [vp, i64, i32, op],
+        "xpcs_rings_unregister": [vp],
         "xpcs_intensity_fft": [vp, i64, i64, ctypes.POINTER(QVolume), i32, dbl, i32, vp, vp, op],
         "xpcs_speckle_histogram": [vp, i64, i64, vp, i32, i32, i32, dbl, vp, op],
         "xpcs_form_factor_gaussian": [vp, i64, ctypes.POINTER(QVolume), i32, ctypes.POINTER(ctypes.c_double),
@@ -383,6 +386,16 @@ def xpcs_intensity_fft(positions, block: QVolume, n_grid, eta, k_cut=0, f_q=None
     _check(load().xpcs_intensity_fft(_ptr(positions), N, T, ctypes.byref(block), int(n_grid), float(eta), int(k_cut),
                                      _ptr(f_q), _ptr(out), ctypes.byref(o)))
     return out
+
+
+def xpcs_rings_register(bins, n_bins, stream=None):
+    """Build and keep the ring plan of a device bin array (reused by every ring reduction given the same tensor)."""
+    o = make_opts(stream=stream)
+    _check(load().xpcs_rings_register(_ptr(bins), bins.shape[0], int(n_bins), ctypes.byref(o)))
+
+
+def xpcs_rings_unregister(bins):
+    _check(load().xpcs_rings_unregister(_ptr(bins)))
 
 
 def xpcs_speckle_histogram(I, bins, n_bins, M, n_hist, kappa_max, out=None, stream=None, profile=False):

@@ -116,22 +116,54 @@ struct PlanBufs {
     int64_t max_warps;
 };
 
-int make_plan(const int32_t* bins, int64_t n_q, int32_t n_bins, cudaStream_t s, PlanBufs& pb) {
-    if (n_bins > 12288) {
-        set_error("xpcs: n_bins must be <= 12288 (got %d)", n_bins);
-        return XPCS_EINVAL;
-    }
+// Ring plans registered by xpcs_rings_register: built once, reused by every ring reduction that passes the same
+// bin_of_q pointer with the same (n_q, n_bins), until xpcs_rings_unregister / xpcs_release.
+struct RegisteredPlan {
+    const int32_t* bins;
+    int64_t n_q;
+    int32_t n_bins;
+    int device;
+    char* mem;
+    PlanBufs pb;
+};
+std::vector<RegisteredPlan>& registered() {
+    static std::vector<RegisteredPlan> v;
+    return v;
+}
+
+int build_plan(const int32_t* bins, int64_t n_q, int32_t n_bins, cudaStream_t s, char* base, PlanBufs& pb) {
     const size_t perm_b = ((sizeof(int32_t) * (size_t)n_q + 255) / 256) * 256;
     const size_t off_b = ((sizeof(int32_t) * (size_t)(n_bins + 1) + 255) / 256) * 256;
-    const size_t cnt_b = sizeof(int32_t) * (size_t)((n_q + 1023) / 1024) * (size_t)n_bins;
-    char* base = (char*)scratch(s, SS_PLAN, perm_b + 2 * off_b + cnt_b + 256);
-    if (!base) return XPCS_ENOMEM;
     pb.plan.perm = (int32_t*)base;
     pb.plan.offsets = (int32_t*)(base + perm_b);
     pb.plan.warp_off = (int32_t*)(base + perm_b + off_b);
     pb.plan.bcounts = (int32_t*)(base + perm_b + 2 * off_b);
     pb.max_warps = (n_q + 31) / 32 + n_bins;
     return cuda_fail(launch_binplan(bins, n_q, n_bins, pb.plan, s), "ring plan");
+}
+
+size_t plan_bytes(int64_t n_q, int32_t n_bins) {
+    const size_t perm_b = ((sizeof(int32_t) * (size_t)n_q + 255) / 256) * 256;
+    const size_t off_b = ((sizeof(int32_t) * (size_t)(n_bins + 1) + 255) / 256) * 256;
+    const size_t cnt_b = sizeof(int32_t) * (size_t)((n_q + 1023) / 1024) * (size_t)n_bins;
+    return perm_b + 2 * off_b + cnt_b + 256;
+}
+
+int make_plan(const int32_t* bins, int64_t n_q, int32_t n_bins, cudaStream_t s, PlanBufs& pb) {
+    if (n_bins > 12288) {
+        set_error("xpcs: n_bins must be <= 12288 (got %d)", n_bins);
+        return XPCS_EINVAL;
+    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    for (const auto& r : registered())
+        if (r.bins == bins && r.n_q == n_q && r.n_bins == n_bins && r.device == dev) {
+            pb = r.pb;
+            return XPCS_OK;
+        }
+    char* base = (char*)scratch(s, SS_PLAN, plan_bytes(n_q, n_bins));
+    if (!base) return XPCS_ENOMEM;
+    return build_plan(bins, n_q, n_bins, s, base, pb);
 }
 
 }  // namespace
@@ -147,6 +179,11 @@ int64_t xpcs_launch_count(void) { return (int64_t)launches(); }
 int xpcs_release(void) {
     clear_error();
     fft_release_plan();
+    if (!registered().empty()) {
+        cudaDeviceSynchronize();
+        for (auto& r : registered()) cudaFree(r.mem);
+        registered().clear();
+    }
     release_scratch();
     return check_sticky();
 }
@@ -802,6 +839,49 @@ int xsvs_contrast(const void* I_series, int64_t frames, int64_t n_q, const int32
     if (!mom) return XPCS_ENOMEM;
     return cuda_fail(launch_xsvs(I_series, o.in_f64, frames, n_q, pb.plan, n_bins, windows, n_windows, pb.max_warps,
                                  mom, nullptr, beta_out, o.s), "xsvs");
+}
+
+int xpcs_rings_register(const int32_t* bin_of_q, int64_t n_q, int32_t n_bins, const xpcs_opts* opts) {
+    clear_error();
+    Opts o;
+    TRY(parse_opts(opts, o));
+    NEED(bin_of_q, "bin_of_q");
+    POS(n_q, "n_q");
+    POS(n_bins, "n_bins");
+    if (n_bins > 12288 || n_q > (int64_t(1) << 31) - 1) {
+        set_error("xpcs: ring plan limits: n_bins <= 12288, n_q < 2^31");
+        return XPCS_EINVAL;
+    }
+    TRY(check_sticky());
+    xpcs_rings_unregister(bin_of_q);
+    clear_error();
+    RegisteredPlan r{};
+    r.bins = bin_of_q;
+    r.n_q = n_q;
+    r.n_bins = n_bins;
+    cudaGetDevice(&r.device);
+    TRY(cuda_fail(cudaMalloc(&r.mem, plan_bytes(n_q, n_bins)), "cudaMalloc (ring plan)"));
+    const int rc = build_plan(bin_of_q, n_q, n_bins, o.s, r.mem, r.pb);
+    if (rc != XPCS_OK) {
+        cudaFree(r.mem);
+        return rc;
+    }
+    registered().push_back(r);
+    return XPCS_OK;
+}
+
+int xpcs_rings_unregister(const int32_t* bin_of_q) {
+    clear_error();
+    auto& v = registered();
+    for (size_t i = 0; i < v.size(); ++i)
+        if (v[i].bins == bin_of_q) {
+            cudaDeviceSynchronize();   // work enqueued with the plan may still be reading it
+            cudaFree(v[i].mem);
+            v.erase(v.begin() + (long)i);
+            return XPCS_OK;
+        }
+    set_error("xpcs: bin_of_q %p is not registered", (const void*)bin_of_q);
+    return XPCS_EINVAL;
 }
 
 int xpcs_speckle_histogram(const void* I_series, int64_t frames, int64_t n_q, const int32_t* bin_of_q, int32_t n_bins,

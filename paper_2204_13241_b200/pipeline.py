@@ -51,9 +51,24 @@ class Pipeline:
             self.grid = None
             self.n_q = wl.q.shape[0]
             self.bins = X.xpcs_radial_bins(wl.q, wl.q_max, wl.n_bins, stream)
+        # the detector geometry is fixed for the workload: build its ring plan once (reused by every reduction)
+        X.xpcs_rings_register(self.bins, wl.n_bins, stream)
+        self._registered = True
         odt = torch.float64 if wl.in_dtype == X.F64 else torch.float32
         self.I = torch.empty((wl.T, self.n_q), dtype=odt, device=self.device)
         self.g2 = torch.empty((len(wl.lags), self.n_q), dtype=torch.float32, device=self.device) if wl.lags else None
+
+    def close(self):
+        """Free the registered ring plan (the bins tensor dies with the pipeline; a stale plan must not outlive it)."""
+        if getattr(self, "bins", None) is not None and getattr(self, "_registered", False):
+            try:
+                X.xpcs_rings_unregister(self.bins)
+            except Exception:
+                pass
+            self._registered = False
+
+    def __del__(self):
+        self.close()
 
     @property
     def pairs_per_step(self) -> int:
@@ -78,7 +93,7 @@ class Pipeline:
         return out
 
     # ---------------------------------------------------------------- end to end from host memory
-    def alloc_host_io(self, pos_host: np.ndarray, f_host: np.ndarray | None, batches: int = 4):
+    def alloc_host_io(self, pos_host: np.ndarray, f_host: np.ndarray | None, batches: int = 8):
         """Pinned host copies of the inputs and pinned result buffers (allocated once, reused per step)."""
         self.h_pos = torch.from_numpy(np.ascontiguousarray(pos_host)).pin_memory()
         self.h_f = torch.from_numpy(np.ascontiguousarray(f_host)).pin_memory() if f_host is not None else None

@@ -178,3 +178,21 @@ def test_erlang_statistics_on_gpu_outputs():
     beta = xp.xsvs_contrast(I, bins, 8, [1, 5, 10, 20]).cpu().numpy()
     for wi, M in enumerate((1, 5, 10, 20)):
         assert np.all(np.abs(beta[wi, 2:] * M - 1.0) < 0.12), (M, beta[wi])
+
+
+def test_registered_ring_plan_gives_identical_reductions():
+    """xpcs_rings_register: the cached plan gives bit-identical ring reductions; unregister frees it."""
+    rng = np.random.default_rng(5)
+    T, n = 20, 64
+    I = _t(rng.exponential(1.0, (T, n * n)).astype(np.float32))
+    bins = _t(oracle.lattice_bins(n, n_bins=8))
+    a = [xp.xsvs_contrast(I, bins, 8, [1, 2, 5]), xp.xpcs_shell_mean(I, bins, 8),
+         xp.xpcs_speckle_histogram(I, bins, 8, 2, 16, 4.0)]
+    xp.xpcs_rings_register(bins, 8)
+    b = [xp.xsvs_contrast(I, bins, 8, [1, 2, 5]), xp.xpcs_shell_mean(I, bins, 8),
+         xp.xpcs_speckle_histogram(I, bins, 8, 2, 16, 4.0)]
+    xp.xpcs_rings_unregister(bins)
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
+    with pytest.raises(xp.XpcsError, match="not registered"):
+        xp.xpcs_rings_unregister(bins)
