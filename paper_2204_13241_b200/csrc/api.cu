@@ -820,9 +820,9 @@ int xsvs_contrast(const void* I_series, int64_t frames, int64_t n_q, const int32
         return XPCS_EINVAL;
     }
     int64_t max_slots = 0;
-    for (int64_t w0 = 0; w0 < n_windows; w0 += 16) {
+    for (int64_t w0 = 0; w0 < n_windows; w0 += 8) {   // windows per k_xsvs_warp pass (XW in k_stats.cu)
         int64_t s = 0;
-        for (int64_t i = w0; i < std::min(n_windows, w0 + 16); ++i) {
+        for (int64_t i = w0; i < std::min(n_windows, w0 + 8); ++i) {
             if (windows[i] < 1 || windows[i] > frames) {
                 set_error("xpcs: window %d out of range [1, %lld]", windows[i], (long long)frames);
                 return XPCS_EINVAL;

@@ -86,7 +86,7 @@ cudaError_t launch_g2(const void* I, int in_f64, int64_t T, int64_t n_q, const i
                       int64_t n_lags, int max_lag, void* out, int out_f64, cudaStream_t s) {
     const int wpb = (int)std::min<int64_t>(G2_WARPS, (n_lags + G2_LPW - 1) / G2_LPW);   // drop idle warps
     dim3 grid((unsigned)((n_q + 31) / 32), (unsigned)((n_lags + G2_LAGS_PER_BLOCK - 1) / G2_LAGS_PER_BLOCK));
-    const size_t elem = in_f64 ? sizeof(double) : sizeof(float);
+    const size_t elem = sizeof(double);                    // the series is staged in FP64 for both input types
     const size_t smem = elem * 32 * (GC + max_lag + 16 + 16);
     (void)wpb;
     note_launch();
@@ -97,7 +97,7 @@ cudaError_t launch_g2(const void* I, int in_f64, int64_t T, int64_t n_q, const i
         kern<<<grid, 256, smem, s>>>((const IN*)I, T, n_q, lags_dev, n_lags, max_lag + 16, (OUT*)out); \
     }
     if (in_f64) { if (out_f64) G2_CASE(double, double, double) else G2_CASE(double, float, double) }
-    else { if (out_f64) G2_CASE(float, double, float) else G2_CASE(float, float, float) }
+    else { if (out_f64) G2_CASE(float, double, double) else G2_CASE(float, float, double) }   // staged as FP64: one conversion per load, not per use
 #undef G2_CASE
     return cudaGetLastError();
 }
@@ -336,7 +336,7 @@ cudaError_t launch_shell_mean(const void* v, int in_f64, int64_t rows, int64_t n
 // reduces (I_W, I_W^2) with shuffles; lane 0 writes the warp's moments for slot (W, s).  A second kernel sums
 // the warps of each ring in fixed order, forms beta_{W,b,s} (population variance / mean^2) and averages over s.
 // =====================================================================================================
-namespace { constexpr int XW = 16; }
+namespace { constexpr int XW = 8; }
 struct WinSet {
     int n;
     int W[XW], S[XW], base[XW];
@@ -371,21 +371,31 @@ k_xsvs_warp(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __r
     int cnt[XW], sidx[XW];
 #pragma unroll
     for (int w = 0; w < XW; ++w) { run[w] = 0.0; cnt[w] = w < ws.n ? ws.W[w] : 1; sidx[w] = 0; }
-    for (int64_t t = 0; t < T; ++t) {
-        const double v = valid ? (double)I[t * n_q + px] : 0.0;
+    // frames are read 8 at a time (independent loads in flight; the series of one ring pixel is a strided walk
+    // through I, so a single outstanding load per lane left this kernel latency-bound)
+    constexpr int TB = 8;
+    for (int64_t t0 = 0; t0 < T; t0 += TB) {
+        double vb[TB];
 #pragma unroll
-        for (int w = 0; w < XW; ++w) {
-            if (w >= ws.n) break;
-            run[w] += v;
-            if (--cnt[w] == 0) {
-                if (sidx[w] < ws.S[w]) {
-                    const double m1 = warp_sum_d(run[w]);
-                    const double m2 = warp_sum_d(run[w] * run[w]);
-                    if (lane == 0) mom[gw * ws.total_slots + ws.base[w] + sidx[w]] = make_double2(m1, m2);
-                    ++sidx[w];
+        for (int u = 0; u < TB; ++u) vb[u] = (valid && t0 + u < T) ? (double)I[(t0 + u) * n_q + px] : 0.0;
+#pragma unroll
+        for (int u = 0; u < TB; ++u) {
+            if (t0 + u >= T) break;
+            const double v = vb[u];
+#pragma unroll
+            for (int w = 0; w < XW; ++w) {
+                if (w >= ws.n) break;
+                run[w] += v;
+                if (--cnt[w] == 0) {
+                    if (sidx[w] < ws.S[w]) {
+                        const double m1 = warp_sum_d(run[w]);
+                        const double m2 = warp_sum_d(run[w] * run[w]);
+                        if (lane == 0) mom[gw * ws.total_slots + ws.base[w] + sidx[w]] = make_double2(m1, m2);
+                        ++sidx[w];
+                    }
+                    run[w] = 0.0;
+                    cnt[w] = ws.W[w];
                 }
-                run[w] = 0.0;
-                cnt[w] = ws.W[w];
             }
         }
     }

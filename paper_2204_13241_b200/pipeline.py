@@ -140,14 +140,25 @@ class Pipeline:
             self.s_d2h.wait_event(e)
             with torch.cuda.stream(self.s_d2h):
                 self.h_out["I"][t0:t1].copy_(I_b, non_blocking=True)
-        out = {"S_rings": X.xpcs_structure_factor_shells(self.I, self.d_f, wl.N, self.bins, wl.n_bins, stream=main)}
+        out = {}
         if wl.lags:
+            # g2 first: its (largest) result streams back on the copy stream while the ring reductions run
             X.xpcs_g2(self.I, wl.lags, out=self.g2, out_dtype=X.F32, stream=main)
             out["g2"] = self.g2
+            if "g2" not in self.h_out:
+                self.h_out["g2"] = torch.empty(self.g2.shape, dtype=self.g2.dtype, pin_memory=True)
+            e = torch.cuda.Event()
+            e.record(main)
+            self.s_d2h.wait_event(e)
+            with torch.cuda.stream(self.s_d2h):
+                self.h_out["g2"].copy_(self.g2, non_blocking=True)
             out["g2_rings"] = X.xpcs_shell_mean(self.g2, self.bins, wl.n_bins, stream=main)
+        out["S_rings"] = X.xpcs_structure_factor_shells(self.I, self.d_f, wl.N, self.bins, wl.n_bins, stream=main)
         if wl.windows:
             out["beta"] = X.xsvs_contrast(self.I, self.bins, wl.n_bins, wl.windows, stream=main)
         for k, v in out.items():
+            if k == "g2":
+                continue
             if k not in self.h_out:
                 self.h_out[k] = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
             self.h_out[k].copy_(v, non_blocking=True)
