@@ -46,8 +46,9 @@ constexpr int MMA_WARP = NPROD_WARPS;               // warps 0-3 (distinct TMEM 
 constexpr int NTHREADS = (MMA_WARP + 1) * 32;       // 608
 constexpr int MMA_N = 2 * TN;                       // 256
 constexpr int TMEM_COLS = 512;                      // HH cols [0, 256), X cols [256, 512)
-constexpr int ASL = 4;                              // atom-record slots per group (cp.async prefetch distance ASL - 1)
-constexpr int ASLOT_BYTES = NGROUPS * ASL * KS * 16;
+constexpr int ASL = 4;                              // atom-record slots per warp (cp.async prefetch distance ASL - 1)
+constexpr int WREC = 16;                            // records a producer warp needs per stage (its 4 atom quads)
+constexpr int ASLOT_BYTES = NPROD_WARPS * ASL * WREC * 16;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + ASLOT_BYTES + 1024 + 256;
 constexpr float MAGIC = 12582912.0f;                // 1.5 * 2^23
 }  // namespace ti8
@@ -237,33 +238,31 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
         const int rh = wi >> 1;                               // X warps: row half (rows mr + 8 r, r in [8 rh, 8 rh + 8))
         const int q = 4 * qh + qq;                            // atom quad: atoms 4q .. 4q + 3 of the stage
         const uint32_t full0 = i8_mapa(su32(full), 0);
-        const uint32_t slot0 = su32(aslot) + (uint32_t)(grp * ASL * KS * 16);
+        // every warp prefetches its own 16 atom records (atoms 16 qh .. 16 qh + 15 of each of its stages) with
+        // cp.async into a private ring: no cross-warp barrier per stage
+        const uint32_t slot0 = su32(aslot) + (uint32_t)(warp * ASL * WREC * 16);
         const float invF = 1.0f / F;
-        auto prefetch = [&](int li) {   // local stage li of this group -> slot li % ASL (warp 0 of the group only)
+        auto prefetch = [&](int li) {   // local stage li of this group -> slot li % ASL of this warp
             const int i = grp + li * NGROUPS;
-            if (i < n_stages) {
-                const int64_t j = a_begin + (int64_t)i * KS + lane;
+            if (i < n_stages && lane < WREC) {
+                const int64_t j = a_begin + (int64_t)i * KS + WREC * qh + lane;
                 const bool ok = j < a_end;
-                i8_cp_async16(slot0 + (uint32_t)(((li % ASL) * KS + lane) * 16), S + (ok ? j : 0), ok ? 16u : 0u);
+                i8_cp_async16(slot0 + (uint32_t)(((li % ASL) * WREC + lane) * 16), S + (ok ? j : 0), ok ? 16u : 0u);
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
         };
-        if (wi == 0) {
 #pragma unroll
-            for (int k = 0; k < ASL - 1; ++k) prefetch(k);
-        }
+        for (int k = 0; k < ASL - 1; ++k) prefetch(k);
         for (int li = 0;; ++li) {
             const int i = grp + li * NGROUPS;
             if (i >= n_stages) break;
             const int s = i % STAGES;
-            if (wi == 0) asm volatile("cp.async.wait_group %0;" ::"n"(ti8::ASL - 2) : "memory");
-            // records of stage i visible to the group; every warp of the group finished local stage li - 1, so the
-            // slot of li - 1 (= (li + ASL - 1) % ASL) can be refilled
-            i8_named_sync(1 + grp, GROUP_WARPS * 32);
-            if (wi == 0) prefetch(li + ASL - 1);
+            asm volatile("cp.async.wait_group %0;" ::"n"(ti8::ASL - 2) : "memory");
+            __syncwarp();                 // the warp's records of stage i are visible to all its lanes; every lane has
+            prefetch(li + ASL - 1);       // finished reading slot (li - 1) % ASL, which is refilled now
             uint4 at[4];
             {
-                const uint32_t ra = slot0 + (uint32_t)(((li % ASL) * KS + 4 * q) * 16);
+                const uint32_t ra = slot0 + (uint32_t)(((li % ASL) * WREC + 4 * qq) * 16);
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
                     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
@@ -352,7 +351,7 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
             __syncwarp();
             if (lane == 0) i8_arrive_cluster(full0 + (uint32_t)(s * 8));
         }
-        if (wi == 0) asm volatile("cp.async.wait_group 0;" ::: "memory");
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     if (warp < 4) {
         // ================= drain (warps 0-3 after production): exact int32 accumulators -> fp32 partial tile ======
