@@ -321,7 +321,7 @@ def main():
                 "config": {"workload": cfg.name, "N": cfg.N, "n_q": P.n_q, "frames": cfg.T,
                            "lags": len(cfg.lags), "windows": list(cfg.windows), "rings": cfg.n_bins,
                            "pairs_per_step_per_gpu": pairs_step, "engine": args.engine,
-                           "engine_used": eng_name if cfg.n_plane and wl.in_dtype == xp.F32 else "generic/f64",
+                           "engine_used": ("fp64" if wl.in_dtype == xp.F64 else eng_name),
                            "l2": "flushed between timed steps (256 MB write, untimed)",
                            "parallelism": f"weak x{ws} (independent trajectories)"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(n_launch),
