@@ -507,18 +507,18 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
         int64_t ch = 4096;
         if (i8) {
             // exact int32 accumulation: chunks only balance the grid (clusters of 2 CTAs, one CTA per SM) and stay
-            // <= kI8MaxChunk; among C in [C0/2, 2 C0] pick the fewest wave-quantisation losses
+            // <= kI8MaxChunk.  Cost model in 32-atom stage units: waves x (stages per CTA + a fixed per-CTA cost of
+            // ~15 stages for the prologue, the single drain and the cluster teardown); the smallest C wins ties.
             const int64_t units = ((g.n_h + 255) / 256) * ((g.n_k + 127) / 128) * V;
             const int64_t wave = std::max<int64_t>(1, sm_count() / 2);
             const int64_t cmin = std::max<int64_t>(1, (Ng + kI8MaxChunk - 1) / kI8MaxChunk);
             const int64_t cmax = std::max<int64_t>(cmin, std::min<int64_t>((Ng + 1023) / 1024, 64));
-            const int64_t C0 = std::min(cmax, std::max(cmin, (8 * wave + units - 1) / units));
-            int64_t best = C0;
-            double best_eff = -1.0;
-            for (int64_t c = std::max(cmin, C0 / 2); c <= std::min(cmax, 2 * C0); ++c) {
-                const double w = (double)(units * c) / (double)wave;
-                const double eff = w / std::ceil(w) - 0.004 * (double)c;   // mild preference for fewer, longer CTAs
-                if (eff > best_eff) { best_eff = eff; best = c; }
+            int64_t best = cmin;
+            double best_cost = 1e300;
+            for (int64_t c = cmin; c <= cmax; ++c) {
+                const double waves = std::ceil((double)(units * c) / (double)wave);
+                const double cost = waves * (std::ceil((double)Ng / (double)(32 * c)) + 15.0);
+                if (cost < best_cost * (1.0 - 1e-9)) { best_cost = cost; best = c; }
             }
             ch = ((Ng + best - 1) / best + 31) / 32 * 32;
             ch = std::min<int64_t>(ch, kI8MaxChunk);

@@ -106,11 +106,15 @@ class Pipeline:
         self.batches = [(edges[i], edges[i + 1]) for i in range(nb) if edges[i + 1] > edges[i]]
         self.s_h2d = torch.cuda.Stream(self.device)
         self.s_d2h = torch.cuda.Stream(self.device)
+        # two compute streams: consecutive frame batches run concurrently, so the last wave of one batch's intensity
+        # kernel shares the GPU with the next batch's first wave (the library keeps scratch per stream)
+        self.s_comp = [torch.cuda.Stream(self.device), torch.cuda.Stream(self.device)]
 
     def run_host(self) -> dict:
         """End to end: pinned H2D of the step's positions, I(q,t), g2, rings and XSVS, D2H of every result.
-        Frames are split into batches on three streams so that the copies of batch b+1 (H2D) and b-1 (D2H)
-        overlap the intensity kernel of batch b; the reductions follow on the compute stream."""
+        Frames are split into batches: H2D on one stream, the intensity kernels alternate between two compute streams
+        (consecutive batches overlap on the GPU), D2H of each batch's I on a copy stream; the reductions follow on the
+        caller's stream, g2 first so that its result streams back while the ring reductions run."""
         wl = self.wl
         main = torch.cuda.current_stream(self.device)
         if "I" not in self.h_out:
@@ -127,19 +131,24 @@ class Pipeline:
                 e = torch.cuda.Event()
                 e.record(self.s_h2d)
                 ev_in.append(e)
+        for sc in self.s_comp:
+            sc.wait_stream(main)
         for bi, (t0, t1) in enumerate(self.batches):
-            main.wait_event(ev_in[bi])
+            sc = self.s_comp[bi % 2]
+            sc.wait_event(ev_in[bi])
             pos_b = self.d_pos[t0:t1]
             I_b = self.I[t0:t1]
             if self.grid is not None:
-                X.xpcs_intensity_grid(pos_b, self.d_f, self.grid, out=I_b, engine=wl.engine, stream=main)
+                X.xpcs_intensity_grid(pos_b, self.d_f, self.grid, out=I_b, engine=wl.engine, stream=sc)
             else:
-                X.xpcs_intensity(pos_b, self.d_f, wl.q, wl.L, out=I_b, stream=main)
+                X.xpcs_intensity(pos_b, self.d_f, wl.q, wl.L, out=I_b, stream=sc)
             e = torch.cuda.Event()
-            e.record(main)
+            e.record(sc)
             self.s_d2h.wait_event(e)
             with torch.cuda.stream(self.s_d2h):
                 self.h_out["I"][t0:t1].copy_(I_b, non_blocking=True)
+        for sc in self.s_comp:
+            main.wait_stream(sc)
         out = {}
         if wl.lags:
             # g2 first: its (largest) result streams back on the copy stream while the ring reductions run
