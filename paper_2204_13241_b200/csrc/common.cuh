@@ -76,6 +76,14 @@ __device__ __forceinline__ double box_fraction(double x, double L) {
     const double u = y / L;
     return u < 1.0 ? u : 0.0;
 }
+// Same wrap with a reciprocal multiply (fp32 staging paths): u = x/L - floor(x/L) from x * (1/L); differs from the
+// exact quotient by <= 1 ulp, far below the 2^-32-turn resolution of the fixed-point phases it feeds.
+__device__ __forceinline__ double box_fraction_fast(double x, double invL) {
+    const double v = x * invL;
+    double u = v - floor(v);
+    if (!(u >= 0.0) || u >= 1.0) u = 0.0;
+    return u;
+}
 __device__ __forceinline__ uint32_t frac_to_fixed32(double u) {
     // round(u * 2^32) mod 2^32 ; u in [0, 1)
     unsigned long long v = (unsigned long long)llrint(u * 4294967296.0);

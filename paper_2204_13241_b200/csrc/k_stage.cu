@@ -27,6 +27,7 @@ template <typename P, typename F>
 __global__ void __launch_bounds__(256) k_stage_lattice32(const P* __restrict__ pos, const F* __restrict__ f,
                                                          int64_t N, int64_t total, LatticeGeom g, StageMap m,
                                                          uint4* __restrict__ out) {
+    const double invL = 1.0 / g.L;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         int64_t v;
         const int64_t src = stage_src(m, N, i, v);
@@ -34,7 +35,7 @@ __global__ void __launch_bounds__(256) k_stage_lattice32(const P* __restrict__ p
         const P* r = pos + 3 * (t * m.n_src + src);
         uint32_t X[3];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) X[c] = frac_to_fixed32(box_fraction((double)r[c], g.L));
+        for (int c = 0; c < 3; ++c) X[c] = frac_to_fixed32(box_fraction_fast((double)r[c], invL));
         uint32_t th[3];
         int32_t m0[3];
 #pragma unroll
@@ -78,12 +79,13 @@ template <typename P, typename F>
 __global__ void __launch_bounds__(256) k_stage_generic32(const P* __restrict__ pos, const F* __restrict__ f,
                                                          int64_t N, int64_t total, double L, StageMap m,
                                                          uint4* __restrict__ out) {
+    const double invL = 1.0 / L;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         int64_t v;
         const int64_t src = stage_src(m, N, i, v);
         const P* r = pos + 3 * (v * m.n_src + src);
-        const double ux = box_fraction((double)r[0], L), uy = box_fraction((double)r[1], L),
-                     uz = box_fraction((double)r[2], L);
+        const double ux = box_fraction_fast((double)r[0], invL), uy = box_fraction_fast((double)r[1], invL),
+                     uz = box_fraction_fast((double)r[2], invL);
         const uint32_t x = frac_to_fixed32(ux), y = frac_to_fixed32(uy), z = frac_to_fixed32(uz);
         const float fj = f ? (float)f[src] : 1.0f;
         out[2 * i] = make_uint4(x, y, z, __float_as_uint(fj));

@@ -16,7 +16,10 @@ namespace xpcs {
 // Consecutive lag groups (tau_l = tau_0 + l) use a register-blocked sliding window: per 16 frames 48 shared loads
 // feed 256 DFMA; other lag lists fall back to one shared load per DFMA.
 // =====================================================================================================
-namespace { constexpr int G2_LPW = 16, G2_WARPS = 8, G2_LAGS_PER_BLOCK = G2_LPW * G2_WARPS, GC = 128; }
+#ifndef XPCS_G2_LPW
+#define XPCS_G2_LPW 8
+#endif
+namespace { constexpr int G2_LPW = XPCS_G2_LPW, G2_WARPS = 8, G2_LAGS_PER_BLOCK = G2_LPW * G2_WARPS, GC = 128; }
 
 template <typename In, typename Out, typename St>
 __global__ void __launch_bounds__(256)
@@ -53,11 +56,11 @@ k_g2(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __restrict
         if (consecutive) {
             const int t0l = tau[0];
             for (int r0 = 0; r0 < rmax; r0 += 16) {          // rows beyond rmax are zero-padded or ignored
-                double a[16], w[32];
+                double a[16], w[16 + G2_LPW];
 #pragma unroll
                 for (int i = 0; i < 16; ++i) a[i] = (r0 + i < rmax) ? (double)S[(r0 + i) * 32 + lane] : 0.0;
 #pragma unroll
-                for (int j = 0; j < 32; ++j) w[j] = (double)S[(r0 + t0l + j) * 32 + lane];
+                for (int j = 0; j < 16 + G2_LPW; ++j) w[j] = (double)S[(r0 + t0l + j) * 32 + lane];
 #pragma unroll
                 for (int i = 0; i < 16; ++i)
 #pragma unroll
@@ -331,8 +334,8 @@ cudaError_t launch_shell_mean(const void* v, int in_f64, int64_t rows, int64_t n
 }
 
 // =====================================================================================================
-// K5: XSVS.  One warp per 32 pixels of a ring segment (pixels from the ring plan).  Each lane streams its pixel's
-// series once, keeps one running window sum per exposure W (registers), and when a window closes the warp
+// K5: XSVS.  One warp per (32 pixels of a ring segment, exposure window W).  Each lane streams its pixel's
+// series, keeps the running window sum (registers), and when a window closes the warp
 // reduces (I_W, I_W^2) with shuffles; lane 0 writes the warp's moments for slot (W, s).  A second kernel sums
 // the warps of each ring in fixed order, forms beta_{W,b,s} (population variance / mean^2) and averages over s.
 // =====================================================================================================
@@ -354,10 +357,12 @@ __global__ void __launch_bounds__(128)
 k_xsvs_warp(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __restrict__ perm,
             const int32_t* __restrict__ off, const int32_t* __restrict__ woff, int32_t n_bins, int64_t total_warps,
             WinSet ws, double2* __restrict__ mom) {
+    // one warp per (32 pixels of a ring segment, exposure window blockIdx.y): the windows of a pass are independent
+    // warps (7-8x the parallelism of one warp walking all windows; the series is re-read from L2)
     const int lane = threadIdx.x & 31;
     const int64_t gw = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
-    if (gw >= total_warps || gw >= woff[n_bins]) return;
-    // ring of this warp (binary search in the warp prefix)
+    const int w = blockIdx.y;
+    if (gw >= total_warps || gw >= woff[n_bins] || w >= ws.n) return;
     int lo = 0, hi = n_bins;
     while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
@@ -367,35 +372,29 @@ k_xsvs_warp(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __r
     const int64_t idx = off[b] + (gw - woff[b]) * 32 + lane;
     const bool valid = idx < off[b + 1];
     const int64_t px = valid ? perm[idx] : 0;
-    double run[XW];
-    int cnt[XW], sidx[XW];
-#pragma unroll
-    for (int w = 0; w < XW; ++w) { run[w] = 0.0; cnt[w] = w < ws.n ? ws.W[w] : 1; sidx[w] = 0; }
-    // frames are read 8 at a time (independent loads in flight; the series of one ring pixel is a strided walk
-    // through I, so a single outstanding load per lane left this kernel latency-bound)
+    const int W = ws.W[w], S = ws.S[w];
+    double2* M = mom + gw * ws.total_slots + ws.base[w];
+    // frames are read 8 at a time (independent loads in flight: the series of one ring pixel is a strided walk
+    // through I, and a single outstanding load per lane left this kernel latency-bound)
     constexpr int TB = 8;
-    for (int64_t t0 = 0; t0 < T; t0 += TB) {
+    double run = 0.0;
+    int cnt = W, sidx = 0;
+    const int64_t Tuse = (int64_t)S * W;     // the remainder frames never close a window
+    for (int64_t t0 = 0; t0 < Tuse; t0 += TB) {
         double vb[TB];
 #pragma unroll
-        for (int u = 0; u < TB; ++u) vb[u] = (valid && t0 + u < T) ? (double)I[(t0 + u) * n_q + px] : 0.0;
+        for (int u = 0; u < TB; ++u) vb[u] = (valid && t0 + u < Tuse) ? (double)I[(t0 + u) * n_q + px] : 0.0;
 #pragma unroll
         for (int u = 0; u < TB; ++u) {
-            if (t0 + u >= T) break;
-            const double v = vb[u];
-#pragma unroll
-            for (int w = 0; w < XW; ++w) {
-                if (w >= ws.n) break;
-                run[w] += v;
-                if (--cnt[w] == 0) {
-                    if (sidx[w] < ws.S[w]) {
-                        const double m1 = warp_sum_d(run[w]);
-                        const double m2 = warp_sum_d(run[w] * run[w]);
-                        if (lane == 0) mom[gw * ws.total_slots + ws.base[w] + sidx[w]] = make_double2(m1, m2);
-                        ++sidx[w];
-                    }
-                    run[w] = 0.0;
-                    cnt[w] = ws.W[w];
-                }
+            if (t0 + u >= Tuse) break;
+            run += vb[u];
+            if (--cnt == 0) {
+                const double m1 = warp_sum_d(run);
+                const double m2 = warp_sum_d(run * run);
+                if (lane == 0) M[sidx] = make_double2(m1, m2);
+                ++sidx;
+                run = 0.0;
+                cnt = W;
             }
         }
     }
@@ -442,8 +441,9 @@ cudaError_t launch_xsvs(const void* I, int in_f64, int64_t T, int64_t n_q, BinPl
         const unsigned blocks = (unsigned)((max_warps + 3) / 4);
         note_launch(2);
         if (blocks > 0) {
-            if (in_f64) k_xsvs_warp<double><<<blocks, 128, 0, s>>>((const double*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, ws, (double2*)warp_moments);
-            else k_xsvs_warp<float><<<blocks, 128, 0, s>>>((const float*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, ws, (double2*)warp_moments);
+            const dim3 gr(blocks, (unsigned)ws.n);
+            if (in_f64) k_xsvs_warp<double><<<gr, 128, 0, s>>>((const double*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, ws, (double2*)warp_moments);
+            else k_xsvs_warp<float><<<gr, 128, 0, s>>>((const float*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, ws, (double2*)warp_moments);
         }
         k_xsvs_final<<<dim3(ws.n, n_bins), 256, 0, s>>>((const double2*)warp_moments, plan.offsets, plan.warp_off, ws,
                                                         (int)w0, n_bins, beta_out);
