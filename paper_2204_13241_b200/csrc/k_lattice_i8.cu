@@ -36,7 +36,10 @@ constexpr int APLANE = TM * KS;                     // int8 A plane: 128 rows x 
 constexpr int BROWS = 3 * BN;                       // [-Ws | Wr | Ws]
 constexpr int BPLANE = BROWS * KS;                  // 6 KB
 constexpr int STAGE_BYTES = 4 * APLANE + 2 * BPLANE;   // Xr_hi Xr_lo Xs_hi Xs_lo | B_hi B_lo = 28 KB
-constexpr int STAGES = 6;
+#ifndef XPCS_I8_STAGES
+#define XPCS_I8_STAGES 6
+#endif
+constexpr int STAGES = XPCS_I8_STAGES;
 #ifndef XPCS_I8_GROUPS
 #define XPCS_I8_GROUPS 3
 #endif
