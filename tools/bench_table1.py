@@ -38,7 +38,7 @@ def main():
     for name, shape in (("81^3 grid", (-h, n, -h, n, -h, n)), ("81^2 slice", (-h, n, -h, n, 0, 1))):
         v = xp.qvolume(t1["L"], *shape)
         pairs = t1["N"] * v.n_q
-        for eng_name, eng in (("tensor", xp.ENGINE_TENSOR), ("simt", xp.ENGINE_SIMT)):
+        for eng_name, eng in (("i8", xp.ENGINE_TENSOR_I8), ("tensor", xp.ENGINE_TENSOR), ("simt", xp.ENGINE_SIMT)):
             I = xp.xpcs_intensity_volume(pos_d, None, v, engine=eng)
             for _ in range(args.warmup):
                 xp.xpcs_intensity_volume(pos_d, None, v, out=I, engine=eng)
