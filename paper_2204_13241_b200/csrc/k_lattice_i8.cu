@@ -51,7 +51,8 @@ constexpr int MMA_N = 2 * TN;                       // 256
 constexpr int TMEM_COLS = 512;                      // HH cols [0, 256), X cols [256, 512)
 constexpr int ASL = 4;                              // atom-record slots per warp (cp.async prefetch distance ASL - 1)
 constexpr int WREC = 16;                            // records a producer warp needs per stage (its 4 atom quads)
-constexpr int ASLOT_BYTES = NPROD_WARPS * ASL * WREC * 16;
+constexpr int WSLOT = WREC + WREC / 4;              // record slots incl. one 16-B pad per quad (conflict-free LDS.128)
+constexpr int ASLOT_BYTES = NPROD_WARPS * ASL * WSLOT * 16;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + ASLOT_BYTES + 1024 + 256;
 constexpr float MAGIC = 12582912.0f;                // 1.5 * 2^23
 }  // namespace ti8
@@ -117,17 +118,9 @@ __device__ __forceinline__ void i8_commit_both(uint64_t* bar) {
 __device__ __forceinline__ void i8_cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
-__device__ __forceinline__ void i8_named_sync(int id, int n) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
 __device__ __forceinline__ unsigned long long f2mul(unsigned long long a, unsigned long long b) {
     unsigned long long d;
     asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-    return d;
-}
-__device__ __forceinline__ unsigned long long f2add(unsigned long long a, unsigned long long b) {
-    unsigned long long d;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
     return d;
 }
 __device__ __forceinline__ unsigned long long swap2(unsigned long long v) { return (v >> 32) | (v << 32); }
@@ -239,18 +232,18 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
         const bool is_x = wi < 4;
         const int qh = is_x ? (wi & 1) : wi - 4;              // quad half (K bytes 0-15 or 16-31 of the stage)
         const int rh = wi >> 1;                               // X warps: row half (rows mr + 8 r, r in [8 rh, 8 rh + 8))
-        const int q = 4 * qh + qq;                            // atom quad: atoms 4q .. 4q + 3 of the stage
         const uint32_t full0 = i8_mapa(su32(full), 0);
         // every warp prefetches its own 16 atom records (atoms 16 qh .. 16 qh + 15 of each of its stages) with
         // cp.async into a private ring: no cross-warp barrier per stage
-        const uint32_t slot0 = su32(aslot) + (uint32_t)(warp * ASL * WREC * 16);
+        const uint32_t slot0 = su32(aslot) + (uint32_t)(warp * ASL * WSLOT * 16);
         const float invF = 1.0f / F;
         auto prefetch = [&](int li) {   // local stage li of this group -> slot li % ASL of this warp
             const int i = grp + li * NGROUPS;
             if (i < n_stages && lane < WREC) {
                 const int64_t j = a_begin + (int64_t)i * KS + WREC * qh + lane;
                 const bool ok = j < a_end;
-                i8_cp_async16(slot0 + (uint32_t)(((li % ASL) * WREC + lane) * 16), S + (ok ? j : 0), ok ? 16u : 0u);
+                i8_cp_async16(slot0 + (uint32_t)(((li % ASL) * WSLOT + lane + (lane >> 2)) * 16), S + (ok ? j : 0),
+                              ok ? 16u : 0u);
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
         };
@@ -265,7 +258,7 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
             prefetch(li + ASL - 1);       // finished reading slot (li - 1) % ASL, which is refilled now
             uint4 at[4];
             {
-                const uint32_t ra = slot0 + (uint32_t)(((li % ASL) * WREC + 4 * qq) * 16);
+                const uint32_t ra = slot0 + (uint32_t)(((li % ASL) * WSLOT + 5 * qq) * 16);   // quad qq at 80 qq bytes
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
                     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
