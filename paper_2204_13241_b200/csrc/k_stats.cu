@@ -407,20 +407,17 @@ k_xsvs_final(const double2* __restrict__ mom, const int32_t* __restrict__ off, c
     const int w = blockIdx.x, b = blockIdx.y;
     const int m0 = off[b + 1] - off[b];
     const int S = ws.S[w];
-    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-    // warp per snapshot s, lanes over the ring's warps g (fixed shuffle-tree order: deterministic)
     double acc = 0.0;
-    for (int s = wp; s < S; s += 8) {
+    for (int s = threadIdx.x; s < S; s += 256) {
         double m1 = 0.0, m2 = 0.0;
-        for (int g = woff[b] + lane; g < woff[b + 1]; g += 32) {
+#pragma unroll 8
+        for (int g = woff[b]; g < woff[b + 1]; ++g) {
             const double2 v = mom[(int64_t)g * ws.total_slots + ws.base[w] + s];
             m1 += v.x;
             m2 += v.y;
         }
-        m1 = warp_sum_d(m1);
-        m2 = warp_sum_d(m2);
         const double mean = m1 / m0;
-        if (lane == 0) acc += (m2 / m0 - mean * mean) / (mean * mean);   // Eq.(17), population variance
+        acc += (m2 / m0 - mean * mean) / (mean * mean);           // Eq.(17), population variance
     }
     const double tot = block_sum_d(acc, sh);
     if (threadIdx.x == 0)
