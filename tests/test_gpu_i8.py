@@ -113,3 +113,19 @@ def test_i8_config2_full_size_sampled():
     ratio, worst, _ = pixel_gate(I[::9][:, pix], ref, cfg.N)
     print(f"c2 i8 sampled: worst err/allowed {ratio:.3f}, max |dI|/N {worst:.2e}")
     assert ratio <= 1.0
+
+
+@pytest.mark.parametrize("N", [1, 2, 31, 33, 1025])
+@pytest.mark.parametrize("shape", [(1, 1), (3, 200), (257, 129)])
+def test_i8_edge_sizes(N, shape):
+    """Degenerate and ragged sizes: a single atom (I = f^2 = 1 everywhere), N around the 32-atom stage, 1 x 1 and
+    ragged planes beyond one 256 x 128 tile, far-from-origin indices (large phase turns)."""
+    L = 11.0
+    pos = xi.uniform_frame(3 + N, N, L, "f32")[None]
+    n_h, n_k = shape
+    g = xp.qgrid(L, -1000, n_h, 417, n_k, m0=(0, 0, -5))
+    I = xp.xpcs_intensity_grid(_t(pos), None, g, engine=I8).cpu().numpy()
+    ref = oracle.intensity(pos, None, _grid_q(g), L)
+    assert_pixels(I, ref, N, f"i8 N={N} shape={shape}")
+    if N == 1:
+        np.testing.assert_allclose(I, 1.0, atol=3e-4)    # limb representation: |dp| <= ~1e-4 per real part
