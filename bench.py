@@ -310,6 +310,34 @@ def main():
         e2e = {"value": ws * pairs_step / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 
+    # ---- secondary kernels against their own bounds (algorithmic work per step / measured class time per step)
+    mhz = peaks.get("sm_max_mhz", 1965.0)
+    T, n_q, nl = cfg.T, P.n_q, len(cfg.lags)
+    i_bytes = (8 if wl.in_dtype == xp.F64 else 4) * T * n_q
+    secondary = {}
+
+    def _sec(cls, bound, work, peak, unit):
+        ms_c = prof.get(cls, (0.0, 0))[0] / max(args.steps, 1)
+        if ms_c > 0:
+            ach = work / (ms_c / 1e3)
+            secondary[cls] = {"ms": ms_c, "bound": bound, "achieved": ach / 1e9, "peak": peak / 1e9, "unit": unit,
+                              "frac": ach / peak}
+
+    hbm = peaks.get("hbm_gbs", 6550.0) * 1e9
+    # g2: one FP64 FMA per (pixel, lag, frame pair); FP64 peak = 148 SMs x 59 DFMA/clk (tools/microbench.cu)
+    if nl:
+        _sec("g2", "fp64", float(sum(T - tau for tau in cfg.lags)) * n_q, sm_count * 58.95 * mhz * 1e6,
+             "G DFMA/s")
+    # XSVS: one read of the intensity series per exposure window (L2 / HBM streaming)
+    if cfg.windows:
+        _sec("xsvs", "hbm", float(len(cfg.windows)) * i_bytes, hbm, "GB/s")
+    # staging: positions read (12 B) + 16-B records written per atom and frame
+    _sec("stage", "hbm", float(cfg.N) * T * (12 + 16), hbm, "GB/s")
+    # (the fold of the atom-chunk partials reads C partial planes, C chosen inside the library: ncu shows it at
+    # ~6 TB/s, profiles/r01_launches_c2_summary.txt; it is left out here rather than under-counted)
+    # rings: one read of I (S rings) and of g2 (g2 rings)
+    _sec("rings", "hbm", float(i_bytes + 4 * nl * n_q), hbm, "GB/s")
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, args.cpu_budget)
@@ -326,7 +354,8 @@ def main():
                            "parallelism": f"weak x{ws} (independent trajectories)"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(n_launch),
                 "clocks": clk.summary(), "step_ms_all": step_ms,
-                "kernel_ms": {k: v[0] / max(args.steps, 1) for k, v in prof.items()}}
+                "kernel_ms": {k: v[0] / max(args.steps, 1) for k, v in prof.items()},
+                "secondary_rooflines": secondary}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
