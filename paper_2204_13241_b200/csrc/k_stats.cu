@@ -339,7 +339,10 @@ cudaError_t launch_shell_mean(const void* v, int in_f64, int64_t rows, int64_t n
 // reduces (I_W, I_W^2) with shuffles; lane 0 writes the warp's moments for slot (W, s).  A second kernel sums
 // the warps of each ring in fixed order, forms beta_{W,b,s} (population variance / mean^2) and averages over s.
 // =====================================================================================================
-namespace { constexpr int XW = 8; }
+#ifndef XPCS_XWPW
+#define XPCS_XWPW 1
+#endif
+namespace { constexpr int XW = 8, XWPW = XPCS_XWPW; }   // windows per pass / per warp
 struct WinSet {
     int n;
     int W[XW], S[XW], base[XW];
@@ -357,12 +360,13 @@ __global__ void __launch_bounds__(128)
 k_xsvs_warp(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __restrict__ perm,
             const int32_t* __restrict__ off, const int32_t* __restrict__ woff, int32_t n_bins, int64_t total_warps,
             WinSet ws, double2* __restrict__ mom) {
-    // one warp per (32 pixels of a ring segment, exposure window blockIdx.y): the windows of a pass are independent
-    // warps (7-8x the parallelism of one warp walking all windows; the series is re-read from L2)
+    // one warp per (32 pixels of a ring segment, group of XWPW exposure windows blockIdx.y): a few windows share one
+    // read of the series, the groups are independent warps (more parallelism than one warp walking all windows)
     const int lane = threadIdx.x & 31;
     const int64_t gw = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
-    const int w = blockIdx.y;
-    if (gw >= total_warps || gw >= woff[n_bins] || w >= ws.n) return;
+    const int w0 = blockIdx.y * XWPW;
+    if (gw >= total_warps || gw >= woff[n_bins] || w0 >= ws.n) return;
+    const int nw = min(XWPW, ws.n - w0);
     int lo = 0, hi = n_bins;
     while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
@@ -372,14 +376,19 @@ k_xsvs_warp(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __r
     const int64_t idx = off[b] + (gw - woff[b]) * 32 + lane;
     const bool valid = idx < off[b + 1];
     const int64_t px = valid ? perm[idx] : 0;
-    const int W = ws.W[w], S = ws.S[w];
-    double2* M = mom + gw * ws.total_slots + ws.base[w];
+    double run[XWPW];
+    int cnt[XWPW], sidx[XWPW];
+    int64_t Tuse = 0;                        // frames beyond the last complete window of every window are not read
+#pragma unroll
+    for (int k = 0; k < XWPW; ++k) {
+        run[k] = 0.0;
+        cnt[k] = k < nw ? ws.W[w0 + k] : 1;
+        sidx[k] = 0;
+        if (k < nw) Tuse = max(Tuse, (int64_t)ws.S[w0 + k] * ws.W[w0 + k]);
+    }
     // frames are read 8 at a time (independent loads in flight: the series of one ring pixel is a strided walk
     // through I, and a single outstanding load per lane left this kernel latency-bound)
     constexpr int TB = 8;
-    double run = 0.0;
-    int cnt = W, sidx = 0;
-    const int64_t Tuse = (int64_t)S * W;     // the remainder frames never close a window
     for (int64_t t0 = 0; t0 < Tuse; t0 += TB) {
         double vb[TB];
 #pragma unroll
@@ -387,14 +396,20 @@ k_xsvs_warp(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __r
 #pragma unroll
         for (int u = 0; u < TB; ++u) {
             if (t0 + u >= Tuse) break;
-            run += vb[u];
-            if (--cnt == 0) {
-                const double m1 = warp_sum_d(run);
-                const double m2 = warp_sum_d(run * run);
-                if (lane == 0) M[sidx] = make_double2(m1, m2);
-                ++sidx;
-                run = 0.0;
-                cnt = W;
+#pragma unroll
+            for (int k = 0; k < XWPW; ++k) {
+                if (k >= nw) break;
+                run[k] += vb[u];
+                if (--cnt[k] == 0) {
+                    if (sidx[k] < ws.S[w0 + k]) {
+                        const double m1 = warp_sum_d(run[k]);
+                        const double m2 = warp_sum_d(run[k] * run[k]);
+                        if (lane == 0) mom[gw * ws.total_slots + ws.base[w0 + k] + sidx[k]] = make_double2(m1, m2);
+                        ++sidx[k];
+                    }
+                    run[k] = 0.0;
+                    cnt[k] = ws.W[w0 + k];
+                }
             }
         }
     }
@@ -403,21 +418,39 @@ k_xsvs_warp(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __r
 __global__ void __launch_bounds__(256)
 k_xsvs_final(const double2* __restrict__ mom, const int32_t* __restrict__ off, const int32_t* __restrict__ woff,
              WinSet ws, int w_first, int32_t n_bins, double* __restrict__ beta_out) {
+    // block = (window, ring).  Snapshots s are spread over the threads; when there are fewer than 256 snapshots,
+    // tp = 256 / S (power of two) threads share one snapshot and split the ring's warps g (strided), their partial
+    // moments combined in a fixed order (deterministic), so long windows (few snapshots) are not one serial chain.
     __shared__ double sh[256];
+    __shared__ double2 part[256];
     const int w = blockIdx.x, b = blockIdx.y;
     const int m0 = off[b + 1] - off[b];
     const int S = ws.S[w];
+    const int g0 = woff[b], g1 = woff[b + 1];
+    int tp = 1;
+    while (tp * 2 * S <= 256 && tp < 64) tp *= 2;
+    const int j = threadIdx.x % tp, sl = threadIdx.x / tp, sstride = 256 / tp;
     double acc = 0.0;
-    for (int s = threadIdx.x; s < S; s += 256) {
+    for (int s0 = 0; s0 < S; s0 += sstride) {
+        const int s = s0 + sl;
         double m1 = 0.0, m2 = 0.0;
-#pragma unroll 8
-        for (int g = woff[b]; g < woff[b + 1]; ++g) {
-            const double2 v = mom[(int64_t)g * ws.total_slots + ws.base[w] + s];
-            m1 += v.x;
-            m2 += v.y;
+        if (s < S) {
+#pragma unroll 4
+            for (int g = g0 + j; g < g1; g += tp) {
+                const double2 v = mom[(int64_t)g * ws.total_slots + ws.base[w] + s];
+                m1 += v.x;
+                m2 += v.y;
+            }
         }
-        const double mean = m1 / m0;
-        acc += (m2 / m0 - mean * mean) / (mean * mean);           // Eq.(17), population variance
+        part[threadIdx.x] = make_double2(m1, m2);
+        __syncthreads();
+        if (j == 0 && s < S) {
+            double a1 = 0.0, a2 = 0.0;
+            for (int k = 0; k < tp; ++k) { a1 += part[threadIdx.x + k].x; a2 += part[threadIdx.x + k].y; }
+            const double mean = a1 / m0;
+            acc += (a2 / m0 - mean * mean) / (mean * mean);           // Eq.(17), population variance
+        }
+        __syncthreads();
     }
     const double tot = block_sum_d(acc, sh);
     if (threadIdx.x == 0)
@@ -441,7 +474,7 @@ cudaError_t launch_xsvs(const void* I, int in_f64, int64_t T, int64_t n_q, BinPl
         const unsigned blocks = (unsigned)((max_warps + 3) / 4);
         note_launch(2);
         if (blocks > 0) {
-            const dim3 gr(blocks, (unsigned)ws.n);
+            const dim3 gr(blocks, (unsigned)((ws.n + XWPW - 1) / XWPW));
             if (in_f64) k_xsvs_warp<double><<<gr, 128, 0, s>>>((const double*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, ws, (double2*)warp_moments);
             else k_xsvs_warp<float><<<gr, 128, 0, s>>>((const float*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, ws, (double2*)warp_moments);
         }
