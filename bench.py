@@ -118,6 +118,9 @@ def run_reference(args):
     ws, rank, _, dist = _dist()
     if rank != 0:
         return 0
+    # the oracle runs on all the host's cores (torchrun exports OMP_NUM_THREADS=1 per rank; libgomp reads the
+    # variable when liboracle is first loaded, which happens below)
+    os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
     import oracle
     cfg = xi.CONFIGS[args.config]
     pos = xi.positions(cfg, frames=1)[0]
