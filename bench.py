@@ -118,10 +118,10 @@ def run_reference(args):
     ws, rank, _, dist = _dist()
     if rank != 0:
         return 0
-    # the oracle runs on all the host's cores (torchrun exports OMP_NUM_THREADS=1 per rank; libgomp reads the
-    # variable when liboracle is first loaded, which happens below)
-    os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
+    # the oracle runs on all the host's cores (torchrun exports OMP_NUM_THREADS=1 per rank, and torch.distributed
+    # has already initialised the OpenMP runtime with it)
     import oracle
+    oracle.set_threads(len(os.sched_getaffinity(0)))
     cfg = xi.CONFIGS[args.config]
     pos = xi.positions(cfg, frames=1)[0]
     f = xi.form_factors(cfg).astype(np.float64) if cfg.two_species else None
@@ -157,6 +157,7 @@ def run_reference(args):
 def cpu_baseline(cfg, budget_s):
     """Oracle timed on the host cores on a bounded sample (rank 0, N = 1 only)."""
     import oracle
+    oracle.set_threads(len(os.sched_getaffinity(0)))
     pos = xi.positions(cfg, frames=1)[0]
     f = xi.form_factors(cfg).astype(np.float64) if cfg.two_species else None
     if cfg.n_plane:

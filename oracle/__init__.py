@@ -57,12 +57,18 @@ def lib():
         L.oracle_species.argtypes = [dp, i64, ip, dp, dp, i64, i64, ctypes.c_double, ctypes.c_int, dp]
         L.oracle_pair_sum_species.argtypes = [dp, i64, ip, dp, dp, i64, ctypes.c_double, dp]
         L.oracle_max_threads.restype = ctypes.c_int
+        L.oracle_set_threads.argtypes = [ctypes.c_int]
         _lib = L
     return _lib
 
 
 def threads() -> int:
     return int(lib().oracle_max_threads())
+
+
+def set_threads(n: int) -> None:
+    """OpenMP threads of the oracle's loops (timing on all host cores)."""
+    lib().oracle_set_threads(int(n))
 
 
 def _d(a):

@@ -152,3 +152,14 @@ void oracle_pair_sum_species(const double* pos, int64_t N, const int32_t* specie
         I_out[iq] = s;
     }
 }
+
+/* Thread count of the OpenMP loops above (the host-core baseline sets it explicitly: a runtime already initialised
+ * by another library in the process would ignore OMP_NUM_THREADS). */
+void oracle_set_threads(int n) {
+#ifdef _OPENMP
+    extern void omp_set_num_threads(int);
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
