@@ -148,10 +148,22 @@ def run_reference(args):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "N": cfg.N, "n_q": int(q.shape[0]), "frames": cfg.T},
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": oracle.threads(), "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": oracle.threads(), "cpu_model": _cpu_model(),
+                             "kind": "oracle", "sample": sample},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def cpu_baseline(cfg, budget_s):
@@ -175,7 +187,7 @@ def cpu_baseline(cfg, budget_s):
     oracle.intensity(pos, f, qs[pix], cfg.L)
     dt = time.perf_counter() - t0
     pairs = cfg.N * len(pix)
-    return {"value": pairs / dt, "unit": UNIT, "cores": oracle.threads(), "kind": "oracle",
+    return {"value": pairs / dt, "unit": UNIT, "cores": oracle.threads(), "cpu_model": _cpu_model(), "kind": "oracle",
             "sample": f"{cfg.name} frame 0, {len(pix)} seeded pixels x {cfg.N} atoms ({pairs:.3g} pairs, {dt:.1f} s)"}
 
 
