@@ -296,6 +296,9 @@ def main():
         roof = {"bound": "alu", "unit": "TFLOP/s (FP32 FMA pipe)", "peak": peak,
                 "achieved": 8.0 * pairs_launch / (per_launch_ms / 1e3) / 1e12}
     roof["frac"] = roof["achieved"] / roof["peak"]
+    if wl.in_dtype == xp.F64:
+        # config 1 (4.1e6 pairs, FP64): launch/latency-bound; the FP32 figure above is context only
+        roof["note"] = "FP64 workload: latency-bound, report ms_per_step; frac against the FP32 pipe is context only"
     eng_name = "i8" if i8_used else ("tensor" if tc_used else ("simt" if cfg.n_plane else "generic"))
     roof["traffic"] = _traffic(cfg.name, eng_name, pairs_launch)
     roof["peak_source"] = (f"{peak_src}, {'burst' if at_max else 'sustained'} bf16"
