@@ -22,8 +22,9 @@
 // owns 4 consecutive atoms (one 32-bit word per row and limb plane) and 8 rows spaced 8 apart (X or W), and walks
 // the rows with the angle-addition recurrence X_{m+8} = X_m X_8 (packed FP32x2, 2 ops per phasor; 2 SFU sincos per
 // atom per thread), quantises with magic-number rounding (3 packed ops per phasor) and packs limb bytes with PRMT.
-// Lanes (quad qq, row mr) write 32 distinct banks per store.  After the last stage, warps 0-3 (one per TMEM lane
-// quarter) wait for the final MMA commit and drain both accumulators: p = (64516 HH + 254 X) F / 32258^2.
+// Lanes (quad qq, row mr) write 32 distinct banks per store.  After the last stage, warps 0-7 (one per TMEM lane
+// quarter, two warps per quarter splitting the columns) wait for the final MMA commit and drain both
+// accumulators: p = (64516 HH + 254 X) F / 32258^2.
 #include "common.cuh"
 
 namespace xpcs {
@@ -349,9 +350,10 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
         }
         asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
-    if (warp < 4) {
-        // ================= drain (warps 0-3 after production): exact int32 accumulators -> fp32 partial tile ======
-        const int quarter = warp & 3;
+    if (warp < 8) {
+        // ================= drain (warps 0-7 after production): exact int32 accumulators -> fp32 partial tile ======
+        // warp w reads TMEM lane quarter w % 4 (the tcgen05.ld lane restriction) and column half w / 4
+        const int quarter = warp & 3, half = warp >> 2;
         i8_mbar_wait(done, 0);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16);
@@ -363,7 +365,7 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
         const float c_hh = (float)(64516.0 * (double)F / (32258.0 * 32258.0));
         const float c_x = (float)(254.0 * (double)F / (32258.0 * 32258.0));
 #pragma unroll 1
-        for (int kb = 0; kb < 8; ++kb) {
+        for (int kb = 4 * half; kb < 4 * half + 4; ++kb) {
             const uint32_t cre = (uint32_t)(kb < 4 ? 16 * kb : 16 * kb + 64);   // [Re k<64 | Im' k<64 | Re k>=64 | Im' k>=64]
             uint32_t hre[16], him[16], xre[16], xim[16];
             I8_TMEM_LD16(tb + cre, hre);

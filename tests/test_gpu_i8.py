@@ -129,3 +129,21 @@ def test_i8_edge_sizes(N, shape):
     assert_pixels(I, ref, N, f"i8 N={N} shape={shape}")
     if N == 1:
         np.testing.assert_allclose(I, 1.0, atol=3e-4)    # limb representation: |dp| <= ~1e-4 per real part
+
+
+def test_i8_many_frames_batched():
+    """More virtual frames than one 1-GiB scratch batch holds (the call splits them into several engine launches):
+    sampled frames from the first, a middle and the last batch against the oracle, and the batches agree with a
+    per-frame call on the same frames."""
+    cfg = xi.scaled(xi.CONFIGS["c2"], N=1500, T=700)
+    pos = xi.positions(cfg)
+    g = xp.lattice_plane(cfg.L, 256)
+    d = _t(pos)
+    I = xp.xpcs_intensity_grid(d, None, g, engine=I8).cpu().numpy()
+    q = oracle.lattice_q(cfg.L, **oracle.plane_grid(256))
+    pix = xi.pixel_subset(q.shape[0], 256, 8)
+    frames = [0, 350, 699]
+    ref = oracle.intensity(pos[frames], None, q[pix], cfg.L)
+    assert_pixels(I[frames][:, pix], ref, cfg.N, "i8 batched frames")
+    one = xp.xpcs_intensity_grid(d[699:700], None, g, engine=I8).cpu().numpy()
+    assert_pixels(one[0][pix], ref[2], cfg.N, "i8 single frame")
