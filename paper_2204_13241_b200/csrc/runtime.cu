@@ -33,11 +33,14 @@ long long launches() { return g_launches.load(); }
 
 // ---------------------------------------------------------------- scratch
 struct Buf { void* p = nullptr; size_t n = 0; };
-static std::map<std::pair<cudaStream_t, int>, Buf> g_scratch;
+// keyed by (device, stream, slot): the legacy default stream (NULL) is the same handle on every device
+static std::map<std::pair<std::pair<int, cudaStream_t>, int>, Buf> g_scratch;
 
 void* scratch(cudaStream_t s, int slot, size_t bytes) {
     std::lock_guard<std::mutex> lk(g_mu);
-    Buf& b = g_scratch[{s, slot}];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    Buf& b = g_scratch[{{dev, s}, slot}];
     if (bytes == 0) bytes = 16;
     if (b.n >= bytes) return b.p;
     if (b.p) {
@@ -65,9 +68,15 @@ void* scratch(cudaStream_t s, int slot, size_t bytes) {
 
 void release_scratch() {
     std::lock_guard<std::mutex> lk(g_mu);
-    cudaDeviceSynchronize();
-    for (auto& kv : g_scratch)
-        if (kv.second.p) cudaFree(kv.second.p);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto& kv : g_scratch) {
+        if (!kv.second.p) continue;
+        cudaSetDevice(kv.first.first.first);
+        cudaDeviceSynchronize();
+        cudaFree(kv.second.p);
+    }
+    cudaSetDevice(cur);
     g_scratch.clear();
 }
 
