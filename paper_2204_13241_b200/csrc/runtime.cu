@@ -80,13 +80,16 @@ void release_scratch() {
     g_scratch.clear();
 }
 
-int sm_count() {
-    static int n = 0;
+int sm_count() {   // of the current device (cached per device)
+    static std::atomic<int> cache[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    int n = cache[dev].load();
     if (n == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
         if (n <= 0) n = 148;
+        cache[dev].store(n);
     }
     return n;
 }
