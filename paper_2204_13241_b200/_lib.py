@@ -199,8 +199,21 @@ def species_desc(species, f_q):
     return d, (sp, f_q)
 
 
-def _positions3(positions):
-    return positions.unsqueeze(0) if positions.dim() == 2 else positions
+def _positions3(positions, *same_dtype, form_factors=None, q_vectors=None):
+    """[T][N][3] view of positions ([N][3] accepted) and argument checks the C ABI cannot make: every float
+    array of the call shares the positions' dtype (one in_dtype), form_factors has N entries, q has 3 columns."""
+    if positions.dim() == 2:
+        positions = positions.unsqueeze(0)
+    if positions.dim() != 3 or positions.shape[2] != 3:
+        raise ValueError(f"xpcs: positions must be [T][N][3] (got {tuple(positions.shape)})")
+    for t in (form_factors, q_vectors) + tuple(same_dtype):
+        if t is not None and t.dtype != positions.dtype:
+            raise TypeError(f"xpcs: all float arrays of a call share the positions' dtype ({positions.dtype}, got {t.dtype})")
+    if form_factors is not None and form_factors.numel() != positions.shape[1]:
+        raise ValueError(f"xpcs: form_factors has {form_factors.numel()} entries for N = {positions.shape[1]} atoms")
+    if q_vectors is not None and (q_vectors.dim() != 2 or q_vectors.shape[1] != 3):
+        raise ValueError(f"xpcs: q_vectors must be [n_q][3] (got {tuple(q_vectors.shape)})")
+    return positions
 
 
 def xpcs_intensity_volume(positions, form_factors, vol: QVolume, species=None, f_q=None, out=None, out_dtype=None,
@@ -208,7 +221,7 @@ def xpcs_intensity_volume(positions, form_factors, vol: QVolume, species=None, f
     """Eq.(7)-(8) on a 3-D lattice block (species/f_q: q-dependent form factors) -> I [T][n_l * n_h * n_k]
     (amplitude=True: p as [..][2])."""
     import torch
-    positions = _positions3(positions)
+    positions = _positions3(positions, f_q, form_factors=form_factors)
     T, N = positions.shape[0], positions.shape[1]
     ind = _dtype_code(positions)
     outd = ind if out_dtype is None else out_dtype
@@ -228,7 +241,7 @@ def xpcs_intensity_species(positions, species, f_q, q_vectors, box_L, out=None, 
                            profile=False, amplitude=False):
     """Eq.(7)-(8) at an explicit q list with q-dependent form factors f_q [n_species][n_q] -> I [T][n_q]."""
     import torch
-    positions = _positions3(positions)
+    positions = _positions3(positions, f_q, q_vectors=q_vectors)
     T, N = positions.shape[0], positions.shape[1]
     n_q = q_vectors.shape[0]
     ind = _dtype_code(positions)
@@ -263,8 +276,7 @@ def xpcs_form_factor_gaussian(a, b, c, q_vectors=None, vol: QVolume = None, out_
 def xpcs_intensity(positions, form_factors, q_vectors, box_L, out=None, out_dtype=None, stream=None, profile=False):
     """Eq.(7)-(8) at an explicit q list.  positions [T][N][3], q [n_q][3] (same dtype), -> I [T][n_q]."""
     import torch
-    if positions.dim() == 2:
-        positions = positions.unsqueeze(0)
+    positions = _positions3(positions, form_factors=form_factors, q_vectors=q_vectors)
     T, N = positions.shape[0], positions.shape[1]
     n_q = q_vectors.shape[0]
     ind = _dtype_code(positions)
@@ -281,8 +293,7 @@ def xpcs_intensity_grid(positions, form_factors, grid: QGrid, out=None, out_dtyp
                         stream=None, profile=False):
     """Eq.(7)-(8) on a reciprocal-lattice plane (exact integer phases).  -> I [T][n_h * n_k]."""
     import torch
-    if positions.dim() == 2:
-        positions = positions.unsqueeze(0)
+    positions = _positions3(positions, form_factors=form_factors)
     T, N = positions.shape[0], positions.shape[1]
     ind = _dtype_code(positions)
     outd = ind if out_dtype is None else out_dtype
@@ -298,8 +309,7 @@ def xpcs_intensity_grid(positions, form_factors, grid: QGrid, out=None, out_dtyp
 def xpcs_amplitude(positions, form_factors, q_vectors, box_L, out=None, out_dtype=None, stream=None):
     """Eq.(7) complex amplitude at an explicit q list -> [T][n_q][2] (Re, Im)."""
     import torch
-    if positions.dim() == 2:
-        positions = positions.unsqueeze(0)
+    positions = _positions3(positions, form_factors=form_factors, q_vectors=q_vectors)
     T, N = positions.shape[0], positions.shape[1]
     n_q = q_vectors.shape[0]
     ind = _dtype_code(positions)
@@ -316,8 +326,7 @@ def xpcs_amplitude_grid(positions, form_factors, grid: QGrid, out=None, out_dtyp
                         stream=None):
     """Eq.(7) complex amplitude on a lattice plane -> [T][n_h * n_k][2] (Re, Im)."""
     import torch
-    if positions.dim() == 2:
-        positions = positions.unsqueeze(0)
+    positions = _positions3(positions, form_factors=form_factors)
     T, N = positions.shape[0], positions.shape[1]
     ind = _dtype_code(positions)
     outd = ind if out_dtype is None else out_dtype
@@ -375,7 +384,7 @@ def xpcs_intensity_fft(positions, block: QVolume, n_grid, eta, k_cut=0, f_q=None
                        stream=None, profile=False):
     """Algorithm 2 (FFT method): I on an axis-aligned block of the n_grid^3 FFT grid -> [T][n_l * n_h * n_k]."""
     import torch
-    positions = _positions3(positions)
+    positions = _positions3(positions, f_q)
     T, N = positions.shape[0], positions.shape[1]
     ind = _dtype_code(positions)
     outd = ind if out_dtype is None else out_dtype

@@ -139,3 +139,20 @@ def test_fft_method_validation(lib):
     rc = lib.xpcs_intensity_fft(dummy, 10, 1, ctypes.byref(ok), 32, -1.0, 0, None, dummy, ctypes.byref(o))
     assert rc == _lib.XPCS_EINVAL and b"eta" in lib.xpcs_last_error()
     assert lib.xpcs_launch_count() == n0
+
+
+def test_binding_argument_checks():
+    """The binding refuses mixed dtypes and mis-shaped arrays before calling the library (the C ABI takes one
+    in_dtype for every float array of a call)."""
+    torch = pytest.importorskip("torch")
+    from paper_2204_13241_b200._lib import _positions3
+    pos = torch.zeros(2, 5, 3)
+    assert _positions3(pos[0]).shape == (1, 5, 3)
+    with pytest.raises(ValueError, match=r"\[T\]\[N\]\[3\]"):
+        _positions3(torch.zeros(2, 5, 2))
+    with pytest.raises(TypeError, match="dtype"):
+        _positions3(pos, form_factors=torch.zeros(5, dtype=torch.float64))
+    with pytest.raises(ValueError, match="form_factors"):
+        _positions3(pos, form_factors=torch.zeros(4))
+    with pytest.raises(ValueError, match="q_vectors"):
+        _positions3(pos, q_vectors=torch.zeros(7, 2))
