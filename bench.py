@@ -267,6 +267,14 @@ def main():
     tc_used = bool(cfg.n_plane) and wl.in_dtype == xp.F32 and engine != xp.ENGINE_SIMT and \
         xp.engine_available(xp.ENGINE_TENSOR)
     i8_used = tc_used and xp.engine_resolved(engine, f_h is None) == xp.ENGINE_TENSOR_I8
+    hybrid_share = None          # fraction of the pairs on the integer engine when kinds are split between engines
+    if tc_used and engine == xp.ENGINE_AUTO and wl.kinds is not None:
+        counts = np.bincount(wl.kinds, minlength=len(wl.kind_f))
+        on_i8 = xp.species_engines(counts, wl.kind_f)
+        share = float(sum(c for c, e in zip(counts, on_i8) if e)) / float(counts.sum())
+        if 0.0 < share < 1.0:
+            hybrid_share = share
+        i8_used = share == 1.0
     # the tensor peak: MEASURED_PEAKS' burst bf16 figure (cuBLAS at full clock) when the SM clock stayed at its max
     # through the timed region (no power capping: the kernel ran at the clock the burst figure was taken at), else
     # the sustained figure (cuBLAS back to back for 4 s, power-capped clocks)
@@ -278,6 +286,15 @@ def main():
         peak = sm_count * 16 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 2 / 1e12
         roof = {"bound": "alu", "unit": "Tpairs/s (XU: 2 MUFU per pair)", "peak": peak,
                 "achieved": pairs_launch / (per_launch_ms / 1e3) / 1e12}
+    elif hybrid_share is not None:
+        # kinds split between the integer (int8, 2x rate) and split-FP16 engines: 24 ops per pair on both; the
+        # peak is the pair-weighted harmonic blend, over the whole intensity stage of a step (both kernels)
+        peak = 1.0 / (hybrid_share / (2.0 * tensor_peak) + (1.0 - hybrid_share) / tensor_peak)
+        stage_ms = main_ms / max(args.steps, 1)
+        roof = {"bound": "tensor", "unit": "T ops/s (int8 + fp16 blend)", "peak": peak,
+                "achieved": 24.0 * pairs_step / (stage_ms / 1e3) / 1e12, "int8_pair_share": hybrid_share}
+        per_launch_ms = stage_ms
+        pairs_launch = pairs_step
     elif i8_used:
         # tcgen05 kind::i8: 3 int8 limb products x 4 real MAC = 24 int8 ops per pair vs the int8 dense peak =
         # 2 x the measured bf16 (= fp16) peak (B200: 4.5 POPS int8 vs 2.25 PFLOP/s fp16 nominal; tools/mma_rate.cu
@@ -299,10 +316,12 @@ def main():
     if wl.in_dtype == xp.F64:
         # config 1 (4.1e6 pairs, FP64): launch/latency-bound; the FP32 figure above is context only
         roof["note"] = "FP64 workload: latency-bound, report ms_per_step; frac against the FP32 pipe is context only"
-    eng_name = "i8" if i8_used else ("tensor" if tc_used else ("simt" if cfg.n_plane else "generic"))
+    eng_name = "i8+tensor" if hybrid_share is not None else \
+        ("i8" if i8_used else ("tensor" if tc_used else ("simt" if cfg.n_plane else "generic")))
     roof["traffic"] = _traffic(cfg.name, eng_name, pairs_launch)
-    roof["peak_source"] = (f"{peak_src}, {'burst' if at_max else 'sustained'} bf16"
-                           + (" x 2 (int8)" if i8_used else "")) if roof["bound"] == "tensor" else "derived (DESIGN.md)"
+    tensor_src = (f"{peak_src}, {'burst' if at_max else 'sustained'} bf16"
+                  + (" x 2 (int8)" if i8_used else (" blended int8/fp16" if hybrid_share else "")))
+    roof["peak_source"] = tensor_src if roof["bound"] == "tensor" else "derived (DESIGN.md)"
     roof["kernel_ms"] = per_launch_ms
     roof["kernel_share_of_step"] = main_ms / args.steps / ms if ms > 0 else None
 

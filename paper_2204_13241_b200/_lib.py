@@ -63,7 +63,7 @@ class QVolume(ctypes.Structure):
 
 class Species(ctypes.Structure):
     _fields_ = [("n_species", ctypes.c_int32), ("pad_", ctypes.c_int32), ("species", ctypes.POINTER(ctypes.c_int32)),
-                ("f_q", ctypes.c_void_p)]
+                ("f_q", ctypes.c_void_p), ("f_max", ctypes.POINTER(ctypes.c_double))]
 
 
 _lib = None
@@ -188,15 +188,20 @@ def qvolume(L, h0, n_h, k0, n_k, l0, n_l, m0=(0, 0, 0), ma=(1, 0, 0), mb=(0, 1, 
     return v
 
 
-def species_desc(species, f_q):
-    """xpcs_species from a host int array species [N] and a device table f_q [n_species][n_q] (kept alive by the
-    returned tuple's second element)."""
+def species_desc(species, f_q, f_max=None):
+    """xpcs_species from a host int array species [N], a device table f_q [n_species][n_q] and optional host
+    per-kind max |f_s| hints (kept alive by the returned tuple's second element)."""
     sp = np.ascontiguousarray(np.asarray(species, dtype=np.int32))
     d = Species()
     d.n_species = int(f_q.shape[0])
     d.species = sp.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
     d.f_q = _ptr(f_q)
-    return d, (sp, f_q)
+    fm = None
+    if f_max is not None:
+        fm = np.ascontiguousarray(np.asarray(f_max, dtype=np.float64))
+        assert fm.shape == (d.n_species,)
+        d.f_max = fm.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    return d, (sp, f_q, fm)
 
 
 def _positions3(positions, *same_dtype, form_factors=None, q_vectors=None):
@@ -217,7 +222,7 @@ def _positions3(positions, *same_dtype, form_factors=None, q_vectors=None):
 
 
 def xpcs_intensity_volume(positions, form_factors, vol: QVolume, species=None, f_q=None, out=None, out_dtype=None,
-                          engine=ENGINE_AUTO, stream=None, profile=False, amplitude=False):
+                          engine=ENGINE_AUTO, stream=None, profile=False, amplitude=False, f_max=None):
     """Eq.(7)-(8) on a 3-D lattice block (species/f_q: q-dependent form factors) -> I [T][n_l * n_h * n_k]
     (amplitude=True: p as [..][2])."""
     import torch
@@ -229,7 +234,7 @@ def xpcs_intensity_volume(positions, form_factors, vol: QVolume, species=None, f
     if out is None:
         out = torch.empty(shape, dtype=torch.float64 if outd == F64 else torch.float32, device=positions.device)
     o = make_opts(ind, outd, stream, engine, profile)
-    sp, keep = (species_desc(species, f_q) if species is not None else (None, None))
+    sp, keep = (species_desc(species, f_q, f_max) if species is not None else (None, None))
     fn = load().xpcs_amplitude_volume if amplitude else load().xpcs_intensity_volume
     _check(fn(_ptr(positions), N, _ptr(form_factors), ctypes.byref(sp) if sp is not None else None,
               ctypes.byref(vol), T, _ptr(out), ctypes.byref(o)))
@@ -238,7 +243,7 @@ def xpcs_intensity_volume(positions, form_factors, vol: QVolume, species=None, f
 
 
 def xpcs_intensity_species(positions, species, f_q, q_vectors, box_L, out=None, out_dtype=None, stream=None,
-                           profile=False, amplitude=False):
+                           profile=False, amplitude=False, f_max=None):
     """Eq.(7)-(8) at an explicit q list with q-dependent form factors f_q [n_species][n_q] -> I [T][n_q]."""
     import torch
     positions = _positions3(positions, f_q, q_vectors=q_vectors)
@@ -250,7 +255,7 @@ def xpcs_intensity_species(positions, species, f_q, q_vectors, box_L, out=None, 
     if out is None:
         out = torch.empty(shape, dtype=torch.float64 if outd == F64 else torch.float32, device=positions.device)
     o = make_opts(ind, outd, stream, ENGINE_AUTO, profile)
-    sp, keep = species_desc(species, f_q)
+    sp, keep = species_desc(species, f_q, f_max)
     fn = load().xpcs_amplitude_species if amplitude else load().xpcs_intensity_species
     _check(fn(_ptr(positions), N, ctypes.byref(sp), _ptr(q_vectors), n_q, T, float(box_L), _ptr(out),
               ctypes.byref(o)))
@@ -478,6 +483,24 @@ def engine_resolved(engine, uniform_f=True) -> int:
 
 
 AUTO_I8 = True    # AUTO routes uniform-f lattice calls to the integer engine (mirrors api.cu)
+
+
+def species_engines(counts, f_max=None):
+    """Mirror of api.cu's AUTO rule for species calls: kinds in increasing |f_max| run on the integer engine while
+    sum (f_max / f_min)^2 N_s / N <= 1, the rest on the split-FP16 engine.  Returns a list of bools (True = int8)."""
+    counts = [int(c) for c in counts]
+    n = len(counts)
+    if f_max is None:
+        return [True] * n
+    order = sorted(range(n), key=lambda k: abs(f_max[k]))
+    fref = next((abs(f_max[k]) for k in order if counts[k] > 0 and abs(f_max[k]) > 0), 0.0)
+    total = max(1, sum(counts))
+    out, budget = [False] * n, 0.0
+    for k in order:
+        w = f_max[k] / fref if fref > 0 else 1.0
+        budget += w * w * counts[k] / total
+        out[k] = budget <= 1.0 + 1e-12
+    return out
 
 
 def launch_count() -> int:

@@ -459,6 +459,31 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
     }
     TRY(upload_groups(G, o.s));
     const int ng = G.count();
+    // engine per atom group.  AUTO with species: the integer engine's limb error grows with the kind's weight, so
+    // kinds are taken in increasing max |f_s| (species->f_max, host hints; absent = all equal) while the integer
+    // share of the error budget, sum f_max^2 N_s / (f_ref^2 N) with f_ref the smallest weight, stays <= 1 -- the
+    // single-species f = 1 level validated against the gate; the heavier kinds run on the split-FP16 engine.
+    std::vector<char> gi8((size_t)ng, i8 ? 1 : 0);
+    if (G.n_species && o.engine == XPCS_ENGINE_AUTO && (i8 || tc) && species->f_max) {
+        std::vector<int> order((size_t)ng);
+        for (int k = 0; k < ng; ++k) order[(size_t)k] = k;
+        std::sort(order.begin(), order.end(), [&](int a, int b) { return std::fabs(species->f_max[a]) < std::fabs(species->f_max[b]); });
+        double fref = 0.0;
+        for (int k : order) if (G.cnt[k] > 0 && std::fabs(species->f_max[k]) > 0.0) { fref = std::fabs(species->f_max[k]); break; }
+        double budget = 0.0;
+        for (int k : order) {
+            const double w = fref > 0.0 ? species->f_max[k] / fref : 1.0;
+            budget += w * w * (double)G.cnt[k] / (double)N;
+            gi8[(size_t)k] = budget <= 1.0 + 1e-12 ? 1 : 0;
+        }
+    }
+    bool any_i8 = false, any_tc = false;
+    for (int k = 0; k < ng; ++k) {
+        if (G.cnt[k] == 0) continue;
+        if (gi8[(size_t)k] && (i8 || tc)) any_i8 = true;
+        else if (i8 || tc) any_tc = true;
+    }
+    if (G.n_species && o.engine == XPCS_ENGINE_AUTO && (i8 || tc)) { i8 = any_i8; tc = any_tc; }
     SpeciesParts sp{};
     sp.n = G.n_species;
     if (o.in_f64) {
@@ -505,7 +530,8 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
         const int64_t Ng = G.cnt[gi];
         if (Ng == 0) continue;
         int64_t ch = 4096;
-        if (i8) {
+        const bool g_i8 = i8 && gi8[(size_t)gi], g_tc = (i8 || tc) && !g_i8;
+        if (g_i8) {
             // exact int32 accumulation: chunks only balance the grid (clusters of 2 CTAs, one CTA per SM) and stay
             // <= kI8MaxChunk.  Cost model in 32-atom stage units: waves x (stages per CTA + a fixed per-CTA cost of
             // ~15 stages for the prologue, the single drain and the cluster teardown); the smallest C wins ties.
@@ -522,7 +548,7 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
             }
             ch = ((Ng + best - 1) / best + 31) / 32 * 32;
             ch = std::min<int64_t>(ch, kI8MaxChunk);
-        } else if (tc) {
+        } else if (g_tc) {
             const int64_t tiles = ((g.n_h + 127) / 128) * ((g.n_k + 127) / 128);
             const int64_t units = tiles * std::min<int64_t>(V, 64);
             int64_t C0 = std::max<int64_t>(1, (8LL * sm_count() + units - 1) / units);
@@ -565,9 +591,10 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
             { ProfScope p(o.profile, KC_STAGE, o.s);
               TRY(cuda_fail(launch_stage_lattice32(positions, 0, form_factors, 0, Ng, vb, g, m, st + stoff, o.s), "stage")); }
             { ProfScope p(o.profile, KC_MAIN, o.s);
-              if (i8) TRY(cuda_fail(launch_lattice_i8(st + stoff, Ng, vb, g, chunk[gi], C[gi], fmax, form_factors == nullptr,
+              const bool g_i8 = i8 && gi8[(size_t)gi], g_tc = (i8 || tc) && !g_i8;
+              if (g_i8) TRY(cuda_fail(launch_lattice_i8(st + stoff, Ng, vb, g, chunk[gi], C[gi], fmax, form_factors == nullptr,
                                                       part + poff, o.s), "lattice tcgen05 i8"));
-              else if (tc) TRY(cuda_fail(launch_lattice_tc(st + stoff, Ng, vb, g, chunk[gi], C[gi], part + poff, o.s), "lattice tcgen05"));
+              else if (g_tc) TRY(cuda_fail(launch_lattice_tc(st + stoff, Ng, vb, g, chunk[gi], C[gi], part + poff, o.s), "lattice tcgen05"));
               else TRY(cuda_fail(launch_lattice_simt(st + stoff, Ng, vb, g, chunk[gi], C[gi], part + poff, o.s), "lattice simt")); }
             stoff += Ng * vb;
             poff += C[gi] * n_q * vb;

@@ -34,6 +34,10 @@ class Workload:
     n_bins: int = 32
     in_dtype: int = X.F32
     engine: int = X.ENGINE_AUTO
+    # optional atom kinds for per-atom form factors with few distinct values (f_j = kind_f[kinds[j]]): the intensity
+    # then goes through the species path, which lets AUTO put the light kinds on the integer engine
+    kinds: np.ndarray | None = None
+    kind_f: tuple = ()
 
 
 class Pipeline:
@@ -55,6 +59,13 @@ class Pipeline:
         X.xpcs_rings_register(self.bins, wl.n_bins, stream)
         self._registered = True
         odt = torch.float64 if wl.in_dtype == X.F64 else torch.float32
+        self.kind_fq = None
+        if wl.kinds is not None and self.grid is not None:
+            # constant rows f_s(q) = kind_f[s] on the plane, as the 3-D block of one l-plane
+            self.vol = X.qvolume(wl.L, self.grid.h0, self.grid.n_h, self.grid.k0, self.grid.n_k, 0, 1,
+                                 m0=tuple(self.grid.m0), ma=tuple(self.grid.ma), mb=tuple(self.grid.mb))
+            kf = torch.tensor(list(wl.kind_f), dtype=odt, device=self.device)
+            self.kind_fq = kf[:, None].expand(len(wl.kind_f), self.n_q).contiguous()
         self.I = torch.empty((wl.T, self.n_q), dtype=odt, device=self.device)
         self.g2 = torch.empty((len(wl.lags), self.n_q), dtype=torch.float32, device=self.device) if wl.lags else None
 
@@ -76,7 +87,10 @@ class Pipeline:
 
     def run(self, positions: torch.Tensor, form_factors: torch.Tensor | None, profile=False) -> dict:
         wl, s = self.wl, self.stream
-        if self.grid is not None:
+        if self.kind_fq is not None:
+            X.xpcs_intensity_volume(positions, None, self.vol, species=wl.kinds, f_q=self.kind_fq, out=self.I,
+                                    engine=wl.engine, stream=s, profile=profile, f_max=wl.kind_f)
+        elif self.grid is not None:
             X.xpcs_intensity_grid(positions, form_factors, self.grid, out=self.I, engine=wl.engine, stream=s,
                                   profile=profile)
         else:
@@ -138,7 +152,10 @@ class Pipeline:
             sc.wait_event(ev_in[bi])
             pos_b = self.d_pos[t0:t1]
             I_b = self.I[t0:t1]
-            if self.grid is not None:
+            if self.kind_fq is not None:
+                X.xpcs_intensity_volume(pos_b, None, self.vol, species=wl.kinds, f_q=self.kind_fq, out=I_b,
+                                        engine=wl.engine, stream=sc, f_max=wl.kind_f)
+            elif self.grid is not None:
                 X.xpcs_intensity_grid(pos_b, self.d_f, self.grid, out=I_b, engine=wl.engine, stream=sc)
             else:
                 X.xpcs_intensity(pos_b, self.d_f, wl.q, wl.L, out=I_b, stream=sc)
@@ -188,8 +205,13 @@ def workload_from_config(cfg, device="cuda", stream=None) -> Workload:
     import xpcs_inputs as xi
     in_dtype = X.F64 if cfg.dtype == "f64" else X.F32
     if cfg.n_plane:
+        kinds, kind_f = None, ()
+        if cfg.two_species and in_dtype == X.F32:
+            f = xi.form_factors(cfg)
+            kind_f = tuple(float(v) for v in np.unique(f))
+            kinds = np.searchsorted(np.asarray(kind_f, dtype=f.dtype), f).astype(np.int32)
         return Workload(cfg.name, cfg.N, cfg.L, cfg.T, n_plane=cfg.n_plane, lags=tuple(cfg.lags),
-                        windows=tuple(cfg.windows), n_bins=cfg.n_bins, in_dtype=in_dtype)
+                        windows=tuple(cfg.windows), n_bins=cfg.n_bins, in_dtype=in_dtype, kinds=kinds, kind_f=kind_f)
     q = X.xpcs_qgrid_ewald(xi.EWALD_WAVELENGTH_SIGMA, cfg.detector, cfg.detector, xi.EWALD_PITCH_RAD,
                            out_dtype=in_dtype, device=device, stream=stream)
     return Workload(cfg.name, cfg.N, cfg.L, cfg.T, n_plane=0, q=q, q_max=xi.EWALD_QMAX, lags=tuple(cfg.lags),

@@ -233,7 +233,10 @@ def test_config2_simt_engine_sampled():
 
 
 def test_end_to_end_host_path_matches_device_path():
-    """pipeline.run_host (pinned H2D in frame batches on 3 streams, D2H of every result) == pipeline.run."""
+    """pipeline.run_host (pinned H2D in frame batches on 4 streams, D2H of every result) == pipeline.run.  The
+    integer engine sizes its atom chunks by the frames of each call, so the host path's smaller batches fold the
+    same exact per-chunk sums in different fp32 partials: results agree to fp32 rounding, not bit for bit; the
+    second run_host of the same batches is bit-identical to the first (determinism)."""
     cfg = xi.scaled(xi.CONFIGS["c3"], N=5000, T=37, lags=(1, 2, 5, 9), windows=(1, 2, 4, 8))
     cfg = xi.Config(**{**cfg.__dict__, "n_plane": 128})
     pos = xi.positions(cfg)
@@ -243,10 +246,20 @@ def test_end_to_end_host_path_matches_device_path():
     dev = P.run(_t(pos), _t(f))
     ref = {k: v.cpu().numpy().copy() for k, v in dev.items()}
     P.alloc_host_io(pos, f, batches=5)
+    first = None
     for _ in range(2):
         host = P.run_host()
         torch.cuda.synchronize()
         for k in ref:
-            np.testing.assert_array_equal(host[k].numpy(), ref[k], err_msg=k)
+            a = host[k].numpy().astype(np.float64)
+            b = ref[k].astype(np.float64)
+            ok = np.isfinite(b)
+            assert np.array_equal(np.isfinite(a), ok), k
+            np.testing.assert_allclose(a[ok], b[ok], rtol=2e-5, atol=2e-5 * np.abs(b[ok]).max(), err_msg=k)
+        if first is None:
+            first = {k: v.numpy().copy() for k, v in host.items()}
+        else:
+            for k in first:
+                np.testing.assert_array_equal(host[k].numpy(), first[k], err_msg=k)
     h2d, d2h = P.io_bytes()
     assert h2d == pos.nbytes + f.nbytes and d2h > pos.shape[0] * 128 * 128 * 4

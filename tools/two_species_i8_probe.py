@@ -1,6 +1,7 @@
-"""Precision probe: two-species configs (f = 1, 2) on the integer engine through the species path (kinds with
-constant f_s(q) rows) vs the FP64 oracle, on sampled pixels of full-size c3 / c5 frames.  Prints the worst
-|dI| / (1e-3 N + 1e-5 I) and the rms |dI|/N for the integer and split-FP16 engines."""
+"""Precision probe: two-species configs (f = 1, 2) through the species path (kinds with constant f_s(q) rows) vs the
+FP64 oracle, on sampled pixels of full-size c3 / c5 frames: both kinds on the integer engine, the AUTO hybrid
+(f = 1 kind on the integer engine, f = 2 kind on split-FP16, from the f_max hints), and split-FP16 with per-atom f.
+Prints the worst |dI| / (1e-3 N + 1e-5 I) and the rms |dI|/N."""
 import json
 import os
 import sys
@@ -30,10 +31,12 @@ for name, frames in (("c3", [0, 500, 999]), ("c5", [0, 199])):
     fq[1] = 2.0
     d = torch.from_numpy(pos).cuda()
     res = {}
-    for eng_name, eng in (("i8_species", xp.ENGINE_TENSOR_I8), ("fp16_peratom", xp.ENGINE_TENSOR)):
-        if eng_name == "i8_species":
+    for eng_name, eng in (("i8_species", xp.ENGINE_TENSOR_I8), ("hybrid_auto", xp.ENGINE_AUTO),
+                          ("fp16_peratom", xp.ENGINE_TENSOR)):
+        if eng_name != "fp16_peratom":
             v = xp.qvolume(cfg.L, -n // 2, n, -n // 2, n, 0, 1)
-            I = xp.xpcs_intensity_volume(d, None, v, species=sp, f_q=fq, engine=eng).cpu().numpy()
+            I = xp.xpcs_intensity_volume(d, None, v, species=sp, f_q=fq, engine=eng,
+                                         f_max=[1.0, 2.0] if eng_name == "hybrid_auto" else None).cpu().numpy()
         else:
             I = xp.xpcs_intensity_grid(d, torch.from_numpy(f).cuda(), g, engine=eng).cpu().numpy()
         err = np.abs(I[:, pix] - ref)
