@@ -156,3 +156,15 @@ def test_binding_argument_checks():
         _positions3(pos, form_factors=torch.zeros(4))
     with pytest.raises(ValueError, match="q_vectors"):
         _positions3(pos, q_vectors=torch.zeros(7, 2))
+
+
+def test_species_engine_rule():
+    """AUTO's per-kind engine choice (mirror of api.cu): light kinds on the integer engine while
+    sum (f_max / f_min)^2 N_s / N <= 1."""
+    se = xp.species_engines
+    assert se([1000], [1.0]) == [True]
+    assert se([500, 500], [1.0, 2.0]) == [True, False]          # c3/c5: f = 1 half only
+    assert se([300, 700], [2.0, 1.0]) == [False, True]
+    assert se([400, 400, 200], [1.0, 1.0, 1.0]) == [True, True, True]
+    assert se([10, 10], None) == [True, True]                   # no hints: every kind
+    assert se([0, 100], [0.5, 1.0])[1] is True                  # an empty kind does not set the reference weight

@@ -163,3 +163,23 @@ def test_table1_grid():
         qp = oracle.lattice_q(t1["L"], -h, t1["n"], -h, t1["n"], m0=(0, 0, il - h))
         ref = oracle.intensity(pos, None, qp, t1["L"])[0].reshape(t1["n"], t1["n"])
         assert_pixels(I[il], ref, t1["N"], f"table1 l-plane {il}")
+
+
+def test_species_hybrid_auto_parity():
+    """AUTO with f_max hints splits kinds between the integer and split-FP16 engines (heavy kind on FP16); parity at
+    the per-kind gate, and the amplitude of the mixed engines (both hold conj(p) partials)."""
+    cfg = xi.scaled(xi.CONFIGS["c3"], N=7001, T=2)
+    pos = xi.positions(cfg)
+    f = xi.form_factors(cfg)
+    sp = (f > 1.5).astype(np.int32)
+    v = xp.qvolume(cfg.L, -60, 120, -40, 150, 0, 1)
+    q = _vol_q(v)
+    fq = np.stack([np.full(q.shape[0], 1.0), np.full(q.shape[0], 2.0)]).astype(np.float32)
+    I = xp.xpcs_intensity_volume(_t(pos), None, v, species=sp, f_q=_t(fq), f_max=[1.0, 2.0]).cpu().numpy()
+    ref = oracle.intensity(pos, f.astype(np.float64), q, cfg.L)
+    assert_pixels(I, ref, cfg.N, "species hybrid")
+    A = xp.xpcs_intensity_volume(_t(pos), None, v, species=sp, f_q=_t(fq), f_max=[1.0, 2.0], amplitude=True)
+    A = A.cpu().numpy().astype(np.float64)
+    Aref = oracle.amplitudes(pos, f.astype(np.float64), q, cfg.L)
+    err = np.abs(A[..., 0] + 1j * A[..., 1] - Aref)
+    assert np.max(err / (1e-3 * np.sqrt(cfg.N) + 1e-5 * np.abs(Aref))) <= 1.0
