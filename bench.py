@@ -270,8 +270,7 @@ def main():
     hybrid_share = None          # fraction of the pairs on the integer engine when kinds are split between engines
     if tc_used and engine == xp.ENGINE_AUTO and wl.kinds is not None:
         counts = np.bincount(wl.kinds, minlength=len(wl.kind_f))
-        on_i8 = xp.species_engines(counts, wl.kind_f)
-        share = float(sum(c for c, e in zip(counts, on_i8) if e)) / float(counts.sum())
+        share = float(sum(xp.species_engines(counts, wl.kind_f))) / float(counts.sum())
         if 0.0 < share < 1.0:
             hybrid_share = share
         i8_used = share == 1.0

@@ -141,8 +141,9 @@ typedef struct {
     const int32_t* species;
     const void* f_q;
     const double* f_max;   /* HOST [n_species] or NULL: max_q |f_s(q)| per kind, a hint for AUTO's engine choice
-                              (lightest kinds on the integer engine while sum f_max^2 N_s / (f_min^2 N) <= 1, heavier
-                              kinds on the split-FP16 engine; NULL: every kind on the integer engine) */
+                              (lightest kinds on the integer engine while sum f_max^2 N_s / (f_min^2 N) <= 1, the kind
+                              crossing the budget split at it, the rest on the split-FP16 engine; NULL: every kind on
+                              the integer engine) */
 } xpcs_species;
 
 /* xpcs_intensity_volume / xpcs_amplitude_volume: I (or p, as (re, im) pairs) on a 3-D lattice block for every

@@ -7,6 +7,7 @@ only things PyTorch provides); host-side integer lists (lags, windows) are plain
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 
 import numpy as np
@@ -486,20 +487,29 @@ AUTO_I8 = True    # AUTO routes uniform-f lattice calls to the integer engine (m
 
 
 def species_engines(counts, f_max=None):
-    """Mirror of api.cu's AUTO rule for species calls: kinds in increasing |f_max| run on the integer engine while
-    sum (f_max / f_min)^2 N_s / N <= 1, the rest on the split-FP16 engine.  Returns a list of bools (True = int8)."""
+    """Mirror of api.cu's AUTO rule for species calls: kinds in increasing |f_max| go to the integer engine while
+    sum (f_max / f_min)^2 N_s / N <= 1; the kind that crosses the budget is split (its first atoms on the integer
+    engine up to the budget), the rest run on split-FP16.  Returns the number of atoms of each kind on the integer
+    engine."""
     counts = [int(c) for c in counts]
     n = len(counts)
     if f_max is None:
-        return [True] * n
+        return list(counts)
     order = sorted(range(n), key=lambda k: abs(f_max[k]))
     fref = next((abs(f_max[k]) for k in order if counts[k] > 0 and abs(f_max[k]) > 0), 0.0)
     total = max(1, sum(counts))
-    out, budget = [False] * n, 0.0
+    out, budget = [0] * n, 0.0
     for k in order:
-        w = f_max[k] / fref if fref > 0 else 1.0
-        budget += w * w * counts[k] / total
-        out[k] = budget <= 1.0 + 1e-12
+        w2 = (f_max[k] / fref) ** 2 if fref > 0 else 1.0
+        room = 1.0 + 1e-12 - budget
+        take = counts[k]
+        if room <= 0:
+            take = 0
+        elif w2 * counts[k] / total > room:
+            take = int(math.floor(room * total / w2))
+        take = min(take, counts[k])
+        out[k] = take
+        budget += w2 * take / total
     return out
 
 

@@ -224,6 +224,7 @@ int xpcs_engine_available(int32_t engine) {
 struct Groups {
     int n_species = 0;                       // 0: no species
     std::vector<int64_t> off, cnt;           // per group: offset into the permutation, atom count
+    std::vector<int32_t> kind;               // per group: species row of f_q (a kind may be split into two groups)
     const int32_t* d_idx = nullptr;          // device permutation (species only)
     std::vector<int32_t> perm;               // host permutation (stable partition by kind)
     const void* fq = nullptr;
@@ -236,14 +237,15 @@ static int prep_groups(const xpcs_species* sp, const void* form_factors, int64_t
     if (!sp) {
         G.off.assign(1, 0);
         G.cnt.assign(1, N);
+        G.kind.assign(1, 0);
         return XPCS_OK;
     }
     if (form_factors) {
         set_error("xpcs: form_factors and species are exclusive (fold per-atom weights into f_q)");
         return XPCS_EINVAL;
     }
-    if (sp->n_species < 1 || sp->n_species > kMaxSpecies) {
-        set_error("xpcs: n_species must be in [1, %d] (got %d)", kMaxSpecies, sp->n_species);
+    if (sp->n_species < 1 || sp->n_species > kMaxKinds) {
+        set_error("xpcs: n_species must be in [1, %d] (got %d)", kMaxKinds, sp->n_species);
         return XPCS_EINVAL;
     }
     NEED(sp->species, "species->species");
@@ -266,6 +268,8 @@ static int prep_groups(const xpcs_species* sp, const void* form_factors, int64_t
     }
     G.off.assign(S, 0);
     for (int k = 1; k < S; ++k) G.off[k] = G.off[k - 1] + G.cnt[k - 1];
+    G.kind.resize(S);
+    for (int k = 0; k < S; ++k) G.kind[k] = k;
     G.perm.resize((size_t)N);
     std::vector<int64_t> fill(G.off);
     for (int64_t j = 0; j < N; ++j) G.perm[(size_t)fill[sp->species[j]]++] = (int32_t)j;
@@ -322,7 +326,8 @@ static int run_direct(const void* positions, int64_t N, const void* form_factors
     const size_t isz = out_size(o.out_f64) * (amp ? 2 : 1);
     const int ng = G.count();
     SpeciesParts sp{};
-    sp.n = G.n_species;
+    sp.n = G.n_species ? ng : 0;
+    for (int k = 0; k < ng && k < kMaxSpecies; ++k) sp.kind[k] = G.kind[k];
     sp.part_f64 = 1;
     if (o.in_f64) {
         const int64_t per_frame = std::max<int64_t>(32 * N, 16 * n_q * ng);
@@ -458,25 +463,50 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
         tc = avail && !i8;
     }
     TRY(upload_groups(G, o.s));
-    const int ng = G.count();
+    int ng = G.count();
     // engine per atom group.  AUTO with species: the integer engine's limb error grows with the kind's weight, so
     // kinds are taken in increasing max |f_s| (species->f_max, host hints; absent = all equal) while the integer
     // share of the error budget, sum f_max^2 N_s / (f_ref^2 N) with f_ref the smallest weight, stays <= 1 -- the
     // single-species f = 1 level validated against the gate; the heavier kinds run on the split-FP16 engine.
     std::vector<char> gi8((size_t)ng, i8 ? 1 : 0);
     if (G.n_species && o.engine == XPCS_ENGINE_AUTO && (i8 || tc) && species->f_max) {
+        // kinds in increasing max|f_s|: whole kinds on the integer engine while the budget allows, the kind that
+        // crosses it split (its first atoms on the integer engine up to the budget), the rest on split-FP16
         std::vector<int> order((size_t)ng);
         for (int k = 0; k < ng; ++k) order[(size_t)k] = k;
         std::sort(order.begin(), order.end(), [&](int a, int b) { return std::fabs(species->f_max[a]) < std::fabs(species->f_max[b]); });
         double fref = 0.0;
         for (int k : order) if (G.cnt[k] > 0 && std::fabs(species->f_max[k]) > 0.0) { fref = std::fabs(species->f_max[k]); break; }
+        std::vector<int64_t> n_int((size_t)ng, 0);
         double budget = 0.0;
         for (int k : order) {
-            const double w = fref > 0.0 ? species->f_max[k] / fref : 1.0;
-            budget += w * w * (double)G.cnt[k] / (double)N;
-            gi8[(size_t)k] = budget <= 1.0 + 1e-12 ? 1 : 0;
+            const double w2 = fref > 0.0 ? (species->f_max[k] / fref) * (species->f_max[k] / fref) : 1.0;
+            const double room = 1.0 + 1e-12 - budget;
+            int64_t take = G.cnt[k];
+            if (room <= 0.0) take = 0;
+            else if (w2 * (double)G.cnt[k] / (double)N > room) take = (int64_t)std::floor(room * (double)N / w2);
+            take = std::min<int64_t>(take, G.cnt[k]);
+            n_int[(size_t)k] = take;
+            budget += w2 * (double)take / (double)N;
         }
+        // regroup: [integer part, FP16 part] per kind (empty parts dropped), kind order kept
+        std::vector<int64_t> off2, cnt2;
+        std::vector<int32_t> kind2;
+        std::vector<char> e2;
+        for (int k = 0; k < ng; ++k) {
+            if (n_int[(size_t)k] > 0) { off2.push_back(G.off[k]); cnt2.push_back(n_int[(size_t)k]); kind2.push_back(G.kind[k]); e2.push_back(1); }
+            if (G.cnt[k] > n_int[(size_t)k]) {
+                off2.push_back(G.off[k] + n_int[(size_t)k]); cnt2.push_back(G.cnt[k] - n_int[(size_t)k]);
+                kind2.push_back(G.kind[k]); e2.push_back(0);
+            }
+        }
+        if ((int)cnt2.size() > kMaxSpecies) {
+            set_error("xpcs: too many atom groups after the engine split");
+            return XPCS_EUNSUPPORTED;
+        }
+        G.off = off2; G.cnt = cnt2; G.kind = kind2; gi8 = e2;
     }
+    ng = G.count();
     bool any_i8 = false, any_tc = false;
     for (int k = 0; k < ng; ++k) {
         if (G.cnt[k] == 0) continue;
@@ -485,7 +515,8 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
     }
     if (G.n_species && o.engine == XPCS_ENGINE_AUTO && (i8 || tc)) { i8 = any_i8; tc = any_tc; }
     SpeciesParts sp{};
-    sp.n = G.n_species;
+    sp.n = G.n_species ? ng : 0;
+    for (int k = 0; k < ng && k < kMaxSpecies; ++k) sp.kind[k] = G.kind[k];
     if (o.in_f64) {
         // FP64: direct per-pixel evaluation with 64-bit turns; with species each kind's amplitude goes to scratch
         sp.part_f64 = 1;

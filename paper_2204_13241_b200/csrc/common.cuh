@@ -131,10 +131,12 @@ cudaError_t launch_stage_generic64(const void* pos, const void* f, int64_t N, in
 // species superposition (q-dependent form factors): out = |sum_s f_s(q) sum_c part_s[c]|^2 (mode 0) or the
 // amplitude (mode 1; mode 2: the partials hold conj(p)).  part_s [C_s][frames][n_q] (float2 | double2);
 // fq [n_species][n_l * n_q] (f32|f64), row of virtual frame v: plane (v0 + v) % n_l.
-constexpr int kMaxSpecies = 16;
+constexpr int kMaxKinds = 16;      // atom kinds a caller may define (xpcs_species.n_species)
+constexpr int kMaxSpecies = 32;    // atom groups of a call (a kind may be split between two engines)
 struct SpeciesParts {
     const void* part[kMaxSpecies];
     int64_t C[kMaxSpecies];
+    int32_t kind[kMaxSpecies];     // f_q row of each group
     int n;
     int part_f64;
 };

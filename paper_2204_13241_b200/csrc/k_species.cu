@@ -28,7 +28,7 @@ __global__ void __launch_bounds__(256) k_species_combine(SpeciesParts sp, int64_
                 pr += (double)w.x;
                 pi += (double)w.y;
             }
-            const double f = (double)fq[(int64_t)s * fq_stride + row];
+            const double f = (double)fq[(int64_t)sp.kind[s] * fq_stride + row];
             re += f * pr;
             im += f * pi;
         }

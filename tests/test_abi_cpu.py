@@ -159,12 +159,12 @@ def test_binding_argument_checks():
 
 
 def test_species_engine_rule():
-    """AUTO's per-kind engine choice (mirror of api.cu): light kinds on the integer engine while
-    sum (f_max / f_min)^2 N_s / N <= 1."""
+    """AUTO's per-kind engine split (mirror of api.cu): kinds in increasing f_max on the integer engine while
+    sum (f_max / f_min)^2 N_s / N <= 1, the crossing kind split at the budget."""
     se = xp.species_engines
-    assert se([1000], [1.0]) == [True]
-    assert se([500, 500], [1.0, 2.0]) == [True, False]          # c3/c5: f = 1 half only
-    assert se([300, 700], [2.0, 1.0]) == [False, True]
-    assert se([400, 400, 200], [1.0, 1.0, 1.0]) == [True, True, True]
-    assert se([10, 10], None) == [True, True]                   # no hints: every kind
-    assert se([0, 100], [0.5, 1.0])[1] is True                  # an empty kind does not set the reference weight
+    assert se([1000], [1.0]) == [1000]
+    assert se([500, 500], [1.0, 2.0]) == [500, 125]            # c3/c5: f = 1 half + a quarter of the f = 2 half
+    assert se([300, 700], [2.0, 1.0]) == [75, 700]
+    assert se([400, 400, 200], [1.0, 1.0, 1.0]) == [400, 400, 200]
+    assert se([10, 10], None) == [10, 10]                      # no hints: every kind
+    assert se([0, 100], [0.5, 1.0])[1] == 100                  # an empty kind does not set the reference weight
