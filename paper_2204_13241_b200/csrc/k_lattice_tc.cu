@@ -45,15 +45,35 @@ constexpr int BROWS = 3 * BN;                     // B rows of this CTA: [-Ws | 
 constexpr int BPLANE = BROWS * KS * 2;            // bytes per fp16 B plane (192 rows x 16 atoms)
 constexpr int STAGE_BYTES = 4 * APLANE + 2 * BPLANE;   // Xr_hi Xr_lo Xs_hi Xs_lo | B_hi B_lo
 constexpr int MMA_N = 2 * TN;                     // N = 256: [Re | Im'] of 64 k per CTA half
+#ifndef XPCS_TC_GROUPED
+#define XPCS_TC_GROUPED 1          // producer groups of 3 warps, 4 atoms x 8 rows per thread, angle-addition recurrence
+#endif
+#ifndef XPCS_TC_GROUPS
+#define XPCS_TC_GROUPS 3
+#endif
+#if XPCS_TC_GROUPED
+constexpr int NGROUPS = XPCS_TC_GROUPS, GROUP_WARPS = 3;   // per group: 2 X warps (row halves), 1 W warp
+constexpr int NPROD_WARPS = NGROUPS * GROUP_WARPS, NDRAIN_WARPS = 4;
+constexpr int WREC = 16, WSLOT = WREC + WREC / 4;          // per-warp records of a stage (16 atoms, padded)
+#else
 constexpr int NPROD_WARPS = 16, NDRAIN_WARPS = 4;
+#endif
 constexpr int MMA_WARP = NPROD_WARPS + NDRAIN_WARPS;
-constexpr int NTHREADS = (MMA_WARP + 1) * 32;     // 672
+constexpr int NTHREADS = (MMA_WARP + 1) * 32;
 constexpr int TMEM_COLS = 512;                    // buffer b: cols [256b, 256b+256) = [Re k<64 | Im' k<64 | Re k>=64 | Im' k>=64]
 constexpr int SUM_LD = 129;                       // running sums [256 cols][129] fp32 (padded: conflict-free)
 constexpr int SUM_BYTES = (XPCS_TC_HALFSUMS ? 128 : 256) * SUM_LD * 4;   // HALFSUMS: timing experiments only
-constexpr int ASLOTS = 4;                         // cp.async prefetch ring depth (distance ASLOTS - 1 stages)
+#ifndef XPCS_TC_ASLOTS
+#define XPCS_TC_ASLOTS 4
+#endif
+constexpr int ASLOTS = XPCS_TC_ASLOTS;            // cp.async prefetch ring depth (distance ASLOTS - 1 stages)
+#if XPCS_TC_GROUPED
+constexpr int ASLOT_BYTES = NPROD_WARPS * ASLOTS * WSLOT * 16;   // per producer warp: its stage's 16 atoms, padded
+#else
 constexpr int ASLOT_BYTES = NPROD_WARPS * ASLOTS * 8 * 16;   // per producer warp: its 8 atoms of ASLOTS stages
+#endif
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + SUM_BYTES + ASLOT_BYTES + 1024 + 256;
+static_assert(SMEM_BYTES <= 227 * 1024, "k_lattice_tc: shared memory over the 227 KB opt-in limit");
 }  // namespace tc
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -224,6 +244,22 @@ __device__ __forceinline__ void split_vals_f(unsigned long long f2, unsigned lon
     h = pack_half2(hi);
     l = pack_half2(lo);
 }
+__device__ __forceinline__ unsigned long long fmul2(unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ unsigned long long swap2(unsigned long long v) { return (v >> 32) | (v << 32); }
+// (upper, lower) fp32 -> half2 bits, lower at the lower address
+__device__ __forceinline__ uint32_t pack_h2(float upper, float lower) {
+    uint32_t r;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(upper), "f"(lower));
+    return r;
+}
+template <int OFF>
+__device__ __forceinline__ void sts64(uint32_t addr, uint32_t a, uint32_t b) {
+    asm volatile("st.shared.v2.b32 [%0+%3], {%1, %2};" ::"r"(addr), "r"(a), "r"(b), "n"(OFF));
+}
 // M = 1.5 * 2^(13 + e), e = max(0, exponent bound of |f|) so that |f| <= 2^e
 __device__ __forceinline__ float split_magic(float f) {
     const int ef = (int)((__float_as_uint(f) >> 23) & 0xFF);
@@ -259,7 +295,11 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
 
     if (threadIdx.x == 0) {
         // in the leader: full[s] counts the 16 producer warps of both CTAs, tempty[b] the 4 drain warps of both
+#if XPCS_TC_GROUPED
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 2 * GROUP_WARPS); mbar_init(&empty[s], 1); }
+#else
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 2 * NPROD_WARPS); mbar_init(&empty[s], 1); }
+#endif
         for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 2 * NDRAIN_WARPS); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -313,6 +353,130 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
         }
         __syncwarp();
     } else if (warp < NPROD_WARPS) {
+#if XPCS_TC_GROUPED
+        // ================= phasor producers: group g fills stages g, g + NGROUPS, ...  A thread owns 4 atoms (one
+        // 8-byte half2 pair per row and plane, STS.64) and 8 rows spaced 8 apart, walked with the angle-addition
+        // recurrence (2 sincos per atom per stage, 2 packed ops per phasor); split into fp16 hi/lo with magic
+        // numbers (3 packed ops per phasor) and packed with cvt.f16x2.  Lanes (quad qq, row mr): conflict-free.
+        const int grp = warp / GROUP_WARPS, wi = warp % GROUP_WARPS;
+        const int qq = lane & 3, mr = lane >> 2;
+        const bool is_x = wi < 2;
+        const uint32_t slot0 = smem_u32(aslot) + (uint32_t)(warp * ASLOTS * WSLOT * 16);
+        const uint32_t full0 = mapa(smem_u32(full), 0);
+        auto prefetch = [&](int li) {
+            const int i = grp + li * NGROUPS;
+            if (i < n_stages && lane < WREC) {
+                const int64_t j = a_begin + (int64_t)i * KS + lane;
+                const bool ok = j < a_end;
+                cp_async16(slot0 + (uint32_t)(((li % ASLOTS) * WSLOT + lane + (lane >> 2)) * 16), S + (ok ? j : 0),
+                           ok ? 16u : 0u);
+            }
+            cp_async_commit();
+        };
+#pragma unroll
+        for (int k = 0; k < ASLOTS - 1; ++k) prefetch(k);
+        const unsigned long long MX2 = pack2(12288.0f, 12288.0f);             // |X| <= 1: hi on the 2^-10 grid
+        for (int li = 0;; ++li) {
+            const int i = grp + li * NGROUPS;
+            if (i >= n_stages) break;
+            const int s = i % STAGES;
+            cp_async_wait<ASLOTS - 2>();
+            __syncwarp();
+            prefetch(li + ASLOTS - 1);
+            uint4 at[4];
+            {
+                const uint32_t ra = slot0 + (uint32_t)(((li % ASLOTS) * WSLOT + 5 * qq) * 16);
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(at[u].x), "=r"(at[u].y), "=r"(at[u].z), "=r"(at[u].w)
+                                 : "r"(ra + 16 * u));
+            }
+            mbar_wait(&empty[s], (uint32_t)(((i / STAGES) + 1) & 1));
+            const uint32_t sbase = smem_u32(smem) + (uint32_t)(s * STAGE_BYTES);
+            // byte offset of (row m, quad qq) in a plane: [m/8][qq/2][m%8][qq%2 * 8 B]
+            const uint32_t qoff = (uint32_t)((qq >> 1) * 128 + mr * 16 + (qq & 1) * 8);
+            if (!(dbg_flags & 2)) {
+                if (is_x) {
+                    const int xw = wi;                                   // rows m = mr + 8 r + 64 xw, r < 8
+                    const uint32_t h = (uint32_t)(g.h0 + th0 + mr + 64 * xw);
+                    unsigned long long v[4], st[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        float s0, c0, s1, c1;
+                        __sincosf(turns_to_radians(h * at[u].x), &s0, &c0);
+                        __sincosf(turns_to_radians(8u * at[u].x), &s1, &c1);
+                        v[u] = pack2(c0, s0);
+                        st[u] = pack2(c1, s1);
+                    }
+                    const uint32_t a0 = sbase + qoff + (uint32_t)(xw * 8 * 256);
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) {
+                        unsigned long long hi[4], lo[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            hi[u] = fsub2(fadd2(v[u], MX2), MX2);          // (c_hi, s_hi), exact in fp16
+                            lo[u] = fsub2(v[u], hi[u]);                     // (c_lo, s_lo)
+                            const unsigned long long cd = pack2(lo2(st[u]), lo2(st[u]));
+                            const unsigned long long sd = pack2(-hi2(st[u]), hi2(st[u]));
+                            v[u] = ffma2(swap2(v[u]), sd, fmul2(v[u], cd));
+                        }
+                        const uint32_t ad = a0 + (uint32_t)(r * 256);
+                        sts64<0 * APLANE>(ad, pack_h2(lo2(hi[1]), lo2(hi[0])), pack_h2(lo2(hi[3]), lo2(hi[2])));   // Xr_hi
+                        sts64<1 * APLANE>(ad, pack_h2(lo2(lo[1]), lo2(lo[0])), pack_h2(lo2(lo[3]), lo2(lo[2])));   // Xr_lo
+                        sts64<2 * APLANE>(ad, pack_h2(hi2(hi[1]), hi2(hi[0])), pack_h2(hi2(hi[3]), hi2(hi[2])));   // Xs_hi
+                        sts64<3 * APLANE>(ad, pack_h2(hi2(lo[1]), hi2(lo[0])), pack_h2(hi2(lo[3]), hi2(lo[2])));   // Xs_lo
+                    }
+                } else {
+                    // W rows k = mr + 8 r of this CTA's 64: W_k = f e^{-2 pi i (Th_0 + kk Th_b)}; B rows: -Ws at k,
+                    // Wr at BN + k, Ws at 2 BN + k.  hi on the 2^(e-10) grid of the quad's max |f| (split_magic)
+                    const uint32_t kk = (uint32_t)(g.k0 + bk0 + mr);
+                    unsigned long long v[4], st[4], f2[4];
+                    float fm = 0.f;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        float s0, c0, s1, c1;
+                        __sincosf(turns_to_radians(at[u].z + kk * at[u].y), &s0, &c0);
+                        __sincosf(turns_to_radians(8u * at[u].y), &s1, &c1);
+                        v[u] = pack2(c0, s0);
+                        st[u] = pack2(c1, s1);
+                        const float fj = __uint_as_float(at[u].w);   // padding atoms: f = 0 -> W = 0
+                        f2[u] = pack2(fj, fj);
+                        fm = fmaxf(fm, fabsf(fj));
+                    }
+                    const float MW = split_magic(fm);
+                    const unsigned long long MW2 = pack2(MW, MW);
+                    const uint32_t a0 = sbase + 4 * APLANE + qoff;
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) {
+                        unsigned long long hi[4], lo[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const unsigned long long t = ffma2(f2[u], v[u], MW2);
+                            hi[u] = fsub2(t, MW2);                           // f (c, s) hi
+                            lo[u] = ffma2(f2[u], v[u], fsub2(MW2, t));       // f (c, s) - hi, from the exact product
+                            const unsigned long long cd = pack2(lo2(st[u]), lo2(st[u]));
+                            const unsigned long long sd = pack2(-hi2(st[u]), hi2(st[u]));
+                            v[u] = ffma2(swap2(v[u]), sd, fmul2(v[u], cd));
+                        }
+                        const uint32_t wr_h0 = pack_h2(lo2(hi[1]), lo2(hi[0])), wr_h1 = pack_h2(lo2(hi[3]), lo2(hi[2]));
+                        const uint32_t wr_l0 = pack_h2(lo2(lo[1]), lo2(lo[0])), wr_l1 = pack_h2(lo2(lo[3]), lo2(lo[2]));
+                        const uint32_t ws_h0 = pack_h2(hi2(hi[1]), hi2(hi[0])), ws_h1 = pack_h2(hi2(hi[3]), hi2(hi[2]));
+                        const uint32_t ws_l0 = pack_h2(hi2(lo[1]), hi2(lo[0])), ws_l1 = pack_h2(hi2(lo[3]), hi2(lo[2]));
+                        const uint32_t ad = a0 + (uint32_t)(r * 256);
+                        sts64<8 * 256>(ad, wr_h0, wr_h1);                      sts64<BPLANE + 8 * 256>(ad, wr_l0, wr_l1);
+                        sts64<16 * 256>(ad, ws_h0, ws_h1);                     sts64<BPLANE + 16 * 256>(ad, ws_l0, ws_l1);
+                        sts64<0>(ad, ws_h0 ^ 0x80008000u, ws_h1 ^ 0x80008000u);
+                        sts64<BPLANE>(ad, ws_l0 ^ 0x80008000u, ws_l1 ^ 0x80008000u);   // -Ws (sign bits)
+                    }
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> async proxy
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(full0 + (uint32_t)(s * 8));   // the leader's full[s]
+        }
+        cp_async_wait<0>();
+#else
         // ================= phasor producers (both CTAs): own 128 A rows, own 64 B rows =================
         const int ah = warp & 1;
         const int a_loc = ah * 8 + 2 * (lane & 3);
@@ -386,6 +550,7 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(full0 + (uint32_t)(s * 8));   // the leader's full[s]
         }
+#endif
     } else {
         // ================= drain warps: TMEM accumulator -> RN fp32 running sums (smem) -> tile =================
         const int quarter = warp & 3;               // TMEM lanes 32*quarter .. +31 = rows of this CTA's half
