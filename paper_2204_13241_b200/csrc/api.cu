@@ -1,6 +1,7 @@
 // api.cu -- the C ABI of libxpcs.so (include/xpcs.h): validation, frame batching, scratch, orchestration.
 // Every computational step is a kernel of this library; this file only validates, sizes and enqueues.
 #include "common.cuh"
+#include <mutex>
 #include "../../include/xpcs.h"
 
 #include <algorithm>
@@ -423,6 +424,57 @@ static int validate_volume(const xpcs_qvolume* vol) {
     return XPCS_OK;
 }
 
+// ---- integer-engine grid planning (k_lattice_i8: clusters of 2 CTAs, one CTA per SM, 32-atom stages) ----
+constexpr double kI8CtaCost = 15.0;     // per-CTA fixed cost in stage units: prologue, the single drain, teardown
+constexpr double kI8BatchCost = 20.0;   // an extra frame batch: its staging, reduction and launch gaps (stage units)
+static int64_t i8_tiles(const LatticeGeom& g) { return ((g.n_h + 255) / 256) * ((g.n_k + 127) / 128); }
+// atoms per chunk for `units` (tile, virtual frame) pairs of Ng atoms: chunks only balance the grid (exact int32
+// accumulation) and stay <= kI8MaxChunk; cost = waves x (stages per CTA + kI8CtaCost), the smallest C wins ties
+static int64_t i8_plan_chunk(int64_t Ng, int64_t units, double* cost_out) {
+    const int64_t wave = std::max<int64_t>(1, i8_cluster_slots());
+    const int64_t cmin = std::max<int64_t>(1, (Ng + kI8MaxChunk - 1) / kI8MaxChunk);
+    const int64_t cmax = std::max<int64_t>(cmin, std::min<int64_t>((Ng + 1023) / 1024, 64));
+    int64_t best = cmin;
+    double best_cost = 1e300;
+    for (int64_t c = cmin; c <= cmax; ++c) {
+        const int64_t ch = std::min<int64_t>(((Ng + c - 1) / c + 31) / 32 * 32, kI8MaxChunk);
+        const int64_t cc = (Ng + ch - 1) / ch;
+        const double waves = std::ceil((double)(units * cc) / (double)wave);
+        const double cost = waves * ((double)(ch / 32) + kI8CtaCost);
+        if (cost < best_cost * (1.0 - 1e-9)) { best_cost = cost; best = c; }
+    }
+    if (cost_out) *cost_out = best_cost;
+    return std::min<int64_t>(((Ng + best - 1) / best + 31) / 32 * 32, kI8MaxChunk);
+}
+
+// split of V virtual frames into [V1 | V - V1] batches with their own chunking (V1 = 0: no split), memoised: the
+// search is O(V x chunk counts) host work that would otherwise sit in front of every launch
+static void i8_plan_split(int64_t Ng, int64_t tiles, int64_t V, int64_t& V1, int64_t& ch1, int64_t& ch2) {
+    struct Key { int64_t Ng, tiles, V; int slots; };
+    struct Entry { Key k; int64_t V1, ch1, ch2; };
+    static std::mutex mu;
+    static std::vector<Entry> memo;
+    const int slots = i8_cluster_slots();
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        for (const Entry& e : memo)
+            if (e.k.Ng == Ng && e.k.tiles == tiles && e.k.V == V && e.k.slots == slots) { V1 = e.V1; ch1 = e.ch1; ch2 = e.ch2; return; }
+    }
+    double whole = 0.0;
+    ch1 = ch2 = i8_plan_chunk(Ng, tiles * V, &whole);
+    V1 = 0;
+    double best = whole;
+    for (int64_t v1 = 1; v1 < V; ++v1) {
+        double c1 = 0.0, c2 = 0.0;
+        const int64_t a = i8_plan_chunk(Ng, tiles * v1, &c1), b = i8_plan_chunk(Ng, tiles * (V - v1), &c2);
+        const double cost = c1 + c2 + kI8BatchCost;
+        if (cost < best * (1.0 - 1e-9)) { best = cost; V1 = v1; ch1 = a; ch2 = b; }
+    }
+    std::lock_guard<std::mutex> lk(mu);
+    if (memo.size() > 256) memo.clear();
+    memo.push_back({{Ng, tiles, V, slots}, V1, ch1, ch2});
+}
+
 static int run_volume(const void* positions, int64_t N, const void* form_factors, const xpcs_species* species,
                       const xpcs_qvolume* vol, int64_t frames, void* I_out, const xpcs_opts* opts, int amp) {
     clear_error();
@@ -566,19 +618,7 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
             // exact int32 accumulation: chunks only balance the grid (clusters of 2 CTAs, one CTA per SM) and stay
             // <= kI8MaxChunk.  Cost model in 32-atom stage units: waves x (stages per CTA + a fixed per-CTA cost of
             // ~15 stages for the prologue, the single drain and the cluster teardown); the smallest C wins ties.
-            const int64_t units = ((g.n_h + 255) / 256) * ((g.n_k + 127) / 128) * V;
-            const int64_t wave = std::max<int64_t>(1, sm_count() / 2);
-            const int64_t cmin = std::max<int64_t>(1, (Ng + kI8MaxChunk - 1) / kI8MaxChunk);
-            const int64_t cmax = std::max<int64_t>(cmin, std::min<int64_t>((Ng + 1023) / 1024, 64));
-            int64_t best = cmin;
-            double best_cost = 1e300;
-            for (int64_t c = cmin; c <= cmax; ++c) {
-                const double waves = std::ceil((double)(units * c) / (double)wave);
-                const double cost = waves * (std::ceil((double)Ng / (double)(32 * c)) + 15.0);
-                if (cost < best_cost * (1.0 - 1e-9)) { best_cost = cost; best = c; }
-            }
-            ch = ((Ng + best - 1) / best + 31) / 32 * 32;
-            ch = std::min<int64_t>(ch, kI8MaxChunk);
+            ch = i8_plan_chunk(Ng, i8_tiles(g) * V, nullptr);
         } else if (g_tc) {
             const int64_t tiles = ((g.n_h + 127) / 128) * ((g.n_k + 127) / 128);
             const int64_t units = tiles * std::min<int64_t>(V, 64);
@@ -600,8 +640,29 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
     }
     sp.part_f64 = 0;
     const int64_t Tb = std::max<int64_t>(1, std::min<int64_t>(V, (int64_t)(kBatchBytes / std::max<int64_t>(16 * N, 8 * sumC * n_q))));
+    // frame batches: memory-bounded (Tb).  A single integer-engine group in one batch is split in two when that
+    // shortens the last, partly filled wave of clusters: the leading frames fill whole waves with unsplit atom
+    // ranges, the remaining frames get their own atom chunking (cost model of i8_plan_chunk), e.g. c2: 100 frames x
+    // 2 tiles on 74 cluster slots = 2.7 waves of 1000 stages -> 74 frames (2 waves) + 26 frames in 7 chunks.
+    struct FrameBatch { int64_t v0, vb, chunk; };
+    std::vector<FrameBatch> batches;
+    int64_t part_elems = sumC * n_q * Tb;
+    {
+        const bool single_i8 = ng == 1 && !G.n_species && i8 && gi8[0] && G.cnt[0] > 0 && V <= Tb &&
+                               !getenv("XPCS_CHUNK_ATOMS") && !(getenv("XPCS_I8_TAILSPLIT") && atoi(getenv("XPCS_I8_TAILSPLIT")) == 0);
+        int64_t V1 = 0, ch1 = chunk[0], ch2 = chunk[0];
+        if (single_i8) i8_plan_split(G.cnt[0], i8_tiles(g), V, V1, ch1, ch2);
+        if (V1 > 0) {
+            batches.push_back({0, V1, ch1});
+            batches.push_back({V1, V - V1, ch2});
+            const int64_t C1 = (G.cnt[0] + ch1 - 1) / ch1, C2 = (G.cnt[0] + ch2 - 1) / ch2;
+            part_elems = std::max(C1 * V1, C2 * (V - V1)) * n_q;
+        } else {
+            for (int64_t v0 = 0; v0 < V; v0 += Tb) batches.push_back({v0, std::min(Tb, V - v0), 0});
+        }
+    }
     uint4* st = (uint4*)scratch(o.s, SS_STAGE, sizeof(uint4) * (size_t)(N * Tb));
-    float2* part = (float2*)scratch(o.s, SS_PARTIAL, sizeof(float2) * (size_t)(sumC * n_q * Tb));
+    float2* part = (float2*)scratch(o.s, SS_PARTIAL, sizeof(float2) * (size_t)part_elems);
     if (!st || !part) return XPCS_ENOMEM;
     float* fmax = nullptr;
     if (i8 && form_factors) {
@@ -610,8 +671,9 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
     }
     // the tensor engines' partials hold conj(p) (R1)
     const int mode = amp ? ((tc || i8) ? 2 : 1) : 0;
-    for (int64_t v0 = 0; v0 < V; v0 += Tb) {
-        const int64_t vb = std::min(Tb, V - v0);
+    for (const FrameBatch& fb : batches) {
+        const int64_t v0 = fb.v0, vb = fb.vb;
+        if (fb.chunk > 0) { chunk[0] = fb.chunk; C[0] = (G.cnt[0] + fb.chunk - 1) / fb.chunk; }
         int64_t stoff = 0, poff = 0;
         for (int gi = 0; gi < ng; ++gi) {
             const int64_t Ng = G.cnt[gi];

@@ -166,6 +166,7 @@ bool lattice_tc_supported(const LatticeGeom& g);
 // partial [C][Tb][n_h*n_k] float2 (conj(p), like the split-FP16 engine); chunk_atoms <= kI8MaxChunk.
 // uniform_f != 0: all f_j = 1 (no W scale); else F = max |f_j| is reduced into fmax_scratch (1 float) first.
 constexpr int64_t kI8MaxChunk = 32768;
+int i8_cluster_slots();   // k_lattice_i8 clusters resident at once (cudaOccupancyMaxActiveClusters)
 cudaError_t launch_lattice_i8(const uint4* staged, int64_t N, int64_t frames, const LatticeGeom& g, int64_t chunk_atoms,
                               int64_t n_chunks, float* fmax_scratch, int uniform_f, float2* partial, cudaStream_t s);
 // lattice FP64 (direct per-pixel evaluation with 64-bit turns): writes I directly (double)

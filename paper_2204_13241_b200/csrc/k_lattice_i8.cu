@@ -3,14 +3,18 @@
 //
 // Same factorisation as k_lattice_tc.cu (Eq. 7, on a reciprocal-lattice plane):
 //     p^e(h,k) = sum_j X_h(j) W_k(j),  X_h = e^{-2 pi i h Th_a(j)},  W_k = (f_j / F) e^{-2 pi i (Th_0 + k Th_b)(j)}
-// with F = max_j |f_j|.  Every phasor component v in [-1, 1] is written as two int8 limbs
-//     v ~ (254 hi + lo) / 32258,  hi = rint(127 v) in [-127, 127],  lo = rint(254 (127 v - hi)) in [-127, 127]
-// (|error| <= 1 / 64516 = 1.55e-5; both limbs always fit: |254 (127 v - hi)| <= 127 exactly), so each real product is
-//     v w ~ [64516 hi.hi' + 254 (hi.lo' + lo.hi')] / 32258^2      (the dropped lo.lo' term is < 1.6e-5)
+// with F = max_j |f_j|.  Every phasor component v in [-1, 1] is written as two int8 limbs (Q16, the default):
+//     x = rint(32512 v) = 256 hi + lo,  hi = round(x / 256) in [-127, 127],  lo in [-128, 127]
+// (|v - x / 32512| <= 1 / 65024 = 1.54e-5).  One FFMA t = fma(v, 32512, 1.5 * 2^23 + 128) leaves y = x + 128 in the
+// low 16 bits of t: byte 1 = hi, byte 0 = lo + 128, so both limbs come from one instruction and two byte permutes.
+// Each real product is
+//     v w ~ [65536 hi.hi' + 256 (hi.lo' + lo.hi')] / 32512^2      (the dropped lo.lo' term is <= 1.55e-5, zero-mean)
 // i.e. three int8 MMAs into two TMEM accumulators, HH = sum hi.hi' and X = sum (hi.lo' + lo.hi').  The integer
 // accumulation is EXACT (no TMEM rounding, unlike the FP32 accumulator of the split-FP16 engine), so
-// a chunk of up to 32768 atoms (int32 overflow bound: 4 x 127^2 x 32768 < 2^31) accumulates in TMEM and is drained
-// once; the result carries only the limb quantisation error (rms |dI| ~ 3e-5 N per pixel for f = 1).
+// a chunk of up to 32768 atoms (int32 overflow bound: 4 x 127 x 128 x 32768 < 2^31) accumulates in TMEM and is
+// drained once; the result carries only the limb quantisation error (rms |dI| ~ 3e-5 N per pixel for f = 1,
+// DESIGN.md 6.3).  XPCS_I8_Q16=0 builds the previous base-254 limbs (hi = rint(127 v), lo = rint(254 (127 v - hi)),
+// v ~ (254 hi + lo) / 32258, three magic-number FFMAs per component; kept for comparison).
 // The int8 tensor rate is twice the fp16 rate on sm_100a (measured 8192 vs 4096 MAC/clk/SM, tools/mma_rate.cu).
 //
 // CTA pair (cluster of 2, cta_group::2): 256 (h) x 128 (k) pixel tile, M = 256, N = 256 ([Re | Im'] of 64 k per CTA
@@ -21,7 +25,7 @@
 // Producers: 3 groups of 6 warps; group g fills stages i = g mod 3 (6-stage ring, 28 KB per stage).  A warp thread
 // owns 4 consecutive atoms (one 32-bit word per row and limb plane) and 8 rows spaced 8 apart (X or W), and walks
 // the rows with the angle-addition recurrence X_{m+8} = X_m X_8 (packed FP32x2, 2 ops per phasor; 2 SFU sincos per
-// atom per thread), quantises with magic-number rounding (3 packed ops per phasor) and packs limb bytes with PRMT.
+// atom per thread), quantises with one packed magic-number FFMA per phasor (Q16) and packs limb bytes with PRMT.
 // Lanes (quad qq, row mr) write 32 distinct banks per store.  After the last stage, warps 0-7 (one per TMEM lane
 // quarter, two warps per quarter splitting the columns) wait for the final MMA commit and drain both
 // accumulators: p = (64516 HH + 254 X) F / 32258^2.
@@ -56,6 +60,13 @@ constexpr int WSLOT = WREC + WREC / 4;              // record slots incl. one 16
 constexpr int ASLOT_BYTES = NPROD_WARPS * ASL * WSLOT * 16;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + ASLOT_BYTES + 1024 + 256;
 constexpr float MAGIC = 12582912.0f;                // 1.5 * 2^23
+#ifndef XPCS_I8_Q16
+#define XPCS_I8_Q16 1
+#endif
+// Q16 limbs: x = rint(QS v) in [-QS, QS], x = 256 hi + lo with hi in [-127, 127], lo in [-128, 127]; one FFMA
+// t = fma(v, QS, M + 128) holds y = x + 128 in its low 16 bits: byte 1 = hi, byte 0 = lo + 128 (= lo ^ 0x80)
+constexpr float QS = 32512.0f;
+constexpr float QMAGIC = MAGIC + 128.0f;
 }  // namespace ti8
 
 namespace {
@@ -138,6 +149,12 @@ __device__ __forceinline__ void quantise(unsigned long long v, unsigned long lon
 // low bytes of four 32-bit words -> one word (byte t = atom t)
 __device__ __forceinline__ uint32_t pack_bytes(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
     return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
+}
+// Q16: four magic words (atoms 0..3) -> (hi bytes, lo bytes) words, byte t = atom t
+__device__ __forceinline__ void q16_pack(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3, uint32_t& hi, uint32_t& lo) {
+    const uint32_t p01 = __byte_perm(t0, t1, 0x5140), p23 = __byte_perm(t2, t3, 0x5140);   // [b0 b0' b1 b1']
+    hi = __byte_perm(p01, p23, 0x7632);
+    lo = __byte_perm(p01, p23, 0x5410) ^ 0x80808080u;
 }
 // per-byte two's-complement negation of four int8 in [-127, 127]
 __device__ __forceinline__ uint32_t neg_bytes(uint32_t w) {
@@ -282,6 +299,29 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
                         st[u] = pack2(c1, s1);
                     }
                     const uint32_t a0 = sbase + (uint32_t)(qh * 128 + mr * 16 + qq * 4 + rh * 8 * 256);
+#if XPCS_I8_Q16
+                    const unsigned long long QS2 = pack2(QS, QS), QM2 = pack2(QMAGIC, QMAGIC);
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) {
+                        uint32_t tc[4], ts[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const unsigned long long tq = ffma2(v[u], QS2, QM2);
+                            tc[u] = (uint32_t)tq; ts[u] = (uint32_t)(tq >> 32);
+                            const unsigned long long cd = pack2(lo2(st[u]), lo2(st[u]));
+                            const unsigned long long sd = pack2(-hi2(st[u]), hi2(st[u]));
+                            v[u] = ffma2(swap2(v[u]), sd, f2mul(v[u], cd));
+                        }
+                        uint32_t xrh, xrl, xsh, xsl;
+                        q16_pack(tc[0], tc[1], tc[2], tc[3], xrh, xrl);
+                        q16_pack(ts[0], ts[1], ts[2], ts[3], xsh, xsl);
+                        const uint32_t ad = a0 + (uint32_t)(r * 256);
+                        i8_sts<0 * APLANE>(ad, xrh);
+                        i8_sts<1 * APLANE>(ad, xrl);
+                        i8_sts<2 * APLANE>(ad, xsh);
+                        i8_sts<3 * APLANE>(ad, xsl);
+                    }
+#else
 #pragma unroll
                     for (int r = 0; r < 8; ++r) {
                         uint32_t hc[4], lc[4], hs[4], ls[4];
@@ -302,6 +342,7 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
                         i8_sts<2 * APLANE>(ad, pack_bytes(hs[0], hs[1], hs[2], hs[3]));
                         i8_sts<3 * APLANE>(ad, pack_bytes(ls[0], ls[1], ls[2], ls[3]));
                     }
+#endif
                 } else {
                     // W rows k = mr + 8 r (r < 8) of this CTA's 64: W_k = (f / F) e^{-2 pi i (Th_0 + kk Th_b)}
                     const uint32_t kk = (uint32_t)(g.k0 + bk0 + mr);
@@ -316,6 +357,35 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
                         st[u] = pack2(c1, s1);
                     }
                     const uint32_t a0 = sbase + (uint32_t)(4 * APLANE + qh * 128 + mr * 16 + qq * 4);
+#if XPCS_I8_Q16
+                    const unsigned long long QS2 = pack2(QS, QS), QM2 = pack2(QMAGIC, QMAGIC);
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) {
+                        uint32_t tc[4], ts[4], tn[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const unsigned long long tq = ffma2(v[u], QS2, QM2);
+                            tc[u] = (uint32_t)tq; ts[u] = (uint32_t)(tq >> 32);
+                            // -Ws limbs from rint(-QS s) = -rint(QS s) (lo = -128 has no int8 negation)
+                            tn[u] = __float_as_uint(fmaf(hi2(v[u]), -QS, QMAGIC));
+                            const unsigned long long cd = pack2(lo2(st[u]), lo2(st[u]));
+                            const unsigned long long sd = pack2(-hi2(st[u]), hi2(st[u]));
+                            v[u] = ffma2(swap2(v[u]), sd, f2mul(v[u], cd));
+                        }
+                        uint32_t whr, wlr, whs, wls, nhs, nls;
+                        q16_pack(tc[0], tc[1], tc[2], tc[3], whr, wlr);
+                        q16_pack(ts[0], ts[1], ts[2], ts[3], whs, wls);
+                        q16_pack(tn[0], tn[1], tn[2], tn[3], nhs, nls);
+                        const uint32_t ad = a0 + (uint32_t)(r * 256);
+                        // B rows: -Ws at k, Wr at BN + k, Ws at 2 BN + k  (BN rows = 8 groups of 256 B)
+                        i8_sts<0>(ad, nhs);
+                        i8_sts<BPLANE>(ad, nls);
+                        i8_sts<8 * 256>(ad, whr);
+                        i8_sts<BPLANE + 8 * 256>(ad, wlr);
+                        i8_sts<16 * 256>(ad, whs);
+                        i8_sts<BPLANE + 16 * 256>(ad, wls);
+                    }
+#else
 #pragma unroll
                     for (int r = 0; r < 8; ++r) {
                         uint32_t hc[4], lc[4], hs[4], ls[4];
@@ -342,6 +412,7 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
                         i8_sts<16 * 256>(ad, whs);
                         i8_sts<BPLANE + 16 * 256>(ad, wls);
                     }
+#endif
                 }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -358,12 +429,22 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16);
         const int row = quarter * 32 + lane;
-        const int64_t ih = th0 + row;
         const int64_t n_q = g.n_h * g.n_k;
         float2* P = partial + (chunk * frames + t) * n_q;
-        // p = (64516 HH + 254 X) F / 32258^2 in FP32 (the partial is fp32; |rounding| <= 2^-23 |p|)
+        // p = (64516 HH + 254 X) F / 32258^2 in FP32 (the partial is fp32; |rounding| <= 2^-23 |p|).  The tile goes
+        // through shared memory (the stage ring is free once `done` fired: every MMA has read its operands) so that
+        // the global writes are row-contiguous: TMEM lane = pixel row, so direct stores would touch 32 rows per
+        // instruction.  Layout [128 rows][64 float4 + 1 pad] (pixel pairs; the pad makes the float4 writes of a
+        // warp's 32 rows conflict-free).
+#if XPCS_I8_Q16
+        const float c_hh = (float)(65536.0 * (double)F / (32512.0 * 32512.0));   // p = (65536 HH + 256 X) F / QS^2
+        const float c_x = (float)(256.0 * (double)F / (32512.0 * 32512.0));
+#else
         const float c_hh = (float)(64516.0 * (double)F / (32258.0 * 32258.0));
         const float c_x = (float)(254.0 * (double)F / (32258.0 * 32258.0));
+#endif
+        float4* tile = reinterpret_cast<float4*>(smem);
+        constexpr int TLD = TN / 2 + 1;
 #pragma unroll 1
         for (int kb = 4 * half; kb < 4 * half + 4; ++kb) {
             const uint32_t cre = (uint32_t)(kb < 4 ? 16 * kb : 16 * kb + 64);   // [Re k<64 | Im' k<64 | Re k>=64 | Im' k>=64]
@@ -373,14 +454,29 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
             I8_TMEM_LD16(tb + 256 + cre, xre);
             I8_TMEM_LD16(tb + 256 + cre + 64, xim);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            if (ih < g.n_h) {
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const int64_t ik = tk0 + 16 * kb + j;
-                    const float re = fmaf((float)(int32_t)hre[j], c_hh, (float)(int32_t)xre[j] * c_x);
-                    const float im = fmaf((float)(int32_t)him[j], c_hh, (float)(int32_t)xim[j] * c_x);
-                    if (ik < g.n_k) P[ih * g.n_k + ik] = make_float2(re, im);
-                }
+            for (int j = 0; j < 16; j += 2) {
+                float4 v;
+                v.x = fmaf((float)(int32_t)hre[j], c_hh, (float)(int32_t)xre[j] * c_x);
+                v.y = fmaf((float)(int32_t)him[j], c_hh, (float)(int32_t)xim[j] * c_x);
+                v.z = fmaf((float)(int32_t)hre[j + 1], c_hh, (float)(int32_t)xre[j + 1] * c_x);
+                v.w = fmaf((float)(int32_t)him[j + 1], c_hh, (float)(int32_t)xim[j + 1] * c_x);
+                tile[row * TLD + 8 * kb + j / 2] = v;
+            }
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");   // drain warps 0-7 only
+        const int tid = threadIdx.x;                     // 0..255
+        const int rows = (int)min((int64_t)TM, g.n_h - th0), cols = (int)min((int64_t)TN, g.n_k - tk0);
+        const bool vec = (g.n_k & 1) == 0;               // 16-B aligned pixel pairs
+        for (int e = tid; e < TM * (TN / 2); e += 256) {
+            const int r = e / (TN / 2), c2 = e % (TN / 2);
+            if (r >= rows || 2 * c2 >= cols) continue;
+            const float4 v = tile[r * TLD + c2];
+            float2* dst = P + (int64_t)(th0 + r) * g.n_k + tk0 + 2 * c2;
+            if (vec && 2 * c2 + 1 < cols) *reinterpret_cast<float4*>(dst) = v;
+            else {
+                dst[0] = make_float2(v.x, v.y);
+                if (2 * c2 + 1 < cols) dst[1] = make_float2(v.z, v.w);
             }
         }
     }
@@ -403,6 +499,33 @@ __global__ void k_absmax_f(const uint4* __restrict__ staged, int64_t n, float* _
         __syncthreads();
     }
     if (threadIdx.x == 0) out[0] = sh[0];
+}
+
+// clusters of k_lattice_i8 resident at once on the current device (one wave); sm_count / 2 if the query fails
+int i8_cluster_slots() {
+    using namespace ti8;
+    static int cached[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return std::max(1, sm_count() / 2);
+    if (cached[dev] > 0) return cached[dev];
+    int n = 0;
+    if (cudaFuncSetAttribute(k_lattice_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) == cudaSuccess) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(2 * 256, 1, 1);
+        cfg.blockDim = dim3(NTHREADS, 1, 1);
+        cfg.dynamicSmemBytes = SMEM_BYTES;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (cudaOccupancyMaxActiveClusters(&n, (void*)k_lattice_i8, &cfg) != cudaSuccess) n = 0;
+    }
+    (void)cudaGetLastError();
+    cached[dev] = n > 0 ? n : std::max(1, sm_count() / 2);
+    return cached[dev];
 }
 
 cudaError_t launch_lattice_i8(const uint4* staged, int64_t N, int64_t frames, const LatticeGeom& g, int64_t chunk_atoms,

@@ -68,6 +68,9 @@ class Pipeline:
             self.kind_fq = kf[:, None].expand(len(wl.kind_f), self.n_q).contiguous()
         self.I = torch.empty((wl.T, self.n_q), dtype=odt, device=self.device)
         self.g2 = torch.empty((len(wl.lags), self.n_q), dtype=torch.float32, device=self.device) if wl.lags else None
+        # the reductions of I are independent (g2 -> g2 rings | XSVS | S rings) and each is too small to fill the
+        # GPU alone: they run concurrently on two side streams and the caller's stream, joined before returning
+        self.s_red = [torch.cuda.Stream(self.device), torch.cuda.Stream(self.device)] if self.device.type == "cuda" else None
 
     def close(self):
         """Free the registered ring plan (the bins tensor dies with the pipeline; a stale plan must not outlive it)."""
@@ -96,15 +99,31 @@ class Pipeline:
         else:
             X.xpcs_intensity(positions, form_factors, wl.q, wl.L, out=self.I, stream=s, profile=profile)
         out = {"I": self.I}
-        out["S_rings"] = X.xpcs_structure_factor_shells(self.I, form_factors, wl.N, self.bins, wl.n_bins, stream=s,
-                                                        profile=profile)
-        if wl.lags:
-            X.xpcs_g2(self.I, wl.lags, out=self.g2, out_dtype=X.F32, stream=s, profile=profile)
-            out["g2"] = self.g2
-            out["g2_rings"] = X.xpcs_shell_mean(self.g2, self.bins, wl.n_bins, stream=s, profile=profile)
-        if wl.windows:
-            out["beta"] = X.xsvs_contrast(self.I, self.bins, wl.n_bins, wl.windows, stream=s, profile=profile)
+        self._reductions(out, self.I, form_factors, s, profile)
         return out
+
+    def _reductions(self, out, I, form_factors, s, profile=False, after_g2=None):
+        """g2 + g2 rings on side stream 0, XSVS on side stream 1, S rings on the caller's stream s; joined into s.
+        after_g2(stream): optional hook enqueued on side stream 0 right after g2 (e.g. its D2H copy)."""
+        wl = self.wl
+        main = s if s is not None else torch.cuda.current_stream(self.device)
+        ev = torch.cuda.Event()
+        ev.record(main)
+        r0, r1 = self.s_red
+        r0.wait_event(ev)
+        r1.wait_event(ev)
+        if wl.lags:
+            X.xpcs_g2(I, wl.lags, out=self.g2, out_dtype=X.F32, stream=r0, profile=profile)
+            out["g2"] = self.g2
+            if after_g2 is not None:
+                after_g2(r0)
+            out["g2_rings"] = X.xpcs_shell_mean(self.g2, self.bins, wl.n_bins, stream=r0, profile=profile)
+        if wl.windows:
+            out["beta"] = X.xsvs_contrast(I, self.bins, wl.n_bins, wl.windows, stream=r1, profile=profile)
+        out["S_rings"] = X.xpcs_structure_factor_shells(I, form_factors, wl.N, self.bins, wl.n_bins, stream=main,
+                                                        profile=profile)
+        main.wait_stream(r0)
+        main.wait_stream(r1)
 
     # ---------------------------------------------------------------- end to end from host memory
     def alloc_host_io(self, pos_host: np.ndarray, f_host: np.ndarray | None, batches: int = 8):
@@ -167,21 +186,18 @@ class Pipeline:
         for sc in self.s_comp:
             main.wait_stream(sc)
         out = {}
-        if wl.lags:
-            # g2 first: its (largest) result streams back on the copy stream while the ring reductions run
-            X.xpcs_g2(self.I, wl.lags, out=self.g2, out_dtype=X.F32, stream=main)
-            out["g2"] = self.g2
-            if "g2" not in self.h_out:
-                self.h_out["g2"] = torch.empty(self.g2.shape, dtype=self.g2.dtype, pin_memory=True)
+        if wl.lags and "g2" not in self.h_out:
+            self.h_out["g2"] = torch.empty(self.g2.shape, dtype=self.g2.dtype, pin_memory=True)
+
+        def g2_back(st):
+            # g2 (the largest reduction result) streams back on the copy stream while the other reductions run
             e = torch.cuda.Event()
-            e.record(main)
+            e.record(st)
             self.s_d2h.wait_event(e)
             with torch.cuda.stream(self.s_d2h):
                 self.h_out["g2"].copy_(self.g2, non_blocking=True)
-            out["g2_rings"] = X.xpcs_shell_mean(self.g2, self.bins, wl.n_bins, stream=main)
-        out["S_rings"] = X.xpcs_structure_factor_shells(self.I, self.d_f, wl.N, self.bins, wl.n_bins, stream=main)
-        if wl.windows:
-            out["beta"] = X.xsvs_contrast(self.I, self.bins, wl.n_bins, wl.windows, stream=main)
+
+        self._reductions(out, self.I, self.d_f, main, after_g2=g2_back)
         for k, v in out.items():
             if k == "g2":
                 continue
