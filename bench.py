@@ -203,6 +203,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of replaying its CUDA graph")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -238,7 +239,14 @@ def main():
     stream = torch.cuda.current_stream()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     xp.profile_reset()
+    graph = None
+    if not args.no_graph:
+        # the step as one CUDA graph (kernels, side-stream fork/join, profiling events): no host launch gaps inside
+        # the timed region; every replay recomputes everything from pos_d
+        graph, _ = P.capture(pos_d, f_d, profile=True)
+        launches_graph = P.capture_launches
     n_launch0 = xp.launch_count()
+    prof = {}
     with ClockSampler(local) as clk:
         for i in range(args.steps):
             flush.zero_()                                   # L2 flush between timed iterations (untimed)
@@ -246,13 +254,23 @@ def main():
                 dist.barrier()
             torch.cuda.synchronize()
             ev[i][0].record(stream)
-            P.run(pos_d, f_d, profile=True)
+            if graph is not None:
+                graph.replay()
+            else:
+                P.run(pos_d, f_d, profile=True)
             ev[i][1].record(stream)
             torch.cuda.synchronize()
-    n_launch = xp.launch_count() - n_launch0
+            if graph is not None:
+                for k, (t_ms, n_k) in xp.profile_query().items():   # this replay's kernel-class times
+                    a0, n0 = prof.get(k, (0.0, 0))
+                    prof[k] = (a0 + t_ms, n0 + n_k)
+    if graph is not None:
+        n_launch = launches_graph * args.steps
+    else:
+        n_launch = xp.launch_count() - n_launch0
+        prof = xp.profile_query()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms = float(np.mean(step_ms))
-    prof = xp.profile_query()
     ms = xd.max_over_ranks(ms, dev)
     pairs_step = P.pairs_per_step
     value = ws * pairs_step / (ms / 1e3)
@@ -330,6 +348,7 @@ def main():
         P.alloc_host_io(pos_h, f_h)
         P.run_host()
         torch.cuda.synchronize()
+        g_host = None if args.no_graph else P.capture_host()[0]
         t_e = []
         for _ in range(max(2, args.steps)):
             if dist is not None:
@@ -338,7 +357,10 @@ def main():
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            P.run_host()
+            if g_host is not None:
+                g_host.replay()
+            else:
+                P.run_host()
             b.record(stream)
             torch.cuda.synchronize()
             t_e.append(a.elapsed_time(b))
@@ -388,6 +410,7 @@ def main():
                            "pairs_per_step_per_gpu": pairs_step, "engine": args.engine,
                            "engine_used": ("fp64" if wl.in_dtype == xp.F64 else eng_name),
                            "l2": "flushed between timed steps (256 MB write, untimed)",
+                           "launch": "eager" if args.no_graph else "cuda graph (one replay per step)",
                            "parallelism": f"weak x{ws} (independent trajectories)"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(n_launch),
                 "clocks": clk.summary(), "step_ms_all": step_ms,

@@ -279,11 +279,10 @@ static int prep_groups(const xpcs_species* sp, const void* form_factors, int64_t
 
 static int upload_groups(Groups& G, cudaStream_t s) {
     if (!G.n_species) return XPCS_OK;
-    const size_t bytes = sizeof(int32_t) * G.perm.size();
-    int32_t* d = (int32_t*)scratch(s, SS_IDX, bytes);
-    if (!d) return XPCS_ENOMEM;
-    // pageable source: the copy is staged before cudaMemcpyAsync returns, so `perm` may be freed afterwards
-    TRY(cuda_fail(cudaMemcpyAsync(d, G.perm.data(), bytes, cudaMemcpyHostToDevice, s), "species upload"));
+    (void)s;
+    // cached device copy keyed by content (graph-capturable after one eager call; see host_table)
+    const int32_t* d = (const int32_t*)host_table(G.perm.data(), sizeof(int32_t) * G.perm.size());
+    if (!d) return XPCS_ECUDA;
     G.d_idx = d;
     return XPCS_OK;
 }
@@ -877,9 +876,8 @@ int xpcs_isf(const void* A_series, int64_t frames, int64_t n_q, const int32_t* l
         return XPCS_EUNSUPPORTED;
     }
     TRY(check_sticky());
-    int32_t* dl = (int32_t*)scratch(o.s, SS_LAGS, sizeof(int32_t) * (size_t)n_lags);
-    if (!dl) return XPCS_ENOMEM;
-    TRY(cuda_fail(cudaMemcpyAsync(dl, lags, sizeof(int32_t) * (size_t)n_lags, cudaMemcpyHostToDevice, o.s), "lag upload"));
+    const int32_t* dl = lag_table(lags, n_lags);
+    if (!dl) return XPCS_ECUDA;
     double* norm = nullptr;
     if (form_factors) {
         norm = (double*)scratch(o.s, SS_SMALL, 64);
@@ -915,9 +913,8 @@ int xpcs_g2(const void* I_series, int64_t frames, int64_t n_q, const int32_t* la
         return XPCS_EUNSUPPORTED;
     }
     TRY(check_sticky());
-    int32_t* dl = (int32_t*)scratch(o.s, SS_LAGS, sizeof(int32_t) * (size_t)n_lags);
-    if (!dl) return XPCS_ENOMEM;
-    TRY(cuda_fail(cudaMemcpyAsync(dl, lags, sizeof(int32_t) * (size_t)n_lags, cudaMemcpyHostToDevice, o.s), "lag upload"));
+    const int32_t* dl = lag_table(lags, n_lags);
+    if (!dl) return XPCS_ECUDA;
     ProfScope p(o.profile, KC_G2, o.s);
     return cuda_fail(launch_g2(I_series, o.in_f64, frames, n_q, dl, n_lags, max_lag, g2_out, o.out_f64, o.s), "g2");
 }

@@ -32,6 +32,8 @@ struct ProfScope {
 };
 
 int sm_count();
+const void* host_table(const void* data, size_t bytes);    // cached device copy of a host table (by content)
+const int32_t* lag_table(const int32_t* lags, int64_t n);   // host_table of a lag list
 
 // ------------------------------------------------------------------------------------------------
 // device helpers

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <vector>
 
+
 namespace xpcs {
 
 // =====================================================================================================
@@ -334,13 +335,18 @@ cudaError_t launch_shell_mean(const void* v, int in_f64, int64_t rows, int64_t n
 }
 
 // =====================================================================================================
-// K5: XSVS.  One warp per (32 pixels of a ring segment, exposure window W).  Each lane streams its pixel's
-// series, keeps the running window sum (registers), and when a window closes the warp
-// reduces (I_W, I_W^2) with shuffles; lane 0 writes the warp's moments for slot (W, s).  A second kernel sums
-// the warps of each ring in fixed order, forms beta_{W,b,s} (population variance / mean^2) and averages over s.
+// K5: XSVS.  Per warp: 32 pixels of a ring segment; each lane streams its pixel's series, keeps the running
+// window sums (registers) and at each window close the warp's moments (sum I_W, sum I_W^2) for slot (W, s) are
+// formed in a fixed order.  k_xsvs_warp2 (used by xsvs_contrast) reads the series once for all windows of the pass;
+// k_xsvs_warp (one warp per window, shuffle reductions) serves the single-window speckle histogram and
+// XPCS_XSVS_V1=1 builds.  A second kernel sums the warps of each ring in fixed order, forms beta_{W,b,s}
+// (population variance / mean^2) and averages over s.
 // =====================================================================================================
 #ifndef XPCS_XWPW
 #define XPCS_XWPW 1
+#endif
+#ifndef XPCS_XSVS_V1
+#define XPCS_XSVS_V1 0       // 1: the previous one-warp-per-window kernel (timing comparisons)
 #endif
 namespace { constexpr int XW = 8, XWPW = XPCS_XWPW; }   // windows per pass / per warp
 struct WinSet {
@@ -415,6 +421,113 @@ k_xsvs_warp(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __r
     }
 }
 
+// One warp per 32 pixels of a ring segment and ALL windows of the pass: the series is read once (the windows share
+// it), gathered by cp.async into a warp-private double-buffered shared ring (FC frames per chunk, every load of a
+// chunk in flight at once: the gather is latency-bound otherwise).  A window close writes the lane's (I_W, I_W^2)
+// into a warp-private buffer [slot][lane] (rows padded to 33 double2: conflict-free both ways); every XB closes the
+// warp sums the buffered slots across lanes (one lane per slot, 32 loads in lane order: a fixed order) and writes
+// the warp's moments.
+namespace { constexpr int XB = 16, XWARPS = 4, XFC = 32; }
+template <typename In>
+__host__ __device__ constexpr size_t xsvs2_smem() {
+    return (size_t)XWARPS * ((size_t)XB * 33 * sizeof(double2) + (size_t)XB * sizeof(int) + 2 * XFC * 32 * sizeof(In));
+}
+template <typename In>
+__global__ void __launch_bounds__(32 * XWARPS)
+k_xsvs_warp2(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __restrict__ perm,
+             const int32_t* __restrict__ off, const int32_t* __restrict__ woff, int32_t n_bins, int64_t total_warps,
+             WinSet ws, double2* __restrict__ mom) {
+    extern __shared__ __align__(16) unsigned char xs_smem[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    unsigned char* base = xs_smem + (size_t)wib * (XB * 33 * sizeof(double2) + XB * sizeof(int) + 2 * XFC * 32 * sizeof(In));
+    double2 (*B)[33] = reinterpret_cast<double2 (*)[33]>(base);
+    In* ser = reinterpret_cast<In*>(base + XB * 33 * sizeof(double2));          // [2][XFC][32]
+    int* ids = reinterpret_cast<int*>(base + XB * 33 * sizeof(double2) + 2 * XFC * 32 * sizeof(In));
+    const int64_t gw = (int64_t)blockIdx.x * XWARPS + wib;
+    if (gw >= total_warps || gw >= woff[n_bins]) return;
+    int lo = 0, hi = n_bins;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (woff[mid] <= gw) lo = mid; else hi = mid;
+    }
+    const int b = lo;
+    const int64_t idx = off[b] + (gw - woff[b]) * 32 + lane;
+    const bool valid = idx < off[b + 1];
+    const int64_t px = valid ? perm[idx] : 0;
+    const int nw = ws.n;
+    double run[XW];
+    int cnt[XW], sidx[XW];
+    int64_t Tuse = 0;
+#pragma unroll
+    for (int k = 0; k < XW; ++k) {
+        run[k] = 0.0;
+        cnt[k] = k < nw ? ws.W[k] : 1;
+        sidx[k] = 0;
+        if (k < nw) Tuse = max(Tuse, (int64_t)ws.S[k] * ws.W[k]);
+    }
+    const int n_chunks = (int)((Tuse + XFC - 1) / XFC);
+    auto prefetch = [&](int c) {
+        if (c < n_chunks) {
+            const uint32_t dst0 = (uint32_t)__cvta_generic_to_shared(ser + (size_t)(c & 1) * XFC * 32 + lane);
+#pragma unroll 8
+            for (int u = 0; u < XFC; ++u) {
+                const int64_t t = (int64_t)c * XFC + u;
+                const bool ok = valid && t < Tuse;
+                const In* src = I + (ok ? t * n_q + px : 0);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(dst0 + (uint32_t)(u * 32 * sizeof(In))),
+                             "l"(src), "n"(sizeof(In)), "r"(ok ? (uint32_t)sizeof(In) : 0u)
+                             : "memory");
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    int nb = 0;                                   // buffered closes (warp-uniform)
+    auto flush = [&]() {
+        __syncwarp();
+        if (lane < nb) {
+            double m1 = 0.0, m2 = 0.0;
+#pragma unroll 8
+            for (int i = 0; i < 32; ++i) {
+                const double2 v = B[lane][i];
+                m1 += v.x;
+                m2 += v.y;
+            }
+            mom[gw * ws.total_slots + ids[lane]] = make_double2(m1, m2);
+        }
+        __syncwarp();
+        nb = 0;
+    };
+    prefetch(0);
+    for (int c = 0; c < n_chunks; ++c) {
+        prefetch(c + 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncwarp();
+        const In* sc = ser + (size_t)(c & 1) * XFC * 32 + lane;
+        const int un = (int)min((int64_t)XFC, Tuse - (int64_t)c * XFC);
+        for (int u = 0; u < un; ++u) {
+            const double v = (double)sc[u * 32];
+#pragma unroll
+            for (int k = 0; k < XW; ++k) {
+                if (k >= nw) break;
+                run[k] += v;
+                if (--cnt[k] == 0) {
+                    if (sidx[k] < ws.S[k]) {
+                        B[nb][lane] = make_double2(run[k], run[k] * run[k]);
+                        if (lane == 0) ids[nb] = ws.base[k] + sidx[k];
+                        ++sidx[k];
+                        if (++nb == XB) flush();
+                    }
+                    run[k] = 0.0;
+                    cnt[k] = ws.W[k];
+                }
+            }
+        }
+        __syncwarp();                             // chunk c's buffer is refilled by prefetch(c + 2)
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    if (nb > 0) flush();
+}
+
 __global__ void __launch_bounds__(256)
 k_xsvs_final(const double2* __restrict__ mom, const int32_t* __restrict__ off, const int32_t* __restrict__ woff,
              WinSet ws, int w_first, int32_t n_bins, double* __restrict__ beta_out) {
@@ -471,13 +584,28 @@ cudaError_t launch_xsvs(const void* I, int in_f64, int64_t T, int64_t n_q, BinPl
             slots += ws.S[i];
         }
         ws.total_slots = slots;
-        const unsigned blocks = (unsigned)((max_warps + 3) / 4);
         note_launch(2);
+#if XPCS_XSVS_V1
+        const unsigned blocks = (unsigned)((max_warps + 3) / 4);
         if (blocks > 0) {
             const dim3 gr(blocks, (unsigned)((ws.n + XWPW - 1) / XWPW));
             if (in_f64) k_xsvs_warp<double><<<gr, 128, 0, s>>>((const double*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, ws, (double2*)warp_moments);
             else k_xsvs_warp<float><<<gr, 128, 0, s>>>((const float*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, ws, (double2*)warp_moments);
         }
+#else
+        const unsigned blocks = (unsigned)((max_warps + XWARPS - 1) / XWARPS);
+        if (blocks > 0) {
+            if (in_f64) {
+                static bool a = false;
+                if (!a) { cudaFuncSetAttribute(k_xsvs_warp2<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsvs2_smem<double>()); a = true; }
+                k_xsvs_warp2<double><<<blocks, 32 * XWARPS, xsvs2_smem<double>(), s>>>((const double*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, ws, (double2*)warp_moments);
+            } else {
+                static bool a = false;
+                if (!a) { cudaFuncSetAttribute(k_xsvs_warp2<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsvs2_smem<float>()); a = true; }
+                k_xsvs_warp2<float><<<blocks, 32 * XWARPS, xsvs2_smem<float>(), s>>>((const float*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, ws, (double2*)warp_moments);
+            }
+        }
+#endif
         k_xsvs_final<<<dim3(ws.n, n_bins), 256, 0, s>>>((const double2*)warp_moments, plan.offsets, plan.warp_off, ws,
                                                         (int)w0, n_bins, beta_out);
         cudaError_t e = cudaGetLastError();

@@ -1,5 +1,7 @@
 // runtime.cu -- error strings, launch counting, cached device scratch and event profiling for libxpcs.so.
 #include "common.cuh"
+#include <algorithm>
+#include <cstring>
 #include "../../include/xpcs.h"
 
 #include <atomic>
@@ -43,6 +45,12 @@ void* scratch(cudaStream_t s, int slot, size_t bytes) {
     Buf& b = g_scratch[{{dev, s}, slot}];
     if (bytes == 0) bytes = 16;
     if (b.n >= bytes) return b.p;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+        // no allocation inside a CUDA graph capture: run the same call once outside the capture first
+        set_error("xpcs: scratch slot %d must grow to %zu bytes during graph capture (warm up outside the capture)", slot, bytes);
+        return nullptr;
+    }
     if (b.p) {
         cudaStreamSynchronize(s);      // the old buffer may still be in use by queued work on s
         cudaFree(b.p);
@@ -94,20 +102,83 @@ int sm_count() {   // of the current device (cached per device)
     return n;
 }
 
+// ---------------------------------------------------------------- host tables
+// device copies of small host tables (lag lists, species permutations), cached by content per device: the upload
+// is synchronous and happens once per distinct table, so calls inside a CUDA graph capture (after one call outside
+// it) carry no pageable host-memory copy.  At most kTables entries; evicting one synchronises the device.
+constexpr size_t kTables = 32;
+const void* host_table(const void* data, size_t bytes) {
+    struct Entry { int dev; uint64_t h; std::vector<unsigned char> v; void* d; };
+    static std::vector<Entry> tab;
+    uint64_t h = 1469598103934665603ull ^ bytes;   // FNV-1a over 64-bit words (then the tail bytes)
+    const unsigned char* p = (const unsigned char*)data;
+    size_t i = 0;
+    for (; i + 8 <= bytes; i += 8) {
+        uint64_t w;
+        std::memcpy(&w, p + i, 8);
+        h ^= w;
+        h *= 1099511628211ull;
+    }
+    for (; i < bytes; ++i) { h ^= p[i]; h *= 1099511628211ull; }
+    std::lock_guard<std::mutex> lk(g_mu);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    for (size_t k = 0; k < tab.size(); ++k) {
+        Entry& e = tab[k];
+        if (e.dev == dev && e.h == h && e.v.size() == bytes && std::memcmp(e.v.data(), data, bytes) == 0) {
+            if (k + 1 < tab.size()) std::rotate(tab.begin() + k, tab.begin() + k + 1, tab.end());   // most recent last
+            return tab.back().d;
+        }
+    }
+    if (tab.size() >= kTables) {
+        cudaDeviceSynchronize();
+        int d0 = 0;
+        cudaGetDevice(&d0);
+        cudaSetDevice(tab.front().dev);
+        cudaFree(tab.front().d);
+        cudaSetDevice(d0);
+        tab.erase(tab.begin());
+    }
+    void* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, std::max<size_t>(bytes, 16));
+    if (e == cudaSuccess) e = cudaMemcpy(d, data, bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        if (d) cudaFree(d);
+        set_error("xpcs: table upload failed (%s); inside a CUDA graph capture, run the call once outside it first",
+                  cudaGetErrorString(e));
+        return nullptr;
+    }
+    tab.push_back({dev, h, std::vector<unsigned char>(p, p + bytes), d});
+    return d;
+}
+const int32_t* lag_table(const int32_t* lags, int64_t n) {
+    return (const int32_t*)host_table(lags, sizeof(int32_t) * (size_t)n);
+}
+
 // ---------------------------------------------------------------- profiling
 static const char* kClassNames[KC_COUNT] = {"intensity_main", "stage", "amplitude_reduce", "g2", "xsvs", "rings"};
 struct ProfRec { std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev; };
 static ProfRec g_prof[KC_COUNT];
 
+// inside a CUDA graph capture the events become external event-record nodes: every replay re-records them, so
+// profile_query() after a replay returns that replay's kernel times
+static void prof_record(cudaEvent_t e, cudaStream_t s) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive)
+        cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+    else
+        cudaEventRecord(e, s);
+}
 ProfScope::ProfScope(bool on, int cls, cudaStream_t s) : on_(on), cls_(cls), s_(s), a_(nullptr), b_(nullptr) {
     if (!on_) return;
     cudaEventCreate(&a_);
     cudaEventCreate(&b_);
-    cudaEventRecord(a_, s_);
+    prof_record(a_, s_);
 }
 ProfScope::~ProfScope() {
     if (!on_) return;
-    cudaEventRecord(b_, s_);
+    prof_record(b_, s_);
     std::lock_guard<std::mutex> lk(g_mu);
     g_prof[cls_].ev.push_back({a_, b_});
 }

@@ -13,6 +13,7 @@ inputs, the device pass, and the device -> host copy of its results.
 from __future__ import annotations
 
 import dataclasses
+import os
 
 import numpy as np
 import torch
@@ -110,6 +111,8 @@ class Pipeline:
         ev = torch.cuda.Event()
         ev.record(main)
         r0, r1 = self.s_red
+        if os.environ.get("XPCS_SERIAL_REDUCTIONS") == "1":   # experiments: isolated kernel timings
+            r0 = r1 = main
         r0.wait_event(ev)
         r1.wait_event(ev)
         if wl.lags:
@@ -124,6 +127,39 @@ class Pipeline:
                                                         profile=profile)
         main.wait_stream(r0)
         main.wait_stream(r1)
+
+    # ---------------------------------------------------------------- CUDA graphs of a step
+    def _capture(self, fn, warmup=2, warm_fn=None):
+        """Capture fn() (one whole step, all streams forked from and joined into the capture stream) into a CUDA
+        graph.  The library's scratch, lag tables and ring plan are sized by `warmup` eager calls on the capture
+        stream first (nothing is allocated inside the capture).  Returns (graph, fn's result); graph.replay() reruns
+        the step on the same buffers."""
+        cur = torch.cuda.current_stream(self.device)
+        cs = torch.cuda.Stream(self.device)
+        cs.wait_stream(cur)
+        with torch.cuda.stream(cs):
+            for _ in range(warmup):
+                (warm_fn or fn)()
+        cur.wait_stream(cs)
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        n0 = X.launch_count()
+        with torch.cuda.graph(g, stream=cs):
+            res = fn()
+        self.capture_launches = X.launch_count() - n0     # library kernels per replay
+        torch.cuda.synchronize(self.device)
+        return g, res
+
+    def capture(self, positions: torch.Tensor, form_factors: torch.Tensor | None, profile=False):
+        """CUDA graph of run(positions, form_factors): replay() recomputes I, g2, rings and XSVS from the current
+        contents of `positions` (same tensor).  With profile=True the library's kernel-class events are external
+        event-record nodes (xpcs_profile_query() after a replay reads that replay's times)."""
+        return self._capture(lambda: self.run(positions, form_factors, profile=profile),
+                             warm_fn=lambda: self.run(positions, form_factors))
+
+    def capture_host(self):
+        """CUDA graph of run_host() (needs alloc_host_io): H2D of the pinned inputs, the step, D2H of every result."""
+        return self._capture(self.run_host)
 
     # ---------------------------------------------------------------- end to end from host memory
     def alloc_host_io(self, pos_host: np.ndarray, f_host: np.ndarray | None, batches: int = 8):
