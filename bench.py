@@ -339,6 +339,18 @@ def main():
     tensor_src = (f"{peak_src}, {'burst' if at_max else 'sustained'} bf16"
                   + (" x 2 (int8)" if i8_used else (" blended int8/fp16" if hybrid_share else "")))
     roof["peak_source"] = tensor_src if roof["bound"] == "tensor" else "derived (DESIGN.md)"
+    if roof["bound"] == "tensor":
+        # context: the same achieved rate against the tcgen05 issue rate microbenchmarked at the run's SM clock
+        # (tools/mma_rate.cu: 8190 int8 / 4095 fp16 MAC per clock per SM; 2 ops per MAC), which sits above the
+        # cuBLAS-measured peak the roofline uses (cuBLAS runs power-capped, MEASURED_PEAKS clocks_under_load)
+        mhz_run = clk_sum.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+        if hybrid_share is not None:
+            rate = 1.0 / (hybrid_share / 8190.0 + (1.0 - hybrid_share) / 4095.0)
+        else:
+            rate = 8190.0 if i8_used else 4095.0
+        mma_peak = sm_count * rate * 2 * mhz_run * 1e6 / 1e12
+        roof["vs_mma_issue_rate"] = {"peak": mma_peak, "frac": roof["achieved"] / mma_peak,
+                                     "clock_mhz": mhz_run, "source": "tools/mma_rate.cu"}
     roof["kernel_ms"] = per_launch_ms
     roof["kernel_share_of_step"] = main_ms / args.steps / ms if ms > 0 else None
 

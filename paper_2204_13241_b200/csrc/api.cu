@@ -673,6 +673,10 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
     for (const FrameBatch& fb : batches) {
         const int64_t v0 = fb.v0, vb = fb.vb;
         if (fb.chunk > 0) { chunk[0] = fb.chunk; C[0] = (G.cnt[0] + fb.chunk - 1) / fb.chunk; }
+        void* dst = (char*)I_out + isz * n_q * v0;
+        // one integer-engine group in a single atom chunk: the kernel writes the result itself (no partial planes)
+        const bool direct = ng == 1 && !G.n_species && i8 && gi8[0] && G.cnt[0] > 0 && C[0] == 1 &&
+                            !(getenv("XPCS_I8_DIRECT") && atoi(getenv("XPCS_I8_DIRECT")) == 0);
         int64_t stoff = 0, poff = 0;
         for (int gi = 0; gi < ng; ++gi) {
             const int64_t Ng = G.cnt[gi];
@@ -685,13 +689,14 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
             { ProfScope p(o.profile, KC_MAIN, o.s);
               const bool g_i8 = i8 && gi8[(size_t)gi], g_tc = (i8 || tc) && !g_i8;
               if (g_i8) TRY(cuda_fail(launch_lattice_i8(st + stoff, Ng, vb, g, chunk[gi], C[gi], fmax, form_factors == nullptr,
-                                                      part + poff, o.s), "lattice tcgen05 i8"));
+                                                      part + poff, o.s, direct ? dst : nullptr, o.out_f64, mode),
+                                    "lattice tcgen05 i8"));
               else if (g_tc) TRY(cuda_fail(launch_lattice_tc(st + stoff, Ng, vb, g, chunk[gi], C[gi], part + poff, o.s), "lattice tcgen05"));
               else TRY(cuda_fail(launch_lattice_simt(st + stoff, Ng, vb, g, chunk[gi], C[gi], part + poff, o.s), "lattice simt")); }
             stoff += Ng * vb;
             poff += C[gi] * n_q * vb;
         }
-        void* dst = (char*)I_out + isz * n_q * v0;
+        if (direct) continue;
         ProfScope p(o.profile, KC_REDUCE, o.s);
         if (G.n_species) TRY(cuda_fail(launch_species_combine(sp, vb, n_q, G.fq, 0, v0, n_l, dst, o.out_f64, mode, o.s), "species combine"));
         else TRY(cuda_fail(launch_amp_reduce_f(part, C[0], vb, n_q, dst, o.out_f64, mode, o.s), "reduce"));

@@ -170,7 +170,8 @@ bool lattice_tc_supported(const LatticeGeom& g);
 constexpr int64_t kI8MaxChunk = 32768;
 int i8_cluster_slots();   // k_lattice_i8 clusters resident at once (cudaOccupancyMaxActiveClusters)
 cudaError_t launch_lattice_i8(const uint4* staged, int64_t N, int64_t frames, const LatticeGeom& g, int64_t chunk_atoms,
-                              int64_t n_chunks, float* fmax_scratch, int uniform_f, float2* partial, cudaStream_t s);
+                              int64_t n_chunks, float* fmax_scratch, int uniform_f, float2* partial, cudaStream_t s,
+                              void* direct_out = nullptr, int out_f64 = 0, int mode = 0);
 // lattice FP64 (direct per-pixel evaluation with 64-bit turns): writes I directly (double)
 cudaError_t launch_lattice_f64(const ulonglong4* staged, int64_t N, int64_t frames, const LatticeGeom& g,
                                void* I_out, int out_f64, int mode, cudaStream_t s);

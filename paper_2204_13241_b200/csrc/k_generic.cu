@@ -176,7 +176,15 @@ __global__ void __launch_bounds__(256)
 k_amp_reduce(const P* __restrict__ partial, int64_t C, int64_t total, O* __restrict__ out, int mode) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         double re = 0.0, im = 0.0;
-        for (int64_t c = 0; c < C; ++c) {
+        int64_t c = 0;
+        for (; c + 4 <= C; c += 4) {          // four loads in flight, added in chunk order
+            P v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = partial[(c + u) * total + i];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) { re += (double)v[u].x; im += (double)v[u].y; }
+        }
+        for (; c < C; ++c) {
             const P v = partial[c * total + i];
             re += (double)v.x;
             im += (double)v.y;

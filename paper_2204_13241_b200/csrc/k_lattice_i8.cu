@@ -137,6 +137,7 @@ __device__ __forceinline__ unsigned long long f2mul(unsigned long long a, unsign
 }
 __device__ __forceinline__ unsigned long long swap2(unsigned long long v) { return (v >> 32) | (v << 32); }
 
+#if !XPCS_I8_Q16
 // (c, s) -> limb magic floats: t1 = M + hi (low byte = hi), t2 = M + lo (low byte = lo), element-wise on (c, s).
 // u = M - 254 hi is exact (an integer < 2^24); t2 = fl(32258 v + u) rounds once to the integer grid of M, so
 // t2 = M + rint(32258 v - 254 hi) = M + lo with |lo| <= 127 (|32258 v - 254 hi| = 254 |127 v - hi| <= 127).
@@ -150,17 +151,20 @@ __device__ __forceinline__ void quantise(unsigned long long v, unsigned long lon
 __device__ __forceinline__ uint32_t pack_bytes(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
     return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
 }
+#endif
 // Q16: four magic words (atoms 0..3) -> (hi bytes, lo bytes) words, byte t = atom t
 __device__ __forceinline__ void q16_pack(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3, uint32_t& hi, uint32_t& lo) {
     const uint32_t p01 = __byte_perm(t0, t1, 0x5140), p23 = __byte_perm(t2, t3, 0x5140);   // [b0 b0' b1 b1']
     hi = __byte_perm(p01, p23, 0x7632);
     lo = __byte_perm(p01, p23, 0x5410) ^ 0x80808080u;
 }
+#if !XPCS_I8_Q16
 // per-byte two's-complement negation of four int8 in [-127, 127]
 __device__ __forceinline__ uint32_t neg_bytes(uint32_t w) {
     const uint32_t n = ~w;
     return ((n & 0x7F7F7F7Fu) + 0x01010101u) ^ (n & 0x80808080u);
 }
+#endif
 template <int OFF>
 __device__ __forceinline__ void i8_sts(uint32_t addr, uint32_t v) {
     asm volatile("st.shared.b32 [%0+%2], %1;" ::"r"(addr), "r"(v), "n"(OFF));
@@ -177,7 +181,8 @@ __device__ __forceinline__ void i8_sts(uint32_t addr, uint32_t v) {
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ti8::NTHREADS, 1)
 k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t chunk_atoms, int tiles_k,
-             float2* __restrict__ partial, int64_t frames, const float* __restrict__ fmax_dev, int dbg_flags) {
+             float2* __restrict__ partial, int64_t frames, const float* __restrict__ fmax_dev, int dbg_flags,
+             void* __restrict__ direct_out, int out_f64, int mode) {
     using namespace ti8;
     extern __shared__ __align__(1024) char smem_raw[];
     char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -468,15 +473,50 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
         const int tid = threadIdx.x;                     // 0..255
         const int rows = (int)min((int64_t)TM, g.n_h - th0), cols = (int)min((int64_t)TN, g.n_k - tk0);
         const bool vec = (g.n_k & 1) == 0;               // 16-B aligned pixel pairs
-        for (int e = tid; e < TM * (TN / 2); e += 256) {
-            const int r = e / (TN / 2), c2 = e % (TN / 2);
-            if (r >= rows || 2 * c2 >= cols) continue;
-            const float4 v = tile[r * TLD + c2];
-            float2* dst = P + (int64_t)(th0 + r) * g.n_k + tk0 + 2 * c2;
-            if (vec && 2 * c2 + 1 < cols) *reinterpret_cast<float4*>(dst) = v;
-            else {
-                dst[0] = make_float2(v.x, v.y);
-                if (2 * c2 + 1 < cols) dst[1] = make_float2(v.z, v.w);
+        if (direct_out == nullptr) {
+            for (int e = tid; e < TM * (TN / 2); e += 256) {
+                const int r = e / (TN / 2), c2 = e % (TN / 2);
+                if (r >= rows || 2 * c2 >= cols) continue;
+                const float4 v = tile[r * TLD + c2];
+                float2* dst = P + (int64_t)(th0 + r) * g.n_k + tk0 + 2 * c2;
+                if (vec && 2 * c2 + 1 < cols) *reinterpret_cast<float4*>(dst) = v;
+                else {
+                    dst[0] = make_float2(v.x, v.y);
+                    if (2 * c2 + 1 < cols) dst[1] = make_float2(v.z, v.w);
+                }
+            }
+        } else {
+            // single atom chunk: the final result straight from the tile, with the arithmetic of k_amp_reduce for
+            // C = 1 (FP64 |p|^2 of the fp32 amplitude, Eq. 8; or the amplitude p = conj of the accumulated value)
+            for (int e = tid; e < TM * (TN / 2); e += 256) {
+                const int r = e / (TN / 2), c2 = e % (TN / 2);
+                if (r >= rows || 2 * c2 >= cols) continue;
+                const float4 v = tile[r * TLD + c2];
+                const bool two = 2 * c2 + 1 < cols;
+                const int64_t i0 = t * n_q + (int64_t)(th0 + r) * g.n_k + tk0 + 2 * c2;
+                if (mode == 0) {
+                    const double I0 = (double)v.x * (double)v.x + (double)v.y * (double)v.y;
+                    const double I1 = (double)v.z * (double)v.z + (double)v.w * (double)v.w;
+                    if (out_f64) {
+                        double* o = (double*)direct_out + i0;
+                        o[0] = I0;
+                        if (two) o[1] = I1;
+                    } else {
+                        float* o = (float*)direct_out + i0;
+                        if (two && vec) *reinterpret_cast<float2*>(o) = make_float2((float)I0, (float)I1);
+                        else { o[0] = (float)I0; if (two) o[1] = (float)I1; }
+                    }
+                } else {
+                    if (out_f64) {
+                        double* o = (double*)direct_out + 2 * i0;
+                        o[0] = (double)v.x; o[1] = -(double)v.y;
+                        if (two) { o[2] = (double)v.z; o[3] = -(double)v.w; }
+                    } else {
+                        float* o = (float*)direct_out + 2 * i0;
+                        if (two && vec) *reinterpret_cast<float4*>(o) = make_float4(v.x, -v.y, v.z, -v.w);
+                        else { o[0] = v.x; o[1] = -v.y; if (two) { o[2] = v.z; o[3] = -v.w; } }
+                    }
+                }
             }
         }
     }
@@ -529,7 +569,9 @@ int i8_cluster_slots() {
 }
 
 cudaError_t launch_lattice_i8(const uint4* staged, int64_t N, int64_t frames, const LatticeGeom& g, int64_t chunk_atoms,
-                              int64_t n_chunks, float* fmax_scratch, int uniform_f, float2* partial, cudaStream_t s) {
+                              int64_t n_chunks, float* fmax_scratch, int uniform_f, float2* partial, cudaStream_t s,
+                              void* direct_out, int out_f64, int mode) {
+    if (direct_out && n_chunks != 1) return cudaErrorInvalidValue;
     using namespace ti8;
     if (chunk_atoms > kI8MaxChunk) return cudaErrorInvalidValue;
     const int tiles_h = (int)((g.n_h + PAIR_M - 1) / PAIR_M), tiles_k = (int)((g.n_k + TN - 1) / TN);
@@ -549,7 +591,8 @@ cudaError_t launch_lattice_i8(const uint4* staged, int64_t N, int64_t frames, co
     if (dbg < 0) { const char* e = getenv("XPCS_I8_DEBUG"); dbg = e ? atoi(e) : 0; }
     dim3 grid(2 * tiles_h * tiles_k, (unsigned)n_chunks, (unsigned)frames);
     note_launch();
-    k_lattice_i8<<<grid, NTHREADS, SMEM_BYTES, s>>>(staged, N, g, chunk_atoms, tiles_k, partial, frames, fm, dbg);
+    k_lattice_i8<<<grid, NTHREADS, SMEM_BYTES, s>>>(staged, N, g, chunk_atoms, tiles_k, partial, frames, fm, dbg,
+                                                    direct_out, out_f64, mode);
     return cudaGetLastError();
 }
 
