@@ -352,6 +352,10 @@ def main():
         mma_peak = sm_count * rate * 2 * mhz_run * 1e6 / 1e12
         roof["vs_mma_issue_rate"] = {"peak": mma_peak, "frac": roof["achieved"] / mma_peak,
                                      "clock_mhz": mhz_run, "source": "tools/mma_rate.cu"}
+    if roof["frac"] > 1.0 and not at_max:
+        roof["note"] = ("frac > 1 against the sustained cuBLAS figure: that figure was taken at the power-capped "
+                        "clock of a back-to-back matmul (MEASURED_PEAKS clocks_under_load), below this run's clock; "
+                        "vs_mma_issue_rate is the same rate against the tcgen05 issue rate at this run's clock")
     roof["kernel_ms"] = per_launch_ms
     roof["kernel_share_of_step"] = main_ms / args.steps / ms if ms > 0 else None
 
