@@ -56,10 +56,12 @@ k_g2(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __restrict
         if (!active) continue;
         if (consecutive) {
             const int t0l = tau[0];
-            for (int r0 = 0; r0 < rmax; r0 += 16) {          // rows beyond rmax are zero-padded or ignored
+            // rows t with t + tau_0 >= T only meet the zero halo: stop before them (the warp's smallest lag)
+            const int rlim = (int)min((int64_t)rmax, max((int64_t)0, T - t0 - t0l));
+            for (int r0 = 0; r0 < rlim; r0 += 16) {          // rows beyond rlim are zero-padded or ignored
                 double a[16], w[16 + G2_LPW];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) a[i] = (r0 + i < rmax) ? (double)S[(r0 + i) * 32 + lane] : 0.0;
+                for (int i = 0; i < 16; ++i) a[i] = (r0 + i < rlim) ? (double)S[(r0 + i) * 32 + lane] : 0.0;
 #pragma unroll
                 for (int j = 0; j < 16 + G2_LPW; ++j) w[j] = (double)S[(r0 + t0l + j) * 32 + lane];
 #pragma unroll
