@@ -11,27 +11,33 @@
 // HBM-bound: reads 12-24 B and writes 16-32 B per atom per frame (32 B for the generic fp32 record).
 // Staging also realises the 3-D q blocks (one virtual frame per (frame, l-plane)) and the species gather.
 #include "common.cuh"
+#include <algorithm>
 
 namespace xpcs {
 
-// Record i of a batch is staged atom j = i % N of virtual frame v = m.v0 + i / N; virtual frame v is source frame
+// Record i = vi * N + j of a batch is staged atom j of virtual frame v = m.v0 + vi; virtual frame v is source frame
 // t = v / m.n_l and reciprocal-lattice plane l = m.l0 + v % m.n_l (3-D q blocks: Th_0 = (m0 + l mc) . Xi); staged
-// atom j reads source atom m.idx[j] (species gather) or j.  Source frames hold m.n_src atoms.
-__device__ __forceinline__ int64_t stage_src(const StageMap& m, int64_t N, int64_t i, int64_t& v) {
-    v = m.v0 + i / N;
-    const int64_t j = i - (i / N) * N;
-    return m.idx ? (int64_t)m.idx[j] : j;
+// atom j reads source atom m.idx[j] (species gather) or j.  Source frames hold m.n_src atoms.  The grid is 2-D
+// (atoms x virtual frames): no per-record 64-bit division.
+#define STAGE_LOOPS(N, V)                                                                                          \
+    for (int64_t vi = blockIdx.y; vi < (V); vi += gridDim.y)                                                       \
+        for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < (N); j += (int64_t)gridDim.x * blockDim.x)
+__device__ __forceinline__ void stage_frame(const StageMap& m, int64_t vi, int64_t& t, int64_t& l) {
+    const int64_t v = m.v0 + vi;
+    t = m.n_l == 1 ? v : v / m.n_l;
+    l = m.l0 + (v - t * m.n_l);
 }
+__device__ __forceinline__ int64_t stage_atom(const StageMap& m, int64_t j) { return m.idx ? (int64_t)m.idx[j] : j; }
 
 template <typename P, typename F>
 __global__ void __launch_bounds__(256) k_stage_lattice32(const P* __restrict__ pos, const F* __restrict__ f,
-                                                         int64_t N, int64_t total, LatticeGeom g, StageMap m,
+                                                         int64_t N, int64_t V, LatticeGeom g, StageMap m,
                                                          uint4* __restrict__ out) {
     const double invL = 1.0 / g.L;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        int64_t v;
-        const int64_t src = stage_src(m, N, i, v);
-        const int64_t t = v / m.n_l, l = m.l0 + (v - t * m.n_l);
+    STAGE_LOOPS(N, V) {
+        int64_t t, l;
+        stage_frame(m, vi, t, l);
+        const int64_t src = stage_atom(m, j), i = vi * N + j;
         const P* r = pos + 3 * (t * m.n_src + src);
         uint32_t X[3];
 #pragma unroll
@@ -50,12 +56,12 @@ __global__ void __launch_bounds__(256) k_stage_lattice32(const P* __restrict__ p
 }
 
 __global__ void __launch_bounds__(256) k_stage_lattice64(const double* __restrict__ pos, const double* __restrict__ f,
-                                                         int64_t N, int64_t total, LatticeGeom g, StageMap m,
+                                                         int64_t N, int64_t V, LatticeGeom g, StageMap m,
                                                          ulonglong4* __restrict__ out) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        int64_t v;
-        const int64_t src = stage_src(m, N, i, v);
-        const int64_t t = v / m.n_l, l = m.l0 + (v - t * m.n_l);
+    STAGE_LOOPS(N, V) {
+        int64_t t, l;
+        stage_frame(m, vi, t, l);
+        const int64_t src = stage_atom(m, j), i = vi * N + j;
         const double* r = pos + 3 * (t * m.n_src + src);
         uint64_t X[3];
 #pragma unroll
@@ -77,12 +83,11 @@ __global__ void __launch_bounds__(256) k_stage_lattice64(const double* __restric
 // fractions as fp32 (for the fractional part of q.r, see k_generic.cu)
 template <typename P, typename F>
 __global__ void __launch_bounds__(256) k_stage_generic32(const P* __restrict__ pos, const F* __restrict__ f,
-                                                         int64_t N, int64_t total, double L, StageMap m,
+                                                         int64_t N, int64_t V, double L, StageMap m,
                                                          uint4* __restrict__ out) {
     const double invL = 1.0 / L;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        int64_t v;
-        const int64_t src = stage_src(m, N, i, v);
+    STAGE_LOOPS(N, V) {
+        const int64_t v = m.v0 + vi, src = stage_atom(m, j), i = vi * N + j;
         const P* r = pos + 3 * (v * m.n_src + src);
         const double ux = box_fraction_fast((double)r[0], invL), uy = box_fraction_fast((double)r[1], invL),
                      uz = box_fraction_fast((double)r[2], invL);
@@ -97,11 +102,10 @@ __global__ void __launch_bounds__(256) k_stage_generic32(const P* __restrict__ p
 }
 
 __global__ void __launch_bounds__(256) k_stage_generic64(const double* __restrict__ pos, const double* __restrict__ f,
-                                                         int64_t N, int64_t total, double L, StageMap m,
+                                                         int64_t N, int64_t V, double L, StageMap m,
                                                          ulonglong4* __restrict__ out) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        int64_t v;
-        const int64_t src = stage_src(m, N, i, v);
+    STAGE_LOOPS(N, V) {
+        const int64_t v = m.v0 + vi, src = stage_atom(m, j), i = vi * N + j;
         const double* r = pos + 3 * (v * m.n_src + src);
         const double fj = f ? f[src] : 1.0;
         out[i] = make_ulonglong4(frac_to_fixed64(box_fraction(r[0], L)), frac_to_fixed64(box_fraction(r[1], L)),
@@ -110,55 +114,53 @@ __global__ void __launch_bounds__(256) k_stage_generic64(const double* __restric
     }
 }
 
-static dim3 grid_for(int64_t total) {
-    int64_t b = (total + 255) / 256;
+// atoms x virtual frames, ~16 blocks of 256 threads per SM in total
+static dim3 grid_for(int64_t N, int64_t V) {
     const int64_t cap = (int64_t)sm_count() * 16;
-    return dim3((unsigned)(b < cap ? (b > 0 ? b : 1) : cap));
+    const int64_t bx = std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, cap));
+    const int64_t by = std::max<int64_t>(1, std::min<int64_t>({V, (cap + bx - 1) / bx, (int64_t)65535}));
+    return dim3((unsigned)bx, (unsigned)by);
 }
 
 cudaError_t launch_stage_lattice32(const void* pos, int pos_f64, const void* f, int f_f64, int64_t N,
                                    int64_t frames, const LatticeGeom& g, const StageMap& m, uint4* out, cudaStream_t s) {
-    const int64_t total = N * frames;
     note_launch();
-    const dim3 gr = grid_for(total);
+    const dim3 gr = grid_for(N, frames);
     if (pos_f64) {
-        if (f_f64) k_stage_lattice32<double, double><<<gr, 256, 0, s>>>((const double*)pos, (const double*)f, N, total, g, m, out);
-        else k_stage_lattice32<double, float><<<gr, 256, 0, s>>>((const double*)pos, (const float*)f, N, total, g, m, out);
+        if (f_f64) k_stage_lattice32<double, double><<<gr, 256, 0, s>>>((const double*)pos, (const double*)f, N, frames, g, m, out);
+        else k_stage_lattice32<double, float><<<gr, 256, 0, s>>>((const double*)pos, (const float*)f, N, frames, g, m, out);
     } else {
-        if (f_f64) k_stage_lattice32<float, double><<<gr, 256, 0, s>>>((const float*)pos, (const double*)f, N, total, g, m, out);
-        else k_stage_lattice32<float, float><<<gr, 256, 0, s>>>((const float*)pos, (const float*)f, N, total, g, m, out);
+        if (f_f64) k_stage_lattice32<float, double><<<gr, 256, 0, s>>>((const float*)pos, (const double*)f, N, frames, g, m, out);
+        else k_stage_lattice32<float, float><<<gr, 256, 0, s>>>((const float*)pos, (const float*)f, N, frames, g, m, out);
     }
     return cudaGetLastError();
 }
 
 cudaError_t launch_stage_lattice64(const void* pos, const void* f, int64_t N, int64_t frames,
                                    const LatticeGeom& g, const StageMap& m, ulonglong4* out, cudaStream_t s) {
-    const int64_t total = N * frames;
     note_launch();
-    k_stage_lattice64<<<grid_for(total), 256, 0, s>>>((const double*)pos, (const double*)f, N, total, g, m, out);
+    k_stage_lattice64<<<grid_for(N, frames), 256, 0, s>>>((const double*)pos, (const double*)f, N, frames, g, m, out);
     return cudaGetLastError();
 }
 
 cudaError_t launch_stage_generic32(const void* pos, int pos_f64, const void* f, int f_f64, int64_t N,
                                    int64_t frames, double L, const StageMap& m, uint4* out, cudaStream_t s) {
-    const int64_t total = N * frames;
     note_launch();
-    const dim3 gr = grid_for(total);
+    const dim3 gr = grid_for(N, frames);
     if (pos_f64) {
-        if (f_f64) k_stage_generic32<double, double><<<gr, 256, 0, s>>>((const double*)pos, (const double*)f, N, total, L, m, out);
-        else k_stage_generic32<double, float><<<gr, 256, 0, s>>>((const double*)pos, (const float*)f, N, total, L, m, out);
+        if (f_f64) k_stage_generic32<double, double><<<gr, 256, 0, s>>>((const double*)pos, (const double*)f, N, frames, L, m, out);
+        else k_stage_generic32<double, float><<<gr, 256, 0, s>>>((const double*)pos, (const float*)f, N, frames, L, m, out);
     } else {
-        if (f_f64) k_stage_generic32<float, double><<<gr, 256, 0, s>>>((const float*)pos, (const double*)f, N, total, L, m, out);
-        else k_stage_generic32<float, float><<<gr, 256, 0, s>>>((const float*)pos, (const float*)f, N, total, L, m, out);
+        if (f_f64) k_stage_generic32<float, double><<<gr, 256, 0, s>>>((const float*)pos, (const double*)f, N, frames, L, m, out);
+        else k_stage_generic32<float, float><<<gr, 256, 0, s>>>((const float*)pos, (const float*)f, N, frames, L, m, out);
     }
     return cudaGetLastError();
 }
 
 cudaError_t launch_stage_generic64(const void* pos, const void* f, int64_t N, int64_t frames, double L,
                                    const StageMap& m, ulonglong4* out, cudaStream_t s) {
-    const int64_t total = N * frames;
     note_launch();
-    k_stage_generic64<<<grid_for(total), 256, 0, s>>>((const double*)pos, (const double*)f, N, total, L, m, out);
+    k_stage_generic64<<<grid_for(N, frames), 256, 0, s>>>((const double*)pos, (const double*)f, N, frames, L, m, out);
     return cudaGetLastError();
 }
 
