@@ -22,7 +22,8 @@
 //     HH += Xr_hi.B1_hi + Xs_hi.B2_hi,   X += Xr_hi.B1_lo + Xr_lo.B1_hi + Xs_hi.B2_lo + Xs_lo.B2_hi
 // (B1 = [Wr | Ws], B2 = [-Ws | Wr]: D = [Re | Im'], Im' = -Im; the partials hold conj(p) like the fp16 engine).
 //
-// Producers: 3 groups of 6 warps; group g fills stages i = g mod 3 (6-stage ring, 28 KB per stage).  A warp thread
+// Producers: 5 groups of 6 warps; group g fills stages i = g mod 5 (5-stage ring, 28 KB per stage; the group count
+// must not exceed the stage count, see the empty-barrier parity note in DESIGN.md 6.1).  A warp thread
 // owns 4 consecutive atoms (one 32-bit word per row and limb plane) and 8 rows spaced 8 apart (X or W), and walks
 // the rows with the angle-addition recurrence X_{m+8} = X_m X_8 (packed FP32x2, 2 ops per phasor; 2 SFU sincos per
 // atom per thread), quantises with one packed magic-number FFMA per phasor (Q16) and packs limb bytes with PRMT.
@@ -42,16 +43,16 @@ constexpr int BROWS = 3 * BN;                       // [-Ws | Wr | Ws]
 constexpr int BPLANE = BROWS * KS;                  // 6 KB
 constexpr int STAGE_BYTES = 4 * APLANE + 2 * BPLANE;   // Xr_hi Xr_lo Xs_hi Xs_lo | B_hi B_lo = 28 KB
 #ifndef XPCS_I8_STAGES
-#define XPCS_I8_STAGES 6
+#define XPCS_I8_STAGES 5
 #endif
 constexpr int STAGES = XPCS_I8_STAGES;
 #ifndef XPCS_I8_GROUPS
-#define XPCS_I8_GROUPS 3
+#define XPCS_I8_GROUPS 5
 #endif
 constexpr int NGROUPS = XPCS_I8_GROUPS, GROUP_WARPS = 6;   // per group: 4 X warps (2 quad halves x 2 row halves), 2 W warps
-constexpr int NPROD_WARPS = NGROUPS * GROUP_WARPS;  // 18
+constexpr int NPROD_WARPS = NGROUPS * GROUP_WARPS;  // 30
 constexpr int MMA_WARP = NPROD_WARPS;               // warps 0-3 (distinct TMEM lane quarters) also drain the tile
-constexpr int NTHREADS = (MMA_WARP + 1) * 32;       // 608
+constexpr int NTHREADS = (MMA_WARP + 1) * 32;       // 992
 constexpr int MMA_N = 2 * TN;                       // 256
 constexpr int TMEM_COLS = 512;                      // HH cols [0, 256), X cols [256, 512)
 constexpr int ASL = 4;                              // atom-record slots per warp (cp.async prefetch distance ASL - 1)
@@ -170,6 +171,10 @@ __device__ __forceinline__ void i8_sts(uint32_t addr, uint32_t v) {
     asm volatile("st.shared.b32 [%0+%2], %1;" ::"r"(addr), "r"(v), "n"(OFF));
 }
 
+#define I8_TMEM_LD8(taddr, r)                                                                                      \
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"                            \
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])    \
+                 : "r"(taddr))
 #define I8_TMEM_LD16(taddr, r)                                                                                     \
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),  \
@@ -249,7 +254,7 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
         }
         __syncwarp();
     } else if (warp < NPROD_WARPS) {
-        // ================= producers: group g fills stages g, g + 3, g + 6, ... =================
+        // ================= producers: group g fills stages g, g + NGROUPS, g + 2 NGROUPS, ... =================
         const int grp = warp / GROUP_WARPS, wi = warp % GROUP_WARPS;
         const int qq = lane & 3, mr = lane >> 2;
         const bool is_x = wi < 4;
@@ -451,22 +456,22 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
         float4* tile = reinterpret_cast<float4*>(smem);
         constexpr int TLD = TN / 2 + 1;
 #pragma unroll 1
-        for (int kb = 4 * half; kb < 4 * half + 4; ++kb) {
-            const uint32_t cre = (uint32_t)(kb < 4 ? 16 * kb : 16 * kb + 64);   // [Re k<64 | Im' k<64 | Re k>=64 | Im' k>=64]
-            uint32_t hre[16], him[16], xre[16], xim[16];
-            I8_TMEM_LD16(tb + cre, hre);
-            I8_TMEM_LD16(tb + cre + 64, him);
-            I8_TMEM_LD16(tb + 256 + cre, xre);
-            I8_TMEM_LD16(tb + 256 + cre + 64, xim);
+        for (int kb = 8 * half; kb < 8 * half + 8; ++kb) {     // 8 pixel columns per step (32 registers of TMEM data)
+            const uint32_t cre = (uint32_t)(kb < 8 ? 8 * kb : 8 * kb + 64);   // [Re k<64 | Im' k<64 | Re k>=64 | Im' k>=64]
+            uint32_t hre[8], him[8], xre[8], xim[8];
+            I8_TMEM_LD8(tb + cre, hre);
+            I8_TMEM_LD8(tb + cre + 64, him);
+            I8_TMEM_LD8(tb + 256 + cre, xre);
+            I8_TMEM_LD8(tb + 256 + cre + 64, xim);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-            for (int j = 0; j < 16; j += 2) {
+            for (int j = 0; j < 8; j += 2) {
                 float4 v;
                 v.x = fmaf((float)(int32_t)hre[j], c_hh, (float)(int32_t)xre[j] * c_x);
                 v.y = fmaf((float)(int32_t)him[j], c_hh, (float)(int32_t)xim[j] * c_x);
                 v.z = fmaf((float)(int32_t)hre[j + 1], c_hh, (float)(int32_t)xre[j + 1] * c_x);
                 v.w = fmaf((float)(int32_t)him[j + 1], c_hh, (float)(int32_t)xim[j + 1] * c_x);
-                tile[row * TLD + 8 * kb + j / 2] = v;
+                tile[row * TLD + 4 * kb + j / 2] = v;
             }
         }
         asm volatile("bar.sync 1, 256;" ::: "memory");   // drain warps 0-7 only
