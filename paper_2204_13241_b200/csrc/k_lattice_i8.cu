@@ -57,7 +57,10 @@ constexpr int MMA_N = 2 * TN;                       // 256
 constexpr int TMEM_COLS = 512;                      // HH cols [0, 256), X cols [256, 512)
 constexpr int ASL = 4;                              // atom-record slots per warp (cp.async prefetch distance ASL - 1)
 constexpr int WREC = 16;                            // records a producer warp needs per stage (its 4 atom quads)
-constexpr int WSLOT = WREC + WREC / 4;              // record slots incl. one 16-B pad per quad (conflict-free LDS.128)
+// record r of a warp's stage sits in 16-B unit r ^ ((r & 8) >> 2) of its slot: the cp.async writes (8 lanes per
+// phase, records 0-7 / 8-15) and the per-field 32-bit reads of records {u, 4 + u, 8 + u, 12 + u} (one per quad)
+// both hit distinct banks, one wavefront per instruction
+constexpr int WSLOT = WREC;
 constexpr int ASLOT_BYTES = NPROD_WARPS * ASL * WSLOT * 16;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + ASLOT_BYTES + 1024 + 256;
 constexpr float MAGIC = 12582912.0f;                // 1.5 * 2^23
@@ -270,7 +273,7 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
             if (i < n_stages && lane < WREC) {
                 const int64_t j = a_begin + (int64_t)i * KS + WREC * qh + lane;
                 const bool ok = j < a_end;
-                i8_cp_async16(slot0 + (uint32_t)(((li % ASL) * WSLOT + lane + (lane >> 2)) * 16), S + (ok ? j : 0),
+                i8_cp_async16(slot0 + (uint32_t)(((li % ASL) * WSLOT + (lane ^ ((lane & 8) >> 2))) * 16), S + (ok ? j : 0),
                               ok ? 16u : 0u);
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
@@ -286,12 +289,21 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
             prefetch(li + ASL - 1);       // finished reading slot (li - 1) % ASL, which is refilled now
             uint4 at[4];
             {
-                const uint32_t ra = slot0 + (uint32_t)(((li % ASL) * WSLOT + 5 * qq) * 16);   // quad qq at 80 qq bytes
+                // only the fields this warp uses: X warps Th_a, W warps (Th_b, Th_0, f)
+                const uint32_t ra = slot0 + (uint32_t)((li % ASL) * WSLOT * 16);
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                                 : "=r"(at[u].x), "=r"(at[u].y), "=r"(at[u].z), "=r"(at[u].w)
-                                 : "r"(ra + 16 * u));
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t a = ra + (uint32_t)((((4 * qq + u) ^ (qq & 2))) * 16);   // record 4 qq + u
+                    if (is_x) {
+                        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(at[u].x) : "r"(a));
+                        at[u].y = at[u].z = at[u].w = 0u;
+                    } else {
+                        at[u].x = 0u;
+                        asm volatile("ld.shared.u32 %0, [%1+4];" : "=r"(at[u].y) : "r"(a));
+                        asm volatile("ld.shared.u32 %0, [%1+8];" : "=r"(at[u].z) : "r"(a));
+                        asm volatile("ld.shared.u32 %0, [%1+12];" : "=r"(at[u].w) : "r"(a));
+                    }
+                }
             }
             i8_mbar_wait(&empty[s], (uint32_t)(((i / STAGES) + 1) & 1));
             const uint32_t sbase = su32(smem) + (uint32_t)(s * STAGE_BYTES);
