@@ -22,7 +22,7 @@
 //     HH += Xr_hi.B1_hi + Xs_hi.B2_hi,   X += Xr_hi.B1_lo + Xr_lo.B1_hi + Xs_hi.B2_lo + Xs_lo.B2_hi
 // (B1 = [Wr | Ws], B2 = [-Ws | Wr]: D = [Re | Im'], Im' = -Im; the partials hold conj(p) like the fp16 engine).
 //
-// Producers: 5 groups of 6 warps; group g fills stages i = g mod 5 (5-stage ring, 28 KB per stage; the group count
+// Producers: 5 groups of 6 warps; group g fills stages i = g mod 5 (6-stage ring, 28 KB per stage; the group count
 // must not exceed the stage count, see the empty-barrier parity note in DESIGN.md 6.1).  A warp thread
 // owns 4 consecutive atoms (one 32-bit word per row and limb plane) and 8 rows spaced 8 apart (X or W), and walks
 // the rows with the angle-addition recurrence X_{m+8} = X_m X_8 (packed FP32x2, 2 ops per phasor; 2 SFU sincos per
@@ -43,7 +43,7 @@ constexpr int BROWS = 3 * BN;                       // [-Ws | Wr | Ws]
 constexpr int BPLANE = BROWS * KS;                  // 6 KB
 constexpr int STAGE_BYTES = 4 * APLANE + 2 * BPLANE;   // Xr_hi Xr_lo Xs_hi Xs_lo | B_hi B_lo = 28 KB
 #ifndef XPCS_I8_STAGES
-#define XPCS_I8_STAGES 5
+#define XPCS_I8_STAGES 6
 #endif
 constexpr int STAGES = XPCS_I8_STAGES;
 #ifndef XPCS_I8_GROUPS
