@@ -115,16 +115,18 @@ class Pipeline:
             r0 = r1 = main
         r0.wait_event(ev)
         r1.wait_event(ev)
-        if wl.lags:
+        skip = os.environ.get("XPCS_SKIP_REDUCTIONS", "").split(",")   # experiments: critical-path attribution
+        if wl.lags and "g2" not in skip:
             X.xpcs_g2(I, wl.lags, out=self.g2, out_dtype=X.F32, stream=r0, profile=profile)
             out["g2"] = self.g2
             if after_g2 is not None:
                 after_g2(r0)
             out["g2_rings"] = X.xpcs_shell_mean(self.g2, self.bins, wl.n_bins, stream=r0, profile=profile)
-        if wl.windows:
+        if wl.windows and "xsvs" not in skip:
             out["beta"] = X.xsvs_contrast(I, self.bins, wl.n_bins, wl.windows, stream=r1, profile=profile)
-        out["S_rings"] = X.xpcs_structure_factor_shells(I, form_factors, wl.N, self.bins, wl.n_bins, stream=main,
-                                                        profile=profile)
+        if "rings" not in skip:
+            out["S_rings"] = X.xpcs_structure_factor_shells(I, form_factors, wl.N, self.bins, wl.n_bins, stream=main,
+                                                            profile=profile)
         main.wait_stream(r0)
         main.wait_stream(r1)
 
