@@ -5,6 +5,7 @@
 // All sums are FP64 and in a fixed order (deterministic, no float atomics).
 #include "common.cuh"
 #include <algorithm>
+#include <climits>
 #include <vector>
 
 
@@ -429,7 +430,16 @@ k_xsvs_warp(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __r
 // into a warp-private buffer [slot][lane] (rows padded to 33 double2: conflict-free both ways); every XB closes the
 // warp sums the buffered slots across lanes (one lane per slot, 32 loads in lane order: a fixed order) and writes
 // the warp's moments.
-namespace { constexpr int XB = 16, XWARPS = 4, XFC = 32; }
+#ifndef XPCS_XSVS_XB
+#define XPCS_XSVS_XB 16
+#endif
+#ifndef XPCS_XSVS_FC
+#define XPCS_XSVS_FC 32
+#endif
+#ifndef XPCS_XSVS_WARPS
+#define XPCS_XSVS_WARPS 4
+#endif
+namespace { constexpr int XB = XPCS_XSVS_XB, XWARPS = XPCS_XSVS_WARPS, XFC = XPCS_XSVS_FC; }
 template <typename In>
 __host__ __device__ constexpr size_t xsvs2_smem() {
     return (size_t)XWARPS * ((size_t)XB * 33 * sizeof(double2) + (size_t)XB * sizeof(int) + 2 * XFC * 32 * sizeof(In));
@@ -457,14 +467,18 @@ k_xsvs_warp2(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __
     const bool valid = idx < off[b + 1];
     const int64_t px = valid ? perm[idx] : 0;
     const int nw = ws.n;
-    double run[XW];
-    int cnt[XW], sidx[XW];
+    // running prefix sum P of the series; window k closes at frames t + 1 = W_k, 2 W_k, ... (aligned, non-overlapping)
+    // and its sum is P - (P at its previous close): per frame one DADD and one compare against the next close
+    double P = 0.0, lastP[XW];
+    int nextc[XW], sidx[XW];
+    int nc = INT_MAX;
     int64_t Tuse = 0;
 #pragma unroll
     for (int k = 0; k < XW; ++k) {
-        run[k] = 0.0;
-        cnt[k] = k < nw ? ws.W[k] : 1;
+        lastP[k] = 0.0;
         sidx[k] = 0;
+        nextc[k] = (k < nw && ws.S[k] > 0) ? ws.W[k] : INT_MAX;
+        nc = min(nc, nextc[k]);
         if (k < nw) Tuse = max(Tuse, (int64_t)ws.S[k] * ws.W[k]);
     }
     const int n_chunks = (int)((Tuse + XFC - 1) / XFC);
@@ -507,21 +521,23 @@ k_xsvs_warp2(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __
         const In* sc = ser + (size_t)(c & 1) * XFC * 32 + lane;
         const int un = (int)min((int64_t)XFC, Tuse - (int64_t)c * XFC);
         for (int u = 0; u < un; ++u) {
-            const double v = (double)sc[u * 32];
+            P += (double)sc[u * 32];
+            const int t1 = c * XFC + u + 1;           // frames consumed
+            if (t1 != nc) continue;                   // warp-uniform
+            nc = INT_MAX;
 #pragma unroll
             for (int k = 0; k < XW; ++k) {
                 if (k >= nw) break;
-                run[k] += v;
-                if (--cnt[k] == 0) {
-                    if (sidx[k] < ws.S[k]) {
-                        B[nb][lane] = make_double2(run[k], run[k] * run[k]);
-                        if (lane == 0) ids[nb] = ws.base[k] + sidx[k];
-                        ++sidx[k];
-                        if (++nb == XB) flush();
-                    }
-                    run[k] = 0.0;
-                    cnt[k] = ws.W[k];
+                if (nextc[k] == t1) {
+                    const double val = P - lastP[k];
+                    lastP[k] = P;
+                    B[nb][lane] = make_double2(val, val * val);
+                    if (lane == 0) ids[nb] = ws.base[k] + sidx[k];
+                    ++sidx[k];
+                    nextc[k] = sidx[k] < ws.S[k] ? nextc[k] + ws.W[k] : INT_MAX;
+                    if (++nb == XB) flush();
                 }
+                nc = min(nc, nextc[k]);
             }
         }
         __syncwarp();                             // chunk c's buffer is refilled by prefetch(c + 2)
