@@ -72,6 +72,7 @@ class Pipeline:
         # the reductions of I are independent (g2 -> g2 rings | XSVS | S rings) and each is too small to fill the
         # GPU alone: they run concurrently on two side streams and the caller's stream, joined before returning
         self.s_red = [torch.cuda.Stream(self.device), torch.cuda.Stream(self.device)] if self.device.type == "cuda" else None
+        self.serial_reductions = False      # True: all reductions on the caller's stream (per-kernel timing)
 
     def close(self):
         """Free the registered ring plan (the bins tensor dies with the pipeline; a stale plan must not outlive it)."""
@@ -111,7 +112,7 @@ class Pipeline:
         ev = torch.cuda.Event()
         ev.record(main)
         r0, r1 = self.s_red
-        if os.environ.get("XPCS_SERIAL_REDUCTIONS") == "1":   # experiments: isolated kernel timings
+        if self.serial_reductions or os.environ.get("XPCS_SERIAL_REDUCTIONS") == "1":   # isolated kernel timings
             r0 = r1 = main
         r0.wait_event(ev)
         r1.wait_event(ev)
