@@ -147,3 +147,47 @@ def test_i8_many_frames_batched():
     assert_pixels(I[frames][:, pix], ref, cfg.N, "i8 batched frames")
     one = xp.xpcs_intensity_grid(d[699:700], None, g, engine=I8).cpu().numpy()
     assert_pixels(one[0][pix], ref[2], cfg.N, "i8 single frame")
+
+
+@pytest.mark.parametrize("shape", [(256, 256), (257, 129)])
+@pytest.mark.parametrize("what", ["I32", "I64", "A32"])
+def test_i8_direct_drain_equals_partial_fold(monkeypatch, shape, what):
+    """With one atom chunk the integer engine writes the result from its drain; the partial-plane path (forced with
+    XPCS_I8_DIRECT=0) folds the same fp32 amplitude in FP64 with k_amp_reduce: the two must agree bit for bit
+    (intensity in fp32 and fp64, amplitude), including odd n_k (unaligned pixel pairs) and ragged tiles."""
+    L = 17.0
+    N = 3000
+    pos = _t(xi.uniform_frame(91, N, L, "f32")[None].repeat(3, axis=0))
+    n_h, n_k = shape
+    g = xp.qgrid(L, -n_h // 2, n_h, -n_k // 2, n_k)
+
+    def run():
+        if what == "A32":
+            return xp.xpcs_amplitude_grid(pos, None, g, engine=I8).cpu().numpy()
+        return xp.xpcs_intensity_grid(pos, None, g, engine=I8,
+                                      out_dtype=xp.F64 if what == "I64" else xp.F32).cpu().numpy()
+
+    direct = run()
+    monkeypatch.setenv("XPCS_I8_DIRECT", "0")
+    folded = run()
+    assert np.array_equal(direct, folded)
+
+
+def test_i8_frame_split_plan_parity(monkeypatch):
+    """Enough (tile, frame) units that the last wave of clusters is partial: the call splits the frames into two
+    batches with their own atom chunking.  Both batches against the oracle, and against the unsplit plan
+    (XPCS_I8_TAILSPLIT=0) within the limb-rounding difference of their chunk folds."""
+    cfg = xi.scaled(xi.CONFIGS["c2"], N=6000, T=100)
+    pos = xi.positions(cfg)
+    g = xp.lattice_plane(cfg.L, 256)
+    d = _t(pos)
+    split = xp.xpcs_intensity_grid(d, None, g, engine=I8).cpu().numpy()
+    monkeypatch.setenv("XPCS_I8_TAILSPLIT", "0")
+    plain = xp.xpcs_intensity_grid(d, None, g, engine=I8).cpu().numpy()
+    q = oracle.lattice_q(cfg.L, **oracle.plane_grid(256))
+    pix = xi.pixel_subset(q.shape[0], 128, 5)
+    frames = [0, 40, 99]
+    ref = oracle.intensity(pos[frames], None, q[pix], cfg.L)
+    assert_pixels(split[frames][:, pix], ref, cfg.N, "i8 split plan")
+    assert_pixels(plain[frames][:, pix], ref, cfg.N, "i8 unsplit plan")
+    assert np.max(np.abs(split - plain)) / cfg.N < 1e-5
