@@ -204,6 +204,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-slots", type=int, default=2, help="pipelines in flight for the end-to-end figure")
+    ap.add_argument("--e2e-batches", type=int, default=8, help="frame batches per step in the end-to-end figure")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of replaying its CUDA graph")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -368,7 +369,7 @@ def main():
     # ---- end to end through the public API from pinned host memory
     e2e = None
     if not args.no_e2e:
-        P.alloc_host_io(pos_h, f_h)
+        P.alloc_host_io(pos_h, f_h, batches=args.e2e_batches)
         P.run_host()
         torch.cuda.synchronize()
         slots = 1 if args.no_graph else max(1, args.e2e_slots)
@@ -392,7 +393,7 @@ def main():
             # step still copies its inputs in and its results out.  Time = whole run / steps (CUDA events).
             pipes = [P] + [pipeline.Pipeline(wl, device=dev) for _ in range(slots - 1)]
             for Q in pipes[1:]:
-                Q.alloc_host_io(pos_h, f_h)
+                Q.alloc_host_io(pos_h, f_h, batches=args.e2e_batches)
                 Q.run_host()
             graphs = [Q.capture_host()[0] for Q in pipes]
             streams = [torch.cuda.Stream() for _ in pipes]

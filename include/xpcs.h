@@ -266,6 +266,51 @@ XPCS_API int xpcs_structure_factor_shells(const void* I, int64_t rows, int64_t n
                                  const int32_t* bin_of_q, int32_t n_bins, double* out, const xpcs_opts* opts);
 
 /* ------------------------------------------------------------------------------------------------
+ * One pass of the whole hot path from HOST memory (the end-to-end entry point):
+ * I(q,t) on a lattice plane (Eq. 7-8, Algorithm 1) for every frame, g2 (Eq. 14), the ring
+ * averages S(q,t) (Eq. 12-13) and of g2, and the XSVS contrast (Eq. 15+17).
+ * The frames are split into `batches`: batch b's positions are copied host -> device on an internal copy stream,
+ * its intensities are computed on opts->stream and copied back on a second internal copy stream while batch b+1
+ * is computed; the reductions follow on opts->stream and their results are copied back.  The internal streams fork
+ * from and join into opts->stream, so all outputs are valid in host memory once opts->stream is synchronised.
+ * Host buffers should be page-locked (cudaHostAlloc / cudaHostRegister) for the copies to overlap the kernels;
+ * pageable memory is correct but serialises the copies (and cannot be captured in a CUDA graph).  Device buffers
+ * are library-owned, cached per (device, opts->stream) and freed by xpcs_release.  After one call outside a
+ * capture, the call can be captured in a CUDA graph on the same stream (pinned host buffers).
+ *   positions    HOST [frames][N][3] in_dtype
+ *   form_factors HOST [N] in_dtype or NULL (f = 1); with species: used only for the S(q) normalisation sum f^2
+ *   species      NULL or atom kinds as for xpcs_intensity_volume (species->species HOST, f_q DEVICE
+ *                [n_species][n_q]); then form_factors may still be given for the normalisation
+ *   bin_of_q     DEVICE [n_q] ring index (-1 excluded), n_bins rings (register it with xpcs_rings_register to
+ *                avoid rebuilding the ring plan in every call)
+ *   lags HOST [n_lags] (n_lags may be 0);  windows HOST [n_windows] (n_windows may be 0)
+ *   I_out HOST [frames][n_q] out_dtype, g2_out HOST [n_lags][n_q] out_dtype, S_rings HOST [frames][n_bins],
+ *   g2_rings HOST [n_lags][n_bins], beta HOST [n_windows][n_bins] (double); any output may be NULL (not copied;
+ *   g2_rings needs g2 to be computed, which happens whenever n_lags > 0).
+ * Errors: EINVAL for a null step/positions/bin_of_q, N/frames/n_bins/batches <= 0, a lag or window out of range;
+ *         the errors of the underlying calls (xpcs_intensity_volume, xpcs_g2, xsvs_contrast, ...). */
+typedef struct {
+    const void* positions;
+    const void* form_factors;
+    const xpcs_species* species;
+    int64_t N, frames;
+    xpcs_qgrid grid;
+    const int32_t* bin_of_q;
+    int32_t n_bins;
+    int32_t batches;
+    const int32_t* lags;
+    int64_t n_lags;
+    const int32_t* windows;
+    int64_t n_windows;
+    void* I_out;
+    void* g2_out;
+    double* S_rings;
+    double* g2_rings;
+    double* beta;
+} xpcs_step;
+XPCS_API int xpcs_step_host(const xpcs_step* step, const xpcs_opts* opts);
+
+/* ------------------------------------------------------------------------------------------------
  * q geometry helpers.
  * xpcs_qgrid_lattice_plane (HOST only, no device work): the configs' plane h, k in [-n/2, n/2 - 1] at height l,
  *   q = (2 pi / L)(h, k, l).  Errors: EINVAL for L <= 0, n <= 0, null out.

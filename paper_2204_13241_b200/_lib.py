@@ -28,7 +28,7 @@ EXPORTED = (
     "xpcs_amplitude", "xpcs_amplitude_grid", "xpcs_isf",
     "xpcs_intensity_volume", "xpcs_amplitude_volume", "xpcs_intensity_species", "xpcs_amplitude_species",
     "xpcs_form_factor_gaussian", "xpcs_speckle_histogram", "xpcs_intensity_fft", "xpcs_rings_register",
-    "xpcs_rings_unregister",
+    "xpcs_rings_unregister", "xpcs_step_host",
 )
 
 
@@ -60,6 +60,16 @@ class QVolume(ctypes.Structure):
     @property
     def n_q(self):
         return int(self.plane.n_h * self.plane.n_k * self.n_l)
+
+
+class Step(ctypes.Structure):
+    """xpcs_step (include/xpcs.h): one host-buffer pass of the whole hot path."""
+    _fields_ = [("positions", ctypes.c_void_p), ("form_factors", ctypes.c_void_p), ("species", ctypes.c_void_p),
+                ("N", ctypes.c_int64), ("frames", ctypes.c_int64), ("grid", QGrid), ("bin_of_q", ctypes.c_void_p),
+                ("n_bins", ctypes.c_int32), ("batches", ctypes.c_int32), ("lags", ctypes.POINTER(ctypes.c_int32)),
+                ("n_lags", ctypes.c_int64), ("windows", ctypes.POINTER(ctypes.c_int32)), ("n_windows", ctypes.c_int64),
+                ("I_out", ctypes.c_void_p), ("g2_out", ctypes.c_void_p), ("S_rings", ctypes.c_void_p),
+                ("g2_rings", ctypes.c_void_p), ("beta", ctypes.c_void_p)]
 
 
 class Species(ctypes.Structure):
@@ -115,6 +125,7 @@ def load():
         "xpcs_speckle_histogram": [vp, i64, i64, vp, i32, i32, i32, dbl, vp, op],
         "xpcs_form_factor_gaussian": [vp, i64, ctypes.POINTER(QVolume), i32, ctypes.POINTER(ctypes.c_double),
                                       ctypes.POINTER(ctypes.c_double), dbl, vp, op],
+        "xpcs_step_host": [ctypes.POINTER(Step), op],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -187,6 +198,48 @@ def qvolume(L, h0, n_h, k0, n_k, l0, n_l, m0=(0, 0, 0), ma=(1, 0, 0), mb=(0, 1, 
     v.mc[:] = list(mc)
     v.l0, v.n_l = int(l0), int(n_l)
     return v
+
+
+def _host_ptr(t):
+    if t is None:
+        return None
+    if t.is_cuda:
+        raise ValueError("xpcs: this argument is a HOST buffer")
+    if not t.is_contiguous():
+        raise ValueError("xpcs: tensors must be contiguous")
+    return t.data_ptr()
+
+
+def xpcs_step_host(positions, form_factors, grid: QGrid, bins, n_bins, lags=(), windows=(), I_out=None, g2_out=None,
+                   S_rings=None, g2_rings=None, beta=None, species=None, batches=8, engine=ENGINE_AUTO, stream=None,
+                   profile=False, out_dtype=None):
+    """xpcs_step_host: the whole hot path from HOST buffers (positions [T][N][3], optional form factors [N]; pinned
+    for overlap) into HOST outputs (any may be None).  `bins` is the DEVICE ring index [n_q]; `species` an optional
+    (host species [N], device f_q [S][n_q], f_max) triple.  Enqueued on `stream`; outputs valid after it syncs."""
+    import torch
+    T, N = positions.shape[0], positions.shape[1]
+    ind = F64 if positions.dtype == torch.float64 else F32
+    outd = ind if out_dtype is None else out_dtype
+    st = Step()
+    st.positions = _host_ptr(positions)
+    st.form_factors = _host_ptr(form_factors)
+    keep = []
+    if species is not None:
+        sp, keep = species_desc(*species)
+        keep = (sp, keep)
+        st.species = ctypes.addressof(sp)
+    st.N, st.frames, st.grid = N, T, grid
+    st.bin_of_q = _ptr(bins).value
+    st.n_bins, st.batches = int(n_bins), int(batches)
+    l_arr, l_p = _i32_array(lags) if len(lags) else (None, None)
+    w_arr, w_p = _i32_array(windows) if len(windows) else (None, None)
+    st.lags, st.n_lags = l_p, len(lags)
+    st.windows, st.n_windows = w_p, len(windows)
+    st.I_out, st.g2_out = _host_ptr(I_out), _host_ptr(g2_out)
+    st.S_rings, st.g2_rings, st.beta = _host_ptr(S_rings), _host_ptr(g2_rings), _host_ptr(beta)
+    o = make_opts(ind, outd, stream, engine, profile)
+    _check(load().xpcs_step_host(ctypes.byref(st), ctypes.byref(o)))
+    return keep, l_arr, w_arr
 
 
 def species_desc(species, f_q, f_max=None):

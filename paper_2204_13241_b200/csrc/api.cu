@@ -19,6 +19,8 @@ int profile_query(int cls, const char** name, double* ms, long long* n);
 
 using namespace xpcs;
 
+void release_host_resources();   // xpcs_step_host's copy streams and events (defined below)
+
 namespace {
 
 constexpr size_t kBatchBytes = size_t(1) << 30;   // cap for staged atoms / partial amplitudes per frame batch
@@ -180,6 +182,7 @@ int64_t xpcs_launch_count(void) { return (int64_t)launches(); }
 int xpcs_release(void) {
     clear_error();
     fft_release_plan();
+    release_host_resources();
     if (!registered().empty()) {
         cudaDeviceSynchronize();
         for (auto& r : registered()) cudaFree(r.mem);
@@ -1089,6 +1092,196 @@ int xpcs_structure_factor_shells(const void* I, int64_t rows, int64_t n_q, const
         scale = 1.0 / (double)N;     // sum_j f_j^2 = N for unit form factors
     }
     return cuda_fail(launch_shell_mean(I, o.in_f64, rows, n_q, pb.plan, n_bins, scale, norm, out, o.s), "rings");
+}
+
+// ------------------------------------------------------------------------------------------- host-buffer step
+}  // extern "C"
+namespace {
+// internal copy streams and events of xpcs_step_host, per (device, caller stream); created on first use (outside any
+// graph capture) and kept until xpcs_release
+struct HostRes {
+    cudaStream_t h2d = nullptr, d2h = nullptr, red = nullptr;   // copies in, copies out, a side stream for reductions
+    std::vector<cudaEvent_t> ev;
+};
+std::mutex g_host_mu;
+std::vector<std::pair<std::pair<int, cudaStream_t>, HostRes>> g_host_res;
+
+int host_resources(cudaStream_t s, size_t n_events, HostRes*& out) {
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    HostRes* r = nullptr;
+    for (auto& kv : g_host_res)
+        if (kv.first.first == dev && kv.first.second == s) r = &kv.second;
+    if (!r || r->ev.size() < n_events) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+            set_error("xpcs: xpcs_step_host must run once on this stream outside a graph capture first");
+            return XPCS_EUNSUPPORTED;
+        }
+        if (!r) {
+            g_host_res.push_back({{dev, s}, HostRes{}});
+            r = &g_host_res.back().second;
+            if (cudaStreamCreateWithFlags(&r->h2d, cudaStreamNonBlocking) != cudaSuccess ||
+                cudaStreamCreateWithFlags(&r->d2h, cudaStreamNonBlocking) != cudaSuccess ||
+                cudaStreamCreateWithFlags(&r->red, cudaStreamNonBlocking) != cudaSuccess) {
+                cudaGetLastError();
+                set_error("xpcs: cannot create the copy streams");
+                return XPCS_ECUDA;
+            }
+        }
+        while (r->ev.size() < n_events) {
+            cudaEvent_t e;
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+                cudaGetLastError();
+                set_error("xpcs: cannot create events");
+                return XPCS_ECUDA;
+            }
+            r->ev.push_back(e);
+        }
+    }
+    out = r;
+    return XPCS_OK;
+}
+}  // namespace
+
+void release_host_resources() {
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    for (auto& kv : g_host_res) {
+        for (cudaEvent_t e : kv.second.ev) cudaEventDestroy(e);
+        if (kv.second.h2d) cudaStreamDestroy(kv.second.h2d);
+        if (kv.second.d2h) cudaStreamDestroy(kv.second.d2h);
+        if (kv.second.red) cudaStreamDestroy(kv.second.red);
+    }
+    g_host_res.clear();
+}
+
+extern "C" {
+
+int xpcs_step_host(const xpcs_step* st, const xpcs_opts* opts) {
+    clear_error();
+    NEED(st, "step");
+    Opts o;
+    TRY(parse_opts(opts, o));
+    NEED(st->positions, "positions");
+    NEED(st->bin_of_q, "bin_of_q");
+    POS(st->N, "N");
+    POS(st->frames, "frames");
+    POS(st->n_bins, "n_bins");
+    POS(st->batches, "batches");
+    TRY(validate_grid(&st->grid));
+    if (st->n_lags < 0 || st->n_windows < 0 || (st->n_lags > 0 && !st->lags) || (st->n_windows > 0 && !st->windows)) {
+        set_error("xpcs: lags/windows: negative count or NULL array");
+        return XPCS_EINVAL;
+    }
+    for (int64_t i = 0; i < st->n_lags; ++i)
+        if (st->lags[i] < 0 || st->lags[i] >= st->frames) {
+            set_error("xpcs: lag %d out of range [0, %lld)", st->lags[i], (long long)st->frames);
+            return XPCS_EINVAL;
+        }
+    for (int64_t i = 0; i < st->n_windows; ++i)
+        if (st->windows[i] < 1 || st->windows[i] > st->frames) {
+            set_error("xpcs: window %d out of range [1, %lld]", st->windows[i], (long long)st->frames);
+            return XPCS_EINVAL;
+        }
+    TRY(check_sticky());
+    const int64_t N = st->N, T = st->frames, n_q = st->grid.n_h * st->grid.n_k, nb = st->n_bins;
+    const int64_t n_bat = std::min<int64_t>(st->batches, T);
+    const size_t pin = o.in_f64 ? 8 : 4, pout = o.out_f64 ? 8 : 4;
+    const size_t pos_bytes = pin * 3 * (size_t)N * (size_t)T, i_bytes = pout * (size_t)n_q * (size_t)T;
+    const size_t g2_bytes = pout * (size_t)n_q * (size_t)st->n_lags;
+    const size_t red_doubles = (size_t)(T + st->n_lags + st->n_windows) * (size_t)nb;
+    char* d_pos = (char*)scratch(o.s, SS_H_POS, pos_bytes);
+    char* d_ff = st->form_factors ? (char*)scratch(o.s, SS_H_FF, pin * (size_t)N) : nullptr;
+    char* d_I = (char*)scratch(o.s, SS_H_I, i_bytes);
+    char* d_g2 = st->n_lags ? (char*)scratch(o.s, SS_H_G2, g2_bytes) : nullptr;
+    double* d_red = (double*)scratch(o.s, SS_H_RED, sizeof(double) * red_doubles);
+    if (!d_pos || !d_I || !d_red || (st->form_factors && !d_ff) || (st->n_lags && !d_g2)) return XPCS_ENOMEM;
+    double* d_sr = d_red;
+    double* d_g2r = d_red + (size_t)T * nb;
+    double* d_beta = d_g2r + (size_t)st->n_lags * nb;
+    HostRes* hr = nullptr;
+    TRY(host_resources(o.s, (size_t)(2 * n_bat + 6), hr));
+    cudaEvent_t* ev = hr->ev.data();         // [0] fork, [1..n_bat] inputs in, [n_bat+1..2 n_bat] I out, then g2, joins, f
+    const cudaEvent_t ev_fork = ev[0], ev_g2 = ev[2 * n_bat + 1], ev_d2h = ev[2 * n_bat + 2], ev_h2d = ev[2 * n_bat + 3],
+                      ev_f = ev[2 * n_bat + 4], ev_red = ev[2 * n_bat + 5];
+    TRY(cuda_fail(cudaEventRecord(ev_fork, o.s), "fork"));
+    TRY(cuda_fail(cudaStreamWaitEvent(hr->h2d, ev_fork, 0), "fork"));
+    TRY(cuda_fail(cudaStreamWaitEvent(hr->d2h, ev_fork, 0), "fork"));
+    if (st->form_factors) {
+        TRY(cuda_fail(cudaMemcpyAsync(d_ff, st->form_factors, pin * (size_t)N, cudaMemcpyHostToDevice, hr->h2d), "H2D f"));
+        TRY(cuda_fail(cudaEventRecord(ev_f, hr->h2d), "event"));
+    }
+    const size_t frame_pos = pin * 3 * (size_t)N, frame_i = pout * (size_t)n_q;
+    for (int64_t b = 0; b < n_bat; ++b) {
+        const int64_t t0 = b * T / n_bat, t1 = (b + 1) * T / n_bat;
+        TRY(cuda_fail(cudaMemcpyAsync(d_pos + t0 * frame_pos, (const char*)st->positions + t0 * frame_pos,
+                                      (size_t)(t1 - t0) * frame_pos, cudaMemcpyHostToDevice, hr->h2d), "H2D positions"));
+        TRY(cuda_fail(cudaEventRecord(ev[1 + b], hr->h2d), "event"));
+    }
+    TRY(cuda_fail(cudaEventRecord(ev_h2d, hr->h2d), "event"));
+    xpcs_opts io{};
+    io.in_dtype = o.in_f64 ? XPCS_F64 : XPCS_F32;
+    io.out_dtype = o.out_f64 ? XPCS_F64 : XPCS_F32;
+    io.stream = (void*)o.s;
+    io.engine = o.engine;
+    io.profile = o.profile ? 1 : 0;
+    xpcs_qvolume vol;
+    std::memset(&vol, 0, sizeof(vol));
+    vol.plane = st->grid;
+    vol.n_l = 1;
+    for (int64_t b = 0; b < n_bat; ++b) {
+        const int64_t t0 = b * T / n_bat, t1 = (b + 1) * T / n_bat;
+        TRY(cuda_fail(cudaStreamWaitEvent(o.s, ev[1 + b], 0), "wait inputs"));
+        if (b == 0 && st->form_factors) TRY(cuda_fail(cudaStreamWaitEvent(o.s, ev_f, 0), "wait f"));
+        TRY(run_volume(d_pos + t0 * frame_pos, N, st->species ? nullptr : d_ff, st->species, &vol, t1 - t0,
+                       d_I + t0 * frame_i, &io, 0));
+        TRY(cuda_fail(cudaEventRecord(ev[1 + n_bat + b], o.s), "event"));
+        if (st->I_out) {
+            TRY(cuda_fail(cudaStreamWaitEvent(hr->d2h, ev[1 + n_bat + b], 0), "wait I"));
+            TRY(cuda_fail(cudaMemcpyAsync((char*)st->I_out + t0 * frame_i, d_I + t0 * frame_i, (size_t)(t1 - t0) * frame_i,
+                                          cudaMemcpyDeviceToHost, hr->d2h), "D2H I"));
+        }
+    }
+    // reductions: g2 (+ its ring means) on the caller's stream, its (largest) result streaming back while the S rings
+    // and XSVS run concurrently on the side stream
+    xpcs_opts ro = io;
+    ro.in_dtype = io.out_dtype;                  // the series fed to the reductions is I (out_dtype)
+    xpcs_opts so = ro;
+    so.stream = (void*)hr->red;
+    TRY(cuda_fail(cudaStreamWaitEvent(hr->red, ev[2 * n_bat], 0), "fork reductions"));   // the last batch's I
+    if (st->S_rings) TRY(xpcs_structure_factor_shells(d_I, T, n_q, st->form_factors ? (const void*)d_ff : nullptr, N,
+                                                      st->bin_of_q, st->n_bins, d_sr, &so));
+    if (st->n_windows && st->beta)
+        TRY(xsvs_contrast(d_I, T, n_q, st->bin_of_q, st->n_bins, st->windows, st->n_windows, d_beta, &so));
+    TRY(cuda_fail(cudaEventRecord(ev_red, hr->red), "event"));
+    if (st->n_lags) {
+        TRY(xpcs_g2(d_I, T, n_q, st->lags, st->n_lags, d_g2, &ro));
+        TRY(cuda_fail(cudaEventRecord(ev_g2, o.s), "event"));
+        if (st->g2_out) {
+            TRY(cuda_fail(cudaStreamWaitEvent(hr->d2h, ev_g2, 0), "wait g2"));
+            TRY(cuda_fail(cudaMemcpyAsync(st->g2_out, d_g2, g2_bytes, cudaMemcpyDeviceToHost, hr->d2h), "D2H g2"));
+        }
+        if (st->g2_rings) {
+            xpcs_opts go = ro;
+            go.in_dtype = io.out_dtype;
+            TRY(xpcs_shell_mean(d_g2, st->n_lags, n_q, st->bin_of_q, st->n_bins, 1.0, d_g2r, &go));
+        }
+    }
+    TRY(cuda_fail(cudaStreamWaitEvent(o.s, ev_red, 0), "join reductions"));
+    // small results back on the caller's stream (after the reductions), then join the copy streams
+    if (st->S_rings)
+        TRY(cuda_fail(cudaMemcpyAsync(st->S_rings, d_sr, sizeof(double) * (size_t)T * nb, cudaMemcpyDeviceToHost, o.s), "D2H S"));
+    if (st->n_lags && st->g2_rings)
+        TRY(cuda_fail(cudaMemcpyAsync(st->g2_rings, d_g2r, sizeof(double) * (size_t)st->n_lags * nb,
+                                      cudaMemcpyDeviceToHost, o.s), "D2H g2 rings"));
+    if (st->n_windows && st->beta)
+        TRY(cuda_fail(cudaMemcpyAsync(st->beta, d_beta, sizeof(double) * (size_t)st->n_windows * nb,
+                                      cudaMemcpyDeviceToHost, o.s), "D2H beta"));
+    TRY(cuda_fail(cudaEventRecord(ev_d2h, hr->d2h), "event"));
+    TRY(cuda_fail(cudaStreamWaitEvent(o.s, ev_d2h, 0), "join"));
+    TRY(cuda_fail(cudaStreamWaitEvent(o.s, ev_h2d, 0), "join"));
+    return XPCS_OK;
 }
 
 // ------------------------------------------------------------------------------------------- geometry

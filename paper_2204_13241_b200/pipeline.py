@@ -174,6 +174,7 @@ class Pipeline:
         self.h_out = {}
         T = self.wl.T
         nb = max(1, min(int(batches), T))
+        self.n_batches = nb
         edges = [round(i * T / nb) for i in range(nb + 1)]
         self.batches = [(edges[i], edges[i + 1]) for i in range(nb) if edges[i + 1] > edges[i]]
         self.s_h2d = torch.cuda.Stream(self.device)
@@ -183,6 +184,33 @@ class Pipeline:
         self.s_comp = [torch.cuda.Stream(self.device), torch.cuda.Stream(self.device)]
 
     def run_host(self) -> dict:
+        """End to end from pinned host memory.  Lattice planes: one `xpcs_step_host` call (the C ABI's host-buffer
+        entry: frame-batched H2D / intensity / D2H overlap on internal copy streams, then g2, rings and XSVS and
+        their D2H), all enqueued on the current stream.  Explicit q lists use the stream orchestration below."""
+        wl = self.wl
+        if self.grid is None:
+            return self._run_host_streams()
+        main = torch.cuda.current_stream(self.device)
+        h = self.h_out
+        T, nl, nw, nb = wl.T, len(wl.lags), len(wl.windows), wl.n_bins
+        if "I" not in h:
+            pin = dict(pin_memory=True)
+            h["I"] = torch.empty(self.I.shape, dtype=self.I.dtype, **pin)
+            h["S_rings"] = torch.empty((T, nb), dtype=torch.float64, **pin)
+            if nl:
+                h["g2"] = torch.empty((nl, self.n_q), dtype=torch.float32, **pin)
+                h["g2_rings"] = torch.empty((nl, nb), dtype=torch.float64, **pin)
+            if nw:
+                h["beta"] = torch.empty((nw, nb), dtype=torch.float64, **pin)
+        sp = (wl.kinds, self.kind_fq, wl.kind_f) if self.kind_fq is not None else None
+        self._keep = X.xpcs_step_host(self.h_pos, self.h_f, self.grid, self.bins, nb, lags=wl.lags, windows=wl.windows,
+                                      I_out=h["I"], g2_out=h.get("g2"), S_rings=h["S_rings"],
+                                      g2_rings=h.get("g2_rings"), beta=h.get("beta"), species=sp,
+                                      batches=self.n_batches, engine=wl.engine, stream=main,
+                                      out_dtype=X.F64 if self.I.dtype == torch.float64 else X.F32)
+        return h
+
+    def _run_host_streams(self) -> dict:
         """End to end: pinned H2D of the step's positions, I(q,t), g2, rings and XSVS, D2H of every result.
         Frames are split into batches: H2D on one stream, the intensity kernels alternate between two compute streams
         (consecutive batches overlap on the GPU), D2H of each batch's I on a copy stream; the reductions follow on the

@@ -168,3 +168,31 @@ def test_species_engine_rule():
     assert se([400, 400, 200], [1.0, 1.0, 1.0]) == [400, 400, 200]
     assert se([10, 10], None) == [10, 10]                      # no hints: every kind
     assert se([0, 100], [0.5, 1.0])[1] == 100                  # an empty kind does not set the reference weight
+
+
+def test_step_host_validation_before_launch(lib):
+    """xpcs_step_host (the host-buffer end-to-end entry) rejects bad arguments before any copy or launch."""
+    n0 = lib.xpcs_launch_count()
+    o = _lib.Opts(0, 0, None, 0, 0)
+    assert lib.xpcs_step_host(None, ctypes.byref(o)) == _lib.XPCS_EINVAL
+    st = _lib.Step()
+    st.positions = 16
+    st.bin_of_q = 32
+    st.N, st.frames, st.n_bins, st.batches = 100, 10, 4, 2
+    st.grid = xp.lattice_plane(10.0, 8)
+    lags, lp = _lib._i32_array([1, 10])
+    st.lags, st.n_lags = lp, 2
+    assert lib.xpcs_step_host(ctypes.byref(st), ctypes.byref(o)) == _lib.XPCS_EINVAL
+    assert b"lag 10" in lib.xpcs_last_error()
+    st.n_lags = 1
+    w, wp = _lib._i32_array([0])
+    st.windows, st.n_windows = wp, 1
+    assert lib.xpcs_step_host(ctypes.byref(st), ctypes.byref(o)) == _lib.XPCS_EINVAL
+    assert b"window 0" in lib.xpcs_last_error()
+    st.n_windows = 0
+    st.batches = 0
+    assert lib.xpcs_step_host(ctypes.byref(st), ctypes.byref(o)) == _lib.XPCS_EINVAL
+    st.batches = 2
+    st.positions = None
+    assert lib.xpcs_step_host(ctypes.byref(st), ctypes.byref(o)) == _lib.XPCS_EINVAL
+    assert lib.xpcs_launch_count() == n0
