@@ -204,7 +204,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-slots", type=int, default=2, help="pipelines in flight for the end-to-end figure")
-    ap.add_argument("--e2e-batches", type=int, default=8, help="frame batches per step in the end-to-end figure")
+    ap.add_argument("--e2e-batches", type=int, default=4, help="frame batches per step in the end-to-end figure")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of replaying its CUDA graph")
     args = ap.parse_args()
     if args.impl == "reference":
