@@ -52,7 +52,11 @@ constexpr int MMA_N = 2 * TN;                     // N = 256: [Re | Im'] of 64 k
 #define XPCS_TC_GROUPS 3
 #endif
 #if XPCS_TC_GROUPED
-constexpr int NGROUPS = XPCS_TC_GROUPS, GROUP_WARPS = 3;   // per group: 2 X warps (row halves), 1 W warp
+#ifndef XPCS_TC_RPT
+#define XPCS_TC_RPT 8              // rows per producer thread (8 or 4): 4 doubles the warps of a group
+#endif
+constexpr int RPT = XPCS_TC_RPT, XWARPS = 2 * (8 / RPT), WWARPS = 8 / RPT;
+constexpr int NGROUPS = XPCS_TC_GROUPS, GROUP_WARPS = XWARPS + WWARPS;   // per group: X warps (row slices), W warps
 constexpr int NPROD_WARPS = NGROUPS * GROUP_WARPS, NDRAIN_WARPS = 4;
 constexpr int WREC = 16, WSLOT = WREC + WREC / 4;          // per-warp records of a stage (16 atoms, padded)
 #else
@@ -360,7 +364,7 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
         // numbers (3 packed ops per phasor) and packed with cvt.f16x2.  Lanes (quad qq, row mr): conflict-free.
         const int grp = warp / GROUP_WARPS, wi = warp % GROUP_WARPS;
         const int qq = lane & 3, mr = lane >> 2;
-        const bool is_x = wi < 2;
+        const bool is_x = wi < XWARPS;
         const uint32_t slot0 = smem_u32(aslot) + (uint32_t)(warp * ASLOTS * WSLOT * 16);
         const uint32_t full0 = mapa(smem_u32(full), 0);
         auto prefetch = [&](int li) {
@@ -398,8 +402,8 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
             const uint32_t qoff = (uint32_t)((qq >> 1) * 128 + mr * 16 + (qq & 1) * 8);
             if (!(dbg_flags & 2)) {
                 if (is_x) {
-                    const int xw = wi;                                   // rows m = mr + 8 r + 64 xw, r < 8
-                    const uint32_t h = (uint32_t)(g.h0 + th0 + mr + 64 * xw);
+                    const int xw = wi;                                   // rows m = mr + 8 r + 8 RPT xw, r < RPT
+                    const uint32_t h = (uint32_t)(g.h0 + th0 + mr + 8 * RPT * xw);
                     unsigned long long v[4], st[4];
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
@@ -409,9 +413,9 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
                         v[u] = pack2(c0, s0);
                         st[u] = pack2(c1, s1);
                     }
-                    const uint32_t a0 = sbase + qoff + (uint32_t)(xw * 8 * 256);
+                    const uint32_t a0 = sbase + qoff + (uint32_t)(xw * RPT * 256);
 #pragma unroll
-                    for (int r = 0; r < 8; ++r) {
+                    for (int r = 0; r < RPT; ++r) {
                         unsigned long long hi[4], lo[4];
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
@@ -430,7 +434,8 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
                 } else {
                     // W rows k = mr + 8 r of this CTA's 64: W_k = f e^{-2 pi i (Th_0 + kk Th_b)}; B rows: -Ws at k,
                     // Wr at BN + k, Ws at 2 BN + k.  hi on the 2^(e-10) grid of the quad's max |f| (split_magic)
-                    const uint32_t kk = (uint32_t)(g.k0 + bk0 + mr);
+                    const int ww = wi - XWARPS;                          // rows k = mr + 8 r + 8 RPT ww, r < RPT
+                    const uint32_t kk = (uint32_t)(g.k0 + bk0 + mr + 8 * RPT * ww);
                     unsigned long long v[4], st[4], f2[4];
                     float fm = 0.f;
 #pragma unroll
@@ -446,9 +451,9 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
                     }
                     const float MW = split_magic(fm);
                     const unsigned long long MW2 = pack2(MW, MW);
-                    const uint32_t a0 = sbase + 4 * APLANE + qoff;
+                    const uint32_t a0 = sbase + 4 * APLANE + qoff + (uint32_t)(ww * RPT * 256);
 #pragma unroll
-                    for (int r = 0; r < 8; ++r) {
+                    for (int r = 0; r < RPT; ++r) {
                         unsigned long long hi[4], lo[4];
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
