@@ -577,8 +577,22 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
         const int64_t per_frame = std::max<int64_t>(32 * N, G.n_species ? 16 * n_q * ng : 0);
         const int64_t Tb = std::max<int64_t>(1, std::min<int64_t>(V, (int64_t)(kBatchBytes / per_frame)));
         ulonglong4* st = (ulonglong4*)scratch(o.s, SS_STAGE, sizeof(ulonglong4) * (size_t)(N * Tb));
-        double2* part = G.n_species ? (double2*)scratch(o.s, SS_PARTIAL, sizeof(double2) * (size_t)(n_q * Tb * ng)) : nullptr;
-        if (!st || (G.n_species && !part)) return XPCS_ENOMEM;
+        // split-K over atoms when (pixel blocks x frames) cannot fill ~4 CTAs of 128 threads per SM (config 1: 32
+        // blocks); the chunk amplitudes are folded in FP64 in chunk order (k_amp_reduce)
+        int64_t C64 = 1, ch64 = N;
+        if (!G.n_species) {
+            const int64_t blocks = ((n_q + 127) / 128) * std::min(Tb, V);
+            const int64_t want = 4LL * sm_count();
+            if (blocks < want) {
+                C64 = std::min<int64_t>((want + blocks - 1) / blocks, std::max<int64_t>(1, N / 32));
+                ch64 = (N + C64 - 1) / C64;
+                C64 = (N + ch64 - 1) / ch64;
+            }
+        }
+        double2* part = (G.n_species || C64 > 1)
+                            ? (double2*)scratch(o.s, SS_PARTIAL, sizeof(double2) * (size_t)(n_q * Tb * std::max<int64_t>(ng, C64)))
+                            : nullptr;
+        if (!st || ((G.n_species || C64 > 1) && !part)) return XPCS_ENOMEM;
         for (int64_t v0 = 0; v0 < V; v0 += Tb) {
             const int64_t vb = std::min(Tb, V - v0);
             void* dst = (char*)I_out + isz * n_q * v0;
@@ -594,12 +608,17 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
                   TRY(cuda_fail(launch_stage_lattice64(positions, form_factors, Ng, vb, g, m, st + stoff, o.s), "stage")); }
                 { ProfScope p(o.profile, KC_MAIN, o.s);
                   if (G.n_species) TRY(cuda_fail(launch_lattice_f64(st + stoff, Ng, vb, g, pg, 1, 1, o.s), "lattice64"));
+                  else if (C64 > 1) TRY(cuda_fail(launch_lattice_f64(st + stoff, Ng, vb, g, nullptr, o.out_f64, amp, o.s,
+                                                                     part, ch64, C64), "lattice64"));
                   else TRY(cuda_fail(launch_lattice_f64(st + stoff, Ng, vb, g, dst, o.out_f64, amp, o.s), "lattice64")); }
                 stoff += Ng * vb;
             }
             if (G.n_species) {
                 ProfScope p(o.profile, KC_REDUCE, o.s);
                 TRY(cuda_fail(launch_species_combine(sp, vb, n_q, G.fq, 1, v0, n_l, dst, o.out_f64, amp, o.s), "species combine"));
+            } else if (C64 > 1) {
+                ProfScope p(o.profile, KC_REDUCE, o.s);
+                TRY(cuda_fail(launch_amp_reduce_d(part, C64, vb, n_q, dst, o.out_f64, amp, o.s), "reduce"));
             }
         }
         return XPCS_OK;

@@ -175,7 +175,8 @@ cudaError_t launch_lattice_i8(const uint4* staged, int64_t N, int64_t frames, co
                               void* direct_out = nullptr, int out_f64 = 0, int mode = 0);
 // lattice FP64 (direct per-pixel evaluation with 64-bit turns): writes I directly (double)
 cudaError_t launch_lattice_f64(const ulonglong4* staged, int64_t N, int64_t frames, const LatticeGeom& g,
-                               void* I_out, int out_f64, int mode, cudaStream_t s);
+                               void* I_out, int out_f64, int mode, cudaStream_t s,
+                               double2* partial = nullptr, int64_t chunk_atoms = 0, int64_t n_chunks = 1);
 // generic q list: partial [C][Tb][n_q] double2
 cudaError_t launch_generic32(const uint4* staged, int64_t N, int64_t frames, const void* q, int q_f64,
                              int64_t n_q, double L, int64_t chunk_atoms, int64_t n_chunks, double2* partial,

@@ -138,7 +138,10 @@ k_generic64(const ulonglong4* __restrict__ staged, int64_t N, const double* __re
 // ---- FP64 lattice: one pixel per thread, 64-bit turns (exact h*Th_a + k*Th_b + Th_0 mod 2^64)
 template <typename O>
 __global__ void __launch_bounds__(128)
-k_lattice64(const ulonglong4* __restrict__ staged, int64_t N, LatticeGeom g, O* __restrict__ I_out, int mode) {
+k_lattice64(const ulonglong4* __restrict__ staged, int64_t N, LatticeGeom g, O* __restrict__ I_out, int mode,
+            int64_t chunk_atoms, int64_t frames, double2* __restrict__ partial) {
+    // partial != NULL: atom chunk blockIdx.z of chunk_atoms atoms -> partial[chunk][t][pix] (re, im), folded by
+    // k_amp_reduce (split-K: a small plane x few frames cannot fill the device with one pixel per thread)
     __shared__ ulonglong4 As[128];
     const int64_t t = blockIdx.y;
     const int64_t n_q = g.n_h * g.n_k;
@@ -146,13 +149,15 @@ k_lattice64(const ulonglong4* __restrict__ staged, int64_t N, LatticeGeom g, O* 
     const int64_t pp = pix < n_q ? pix : 0;
     const uint64_t h = (uint64_t)(g.h0 + pp / g.n_k), k = (uint64_t)(g.k0 + pp % g.n_k);
     const ulonglong4* S = staged + t * N;
+    const int64_t a_begin = partial ? (int64_t)blockIdx.z * chunk_atoms : 0;
+    const int64_t a_end = partial ? min(N, a_begin + chunk_atoms) : N;
     double re = 0.0, im = 0.0;
-    for (int64_t a0 = 0; a0 < N; a0 += 128) {
+    for (int64_t a0 = a_begin; a0 < a_end; a0 += 128) {
         __syncthreads();
         const int64_t j = a0 + threadIdx.x;
-        As[threadIdx.x] = j < N ? S[j] : make_ulonglong4(0, 0, 0, 0);
+        As[threadIdx.x] = j < a_end ? S[j] : make_ulonglong4(0, 0, 0, 0);
         __syncthreads();
-        const int cnt = (int)min((int64_t)128, N - a0);
+        const int cnt = (int)min((int64_t)128, a_end - a0);
         for (int a = 0; a < cnt; ++a) {
             const ulonglong4 at = As[a];
             const uint64_t T = h * at.x + k * at.y + at.z;
@@ -164,7 +169,8 @@ k_lattice64(const ulonglong4* __restrict__ staged, int64_t N, LatticeGeom g, O* 
         }
     }
     if (pix < n_q) {
-        if (mode == 0) I_out[t * n_q + pix] = (O)(re * re + im * im);          // Eq.(8)
+        if (partial) partial[((int64_t)blockIdx.z * frames + t) * n_q + pix] = make_double2(re, im);
+        else if (mode == 0) I_out[t * n_q + pix] = (O)(re * re + im * im);          // Eq.(8)
         else { I_out[2 * (t * n_q + pix)] = (O)re; I_out[2 * (t * n_q + pix) + 1] = (O)im; }   // Eq.(7)
     }
 }
@@ -214,12 +220,13 @@ cudaError_t launch_generic64(const ulonglong4* staged, int64_t N, int64_t frames
 }
 
 cudaError_t launch_lattice_f64(const ulonglong4* staged, int64_t N, int64_t frames, const LatticeGeom& g,
-                               void* I_out, int out_f64, int mode, cudaStream_t s) {
+                               void* I_out, int out_f64, int mode, cudaStream_t s, double2* partial,
+                               int64_t chunk_atoms, int64_t n_chunks) {
     const int64_t n_q = g.n_h * g.n_k;
-    dim3 grid((unsigned)((n_q + 127) / 128), (unsigned)frames);
+    dim3 grid((unsigned)((n_q + 127) / 128), (unsigned)frames, (unsigned)(partial ? n_chunks : 1));
     note_launch();
-    if (out_f64) k_lattice64<double><<<grid, 128, 0, s>>>(staged, N, g, (double*)I_out, mode);
-    else k_lattice64<float><<<grid, 128, 0, s>>>(staged, N, g, (float*)I_out, mode);
+    if (out_f64) k_lattice64<double><<<grid, 128, 0, s>>>(staged, N, g, (double*)I_out, mode, chunk_atoms, frames, partial);
+    else k_lattice64<float><<<grid, 128, 0, s>>>(staged, N, g, (float*)I_out, mode, chunk_atoms, frames, partial);
     return cudaGetLastError();
 }
 
