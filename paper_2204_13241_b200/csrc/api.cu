@@ -427,7 +427,12 @@ static int validate_volume(const xpcs_qvolume* vol) {
 }
 
 // ---- integer-engine grid planning (k_lattice_i8: clusters of 2 CTAs, one CTA per SM, 32-atom stages) ----
-constexpr double kI8CtaCost = 15.0;     // per-CTA fixed cost in stage units: prologue, the single drain, teardown
+constexpr double kI8CtaCostDefault = 40.0;   // per-CTA fixed cost in stage units: prologue, the single drain, teardown
+static double i8_cta_cost() {
+    static double c = -1.0;
+    if (c < 0.0) { const char* e = getenv("XPCS_I8_CTA_COST"); c = e ? atof(e) : kI8CtaCostDefault; }   // experiments
+    return c;
+}
 constexpr double kI8BatchCost = 20.0;   // an extra frame batch: its staging, reduction and launch gaps (stage units)
 static int64_t i8_tiles(const LatticeGeom& g) { return ((g.n_h + 255) / 256) * ((g.n_k + 127) / 128); }
 // atoms per chunk for `units` (tile, virtual frame) pairs of Ng atoms: chunks only balance the grid (exact int32
@@ -442,7 +447,7 @@ static int64_t i8_plan_chunk(int64_t Ng, int64_t units, double* cost_out) {
         const int64_t ch = std::min<int64_t>(((Ng + c - 1) / c + 31) / 32 * 32, kI8MaxChunk);
         const int64_t cc = (Ng + ch - 1) / ch;
         const double waves = std::ceil((double)(units * cc) / (double)wave);
-        const double cost = waves * ((double)(ch / 32) + kI8CtaCost);
+        const double cost = waves * ((double)(ch / 32) + i8_cta_cost());
         if (cost < best_cost * (1.0 - 1e-9)) { best_cost = cost; best = c; }
     }
     if (cost_out) *cost_out = best_cost;
