@@ -1,6 +1,7 @@
 // api.cu -- the C ABI of libxpcs.so (include/xpcs.h): validation, frame batching, scratch, orchestration.
 // Every computational step is a kernel of this library; this file only validates, sizes and enqueues.
 #include "common.cuh"
+#include <map>
 #include <mutex>
 #include "../../include/xpcs.h"
 
@@ -1128,15 +1129,14 @@ struct HostRes {
     std::vector<cudaEvent_t> ev;
 };
 std::mutex g_host_mu;
-std::vector<std::pair<std::pair<int, cudaStream_t>, HostRes>> g_host_res;
+std::map<std::pair<int, cudaStream_t>, HostRes> g_host_res;   // node-based: references stay valid
 
 int host_resources(cudaStream_t s, size_t n_events, HostRes*& out) {
     std::lock_guard<std::mutex> lk(g_host_mu);
     int dev = 0;
     cudaGetDevice(&dev);
-    HostRes* r = nullptr;
-    for (auto& kv : g_host_res)
-        if (kv.first.first == dev && kv.first.second == s) r = &kv.second;
+    auto it = g_host_res.find({dev, s});
+    HostRes* r = it == g_host_res.end() ? nullptr : &it->second;
     if (!r || r->ev.size() < n_events) {
         cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
         if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
@@ -1144,8 +1144,7 @@ int host_resources(cudaStream_t s, size_t n_events, HostRes*& out) {
             return XPCS_EUNSUPPORTED;
         }
         if (!r) {
-            g_host_res.push_back({{dev, s}, HostRes{}});
-            r = &g_host_res.back().second;
+            r = &g_host_res[{dev, s}];
             if (cudaStreamCreateWithFlags(&r->h2d, cudaStreamNonBlocking) != cudaSuccess ||
                 cudaStreamCreateWithFlags(&r->d2h, cudaStreamNonBlocking) != cudaSuccess ||
                 cudaStreamCreateWithFlags(&r->red, cudaStreamNonBlocking) != cudaSuccess) {
