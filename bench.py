@@ -191,6 +191,58 @@ def cpu_baseline(cfg, budget_s):
             "sample": f"{cfg.name} frame 0, {len(pix)} seeded pixels x {cfg.N} atoms ({pairs:.3g} pairs, {dt:.1f} s)"}
 
 
+def run_qslab(args, cfg, ws, rank, dev, dist):
+    """--qslab: every rank holds the same trajectory and computes its slab of detector rows; one NCCL all-reduce of
+    the ring / XSVS moments per step; value = the whole detector's pairs / the max-over-ranks step time."""
+    import torch
+    import paper_2204_13241_b200 as xp
+    from paper_2204_13241_b200 import pipeline
+    from paper_2204_13241_b200 import dist as xd
+    assert cfg.n_plane and not cfg.two_species, "--qslab: lattice configs with unit form factors (c2)"
+    wl = pipeline.workload_from_config(cfg, device=dev)
+    wl.engine = {"auto": xp.ENGINE_AUTO, "simt": xp.ENGINE_SIMT, "tensor": xp.ENGINE_TENSOR,
+                 "i8": xp.ENGINE_TENSOR_I8}[args.engine]
+    Q = pipeline.QSlabPipeline(wl, rank, ws, device=dev)
+    pos_d = torch.from_numpy(xi.positions(cfg)).to(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(args.warmup):
+        Q.run(pos_d, None)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    t_ms = []
+    with ClockSampler(dev.index) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            if dist is not None:
+                dist.barrier()
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            Q.run(pos_d, None)
+            b.record(stream)
+            torch.cuda.synchronize()
+            t_ms.append(a.elapsed_time(b))
+    ms = xd.max_over_ranks(float(np.mean(t_ms)), dev)
+    pairs = int(cfg.N) * int(cfg.n_plane) ** 2 * int(cfg.T)
+    if rank == 0:
+        line = {"metric": METRIC, "value": pairs / (ms / 1e3), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic", "mode": "qslab",
+                "config": {"workload": cfg.name, "N": cfg.N, "n_q": cfg.n_plane ** 2, "frames": cfg.T,
+                           "parallelism": f"q-slab x{ws} (one trajectory, detector rows split, moments all-reduced)",
+                           "rows_per_rank": [xd.qslab(cfg.n_plane, -cfg.n_plane // 2, r, ws)[1] for r in range(ws)],
+                           "allreduce_bytes": int(Q.mom.numel() * 8),
+                           "l2": "flushed between timed steps (256 MB write, untimed)"},
+                "e2e": None, "clocks": clk.summary(), "step_ms_all": t_ms}
+        print(json.dumps(line), flush=True)
+    Q.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -206,6 +258,9 @@ def main():
     ap.add_argument("--e2e-slots", type=int, default=2, help="pipelines in flight for the end-to-end figure")
     ap.add_argument("--e2e-batches", type=int, default=4, help="frame batches per step in the end-to-end figure")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of replaying its CUDA graph")
+    ap.add_argument("--qslab", action="store_true",
+                    help="strong scaling: ONE trajectory, the detector split into row slabs across the ranks, ring "
+                         "moments all-reduced once per step (SURVEY 8(e)); lattice configs without species")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -220,6 +275,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     cfg = xi.CONFIGS[args.config]
+    if args.qslab:
+        return run_qslab(args, cfg, ws, rank, dev, dist)
     # weak scaling: each rank its own independent trajectory
     from paper_2204_13241_b200 import dist as xd
     cfg_r = xi.scaled(cfg, seed=xd.trajectory_seed(cfg.seed, rank)) if rank else cfg

@@ -241,6 +241,27 @@ XPCS_API int xpcs_speckle_histogram(const void* I_series, int64_t frames, int64_
                                     int32_t n_bins, int32_t M, int32_t n_hist, double kappa_max, int64_t* counts_out,
                                     const xpcs_opts* opts);
 
+/* Additive ring moments (a detector split into slabs across devices adds these -- e.g. with one
+ * NCCL all-reduce -- and then forms the ring means and the XSVS contrast exactly as the single-device calls do).
+ * xpcs_ring_moments: moments_out DEVICE [rows][n_bins][2] = (count of finite values, their sum) per ring and row,
+ *   for values [rows][n_q] in_dtype (I for S(q,t), g2 for the ring-averaged g2).
+ * xpcs_ring_means_from_moments: out DEVICE [rows][n_bins] = scale * sum / count (NaN for count 0), divided by
+ *   sum_j f_j^2 reduced on the device from form_factors [N] (in_dtype) when form_factors != NULL (S(q), Eq. 12-13).
+ * xsvs_moments: moments_out DEVICE [n_slots][n_bins][3] = (m0 = ring pixel count, m1 = sum I_W, m2 = sum I_W^2) for
+ *   every window W (in list order) and snapshot s = 0 .. floor(frames/W) - 1, slot = (windows before W) + s;
+ *   n_slots = sum_W floor(frames / W) (Eq. 15 windows, as xsvs_contrast).
+ * xsvs_contrast_from_moments: beta_out DEVICE [n_windows][n_bins] from (summed) moments, Eq.(17) per snapshot then
+ *   the mean over snapshots; NaN for a ring with m0 = 0.
+ * Errors: EINVAL for null pointers, sizes <= 0, windows outside [1, frames]. */
+XPCS_API int xpcs_ring_moments(const void* values, int64_t rows, int64_t n_q, const int32_t* bin_of_q, int32_t n_bins,
+                               double* moments_out, const xpcs_opts* opts);
+XPCS_API int xpcs_ring_means_from_moments(const double* moments, int64_t rows, int32_t n_bins, double scale,
+                                          const void* form_factors, int64_t N, double* out, const xpcs_opts* opts);
+XPCS_API int xsvs_moments(const void* I_series, int64_t frames, int64_t n_q, const int32_t* bin_of_q, int32_t n_bins,
+                          const int32_t* windows, int64_t n_windows, double* moments_out, const xpcs_opts* opts);
+XPCS_API int xsvs_contrast_from_moments(const double* moments, int64_t frames, const int32_t* windows,
+                                        int64_t n_windows, int32_t n_bins, double* beta_out, const xpcs_opts* opts);
+
 /* Ring plans.  Every ring reduction (xsvs_contrast, xpcs_shell_mean, xpcs_structure_factor_shells,
  * xpcs_speckle_histogram) first groups the detector pixels by ring (a deterministic counting sort of bin_of_q, three
  * small kernels).  xpcs_rings_register builds that plan once for a DEVICE bin_of_q array (n_q entries, n_bins rings)

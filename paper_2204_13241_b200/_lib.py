@@ -28,7 +28,8 @@ EXPORTED = (
     "xpcs_amplitude", "xpcs_amplitude_grid", "xpcs_isf",
     "xpcs_intensity_volume", "xpcs_amplitude_volume", "xpcs_intensity_species", "xpcs_amplitude_species",
     "xpcs_form_factor_gaussian", "xpcs_speckle_histogram", "xpcs_intensity_fft", "xpcs_rings_register",
-    "xpcs_rings_unregister", "xpcs_step_host",
+    "xpcs_rings_unregister", "xpcs_step_host", "xpcs_ring_moments", "xpcs_ring_means_from_moments", "xsvs_moments",
+    "xsvs_contrast_from_moments",
 )
 
 
@@ -126,6 +127,10 @@ def load():
         "xpcs_form_factor_gaussian": [vp, i64, ctypes.POINTER(QVolume), i32, ctypes.POINTER(ctypes.c_double),
                                       ctypes.POINTER(ctypes.c_double), dbl, vp, op],
         "xpcs_step_host": [ctypes.POINTER(Step), op],
+        "xpcs_ring_moments": [vp, i64, i64, vp, i32, vp, op],
+        "xpcs_ring_means_from_moments": [vp, i64, i32, dbl, vp, i64, vp, op],
+        "xsvs_moments": [vp, i64, i64, vp, i32, ip32, i64, vp, op],
+        "xsvs_contrast_from_moments": [vp, i64, ip32, i64, i32, vp, op],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -475,6 +480,60 @@ def xpcs_speckle_histogram(I, bins, n_bins, M, n_hist, kappa_max, out=None, stre
     o = make_opts(_dtype_code(I), F64, stream, ENGINE_AUTO, profile)
     _check(load().xpcs_speckle_histogram(_ptr(I), T, n_q, _ptr(bins), int(n_bins), int(M), int(n_hist),
                                          float(kappa_max), _ptr(out), ctypes.byref(o)))
+    return out
+
+
+def xpcs_ring_moments(values, bins, n_bins, out=None, stream=None, profile=False):
+    """Additive ring moments [rows][n_bins][2] = (count of finite values, sum) (float64, device)."""
+    import torch
+    if values.dim() == 1:
+        values = values.unsqueeze(0)
+    rows, n_q = values.shape
+    if out is None:
+        out = torch.empty((rows, n_bins, 2), dtype=torch.float64, device=values.device)
+    o = make_opts(_dtype_code(values), F64, stream, ENGINE_AUTO, profile)
+    _check(load().xpcs_ring_moments(_ptr(values), rows, n_q, _ptr(bins), int(n_bins), _ptr(out), ctypes.byref(o)))
+    return out
+
+
+def xpcs_ring_means_from_moments(moments, scale=1.0, form_factors=None, N=0, out=None, stream=None):
+    """scale * sum / count per (row, ring) from [rows][n_bins][2] moments, / sum f^2 when form_factors is given."""
+    import torch
+    rows, n_bins = moments.shape[0], moments.shape[1]
+    if out is None:
+        out = torch.empty((rows, n_bins), dtype=torch.float64, device=moments.device)
+    ind = _dtype_code(form_factors) if form_factors is not None else F32
+    o = make_opts(ind, F64, stream)
+    _check(load().xpcs_ring_means_from_moments(_ptr(moments), rows, int(n_bins), float(scale), _ptr(form_factors),
+                                               int(N), _ptr(out), ctypes.byref(o)))
+    return out
+
+
+def xsvs_n_slots(frames, windows):
+    return int(sum(int(frames) // int(w) for w in windows))
+
+
+def xsvs_moments(I, bins, n_bins, windows, out=None, stream=None, profile=False):
+    """XSVS moments [n_slots][n_bins][3] = (ring pixel count, sum I_W, sum I_W^2) (float64, device)."""
+    import torch
+    T, n_q = I.shape
+    w_arr, w_p = _i32_array(windows)
+    if out is None:
+        out = torch.empty((xsvs_n_slots(T, windows), n_bins, 3), dtype=torch.float64, device=I.device)
+    o = make_opts(_dtype_code(I), F64, stream, ENGINE_AUTO, profile)
+    _check(load().xsvs_moments(_ptr(I), T, n_q, _ptr(bins), int(n_bins), w_p, len(w_arr), _ptr(out), ctypes.byref(o)))
+    return out
+
+
+def xsvs_contrast_from_moments(moments, frames, windows, out=None, stream=None):
+    import torch
+    n_bins = moments.shape[1]
+    w_arr, w_p = _i32_array(windows)
+    if out is None:
+        out = torch.empty((len(w_arr), n_bins), dtype=torch.float64, device=moments.device)
+    o = make_opts(F32, F64, stream)
+    _check(load().xsvs_contrast_from_moments(_ptr(moments), int(frames), w_p, len(w_arr), int(n_bins), _ptr(out),
+                                             ctypes.byref(o)))
     return out
 
 

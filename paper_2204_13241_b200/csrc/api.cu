@@ -991,6 +991,107 @@ int xsvs_contrast(const void* I_series, int64_t frames, int64_t n_q, const int32
                                  mom, nullptr, beta_out, o.s), "xsvs");
 }
 
+// ------------------------------------------------------------------------------------------- ring moments
+// (the additive form of the ring reductions: a detector split across devices adds these before forming the
+// means / beta)
+static int window_slots(const int32_t* windows, int64_t n_windows, int64_t frames, int64_t& n_slots, int64_t& max_pass) {
+    n_slots = 0;
+    max_pass = 0;
+    for (int64_t w0 = 0; w0 < n_windows; w0 += 8) {   // windows per XSVS pass (XW in k_stats.cu)
+        int64_t sp = 0;
+        for (int64_t i = w0; i < std::min(n_windows, w0 + 8); ++i) {
+            if (windows[i] < 1 || windows[i] > frames) {
+                set_error("xpcs: window %d out of range [1, %lld]", windows[i], (long long)frames);
+                return XPCS_EINVAL;
+            }
+            sp += frames / windows[i];
+        }
+        n_slots += sp;
+        max_pass = std::max(max_pass, sp);
+    }
+    return XPCS_OK;
+}
+
+int xpcs_ring_moments(const void* values, int64_t rows, int64_t n_q, const int32_t* bin_of_q, int32_t n_bins,
+                      double* moments_out, const xpcs_opts* opts) {
+    clear_error();
+    Opts o;
+    TRY(parse_opts(opts, o));
+    NEED(values, "values");
+    NEED(bin_of_q, "bin_of_q");
+    NEED(moments_out, "moments_out");
+    POS(rows, "rows");
+    POS(n_q, "n_q");
+    POS(n_bins, "n_bins");
+    TRY(check_sticky());
+    ProfScope p(o.profile, KC_RINGS, o.s);
+    PlanBufs pb;
+    TRY(make_plan(bin_of_q, n_q, n_bins, o.s, pb));
+    return cuda_fail(launch_shell_moments(values, o.in_f64, rows, n_q, pb.plan, n_bins, moments_out, o.s), "ring moments");
+}
+
+int xpcs_ring_means_from_moments(const double* moments, int64_t rows, int32_t n_bins, double scale,
+                                 const void* form_factors, int64_t N, double* out, const xpcs_opts* opts) {
+    clear_error();
+    Opts o;
+    TRY(parse_opts(opts, o));
+    NEED(moments, "moments");
+    NEED(out, "out");
+    POS(rows, "rows");
+    POS(n_bins, "n_bins");
+    if (form_factors) POS(N, "N");
+    TRY(check_sticky());
+    double* norm = nullptr;
+    if (form_factors) {
+        norm = (double*)scratch(o.s, SS_SMALL, 64);
+        if (!norm) return XPCS_ENOMEM;
+        TRY(cuda_fail(launch_sum_f2(form_factors, o.in_f64, N, norm, o.s), "sum f^2"));
+    }
+    return cuda_fail(launch_ring_means_from_moments(moments, rows * n_bins, scale, norm, out, o.s), "ring means");
+}
+
+int xsvs_moments(const void* I_series, int64_t frames, int64_t n_q, const int32_t* bin_of_q, int32_t n_bins,
+                 const int32_t* windows, int64_t n_windows, double* moments_out, const xpcs_opts* opts) {
+    clear_error();
+    Opts o;
+    TRY(parse_opts(opts, o));
+    NEED(I_series, "I_series");
+    NEED(bin_of_q, "bin_of_q");
+    NEED(windows, "windows");
+    NEED(moments_out, "moments_out");
+    POS(frames, "frames");
+    POS(n_q, "n_q");
+    POS(n_bins, "n_bins");
+    POS(n_windows, "n_windows");
+    int64_t n_slots = 0, max_pass = 0;
+    TRY(window_slots(windows, n_windows, frames, n_slots, max_pass));
+    TRY(check_sticky());
+    ProfScope p(o.profile, KC_XSVS, o.s);
+    PlanBufs pb;
+    TRY(make_plan(bin_of_q, n_q, n_bins, o.s, pb));
+    double* mom = (double*)scratch(o.s, SS_XSVS, sizeof(double2) * (size_t)(pb.max_warps * max_pass));
+    if (!mom) return XPCS_ENOMEM;
+    return cuda_fail(launch_xsvs(I_series, o.in_f64, frames, n_q, pb.plan, n_bins, windows, n_windows, pb.max_warps,
+                                 mom, moments_out, nullptr, o.s), "xsvs moments");
+}
+
+int xsvs_contrast_from_moments(const double* moments, int64_t frames, const int32_t* windows, int64_t n_windows,
+                               int32_t n_bins, double* beta_out, const xpcs_opts* opts) {
+    clear_error();
+    Opts o;
+    TRY(parse_opts(opts, o));
+    NEED(moments, "moments");
+    NEED(windows, "windows");
+    NEED(beta_out, "beta_out");
+    POS(frames, "frames");
+    POS(n_bins, "n_bins");
+    POS(n_windows, "n_windows");
+    int64_t n_slots = 0, max_pass = 0;
+    TRY(window_slots(windows, n_windows, frames, n_slots, max_pass));
+    TRY(check_sticky());
+    return cuda_fail(launch_xsvs_beta_from_moments(moments, frames, windows, n_windows, n_bins, beta_out, o.s), "beta");
+}
+
 int xpcs_rings_register(const int32_t* bin_of_q, int64_t n_q, int32_t n_bins, const xpcs_opts* opts) {
     clear_error();
     Opts o;

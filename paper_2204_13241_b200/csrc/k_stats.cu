@@ -321,6 +321,56 @@ k_shell_mean(const In* __restrict__ v, int64_t n_q, const int32_t* __restrict__ 
     }
 }
 
+// ring moments per row (count of finite values, their sum) in the fixed block order of k_shell_mean
+template <typename In>
+__global__ void __launch_bounds__(256)
+k_shell_moments(const In* __restrict__ v, int64_t n_q, const int32_t* __restrict__ perm, const int32_t* __restrict__ off,
+                double* __restrict__ out, int32_t n_bins) {
+    __shared__ double sh[256];
+    const int b = blockIdx.x;
+    const int64_t row = blockIdx.y;
+    const In* V = v + row * n_q;
+    double acc = 0.0, cnt = 0.0;
+    for (int i = off[b] + threadIdx.x; i < off[b + 1]; i += 256) {
+        const double x = (double)V[perm[i]];
+        if (isfinite(x)) { acc += x; cnt += 1.0; }
+    }
+    const double sm = block_sum_d(acc, sh);
+    const double c = block_sum_d(cnt, sh);
+    if (threadIdx.x == 0) {
+        out[(row * n_bins + b) * 2] = c;
+        out[(row * n_bins + b) * 2 + 1] = sm;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+k_ring_means_from_moments(const double* __restrict__ mom, int64_t n, double scale, const double* __restrict__ norm,
+                          double* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double c = mom[2 * i], sm = mom[2 * i + 1];
+        double r = c > 0.0 ? scale * (sm / c) : __longlong_as_double(0x7ff8000000000000ll);
+        if (norm) r = r / norm[0];
+        out[i] = r;
+    }
+}
+
+cudaError_t launch_shell_moments(const void* v, int in_f64, int64_t rows, int64_t n_q, BinPlan plan, int32_t n_bins,
+                                 double* out, cudaStream_t s) {
+    dim3 grid((unsigned)n_bins, (unsigned)rows);
+    note_launch();
+    if (in_f64) k_shell_moments<double><<<grid, 256, 0, s>>>((const double*)v, n_q, plan.perm, plan.offsets, out, n_bins);
+    else k_shell_moments<float><<<grid, 256, 0, s>>>((const float*)v, n_q, plan.perm, plan.offsets, out, n_bins);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ring_means_from_moments(const double* mom, int64_t n, double scale, const double* norm, double* out,
+                                           cudaStream_t s) {
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 4096));
+    note_launch();
+    k_ring_means_from_moments<<<(unsigned)blocks, 256, 0, s>>>(mom, n, scale, norm, out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_sum_f2(const void* f, int f_f64, int64_t N, double* out, cudaStream_t s) {
     note_launch();
     if (f_f64) k_sum_f2<double><<<1, 256, 0, s>>>((const double*)f, N, out);
@@ -588,9 +638,72 @@ k_xsvs_final(const double2* __restrict__ mom, const int32_t* __restrict__ off, c
         beta_out[(int64_t)(w_first + w) * n_bins + b] = m0 > 0 ? tot / S : __longlong_as_double(0x7ff8000000000000ll);
 }
 
+// per (slot, ring) moments (m0 = ring pixel count, m1, m2) summed over the ring's warps in warp order, for
+// xsvs_moments (a q-sharded detector adds these over ranks before forming beta)
+__global__ void __launch_bounds__(256)
+k_xsvs_final_moments(const double2* __restrict__ mom, const int32_t* __restrict__ off, const int32_t* __restrict__ woff,
+                     WinSet ws, int64_t slot_first, int32_t n_bins, double* __restrict__ out) {
+    const int w = blockIdx.x, b = blockIdx.y;
+    const double m0 = (double)(off[b + 1] - off[b]);
+    for (int s = threadIdx.x; s < ws.S[w]; s += blockDim.x) {
+        double m1 = 0.0, m2 = 0.0;
+        for (int g = woff[b]; g < woff[b + 1]; ++g) {
+            const double2 v = mom[(int64_t)g * ws.total_slots + ws.base[w] + s];
+            m1 += v.x;
+            m2 += v.y;
+        }
+        double* o = out + ((slot_first + ws.base[w] + s) * n_bins + b) * 3;
+        o[0] = m0;
+        o[1] = m1;
+        o[2] = m2;
+    }
+}
+
+// beta_{W,b} from summed moments (Eq. 17 per snapshot, population variance, then the mean over snapshots)
+__global__ void __launch_bounds__(256)
+k_xsvs_beta_from_moments(const double* __restrict__ mom, WinSet ws, int64_t slot_first, int w_first, int32_t n_bins,
+                         double* __restrict__ beta_out) {
+    const int w = blockIdx.x;
+    for (int b = threadIdx.x; b < n_bins; b += blockDim.x) {
+        double acc = 0.0;
+        bool ok = ws.S[w] > 0;
+        for (int sI = 0; sI < ws.S[w]; ++sI) {
+            const double* o = mom + ((slot_first + ws.base[w] + sI) * n_bins + b) * 3;
+            if (!(o[0] > 0.0)) { ok = false; break; }
+            const double mean = o[1] / o[0];
+            acc += (o[2] / o[0] - mean * mean) / (mean * mean);
+        }
+        beta_out[(int64_t)(w_first + w) * n_bins + b] = ok ? acc / ws.S[w] : __longlong_as_double(0x7ff8000000000000ll);
+    }
+}
+
+cudaError_t launch_xsvs_beta_from_moments(const double* mom, int64_t T, const int32_t* windows_host, int64_t n_windows,
+                                          int32_t n_bins, double* beta_out, cudaStream_t s) {
+    int64_t slot_first = 0;
+    for (int64_t w0 = 0; w0 < n_windows; w0 += XW) {
+        WinSet ws{};
+        ws.n = (int)min((int64_t)XW, n_windows - w0);
+        int slots = 0;
+        for (int i = 0; i < ws.n; ++i) {
+            ws.W[i] = windows_host[w0 + i];
+            ws.S[i] = (int)(T / ws.W[i]);
+            ws.base[i] = slots;
+            slots += ws.S[i];
+        }
+        ws.total_slots = slots;
+        note_launch();
+        k_xsvs_beta_from_moments<<<ws.n, 256, 0, s>>>(mom, ws, slot_first, (int)w0, n_bins, beta_out);
+        slot_first += slots;
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
 cudaError_t launch_xsvs(const void* I, int in_f64, int64_t T, int64_t n_q, BinPlan plan, int32_t n_bins,
                         const int32_t* windows_host, int64_t n_windows, int64_t max_warps, double* warp_moments,
-                        int32_t* /*dev_windows*/, double* beta_out, cudaStream_t s) {
+                        double* mom_out, double* beta_out, cudaStream_t s) {
+    int64_t slot_first = 0;
     for (int64_t w0 = 0; w0 < n_windows; w0 += XW) {
         WinSet ws{};
         ws.n = (int)min((int64_t)XW, n_windows - w0);
@@ -624,8 +737,13 @@ cudaError_t launch_xsvs(const void* I, int in_f64, int64_t T, int64_t n_q, BinPl
             }
         }
 #endif
-        k_xsvs_final<<<dim3(ws.n, n_bins), 256, 0, s>>>((const double2*)warp_moments, plan.offsets, plan.warp_off, ws,
-                                                        (int)w0, n_bins, beta_out);
+        if (mom_out)
+            k_xsvs_final_moments<<<dim3(ws.n, n_bins), 256, 0, s>>>((const double2*)warp_moments, plan.offsets,
+                                                                    plan.warp_off, ws, slot_first, n_bins, mom_out);
+        else
+            k_xsvs_final<<<dim3(ws.n, n_bins), 256, 0, s>>>((const double2*)warp_moments, plan.offsets, plan.warp_off,
+                                                            ws, (int)w0, n_bins, beta_out);
+        slot_first += ws.total_slots;
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }

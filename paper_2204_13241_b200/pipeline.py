@@ -299,3 +299,89 @@ def workload_from_config(cfg, device="cuda", stream=None) -> Workload:
                            out_dtype=in_dtype, device=device, stream=stream)
     return Workload(cfg.name, cfg.N, cfg.L, cfg.T, n_plane=0, q=q, q_max=xi.EWALD_QMAX, lags=tuple(cfg.lags),
                     windows=tuple(cfg.windows), n_bins=cfg.n_bins, in_dtype=in_dtype)
+
+
+class QSlabPipeline:
+    """One trajectory on a detector split into slabs of rows across ranks ("partition by q ... each GPU
+    then owns complete time series, so g2 stays local; shell sums need one small all-reduce").  Rank r computes I and
+    g2 on its rows [h0 + lo, h0 + hi) of the lattice plane, the additive ring moments of I (S rings), of g2 (g2 rings)
+    and the XSVS moments on its pixels, all-reduces the moments once (one flat FP64 buffer: NCCL on GPUs), and forms
+    S_b(t), g2_b(tau) and beta_{W,b} from the sums -- equal to the single-device reductions up to summation order.
+    Orchestration only: every step is an ABI call; `allreduce(t)` sums a device tensor in place over the ranks
+    (torch.distributed.all_reduce when a process group exists)."""
+
+    def __init__(self, wl: Workload, rank: int, world: int, device="cuda", allreduce=None):
+        from . import dist as xd
+        assert wl.n_plane and wl.kinds is None, "q-slab mode: lattice plane, per-atom (or unit) form factors"
+        self.wl, self.rank, self.world = wl, rank, world
+        self.device = torch.device(device)
+        full = X.lattice_plane(wl.L, wl.n_plane, 0)
+        h0, n_h, self.row0 = xd.qslab(full.n_h, full.h0, rank, world)
+        self.full = full
+        self.grid = X.qgrid(wl.L, h0, n_h, full.k0, full.n_k, tuple(full.m0), tuple(full.ma), tuple(full.mb))
+        self.n_q = self.grid.n_q
+        self.bins = X.xpcs_lattice_bins(self.grid, wl.n_bins, wl.n_plane // (2 * wl.n_bins), self.device)
+        X.xpcs_rings_register(self.bins, wl.n_bins)
+        odt = torch.float64 if wl.in_dtype == X.F64 else torch.float32
+        self.I = torch.empty((wl.T, self.n_q), dtype=odt, device=self.device)
+        self.g2 = torch.empty((len(wl.lags), self.n_q), dtype=torch.float32, device=self.device) if wl.lags else None
+        nb, T, nl = wl.n_bins, wl.T, len(wl.lags)
+        self.n_slots = X.xsvs_n_slots(T, wl.windows) if wl.windows else 0
+        sizes = [T * nb * 2, nl * nb * 2, self.n_slots * nb * 3]
+        self.mom = torch.zeros(sum(sizes), dtype=torch.float64, device=self.device)
+        o1, o2 = sizes[0], sizes[0] + sizes[1]
+        self.mS = self.mom[:o1].view(T, nb, 2)
+        self.mG = self.mom[o1:o2].view(nl, nb, 2) if nl else None
+        self.mX = self.mom[o2:].view(self.n_slots, nb, 3) if self.n_slots else None
+        self._allreduce = allreduce if allreduce is not None else self._default_allreduce
+
+    @staticmethod
+    def _default_allreduce(t):
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+
+    @property
+    def pairs_per_step(self) -> int:
+        return int(self.wl.N) * int(self.n_q) * int(self.wl.T)
+
+    def local(self, positions, form_factors, profile=False):
+        """This rank's slab: I, g2 and the ring / XSVS moments (before the all-reduce)."""
+        wl = self.wl
+        X.xpcs_intensity_grid(positions, form_factors, self.grid, out=self.I, engine=wl.engine, profile=profile)
+        X.xpcs_ring_moments(self.I, self.bins, wl.n_bins, out=self.mS, profile=profile)
+        if wl.lags:
+            X.xpcs_g2(self.I, wl.lags, out=self.g2, out_dtype=X.F32, profile=profile)
+            X.xpcs_ring_moments(self.g2, self.bins, wl.n_bins, out=self.mG, profile=profile)
+        if self.n_slots:
+            X.xsvs_moments(self.I, self.bins, wl.n_bins, wl.windows, out=self.mX, profile=profile)
+        return self.mom
+
+    def finish(self, form_factors, moments=None):
+        """Ring results from (summed) moments."""
+        wl = self.wl
+        m = self.mom if moments is None else moments
+        T, nb, nl = wl.T, wl.n_bins, len(wl.lags)
+        mS = m[:T * nb * 2].view(T, nb, 2)
+        out = {"I": self.I}
+        if form_factors is not None:
+            out["S_rings"] = X.xpcs_ring_means_from_moments(mS, 1.0, form_factors, wl.N)
+        else:
+            out["S_rings"] = X.xpcs_ring_means_from_moments(mS, 1.0 / wl.N)
+        if nl:
+            out["g2"] = self.g2
+            out["g2_rings"] = X.xpcs_ring_means_from_moments(m[T * nb * 2:(T + nl) * nb * 2].view(nl, nb, 2))
+        if self.n_slots:
+            out["beta"] = X.xsvs_contrast_from_moments(m[(T + nl) * nb * 2:].view(self.n_slots, nb, 3), T, wl.windows)
+        return out
+
+    def run(self, positions, form_factors, profile=False):
+        self.local(positions, form_factors, profile)
+        self._allreduce(self.mom)
+        return self.finish(form_factors)
+
+    def close(self):
+        try:
+            X.xpcs_rings_unregister(self.bins)
+        except Exception:
+            pass

@@ -47,6 +47,10 @@ def test_two_rank_gloo(tmp_path):
     np.testing.assert_allclose(res[0]["rings"], ref, rtol=1e-12)
     np.testing.assert_allclose(res[1]["rings"], ref, rtol=1e-12)
     assert res[0]["seed"] != res[1]["seed"]
+    assert res[0]["allreduce"] == res[1]["allreduce"] == [3.0] * 7
+    bref = np.nan_to_num(oracle.xsvs_beta(I, oracle.lattice_bins(n), 32, [1, 2]), nan=-1.0)
+    np.testing.assert_allclose(res[0]["beta"], bref, rtol=1e-12)
+    np.testing.assert_allclose(res[1]["beta"], bref, rtol=1e-12)
 
 
 def test_shard_properties():
