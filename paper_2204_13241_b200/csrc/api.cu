@@ -363,14 +363,14 @@ static int run_direct(const void* positions, int64_t N, const void* form_factors
         return XPCS_OK;
     }
     // fp32: split atoms only when (q tiles x frames) cannot fill the device
-    const int64_t qtiles = (n_q + 1023) / 1024;
+    const int64_t qtiles = (n_q + generic_q_per_block() - 1) / generic_q_per_block();
     std::vector<int64_t> chunk(ng, 512), C(ng, 0);
     int64_t sumC = 0;
     for (int g = 0; g < ng; ++g) {
         const int64_t Ng = G.cnt[g];
         if (Ng == 0) continue;
         int64_t c = 1;
-        const int64_t want = 2LL * sm_count();
+        const int64_t want = (int64_t)generic_blocks_per_sm() * sm_count();
         if (qtiles * frames < want) c = std::min<int64_t>((want + qtiles * frames - 1) / (qtiles * frames), (Ng + 511) / 512);
         int64_t ch = (Ng + c - 1) / c;
         ch = ((ch + 511) / 512) * 512;

@@ -33,6 +33,8 @@ struct ProfScope {
 };
 
 int sm_count();
+int generic_q_per_block();    // k_generic32 tile: q per CTA
+int generic_blocks_per_sm();  // k_generic32: CTAs per SM its registers are sized for
 const void* host_table(const void* data, size_t bytes);    // cached device copy of a host table (by content)
 const int32_t* lag_table(const int32_t* lags, int64_t n);   // host_table of a lag list
 

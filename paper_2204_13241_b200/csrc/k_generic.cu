@@ -16,11 +16,20 @@
 
 namespace xpcs {
 
+#ifndef XPCS_GEN_QT
+#define XPCS_GEN_QT 2          // q per thread (c4: 2 q x 3 CTAs/SM 1.915e12 pairs/s vs 4 q x 2 CTAs/SM 1.881e12)
+#endif
+#ifndef XPCS_GEN_MINB
+#define XPCS_GEN_MINB 3        // resident CTAs per SM the register budget is sized for
+#endif
 namespace {
 constexpr int GT = 256;     // threads per CTA
-constexpr int QT = 4;       // q per thread
+constexpr int QT = XPCS_GEN_QT;       // q per thread
 constexpr int SUB = 512;    // atoms per shared-memory sub-block (also the fp32 accumulation length)
 }
+
+int generic_q_per_block() { return GT * QT; }
+int generic_blocks_per_sm() { return XPCS_GEN_MINB; }
 
 __device__ __forceinline__ void q_split(double qc, double L_over_2pi, uint32_t& n, float& two_pi_phi) {
     const double gq = qc * L_over_2pi;
@@ -30,7 +39,7 @@ __device__ __forceinline__ void q_split(double qc, double L_over_2pi, uint32_t& 
 }
 
 template <typename Q>
-__global__ void __launch_bounds__(GT, 2)
+__global__ void __launch_bounds__(GT, XPCS_GEN_MINB)
 k_generic32(const uint4* __restrict__ staged, int64_t N, const Q* __restrict__ q, int64_t n_q, double L_over_2pi,
             int64_t chunk_atoms, int64_t frames, double2* __restrict__ partial) {
     __shared__ uint4 As[2 * SUB];
