@@ -288,7 +288,7 @@ XPCS_API int xpcs_structure_factor_shells(const void* I, int64_t rows, int64_t n
 
 /* ------------------------------------------------------------------------------------------------
  * One pass of the whole hot path from HOST memory (the end-to-end entry point):
- * I(q,t) on a lattice plane (Eq. 7-8, Algorithm 1) for every frame, g2 (Eq. 14), the ring
+ * I(q,t) on a lattice plane or an explicit q list (Eq. 7-8, Algorithm 1) for every frame, g2 (Eq. 14), the ring
  * averages S(q,t) (Eq. 12-13) and of g2, and the XSVS contrast (Eq. 15+17).
  * The frames are split into `batches`: batch b's positions are copied host -> device on an internal copy stream,
  * its intensities are computed on opts->stream and copied back on a second internal copy stream while batch b+1
@@ -315,7 +315,10 @@ typedef struct {
     const void* form_factors;
     const xpcs_species* species;
     int64_t N, frames;
-    xpcs_qgrid grid;
+    xpcs_qgrid grid;           /* lattice plane (used when q_vectors == NULL) */
+    const void* q_vectors;     /* DEVICE [n_q][3] in_dtype explicit q (e.g. an Ewald detector), or NULL */
+    int64_t n_q;               /* with q_vectors */
+    double box_L;              /* with q_vectors: box edge (positions are wrapped into [0, L)^3) */
     const int32_t* bin_of_q;
     int32_t n_bins;
     int32_t batches;

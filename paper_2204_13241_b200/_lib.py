@@ -66,7 +66,8 @@ class QVolume(ctypes.Structure):
 class Step(ctypes.Structure):
     """xpcs_step (include/xpcs.h): one host-buffer pass of the whole hot path."""
     _fields_ = [("positions", ctypes.c_void_p), ("form_factors", ctypes.c_void_p), ("species", ctypes.c_void_p),
-                ("N", ctypes.c_int64), ("frames", ctypes.c_int64), ("grid", QGrid), ("bin_of_q", ctypes.c_void_p),
+                ("N", ctypes.c_int64), ("frames", ctypes.c_int64), ("grid", QGrid), ("q_vectors", ctypes.c_void_p),
+                ("n_q", ctypes.c_int64), ("box_L", ctypes.c_double), ("bin_of_q", ctypes.c_void_p),
                 ("n_bins", ctypes.c_int32), ("batches", ctypes.c_int32), ("lags", ctypes.POINTER(ctypes.c_int32)),
                 ("n_lags", ctypes.c_int64), ("windows", ctypes.POINTER(ctypes.c_int32)), ("n_windows", ctypes.c_int64),
                 ("I_out", ctypes.c_void_p), ("g2_out", ctypes.c_void_p), ("S_rings", ctypes.c_void_p),
@@ -215,9 +216,9 @@ def _host_ptr(t):
     return t.data_ptr()
 
 
-def xpcs_step_host(positions, form_factors, grid: QGrid, bins, n_bins, lags=(), windows=(), I_out=None, g2_out=None,
+def xpcs_step_host(positions, form_factors, grid, bins, n_bins, lags=(), windows=(), I_out=None, g2_out=None,
                    S_rings=None, g2_rings=None, beta=None, species=None, batches=8, engine=ENGINE_AUTO, stream=None,
-                   profile=False, out_dtype=None):
+                   profile=False, out_dtype=None, q_vectors=None, box_L=0.0):
     """xpcs_step_host: the whole hot path from HOST buffers (positions [T][N][3], optional form factors [N]; pinned
     for overlap) into HOST outputs (any may be None).  `bins` is the DEVICE ring index [n_q]; `species` an optional
     (host species [N], device f_q [S][n_q], f_max) triple.  Enqueued on `stream`; outputs valid after it syncs."""
@@ -233,7 +234,11 @@ def xpcs_step_host(positions, form_factors, grid: QGrid, bins, n_bins, lags=(), 
         sp, keep = species_desc(*species)
         keep = (sp, keep)
         st.species = ctypes.addressof(sp)
-    st.N, st.frames, st.grid = N, T, grid
+    st.N, st.frames = N, T
+    if q_vectors is not None:
+        st.q_vectors, st.n_q, st.box_L = _ptr(q_vectors).value, q_vectors.shape[0], float(box_L)
+    else:
+        st.grid = grid
     st.bin_of_q = _ptr(bins).value
     st.n_bins, st.batches = int(n_bins), int(batches)
     l_arr, l_p = _i32_array(lags) if len(lags) else (None, None)

@@ -1293,7 +1293,14 @@ int xpcs_step_host(const xpcs_step* st, const xpcs_opts* opts) {
     POS(st->frames, "frames");
     POS(st->n_bins, "n_bins");
     POS(st->batches, "batches");
-    TRY(validate_grid(&st->grid));
+    if (!st->q_vectors) TRY(validate_grid(&st->grid));
+    else {
+        POS(st->n_q, "n_q");
+        if (!(st->box_L > 0.0) || !std::isfinite(st->box_L)) {
+            set_error("xpcs: box_L must be finite and > 0");
+            return XPCS_EINVAL;
+        }
+    }
     if (st->n_lags < 0 || st->n_windows < 0 || (st->n_lags > 0 && !st->lags) || (st->n_windows > 0 && !st->windows)) {
         set_error("xpcs: lags/windows: negative count or NULL array");
         return XPCS_EINVAL;
@@ -1309,7 +1316,8 @@ int xpcs_step_host(const xpcs_step* st, const xpcs_opts* opts) {
             return XPCS_EINVAL;
         }
     TRY(check_sticky());
-    const int64_t N = st->N, T = st->frames, n_q = st->grid.n_h * st->grid.n_k, nb = st->n_bins;
+    const int64_t N = st->N, T = st->frames, nb = st->n_bins;
+    const int64_t n_q = st->q_vectors ? st->n_q : st->grid.n_h * st->grid.n_k;
     const int64_t n_bat = std::min<int64_t>(st->batches, T);
     const size_t pin = o.in_f64 ? 8 : 4, pout = o.out_f64 ? 8 : 4;
     const size_t pos_bytes = pin * 3 * (size_t)N * (size_t)T, i_bytes = pout * (size_t)n_q * (size_t)T;
@@ -1358,8 +1366,12 @@ int xpcs_step_host(const xpcs_step* st, const xpcs_opts* opts) {
         const int64_t t0 = b * T / n_bat, t1 = (b + 1) * T / n_bat;
         TRY(cuda_fail(cudaStreamWaitEvent(o.s, ev[1 + b], 0), "wait inputs"));
         if (b == 0 && st->form_factors) TRY(cuda_fail(cudaStreamWaitEvent(o.s, ev_f, 0), "wait f"));
-        TRY(run_volume(d_pos + t0 * frame_pos, N, st->species ? nullptr : d_ff, st->species, &vol, t1 - t0,
-                       d_I + t0 * frame_i, &io, 0));
+        if (st->q_vectors)
+            TRY(run_direct(d_pos + t0 * frame_pos, N, st->species ? nullptr : d_ff, st->species, st->q_vectors, n_q,
+                           t1 - t0, st->box_L, d_I + t0 * frame_i, &io, 0));
+        else
+            TRY(run_volume(d_pos + t0 * frame_pos, N, st->species ? nullptr : d_ff, st->species, &vol, t1 - t0,
+                           d_I + t0 * frame_i, &io, 0));
         TRY(cuda_fail(cudaEventRecord(ev[1 + n_bat + b], o.s), "event"));
         if (st->I_out) {
             TRY(cuda_fail(cudaStreamWaitEvent(hr->d2h, ev[1 + n_bat + b], 0), "wait I"));

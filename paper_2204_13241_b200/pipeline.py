@@ -184,12 +184,11 @@ class Pipeline:
         self.s_comp = [torch.cuda.Stream(self.device), torch.cuda.Stream(self.device)]
 
     def run_host(self) -> dict:
-        """End to end from pinned host memory.  Lattice planes: one `xpcs_step_host` call (the C ABI's host-buffer
-        entry: frame-batched H2D / intensity / D2H overlap on internal copy streams, then g2, rings and XSVS and
-        their D2H), all enqueued on the current stream.  Explicit q lists use the stream orchestration below."""
+        """End to end from pinned host memory: one `xpcs_step_host` call (the C ABI's host-buffer entry: frame-batched
+        H2D / intensity / D2H overlap on internal copy streams, then g2, rings and XSVS and their D2H), enqueued on
+        the current stream (lattice planes and explicit q lists).  `_run_host_streams` is the earlier Python stream
+        orchestration of the same copies (kept for comparison)."""
         wl = self.wl
-        if self.grid is None:
-            return self._run_host_streams()
         main = torch.cuda.current_stream(self.device)
         h = self.h_out
         T, nl, nw, nb = wl.T, len(wl.lags), len(wl.windows), wl.n_bins
@@ -207,7 +206,8 @@ class Pipeline:
                                       I_out=h["I"], g2_out=h.get("g2"), S_rings=h["S_rings"],
                                       g2_rings=h.get("g2_rings"), beta=h.get("beta"), species=sp,
                                       batches=self.n_batches, engine=wl.engine, stream=main,
-                                      out_dtype=X.F64 if self.I.dtype == torch.float64 else X.F32)
+                                      out_dtype=X.F64 if self.I.dtype == torch.float64 else X.F32,
+                                      q_vectors=wl.q if self.grid is None else None, box_L=wl.L)
         return h
 
     def _run_host_streams(self) -> dict:
