@@ -165,29 +165,18 @@ class Pipeline:
         return self._capture(self.run_host)
 
     # ---------------------------------------------------------------- end to end from host memory
-    def alloc_host_io(self, pos_host: np.ndarray, f_host: np.ndarray | None, batches: int = 8):
-        """Pinned host copies of the inputs and pinned result buffers (allocated once, reused per step)."""
+    def alloc_host_io(self, pos_host: np.ndarray, f_host: np.ndarray | None, batches: int = 4):
+        """Pinned host copies of the inputs (allocated once, reused per step); the pinned result buffers are made by
+        the first run_host.  `batches`: frame batches of the copy / compute overlap inside xpcs_step_host."""
         self.h_pos = torch.from_numpy(np.ascontiguousarray(pos_host)).pin_memory()
         self.h_f = torch.from_numpy(np.ascontiguousarray(f_host)).pin_memory() if f_host is not None else None
-        self.d_pos = torch.empty(self.h_pos.shape, dtype=self.h_pos.dtype, device=self.device)
-        self.d_f = torch.empty(self.h_f.shape, dtype=self.h_f.dtype, device=self.device) if f_host is not None else None
         self.h_out = {}
-        T = self.wl.T
-        nb = max(1, min(int(batches), T))
-        self.n_batches = nb
-        edges = [round(i * T / nb) for i in range(nb + 1)]
-        self.batches = [(edges[i], edges[i + 1]) for i in range(nb) if edges[i + 1] > edges[i]]
-        self.s_h2d = torch.cuda.Stream(self.device)
-        self.s_d2h = torch.cuda.Stream(self.device)
-        # two compute streams: consecutive frame batches run concurrently, so the last wave of one batch's intensity
-        # kernel shares the GPU with the next batch's first wave (the library keeps scratch per stream)
-        self.s_comp = [torch.cuda.Stream(self.device), torch.cuda.Stream(self.device)]
+        self.n_batches = max(1, min(int(batches), self.wl.T))
 
     def run_host(self) -> dict:
         """End to end from pinned host memory: one `xpcs_step_host` call (the C ABI's host-buffer entry: frame-batched
         H2D / intensity / D2H overlap on internal copy streams, then g2, rings and XSVS and their D2H), enqueued on
-        the current stream (lattice planes and explicit q lists).  `_run_host_streams` is the earlier Python stream
-        orchestration of the same copies (kept for comparison)."""
+        the current stream (lattice planes and explicit q lists)."""
         wl = self.wl
         main = torch.cuda.current_stream(self.device)
         h = self.h_out
@@ -209,71 +198,6 @@ class Pipeline:
                                       out_dtype=X.F64 if self.I.dtype == torch.float64 else X.F32,
                                       q_vectors=wl.q if self.grid is None else None, box_L=wl.L)
         return h
-
-    def _run_host_streams(self) -> dict:
-        """End to end: pinned H2D of the step's positions, I(q,t), g2, rings and XSVS, D2H of every result.
-        Frames are split into batches: H2D on one stream, the intensity kernels alternate between two compute streams
-        (consecutive batches overlap on the GPU), D2H of each batch's I on a copy stream; the reductions follow on the
-        caller's stream, g2 first so that its result streams back while the ring reductions run."""
-        wl = self.wl
-        main = torch.cuda.current_stream(self.device)
-        if "I" not in self.h_out:
-            self.h_out["I"] = torch.empty(self.I.shape, dtype=self.I.dtype, pin_memory=True)
-        if self.d_f is not None:
-            with torch.cuda.stream(self.s_h2d):
-                self.d_f.copy_(self.h_f, non_blocking=True)
-        self.s_h2d.wait_stream(main)            # previous step's readers of d_pos are done
-        self.s_d2h.wait_stream(main)
-        ev_in = []
-        for (t0, t1) in self.batches:
-            with torch.cuda.stream(self.s_h2d):
-                self.d_pos[t0:t1].copy_(self.h_pos[t0:t1], non_blocking=True)
-                e = torch.cuda.Event()
-                e.record(self.s_h2d)
-                ev_in.append(e)
-        for sc in self.s_comp:
-            sc.wait_stream(main)
-        for bi, (t0, t1) in enumerate(self.batches):
-            sc = self.s_comp[bi % 2]
-            sc.wait_event(ev_in[bi])
-            pos_b = self.d_pos[t0:t1]
-            I_b = self.I[t0:t1]
-            if self.kind_fq is not None:
-                X.xpcs_intensity_volume(pos_b, None, self.vol, species=wl.kinds, f_q=self.kind_fq, out=I_b,
-                                        engine=wl.engine, stream=sc, f_max=wl.kind_f)
-            elif self.grid is not None:
-                X.xpcs_intensity_grid(pos_b, self.d_f, self.grid, out=I_b, engine=wl.engine, stream=sc)
-            else:
-                X.xpcs_intensity(pos_b, self.d_f, wl.q, wl.L, out=I_b, stream=sc)
-            e = torch.cuda.Event()
-            e.record(sc)
-            self.s_d2h.wait_event(e)
-            with torch.cuda.stream(self.s_d2h):
-                self.h_out["I"][t0:t1].copy_(I_b, non_blocking=True)
-        for sc in self.s_comp:
-            main.wait_stream(sc)
-        out = {}
-        if wl.lags and "g2" not in self.h_out:
-            self.h_out["g2"] = torch.empty(self.g2.shape, dtype=self.g2.dtype, pin_memory=True)
-
-        def g2_back(st):
-            # g2 (the largest reduction result) streams back on the copy stream while the other reductions run
-            e = torch.cuda.Event()
-            e.record(st)
-            self.s_d2h.wait_event(e)
-            with torch.cuda.stream(self.s_d2h):
-                self.h_out["g2"].copy_(self.g2, non_blocking=True)
-
-        self._reductions(out, self.I, self.d_f, main, after_g2=g2_back)
-        for k, v in out.items():
-            if k == "g2":
-                continue
-            if k not in self.h_out:
-                self.h_out[k] = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
-            self.h_out[k].copy_(v, non_blocking=True)
-        main.wait_stream(self.s_d2h)
-        main.wait_stream(self.s_h2d)
-        return self.h_out
 
     def io_bytes(self):
         h2d = self.h_pos.numel() * self.h_pos.element_size()

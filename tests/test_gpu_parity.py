@@ -233,7 +233,8 @@ def test_config2_simt_engine_sampled():
 
 
 def test_end_to_end_host_path_matches_device_path():
-    """pipeline.run_host (pinned H2D in frame batches on 4 streams, D2H of every result) == pipeline.run.  The
+    """pipeline.run_host (xpcs_step_host: pinned H2D in frame batches on internal copy streams, D2H of every result)
+    == pipeline.run.  The
     integer engine sizes its atom chunks by the frames of each call, so the host path's smaller batches fold the
     same exact per-chunk sums in different fp32 partials: results agree to fp32 rounding, not bit for bit; the
     second run_host of the same batches is bit-identical to the first (determinism)."""
