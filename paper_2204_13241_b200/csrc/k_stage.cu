@@ -33,25 +33,31 @@ template <typename P, typename F>
 __global__ void __launch_bounds__(256) k_stage_lattice32(const P* __restrict__ pos, const F* __restrict__ f,
                                                          int64_t N, int64_t V, LatticeGeom g, StageMap m,
                                                          uint4* __restrict__ out) {
-    const double invL = 1.0 / g.L;
-    STAGE_LOOPS(N, V) {
+    // Xi = round(frac(x / L) 2^32) = rint(x (2^32 / L)) mod 2^32: the integer part of x / L only moves bits >= 32,
+    // and x (2^32 / L) = (x / L) 2^32 exactly (power-of-two scaling), so one DMUL + one F2I per coordinate
+    const double s32 = (1.0 / g.L) * 4294967296.0;
+    for (int64_t vi = blockIdx.y; vi < V; vi += gridDim.y) {
         int64_t t, l;
         stage_frame(m, vi, t, l);
-        const int64_t src = stage_atom(m, j), i = vi * N + j;
-        const P* r = pos + 3 * (t * m.n_src + src);
-        uint32_t X[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) X[c] = frac_to_fixed32(box_fraction_fast((double)r[c], invL));
-        uint32_t th[3];
         int32_t m0[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) m0[c] = g.m0[c] + (int32_t)l * m.mc[c];
-        const int32_t* mv[3] = {g.ma, g.mb, m0};
+        const P* base = pos + 3 * t * m.n_src;
+        uint4* o = out + vi * N;
+#pragma unroll 1
+        for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t src = stage_atom(m, j);
+            const P* r = base + 3 * src;
+            uint32_t X[3];
 #pragma unroll
-        for (int k = 0; k < 3; ++k)
-            th[k] = (uint32_t)mv[k][0] * X[0] + (uint32_t)mv[k][1] * X[1] + (uint32_t)mv[k][2] * X[2];
-        const float fj = f ? (float)f[src] : 1.0f;
-        out[i] = make_uint4(th[0], th[1], th[2], __float_as_uint(fj));
+            for (int c = 0; c < 3; ++c) X[c] = (uint32_t)(unsigned long long)llrint((double)r[c] * s32);
+            uint32_t th[3];
+            th[0] = (uint32_t)g.ma[0] * X[0] + (uint32_t)g.ma[1] * X[1] + (uint32_t)g.ma[2] * X[2];
+            th[1] = (uint32_t)g.mb[0] * X[0] + (uint32_t)g.mb[1] * X[1] + (uint32_t)g.mb[2] * X[2];
+            th[2] = (uint32_t)m0[0] * X[0] + (uint32_t)m0[1] * X[1] + (uint32_t)m0[2] * X[2];
+            const float fj = f ? (float)f[src] : 1.0f;
+            o[j] = make_uint4(th[0], th[1], th[2], __float_as_uint(fj));
+        }
     }
 }
 
