@@ -243,6 +243,39 @@ def run_qslab(args, cfg, ws, rank, dev, dist):
     return 0
 
 
+def _e2e_streamed(args, P, pipeline, wl, dev, pos_h, f_h, slots, stream, dist):
+    import torch
+    # streaming: `slots` pipelines (own device buffers, pinned host buffers and CUDA graph each) replayed
+    # round-robin on their own streams, so step k+1's H2D and kernels overlap step k's result D2H; every
+    # step still copies its inputs in and its results out.  Time = whole run / steps (CUDA events).
+    pipes = [P] + [pipeline.Pipeline(wl, device=dev) for _ in range(slots - 1)]
+    for Q in pipes[1:]:
+        Q.alloc_host_io(pos_h, f_h, batches=args.e2e_batches)
+        Q.run_host()
+    graphs = [Q.capture_host()[0] for Q in pipes]
+    streams = [torch.cuda.Stream() for _ in pipes]
+    n_e = max(2 * slots, args.steps)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for st_ in streams:
+        st_.wait_stream(stream)
+    for k in range(n_e):
+        with torch.cuda.stream(streams[k % slots]):
+            graphs[k % slots].replay()
+    for st_ in streams:
+        stream.wait_stream(st_)
+    b.record(stream)
+    torch.cuda.synchronize()
+    e_ms = a.elapsed_time(b) / n_e
+    for Q in pipes[1:]:
+        Q.close()
+    return e_ms
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -299,15 +332,22 @@ def main():
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     xp.profile_reset()
     graph = None
+    launch_note = "eager" if args.no_graph else "cuda graph (one replay per step)"
     if not args.no_graph:
         # the step as one CUDA graph (kernels, side-stream fork/join, profiling events): no host launch gaps inside
         # the timed region; every replay recomputes everything from pos_d
-        graph, _ = P.capture(pos_d, f_d, profile=True)
-        launches_graph = P.capture_launches
-        for _ in range(args.warmup):                    # the first replays upload the graph: untimed
-            flush.zero_()
-            graph.replay()
-        torch.cuda.synchronize()
+        try:
+            graph, _ = P.capture(pos_d, f_d, profile=True)
+            launches_graph = P.capture_launches
+            for _ in range(args.warmup):                    # the first replays upload the graph: untimed
+                flush.zero_()
+                graph.replay()
+            torch.cuda.synchronize()
+        except Exception as e:                              # capture failed: time the eager step instead
+            graph = None
+            launch_note = f"eager (graph capture failed: {type(e).__name__})"
+            torch.cuda.synchronize()
+            xp.profile_reset()
     n_launch0 = xp.launch_count()
     prof = {}
     with ClockSampler(local) as clk:
@@ -430,7 +470,14 @@ def main():
         P.run_host()
         torch.cuda.synchronize()
         slots = 1 if args.no_graph else max(1, args.e2e_slots)
-        if args.no_graph:
+        e_ms = None
+        if not args.no_graph:
+            try:
+                e_ms = _e2e_streamed(args, P, pipeline, wl, dev, pos_h, f_h, slots, stream, dist)
+            except Exception:                                  # capture failed: eager host steps instead
+                torch.cuda.synchronize()
+                slots = 1
+        if e_ms is None:
             t_e = []
             for _ in range(max(2, args.steps)):
                 if dist is not None:
@@ -444,35 +491,6 @@ def main():
                 torch.cuda.synchronize()
                 t_e.append(a.elapsed_time(b))
             e_ms = float(np.mean(t_e))
-        else:
-            # streaming: `slots` pipelines (own device buffers, pinned host buffers and CUDA graph each) replayed
-            # round-robin on their own streams, so step k+1's H2D and kernels overlap step k's result D2H; every
-            # step still copies its inputs in and its results out.  Time = whole run / steps (CUDA events).
-            pipes = [P] + [pipeline.Pipeline(wl, device=dev) for _ in range(slots - 1)]
-            for Q in pipes[1:]:
-                Q.alloc_host_io(pos_h, f_h, batches=args.e2e_batches)
-                Q.run_host()
-            graphs = [Q.capture_host()[0] for Q in pipes]
-            streams = [torch.cuda.Stream() for _ in pipes]
-            n_e = max(2 * slots, args.steps)
-            if dist is not None:
-                dist.barrier()
-            torch.cuda.synchronize()
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            for st_ in streams:
-                st_.wait_stream(stream)
-            for k in range(n_e):
-                with torch.cuda.stream(streams[k % slots]):
-                    graphs[k % slots].replay()
-            for st_ in streams:
-                stream.wait_stream(st_)
-            b.record(stream)
-            torch.cuda.synchronize()
-            e_ms = a.elapsed_time(b) / n_e
-            for Q in pipes[1:]:
-                Q.close()
         e_ms = xd.max_over_ranks(e_ms, dev)
         h2d, d2h = P.io_bytes()
         e2e = {"value": ws * pairs_step / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms, "streams": slots,
@@ -530,7 +548,7 @@ def main():
                            "pairs_per_step_per_gpu": pairs_step, "engine": args.engine,
                            "engine_used": ("fp64" if wl.in_dtype == xp.F64 else eng_name),
                            "l2": "flushed between timed steps (256 MB write, untimed)",
-                           "launch": "eager" if args.no_graph else "cuda graph (one replay per step)",
+                           "launch": launch_note,
                            "parallelism": f"weak x{ws} (independent trajectories)"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(n_launch),
                 "clocks": clk.summary(), "step_ms_all": step_ms,
