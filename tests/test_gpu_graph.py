@@ -102,3 +102,50 @@ def test_host_step_explicit_q_matches_device_run():
     assert_pixels(h["I"].numpy(), I_dev, cfg.N, "host step, explicit q")
     np.testing.assert_allclose(h["S_rings"].numpy(), S_dev, rtol=1e-5, equal_nan=True)
     P.close()
+
+
+def test_host_step_edge_cases():
+    """xpcs_step_host: pageable (unpinned) host buffers, more batches than frames, no lags / windows, NULL outputs,
+    rings that are empty (NaN), and f64 positions (FP64 path) -- each against the device-buffer calls."""
+    cfg = xi.scaled(xi.CONFIGS["c2"], N=1500, T=3, n_plane=64, lags=(), windows=(), n_bins=40)
+    pos = xi.positions(cfg)
+    g = xp.lattice_plane(cfg.L, 64)
+    bins = xp.xpcs_lattice_bins(g, 40, 2, DEV)          # rings of width 2 up to r < 80: r <= 45 fills rings 0..22
+    I_dev = xp.xpcs_intensity_grid(torch.from_numpy(pos).to(DEV), None, g).cpu().numpy()
+    S_dev = xp.xpcs_structure_factor_shells(torch.from_numpy(I_dev).to(DEV), None, cfg.N, bins, 40).cpu().numpy()
+    hp = torch.from_numpy(pos.copy())                   # pageable
+    hI = torch.empty((cfg.T, 64 * 64), dtype=torch.float32)
+    hS = torch.empty((cfg.T, 40), dtype=torch.float64)
+    xp.xpcs_step_host(hp, None, g, bins, 40, I_out=hI, S_rings=hS, batches=7)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(hI.numpy(), I_dev, rtol=2e-5, atol=2e-5 * np.abs(I_dev).max())
+    np.testing.assert_allclose(hS.numpy(), S_dev, rtol=1e-5, equal_nan=True)
+    assert np.isnan(hS.numpy()[:, 23:]).all()           # empty rings
+    # nothing requested but I: NULL reductions outputs are skipped
+    hI2 = torch.zeros_like(hI)
+    xp.xpcs_step_host(hp, None, g, bins, 40, I_out=hI2, batches=1)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(hI2.numpy(), xp.xpcs_intensity_grid(torch.from_numpy(pos).to(DEV), None, g).cpu().numpy())
+    # FP64 positions -> FP64 kernels, FP64 output
+    p64 = torch.from_numpy(pos.astype(np.float64))
+    hI64 = torch.empty((cfg.T, 64 * 64), dtype=torch.float64)
+    xp.xpcs_step_host(p64, None, g, bins, 40, I_out=hI64, batches=2)
+    torch.cuda.synchronize()
+    ref64 = xp.xpcs_intensity_grid(p64.to(DEV), None, g).cpu().numpy()
+    np.testing.assert_allclose(hI64.numpy(), ref64, rtol=1e-12, atol=1e-9)
+
+
+def test_moments_empty_rings_are_nan():
+    cfg = xi.scaled(xi.CONFIGS["c2"], N=800, T=8, n_plane=32, lags=(1,), windows=(1, 2), n_bins=24)
+    g = xp.lattice_plane(cfg.L, 32)
+    bins = xp.xpcs_lattice_bins(g, 24, 1, DEV)           # r <= 22.6: rings 23 empty
+    I = xp.xpcs_intensity_grid(torch.from_numpy(xi.positions(cfg)).to(DEV), None, g)
+    m = xp.xpcs_ring_moments(I, bins, 24)
+    means = xp.xpcs_ring_means_from_moments(m, 1.0).cpu().numpy()
+    assert np.isnan(means[:, 23:]).all() and np.isfinite(means[:, 1:15]).all()
+    mx = xp.xsvs_moments(I, bins, 24, [1, 2])
+    beta = xp.xsvs_contrast_from_moments(mx, cfg.T, [1, 2]).cpu().numpy()
+    ref = xp.xsvs_contrast(I, bins, 24, [1, 2]).cpu().numpy()
+    assert np.array_equal(np.isnan(beta), np.isnan(ref))
+    ok = ~np.isnan(ref)
+    np.testing.assert_allclose(beta[ok], ref[ok], rtol=1e-12)
