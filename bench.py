@@ -288,7 +288,9 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-slots", type=int, default=2, help="pipelines in flight for the end-to-end figure")
+    ap.add_argument("--e2e-slots", type=int, default=0,
+                    help="pipelines in flight for the end-to-end figure (0: 3 when a step's pinned inputs are < 512 MB, "
+                         "else 2)")
     ap.add_argument("--e2e-batches", type=int, default=4, help="frame batches per step in the end-to-end figure")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of replaying its CUDA graph")
     ap.add_argument("--qslab", action="store_true",
@@ -469,7 +471,8 @@ def main():
         P.alloc_host_io(pos_h, f_h, batches=args.e2e_batches)
         P.run_host()
         torch.cuda.synchronize()
-        slots = 1 if args.no_graph else max(1, args.e2e_slots)
+        auto_slots = 3 if pos_h.nbytes < (512 << 20) else 2
+        slots = 1 if args.no_graph else (args.e2e_slots if args.e2e_slots > 0 else auto_slots)
         e_ms = None
         if not args.no_graph:
             try:
