@@ -58,7 +58,9 @@ constexpr int MMA_N = 2 * TN;                     // N = 256: [Re | Im'] of 64 k
 constexpr int RPT = XPCS_TC_RPT, XWARPS = 2 * (8 / RPT), WWARPS = 8 / RPT;
 constexpr int NGROUPS = XPCS_TC_GROUPS, GROUP_WARPS = XWARPS + WWARPS;   // per group: X warps (row slices), W warps
 constexpr int NPROD_WARPS = NGROUPS * GROUP_WARPS, NDRAIN_WARPS = 4;
-constexpr int WREC = 16, WSLOT = WREC + WREC / 4;          // per-warp records of a stage (16 atoms, padded)
+// per-warp records of a stage (16 atoms); record r sits in 16-B unit r ^ ((r & 8) >> 2): conflict-free cp.async
+// writes (8 lanes per phase) and per-field 32-bit reads of records {u, 4 + u, 8 + u, 12 + u}
+constexpr int WREC = 16, WSLOT = WREC;
 #else
 constexpr int NPROD_WARPS = 16, NDRAIN_WARPS = 4;
 #endif
@@ -385,7 +387,9 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
         // recurrence (2 sincos per atom per stage, 2 packed ops per phasor); split into fp16 hi/lo with magic
         // numbers (3 packed ops per phasor) and packed with cvt.f16x2.  Lanes (quad qq, row mr): conflict-free.
         const int grp = warp / GROUP_WARPS, wi = warp % GROUP_WARPS;
-        const int qq = lane & 3, mr = lane >> 2;
+        // lanes: each half-warp owns one 128-B K half of a row group (qq in {0,1} | {2,3}, mr 0..7), so the
+        // STS.64 of a half-warp phase covers 128 contiguous bytes (no bank conflict between the K halves)
+        const int qq = (lane & 1) | ((lane >> 4) << 1), mr = (lane >> 1) & 7;
         const bool is_x = wi < XWARPS;
         const uint32_t slot0 = smem_u32(aslot) + (uint32_t)(warp * ASLOTS * WSLOT * 16);
         const uint32_t full0 = mapa(smem_u32(full), 0);
@@ -394,7 +398,7 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
             if (i < n_stages && lane < WREC) {
                 const int64_t j = a_begin + (int64_t)i * KS + lane;
                 const bool ok = j < a_end;
-                cp_async16(slot0 + (uint32_t)(((li % ASLOTS) * WSLOT + lane + (lane >> 2)) * 16), S + (ok ? j : 0),
+                cp_async16(slot0 + (uint32_t)(((li % ASLOTS) * WSLOT + (lane ^ ((lane & 8) >> 2))) * 16), S + (ok ? j : 0),
                            ok ? 16u : 0u);
             }
             cp_async_commit();
@@ -411,12 +415,21 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
             prefetch(li + ASLOTS - 1);
             uint4 at[4];
             {
-                const uint32_t ra = slot0 + (uint32_t)(((li % ASLOTS) * WSLOT + 5 * qq) * 16);
+                // only the fields this warp uses: X warps Th_a, W warps (Th_b, Th_0, f)
+                const uint32_t ra = slot0 + (uint32_t)((li % ASLOTS) * WSLOT * 16);
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                                 : "=r"(at[u].x), "=r"(at[u].y), "=r"(at[u].z), "=r"(at[u].w)
-                                 : "r"(ra + 16 * u));
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t a = ra + (uint32_t)((((4 * qq + u) ^ (qq & 2))) * 16);   // record 4 qq + u
+                    if (is_x) {
+                        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(at[u].x) : "r"(a));
+                        at[u].y = at[u].z = at[u].w = 0u;
+                    } else {
+                        at[u].x = 0u;
+                        asm volatile("ld.shared.u32 %0, [%1+4];" : "=r"(at[u].y) : "r"(a));
+                        asm volatile("ld.shared.u32 %0, [%1+8];" : "=r"(at[u].z) : "r"(a));
+                        asm volatile("ld.shared.u32 %0, [%1+12];" : "=r"(at[u].w) : "r"(a));
+                    }
+                }
             }
             mbar_wait(&empty[s], (uint32_t)(((i / STAGES) + 1) & 1));
             const uint32_t sbase = smem_u32(smem) + (uint32_t)(s * STAGE_BYTES);
