@@ -24,7 +24,7 @@ for name, frames in (("c3", [0, 500, 999]), ("c5", [0, 199])):
     n = cfg.n_plane
     g = xp.lattice_plane(cfg.L, n)
     q = oracle.lattice_q(cfg.L, **oracle.plane_grid(n))
-    pix = xi.pixel_subset(q.shape[0], 3000, 5)
+    pix = xi.pixel_subset(q.shape[0], int(os.environ.get("PROBE_PIXELS", "3000")), 5)
     ref = oracle.intensity(pos, f.astype(np.float64), q[pix], cfg.L)
     sp = (f > 1.5).astype(np.int32)
     fq = torch.ones((2, n * n), dtype=torch.float32, device="cuda")
