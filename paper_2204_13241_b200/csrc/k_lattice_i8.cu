@@ -27,9 +27,10 @@
 // owns 4 consecutive atoms (one 32-bit word per row and limb plane) and 8 rows spaced 8 apart (X or W), and walks
 // the rows with the angle-addition recurrence X_{m+8} = X_m X_8 (packed FP32x2, 2 ops per phasor; 2 SFU sincos per
 // atom per thread), quantises with one packed magic-number FFMA per phasor (Q16) and packs limb bytes with PRMT.
-// Lanes (quad qq, row mr) write 32 distinct banks per store.  After the last stage, warps 0-7 (one per TMEM lane
-// quarter, two warps per quarter splitting the columns) wait for the final MMA commit and drain both
-// accumulators: p = (64516 HH + 254 X) F / 32258^2.
+// Lanes (quad qq, row mr) write 32 distinct banks per store.  After the last stage, warps 0-7 (two per TMEM lane
+// quarter, splitting the columns) wait for the final MMA commit and drain both accumulators,
+// p = (65536 HH + 256 X) F / 32512^2 (Q16), through a shared-memory tile into row-contiguous global writes: the
+// partial amplitude, or with a single atom chunk the final I = |p|^2 (or p) itself.
 #include "common.cuh"
 
 namespace xpcs {
@@ -51,7 +52,7 @@ constexpr int STAGES = XPCS_I8_STAGES;
 #endif
 constexpr int NGROUPS = XPCS_I8_GROUPS, GROUP_WARPS = 6;   // per group: 4 X warps (2 quad halves x 2 row halves), 2 W warps
 constexpr int NPROD_WARPS = NGROUPS * GROUP_WARPS;  // 30
-constexpr int MMA_WARP = NPROD_WARPS;               // warps 0-3 (distinct TMEM lane quarters) also drain the tile
+constexpr int MMA_WARP = NPROD_WARPS;               // producer warps 0-7 (two per TMEM lane quarter) also drain the tile
 constexpr int NTHREADS = (MMA_WARP + 1) * 32;       // 992
 constexpr int MMA_N = 2 * TN;                       // 256
 constexpr int TMEM_COLS = 512;                      // HH cols [0, 256), X cols [256, 512)
