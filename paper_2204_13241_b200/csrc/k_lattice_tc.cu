@@ -2,24 +2,26 @@
 //
 // The per-axis factorisation of Eq.(7) on a reciprocal-lattice plane,
 //     p^e(h,k) = sum_j X_h(j) W_k(j),   X_h(j) = e^{-2 pi i h Th_a(j)},  W_k(j) = f_j e^{-2 pi i (Th_0(j) + k Th_b(j))},
-// is a complex matrix product with the atoms as the contraction dimension K.  Each CTA owns a 128 (h) x 128 (k)
-// pixel tile of one frame and a chunk of <= 4096 atoms (split-K; chunks are folded in FP64 by k_amp_reduce):
-//     Re = Xr Wr^T - Xi Wi^T ,   Im = Xr Wi^T + Xi Wr^T           (A-negate bit of the instruction descriptor)
-// on tcgen05.mma.cta_group::1.kind::f16, M = 128, N = 128, K = 16, FP32 accumulators in TMEM (256 columns).
-// Precision: every phasor component v is split v = hi + lo (hi on a 2^-10 grid, exact in fp16; lo = fp16(v - hi)) and each real
-// product uses three MMAs (hi.hi + hi.lo + lo.hi; the dropped lo.lo term is < 2^-22 per term), i.e. FP32-class
-// products (a single fp16/tf32 pass fails the 1e-3 N gate).
+// is a complex matrix product with the atoms as the contraction dimension K.  A cluster of 2 CTAs (one per SM) owns
+// a 256 (h) x 128 (k) pixel tile of one frame and a chunk of atoms (split-K; chunks are folded in FP64 by
+// k_amp_reduce): tcgen05.mma.cta_group::2.kind::f16, M = 256 (each CTA its 128 X rows), N = 256 = [Re | Im'] of the
+// 128 k (each CTA holds 64 k of B, rows [-Ws | Wr | Ws]: B1 = [Wr | Ws] and B2 = [-Ws | Wr] are overlapping windows),
+// K = 16, FP32 accumulators in TMEM; the tile holds conj(p) (Im' = -Im, R1).
+// Precision: every phasor component v is split v = hi + lo (hi on a 2^-10 grid, exact in fp16; lo = fp16(v - hi)) and
+// each real product uses three MMAs (hi.hi + hi.lo + lo.hi; the dropped lo.lo term is < 2^-22 per term), i.e.
+// FP32-class products (a single fp16/tf32 pass fails the 1e-3 N gate).
 //
 // Accumulation: the tcgen05 FP32 accumulator is not round-to-nearest (measured: the error of a TMEM accumulation
 // grows linearly with its length, SURVEY A.8 / DESIGN.md "tensor accumulator"), so no TMEM accumulator ever sums
-// more than SUB_STAGES * 16 = 128 atoms: two TMEM accumulators (2 x 256 columns) alternate, and while the MMA
+// more than SUB_STAGES * 16 = 256 atoms: two TMEM accumulators (2 x 256 columns) alternate, and while the MMA
 // fills one, four drain warps add the other into round-to-nearest FP32 running sums in shared memory.
 //
-// One CTA per SM (TMEM 512 columns), 21 warps: warps 0-15 generate the phasor planes of 16-atom stages into a
-// 3-stage shared-memory ring (exact integer turns -> SFU sin/cos -> fp16 hi/lo, K-major canonical no-swizzle
-// layout); warps 16-19 drain TMEM and write the tile; warp 20 allocates TMEM and one lane issues the 12 MMAs per
-// stage.  Producer -> MMA: mbarrier full[s] (16 warp arrivals after fence.proxy.async); MMA -> producer:
-// tcgen05.commit -> empty[s]; MMA -> drain: tcgen05.commit -> tfull[b]; drain -> MMA: tempty[b] (4 arrivals).
+// One CTA per SM (TMEM 512 columns): 3 producer groups of 3 warps (2 X warps, 1 W warp; group g fills stages
+// g, g + 3, ... of a 3-stage ring of 16-atom stages; a thread owns 4 atoms x 8 rows and walks the rows with the
+// angle-addition recurrence), 4 drain warps, and one warp that allocates TMEM and whose lane 0
+// issues the 6 MMAs per stage.  Producer -> MMA: mbarrier full[s] (6 warp arrivals of the pair after
+// fence.proxy.async); MMA -> producer: tcgen05.commit -> empty[s]; MMA -> drain: tcgen05.commit -> tfull[b];
+// drain -> MMA: tempty[b] (8 arrivals).  XPCS_TC_GROUPED=0 builds the earlier 16-warp producer.
 #include "common.cuh"
 #include <cuda_fp16.h>
 
