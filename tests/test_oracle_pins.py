@@ -528,3 +528,43 @@ def test_fft_method_matches_direct_method_at_low_q():
     Id = oracle.intensity(pos, None, oracle.lattice_volume_q(L, -h, 2 * h, -h, 2 * h, -h, 2 * h), L)[0]
     assert np.max(np.abs(Ib - Id)) < 1e-3 * N
     assert abs(Ib.reshape(2 * h, 2 * h, 2 * h)[h, h, h] - N * N) < 1e-3 * N * N    # forward point ~ N^2
+
+
+# ------------------------------------------------------------------ hand-computed estimator examples (golden)
+# tests/golden/estimators.json holds worked examples written by hand from the definitions; each fixes a choice a
+# plausible estimator could get wrong (symmetric g2 normalisation, sample variance, a kept remainder window,
+# binning |q|^2, the conjugate amplitude).
+def _nan(a):
+    return np.array([[np.nan if v is None else v for v in row] for row in a], dtype=np.float64)
+
+
+def test_golden_g2_literal_eq14():
+    """Eq.(14), literal normalisation (R6): hand-computed g2 of a 4-frame series."""
+    g = _gold("estimators.json")["g2_literal"]
+    out = oracle.g2(np.array(g["I"]), g["lags"])
+    np.testing.assert_allclose(out, _nan(g["g2"]), rtol=1e-14, atol=1e-15, equal_nan=True)
+
+
+def test_golden_xsvs_population_variance_and_dropped_remainder():
+    """Eq.(15)+(17): hand-computed beta with T = 5 not divisible by W = 2, 3,
+    a 3-pixel ring, a single-pixel ring (population variance 0) and an empty ring (NaN)."""
+    g = _gold("estimators.json")["xsvs_population_variance_remainder_dropped"]
+    out = oracle.xsvs_beta(np.array(g["I"]), np.array(g["bins"]), g["n_bins"], g["windows"])
+    np.testing.assert_allclose(out, _nan(g["beta"]), rtol=1e-13, atol=1e-15, equal_nan=True)
+
+
+def test_golden_radial_bins_edges():
+    """PAPER.md:192 half-open rings of |q|: explicit |q| values at and either side of the bin edges."""
+    g = _gold("estimators.json")["radial_bins_edges"]
+    out = oracle.radial_bins(np.array(g["q"]), g["q_max"], g["n_bins"])
+    np.testing.assert_array_equal(out, g["bins"])
+
+
+def test_golden_amplitude_sign_quarter_box():
+    """Eq.(7): e^{-i q.r}; an atom at L/4 with q = 2 pi / L x gives p = -i."""
+    g = _gold("estimators.json")["amplitude_sign"]
+    L = g["L"]
+    for c in g["cases"]:
+        A = oracle.amplitude(np.array(c["pos"]), np.array(c["f"]), _hkl_q(L, c["hkl"]), L)
+        np.testing.assert_allclose(A.real, c["re"], atol=1e-12)
+        np.testing.assert_allclose(A.imag, c["im"], atol=1e-12)
