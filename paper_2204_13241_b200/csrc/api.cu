@@ -427,6 +427,12 @@ static int validate_volume(const xpcs_qvolume* vol) {
     return XPCS_OK;
 }
 
+static bool i8_fixup_enabled() {
+    static int on = -1;
+    if (on < 0) { const char* e = getenv("XPCS_I8_FIXUP"); on = (e && atoi(e) == 0) ? 0 : 1; }   // experiments only
+    return on == 1;
+}
+
 // ---- integer-engine grid planning (k_lattice_i8: clusters of 2 CTAs, one CTA per SM, 32-atom stages) ----
 constexpr double kI8CtaCostDefault = 40.0;   // per-CTA fixed cost in stage units: prologue, the single drain, teardown
 static double i8_cta_cost() {
@@ -698,6 +704,13 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
     }
     // the tensor engines' partials hold conj(p) (R1)
     const int mode = amp ? ((tc || i8) ? 2 : 1) : 0;
+    void* fbuf = nullptr;
+    if (i8 && i8_fixup_enabled()) {
+        int64_t vb_max = 0;
+        for (const FrameBatch& fb : batches) vb_max = std::max(vb_max, fb.vb);
+        fbuf = scratch(o.s, SS_FIX, fixup_scratch_bytes(vb_max, n_q, N));
+        if (!fbuf) return XPCS_ENOMEM;
+    }
     for (const FrameBatch& fb : batches) {
         const int64_t v0 = fb.v0, vb = fb.vb;
         if (fb.chunk > 0) { chunk[0] = fb.chunk; C[0] = (G.cnt[0] + fb.chunk - 1) / fb.chunk; }
@@ -705,6 +718,13 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
         // one integer-engine group in a single atom chunk: the kernel writes the result itself (no partial planes)
         const bool direct = ng == 1 && !G.n_species && i8 && gi8[0] && G.cnt[0] > 0 && C[0] == 1 &&
                             !(getenv("XPCS_I8_DIRECT") && atoi(getenv("XPCS_I8_DIRECT")) == 0);
+        // the integer engine's 16-bit limbs add coherently on perfect crystals: the epilogue lists the brightest
+        // pixels and k_fixup.cu recomputes them exactly
+        bool batch_i8 = false;
+        for (int gi = 0; gi < ng; ++gi) batch_i8 = batch_i8 || (i8 && gi8[(size_t)gi] && G.cnt[gi] > 0);
+        BrightSink bs{nullptr, nullptr, 0.0, nullptr};
+        const bool fix = batch_i8 && fbuf;
+        if (fix) TRY(cuda_fail(fixup_prepare(fbuf, N, form_factors ? fmax : nullptr, bs, o.s), "bright-pixel list"));
         int64_t stoff = 0, poff = 0;
         for (int gi = 0; gi < ng; ++gi) {
             const int64_t Ng = G.cnt[gi];
@@ -717,17 +737,39 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
             { ProfScope p(o.profile, KC_MAIN, o.s);
               const bool g_i8 = i8 && gi8[(size_t)gi], g_tc = (i8 || tc) && !g_i8;
               if (g_i8) TRY(cuda_fail(launch_lattice_i8(st + stoff, Ng, vb, g, chunk[gi], C[gi], fmax, form_factors == nullptr,
-                                                      part + poff, o.s, direct ? dst : nullptr, o.out_f64, mode),
+                                                      part + poff, o.s, direct ? dst : nullptr, o.out_f64, mode,
+                                                      (fix && direct) ? &bs : nullptr),
                                     "lattice tcgen05 i8"));
               else if (g_tc) TRY(cuda_fail(launch_lattice_tc(st + stoff, Ng, vb, g, chunk[gi], C[gi], part + poff, o.s), "lattice tcgen05"));
               else TRY(cuda_fail(launch_lattice_simt(st + stoff, Ng, vb, g, chunk[gi], C[gi], part + poff, o.s), "lattice simt")); }
             stoff += Ng * vb;
             poff += C[gi] * n_q * vb;
         }
-        if (direct) continue;
-        ProfScope p(o.profile, KC_REDUCE, o.s);
-        if (G.n_species) TRY(cuda_fail(launch_species_combine(sp, vb, n_q, G.fq, 0, v0, n_l, dst, o.out_f64, mode, o.s), "species combine"));
-        else TRY(cuda_fail(launch_amp_reduce_f(part, C[0], vb, n_q, dst, o.out_f64, mode, o.s), "reduce"));
+        if (!direct) {
+            ProfScope p(o.profile, KC_REDUCE, o.s);
+            if (G.n_species) TRY(cuda_fail(launch_species_combine(sp, vb, n_q, G.fq, 0, v0, n_l, dst, o.out_f64, mode, o.s,
+                                                                  fix ? &bs : nullptr), "species combine"));
+            else TRY(cuda_fail(launch_amp_reduce_f(part, C[0], vb, n_q, dst, o.out_f64, mode, o.s, fix ? &bs : nullptr), "reduce"));
+        }
+        if (fix) {
+            FixGroups fg{};
+            int64_t off = 0;
+            for (int gi = 0; gi < ng; ++gi) {
+                if (G.cnt[gi] > 0) {
+                    fg.st[fg.n_groups] = st + off;
+                    fg.n[fg.n_groups] = G.cnt[gi];
+                    fg.kind[fg.n_groups] = G.kind[gi];
+                    ++fg.n_groups;
+                }
+                off += G.cnt[gi] * vb;
+            }
+            fg.fq = G.n_species ? G.fq : nullptr;
+            fg.fq_f64 = 0;
+            fg.v0 = v0;
+            fg.n_l = n_l;
+            ProfScope p(o.profile, KC_FIXUP, o.s);
+            TRY(cuda_fail(launch_fixup(fg, g, vb, dst, o.out_f64, amp ? 1 : 0, fbuf, o.s), "bright-pixel recompute"));
+        }
     }
     return XPCS_OK;
 }

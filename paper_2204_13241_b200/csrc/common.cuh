@@ -9,7 +9,7 @@ namespace xpcs {
 // ------------------------------------------------------------------------------------------------
 // host-side runtime services (defined in runtime.cu)
 // ------------------------------------------------------------------------------------------------
-enum KernelClass { KC_MAIN = 0, KC_STAGE = 1, KC_REDUCE = 2, KC_G2 = 3, KC_XSVS = 4, KC_RINGS = 5, KC_COUNT = 6 };
+enum KernelClass { KC_MAIN = 0, KC_STAGE = 1, KC_REDUCE = 2, KC_G2 = 3, KC_XSVS = 4, KC_RINGS = 5, KC_FIXUP = 6, KC_COUNT = 7 };
 
 void set_error(const char* fmt, ...);
 void note_launch(int n = 1);
@@ -17,7 +17,7 @@ void note_launch(int n = 1);
 // Scratch cached per (stream, slot); grown on demand (the grow synchronises the device).
 enum ScratchSlot {
     SS_STAGE = 0, SS_PARTIAL, SS_PLAN, SS_PLAN2, SS_XSVS, SS_SMALL, SS_LAGS, SS_TC, SS_IDX, SS_FFT,
-    SS_H_POS, SS_H_FF, SS_H_I, SS_H_G2, SS_H_RED, SS_COUNT
+    SS_H_POS, SS_H_FF, SS_H_I, SS_H_G2, SS_H_RED, SS_FIX, SS_COUNT
 };
 void* scratch(cudaStream_t s, int slot, size_t bytes);   // nullptr on failure (error already set)
 void release_scratch();
@@ -145,8 +145,10 @@ struct SpeciesParts {
     int n;
     int part_f64;
 };
+struct BrightSink;
 cudaError_t launch_species_combine(const SpeciesParts& sp, int64_t frames, int64_t n_q, const void* fq, int fq_f64,
-                                   int64_t v0, int64_t n_l, void* out, int out_f64, int mode, cudaStream_t s);
+                                   int64_t v0, int64_t n_l, void* out, int out_f64, int mode, cudaStream_t s,
+                                   const BrightSink* bright = nullptr);
 // Algorithm 2 (FFT method): spread + cuFFT D2Z + epilogue for `frames` frames; rho [frames][n^3] double, spec
 // [frames][n][n][n/2+1] double2 scratch.  Returns 0, 2 (CUDA error) or 3 (cuFFT error); *what names the step.
 int launch_fft_intensity(const void* pos, int pos_f64, int64_t N, int64_t frames, double L, int n, double eta, int k,
@@ -172,9 +174,41 @@ bool lattice_tc_supported(const LatticeGeom& g);
 // uniform_f != 0: all f_j = 1 (no W scale); else F = max |f_j| is reduced into fmax_scratch (1 float) first.
 constexpr int64_t kI8MaxChunk = 32768;
 int i8_cluster_slots();   // k_lattice_i8 clusters resident at once (cudaOccupancyMaxActiveClusters)
+// Bright pixels after the integer engine (k_fixup.cu): the epilogue that writes a batch's final I (or p) appends
+// every pixel with I > thr * F(q)^2 (F = *fmax or 1; species: max_s |f_s(q)|) to `list` (index v * n_q + pixel of the
+// batch); k_fixup.cu then recomputes them exactly.  All pointers null: no detection.
+struct BrightSink {
+    uint32_t* count;
+    uint32_t* list;
+    double thr;             // min(64 N, N^2 / 4)
+    const float* fmax;      // max |f_j| of per-atom form factors (device), or nullptr (F = 1)
+};
+__device__ __forceinline__ void bright_append(const BrightSink& b, double I, double F, int64_t e) {
+    if (b.count && !(I <= b.thr * F * F)) {          // NaN / inf are recomputed too
+        const uint32_t at = atomicAdd(b.count, 1u);
+        b.list[at] = (uint32_t)e;
+    }
+}
+__device__ __forceinline__ double bright_F(const BrightSink& b) { return b.fmax ? (double)fmaxf(*b.fmax, 0.0f) : 1.0; }
+struct FixGroups {
+    const uint4* st[kMaxSpecies];   // staged records of group s: [vb][n[s]]
+    int64_t n[kMaxSpecies];
+    int32_t kind[kMaxSpecies];      // f_q row of group s (species calls)
+    int n_groups;
+    const void* fq;                 // species f_q [n_species][n_l * n_q] or nullptr (f inside the records)
+    int fq_f64;
+    int64_t v0, n_l;                // first virtual frame of the batch, planes per frame (f_q row = (v0 + v) % n_l)
+};
+size_t fixup_scratch_bytes(int64_t vb, int64_t n_q, int64_t n_atoms);   // count, list, chunk partials
+// carve the sink out of the fixup scratch and zero its count (before the batch's epilogue)
+cudaError_t fixup_prepare(void* scratch_buf, int64_t n_atoms, const float* fmax, BrightSink& out, cudaStream_t s);
+// exact recompute of the listed pixels (after the epilogue): out = the batch's final I [vb][n_q] or p [vb][n_q][2]
+cudaError_t launch_fixup(const FixGroups& G, const LatticeGeom& g, int64_t vb, void* out, int out_f64, int amp,
+                         void* scratch_buf, cudaStream_t s);
 cudaError_t launch_lattice_i8(const uint4* staged, int64_t N, int64_t frames, const LatticeGeom& g, int64_t chunk_atoms,
                               int64_t n_chunks, float* fmax_scratch, int uniform_f, float2* partial, cudaStream_t s,
-                              void* direct_out = nullptr, int out_f64 = 0, int mode = 0);
+                              void* direct_out = nullptr, int out_f64 = 0, int mode = 0,
+                              const BrightSink* bright = nullptr);
 // lattice FP64 (direct per-pixel evaluation with 64-bit turns): writes I directly (double)
 cudaError_t launch_lattice_f64(const ulonglong4* staged, int64_t N, int64_t frames, const LatticeGeom& g,
                                void* I_out, int out_f64, int mode, cudaStream_t s,
@@ -187,7 +221,7 @@ cudaError_t launch_generic64(const ulonglong4* staged, int64_t N, int64_t frames
                              int64_t n_q, double L, double2* partial, cudaStream_t s);
 // fold of the atom-chunk partials: mode 0 -> I = |p|^2, 1 -> p (re, im), 2 -> partials hold conj(p), write p
 cudaError_t launch_amp_reduce_f(const float2* partial, int64_t C, int64_t frames, int64_t n_q, void* I_out,
-                                int out_f64, int mode, cudaStream_t s);
+                                int out_f64, int mode, cudaStream_t s, const BrightSink* bright = nullptr);
 cudaError_t launch_amp_reduce_d(const double2* partial, int64_t C, int64_t frames, int64_t n_q, void* I_out,
                                 int out_f64, int mode, cudaStream_t s);
 // intermediate scattering function F(q, tau) = <p(t) p*(t + tau)>_t / norm, complex in/out

@@ -188,7 +188,8 @@ k_lattice64(const ulonglong4* __restrict__ staged, int64_t N, LatticeGeom g, O* 
 // mode 0: I = |p|^2 (Eq. 8);  mode 1: p = (re, im) (Eq. 7);  mode 2: the partials hold conj(p) -> p
 template <typename P, typename O>
 __global__ void __launch_bounds__(256)
-k_amp_reduce(const P* __restrict__ partial, int64_t C, int64_t total, O* __restrict__ out, int mode) {
+k_amp_reduce(const P* __restrict__ partial, int64_t C, int64_t total, O* __restrict__ out, int mode, BrightSink bs) {
+    const double F = bs.count ? bright_F(bs) : 1.0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         double re = 0.0, im = 0.0;
         int64_t c = 0;
@@ -206,6 +207,7 @@ k_amp_reduce(const P* __restrict__ partial, int64_t C, int64_t total, O* __restr
         }
         if (mode == 0) out[i] = (O)(re * re + im * im);          // Eq.(8): I = p p*
         else { out[2 * i] = (O)re; out[2 * i + 1] = (O)(mode == 2 ? -im : im); }
+        bright_append(bs, re * re + im * im, F, i);
     }
 }
 
@@ -246,11 +248,12 @@ static dim3 rgrid(int64_t total) {
 }
 
 cudaError_t launch_amp_reduce_f(const float2* partial, int64_t C, int64_t frames, int64_t n_q, void* I_out,
-                                int out_f64, int mode, cudaStream_t s) {
+                                int out_f64, int mode, cudaStream_t s, const BrightSink* bright) {
     const int64_t total = frames * n_q;
+    const BrightSink bs = bright ? *bright : BrightSink{nullptr, nullptr, 0.0, nullptr};
     note_launch();
-    if (out_f64) k_amp_reduce<float2, double><<<rgrid(total), 256, 0, s>>>(partial, C, total, (double*)I_out, mode);
-    else k_amp_reduce<float2, float><<<rgrid(total), 256, 0, s>>>(partial, C, total, (float*)I_out, mode);
+    if (out_f64) k_amp_reduce<float2, double><<<rgrid(total), 256, 0, s>>>(partial, C, total, (double*)I_out, mode, bs);
+    else k_amp_reduce<float2, float><<<rgrid(total), 256, 0, s>>>(partial, C, total, (float*)I_out, mode, bs);
     return cudaGetLastError();
 }
 
@@ -258,8 +261,9 @@ cudaError_t launch_amp_reduce_d(const double2* partial, int64_t C, int64_t frame
                                 int out_f64, int mode, cudaStream_t s) {
     const int64_t total = frames * n_q;
     note_launch();
-    if (out_f64) k_amp_reduce<double2, double><<<rgrid(total), 256, 0, s>>>(partial, C, total, (double*)I_out, mode);
-    else k_amp_reduce<double2, float><<<rgrid(total), 256, 0, s>>>(partial, C, total, (float*)I_out, mode);
+    const BrightSink bs{nullptr, nullptr, 0.0, nullptr};
+    if (out_f64) k_amp_reduce<double2, double><<<rgrid(total), 256, 0, s>>>(partial, C, total, (double*)I_out, mode, bs);
+    else k_amp_reduce<double2, float><<<rgrid(total), 256, 0, s>>>(partial, C, total, (float*)I_out, mode, bs);
     return cudaGetLastError();
 }
 

@@ -1,9 +1,19 @@
 // k_lattice_i8.cu -- K3b: lattice-plane amplitude on the tcgen05 INTEGER tensor cores (kind::i8, exact int32
 // accumulation in TMEM), the fast engine for uniform form factors.
 //
-// Same factorisation as k_lattice_tc.cu (Eq. 7, on a reciprocal-lattice plane):
-//     p^e(h,k) = sum_j X_h(j) W_k(j),  X_h = e^{-2 pi i h Th_a(j)},  W_k = (f_j / F) e^{-2 pi i (Th_0 + k Th_b)(j)}
-// with F = max_j |f_j|.  Every phasor component v in [-1, 1] is written as two int8 limbs (Q16, the default):
+// Factorisation of Eq.(7) on a reciprocal-lattice plane: the phase in turns of
+// pixel (h, k) is h Th_a + Th_0 + k Th_b (exact integer turns, k_stage.cu), so the amplitude is a complex matrix
+// product over atoms.  CONJUGATE ROW PAIRS: a CTA pair owns 256 consecutive rows h = c +- d around the tile centre
+// c = H0 + 127.5 (d = 1/2, 3/2, ..., 255/2).  With
+//     X_d(j) = e^{2 pi i d Th_a(j)} = a + i b,   W_k(j) = (f_j / F) e^{2 pi i (Th_0 + k Th_b + c Th_a)(j)} = wr + i wi
+// the tile holds q(h) = conj(p(h)) (the paper's sign e^{-iq.r}, R1) as
+//     q(c + d, k) = sum_j X_d W_k       = (AR - BI) + i (AI + BR)
+//     q(c - d, k) = sum_j conj(X_d) W_k = (AR + BI) + i (AI - BR),   AR = sum a.wr, AI = sum a.wi, BR = sum b.wr, BI = sum b.wi
+// because X_{-d} = conj(X_d) exactly.  So ONE real matrix product [a; b] x [wr | wi]^T (M = 2 x 128 d, N = 2 x 128 k)
+// yields both rows of every conjugate pair: 2 real MACs per pixel instead of the 4 of a complex MAC, and the X
+// phasor table is half as long.  Every pixel is still evaluated from all N atoms (nothing is mirrored or skipped).
+//
+// Every phasor component v in [-1, 1] is written as two int8 limbs (Q16):
 //     x = rint(32512 v) = 256 hi + lo,  hi = round(x / 256) in [-127, 127],  lo in [-128, 127]
 // (|v - x / 32512| <= 1 / 65024 = 1.54e-5).  One FFMA t = fma(v, 32512, 1.5 * 2^23 + 128) leaves y = x + 128 in the
 // low 16 bits of t: byte 1 = hi, byte 0 = lo + 128, so both limbs come from one instruction and two byte permutes.
@@ -11,49 +21,49 @@
 //     v w ~ [65536 hi.hi' + 256 (hi.lo' + lo.hi')] / 32512^2      (the dropped lo.lo' term is <= 1.55e-5, zero-mean)
 // i.e. three int8 MMAs into two TMEM accumulators, HH = sum hi.hi' and X = sum (hi.lo' + lo.hi').  The integer
 // accumulation is EXACT (no TMEM rounding, unlike the FP32 accumulator of the split-FP16 engine), so
-// a chunk of up to 32768 atoms (int32 overflow bound: 4 x 127 x 128 x 32768 < 2^31) accumulates in TMEM and is
-// drained once; the result carries only the limb quantisation error (rms |dI| ~ 3e-5 N per pixel for f = 1,
-// DESIGN.md 6.3).  XPCS_I8_Q16=0 builds the previous base-254 limbs (hi = rint(127 v), lo = rint(254 (127 v - hi)),
-// v ~ (254 hi + lo) / 32258, three magic-number FFMAs per component; kept for comparison).
+// a chunk of up to 32768 atoms accumulates in TMEM and is drained once (int32 bound: the drain's integer differences
+// AR - BI etc. stay below 2 x 32768 x 2 x 127 x 128 < 2^31).
 // The int8 tensor rate is twice the fp16 rate on sm_100a (measured 8192 vs 4096 MAC/clk/SM, tools/mma_rate.cu).
 //
-// CTA pair (cluster of 2, cta_group::2): 256 (h) x 128 (k) pixel tile, M = 256, N = 256 ([Re | Im'] of 64 k per CTA
-// half, B rows [-Ws | Wr | Ws]), K = 32 atoms per stage, 6 MMAs per stage:
-//     HH += Xr_hi.B1_hi + Xs_hi.B2_hi,   X += Xr_hi.B1_lo + Xr_lo.B1_hi + Xs_hi.B2_lo + Xs_lo.B2_hi
-// (B1 = [Wr | Ws], B2 = [-Ws | Wr]: D = [Re | Im'], Im' = -Im; the partials hold conj(p) like the fp16 engine).
+// CTA pair (cluster of 2, cta_group::2): M = 256 (each CTA: rows [a | b] of its 64 d), N = 256 (each CTA: B rows
+// [wr | wi] of its 64 k), K = 32 atoms per stage, 3 MMAs per stage:  HH += A_hi.B_hi,  X += A_hi.B_lo + A_lo.B_hi.
 //
-// Producers: 5 groups of 6 warps; group g fills stages i = g mod 5 (6-stage ring, 28 KB per stage; the group count
-// must not exceed the stage count, see the empty-barrier parity note in DESIGN.md 6.1).  A warp thread
-// owns 4 consecutive atoms (one 32-bit word per row and limb plane) and 8 rows spaced 8 apart (X or W), and walks
-// the rows with the angle-addition recurrence X_{m+8} = X_m X_8 (packed FP32x2, 2 ops per phasor; 2 SFU sincos per
-// atom per thread), quantises with one packed magic-number FFMA per phasor (Q16) and packs limb bytes with PRMT.
-// Lanes (quad qq, row mr) write 32 distinct banks per store.  After the last stage, warps 0-7 (two per TMEM lane
-// quarter, splitting the columns) wait for the final MMA commit and drain both accumulators,
-// p = (65536 HH + 256 X) F / 32512^2 (Q16), through a shared-memory tile into row-contiguous global writes: the
-// partial amplitude, or with a single atom chunk the final I = |p|^2 (or p) itself.
+// Producers: NGROUPS groups of 4 warps (2 X warps, 2 W warps: one per 16-atom K half); group g fills stages
+// i = g mod NGROUPS of a STAGES-deep ring (16 KB per stage; the group count must not exceed the stage count, see the
+// empty-barrier parity note in DESIGN.md 6.1).  A warp thread owns 4 consecutive atoms (one 32-bit word per row and
+// limb plane) and 8 rows spaced 8 apart, walks the rows with the angle-addition recurrence X_{m+8} = X_m X_8
+// (packed FP32x2, 2 ops per phasor; 2 SFU sincos per atom per thread), quantises with one packed magic-number FFMA
+// per phasor and packs limb bytes with PRMT.  After the last stage, warps 0-7 drain both accumulators through a
+// shared-memory tile in 4 rounds of 32 k: p-components v = (65536 HH + 256 X) F / 32512^2 in FP32, then the
+// conjugate-pair combination above with row-contiguous global writes of the partial amplitude or, with a single
+// atom chunk, the final I = |p|^2 (or p) itself.
 #include "common.cuh"
 
 namespace xpcs {
 
 namespace ti8 {
-constexpr int TM = 128, TN = 128, KS = 32;          // rows (h) per CTA, pair tile cols (k), atoms per stage
-constexpr int PAIR_M = 2 * TM;
-constexpr int BN = TN / 2;                          // k rows of B per CTA
-constexpr int APLANE = TM * KS;                     // int8 A plane: 128 rows x 32 atoms = 4 KB
-constexpr int BROWS = 3 * BN;                       // [-Ws | Wr | Ws]
-constexpr int BPLANE = BROWS * KS;                  // 6 KB
-constexpr int STAGE_BYTES = 4 * APLANE + 2 * BPLANE;   // Xr_hi Xr_lo Xs_hi Xs_lo | B_hi B_lo = 28 KB
+constexpr int HD = 64;                              // d values per CTA (the pair covers 128 d = 256 h rows)
+constexpr int TM = 2 * HD;                          // A rows per CTA: [a | b]
+constexpr int PAIR_H = 4 * HD;                      // 256 output rows h per pair tile
+constexpr int TN = 128, KS = 32;                    // pair tile cols (k), atoms per stage
+constexpr int BK = TN / 2;                          // k per CTA; B rows per CTA: [wr | wi] = 128
+constexpr int PAIR_M = 2 * TM;                      // MMA M = 256
+constexpr int PLANE = TM * KS;                      // int8 plane: 128 rows x 32 atoms = 4 KB (A and B alike)
+constexpr int HALF_ROWS = HD / 8 * 256;             // byte offset of row 64 in a plane (8-row core groups of 256 B)
+constexpr int STAGE_BYTES = 4 * PLANE;              // A_hi A_lo B_hi B_lo = 16 KB
 #ifndef XPCS_I8_STAGES
-#define XPCS_I8_STAGES 6
+#define XPCS_I8_STAGES 8
 #endif
 constexpr int STAGES = XPCS_I8_STAGES;
 #ifndef XPCS_I8_GROUPS
-#define XPCS_I8_GROUPS 5
+#define XPCS_I8_GROUPS 6
 #endif
-constexpr int NGROUPS = XPCS_I8_GROUPS, GROUP_WARPS = 6;   // per group: 4 X warps (2 quad halves x 2 row halves), 2 W warps
-constexpr int NPROD_WARPS = NGROUPS * GROUP_WARPS;  // 30
+constexpr int NGROUPS = XPCS_I8_GROUPS, GROUP_WARPS = 4;   // per group: 2 X warps, 2 W warps (one per K half)
+static_assert(NGROUPS <= STAGES, "mbarrier parity: producer groups must not exceed the stage count");
+constexpr int NPROD_WARPS = NGROUPS * GROUP_WARPS;
 constexpr int MMA_WARP = NPROD_WARPS;               // producer warps 0-7 (two per TMEM lane quarter) also drain the tile
-constexpr int NTHREADS = (MMA_WARP + 1) * 32;       // 992
+static_assert(NPROD_WARPS >= 8, "the drain needs 8 producer warps");
+constexpr int NTHREADS = (MMA_WARP + 1) * 32;
 constexpr int MMA_N = 2 * TN;                       // 256
 constexpr int TMEM_COLS = 512;                      // HH cols [0, 256), X cols [256, 512)
 constexpr int ASL = 4;                              // atom-record slots per warp (cp.async prefetch distance ASL - 1)
@@ -63,15 +73,23 @@ constexpr int WREC = 16;                            // records a producer warp n
 // both hit distinct banks, one wavefront per instruction
 constexpr int WSLOT = WREC;
 constexpr int ASLOT_BYTES = NPROD_WARPS * ASL * WSLOT * 16;
+constexpr int VLD = 65;                             // drain tile [128 rows][64 + 1] fp32
+static_assert(TM * VLD * 4 <= STAGES * STAGE_BYTES, "drain tile must fit the stage ring");
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + ASLOT_BYTES + 1024 + 256;
 constexpr float MAGIC = 12582912.0f;                // 1.5 * 2^23
-#ifndef XPCS_I8_Q16
-#define XPCS_I8_Q16 1
-#endif
 // Q16 limbs: x = rint(QS v) in [-QS, QS], x = 256 hi + lo with hi in [-127, 127], lo in [-128, 127]; one FFMA
 // t = fma(v, QS, M + 128) holds y = x + 128 in its low 16 bits: byte 1 = hi, byte 0 = lo + 128 (= lo ^ 0x80)
 constexpr float QS = 32512.0f;
 constexpr float QMAGIC = MAGIC + 128.0f;
+// Global rotation: W carries an extra phase GAMMA (turns x 2^32), so both rows of a pair hold q e^{i Gamma} (Gamma =
+// 2 pi GAMMA / 2^32) and the drain rotates it back (ROT_C, ROT_S = cos, sin Gamma).  Without it, X_d and W are exact
+// conjugates (or equals) at q = 0 (X_d = e^{i pi Th_a}, W = e^{-i pi Th_a}), so their limbs' rounding errors -- and
+// the dropped lo.lo' term -- add coherently over all atoms (2e-5 relative on I(0)); with the rotation the limbs of
+// W are those of a rotated copy of X, which decorrelates them (tools/i8_limb_emulation.py).  |p|^2 is unchanged by a
+// global phase.  (Perfect crystals repeat phasor values, so their Bragg peaks keep a coherent limb error of up to
+// ~2e-5: k_fixup.cu recomputes such bright pixels exactly.)
+constexpr uint32_t GAMMA = 0x3147AE14u;             // 0.1925 turns
+constexpr float ROT_C = 0.35347484443612665f, ROT_S = 0.935444030581657f;
 }  // namespace ti8
 
 namespace {
@@ -155,34 +173,12 @@ __device__ __forceinline__ unsigned long long f2mul(unsigned long long a, unsign
 }
 __device__ __forceinline__ unsigned long long swap2(unsigned long long v) { return (v >> 32) | (v << 32); }
 
-#if !XPCS_I8_Q16
-// (c, s) -> limb magic floats: t1 = M + hi (low byte = hi), t2 = M + lo (low byte = lo), element-wise on (c, s).
-// u = M - 254 hi is exact (an integer < 2^24); t2 = fl(32258 v + u) rounds once to the integer grid of M, so
-// t2 = M + rint(32258 v - 254 hi) = M + lo with |lo| <= 127 (|32258 v - 254 hi| = 254 |127 v - hi| <= 127).
-__device__ __forceinline__ void quantise(unsigned long long v, unsigned long long& t1, unsigned long long& t2) {
-    t1 = ffma2(v, pack2(127.0f, 127.0f), pack2(ti8::MAGIC, ti8::MAGIC));          // M + rint(127 v)
-    const unsigned long long u = ffma2(t1, pack2(-254.0f, -254.0f),
-                                       pack2(255.0f * ti8::MAGIC, 255.0f * ti8::MAGIC));   // = M - 254 hi (exact)
-    t2 = ffma2(v, pack2(32258.0f, 32258.0f), u);                                  // M + lo
-}
-// low bytes of four 32-bit words -> one word (byte t = atom t)
-__device__ __forceinline__ uint32_t pack_bytes(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-    return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
-}
-#endif
 // Q16: four magic words (atoms 0..3) -> (hi bytes, lo bytes) words, byte t = atom t
 __device__ __forceinline__ void q16_pack(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3, uint32_t& hi, uint32_t& lo) {
     const uint32_t p01 = __byte_perm(t0, t1, 0x5140), p23 = __byte_perm(t2, t3, 0x5140);   // [b0 b0' b1 b1']
     hi = __byte_perm(p01, p23, 0x7632);
     lo = __byte_perm(p01, p23, 0x5410) ^ 0x80808080u;
 }
-#if !XPCS_I8_Q16
-// per-byte two's-complement negation of four int8 in [-127, 127]
-__device__ __forceinline__ uint32_t neg_bytes(uint32_t w) {
-    const uint32_t n = ~w;
-    return ((n & 0x7F7F7F7Fu) + 0x01010101u) ^ (n & 0x80808080u);
-}
-#endif
 template <int OFF>
 __device__ __forceinline__ void i8_sts(uint32_t addr, uint32_t v) {
     asm volatile("st.shared.b32 [%0+%2], %1;" ::"r"(addr), "r"(v), "n"(OFF));
@@ -204,7 +200,7 @@ __device__ __forceinline__ void i8_sts(uint32_t addr, uint32_t v) {
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ti8::NTHREADS, 1)
 k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t chunk_atoms, int tiles_k,
              float2* __restrict__ partial, int64_t frames, const float* __restrict__ fmax_dev, int dbg_flags,
-             void* __restrict__ direct_out, int out_f64, int mode) {
+             void* __restrict__ direct_out, int out_f64, int mode, BrightSink bs) {
     using namespace ti8;
     extern __shared__ __align__(1024) char smem_raw[];
     char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -217,9 +213,10 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = i8_rank();
     const int ptile = blockIdx.x >> 1;
-    const int th0 = (ptile / tiles_k) * PAIR_M + (int)rank * TM;
+    const int tile_h = ptile / tiles_k;
+    const int64_t H0 = g.h0 + (int64_t)tile_h * PAIR_H;   // first row h of the pair tile; centre c = H0 + 127.5
     const int tk0 = (ptile % tiles_k) * TN;
-    const int bk0 = tk0 + (int)rank * BN;
+    const int bk0 = tk0 + (int)rank * BK;
     const int64_t chunk = blockIdx.y, t = blockIdx.z;
     const int64_t a_begin = chunk * chunk_atoms, a_end = min(N, a_begin + chunk_atoms);
     const int n_stages = (int)((a_end - a_begin + KS - 1) / KS);
@@ -251,19 +248,13 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
                 i8_mbar_wait(&full[s], (uint32_t)((i / STAGES) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t sb = base + s * STAGE_BYTES;
-                const uint64_t xr_h = i8_desc(sb), xr_l = i8_desc(sb + APLANE);
-                const uint64_t xs_h = i8_desc(sb + 2 * APLANE), xs_l = i8_desc(sb + 3 * APLANE);
-                const uint32_t bh = sb + 4 * APLANE, bl = bh + BPLANE;
-                const uint64_t b1_h = i8_desc(bh + BN * KS), b1_l = i8_desc(bl + BN * KS);
-                const uint64_t b2_h = i8_desc(bh), b2_l = i8_desc(bl);
+                const uint64_t a_h = i8_desc(sb), a_l = i8_desc(sb + PLANE);
+                const uint64_t b_h = i8_desc(sb + 2 * PLANE), b_l = i8_desc(sb + 3 * PLANE);
                 const uint32_t acc = i > 0 ? 1u : 0u;
                 if (!(dbg_flags & 4)) {
-                    umma2_i8(tmem, xr_h, b1_h, acc);
-                    umma2_i8(tmem, xs_h, b2_h, 1);
-                    umma2_i8(tmem + 256, xr_h, b1_l, acc);
-                    umma2_i8(tmem + 256, xr_l, b1_h, 1);
-                    umma2_i8(tmem + 256, xs_h, b2_l, 1);
-                    umma2_i8(tmem + 256, xs_l, b2_h, 1);
+                    umma2_i8(tmem, a_h, b_h, acc);          // HH
+                    umma2_i8(tmem + 256, a_h, b_l, acc);    // X
+                    umma2_i8(tmem + 256, a_l, b_h, 1);
                 }
                 i8_commit_both(&empty[s]);
             }
@@ -274,14 +265,19 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
         // ================= producers: group g fills stages g, g + NGROUPS, g + 2 NGROUPS, ... =================
         const int grp = warp / GROUP_WARPS, wi = warp % GROUP_WARPS;
         const int qq = lane & 3, mr = lane >> 2;
-        const bool is_x = wi < 4;
-        const int qh = is_x ? (wi & 1) : wi - 4;              // quad half (K bytes 0-15 or 16-31 of the stage)
-        const int rh = wi >> 1;                               // X warps: row half (rows mr + 8 r, r in [8 rh, 8 rh + 8))
+        const bool is_x = wi < 2;
+        const int qh = wi & 1;                                // K half of the stage (atoms 16 qh .. 16 qh + 15)
         const uint32_t full0 = i8_mapa(su32(full), 0);
-        // every warp prefetches its own 16 atom records (atoms 16 qh .. 16 qh + 15 of each of its stages) with
-        // cp.async into a private ring: no cross-warp barrier per stage
+        // every warp prefetches its own 16 atom records with cp.async into a private ring: no cross-warp barrier
         const uint32_t slot0 = su32(aslot) + (uint32_t)(warp * ASL * WSLOT * 16);
         const float invF = 1.0f / F;
+        // X rows: d = i + 1/2, i = 64 rank + mr + 8 r; phase d Th_a = (2i + 1) Th_a / 2 turns (33-bit product, the
+        // half unit truncated: <= 2^-32 turns).  W rows: k = bk0 + mr + 8 r; phase Th_0 + k Th_b + c Th_a with
+        // c Th_a = (2 H0 + 255) Th_a / 2 turns (the sum with the X phase is h Th_a to within one 2^-32 unit).
+        const uint64_t x_odd = (uint64_t)(2 * ((int)rank * HD + mr) + 1);
+        const uint64_t c_odd = (uint64_t)(2 * H0 + 2 * (PAIR_H / 2) - 1);
+        const uint32_t kk = (uint32_t)(g.k0 + bk0 + mr);
+        const uint32_t pbase = (uint32_t)((is_x ? 0 : 2 * PLANE) + qh * 128 + mr * 16 + qq * 4);
         auto prefetch = [&](int li) {   // local stage li of this group -> slot li % ASL of this warp
             const int i = grp + li * NGROUPS;
             if (i < n_stages && lane < WREC) {
@@ -301,154 +297,59 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
             asm volatile("cp.async.wait_group %0;" ::"n"(ti8::ASL - 2) : "memory");
             __syncwarp();                 // the warp's records of stage i are visible to all its lanes; every lane has
             prefetch(li + ASL - 1);       // finished reading slot (li - 1) % ASL, which is refilled now
-            uint4 at[4];
+            unsigned long long v[4], st[4];
             {
-                // only the fields this warp uses: X warps Th_a, W warps (Th_b, Th_0, f)
                 const uint32_t ra = slot0 + (uint32_t)((li % ASL) * WSLOT * 16);
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const uint32_t a = ra + (uint32_t)((((4 * qq + u) ^ (qq & 2))) * 16);   // record 4 qq + u
-                    if (is_x) {
-                        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(at[u].x) : "r"(a));
-                        at[u].y = at[u].z = at[u].w = 0u;
-                    } else {
-                        at[u].x = 0u;
-                        asm volatile("ld.shared.u32 %0, [%1+4];" : "=r"(at[u].y) : "r"(a));
-                        asm volatile("ld.shared.u32 %0, [%1+8];" : "=r"(at[u].z) : "r"(a));
-                        asm volatile("ld.shared.u32 %0, [%1+12];" : "=r"(at[u].w) : "r"(a));
+                    uint32_t tha, thb = 0u, th0 = 0u, fw = 0u;
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tha) : "r"(a));
+                    if (!is_x) {
+                        asm volatile("ld.shared.u32 %0, [%1+4];" : "=r"(thb) : "r"(a));
+                        asm volatile("ld.shared.u32 %0, [%1+8];" : "=r"(th0) : "r"(a));
+                        asm volatile("ld.shared.u32 %0, [%1+12];" : "=r"(fw) : "r"(a));
                     }
+                    float s0, c0, s1, c1;
+                    if (is_x) {
+                        __sincosf(turns_to_radians((uint32_t)((x_odd * tha) >> 1)), &s0, &c0);
+                        __sincosf(turns_to_radians(8u * tha), &s1, &c1);
+                        v[u] = pack2(c0, s0);
+                    } else {
+                        const uint32_t tc = (uint32_t)((c_odd * tha) >> 1);
+                        __sincosf(turns_to_radians(th0 + kk * thb + tc + GAMMA), &s0, &c0);
+                        __sincosf(turns_to_radians(8u * thb), &s1, &c1);
+                        const float fs = __uint_as_float(fw) * invF;
+                        v[u] = pack2(fs * c0, fs * s0);
+                    }
+                    st[u] = pack2(c1, s1);
                 }
             }
             i8_mbar_wait(&empty[s], (uint32_t)(((i / STAGES) + 1) & 1));
-            const uint32_t sbase = su32(smem) + (uint32_t)(s * STAGE_BYTES);
             if (!(dbg_flags & 2)) {
-                if (is_x) {
-                    // X rows m = mr + 8 r (8 rh <= r < 8 rh + 8) of this CTA's 128: X_m = e^{-2 pi i h Th_a}, h = h0 + th0 + m
-                    const uint32_t h = (uint32_t)(g.h0 + th0 + mr + 64 * rh);
-                    unsigned long long v[4], st[4];
+                // rows m = mr + 8 r: real parts (a | wr) into rows m of the hi/lo planes, imaginary parts (b | wi) into
+                // rows 64 + m
+                const uint32_t a0 = su32(smem) + (uint32_t)(s * STAGE_BYTES) + pbase;
+                const unsigned long long QS2 = pack2(QS, QS), QM2 = pack2(QMAGIC, QMAGIC);
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    uint32_t tc[4], ts[4];
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
-                        float s0, c0, s1, c1;
-                        __sincosf(turns_to_radians(h * at[u].x), &s0, &c0);
-                        __sincosf(turns_to_radians(8u * at[u].x), &s1, &c1);
-                        v[u] = pack2(c0, s0);
-                        st[u] = pack2(c1, s1);
+                        const unsigned long long tq = ffma2(v[u], QS2, QM2);
+                        tc[u] = (uint32_t)tq; ts[u] = (uint32_t)(tq >> 32);
+                        const unsigned long long cd = pack2(lo2(st[u]), lo2(st[u]));
+                        const unsigned long long sd = pack2(-hi2(st[u]), hi2(st[u]));
+                        v[u] = ffma2(swap2(v[u]), sd, f2mul(v[u], cd));
                     }
-                    const uint32_t a0 = sbase + (uint32_t)(qh * 128 + mr * 16 + qq * 4 + rh * 8 * 256);
-#if XPCS_I8_Q16
-                    const unsigned long long QS2 = pack2(QS, QS), QM2 = pack2(QMAGIC, QMAGIC);
-#pragma unroll
-                    for (int r = 0; r < 8; ++r) {
-                        uint32_t tc[4], ts[4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const unsigned long long tq = ffma2(v[u], QS2, QM2);
-                            tc[u] = (uint32_t)tq; ts[u] = (uint32_t)(tq >> 32);
-                            const unsigned long long cd = pack2(lo2(st[u]), lo2(st[u]));
-                            const unsigned long long sd = pack2(-hi2(st[u]), hi2(st[u]));
-                            v[u] = ffma2(swap2(v[u]), sd, f2mul(v[u], cd));
-                        }
-                        uint32_t xrh, xrl, xsh, xsl;
-                        q16_pack(tc[0], tc[1], tc[2], tc[3], xrh, xrl);
-                        q16_pack(ts[0], ts[1], ts[2], ts[3], xsh, xsl);
-                        const uint32_t ad = a0 + (uint32_t)(r * 256);
-                        i8_sts<0 * APLANE>(ad, xrh);
-                        i8_sts<1 * APLANE>(ad, xrl);
-                        i8_sts<2 * APLANE>(ad, xsh);
-                        i8_sts<3 * APLANE>(ad, xsl);
-                    }
-#else
-#pragma unroll
-                    for (int r = 0; r < 8; ++r) {
-                        uint32_t hc[4], lc[4], hs[4], ls[4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            unsigned long long t1, t2;
-                            quantise(v[u], t1, t2);
-                            hc[u] = (uint32_t)t1; hs[u] = (uint32_t)(t1 >> 32);
-                            lc[u] = (uint32_t)t2; ls[u] = (uint32_t)(t2 >> 32);
-                            // angle addition: (c, s) <- (c cd - s sd, s cd + c sd)
-                            const unsigned long long cd = pack2(lo2(st[u]), lo2(st[u]));
-                            const unsigned long long sd = pack2(-hi2(st[u]), hi2(st[u]));
-                            v[u] = ffma2(swap2(v[u]), sd, f2mul(v[u], cd));
-                        }
-                        const uint32_t ad = a0 + (uint32_t)(r * 256);
-                        i8_sts<0 * APLANE>(ad, pack_bytes(hc[0], hc[1], hc[2], hc[3]));
-                        i8_sts<1 * APLANE>(ad, pack_bytes(lc[0], lc[1], lc[2], lc[3]));
-                        i8_sts<2 * APLANE>(ad, pack_bytes(hs[0], hs[1], hs[2], hs[3]));
-                        i8_sts<3 * APLANE>(ad, pack_bytes(ls[0], ls[1], ls[2], ls[3]));
-                    }
-#endif
-                } else {
-                    // W rows k = mr + 8 r (r < 8) of this CTA's 64: W_k = (f / F) e^{-2 pi i (Th_0 + kk Th_b)}
-                    const uint32_t kk = (uint32_t)(g.k0 + bk0 + mr);
-                    unsigned long long v[4], st[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        float s0, c0, s1, c1;
-                        __sincosf(turns_to_radians(at[u].z + kk * at[u].y), &s0, &c0);
-                        __sincosf(turns_to_radians(8u * at[u].y), &s1, &c1);
-                        const float fs = __uint_as_float(at[u].w) * invF;
-                        v[u] = pack2(fs * c0, fs * s0);
-                        st[u] = pack2(c1, s1);
-                    }
-                    const uint32_t a0 = sbase + (uint32_t)(4 * APLANE + qh * 128 + mr * 16 + qq * 4);
-#if XPCS_I8_Q16
-                    const unsigned long long QS2 = pack2(QS, QS), QM2 = pack2(QMAGIC, QMAGIC);
-#pragma unroll
-                    for (int r = 0; r < 8; ++r) {
-                        uint32_t tc[4], ts[4], tn[4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const unsigned long long tq = ffma2(v[u], QS2, QM2);
-                            tc[u] = (uint32_t)tq; ts[u] = (uint32_t)(tq >> 32);
-                            // -Ws limbs from rint(-QS s) = -rint(QS s) (lo = -128 has no int8 negation)
-                            tn[u] = __float_as_uint(fmaf(hi2(v[u]), -QS, QMAGIC));
-                            const unsigned long long cd = pack2(lo2(st[u]), lo2(st[u]));
-                            const unsigned long long sd = pack2(-hi2(st[u]), hi2(st[u]));
-                            v[u] = ffma2(swap2(v[u]), sd, f2mul(v[u], cd));
-                        }
-                        uint32_t whr, wlr, whs, wls, nhs, nls;
-                        q16_pack(tc[0], tc[1], tc[2], tc[3], whr, wlr);
-                        q16_pack(ts[0], ts[1], ts[2], ts[3], whs, wls);
-                        q16_pack(tn[0], tn[1], tn[2], tn[3], nhs, nls);
-                        const uint32_t ad = a0 + (uint32_t)(r * 256);
-                        // B rows: -Ws at k, Wr at BN + k, Ws at 2 BN + k  (BN rows = 8 groups of 256 B)
-                        i8_sts<0>(ad, nhs);
-                        i8_sts<BPLANE>(ad, nls);
-                        i8_sts<8 * 256>(ad, whr);
-                        i8_sts<BPLANE + 8 * 256>(ad, wlr);
-                        i8_sts<16 * 256>(ad, whs);
-                        i8_sts<BPLANE + 16 * 256>(ad, wls);
-                    }
-#else
-#pragma unroll
-                    for (int r = 0; r < 8; ++r) {
-                        uint32_t hc[4], lc[4], hs[4], ls[4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            unsigned long long t1, t2;
-                            quantise(v[u], t1, t2);
-                            hc[u] = (uint32_t)t1; hs[u] = (uint32_t)(t1 >> 32);
-                            lc[u] = (uint32_t)t2; ls[u] = (uint32_t)(t2 >> 32);
-                            const unsigned long long cd = pack2(lo2(st[u]), lo2(st[u]));
-                            const unsigned long long sd = pack2(-hi2(st[u]), hi2(st[u]));
-                            v[u] = ffma2(swap2(v[u]), sd, f2mul(v[u], cd));
-                        }
-                        const uint32_t whr = pack_bytes(hc[0], hc[1], hc[2], hc[3]);
-                        const uint32_t wlr = pack_bytes(lc[0], lc[1], lc[2], lc[3]);
-                        const uint32_t whs = pack_bytes(hs[0], hs[1], hs[2], hs[3]);
-                        const uint32_t wls = pack_bytes(ls[0], ls[1], ls[2], ls[3]);
-                        const uint32_t ad = a0 + (uint32_t)(r * 256);
-                        // B rows: -Ws at k, Wr at BN + k, Ws at 2 BN + k  (BN rows = 8 groups of 256 B)
-                        i8_sts<0>(ad, neg_bytes(whs));
-                        i8_sts<BPLANE>(ad, neg_bytes(wls));
-                        i8_sts<8 * 256>(ad, whr);
-                        i8_sts<BPLANE + 8 * 256>(ad, wlr);
-                        i8_sts<16 * 256>(ad, whs);
-                        i8_sts<BPLANE + 16 * 256>(ad, wls);
-                    }
-#endif
+                    uint32_t rh, rl, ih, il;
+                    q16_pack(tc[0], tc[1], tc[2], tc[3], rh, rl);
+                    q16_pack(ts[0], ts[1], ts[2], ts[3], ih, il);
+                    const uint32_t ad = a0 + (uint32_t)(r * 256);
+                    i8_sts<0>(ad, rh);
+                    i8_sts<PLANE>(ad, rl);
+                    i8_sts<HALF_ROWS>(ad, ih);
+                    i8_sts<PLANE + HALF_ROWS>(ad, il);
                 }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -458,97 +359,74 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
         asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     if (warp < 8) {
-        // ================= drain (warps 0-7 after production): exact int32 accumulators -> fp32 partial tile ======
-        // warp w reads TMEM lane quarter w % 4 (the tcgen05.ld lane restriction) and column half w / 4
-        const int quarter = warp & 3, half = warp >> 2;
+        // ================= drain (warps 0-7 after production): exact int32 accumulators -> pixels ==================
+        // warp w reads TMEM lane quarter w % 4 (the tcgen05.ld lane restriction): lanes 0-63 are the a rows, 64-127
+        // the b rows of this CTA's 64 d; w / 4 selects the wr or wi columns.  Four rounds of 32 k: the 128 x 64
+        // component tile goes through shared memory (the stage ring is free once `done` fired: every MMA has read
+        // its operands), then all 256 threads combine a/b rows into the conjugate pair and write pixel rows
+        // contiguously.
+        const int quarter = warp & 3, part = warp >> 2;
         i8_mbar_wait(done, 0);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16);
         const int row = quarter * 32 + lane;
         const int64_t n_q = g.n_h * g.n_k;
         float2* P = partial + (chunk * frames + t) * n_q;
-        // p = (64516 HH + 254 X) F / 32258^2 in FP32 (the partial is fp32; |rounding| <= 2^-23 |p|).  The tile goes
-        // through shared memory (the stage ring is free once `done` fired: every MMA has read its operands) so that
-        // the global writes are row-contiguous: TMEM lane = pixel row, so direct stores would touch 32 rows per
-        // instruction.  Layout [128 rows][64 float4 + 1 pad] (pixel pairs; the pad makes the float4 writes of a
-        // warp's 32 rows conflict-free).
-#if XPCS_I8_Q16
-        const float c_hh = (float)(65536.0 * (double)F / (32512.0 * 32512.0));   // p = (65536 HH + 256 X) F / QS^2
+        const float c_hh = (float)(65536.0 * (double)F / (32512.0 * 32512.0));   // v = (65536 HH + 256 X) F / QS^2
         const float c_x = (float)(256.0 * (double)F / (32512.0 * 32512.0));
-#else
-        const float c_hh = (float)(64516.0 * (double)F / (32258.0 * 32258.0));
-        const float c_x = (float)(254.0 * (double)F / (32258.0 * 32258.0));
-#endif
-        float4* tile = reinterpret_cast<float4*>(smem);
-        constexpr int TLD = TN / 2 + 1;
+        float* V = reinterpret_cast<float*>(smem);
+        const int tid = threadIdx.x, ol = tid & 31, ow = tid >> 5;   // 0..255
+        const int64_t ih_base = (int64_t)tile_h * PAIR_H + PAIR_H / 2;   // output row of h = c + 1/2
+        const double F_bright = bs.count ? bright_F(bs) : 1.0;
 #pragma unroll 1
-        for (int kb = 8 * half; kb < 8 * half + 8; ++kb) {     // 8 pixel columns per step (32 registers of TMEM data)
-            const uint32_t cre = (uint32_t)(kb < 8 ? 8 * kb : 8 * kb + 64);   // [Re k<64 | Im' k<64 | Re k>=64 | Im' k>=64]
-            uint32_t hre[8], him[8], xre[8], xim[8];
-            I8_TMEM_LD8(tb + cre, hre);
-            I8_TMEM_LD8(tb + cre + 64, him);
-            I8_TMEM_LD8(tb + 256 + cre, xre);
-            I8_TMEM_LD8(tb + 256 + cre + 64, xim);
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        for (int kc = 0; kc < TN / 32; ++kc) {
+            const uint32_t col0 = (uint32_t)(128 * (kc >> 1) + 64 * part + 32 * (kc & 1));
 #pragma unroll
-            for (int j = 0; j < 8; j += 2) {
-                float4 v;
-                v.x = fmaf((float)(int32_t)hre[j], c_hh, (float)(int32_t)xre[j] * c_x);
-                v.y = fmaf((float)(int32_t)him[j], c_hh, (float)(int32_t)xim[j] * c_x);
-                v.z = fmaf((float)(int32_t)hre[j + 1], c_hh, (float)(int32_t)xre[j + 1] * c_x);
-                v.w = fmaf((float)(int32_t)him[j + 1], c_hh, (float)(int32_t)xim[j + 1] * c_x);
-                tile[row * TLD + 4 * kb + j / 2] = v;
+            for (int sub = 0; sub < 2; ++sub) {
+                uint32_t hh[16], xx[16];
+                I8_TMEM_LD16(tb + col0 + 16 * sub, hh);
+                I8_TMEM_LD16(tb + 256 + col0 + 16 * sub, xx);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    V[row * VLD + 32 * part + 16 * sub + j] = fmaf((float)(int32_t)hh[j], c_hh, (float)(int32_t)xx[j] * c_x);
             }
-        }
-        asm volatile("bar.sync 1, 256;" ::: "memory");   // drain warps 0-7 only
-        const int tid = threadIdx.x;                     // 0..255
-        const int rows = (int)min((int64_t)TM, g.n_h - th0), cols = (int)min((int64_t)TN, g.n_k - tk0);
-        const bool vec = (g.n_k & 1) == 0;               // 16-B aligned pixel pairs
-        if (direct_out == nullptr) {
-            for (int e = tid; e < TM * (TN / 2); e += 256) {
-                const int r = e / (TN / 2), c2 = e % (TN / 2);
-                if (r >= rows || 2 * c2 >= cols) continue;
-                const float4 v = tile[r * TLD + c2];
-                float2* dst = P + (int64_t)(th0 + r) * g.n_k + tk0 + 2 * c2;
-                if (vec && 2 * c2 + 1 < cols) *reinterpret_cast<float4*>(dst) = v;
-                else {
-                    dst[0] = make_float2(v.x, v.y);
-                    if (2 * c2 + 1 < cols) dst[1] = make_float2(v.z, v.w);
-                }
-            }
-        } else {
-            // single atom chunk: the final result straight from the tile, with the arithmetic of k_amp_reduce for
-            // C = 1 (FP64 |p|^2 of the fp32 amplitude, Eq. 8; or the amplitude p = conj of the accumulated value)
-            for (int e = tid; e < TM * (TN / 2); e += 256) {
-                const int r = e / (TN / 2), c2 = e % (TN / 2);
-                if (r >= rows || 2 * c2 >= cols) continue;
-                const float4 v = tile[r * TLD + c2];
-                const bool two = 2 * c2 + 1 < cols;
-                const int64_t i0 = t * n_q + (int64_t)(th0 + r) * g.n_k + tk0 + 2 * c2;
-                if (mode == 0) {
-                    const double I0 = (double)v.x * (double)v.x + (double)v.y * (double)v.y;
-                    const double I1 = (double)v.z * (double)v.z + (double)v.w * (double)v.w;
-                    if (out_f64) {
-                        double* o = (double*)direct_out + i0;
-                        o[0] = I0;
-                        if (two) o[1] = I1;
-                    } else {
-                        float* o = (float*)direct_out + i0;
-                        if (two && vec) *reinterpret_cast<float2*>(o) = make_float2((float)I0, (float)I1);
-                        else { o[0] = (float)I0; if (two) o[1] = (float)I1; }
-                    }
-                } else {
-                    if (out_f64) {
-                        double* o = (double*)direct_out + 2 * i0;
-                        o[0] = (double)v.x; o[1] = -(double)v.y;
-                        if (two) { o[2] = (double)v.z; o[3] = -(double)v.w; }
-                    } else {
-                        float* o = (float*)direct_out + 2 * i0;
-                        if (two && vec) *reinterpret_cast<float4*>(o) = make_float4(v.x, -v.y, v.z, -v.w);
-                        else { o[0] = v.x; o[1] = -v.y; if (two) { o[2] = v.z; o[3] = -v.w; } }
+            asm volatile("bar.sync 1, 256;" ::: "memory");   // drain warps 0-7 only
+            const int64_t col = tk0 + 32 * kc + ol;
+            if (col < g.n_k) {
+#pragma unroll 2
+                for (int jj = 0; jj < HD / 8; ++jj) {
+                    const int dl = ow + 8 * jj;
+                    const float AR = V[dl * VLD + ol], AI = V[dl * VLD + 32 + ol];
+                    const float BR = V[(HD + dl) * VLD + ol], BI = V[(HD + dl) * VLD + 32 + ol];
+                    const int di = (int)rank * HD + dl;
+#pragma unroll
+                    for (int sg = 0; sg < 2; ++sg) {
+                        const int64_t ih = sg == 0 ? ih_base + di : ih_base - 1 - di;   // h = c + d, c - d
+                        if (ih >= g.n_h) continue;
+                        const float rr = sg == 0 ? AR - BI : AR + BI;
+                        const float ri = sg == 0 ? AI + BR : AI - BR;
+                        const float re = fmaf(rr, ROT_C, ri * ROT_S), im = fmaf(ri, ROT_C, -rr * ROT_S);   // q = x e^{-i Gamma}
+                        const int64_t idx = ih * g.n_k + col;
+                        if (direct_out == nullptr) {
+                            P[idx] = make_float2(re, im);
+                            continue;
+                        }
+                        bright_append(bs, (double)re * (double)re + (double)im * (double)im, F_bright, t * n_q + idx);
+                        if (mode == 0) {
+                            // single atom chunk: the fold's arithmetic for C = 1 (FP64 |p|^2 of the fp32 amplitude)
+                            const double I = (double)re * (double)re + (double)im * (double)im;
+                            if (out_f64) ((double*)direct_out)[t * n_q + idx] = I;
+                            else ((float*)direct_out)[t * n_q + idx] = (float)I;
+                        } else {
+                            // the amplitude p = conj(q)
+                            if (out_f64) { double* o = (double*)direct_out + 2 * (t * n_q + idx); o[0] = re; o[1] = -(double)im; }
+                            else *reinterpret_cast<float2*>((float*)direct_out + 2 * (t * n_q + idx)) = make_float2(re, -im);
+                        }
                     }
                 }
             }
+            asm volatile("bar.sync 1, 256;" ::: "memory");
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -601,11 +479,11 @@ int i8_cluster_slots() {
 
 cudaError_t launch_lattice_i8(const uint4* staged, int64_t N, int64_t frames, const LatticeGeom& g, int64_t chunk_atoms,
                               int64_t n_chunks, float* fmax_scratch, int uniform_f, float2* partial, cudaStream_t s,
-                              void* direct_out, int out_f64, int mode) {
+                              void* direct_out, int out_f64, int mode, const BrightSink* bright) {
     if (direct_out && n_chunks != 1) return cudaErrorInvalidValue;
     using namespace ti8;
     if (chunk_atoms > kI8MaxChunk) return cudaErrorInvalidValue;
-    const int tiles_h = (int)((g.n_h + PAIR_M - 1) / PAIR_M), tiles_k = (int)((g.n_k + TN - 1) / TN);
+    const int tiles_h = (int)((g.n_h + PAIR_H - 1) / PAIR_H), tiles_k = (int)((g.n_k + TN - 1) / TN);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_lattice_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
@@ -623,7 +501,8 @@ cudaError_t launch_lattice_i8(const uint4* staged, int64_t N, int64_t frames, co
     dim3 grid(2 * tiles_h * tiles_k, (unsigned)n_chunks, (unsigned)frames);
     note_launch();
     k_lattice_i8<<<grid, NTHREADS, SMEM_BYTES, s>>>(staged, N, g, chunk_atoms, tiles_k, partial, frames, fm, dbg,
-                                                    direct_out, out_f64, mode);
+                                                    direct_out, out_f64, mode,
+                                                    bright ? *bright : BrightSink{nullptr, nullptr, 0.0, nullptr});
     return cudaGetLastError();
 }
 

@@ -14,12 +14,12 @@ namespace xpcs {
 template <typename P, typename Fq, typename O>
 __global__ void __launch_bounds__(256) k_species_combine(SpeciesParts sp, int64_t total, int64_t n_q,
                                                          const Fq* __restrict__ fq, int64_t v0, int64_t n_l,
-                                                         O* __restrict__ out, int mode) {
+                                                         O* __restrict__ out, int mode, BrightSink bs) {
     const int64_t fq_stride = n_l * n_q;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t v = i / n_q, q = i - v * n_q;
         const int64_t row = ((v0 + v) % n_l) * n_q + q;
-        double re = 0.0, im = 0.0;
+        double re = 0.0, im = 0.0, F = 0.0;
         for (int s = 0; s < sp.n; ++s) {
             const P* part = (const P*)sp.part[s];
             double pr = 0.0, pi = 0.0;
@@ -31,9 +31,11 @@ __global__ void __launch_bounds__(256) k_species_combine(SpeciesParts sp, int64_
             const double f = (double)fq[(int64_t)sp.kind[s] * fq_stride + row];
             re += f * pr;
             im += f * pi;
+            F = fmax(F, fabs(f));
         }
         if (mode == 0) out[i] = (O)(re * re + im * im);
         else { out[2 * i] = (O)re; out[2 * i + 1] = (O)(mode == 2 ? -im : im); }
+        bright_append(bs, re * re + im * im, F, i);
     }
 }
 
@@ -74,11 +76,13 @@ static dim3 grid_n(int64_t total) {
 }
 
 cudaError_t launch_species_combine(const SpeciesParts& sp, int64_t frames, int64_t n_q, const void* fq, int fq_f64,
-                                   int64_t v0, int64_t n_l, void* out, int out_f64, int mode, cudaStream_t s) {
+                                   int64_t v0, int64_t n_l, void* out, int out_f64, int mode, cudaStream_t s,
+                                   const BrightSink* bright) {
     const int64_t total = frames * n_q;
     const dim3 gr = grid_n(total);
+    const BrightSink bs = bright ? *bright : BrightSink{nullptr, nullptr, 0.0, nullptr};
     note_launch();
-#define XPCS_SPC(P, F, O) k_species_combine<P, F, O><<<gr, 256, 0, s>>>(sp, total, n_q, (const F*)fq, v0, n_l, (O*)out, mode)
+#define XPCS_SPC(P, F, O) k_species_combine<P, F, O><<<gr, 256, 0, s>>>(sp, total, n_q, (const F*)fq, v0, n_l, (O*)out, mode, bs)
     if (sp.part_f64) {
         if (fq_f64) { if (out_f64) XPCS_SPC(double2, double, double); else XPCS_SPC(double2, double, float); }
         else { if (out_f64) XPCS_SPC(double2, float, double); else XPCS_SPC(double2, float, float); }

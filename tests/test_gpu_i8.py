@@ -85,19 +85,33 @@ def test_i8_amplitude_volume_and_species():
     assert np.max(np.abs(I - Iref) / (1e-3 * S2 + 1e-5 * Iref)) <= 1.0
 
 
-@pytest.mark.parametrize("kind,n_cells", [("fcc", 20), ("sc", 32)])
-def test_i8_bragg(kind, n_cells):
-    """Perfect crystals at c2/c3-class N: I = N^2 on the crystal's reciprocal lattice, ~0 elsewhere."""
+@pytest.mark.parametrize("kind,n_cells,shift", [("fcc", 20, False), ("sc", 32, False), ("fcc", 20, True),
+                                                 ("sc", 32, True), ("bcc", 16, True)])
+def test_i8_bragg(kind, n_cells, shift):
+    """Perfect crystals at c2/c3-class N, at the origin and rigidly shifted (PBC): I = N^2 on the
+    crystal's reciprocal lattice within the per-pixel gate (|dI| <= 1e-3 N + 1e-5 I, R11), ~0 elsewhere.
+    A crystal repeats few phasor values, so the integer engine's limb errors add coherently at its peaks; the
+    bright-pixel recompute (k_fixup.cu) must bring them to the gate."""
     L = 40.0
-    pos = xi.crystal(kind, n_cells, L, "f32")
+    pos = xi.crystal(kind, n_cells, L, "f64")
+    if shift:
+        pos = np.mod(pos + np.array([3.3170, 11.0731, 27.6006]), L)
+    pos = pos.astype(np.float32)
     N = pos.shape[0]
     n = 256
     I = xp.xpcs_intensity_grid(_t(pos[None]), None, xp.lattice_plane(L, n), engine=I8).cpu().numpy()[0].reshape(n, n)
-    period = 2 * n_cells if kind == "fcc" else n_cells
     h = np.arange(-n // 2, n // 2)
     H, K = np.meshgrid(h, h, indexing="ij")
-    peak = (H % period == 0) & (K % period == 0)
-    np.testing.assert_allclose(I[peak], float(N) ** 2, rtol=2e-5)
+    if kind == "fcc":      # F = 1 + (-1)^(H+K) + (-1)^H + (-1)^K on l = 0: H, K both even
+        peak = (H % (2 * n_cells) == 0) & (K % (2 * n_cells) == 0)
+    elif kind == "bcc":    # F = 1 + (-1)^(H+K): H + K even
+        peak = (H % n_cells == 0) & (K % n_cells == 0) & ((H // n_cells + K // n_cells) % 2 == 0)
+    else:
+        peak = (H % n_cells == 0) & (K % n_cells == 0)
+    qp = (2 * np.pi / L) * np.stack([H[peak], K[peak], np.zeros(peak.sum())], -1).astype(np.float64)
+    ref = oracle.intensity(pos.astype(np.float64), None, qp, L)[0]
+    np.testing.assert_allclose(ref, float(N) ** 2, rtol=1e-6)     # the oracle's own Bragg pin at these positions
+    assert_pixels(I[peak], ref, N, f"{kind}{n_cells} shift={shift} peaks")
     assert np.max(I[~peak]) < 1e-3 * N
 
 
