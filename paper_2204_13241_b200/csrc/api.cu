@@ -427,9 +427,9 @@ static int validate_volume(const xpcs_qvolume* vol) {
     return XPCS_OK;
 }
 
-static bool i8_fixup_enabled() {
+static bool fixup_enabled() {
     static int on = -1;
-    if (on < 0) { const char* e = getenv("XPCS_I8_FIXUP"); on = (e && atoi(e) == 0) ? 0 : 1; }   // experiments only
+    if (on < 0) { const char* e = getenv("XPCS_FIXUP"); on = (e && atoi(e) == 0) ? 0 : 1; }   // experiments only
     return on == 1;
 }
 
@@ -653,7 +653,7 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
             // ~15 stages for the prologue, the single drain and the cluster teardown); the smallest C wins ties.
             ch = i8_plan_chunk(Ng, i8_tiles(g) * V, nullptr);
         } else if (g_tc) {
-            const int64_t tiles = ((g.n_h + 127) / 128) * ((g.n_k + 127) / 128);
+            const int64_t tiles = ((g.n_h + 255) / 256) * ((g.n_k + 127) / 128);
             const int64_t units = tiles * std::min<int64_t>(V, 64);
             int64_t C0 = std::max<int64_t>(1, (8LL * sm_count() + units - 1) / units);
             C0 = std::min<int64_t>(C0, std::max<int64_t>(1, Ng / 1024));
@@ -698,14 +698,14 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
     float2* part = (float2*)scratch(o.s, SS_PARTIAL, sizeof(float2) * (size_t)part_elems);
     if (!st || !part) return XPCS_ENOMEM;
     float* fmax = nullptr;
-    if (i8 && form_factors) {
+    if ((i8 || tc) && form_factors) {
         fmax = (float*)scratch(o.s, SS_SMALL, 64);
         if (!fmax) return XPCS_ENOMEM;
     }
     // the tensor engines' partials hold conj(p) (R1)
     const int mode = amp ? ((tc || i8) ? 2 : 1) : 0;
     void* fbuf = nullptr;
-    if (i8 && i8_fixup_enabled()) {
+    if ((i8 || tc) && fixup_enabled()) {
         int64_t vb_max = 0;
         for (const FrameBatch& fb : batches) vb_max = std::max(vb_max, fb.vb);
         fbuf = scratch(o.s, SS_FIX, fixup_scratch_bytes(vb_max, n_q, N));
@@ -718,12 +718,11 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
         // one integer-engine group in a single atom chunk: the kernel writes the result itself (no partial planes)
         const bool direct = ng == 1 && !G.n_species && i8 && gi8[0] && G.cnt[0] > 0 && C[0] == 1 &&
                             !(getenv("XPCS_I8_DIRECT") && atoi(getenv("XPCS_I8_DIRECT")) == 0);
-        // the integer engine's 16-bit limbs add coherently on perfect crystals: the epilogue lists the brightest
-        // pixels and k_fixup.cu recomputes them exactly
-        bool batch_i8 = false;
-        for (int gi = 0; gi < ng; ++gi) batch_i8 = batch_i8 || (i8 && gi8[(size_t)gi] && G.cnt[gi] > 0);
+        // the tensor engines' errors add coherently where the phasors repeat (q = 0 and the Bragg peaks of perfect
+        // crystals: the integer engine's 16-bit limbs, the split-FP16 engine's truncating FP32 accumulator): the
+        // epilogue lists the brightest pixels and k_fixup.cu recomputes them exactly
+        const bool fix = (i8 || tc) && fbuf;
         BrightSink bs{nullptr, nullptr, 0.0, nullptr};
-        const bool fix = batch_i8 && fbuf;
         if (fix) TRY(cuda_fail(fixup_prepare(fbuf, N, form_factors ? fmax : nullptr, bs, o.s), "bright-pixel list"));
         int64_t stoff = 0, poff = 0;
         for (int gi = 0; gi < ng; ++gi) {
@@ -740,7 +739,10 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
                                                       part + poff, o.s, direct ? dst : nullptr, o.out_f64, mode,
                                                       (fix && direct) ? &bs : nullptr),
                                     "lattice tcgen05 i8"));
-              else if (g_tc) TRY(cuda_fail(launch_lattice_tc(st + stoff, Ng, vb, g, chunk[gi], C[gi], part + poff, o.s), "lattice tcgen05"));
+              else if (g_tc) {
+                  if (fmax) TRY(cuda_fail(launch_absmax_f(st + stoff, Ng, fmax, o.s), "max |f|"));   // the fix-up threshold
+                  TRY(cuda_fail(launch_lattice_tc(st + stoff, Ng, vb, g, chunk[gi], C[gi], part + poff, o.s), "lattice tcgen05"));
+              }
               else TRY(cuda_fail(launch_lattice_simt(st + stoff, Ng, vb, g, chunk[gi], C[gi], part + poff, o.s), "lattice simt")); }
             stoff += Ng * vb;
             poff += C[gi] * n_q * vb;

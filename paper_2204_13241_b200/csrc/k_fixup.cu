@@ -1,15 +1,16 @@
-// k_fixup.cu -- exact recompute of the brightest pixels after the integer engine (k_lattice_i8.cu).
+// k_fixup.cu -- exact recompute of the brightest pixels after the tensor engines (k_lattice_i8.cu, k_lattice_tc.cu).
 //
-// The integer engine's phasors are 16-bit fixed point (two int8 limbs).  For disordered frames the limb errors are
-// independent across atoms and add like a random walk (rms |dI| ~ 3e-5 N), but a PERFECT crystal
-// repeats a few phasor values over all atoms, so at its Bragg peaks the errors add coherently: up to ~2e-5 of I
-// (tools/i8_limb_emulation.py), above the 1e-5 relative branch of the per-pixel gate (R11), which only
-// matters where I > 100 N.  So every pixel whose intensity exceeds
+// The tensor engines' per-term errors are independent across atoms for disordered frames and add like a random walk
+// (rms |dI| ~ 3e-5 N), but where the phasors repeat -- q = 0 of any frame, where the conjugate-pair
+// factors X_d and W are conjugates for every atom, and the Bragg peaks of a PERFECT crystal -- they add coherently:
+// the integer engine's 16-bit limbs up to ~2e-5 of I (tools/i8_limb_emulation.py), the split-FP16 engine's
+// truncating FP32 TMEM accumulator ~1.5e-5; both above the 1e-5 relative branch of the per-pixel gate (DESIGN.md
+// R11), which only matters where I > 100 N.  So every pixel whose intensity exceeds
 //     thresh(q) = min(64 N, N^2 / 4) * F(q)^2,   F(q) = max |f| of the call's atoms at q,
 // is recomputed here by the plain Eq.(7)/(8) sum over the staged atoms: exact 32-bit phase turns
-// -> sincospi (FP32, ~1 ulp per term, ~1e-7 of I even when coherent) -> FP64 sums, one block per pixel with a
-// fixed-order reduction (deterministic).  A disordered frame has no such pixel except q = 0 (I = (sum f)^2;
-// P(I > 64 <I>) = e^-64), so the cost is one N-atom sum per frame plus a read of I; a crystal adds its Bragg peaks.
+// -> sincospi (FP32, ~1 ulp per term, ~1e-7 of I even when coherent) -> FP64 sums, fixed-order reductions
+// (deterministic).  A disordered frame has no such pixel except q = 0 (I = (sum f)^2; P(I > 64 <I>) = e^-64), so the
+// cost is one N-atom sum per frame; a crystal adds its Bragg peaks.
 // The epilogue that writes the batch's I (the integer engine's direct drain, the chunk fold or the species combine)
 // appends bright pixels to a list (BrightSink, common.cuh); the kernels here recompute the listed pixels.
 #include "common.cuh"

@@ -56,7 +56,7 @@ constexpr int STAGE_BYTES = 4 * PLANE;              // A_hi A_lo B_hi B_lo = 16 
 #endif
 constexpr int STAGES = XPCS_I8_STAGES;
 #ifndef XPCS_I8_GROUPS
-#define XPCS_I8_GROUPS 6
+#define XPCS_I8_GROUPS 5
 #endif
 constexpr int NGROUPS = XPCS_I8_GROUPS, GROUP_WARPS = 4;   // per group: 2 X warps, 2 W warps (one per K half)
 static_assert(NGROUPS <= STAGES, "mbarrier parity: producer groups must not exceed the stage count");
@@ -448,6 +448,12 @@ __global__ void k_absmax_f(const uint4* __restrict__ staged, int64_t n, float* _
         __syncthreads();
     }
     if (threadIdx.x == 0) out[0] = sh[0];
+}
+
+cudaError_t launch_absmax_f(const uint4* staged, int64_t n, float* out, cudaStream_t s) {
+    note_launch();
+    k_absmax_f<<<1, 256, 0, s>>>(staged, n, out);
+    return cudaGetLastError();
 }
 
 // clusters of k_lattice_i8 resident at once on the current device (one wave); sm_count / 2 if the query fails

@@ -1,12 +1,14 @@
-// k_lattice_tc.cu -- K3: lattice-plane amplitude on the 5th-generation tensor cores (tcgen05, TMEM accumulators).
+// k_lattice_tc.cu -- K3: lattice-plane amplitude on the 5th-generation tensor cores (tcgen05, TMEM accumulators),
+// split-FP16 operands: the precise tensor engine (per-atom form factors and the heavy kinds of species calls).
 //
-// The per-axis factorisation of Eq.(7) on a reciprocal-lattice plane,
-//     p^e(h,k) = sum_j X_h(j) W_k(j),   X_h(j) = e^{-2 pi i h Th_a(j)},  W_k(j) = f_j e^{-2 pi i (Th_0(j) + k Th_b(j))},
-// is a complex matrix product with the atoms as the contraction dimension K.  A cluster of 2 CTAs (one per SM) owns
-// a 256 (h) x 128 (k) pixel tile of one frame and a chunk of atoms (split-K; chunks are folded in FP64 by
-// k_amp_reduce): tcgen05.mma.cta_group::2.kind::f16, M = 256 (each CTA its 128 X rows), N = 256 = [Re | Im'] of the
-// 128 k (each CTA holds 64 k of B, rows [-Ws | Wr | Ws]: B1 = [Wr | Ws] and B2 = [-Ws | Wr] are overlapping windows),
-// K = 16, FP32 accumulators in TMEM; the tile holds conj(p) (Im' = -Im, R1).
+// The per-axis factorisation of Eq.(7) on a reciprocal-lattice plane makes the
+// amplitude a matrix product over atoms.  CONJUGATE ROW PAIRS (as k_lattice_i8.cu): a cluster of 2 CTAs (one per SM)
+// owns 256 consecutive rows h = c +- d around the tile centre c = H0 + 127.5 and 128 k of one frame and a chunk of
+// atoms (split-K; chunks are folded in FP64 by k_amp_reduce / k_species_combine).  With X_d = e^{2 pi i d Th_a} =
+// a + i b and W_k = f e^{2 pi i (Th_0 + k Th_b + c Th_a)} = wr + i wi, ONE real product [a; b] x [wr | wi]^T gives both
+// rows of a pair: q(c + d) = (AR - BI) + i (AI + BR), q(c - d) = (AR + BI) + i (AI - BR), q = conj(p) (R1).
+// tcgen05.mma.cta_group::2.kind::f16, M = 256 (each CTA rows [a | b] of its 64 d), N = 256 (each CTA B rows [wr | wi]
+// of its 64 k), K = 16, FP32 accumulators in TMEM.
 // Precision: every phasor component v is split v = hi + lo (hi on a 2^-10 grid, exact in fp16; lo = fp16(v - hi)) and
 // each real product uses three MMAs (hi.hi + hi.lo + lo.hi; the dropped lo.lo term is < 2^-22 per term), i.e.
 // FP32-class products (a single fp16/tf32 pass fails the 1e-3 N gate).
@@ -14,72 +16,59 @@
 // Accumulation: the tcgen05 FP32 accumulator is not round-to-nearest (measured: the error of a TMEM accumulation
 // grows linearly with its length, SURVEY A.8 / DESIGN.md "tensor accumulator"), so no TMEM accumulator ever sums
 // more than SUB_STAGES * 16 = 256 atoms: two TMEM accumulators (2 x 256 columns) alternate, and while the MMA
-// fills one, four drain warps add the other into round-to-nearest FP32 running sums in shared memory.
+// fills one, four drain warps add the other into round-to-nearest FP32 running sums in shared memory; at the end the
+// drain warps combine the a/b rows of the sums into the conjugate pair and write the tile.
 //
-// One CTA per SM (TMEM 512 columns): 3 producer groups of 3 warps (2 X warps, 1 W warp; group g fills stages
-// g, g + 3, ... of a 3-stage ring of 16-atom stages; a thread owns 4 atoms x 8 rows and walks the rows with the
-// angle-addition recurrence), 4 drain warps, and one warp that allocates TMEM and whose lane 0
-// issues the 6 MMAs per stage.  Producer -> MMA: mbarrier full[s] (6 warp arrivals of the pair after
+// One CTA per SM (TMEM 512 columns): NGROUPS producer groups of 2 warps (1 X warp, 1 W warp; group g fills stages
+// g, g + NGROUPS, ... of a STAGES-deep ring of 16-atom stages; a thread owns 4 atoms x 8 rows and walks the rows
+// with the angle-addition recurrence), 4 drain warps, and one warp that allocates TMEM and whose lane 0
+// issues the 3 MMAs per stage.  Producer -> MMA: mbarrier full[s] (2 x 2 warp arrivals of the pair after
 // fence.proxy.async); MMA -> producer: tcgen05.commit -> empty[s]; MMA -> drain: tcgen05.commit -> tfull[b];
-// drain -> MMA: tempty[b] (8 arrivals).  XPCS_TC_GROUPED=0 builds the earlier 16-warp producer.
+// drain -> MMA: tempty[b] (8 arrivals).
 #include "common.cuh"
 #include <cuda_fp16.h>
 
 namespace xpcs {
 
 namespace tc {
-constexpr int TM = 128, TN = 128, KS = 16;        // rows (h) per CTA, tile cols (k), atoms per stage
-constexpr int PAIR_M = 2 * TM;                    // a CTA pair (cluster of 2 SMs) owns 256 h x 128 k
-constexpr int BN = TN / 2;                        // each CTA of the pair holds half of B (64 k rows)
+constexpr int HD = 64;                            // d values per CTA (the pair covers 128 d = 256 h rows)
+constexpr int TM = 2 * HD, TN = 128, KS = 16;     // A rows per CTA ([a | b]), pair tile cols (k), atoms per stage
+constexpr int PAIR_M = 2 * TM;                    // MMA M = 256
+constexpr int PAIR_H = 4 * HD;                    // 256 output rows h per pair tile
+constexpr int BN = TN / 2;                        // k per CTA; B rows per CTA: [wr | wi] = 128
 #ifndef XPCS_TC_STAGES
-#define XPCS_TC_STAGES 3
-#endif
-#ifndef XPCS_TC_HALFSUMS
-#define XPCS_TC_HALFSUMS 0
+#define XPCS_TC_STAGES 5
 #endif
 constexpr int STAGES = XPCS_TC_STAGES;
 #ifndef XPCS_TC_SUB_STAGES
 #define XPCS_TC_SUB_STAGES 16
 #endif
 constexpr int SUB_STAGES = XPCS_TC_SUB_STAGES;    // stages per TMEM accumulator (16 stages = 256 atoms)
-constexpr int APLANE = TM * KS * 2;               // bytes per fp16 A plane (128 rows x 16 atoms)
-constexpr int BROWS = 3 * BN;                     // B rows of this CTA: [-Ws | Wr | Ws] for its 64 k
-constexpr int BPLANE = BROWS * KS * 2;            // bytes per fp16 B plane (192 rows x 16 atoms)
-constexpr int STAGE_BYTES = 4 * APLANE + 2 * BPLANE;   // Xr_hi Xr_lo Xs_hi Xs_lo | B_hi B_lo
-constexpr int MMA_N = 2 * TN;                     // N = 256: [Re | Im'] of 64 k per CTA half
-#ifndef XPCS_TC_GROUPED
-#define XPCS_TC_GROUPED 1          // producer groups of 3 warps, 4 atoms x 8 rows per thread, angle-addition recurrence
-#endif
+constexpr int APLANE = TM * KS * 2;               // bytes per fp16 plane (128 rows x 16 atoms), A and B alike
+constexpr int BPLANE = APLANE;
+constexpr int HALF_ROWS = HD / 8 * 256;           // byte offset of row 64 in a plane (8-row core groups of 256 B)
+constexpr int STAGE_BYTES = 2 * APLANE + 2 * BPLANE;   // A_hi A_lo | B_hi B_lo = 16 KB
+constexpr int MMA_N = 2 * TN;                     // N = 256: [wr | wi] of 64 k per CTA half
 #ifndef XPCS_TC_GROUPS
-#define XPCS_TC_GROUPS 3
+#define XPCS_TC_GROUPS 5
 #endif
-#if XPCS_TC_GROUPED
-#ifndef XPCS_TC_RPT
-#define XPCS_TC_RPT 8              // rows per producer thread (8 or 4): 4 doubles the warps of a group
-#endif
-constexpr int RPT = XPCS_TC_RPT, XWARPS = 2 * (8 / RPT), WWARPS = 8 / RPT;
-constexpr int NGROUPS = XPCS_TC_GROUPS, GROUP_WARPS = XWARPS + WWARPS;   // per group: X warps (row slices), W warps
+constexpr int RPT = 8, XWARPS = 1, WWARPS = 1;    // rows per producer thread; X / W warps per group
+constexpr int NGROUPS = XPCS_TC_GROUPS, GROUP_WARPS = XWARPS + WWARPS;
+static_assert(NGROUPS <= STAGES, "mbarrier parity: producer groups must not exceed the stage count");
 constexpr int NPROD_WARPS = NGROUPS * GROUP_WARPS, NDRAIN_WARPS = 4;
 // per-warp records of a stage (16 atoms); record r sits in 16-B unit r ^ ((r & 8) >> 2): conflict-free cp.async
 // writes (8 lanes per phase) and per-field 32-bit reads of records {u, 4 + u, 8 + u, 12 + u}
 constexpr int WREC = 16, WSLOT = WREC;
-#else
-constexpr int NPROD_WARPS = 16, NDRAIN_WARPS = 4;
-#endif
 constexpr int MMA_WARP = NPROD_WARPS + NDRAIN_WARPS;
 constexpr int NTHREADS = (MMA_WARP + 1) * 32;
-constexpr int TMEM_COLS = 512;                    // buffer b: cols [256b, 256b+256) = [Re k<64 | Im' k<64 | Re k>=64 | Im' k>=64]
+constexpr int TMEM_COLS = 512;                    // buffer b: cols [256b, 256b+256) = [wr k<64 | wi k<64 | wr k>=64 | wi k>=64]
 constexpr int SUM_LD = 129;                       // running sums [256 cols][129] fp32 (padded: conflict-free)
-constexpr int SUM_BYTES = (XPCS_TC_HALFSUMS ? 128 : 256) * SUM_LD * 4;   // HALFSUMS: timing experiments only
+constexpr int SUM_BYTES = 256 * SUM_LD * 4;
 #ifndef XPCS_TC_ASLOTS
 #define XPCS_TC_ASLOTS 4
 #endif
 constexpr int ASLOTS = XPCS_TC_ASLOTS;            // cp.async prefetch ring depth (distance ASLOTS - 1 stages)
-#if XPCS_TC_GROUPED
 constexpr int ASLOT_BYTES = NPROD_WARPS * ASLOTS * WSLOT * 16;   // per producer warp: its stage's 16 atoms, padded
-#else
-constexpr int ASLOT_BYTES = NPROD_WARPS * ASLOTS * 8 * 16;   // per producer warp: its 8 atoms of ASLOTS stages
-#endif
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + SUM_BYTES + ASLOT_BYTES + 1024 + 256;
 static_assert(SMEM_BYTES <= 227 * 1024, "k_lattice_tc: shared memory over the 227 KB opt-in limit");
 }  // namespace tc
@@ -314,9 +303,10 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();                  // 0 = leader (issues the pair's MMAs)
     const int ptile = blockIdx.x >> 1;                     // pair tile: 256 h x 128 k
-    const int th0 = (ptile / tiles_k) * PAIR_M + (int)rank * TM;   // this CTA's 128 h rows (A half)
-    const int tk0 = (ptile % tiles_k) * TN;                        // the pair's 128 k columns
-    const int bk0 = tk0 + (int)rank * BN;                          // this CTA's 64 k rows of B
+    const int tile_h = ptile / tiles_k;
+    const int64_t H0 = g.h0 + (int64_t)tile_h * PAIR_H;    // first row h of the pair tile; centre c = H0 + 127.5
+    const int tk0 = (ptile % tiles_k) * TN;                // the pair's 128 k columns
+    const int bk0 = tk0 + (int)rank * BN;                  // this CTA's 64 k rows of B
     const int64_t chunk = blockIdx.y, t = blockIdx.z;
     const int64_t a_begin = chunk * chunk_atoms, a_end = min(N, a_begin + chunk_atoms);
     const int n_stages = (int)((a_end - a_begin + KS - 1) / KS);
@@ -324,12 +314,8 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
     const uint4* S = staged + t * N;
 
     if (threadIdx.x == 0) {
-        // in the leader: full[s] counts the 16 producer warps of both CTAs, tempty[b] the 4 drain warps of both
-#if XPCS_TC_GROUPED
+        // in the leader: full[s] counts the producer warps of one group in both CTAs, tempty[b] the drain warps
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 2 * GROUP_WARPS); mbar_init(&empty[s], 1); }
-#else
-        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 2 * NPROD_WARPS); mbar_init(&empty[s], 1); }
-#endif
         for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 2 * NDRAIN_WARPS); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -361,21 +347,13 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
                 mbar_wait_cluster(&full[s], (uint32_t)((i / STAGES) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t sb = base + s * STAGE_BYTES;
-                // A planes: Xr_hi Xr_lo Xs_hi Xs_lo.  B rows of each CTA: [-Ws | Wr | Ws] (64 k each):
-                //   B1 = rows 64..191 = [Wr | Ws],  B2 = rows 0..127 = [-Ws | Wr]
-                //   Xr . B1 -> (Xr Wr, Xr Ws),  Xs . B2 -> (-Xs Ws, Xs Wr):  D = [Re | Im'] with Im' = -Im
-                const uint64_t xr_h = umma_desc(sb + 0 * APLANE, 128, 256), xr_l = umma_desc(sb + 1 * APLANE, 128, 256);
-                const uint64_t xs_h = umma_desc(sb + 2 * APLANE, 128, 256), xs_l = umma_desc(sb + 3 * APLANE, 128, 256);
-                const uint32_t bh = sb + 4 * APLANE, bl = bh + BPLANE;
-                const uint64_t b1_h = umma_desc(bh + BN * 32, 128, 256), b1_l = umma_desc(bl + BN * 32, 128, 256);
-                const uint64_t b2_h = umma_desc(bh, 128, 256), b2_l = umma_desc(bl, 128, 256);
+                const uint64_t a_h = umma_desc(sb, 128, 256), a_l = umma_desc(sb + APLANE, 128, 256);
+                const uint64_t b_h = umma_desc(sb + 2 * APLANE, 128, 256), b_l = umma_desc(sb + 2 * APLANE + BPLANE, 128, 256);
                 const uint32_t d = tmem + (uint32_t)(b * 256);
                 const uint32_t first = sub_first ? 0u : 1u;
                 if (!(dbg_flags & 4)) {   // experiments: bit 2 skips the MMAs (producer/drain cost alone)
-                    umma2_f16(d, xr_h, b1_h, idesc, first);
-                    if (lo_on) { umma2_f16(d, xr_h, b1_l, idesc, 1); umma2_f16(d, xr_l, b1_h, idesc, 1); }
-                    umma2_f16(d, xs_h, b2_h, idesc, 1);
-                    if (lo_on) { umma2_f16(d, xs_h, b2_l, idesc, 1); umma2_f16(d, xs_l, b2_h, idesc, 1); }
+                    umma2_f16(d, a_h, b_h, idesc, first);
+                    if (lo_on) { umma2_f16(d, a_h, b_l, idesc, 1); umma2_f16(d, a_l, b_h, idesc, 1); }
                 }
                 umma2_commit_both(&empty[s]);                     // frees the stage in both CTAs
                 if ((i % SUB_STAGES) == SUB_STAGES - 1 || i == n_stages - 1) umma2_commit_both(&tfull[b]);
@@ -383,7 +361,6 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
         }
         __syncwarp();
     } else if (warp < NPROD_WARPS) {
-#if XPCS_TC_GROUPED
         // ================= phasor producers: group g fills stages g, g + NGROUPS, ...  A thread owns 4 atoms (one
         // 8-byte half2 pair per row and plane, STS.64) and 8 rows spaced 8 apart, walked with the angle-addition
         // recurrence (2 sincos per atom per stage, 2 packed ops per phasor); split into fp16 hi/lo with magic
@@ -395,6 +372,11 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
         const bool is_x = wi < XWARPS;
         const uint32_t slot0 = smem_u32(aslot) + (uint32_t)(warp * ASLOTS * WSLOT * 16);
         const uint32_t full0 = mapa(smem_u32(full), 0);
+        // X rows: d = i + 1/2, i = 64 rank + mr + 8 r, phase d Th_a = (2i + 1) Th_a / 2 turns (33-bit product, the half
+        // unit truncated); W rows: k = bk0 + mr + 8 r, phase Th_0 + k Th_b + c Th_a, c Th_a = (2 H0 + 255) Th_a / 2
+        const uint64_t x_odd = (uint64_t)(2 * ((int)rank * HD + mr) + 1);
+        const uint64_t c_odd = (uint64_t)(2 * H0 + 2 * (PAIR_H / 2) - 1);
+        const uint32_t kk = (uint32_t)(g.k0 + bk0 + mr);
         auto prefetch = [&](int li) {
             const int i = grp + li * NGROUPS;
             if (i < n_stages && lane < WREC) {
@@ -415,22 +397,33 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
             cp_async_wait<ASLOTS - 2>();
             __syncwarp();
             prefetch(li + ASLOTS - 1);
-            uint4 at[4];
+            unsigned long long v[4], st[4], f2[4];
+            float fm = 0.f;
             {
-                // only the fields this warp uses: X warps Th_a, W warps (Th_b, Th_0, f)
                 const uint32_t ra = slot0 + (uint32_t)((li % ASLOTS) * WSLOT * 16);
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const uint32_t a = ra + (uint32_t)((((4 * qq + u) ^ (qq & 2))) * 16);   // record 4 qq + u
-                    if (is_x) {
-                        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(at[u].x) : "r"(a));
-                        at[u].y = at[u].z = at[u].w = 0u;
-                    } else {
-                        at[u].x = 0u;
-                        asm volatile("ld.shared.u32 %0, [%1+4];" : "=r"(at[u].y) : "r"(a));
-                        asm volatile("ld.shared.u32 %0, [%1+8];" : "=r"(at[u].z) : "r"(a));
-                        asm volatile("ld.shared.u32 %0, [%1+12];" : "=r"(at[u].w) : "r"(a));
+                    uint32_t tha, thb = 0u, th0 = 0u, fw = 0u;
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tha) : "r"(a));
+                    if (!is_x) {
+                        asm volatile("ld.shared.u32 %0, [%1+4];" : "=r"(thb) : "r"(a));
+                        asm volatile("ld.shared.u32 %0, [%1+8];" : "=r"(th0) : "r"(a));
+                        asm volatile("ld.shared.u32 %0, [%1+12];" : "=r"(fw) : "r"(a));
                     }
+                    float s0, c0, s1, c1;
+                    if (is_x) {
+                        __sincosf(turns_to_radians((uint32_t)((x_odd * tha) >> 1)), &s0, &c0);
+                        twiddle8(tha, s1, c1);
+                    } else {
+                        __sincosf(turns_to_radians(th0 + kk * thb + (uint32_t)((c_odd * tha) >> 1)), &s0, &c0);
+                        twiddle8(thb, s1, c1);
+                        const float fj = __uint_as_float(fw);             // padding atoms: f = 0 -> W = 0
+                        f2[u] = pack2(fj, fj);
+                        fm = fmaxf(fm, fabsf(fj));
+                    }
+                    v[u] = pack2(c0, s0);
+                    st[u] = pack2(c1, s1);
                 }
             }
             mbar_wait(&empty[s], (uint32_t)(((i / STAGES) + 1) & 1));
@@ -438,79 +431,32 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
             // byte offset of (row m, quad qq) in a plane: [m/8][qq/2][m%8][qq%2 * 8 B]
             const uint32_t qoff = (uint32_t)((qq >> 1) * 128 + mr * 16 + (qq & 1) * 8);
             if (!(dbg_flags & 2)) {
-                if (is_x) {
-                    const int xw = wi;                                   // rows m = mr + 8 r + 8 RPT xw, r < RPT
-                    const uint32_t h = (uint32_t)(g.h0 + th0 + mr + 8 * RPT * xw);
-                    unsigned long long v[4], st[4];
+                // rows m = mr + 8 r: real parts (a | wr) into rows m of the hi/lo planes, imaginary parts (b | wi) into
+                // rows 64 + m
+                const uint32_t a0 = sbase + (is_x ? 0u : (uint32_t)(2 * APLANE)) + qoff;
+                const unsigned long long M2 = is_x ? MX2 : pack2(split_magic(fm), split_magic(fm));
+#pragma unroll
+                for (int r = 0; r < RPT; ++r) {
+                    unsigned long long hi[4], lo[4];
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
-                        float s0, c0, s1, c1;
-                        __sincosf(turns_to_radians(h * at[u].x), &s0, &c0);
-                        twiddle8(at[u].x, s1, c1);
-                        v[u] = pack2(c0, s0);
-                        st[u] = pack2(c1, s1);
-                    }
-                    const uint32_t a0 = sbase + qoff + (uint32_t)(xw * RPT * 256);
-#pragma unroll
-                    for (int r = 0; r < RPT; ++r) {
-                        unsigned long long hi[4], lo[4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            hi[u] = fsub2(fadd2(v[u], MX2), MX2);          // (c_hi, s_hi), exact in fp16
-                            lo[u] = fsub2(v[u], hi[u]);                     // (c_lo, s_lo)
-                            const unsigned long long cd = pack2(lo2(st[u]), lo2(st[u]));
-                            const unsigned long long sd = pack2(-hi2(st[u]), hi2(st[u]));
-                            v[u] = ffma2(swap2(v[u]), sd, fmul2(v[u], cd));
+                        if (is_x) {
+                            hi[u] = fsub2(fadd2(v[u], M2), M2);               // (c_hi, s_hi), exact in fp16
+                            lo[u] = fsub2(v[u], hi[u]);                        // (c_lo, s_lo)
+                        } else {
+                            const unsigned long long tt = ffma2(f2[u], v[u], M2);
+                            hi[u] = fsub2(tt, M2);                             // f (c, s) hi
+                            lo[u] = ffma2(f2[u], v[u], fsub2(M2, tt));         // f (c, s) - hi, from the exact product
                         }
-                        const uint32_t ad = a0 + (uint32_t)(r * 256);
-                        sts64<0 * APLANE>(ad, pack_h2(lo2(hi[1]), lo2(hi[0])), pack_h2(lo2(hi[3]), lo2(hi[2])));   // Xr_hi
-                        sts64<1 * APLANE>(ad, pack_h2(lo2(lo[1]), lo2(lo[0])), pack_h2(lo2(lo[3]), lo2(lo[2])));   // Xr_lo
-                        sts64<2 * APLANE>(ad, pack_h2(hi2(hi[1]), hi2(hi[0])), pack_h2(hi2(hi[3]), hi2(hi[2])));   // Xs_hi
-                        sts64<3 * APLANE>(ad, pack_h2(hi2(lo[1]), hi2(lo[0])), pack_h2(hi2(lo[3]), hi2(lo[2])));   // Xs_lo
+                        const unsigned long long cd = pack2(lo2(st[u]), lo2(st[u]));
+                        const unsigned long long sd = pack2(-hi2(st[u]), hi2(st[u]));
+                        v[u] = ffma2(swap2(v[u]), sd, fmul2(v[u], cd));
                     }
-                } else {
-                    // W rows k = mr + 8 r of this CTA's 64: W_k = f e^{-2 pi i (Th_0 + kk Th_b)}; B rows: -Ws at k,
-                    // Wr at BN + k, Ws at 2 BN + k.  hi on the 2^(e-10) grid of the quad's max |f| (split_magic)
-                    const int ww = wi - XWARPS;                          // rows k = mr + 8 r + 8 RPT ww, r < RPT
-                    const uint32_t kk = (uint32_t)(g.k0 + bk0 + mr + 8 * RPT * ww);
-                    unsigned long long v[4], st[4], f2[4];
-                    float fm = 0.f;
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        float s0, c0, s1, c1;
-                        __sincosf(turns_to_radians(at[u].z + kk * at[u].y), &s0, &c0);
-                        twiddle8(at[u].y, s1, c1);
-                        v[u] = pack2(c0, s0);
-                        st[u] = pack2(c1, s1);
-                        const float fj = __uint_as_float(at[u].w);   // padding atoms: f = 0 -> W = 0
-                        f2[u] = pack2(fj, fj);
-                        fm = fmaxf(fm, fabsf(fj));
-                    }
-                    const float MW = split_magic(fm);
-                    const unsigned long long MW2 = pack2(MW, MW);
-                    const uint32_t a0 = sbase + 4 * APLANE + qoff + (uint32_t)(ww * RPT * 256);
-#pragma unroll
-                    for (int r = 0; r < RPT; ++r) {
-                        unsigned long long hi[4], lo[4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const unsigned long long t = ffma2(f2[u], v[u], MW2);
-                            hi[u] = fsub2(t, MW2);                           // f (c, s) hi
-                            lo[u] = ffma2(f2[u], v[u], fsub2(MW2, t));       // f (c, s) - hi, from the exact product
-                            const unsigned long long cd = pack2(lo2(st[u]), lo2(st[u]));
-                            const unsigned long long sd = pack2(-hi2(st[u]), hi2(st[u]));
-                            v[u] = ffma2(swap2(v[u]), sd, fmul2(v[u], cd));
-                        }
-                        const uint32_t wr_h0 = pack_h2(lo2(hi[1]), lo2(hi[0])), wr_h1 = pack_h2(lo2(hi[3]), lo2(hi[2]));
-                        const uint32_t wr_l0 = pack_h2(lo2(lo[1]), lo2(lo[0])), wr_l1 = pack_h2(lo2(lo[3]), lo2(lo[2]));
-                        const uint32_t ws_h0 = pack_h2(hi2(hi[1]), hi2(hi[0])), ws_h1 = pack_h2(hi2(hi[3]), hi2(hi[2]));
-                        const uint32_t ws_l0 = pack_h2(hi2(lo[1]), hi2(lo[0])), ws_l1 = pack_h2(hi2(lo[3]), hi2(lo[2]));
-                        const uint32_t ad = a0 + (uint32_t)(r * 256);
-                        sts64<8 * 256>(ad, wr_h0, wr_h1);                      sts64<BPLANE + 8 * 256>(ad, wr_l0, wr_l1);
-                        sts64<16 * 256>(ad, ws_h0, ws_h1);                     sts64<BPLANE + 16 * 256>(ad, ws_l0, ws_l1);
-                        sts64<0>(ad, ws_h0 ^ 0x80008000u, ws_h1 ^ 0x80008000u);
-                        sts64<BPLANE>(ad, ws_l0 ^ 0x80008000u, ws_l1 ^ 0x80008000u);   // -Ws (sign bits)
-                    }
+                    const uint32_t ad = a0 + (uint32_t)(r * 256);
+                    sts64<0>(ad, pack_h2(lo2(hi[1]), lo2(hi[0])), pack_h2(lo2(hi[3]), lo2(hi[2])));                    // re hi
+                    sts64<APLANE>(ad, pack_h2(lo2(lo[1]), lo2(lo[0])), pack_h2(lo2(lo[3]), lo2(lo[2])));               // re lo
+                    sts64<HALF_ROWS>(ad, pack_h2(hi2(hi[1]), hi2(hi[0])), pack_h2(hi2(hi[3]), hi2(hi[2])));            // im hi
+                    sts64<APLANE + HALF_ROWS>(ad, pack_h2(hi2(lo[1]), hi2(lo[0])), pack_h2(hi2(lo[3]), hi2(lo[2])));   // im lo
                 }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> async proxy
@@ -518,87 +464,12 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
             if (lane == 0) mbar_arrive_cluster(full0 + (uint32_t)(s * 8));   // the leader's full[s]
         }
         cp_async_wait<0>();
-#else
-        // ================= phasor producers (both CTAs): own 128 A rows, own 64 B rows =================
-        const int ah = warp & 1;
-        const int a_loc = ah * 8 + 2 * (lane & 3);
-        const int mrow = lane >> 2;
-        const int gi = warp >> 1;                            // 0..7
-        // atom records are prefetched ASLOTS - 1 stages ahead with cp.async into this warp's shared ring (the warp
-        // needs atoms ah*8 .. ah*8+7 of each stage; the per-stage MEMBAR of the release-arrive does not wait on
-        // cp.async, unlike on register loads in flight)
-        const uint32_t slot = smem_u32(aslot) + (uint32_t)(warp * ASLOTS * 8 * 16);
-        const uint32_t full0 = mapa(smem_u32(full), 0);
-        auto prefetch = [&](int stage_idx) {
-            if (lane < 8) {
-                const int64_t j = a_begin + (int64_t)stage_idx * KS + ah * 8 + lane;
-                const bool ok = j < a_end;
-                cp_async16(slot + (uint32_t)(((stage_idx % ASLOTS) * 8 + lane) * 16), S + (ok ? j : 0), ok ? 16u : 0u);
-            }
-            cp_async_commit();
-        };
-#pragma unroll
-        for (int k = 0; k < ASLOTS - 1; ++k) prefetch(k);
-        for (int i = 0; i < n_stages; ++i) {
-            const int s = i % STAGES;
-            prefetch(i + ASLOTS - 1);
-            cp_async_wait<ASLOTS - 1>();      // stage i's records have landed
-            __syncwarp();
-            uint4 at0, at1;
-            {
-                const uint32_t ra = slot + (uint32_t)(((i % ASLOTS) * 8 + 2 * (lane & 3)) * 16);
-                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(at0.x), "=r"(at0.y), "=r"(at0.z), "=r"(at0.w) : "r"(ra));
-                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4+16];" : "=r"(at1.x), "=r"(at1.y), "=r"(at1.z), "=r"(at1.w) : "r"(ra));
-            }
-            __syncwarp();
-            mbar_wait(&empty[s], (uint32_t)(((i / STAGES) + 1) & 1));
-            // padding atoms have f = 0, so W = 0 and their (finite) X values never contribute
-            const float f0 = __uint_as_float(at0.w), f1 = __uint_as_float(at1.w);
-            const unsigned long long F2 = pack2(f0, f1);
-            const float MX = 12288.0f;                                       // |X| <= 1: grid 2^-10
-            const float MW = split_magic(fmaxf(fabsf(f0), fabsf(f1)));
-            const unsigned long long MX2 = pack2(MX, MX), MW2 = pack2(MW, MW);
-            const uint32_t sbase = smem_u32(smem) + (uint32_t)(s * STAGE_BYTES);
-            if (!(dbg_flags & 2)) {   // experiments: bit 1 skips generation
-#pragma unroll
-                for (int it = 0; it < 2; ++it) {   // X rows: groups gi and gi + 8 of this CTA's 128 rows
-                    const int m = (gi + 8 * it) * 8 + mrow;
-                    const uint32_t off = sbase + plane_off(m, a_loc);
-                    const uint32_t hh = (uint32_t)(g.h0 + th0 + m);
-                    float s0, c0, s1, c1;
-                    __sincosf(turns_to_radians(hh * at0.x), &s0, &c0);
-                    __sincosf(turns_to_radians(hh * at1.x), &s1, &c1);
-                    split_store<0 * APLANE, 1 * APLANE>(off, pack2(c0, c1), MX2);     // Xr = cos
-                    split_store<2 * APLANE, 3 * APLANE>(off, pack2(s0, s1), MX2);     // Xs = sin
-                }
-                {   // W rows: group gi of this CTA's 64 k, k = k0 + bk0 + m;  B rows: -Ws at m, Wr at 64+m, Ws at 128+m
-                    const int m = gi * 8 + mrow;
-                    const uint32_t kk = (uint32_t)(g.k0 + bk0 + m);
-                    float s0, c0, s1, c1;
-                    __sincosf(turns_to_radians(at0.z + kk * at0.y), &s0, &c0);
-                    __sincosf(turns_to_radians(at1.z + kk * at1.y), &s1, &c1);
-                    uint32_t wr_h, wr_l, ws_h, ws_l;
-                    split_vals_f(F2, pack2(c0, c1), MW2, wr_h, wr_l);       // Wr = f cos
-                    split_vals_f(F2, pack2(s0, s1), MW2, ws_h, ws_l);       // Ws = f sin
-                    const uint32_t ob = sbase + 4 * APLANE;
-                    const uint32_t o_ns = ob + plane_off(m, a_loc), o_r = ob + plane_off(BN + m, a_loc),
-                                   o_s = ob + plane_off(2 * BN + m, a_loc);
-                    sts32<0>(o_r, wr_h);      sts32<BPLANE>(o_r, wr_l);
-                    sts32<0>(o_s, ws_h);      sts32<BPLANE>(o_s, ws_l);
-                    sts32<0>(o_ns, ws_h ^ 0x80008000u); sts32<BPLANE>(o_ns, ws_l ^ 0x80008000u);   // -Ws (sign bits)
-                }
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> async proxy
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(full0 + (uint32_t)(s * 8));   // the leader's full[s]
-        }
-#endif
     } else {
         // ================= drain warps: TMEM accumulator -> RN fp32 running sums (smem) -> tile =================
         const int quarter = warp & 3;               // TMEM lanes 32*quarter .. +31 = rows of this CTA's half
         const int r = quarter * 32 + lane;
         const uint32_t tempty0 = mapa(smem_u32(tempty), 0);
-        for (int c = 0; c < (XPCS_TC_HALFSUMS ? 128 : 256); ++c) sums[c * SUM_LD + r] = 0.f;
+        for (int c = 0; c < 256; ++c) sums[c * SUM_LD + r] = 0.f;
         for (int u = 0; u < ((dbg_flags & 8) ? 0 : n_sub); ++u) {   // experiments: bit 3 skips the drain
             const int b = u & 1;
             mbar_wait_cluster(&tfull[b], (uint32_t)((u >> 1) & 1));
@@ -607,7 +478,6 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
             uint32_t v[2][32];
 #pragma unroll
             for (int blk = 0; blk < 8; blk += 2) {
-                if (XPCS_TC_HALFSUMS && blk >= 4) { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); __syncwarp(); if (lane == 0 && blk == 6) mbar_arrive_cluster(tempty0 + (uint32_t)(b * 8)); continue; }
 #pragma unroll
                 for (int q = 0; q < 2; ++q) TMEM_LD32(tb + (uint32_t)((blk + q) * 32), v[q]);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -627,21 +497,26 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
                 }
             }
         }
-        // ---- write this CTA's 128 x 128 half tile: row-major partial[chunk][t][ih][ik], coalesced along k
-        __syncwarp();
+        // ---- conjugate-pair combination and the tile write: this CTA's 64 d give output rows h = c + d and c - d
+        // (partial[chunk][t][ih][ik] = q, coalesced along k).  sums column of (k, comp): 128 (k / 64) + 64 comp + k % 64
+        asm volatile("bar.sync 1, 128;" ::: "memory");   // the four drain warps' running sums are complete
         const int64_t n_q = g.n_h * g.n_k;
         float2* P = partial + (chunk * frames + t) * n_q;
-        for (int rr = 0; rr < 32; ++rr) {
-            const int row = quarter * 32 + rr;
-            const int64_t ih = th0 + row;
-            if (ih >= g.n_h) break;
+        const int64_t ih_base = (int64_t)tile_h * PAIR_H + PAIR_H / 2;   // output row of h = c + 1/2
+        for (int dl = quarter; dl < HD; dl += 4) {
+            const int di = (int)rank * HD + dl;
+            const int64_t ihp = ih_base + di, ihm = ih_base - 1 - di;
 #pragma unroll
             for (int j = 0; j < TN / 32; ++j) {
                 const int c = lane + 32 * j;
                 const int64_t ik = tk0 + c;
-                // accumulator columns: [Re k<64 | Im' k<64 | Re k>=64 | Im' k>=64]
-                const int cre = (c < BN) ? c : c + BN, cim = cre + BN;
-                if (ik < g.n_k) P[ih * g.n_k + ik] = make_float2(sums[cre * SUM_LD + row], XPCS_TC_HALFSUMS ? 0.f : sums[cim * SUM_LD + row]);
+                const int cr = 128 * (c >> 6) + (c & 63), ci = cr + 64;
+                const float AR = sums[cr * SUM_LD + dl], AI = sums[ci * SUM_LD + dl];
+                const float BR = sums[cr * SUM_LD + HD + dl], BI = sums[ci * SUM_LD + HD + dl];
+                if (ik < g.n_k) {
+                    if (ihp < g.n_h) P[ihp * g.n_k + ik] = make_float2(AR - BI, AI + BR);
+                    if (ihm < g.n_h) P[ihm * g.n_k + ik] = make_float2(AR + BI, AI - BR);
+                }
             }
         }
     }
@@ -671,7 +546,7 @@ bool lattice_tc_supported(const LatticeGeom& g) {
 cudaError_t launch_lattice_tc(const uint4* staged, int64_t N, int64_t frames, const LatticeGeom& g,
                               int64_t chunk_atoms, int64_t n_chunks, float2* partial, cudaStream_t s) {
     using namespace tc;
-    const int tiles_h = (int)((g.n_h + PAIR_M - 1) / PAIR_M), tiles_k = (int)((g.n_k + TN - 1) / TN);
+    const int tiles_h = (int)((g.n_h + PAIR_H - 1) / PAIR_H), tiles_k = (int)((g.n_k + TN - 1) / TN);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_lattice_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
