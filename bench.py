@@ -6,9 +6,11 @@
 
 A "step" = one pass of the whole hot path over one batch of synthetic input: frame staging, I(q,t) for every
 pixel of every frame, g2 for all lags, ring-averaged S(q,t) and g2, XSVS contrast for every exposure window.
-Default workload = BASELINE.json configs[1] ("c2": N = 32000, 100 Brownian frames, 256 x 256 lattice plane,
-g2 tau = 1..50).  Metric: atom.q pairs/s for I(q,t) (whole job, all ranks).  Multi-GPU = weak scaling: every
-rank processes its own independent trajectory (no data-path collective).
+Default workload = BASELINE.json configs[2] ("c3": N = 262144 atoms of two species, 1000 Brownian frames, 512 x 512
+lattice plane, g2 tau = 1..200), the largest configuration that fits one GPU (BASELINE.json quotes its metric on no
+config; c3 is 6.9e13 pairs per step, c2 2.1e11).  Metric: atom.q pairs/s for I(q,t) (whole job, all ranks).
+Multi-GPU = weak scaling: every rank processes its own independent trajectory (no data-path collective);
+--qslab splits one trajectory's detector across the ranks instead.
 """
 from __future__ import annotations
 
@@ -111,6 +113,89 @@ def _traffic(workload, engine, pairs_launch):
         return rec["dram_bytes"] * pairs_launch / rec["pairs"]
     except (OSError, KeyError, ValueError, ZeroDivisionError):
         return None
+
+
+def _roofline(cfg, wl, engine, f_h, prof, pairs_step, steps, step_ms, peaks, peak_src, sm_count, clk, xp):
+    """Roofline of the dominant kernel of the step.
+
+    achieved = the method's ALGORITHMIC work per launch / that kernel's average launch time (CUDA events on its
+    stream, the library's per-class profiling over the timed graph replays).  Algorithmic work: on a
+    lattice plane one complex MAC = 8 ops per atom.q pair, whatever the engine issues; for generic q one complex
+    exponential = 2 XU (MUFU) ops per pair.  peak = MEASURED_PEAKS for the kernel's own dtype: fp16 = the measured
+    bf16 dense rate, int8 = 2 x that (the guide's nominal int8/fp16 ratio; tools/mma_rate.cu measured 8192 vs 4096
+    MAC/clk/SM); the burst figure for a short step, the sustained one for a step >= 50 ms (a kernel inside a long,
+    power-capped step).  "pipe" reports what the tensor pipe actually issues (12 ops per pair: 3 split-precision
+    products x 2 real MACs per pixel of a conjugate pair) against the same peak and against the tcgen05 issue rate
+    at the run's SM clock."""
+    mhz_max = peaks.get("sm_max_mhz", 1965.0)
+    mhz_run = clk.get("sm_mhz") or mhz_max
+    long_step = step_ms >= 50.0
+    bf16 = peaks["bf16_tflops_sustained"] if long_step else peaks["bf16_tflops"]
+    which = "sustained" if long_step else "burst"
+    ms_i8, n_i8 = prof.get("intensity_i8", (0.0, 0))
+    ms_tc, n_tc = prof.get("intensity_tc", (0.0, 0))
+    ms_main, n_main = prof["intensity_main"]
+    share_i8 = None
+    if ms_i8 > 0 and ms_tc > 0:
+        counts = np.bincount(wl.kinds, minlength=len(wl.kind_f))
+        share_i8 = float(sum(xp.species_engines(counts, wl.kind_f))) / float(counts.sum())
+    elif ms_i8 > 0:
+        share_i8 = 1.0
+    elif ms_tc > 0:
+        share_i8 = 0.0
+    engines = {}
+    spec = {"i8": ("k_lattice_i8", ms_i8, n_i8, "int8 (two Q16 limbs) -> exact int32", 2.0 * bf16, "TOPS (int8)", 8190.0,
+                   f"{peak_src} {which} bf16 x 2 (int8)"),
+            "tensor": ("k_lattice_tc", ms_tc, n_tc, "fp16 (hi/lo split) -> fp32", bf16, "TFLOP/s (fp16)", 4095.0,
+                       f"{peak_src} {which} bf16 (= fp16 rate)")}
+    for name, (kern, ms_e, n_e, dt, peak, unit, rate, src) in spec.items():
+        if ms_e <= 0:
+            continue
+        pairs = pairs_step * (share_i8 if name == "i8" else 1.0 - share_i8)
+        t = ms_e / steps / 1e3                              # seconds per step in this engine
+        ach = 8.0 * pairs / t / 1e12
+        issued = 12.0 * pairs / t / 1e12
+        issue_peak = sm_count * rate * 2 * mhz_run * 1e6 / 1e12
+        engines[name] = {"kernel": kern, "dtype": dt, "bound": "tensor", "unit": unit, "peak": peak, "peak_source": src,
+                         "achieved": ach, "frac": ach / peak, "ops_per_pair": 8,
+                         "pairs_per_step": pairs, "kernel_ms_per_step": ms_e / steps, "launches_per_step": n_e / steps,
+                         "pairs_per_launch": pairs / max(n_e / steps, 1e-9),
+                         "pipe": {"issued_ops_per_pair": 12, "achieved": issued, "frac_of_peak": issued / peak,
+                                  "vs_issue_rate": issued / issue_peak, "issue_rate_peak": issue_peak,
+                                  "clock_mhz": mhz_run, "source": "tools/mma_rate.cu"}}
+    if engines:
+        dom = max(engines, key=lambda k: engines[k]["kernel_ms_per_step"])
+        roof = dict(engines[dom])
+        roof["engine"] = dom
+        if len(engines) > 1:
+            roof["engines"] = engines
+            roof["int8_pair_share"] = share_i8
+        eng_name = "i8+tensor" if len(engines) > 1 else dom
+        dtype = " + ".join(f"{e['dtype']} ({e['kernel']}{'' if len(engines) == 1 else f', {100 * e['pairs_per_step'] / pairs_step:.1f}% of pairs'})"
+                           for e in engines.values()) + "; positions f32, I f32"
+        return roof, eng_name, dtype
+    t = ms_main / steps / 1e3
+    launches = max(n_main / steps, 1e-9)
+    if cfg.n_plane == 0:
+        # generic q: 2 XU (MUFU) ops per pair; ceiling = 148 SM x 16 XU/clk x max clock / 2 (DESIGN.md)
+        peak = sm_count * 16 * mhz_max * 1e6 / 2 / 1e12
+        roof = {"kernel": "k_generic32", "bound": "alu", "unit": "Tpairs/s (XU: 2 MUFU per pair)", "peak": peak,
+                "achieved": pairs_step / t / 1e12, "peak_source": "derived (DESIGN.md)"}
+        eng_name, dtype = "generic", "f32 (exact integer phase turns, SFU sincos, FP64 chunk folds)"
+    else:
+        peak = sm_count * 128 * 2 * mhz_max * 1e6 / 1e12
+        roof = {"kernel": "k_lattice_simt" if wl.in_dtype != xp.F64 else "k_lattice64", "bound": "alu",
+                "unit": "TFLOP/s (FP32 FMA pipe)", "peak": peak, "achieved": 8.0 * pairs_step / t / 1e12,
+                "peak_source": "derived (DESIGN.md)"}
+        eng_name = "fp64" if wl.in_dtype == xp.F64 else "simt"
+        dtype = "f64" if wl.in_dtype == xp.F64 else "f32"
+        if wl.in_dtype == xp.F64:
+            roof["note"] = "FP64 workload: latency-bound (SURVEY 8(d)), report ms_per_step; frac is context only"
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["kernel_ms_per_step"] = ms_main / steps
+    roof["launches_per_step"] = n_main / steps
+    roof["pairs_per_launch"] = pairs_step / launches
+    return roof, eng_name, dtype
 
 
 def run_reference(args):
@@ -281,7 +366,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=sorted(xi.CONFIGS))
+    ap.add_argument("--config", default="c3", choices=sorted(xi.CONFIGS))
     ap.add_argument("--engine", default="auto", choices=["auto", "simt", "tensor", "i8"])
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--ref-pixels", type=int, default=4096)
@@ -380,107 +465,38 @@ def main():
     pairs_step = P.pairs_per_step
     value = ws * pairs_step / (ms / 1e3)
 
-    # ---- roofline of the dominant kernel (intensity main kernel), CUDA events on its stream
-    main_ms, main_n = prof["intensity_main"]
-    per_launch_ms = main_ms / max(main_n, 1)
-    launches_per_step = max(main_n // args.steps, 1)
-    pairs_launch = pairs_step / launches_per_step
+    # ---- roofline of the dominant kernel, CUDA events on its stream (the library's per-class profiling)
     peaks, peak_src = _peaks()
     sm_count, _ = xp.device_info()
-    tc_used = bool(cfg.n_plane) and wl.in_dtype == xp.F32 and engine != xp.ENGINE_SIMT and \
-        xp.engine_available(xp.ENGINE_TENSOR)
-    i8_used = tc_used and xp.engine_resolved(engine, f_h is None) == xp.ENGINE_TENSOR_I8
-    hybrid_share = None          # fraction of the pairs on the integer engine when kinds are split between engines
-    if tc_used and engine == xp.ENGINE_AUTO and wl.kinds is not None:
-        counts = np.bincount(wl.kinds, minlength=len(wl.kind_f))
-        share = float(sum(xp.species_engines(counts, wl.kind_f))) / float(counts.sum())
-        if 0.0 < share < 1.0:
-            hybrid_share = share
-        i8_used = share == 1.0
-    # the tensor peak: MEASURED_PEAKS' burst bf16 figure (cuBLAS at full clock) when the SM clock stayed at its max
-    # through the timed region (no power capping: the kernel ran at the clock the burst figure was taken at), else
-    # the sustained figure (cuBLAS back to back for 4 s, power-capped clocks)
     clk_sum = clk.summary()
-    at_max = bool(clk_sum.get("sm_mhz") and clk_sum.get("sm_max_mhz") and clk_sum["sm_mhz"] >= 0.97 * clk_sum["sm_max_mhz"])
-    tensor_peak = peaks["bf16_tflops"] if at_max else peaks["bf16_tflops_sustained"]
-    if cfg.n_plane == 0:
-        # generic q: 2 XU (MUFU) ops per pair; peak = 148 SM x 16 XU/clk x max clock
-        peak = sm_count * 16 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 2 / 1e12
-        roof = {"bound": "alu", "unit": "Tpairs/s (XU: 2 MUFU per pair)", "peak": peak,
-                "achieved": pairs_launch / (per_launch_ms / 1e3) / 1e12}
-    elif hybrid_share is not None:
-        # kinds split between the integer (int8, 2x rate) and split-FP16 engines: 24 ops per pair on both; the
-        # peak is the pair-weighted harmonic blend, over the whole intensity stage of a step (both kernels)
-        peak = 1.0 / (hybrid_share / (2.0 * tensor_peak) + (1.0 - hybrid_share) / tensor_peak)
-        stage_ms = main_ms / max(args.steps, 1)
-        roof = {"bound": "tensor", "unit": "T ops/s (int8 + fp16 blend)", "peak": peak,
-                "achieved": 24.0 * pairs_step / (stage_ms / 1e3) / 1e12, "int8_pair_share": hybrid_share}
-        per_launch_ms = stage_ms
-        pairs_launch = pairs_step
-    elif i8_used:
-        # tcgen05 kind::i8: 3 int8 limb products x 4 real MAC = 24 int8 ops per pair vs the int8 dense peak =
-        # 2 x the measured bf16 (= fp16) peak (B200: 4.5 POPS int8 vs 2.25 PFLOP/s fp16 nominal; tools/mma_rate.cu
-        # measured 8192 vs 4096 MAC/clk/SM)
-        peak = 2.0 * tensor_peak
-        roof = {"bound": "tensor", "unit": "TOPS (int8)", "peak": peak,
-                "achieved": 24.0 * pairs_launch / (per_launch_ms / 1e3) / 1e12}
-    elif tc_used:
-        # tcgen05 split-FP16: 3 fp16 products x 4 real MAC = 24 flop per pair vs measured bf16 (= fp16) dense peak
-        peak = tensor_peak
-        roof = {"bound": "tensor", "unit": "TFLOP/s", "peak": peak,
-                "achieved": 24.0 * pairs_launch / (per_launch_ms / 1e3) / 1e12}
-    else:
-        # FP32 CUDA cores: 1 complex MAC = 4 FMA = 8 flop per pair; peak = 148 x 128 FMA/clk x 2 x max clock
-        peak = sm_count * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-        roof = {"bound": "alu", "unit": "TFLOP/s (FP32 FMA pipe)", "peak": peak,
-                "achieved": 8.0 * pairs_launch / (per_launch_ms / 1e3) / 1e12}
-    roof["frac"] = roof["achieved"] / roof["peak"]
-    if wl.in_dtype == xp.F64:
-        # config 1 (4.1e6 pairs, FP64): launch/latency-bound; the FP32 figure above is context only
-        roof["note"] = "FP64 workload: latency-bound, report ms_per_step; frac against the FP32 pipe is context only"
-    eng_name = "i8+tensor" if hybrid_share is not None else \
-        ("i8" if i8_used else ("tensor" if tc_used else ("simt" if cfg.n_plane else "generic")))
-    roof["traffic"] = _traffic(cfg.name, eng_name, pairs_launch)
-    tensor_src = (f"{peak_src}, {'burst' if at_max else 'sustained'} bf16"
-                  + (" x 2 (int8)" if i8_used else (" blended int8/fp16" if hybrid_share else "")))
-    roof["peak_source"] = tensor_src if roof["bound"] == "tensor" else "derived (DESIGN.md)"
-    if roof["bound"] == "tensor":
-        # context: the same achieved rate against the tcgen05 issue rate microbenchmarked at the run's SM clock
-        # (tools/mma_rate.cu: 8190 int8 / 4095 fp16 MAC per clock per SM; 2 ops per MAC), which sits above the
-        # cuBLAS-measured peak the roofline uses (cuBLAS runs power-capped, MEASURED_PEAKS clocks_under_load)
-        mhz_run = clk_sum.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
-        if hybrid_share is not None:
-            rate = 1.0 / (hybrid_share / 8190.0 + (1.0 - hybrid_share) / 4095.0)
-        else:
-            rate = 8190.0 if i8_used else 4095.0
-        mma_peak = sm_count * rate * 2 * mhz_run * 1e6 / 1e12
-        roof["vs_mma_issue_rate"] = {"peak": mma_peak, "frac": roof["achieved"] / mma_peak,
-                                     "clock_mhz": mhz_run, "source": "tools/mma_rate.cu"}
-    if roof["frac"] > 1.0:
-        roof["note"] = ("frac > 1: the peak is the cuBLAS bf16 matmul figure of MEASURED_PEAKS (x 2 for int8), taken "
-                        "while the matmul ran power-capped (clocks_under_load median "
-                        f"{peaks.get('clocks_under_load', {}).get('sm_mhz_median', '?')} MHz), whereas this kernel ran "
-                        f"at {clk_sum.get('sm_mhz')} MHz; vs_mma_issue_rate is the same rate against the tcgen05 "
-                        "issue rate (tools/mma_rate.cu) at this run's clock")
-    roof["kernel_ms"] = per_launch_ms
-    roof["kernel_share_of_step"] = main_ms / args.steps / ms if ms > 0 else None
+    roof, eng_name, dtype = _roofline(cfg, wl, engine, f_h, prof, pairs_step, args.steps, ms, peaks, peak_src, sm_count,
+                                      clk_sum, xp)
+    main_ms = prof["intensity_main"][0]
+    roof["traffic"] = _traffic(cfg.name, roof.get("kernel", eng_name), roof.get("pairs_per_launch", 0.0))
+    roof["kernel_share_of_step"] = (roof["kernel_ms_per_step"] / ms) if ms > 0 else None
 
-    # ---- end to end through the public API from pinned host memory
+    # ---- end to end through the public API from pinned host memory: every step copies its positions in and I, g2,
+    # rings and beta out (xpcs_step_host, frame-batched H2D / compute / D2H overlap inside the step).  value = one
+    # pipeline, steps back to back (synchronous); "pipelined" = 2-3 pipelines in flight, so that step k's copies
+    # overlap step k+1's kernels (no L2 flush between steps)
     e2e = None
     if not args.no_e2e:
         P.alloc_host_io(pos_h, f_h, batches=args.e2e_batches)
         P.run_host()
         torch.cuda.synchronize()
+        h2d, d2h = P.io_bytes()
         auto_slots = 3 if pos_h.nbytes < (512 << 20) else 2
-        slots = 1 if args.no_graph else (args.e2e_slots if args.e2e_slots > 0 else auto_slots)
-        e_ms = None
+        slots = args.e2e_slots if args.e2e_slots > 0 else auto_slots
+        e_sync = e_pipe = None
         if not args.no_graph:
             try:
-                e_ms = _e2e_streamed(args, P, pipeline, wl, dev, pos_h, f_h, slots, stream, dist)
+                e_sync = _e2e_streamed(args, P, pipeline, wl, dev, pos_h, f_h, 1, stream, dist)
+                if slots > 1:
+                    e_pipe = _e2e_streamed(args, P, pipeline, wl, dev, pos_h, f_h, slots, stream, dist)
             except Exception:                                  # capture failed: eager host steps instead
                 torch.cuda.synchronize()
-                slots = 1
-        if e_ms is None:
+                e_sync = e_pipe = None
+        if e_sync is None:
             t_e = []
             for _ in range(max(2, args.steps)):
                 if dist is not None:
@@ -493,11 +509,15 @@ def main():
                 b.record(stream)
                 torch.cuda.synchronize()
                 t_e.append(a.elapsed_time(b))
-            e_ms = float(np.mean(t_e))
-        e_ms = xd.max_over_ranks(e_ms, dev)
-        h2d, d2h = P.io_bytes()
-        e2e = {"value": ws * pairs_step / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms, "streams": slots,
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+            e_sync = float(np.mean(t_e))
+        e_sync = xd.max_over_ranks(e_sync, dev)
+        e2e = {"value": ws * pairs_step / (e_sync / 1e3), "unit": UNIT, "ms_per_step": e_sync, "streams": 1,
+               "mode": "one pipeline, steps back to back", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h)}
+        if e_pipe is not None:
+            e_pipe = xd.max_over_ranks(e_pipe, dev)
+            e2e["pipelined"] = {"value": ws * pairs_step / (e_pipe / 1e3), "ms_per_step": e_pipe, "streams": slots,
+                                "mode": f"{slots} pipelines in flight (step k's copies overlap step k+1's kernels)"}
 
     # ---- secondary kernels against their own bounds (algorithmic work per step / measured class time per step).
     # In the timed step the reductions run concurrently, so their event times overlap; they are timed here in a few
@@ -528,9 +548,9 @@ def main():
     if nl:
         _sec("g2", "fp64", float(sum(T - tau for tau in cfg.lags)) * n_q, sm_count * 58.95 * mhz * 1e6,
              "G DFMA/s")
-    # XSVS: one read of the intensity series per exposure window (L2 / HBM streaming)
+    # XSVS: one read of the intensity series for all exposure windows (4 T bytes per pixel)
     if cfg.windows:
-        _sec("xsvs", "hbm", float(len(cfg.windows)) * i_bytes, hbm, "GB/s")
+        _sec("xsvs", "hbm", float(i_bytes), hbm, "GB/s")
     # staging: positions read (12 B) + 16-B records written per atom and frame
     _sec("stage", "hbm", float(cfg.N) * T * (12 + 16), hbm, "GB/s")
     # (the fold of the atom-chunk partials reads C partial planes, C chosen inside the library: ncu shows it at
@@ -545,7 +565,7 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64" if wl.in_dtype == xp.F64 else "f32", "data": "synthetic",
+                "vs_baseline": None, "dtype": dtype, "data": "synthetic",
                 "config": {"workload": cfg.name, "N": cfg.N, "n_q": P.n_q, "frames": cfg.T,
                            "lags": len(cfg.lags), "windows": list(cfg.windows), "rings": cfg.n_bins,
                            "pairs_per_step_per_gpu": pairs_step, "engine": args.engine,

@@ -364,7 +364,8 @@ XPCS_API int xpcs_radial_bins(const void* q_vectors, int64_t n_q, double q_max, 
  * xpcs_profile_reset / xpcs_profile_query: when opts->profile != 0 the library brackets each launch of its
  *   main kernels with CUDA events on opts->stream.  query(i) synchronises and returns, for kernel class i
  *   (0 = intensity main kernel, 1 = staging, 2 = amplitude reduction, 3 = g2, 4 = XSVS, 5 = rings,
- *   6 = the integer engine's bright-pixel recompute),
+ *   6 = the tensor engines' bright-pixel recompute, 7 / 8 = the integer / split-FP16 tensor engine's launches,
+ *   which are also counted in class 0),
  *   its name, the summed device time in ms and the number of timed launches; returns EINVAL past the end.
  * xpcs_device_info: SM count and SM clock (kHz) of the current device (HOST outputs). */
 XPCS_API const char* xpcs_last_error(void);

@@ -18,7 +18,8 @@ LIB_PATH = os.environ.get("XPCS_LIB", os.path.join(_HERE, "lib", "libxpcs.so")) 
 XPCS_OK, XPCS_EINVAL, XPCS_ECUDA, XPCS_ENOMEM, XPCS_EUNSUPPORTED = 0, 1, 2, 3, 4
 F32, F64 = 0, 1
 ENGINE_AUTO, ENGINE_SIMT, ENGINE_TENSOR, ENGINE_TENSOR_I8 = 0, 1, 2, 3
-KERNEL_CLASSES = ("intensity_main", "stage", "amplitude_reduce", "g2", "xsvs", "rings", "fixup")
+KERNEL_CLASSES = ("intensity_main", "stage", "amplitude_reduce", "g2", "xsvs", "rings", "fixup", "intensity_i8",
+                  "intensity_tc")
 
 EXPORTED = (
     "xpcs_intensity", "xpcs_intensity_grid", "xpcs_g2", "xsvs_contrast", "xpcs_shell_mean",

@@ -735,6 +735,7 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
               TRY(cuda_fail(launch_stage_lattice32(positions, 0, form_factors, 0, Ng, vb, g, m, st + stoff, o.s), "stage")); }
             { ProfScope p(o.profile, KC_MAIN, o.s);
               const bool g_i8 = i8 && gi8[(size_t)gi], g_tc = (i8 || tc) && !g_i8;
+              ProfScope pe(o.profile && (g_i8 || g_tc), g_i8 ? KC_I8 : KC_TC, o.s);
               if (g_i8) TRY(cuda_fail(launch_lattice_i8(st + stoff, Ng, vb, g, chunk[gi], C[gi], fmax, form_factors == nullptr,
                                                       part + poff, o.s, direct ? dst : nullptr, o.out_f64, mode,
                                                       (fix && direct) ? &bs : nullptr),

@@ -9,7 +9,8 @@ namespace xpcs {
 // ------------------------------------------------------------------------------------------------
 // host-side runtime services (defined in runtime.cu)
 // ------------------------------------------------------------------------------------------------
-enum KernelClass { KC_MAIN = 0, KC_STAGE = 1, KC_REDUCE = 2, KC_G2 = 3, KC_XSVS = 4, KC_RINGS = 5, KC_FIXUP = 6, KC_COUNT = 7 };
+enum KernelClass { KC_MAIN = 0, KC_STAGE = 1, KC_REDUCE = 2, KC_G2 = 3, KC_XSVS = 4, KC_RINGS = 5, KC_FIXUP = 6, KC_I8 = 7, KC_TC = 8,
+                   KC_COUNT = 9 };   // KC_I8 / KC_TC: the tensor engines' launches inside KC_MAIN
 
 void set_error(const char* fmt, ...);
 void note_launch(int n = 1);

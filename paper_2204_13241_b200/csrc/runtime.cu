@@ -157,7 +157,8 @@ const int32_t* lag_table(const int32_t* lags, int64_t n) {
 }
 
 // ---------------------------------------------------------------- profiling
-static const char* kClassNames[KC_COUNT] = {"intensity_main", "stage", "amplitude_reduce", "g2", "xsvs", "rings", "fixup"};
+static const char* kClassNames[KC_COUNT] = {"intensity_main", "stage", "amplitude_reduce", "g2", "xsvs", "rings", "fixup",
+                                             "intensity_i8", "intensity_tc"};
 struct ProfRec { std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev; };
 static ProfRec g_prof[KC_COUNT];
 
