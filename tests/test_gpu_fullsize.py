@@ -8,7 +8,12 @@
   3. the statistical pins of SURVEY 8(c) applied to the *full* GPU outputs (the only end-to-end check at full scale
      that the CPU oracle cannot afford): the Siegert + diffusion law of the g2 numerator (Eq. 24-25), mean S = 1 for
      the ideal gas, the discrete Eq.(28) XSVS law, and the off-lattice expectation with the box shape transform.
-Plus the perfect-crystal Bragg variant of every config at its own N (I = N^2 at peaks, ~0 elsewhere).
+  4. END-TO-END ring-level acceptance (north_star: <= 1e-4 relative on the azimuthally averaged S(q) and on g2,
+     DESIGN.md R12; XSVS beta at the same 1e-4): the oracle computes I itself on whole rings (the
+     SURVEY 8(d) parity subsets) and its S_b(t), ring g2 and beta are compared with the GPU pipeline's outputs --
+     c2 full plane x frames {0, 49, 99} (S_b) and shells 0-3 x 100 frames (ring g2), c3 shell 0 x 1000 frames
+     (ring g2, S_b), c5 shells {0, 1} x 200 frames (beta); every oracle pixel-frame also passes the per-pixel gate.
+Plus the perfect-crystal Bragg variant of every config at its own N (I = N^2 at peaks within the gate, ~0 elsewhere).
 """
 import numpy as np
 import pytest
@@ -83,6 +88,23 @@ def _reductions(cfg, res, pix):
         assert_rel(res["beta"], oracle.xsvs_beta(I, bins, cfg.n_bins, cfg.windows), 1e-10, "beta")
 
 
+def _oracle_I(cfg, pos, f, q_sel, frames=None, chunk=100):
+    """Oracle I(q, t) at the selected q for the given frames (all by default), in frame chunks (bounded memory)."""
+    frames = np.arange(pos.shape[0]) if frames is None else np.asarray(frames)
+    ff = f.astype(np.float64) if cfg.two_species else None
+    out = [oracle.intensity(pos[frames[i:i + chunk]], ff, q_sel, cfg.L) for i in range(0, len(frames), chunk)]
+    return np.concatenate(out, 0)
+
+
+def _shell_pixels(bins, shells):
+    return np.flatnonzero(np.isin(bins, list(shells)))
+
+
+def _ring_mean(values, bins_sel, shells):
+    """Mean over each shell's pixels (values [rows][n_sel], bins_sel [n_sel]) -> [rows][len(shells)]."""
+    return np.stack([values[:, bins_sel == b].mean(1) for b in shells], 1)
+
+
 def _species(cfg):
     f = xi.form_factors(cfg).astype(np.float64)
     return f.sum(), (f ** 2).sum(), (f ** 4).sum()
@@ -118,22 +140,46 @@ def _g2_numerator_pin(cfg, res, q, lags, shells):
 def test_config2_full_size():
     cfg = xi.CONFIGS["c2"]
     res, pos, f, q, inc = _run(cfg)
-    pix = _pixel_parity(cfg, res, pos, f, q, inc, [0, 49, 99], 384, 2)
-    _reductions(cfg, res, pix)
+    bins = res["bins"]
+    # full plane at frames {0, 49, 99}: per-pixel gate on every pixel and S_b(t) end to end (SURVEY 8(d) subset)
+    frames = [0, 49, 99]
+    Io = _oracle_I(cfg, pos, f, q, frames)
+    assert_pixels(res["I"][frames], Io, cfg.N, "c2 full plane")
+    S_o = oracle.structure_factor_shells(Io, None, cfg.N, bins, cfg.n_bins)
+    assert_rel(res["S_rings"][frames], S_o, 1e-4, "c2 S_b(t) vs oracle I (end to end)")
+    # shells 0-3 x all 100 frames: per-pixel gate and the ring-averaged g2 end to end
+    shells = range(4)
+    pix = _shell_pixels(bins, shells)
+    Ir = _oracle_I(cfg, pos, f, q[pix])
+    assert_pixels(res["I"][:, pix], Ir, cfg.N, "c2 shells 0-3 x 100 frames")
+    g2_ring_o = _ring_mean(oracle.g2(Ir, cfg.lags), bins[pix], shells)
+    assert_rel(res["g2_rings"][:, :4], g2_ring_o, 1e-4, "c2 ring g2 vs oracle I (end to end)")
+    pix_s = _pixel_parity(cfg, res, pos, f, q, inc, [0, 49, 99], 384, 2)
+    _reductions(cfg, res, pix_s)
     _g2_numerator_pin(cfg, res, q, cfg.lags, range(cfg.n_bins))
     assert abs(np.nanmean(res["S_rings"][:, 4:]) - 1) < 0.01
 
 
 @pytest.mark.slow
 def test_config3_full_size():
-    """1000 frames x 262144 atoms x 512^2 pixels (6.9e13 pairs), two species, g2 for tau = 1..200."""
+    """1000 frames x 262144 atoms x 512^2 pixels (6.9e13 pairs), two species, g2 for tau = 1..200.  End to end: the
+    oracle's I on shell 0 (~200 pixels) x all 1000 frames (5e10 pairs, ~2 min on 16 cores): per-pixel gate on 2e5
+    pixel-frames, ring g2 and S_b(t) of shell 0 within 1e-4."""
     cfg = xi.CONFIGS["c3"]
     res, pos, f, q, inc = _run(cfg)
+    bins = res["bins"]
+    pix0 = _shell_pixels(bins, [0])
+    Ir = _oracle_I(cfg, pos, f, q[pix0])
+    assert Ir.size >= 1e5
+    assert_pixels(res["I"][:, pix0], Ir, cfg.N, "c3 shell 0 x 1000 frames")
+    assert_rel(res["g2_rings"][:, :1], _ring_mean(oracle.g2(Ir, cfg.lags), bins[pix0], [0]), 1e-4,
+               "c3 ring g2 (shell 0) vs oracle I (end to end)")
+    _, S2, _ = _species(cfg)
+    assert_rel(res["S_rings"][:, :1], _ring_mean(Ir, bins[pix0], [0]) / S2, 1e-4, "c3 S_b(t) (shell 0) end to end")
     pix = _pixel_parity(cfg, res, pos, f, q, inc, [0, 999], 64, 3)
     del pos
     _reductions(cfg, res, pix)
     _g2_numerator_pin(cfg, res, q, [1, 2, 4, 8, 16, 32, 64, 128, 200], range(cfg.n_bins))
-    _, S2, _ = _species(cfg)
     assert abs(np.nanmean(res["S_rings"][:, 4:]) - 1) < 0.005
 
 
@@ -144,7 +190,7 @@ def test_config4_full_size():
     speckle is oversampled ~1.4x per axis, so n_eff = pixels x frames / 4)."""
     cfg = xi.CONFIGS["c4"]
     res, pos, f, q, inc = _run(cfg)
-    pix = _pixel_parity(cfg, res, pos, f, q, inc, [0, 19], 96, 4)
+    pix = _pixel_parity(cfg, res, pos, f, q, inc, list(range(20)), 512, 4)     # 512 pixels x 20 frames = 1e4
     del pos
     _reductions(cfg, res, pix)
     S1, S2, _ = _species(cfg)
@@ -167,6 +213,15 @@ def test_config5_full_size():
     rings with 2 D q^2 dt T >= 20 for W <= 64 (SURVEY 8(c) XSVS pin, A.11)."""
     cfg = xi.CONFIGS["c5"]
     res, pos, f, q, inc = _run(cfg)
+    bins = res["bins"]
+    # end to end: the oracle's I on shells {0, 1} (~800 pixels) x 200 frames (8e10 pairs, ~3 min on 16 cores):
+    # per-pixel gate on 1.6e5 pixel-frames and beta of both shells for every window within 1e-4
+    shells = [0, 1]
+    pixr = _shell_pixels(bins, shells)
+    Ir = _oracle_I(cfg, pos, f, q[pixr])
+    assert_pixels(res["I"][:, pixr], Ir, cfg.N, "c5 shells 0-1 x 200 frames")
+    beta_o = oracle.xsvs_beta(Ir, bins[pixr], cfg.n_bins, cfg.windows)[:, :2]
+    assert_rel(res["beta"][:, :2], beta_o, 1e-4, "c5 beta (shells 0, 1) vs oracle I (end to end)")
     pix = _pixel_parity(cfg, res, pos, f, q, inc, [0, 199], 64, 5)
     del pos
     _reductions(cfg, res, pix)
@@ -209,5 +264,6 @@ def test_bragg_variant_at_config_size(kind, n_cells, cfg_name, n):
     peak = (H % period == 0) & (K % period == 0)
     if kind == "bcc":
         peak &= ((H // period + K // period) % 2 == 0)
-    np.testing.assert_allclose(I[peak], float(N) ** 2, rtol=1e-5)
+    qp = (2 * np.pi / cfg.L) * np.stack([H[peak], K[peak], np.zeros(peak.sum())], -1)
+    assert_pixels(I[peak], oracle.intensity(pos.astype(np.float64), None, qp, cfg.L)[0], N, f"{kind} Bragg peaks")
     assert np.max(I[~peak]) <= 1e-3 * N
