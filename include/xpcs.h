@@ -57,6 +57,11 @@ typedef struct {
     void*   stream;     /* cudaStream_t; NULL = legacy default stream                                           */
     int32_t engine;     /* xpcs_engine (lattice grids only)                                                     */
     int32_t profile;    /* nonzero: time the dominant kernels with CUDA events (see xpcs_profile_query)        */
+    int32_t workspace;  /* 0: library scratch cached per (device, stream); k > 0: per (device, k, stream), so that
+                           callers replaying CUDA graphs concurrently (one workspace id each) never share scratch
+                           even if their streams are recycled.  A scratch buffer that a graph capture has used is
+                           never freed before xpcs_release (a later, larger call gets a new buffer).          */
+    int32_t pad_;
 } xpcs_opts;
 
 /* A plane of the reciprocal lattice of a cubic periodic box of edge L (Algorithm 1 step 1,
@@ -142,8 +147,9 @@ typedef struct {
     const void* f_q;
     const double* f_max;   /* HOST [n_species] or NULL: max_q |f_s(q)| per kind, a hint for AUTO's engine choice
                               (lightest kinds on the integer engine while sum f_max^2 N_s / (f_min^2 N) <= 1, the kind
-                              crossing the budget split at it, the rest on the split-FP16 engine; NULL: every kind on
-                              the integer engine) */
+                              crossing the budget split at it, the rest on the split-FP16 engine; NULL: AUTO runs
+                              every kind on the split-FP16 engine, XPCS_ENGINE_TENSOR_I8 every kind on the integer
+                              engine) */
 } xpcs_species;
 
 /* xpcs_intensity_volume / xpcs_amplitude_volume: I (or p, as (re, im) pairs) on a 3-D lattice block for every
@@ -299,7 +305,10 @@ XPCS_API int xpcs_structure_factor_shells(const void* I, int64_t rows, int64_t n
  * are library-owned, cached per (device, opts->stream) and freed by xpcs_release.  After one call outside a
  * capture, the call can be captured in a CUDA graph on the same stream (pinned host buffers).
  *   positions    HOST [frames][N][3] in_dtype
- *   form_factors HOST [N] in_dtype or NULL (f = 1); with species: used only for the S(q) normalisation sum f^2
+ *   form_factors HOST [N] in_dtype or NULL (f = 1); with species: used only for the S(q) normalisation sum f^2.
+ *                Without species, under XPCS_ENGINE_AUTO with f32 inputs, per-atom values with at most 16 distinct
+ *                values are run as atom kinds with q-independent f_s (so the light kinds can use the integer
+ *                engine; the result is the same Eq.(7) sum)
  *   species      NULL or atom kinds as for xpcs_intensity_volume (species->species HOST, f_q DEVICE
  *                [n_species][n_q]); then form_factors may still be given for the normalisation
  *   bin_of_q     DEVICE [n_q] ring index (-1 excluded), n_bins rings (register it with xpcs_rings_register to
@@ -308,8 +317,10 @@ XPCS_API int xpcs_structure_factor_shells(const void* I, int64_t rows, int64_t n
  *   I_out HOST [frames][n_q] out_dtype, g2_out HOST [n_lags][n_q] out_dtype, S_rings HOST [frames][n_bins],
  *   g2_rings HOST [n_lags][n_bins], beta HOST [n_windows][n_bins] (double); any output may be NULL (not copied;
  *   g2_rings needs g2 to be computed, which happens whenever n_lags > 0).
- * Errors: EINVAL for a null step/positions/bin_of_q, N/frames/n_bins/batches <= 0, a lag or window out of range;
- *         the errors of the underlying calls (xpcs_intensity_volume, xpcs_g2, xsvs_contrast, ...). */
+ * Errors: EINVAL for a null step/positions/bin_of_q, N/frames/n_bins/batches <= 0, a lag or window out of range,
+ *         n_bins > 12288, n_q >= 2^31, invalid species; EUNSUPPORTED for a lag > 640 -- all checked before any work is
+ *         enqueued; then the errors of the underlying calls (xpcs_intensity_volume, xpcs_g2, xsvs_contrast, ...), after
+ *         which the internal streams are still joined into opts->stream. */
 typedef struct {
     const void* positions;
     const void* form_factors;

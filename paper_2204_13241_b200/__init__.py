@@ -10,5 +10,5 @@ from ._lib import (  # noqa: F401
     device_info, engine_available, engine_resolved, species_engines, launch_count, lattice_plane, load, profile_query, profile_reset, qgrid, release,
     xpcs_amplitude, xpcs_amplitude_grid, xpcs_g2, xpcs_intensity, xpcs_intensity_grid, xpcs_isf, xpcs_lattice_bins, xpcs_qgrid_ewald, xpcs_radial_bins,
     xpcs_shell_mean, xpcs_structure_factor_shells, xsvs_contrast, xpcs_step_host, xpcs_ring_moments,
-    xpcs_ring_means_from_moments, xsvs_moments, xsvs_contrast_from_moments, xsvs_n_slots,
+    xpcs_ring_means_from_moments, xsvs_moments, xsvs_contrast_from_moments, xsvs_n_slots, new_workspace, workspace,
 )

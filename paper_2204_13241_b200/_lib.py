@@ -7,6 +7,8 @@ only things PyTorch provides); host-side integer lists (lags, windows) are plain
 from __future__ import annotations
 
 import ctypes
+import itertools
+import threading
 import math
 import os
 
@@ -42,7 +44,8 @@ class XpcsError(RuntimeError):
 
 class Opts(ctypes.Structure):
     _fields_ = [("in_dtype", ctypes.c_int32), ("out_dtype", ctypes.c_int32), ("stream", ctypes.c_void_p),
-                ("engine", ctypes.c_int32), ("profile", ctypes.c_int32)]
+                ("engine", ctypes.c_int32), ("profile", ctypes.c_int32), ("workspace", ctypes.c_int32),
+                ("pad_", ctypes.c_int32)]
 
 
 class QGrid(ctypes.Structure):
@@ -174,8 +177,34 @@ def _stream(stream=None):
     return ctypes.c_void_p(s.cuda_stream)
 
 
+_WORKSPACE = threading.local()
+
+
 def make_opts(in_dtype=F32, out_dtype=F32, stream=None, engine=ENGINE_AUTO, profile=False):
-    return Opts(in_dtype, out_dtype, _stream(stream), engine, 1 if profile else 0)
+    return Opts(in_dtype, out_dtype, _stream(stream), engine, 1 if profile else 0, getattr(_WORKSPACE, "id", 0), 0)
+
+
+_ws_counter = itertools.count(1)
+
+
+def new_workspace() -> int:
+    """A fresh scratch workspace id (xpcs_opts.workspace) for one user of the library, e.g. one Pipeline."""
+    return next(_ws_counter)
+
+
+class workspace:
+    """Context manager: library calls made inside use scratch workspace `ws_id` (0 = per-stream default)."""
+
+    def __init__(self, ws_id: int):
+        self.ws_id = int(ws_id)
+
+    def __enter__(self):
+        self.prev = getattr(_WORKSPACE, "id", 0)
+        _WORKSPACE.id = self.ws_id
+        return self
+
+    def __exit__(self, *a):
+        _WORKSPACE.id = self.prev
 
 
 def _i32_array(seq):
@@ -607,12 +636,12 @@ AUTO_I8 = True    # AUTO routes uniform-f lattice calls to the integer engine (m
 def species_engines(counts, f_max=None):
     """Mirror of api.cu's AUTO rule for species calls: kinds in increasing |f_max| go to the integer engine while
     sum (f_max / f_min)^2 N_s / N <= 1; the kind that crosses the budget is split (its first atoms on the integer
-    engine up to the budget), the rest run on split-FP16.  Returns the number of atoms of each kind on the integer
-    engine."""
+    engine up to the budget), the rest run on split-FP16.  Without f_max hints every kind runs on split-FP16.
+    Returns the number of atoms of each kind on the integer engine."""
     counts = [int(c) for c in counts]
     n = len(counts)
     if f_max is None:
-        return list(counts)
+        return [0] * n
     order = sorted(range(n), key=lambda k: abs(f_max[k]))
     fref = next((abs(f_max[k]) for k in order if counts[k] > 0 and abs(f_max[k]) > 0), 0.0)
     total = max(1, sum(counts))

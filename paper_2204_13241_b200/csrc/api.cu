@@ -29,6 +29,7 @@ constexpr size_t kBatchBytes = size_t(1) << 30;   // cap for staged atoms / part
 struct Opts {
     bool in_f64 = false, out_f64 = false, profile = false;
     int engine = XPCS_ENGINE_AUTO;
+    int workspace = 0;
     cudaStream_t s = nullptr;
 };
 
@@ -47,7 +48,13 @@ int parse_opts(const xpcs_opts* o, Opts& out) {
         out.s = (cudaStream_t)o->stream;
         out.engine = o->engine;
         out.profile = o->profile != 0;
+        if (o->workspace < 0) {
+            set_error("xpcs: workspace must be >= 0 (got %d)", o->workspace);
+            return XPCS_EINVAL;
+        }
+        out.workspace = o->workspace;
     }
+    set_workspace(out.workspace);   // scratch() of this call (and of the calls it makes) keys on it
     return XPCS_OK;
 }
 
@@ -283,9 +290,8 @@ static int prep_groups(const xpcs_species* sp, const void* form_factors, int64_t
 
 static int upload_groups(Groups& G, cudaStream_t s) {
     if (!G.n_species) return XPCS_OK;
-    (void)s;
     // cached device copy keyed by content (graph-capturable after one eager call; see host_table)
-    const int32_t* d = (const int32_t*)host_table(G.perm.data(), sizeof(int32_t) * G.perm.size());
+    const int32_t* d = (const int32_t*)host_table(G.perm.data(), sizeof(int32_t) * G.perm.size(), s);
     if (!d) return XPCS_ECUDA;
     G.d_idx = d;
     return XPCS_OK;
@@ -535,6 +541,10 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
     // share of the error budget, sum f_max^2 N_s / (f_ref^2 N) with f_ref the smallest weight, stays <= 1 -- the
     // single-species f = 1 level validated against the gate; the heavier kinds run on the split-FP16 engine.
     std::vector<char> gi8((size_t)ng, i8 ? 1 : 0);
+    // AUTO species call without f_max hints: the kinds' weights are unknown (f_q lives on the device), so the
+    // error budget cannot be applied -- every kind runs on the precise split-FP16 engine (an explicit TENSOR_I8
+    // request still puts every kind on the integer engine)
+    if (G.n_species && o.engine == XPCS_ENGINE_AUTO && (i8 || tc) && !species->f_max) std::fill(gi8.begin(), gi8.end(), 0);
     if (G.n_species && o.engine == XPCS_ENGINE_AUTO && (i8 || tc) && species->f_max) {
         // kinds in increasing max|f_s|: whole kinds on the integer engine while the budget allows, the kind that
         // crosses it split (its first atoms on the integer engine up to the budget), the rest on split-FP16
@@ -954,7 +964,7 @@ int xpcs_isf(const void* A_series, int64_t frames, int64_t n_q, const int32_t* l
         return XPCS_EUNSUPPORTED;
     }
     TRY(check_sticky());
-    const int32_t* dl = lag_table(lags, n_lags);
+    const int32_t* dl = lag_table(lags, n_lags, o.s);
     if (!dl) return XPCS_ECUDA;
     double* norm = nullptr;
     if (form_factors) {
@@ -991,7 +1001,7 @@ int xpcs_g2(const void* I_series, int64_t frames, int64_t n_q, const int32_t* la
         return XPCS_EUNSUPPORTED;
     }
     TRY(check_sticky());
-    const int32_t* dl = lag_table(lags, n_lags);
+    const int32_t* dl = lag_table(lags, n_lags, o.s);
     if (!dl) return XPCS_ECUDA;
     ProfScope p(o.profile, KC_G2, o.s);
     return cuda_fail(launch_g2(I_series, o.in_f64, frames, n_q, dl, n_lags, max_lag, g2_out, o.out_f64, o.s), "g2");
@@ -1237,11 +1247,10 @@ int xpcs_shell_mean(const void* values, int64_t rows, int64_t n_q, const int32_t
     return cuda_fail(launch_shell_mean(values, o.in_f64, rows, n_q, pb.plan, n_bins, scale, nullptr, out, o.s), "rings");
 }
 
-int xpcs_structure_factor_shells(const void* I, int64_t rows, int64_t n_q, const void* form_factors, int64_t N,
-                                 const int32_t* bin_of_q, int32_t n_bins, double* out, const xpcs_opts* opts) {
-    clear_error();
-    Opts o;
-    TRY(parse_opts(opts, o));
+}  // extern "C"
+// S(q,t) ring means with the form factors' own dtype (xpcs_step_host: I is out_dtype, f the caller's in_dtype)
+static int structure_factor_shells(const void* I, int64_t rows, int64_t n_q, const void* form_factors, int ff_f64,
+                                   int64_t N, const int32_t* bin_of_q, int32_t n_bins, double* out, const Opts& o) {
     NEED(I, "I");
     NEED(bin_of_q, "bin_of_q");
     NEED(out, "out");
@@ -1258,11 +1267,20 @@ int xpcs_structure_factor_shells(const void* I, int64_t rows, int64_t n_q, const
     if (form_factors) {
         norm = (double*)scratch(o.s, SS_SMALL, 64);
         if (!norm) return XPCS_ENOMEM;
-        TRY(cuda_fail(launch_sum_f2(form_factors, o.in_f64, N, norm, o.s), "sum f^2"));
+        TRY(cuda_fail(launch_sum_f2(form_factors, ff_f64, N, norm, o.s), "sum f^2"));
     } else {
         scale = 1.0 / (double)N;     // sum_j f_j^2 = N for unit form factors
     }
     return cuda_fail(launch_shell_mean(I, o.in_f64, rows, n_q, pb.plan, n_bins, scale, norm, out, o.s), "rings");
+}
+extern "C" {
+
+int xpcs_structure_factor_shells(const void* I, int64_t rows, int64_t n_q, const void* form_factors, int64_t N,
+                                 const int32_t* bin_of_q, int32_t n_bins, double* out, const xpcs_opts* opts) {
+    clear_error();
+    Opts o;
+    TRY(parse_opts(opts, o));
+    return structure_factor_shells(I, rows, n_q, form_factors, o.in_f64 ? 1 : 0, N, bin_of_q, n_bins, out, o);
 }
 
 // ------------------------------------------------------------------------------------------- host-buffer step
@@ -1327,6 +1345,32 @@ void release_host_resources() {
 
 extern "C" {
 
+}  // extern "C"
+
+// xpcs_step_host: per-atom HOST form factors with few distinct values (e.g. two species given as f in {1, 2}) are run
+// as atom kinds with q-independent f_s, so that AUTO can place the light kinds on the integer engine (per-atom f
+// would scale every phasor by max |f| and keep the whole call on the split-FP16 engine).  Returns the kind count
+// (0: too many distinct values or none given).
+static int host_kinds(const void* ff, int f64, int64_t N, std::vector<int32_t>& kind, std::vector<double>& val) {
+    kind.clear();
+    val.clear();
+    if (!ff) return 0;
+    kind.resize((size_t)N);
+    for (int64_t j = 0; j < N; ++j) {
+        const double f = f64 ? ((const double*)ff)[j] : (double)((const float*)ff)[j];
+        size_t k = 0;
+        while (k < val.size() && !(val[k] == f)) ++k;     // exact value match (NaN never matches: falls out below)
+        if (k == val.size()) {
+            if (val.size() == (size_t)kMaxKinds || !std::isfinite(f)) { kind.clear(); val.clear(); return 0; }
+            val.push_back(f);
+        }
+        kind[(size_t)j] = (int32_t)k;
+    }
+    return (int)val.size();
+}
+
+extern "C" {
+
 int xpcs_step_host(const xpcs_step* st, const xpcs_opts* opts) {
     clear_error();
     NEED(st, "step");
@@ -1350,21 +1394,57 @@ int xpcs_step_host(const xpcs_step* st, const xpcs_opts* opts) {
         set_error("xpcs: lags/windows: negative count or NULL array");
         return XPCS_EINVAL;
     }
-    for (int64_t i = 0; i < st->n_lags; ++i)
+    int max_lag = 0;
+    for (int64_t i = 0; i < st->n_lags; ++i) {
         if (st->lags[i] < 0 || st->lags[i] >= st->frames) {
             set_error("xpcs: lag %d out of range [0, %lld)", st->lags[i], (long long)st->frames);
             return XPCS_EINVAL;
         }
+        max_lag = std::max(max_lag, (int)st->lags[i]);
+    }
     for (int64_t i = 0; i < st->n_windows; ++i)
         if (st->windows[i] < 1 || st->windows[i] > st->frames) {
             set_error("xpcs: window %d out of range [1, %lld]", st->windows[i], (long long)st->frames);
             return XPCS_EINVAL;
         }
+    // every limit of the calls below is checked here, before any stream is forked (an error after the fork would
+    // leave the copy streams unjoined)
+    const int64_t n_q = st->q_vectors ? st->n_q : st->grid.n_h * st->grid.n_k;
+    if (max_lag > 640) {
+        set_error("xpcs: lags > 640 frames are not supported by this build");
+        return XPCS_EUNSUPPORTED;
+    }
+    if (st->n_bins > 12288 || n_q > (int64_t(1) << 31) - 1) {
+        set_error("xpcs: ring plan limits: n_bins <= 12288, n_q < 2^31");
+        return XPCS_EINVAL;
+    }
+    if (st->species) {
+        Groups Gv;
+        TRY(prep_groups(st->species, nullptr, st->N, Gv));      // validates kinds and indices (host only)
+    }
     TRY(check_sticky());
     const int64_t N = st->N, T = st->frames, nb = st->n_bins;
-    const int64_t n_q = st->q_vectors ? st->n_q : st->grid.n_h * st->grid.n_k;
     const int64_t n_bat = std::min<int64_t>(st->batches, T);
     const size_t pin = o.in_f64 ? 8 : 4, pout = o.out_f64 ? 8 : 4;
+    // few distinct per-atom form factors -> atom kinds (see host_kinds)
+    std::vector<int32_t> kinds;
+    std::vector<double> kval, kabs;
+    const int n_kinds = (!st->species && o.engine == XPCS_ENGINE_AUTO && !o.in_f64)
+                            ? host_kinds(st->form_factors, o.in_f64, N, kinds, kval) : 0;
+    xpcs_species ksp;
+    std::memset(&ksp, 0, sizeof(ksp));
+    const xpcs_species* species = st->species;
+    void* d_fq = nullptr;
+    if (n_kinds > 0) {
+        d_fq = scratch(o.s, SS_H_FQ, pin * (size_t)n_kinds * (size_t)n_q);
+        if (!d_fq) return XPCS_ENOMEM;
+        ksp.n_species = n_kinds;
+        ksp.species = kinds.data();
+        ksp.f_q = d_fq;
+        for (double v : kval) kabs.push_back(std::fabs(v));
+        ksp.f_max = kabs.data();
+        species = &ksp;
+    }
     const size_t pos_bytes = pin * 3 * (size_t)N * (size_t)T, i_bytes = pout * (size_t)n_q * (size_t)T;
     const size_t g2_bytes = pout * (size_t)n_q * (size_t)st->n_lags;
     const size_t red_doubles = (size_t)(T + st->n_lags + st->n_windows) * (size_t)nb;
@@ -1385,84 +1465,101 @@ int xpcs_step_host(const xpcs_step* st, const xpcs_opts* opts) {
     TRY(cuda_fail(cudaEventRecord(ev_fork, o.s), "fork"));
     TRY(cuda_fail(cudaStreamWaitEvent(hr->h2d, ev_fork, 0), "fork"));
     TRY(cuda_fail(cudaStreamWaitEvent(hr->d2h, ev_fork, 0), "fork"));
-    if (st->form_factors) {
-        TRY(cuda_fail(cudaMemcpyAsync(d_ff, st->form_factors, pin * (size_t)N, cudaMemcpyHostToDevice, hr->h2d), "H2D f"));
-        TRY(cuda_fail(cudaEventRecord(ev_f, hr->h2d), "event"));
-    }
-    const size_t frame_pos = pin * 3 * (size_t)N, frame_i = pout * (size_t)n_q;
-    for (int64_t b = 0; b < n_bat; ++b) {
-        const int64_t t0 = b * T / n_bat, t1 = (b + 1) * T / n_bat;
-        TRY(cuda_fail(cudaMemcpyAsync(d_pos + t0 * frame_pos, (const char*)st->positions + t0 * frame_pos,
-                                      (size_t)(t1 - t0) * frame_pos, cudaMemcpyHostToDevice, hr->h2d), "H2D positions"));
-        TRY(cuda_fail(cudaEventRecord(ev[1 + b], hr->h2d), "event"));
-    }
-    TRY(cuda_fail(cudaEventRecord(ev_h2d, hr->h2d), "event"));
-    xpcs_opts io{};
-    io.in_dtype = o.in_f64 ? XPCS_F64 : XPCS_F32;
-    io.out_dtype = o.out_f64 ? XPCS_F64 : XPCS_F32;
-    io.stream = (void*)o.s;
-    io.engine = o.engine;
-    io.profile = o.profile ? 1 : 0;
-    xpcs_qvolume vol;
-    std::memset(&vol, 0, sizeof(vol));
-    vol.plane = st->grid;
-    vol.n_l = 1;
-    for (int64_t b = 0; b < n_bat; ++b) {
-        const int64_t t0 = b * T / n_bat, t1 = (b + 1) * T / n_bat;
-        TRY(cuda_fail(cudaStreamWaitEvent(o.s, ev[1 + b], 0), "wait inputs"));
-        if (b == 0 && st->form_factors) TRY(cuda_fail(cudaStreamWaitEvent(o.s, ev_f, 0), "wait f"));
-        if (st->q_vectors)
-            TRY(run_direct(d_pos + t0 * frame_pos, N, st->species ? nullptr : d_ff, st->species, st->q_vectors, n_q,
-                           t1 - t0, st->box_L, d_I + t0 * frame_i, &io, 0));
-        else
-            TRY(run_volume(d_pos + t0 * frame_pos, N, st->species ? nullptr : d_ff, st->species, &vol, t1 - t0,
-                           d_I + t0 * frame_i, &io, 0));
-        TRY(cuda_fail(cudaEventRecord(ev[1 + n_bat + b], o.s), "event"));
-        if (st->I_out) {
-            TRY(cuda_fail(cudaStreamWaitEvent(hr->d2h, ev[1 + n_bat + b], 0), "wait I"));
-            TRY(cuda_fail(cudaMemcpyAsync((char*)st->I_out + t0 * frame_i, d_I + t0 * frame_i, (size_t)(t1 - t0) * frame_i,
-                                          cudaMemcpyDeviceToHost, hr->d2h), "D2H I"));
+    TRY(cuda_fail(cudaStreamWaitEvent(hr->red, ev_fork, 0), "fork"));
+    // from here on every exit joins the three side streams back into o.s
+    auto body = [&]() -> int {
+        if (st->form_factors) {
+            TRY(cuda_fail(cudaMemcpyAsync(d_ff, st->form_factors, pin * (size_t)N, cudaMemcpyHostToDevice, hr->h2d), "H2D f"));
+            TRY(cuda_fail(cudaEventRecord(ev_f, hr->h2d), "event"));
         }
-    }
-    // reductions: g2 (+ its ring means) on the caller's stream, its (largest) result streaming back while the S rings
-    // and XSVS run concurrently on the side stream
-    xpcs_opts ro = io;
-    ro.in_dtype = io.out_dtype;                  // the series fed to the reductions is I (out_dtype)
-    xpcs_opts so = ro;
-    so.stream = (void*)hr->red;
-    TRY(cuda_fail(cudaStreamWaitEvent(hr->red, ev[2 * n_bat], 0), "fork reductions"));   // the last batch's I
-    if (st->S_rings) TRY(xpcs_structure_factor_shells(d_I, T, n_q, st->form_factors ? (const void*)d_ff : nullptr, N,
-                                                      st->bin_of_q, st->n_bins, d_sr, &so));
-    if (st->n_windows && st->beta)
-        TRY(xsvs_contrast(d_I, T, n_q, st->bin_of_q, st->n_bins, st->windows, st->n_windows, d_beta, &so));
-    TRY(cuda_fail(cudaEventRecord(ev_red, hr->red), "event"));
-    if (st->n_lags) {
-        TRY(xpcs_g2(d_I, T, n_q, st->lags, st->n_lags, d_g2, &ro));
-        TRY(cuda_fail(cudaEventRecord(ev_g2, o.s), "event"));
-        if (st->g2_out) {
-            TRY(cuda_fail(cudaStreamWaitEvent(hr->d2h, ev_g2, 0), "wait g2"));
-            TRY(cuda_fail(cudaMemcpyAsync(st->g2_out, d_g2, g2_bytes, cudaMemcpyDeviceToHost, hr->d2h), "D2H g2"));
+        if (n_kinds > 0)
+            TRY(cuda_fail(launch_fill_rows(d_fq, o.in_f64 ? 1 : 0, n_kinds, n_q, kval.data(), o.s), "kind form factors"));
+        const size_t frame_pos = pin * 3 * (size_t)N, frame_i = pout * (size_t)n_q;
+        for (int64_t b = 0; b < n_bat; ++b) {
+            const int64_t t0 = b * T / n_bat, t1 = (b + 1) * T / n_bat;
+            TRY(cuda_fail(cudaMemcpyAsync(d_pos + t0 * frame_pos, (const char*)st->positions + t0 * frame_pos,
+                                          (size_t)(t1 - t0) * frame_pos, cudaMemcpyHostToDevice, hr->h2d), "H2D positions"));
+            TRY(cuda_fail(cudaEventRecord(ev[1 + b], hr->h2d), "event"));
         }
-        if (st->g2_rings) {
-            xpcs_opts go = ro;
-            go.in_dtype = io.out_dtype;
-            TRY(xpcs_shell_mean(d_g2, st->n_lags, n_q, st->bin_of_q, st->n_bins, 1.0, d_g2r, &go));
+        xpcs_opts io{};
+        io.in_dtype = o.in_f64 ? XPCS_F64 : XPCS_F32;
+        io.out_dtype = o.out_f64 ? XPCS_F64 : XPCS_F32;
+        io.stream = (void*)o.s;
+        io.engine = o.engine;
+        io.profile = o.profile ? 1 : 0;
+        io.workspace = o.workspace;
+        xpcs_qvolume vol;
+        std::memset(&vol, 0, sizeof(vol));
+        vol.plane = st->grid;
+        vol.n_l = 1;
+        const void* ff_int = species ? nullptr : d_ff;     // per-atom f inside the contraction (no kinds)
+        for (int64_t b = 0; b < n_bat; ++b) {
+            const int64_t t0 = b * T / n_bat, t1 = (b + 1) * T / n_bat;
+            TRY(cuda_fail(cudaStreamWaitEvent(o.s, ev[1 + b], 0), "wait inputs"));
+            if (b == 0 && st->form_factors) TRY(cuda_fail(cudaStreamWaitEvent(o.s, ev_f, 0), "wait f"));
+            if (st->q_vectors)
+                TRY(run_direct(d_pos + t0 * frame_pos, N, ff_int, species, st->q_vectors, n_q, t1 - t0, st->box_L,
+                               d_I + t0 * frame_i, &io, 0));
+            else
+                TRY(run_volume(d_pos + t0 * frame_pos, N, ff_int, species, &vol, t1 - t0, d_I + t0 * frame_i, &io, 0));
+            TRY(cuda_fail(cudaEventRecord(ev[1 + n_bat + b], o.s), "event"));
+            if (st->I_out) {
+                TRY(cuda_fail(cudaStreamWaitEvent(hr->d2h, ev[1 + n_bat + b], 0), "wait I"));
+                TRY(cuda_fail(cudaMemcpyAsync((char*)st->I_out + t0 * frame_i, d_I + t0 * frame_i, (size_t)(t1 - t0) * frame_i,
+                                              cudaMemcpyDeviceToHost, hr->d2h), "D2H I"));
+            }
         }
+        // reductions: g2 (+ its ring means) on the caller's stream, its (largest) result streaming back while the S
+        // rings and XSVS run concurrently on the side stream
+        xpcs_opts ro = io;
+        ro.in_dtype = io.out_dtype;                  // the series fed to the reductions is I (out_dtype)
+        xpcs_opts so = ro;
+        so.stream = (void*)hr->red;
+        Opts so_o;
+        TRY(parse_opts(&so, so_o));
+        TRY(cuda_fail(cudaStreamWaitEvent(hr->red, ev[2 * n_bat], 0), "fork reductions"));   // the last batch's I
+        if (st->form_factors) TRY(cuda_fail(cudaStreamWaitEvent(hr->red, ev_f, 0), "wait f"));
+        // S(q,t) normalisation sum f^2 from the caller's form factors, read at THEIR dtype (in_dtype)
+        if (st->S_rings) TRY(structure_factor_shells(d_I, T, n_q, st->form_factors ? (const void*)d_ff : nullptr,
+                                                     o.in_f64 ? 1 : 0, N, st->bin_of_q, st->n_bins, d_sr, so_o));
+        if (st->n_windows && st->beta)
+            TRY(xsvs_contrast(d_I, T, n_q, st->bin_of_q, st->n_bins, st->windows, st->n_windows, d_beta, &so));
+        if (st->n_lags) {
+            TRY(xpcs_g2(d_I, T, n_q, st->lags, st->n_lags, d_g2, &ro));
+            TRY(cuda_fail(cudaEventRecord(ev_g2, o.s), "event"));
+            if (st->g2_out) {
+                TRY(cuda_fail(cudaStreamWaitEvent(hr->d2h, ev_g2, 0), "wait g2"));
+                TRY(cuda_fail(cudaMemcpyAsync(st->g2_out, d_g2, g2_bytes, cudaMemcpyDeviceToHost, hr->d2h), "D2H g2"));
+            }
+            if (st->g2_rings) {
+                xpcs_opts go = ro;
+                go.in_dtype = io.out_dtype;
+                TRY(xpcs_shell_mean(d_g2, st->n_lags, n_q, st->bin_of_q, st->n_bins, 1.0, d_g2r, &go));
+            }
+        }
+        return XPCS_OK;
+    };
+    const int rc = body();
+    // join: the reductions' side stream first (the small results are copied back after it on o.s), then the copies
+    cudaEventRecord(ev_red, hr->red);
+    cudaStreamWaitEvent(o.s, ev_red, 0);
+    if (rc == XPCS_OK) {
+        // small results back on the caller's stream (after the reductions)
+        if (st->S_rings)
+            TRY(cuda_fail(cudaMemcpyAsync(st->S_rings, d_sr, sizeof(double) * (size_t)T * nb, cudaMemcpyDeviceToHost, o.s), "D2H S"));
+        if (st->n_lags && st->g2_rings)
+            TRY(cuda_fail(cudaMemcpyAsync(st->g2_rings, d_g2r, sizeof(double) * (size_t)st->n_lags * nb,
+                                          cudaMemcpyDeviceToHost, o.s), "D2H g2 rings"));
+        if (st->n_windows && st->beta)
+            TRY(cuda_fail(cudaMemcpyAsync(st->beta, d_beta, sizeof(double) * (size_t)st->n_windows * nb,
+                                          cudaMemcpyDeviceToHost, o.s), "D2H beta"));
     }
-    TRY(cuda_fail(cudaStreamWaitEvent(o.s, ev_red, 0), "join reductions"));
-    // small results back on the caller's stream (after the reductions), then join the copy streams
-    if (st->S_rings)
-        TRY(cuda_fail(cudaMemcpyAsync(st->S_rings, d_sr, sizeof(double) * (size_t)T * nb, cudaMemcpyDeviceToHost, o.s), "D2H S"));
-    if (st->n_lags && st->g2_rings)
-        TRY(cuda_fail(cudaMemcpyAsync(st->g2_rings, d_g2r, sizeof(double) * (size_t)st->n_lags * nb,
-                                      cudaMemcpyDeviceToHost, o.s), "D2H g2 rings"));
-    if (st->n_windows && st->beta)
-        TRY(cuda_fail(cudaMemcpyAsync(st->beta, d_beta, sizeof(double) * (size_t)st->n_windows * nb,
-                                      cudaMemcpyDeviceToHost, o.s), "D2H beta"));
-    TRY(cuda_fail(cudaEventRecord(ev_d2h, hr->d2h), "event"));
-    TRY(cuda_fail(cudaStreamWaitEvent(o.s, ev_d2h, 0), "join"));
-    TRY(cuda_fail(cudaStreamWaitEvent(o.s, ev_h2d, 0), "join"));
-    return XPCS_OK;
+    cudaEventRecord(ev_d2h, hr->d2h);
+    cudaStreamWaitEvent(o.s, ev_d2h, 0);
+    cudaEventRecord(ev_h2d, hr->h2d);
+    cudaStreamWaitEvent(o.s, ev_h2d, 0);
+    if (rc != XPCS_OK) return rc;
+    return check_sticky();
 }
 
 // ------------------------------------------------------------------------------------------- geometry

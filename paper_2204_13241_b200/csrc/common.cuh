@@ -18,9 +18,12 @@ void note_launch(int n = 1);
 // Scratch cached per (stream, slot); grown on demand (the grow synchronises the device).
 enum ScratchSlot {
     SS_STAGE = 0, SS_PARTIAL, SS_PLAN, SS_PLAN2, SS_XSVS, SS_SMALL, SS_LAGS, SS_TC, SS_IDX, SS_FFT,
-    SS_H_POS, SS_H_FF, SS_H_I, SS_H_G2, SS_H_RED, SS_FIX, SS_COUNT
+    SS_H_POS, SS_H_FF, SS_H_I, SS_H_G2, SS_H_RED, SS_FIX, SS_H_FQ, SS_COUNT
 };
 void* scratch(cudaStream_t s, int slot, size_t bytes);   // nullptr on failure (error already set)
+// workspace id of the calling thread's current API call (xpcs_opts.workspace): scratch is keyed by (device, workspace,
+// stream, slot); set by parse_opts at the start of every call
+void set_workspace(int ws);
 void release_scratch();
 
 // Profiling: events around launches of one kernel class on a stream (opts->profile).
@@ -36,8 +39,9 @@ struct ProfScope {
 int sm_count();
 int generic_q_per_block();    // k_generic32 tile: q per CTA
 int generic_blocks_per_sm();  // k_generic32: CTAs per SM its registers are sized for
-const void* host_table(const void* data, size_t bytes);    // cached device copy of a host table (by content)
-const int32_t* lag_table(const int32_t* lags, int64_t n);   // host_table of a lag list
+// cached device copy of a host table (by content); pinned if handed out during a capture on s
+const void* host_table(const void* data, size_t bytes, cudaStream_t s);
+const int32_t* lag_table(const int32_t* lags, int64_t n, cudaStream_t s);   // host_table of a lag list
 
 // ------------------------------------------------------------------------------------------------
 // device helpers
@@ -147,6 +151,8 @@ struct SpeciesParts {
     int part_f64;
 };
 struct BrightSink;
+// rows of constants: out[r][i] = vals[r] (f32 | f64), n_rows <= kMaxKinds (kind form factors of xpcs_step_host)
+cudaError_t launch_fill_rows(void* out, int out_f64, int n_rows, int64_t n, const double* vals, cudaStream_t s);
 cudaError_t launch_species_combine(const SpeciesParts& sp, int64_t frames, int64_t n_q, const void* fq, int fq_f64,
                                    int64_t v0, int64_t n_l, void* out, int out_f64, int mode, cudaStream_t s,
                                    const BrightSink* bright = nullptr);

@@ -69,6 +69,13 @@ __global__ void __launch_bounds__(256) k_form_factor_gaussian(const Q* __restric
     }
 }
 
+struct RowVals { double v[kMaxKinds]; };
+template <typename O>
+__global__ void __launch_bounds__(256) k_fill_rows(O* __restrict__ out, int n_rows, int64_t n, RowVals rv) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_rows * n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (O)rv.v[i / n];
+}
+
 static dim3 grid_n(int64_t total) {
     int64_t b = (total + 255) / 256;
     const int64_t cap = (int64_t)sm_count() * 16;
@@ -91,6 +98,17 @@ cudaError_t launch_species_combine(const SpeciesParts& sp, int64_t frames, int64
         else { if (out_f64) XPCS_SPC(float2, float, double); else XPCS_SPC(float2, float, float); }
     }
 #undef XPCS_SPC
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill_rows(void* out, int out_f64, int n_rows, int64_t n, const double* vals, cudaStream_t s) {
+    if (n_rows < 1 || n_rows > kMaxKinds) return cudaErrorInvalidValue;
+    RowVals rv{};
+    for (int r = 0; r < n_rows; ++r) rv.v[r] = vals[r];
+    const dim3 gr = grid_n(n_rows * n);
+    note_launch();
+    if (out_f64) k_fill_rows<double><<<gr, 256, 0, s>>>((double*)out, n_rows, n, rv);
+    else k_fill_rows<float><<<gr, 256, 0, s>>>((float*)out, n_rows, n, rv);
     return cudaGetLastError();
 }
 

@@ -34,28 +34,51 @@ void note_launch(int n) { g_launches.fetch_add(n); }
 long long launches() { return g_launches.load(); }
 
 // ---------------------------------------------------------------- scratch
-struct Buf { void* p = nullptr; size_t n = 0; };
-// keyed by (device, stream, slot): the legacy default stream (NULL) is the same handle on every device
-static std::map<std::pair<std::pair<int, cudaStream_t>, int>, Buf> g_scratch;
+// Buffers keyed by (device, workspace, stream, slot).  A buffer that was handed out during a CUDA graph capture is
+// referenced by that graph's nodes: when the slot later has to grow it is RETIRED (kept until xpcs_release) rather
+// than freed, so replaying the old graph never touches freed memory.
+struct Buf { void* p = nullptr; size_t n = 0; bool captured = false; };
+struct ScratchKey {
+    int dev, ws;
+    cudaStream_t s;
+    int slot;
+    bool operator<(const ScratchKey& o) const {
+        if (dev != o.dev) return dev < o.dev;
+        if (ws != o.ws) return ws < o.ws;
+        if (s != o.s) return s < o.s;
+        return slot < o.slot;
+    }
+};
+static std::map<ScratchKey, Buf> g_scratch;
+static std::vector<std::pair<int, void*>> g_retired;   // (device, buffer) of grown slots that a graph may reference
+static thread_local int g_ws = 0;
+
+void set_workspace(int ws) { g_ws = ws; }
 
 void* scratch(cudaStream_t s, int slot, size_t bytes) {
     std::lock_guard<std::mutex> lk(g_mu);
     int dev = 0;
     cudaGetDevice(&dev);
-    Buf& b = g_scratch[{{dev, s}, slot}];
+    Buf& b = g_scratch[ScratchKey{dev, g_ws, s, slot}];
     if (bytes == 0) bytes = 16;
-    if (b.n >= bytes) return b.p;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+    const bool capturing = cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
+    if (b.n >= bytes) {
+        if (capturing) b.captured = true;
+        return b.p;
+    }
+    if (capturing) {
         // no allocation inside a CUDA graph capture: run the same call once outside the capture first
         set_error("xpcs: scratch slot %d must grow to %zu bytes during graph capture (warm up outside the capture)", slot, bytes);
         return nullptr;
     }
     if (b.p) {
         cudaStreamSynchronize(s);      // the old buffer may still be in use by queued work on s
-        cudaFree(b.p);
+        if (b.captured) g_retired.push_back({dev, b.p});   // a captured graph may still replay with it
+        else cudaFree(b.p);
         b.p = nullptr;
         b.n = 0;
+        b.captured = false;
     }
     size_t want = bytes + bytes / 8;  // grow with slack
     cudaError_t e = cudaMalloc(&b.p, want);
@@ -80,12 +103,18 @@ void release_scratch() {
     cudaGetDevice(&cur);
     for (auto& kv : g_scratch) {
         if (!kv.second.p) continue;
-        cudaSetDevice(kv.first.first.first);
+        cudaSetDevice(kv.first.dev);
         cudaDeviceSynchronize();
         cudaFree(kv.second.p);
     }
+    for (auto& r : g_retired) {
+        cudaSetDevice(r.first);
+        cudaDeviceSynchronize();
+        cudaFree(r.second);
+    }
     cudaSetDevice(cur);
     g_scratch.clear();
+    g_retired.clear();
 }
 
 int sm_count() {   // of the current device (cached per device)
@@ -105,10 +134,13 @@ int sm_count() {   // of the current device (cached per device)
 // ---------------------------------------------------------------- host tables
 // device copies of small host tables (lag lists, species permutations), cached by content per device: the upload
 // is synchronous and happens once per distinct table, so calls inside a CUDA graph capture (after one call outside
-// it) carry no pageable host-memory copy.  At most kTables entries; evicting one synchronises the device.
+// it) carry no pageable host-memory copy.  At most kTables entries (more while every entry is pinned); an entry
+// handed out during a capture on `s` is pinned (the graph holds its pointer) and never evicted before release;
+// evicting an unpinned one synchronises its own device first.
 constexpr size_t kTables = 32;
-const void* host_table(const void* data, size_t bytes) {
-    struct Entry { int dev; uint64_t h; std::vector<unsigned char> v; void* d; };
+const void* host_table(const void* data, size_t bytes, cudaStream_t s) {
+    // pinned: handed out during a graph capture (the graph holds the pointer) -> never evicted before release
+    struct Entry { int dev; uint64_t h; std::vector<unsigned char> v; void* d; bool pinned; };
     static std::vector<Entry> tab;
     uint64_t h = 1469598103934665603ull ^ bytes;   // FNV-1a over 64-bit words (then the tail bytes)
     const unsigned char* p = (const unsigned char*)data;
@@ -123,21 +155,29 @@ const void* host_table(const void* data, size_t bytes) {
     std::lock_guard<std::mutex> lk(g_mu);
     int dev = 0;
     cudaGetDevice(&dev);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    const bool pin = cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
     for (size_t k = 0; k < tab.size(); ++k) {
         Entry& e = tab[k];
         if (e.dev == dev && e.h == h && e.v.size() == bytes && std::memcmp(e.v.data(), data, bytes) == 0) {
+            if (pin) e.pinned = true;
             if (k + 1 < tab.size()) std::rotate(tab.begin() + k, tab.begin() + k + 1, tab.end());   // most recent last
             return tab.back().d;
         }
     }
     if (tab.size() >= kTables) {
-        cudaDeviceSynchronize();
-        int d0 = 0;
-        cudaGetDevice(&d0);
-        cudaSetDevice(tab.front().dev);
-        cudaFree(tab.front().d);
-        cudaSetDevice(d0);
-        tab.erase(tab.begin());
+        // evict the least recently used entry that no captured graph references; synchronise its own device first
+        for (size_t k = 0; k < tab.size(); ++k) {
+            if (tab[k].pinned) continue;
+            int d0 = 0;
+            cudaGetDevice(&d0);
+            cudaSetDevice(tab[k].dev);
+            cudaDeviceSynchronize();
+            cudaFree(tab[k].d);
+            cudaSetDevice(d0);
+            tab.erase(tab.begin() + (long)k);
+            break;
+        }
     }
     void* d = nullptr;
     cudaError_t e = cudaMalloc(&d, std::max<size_t>(bytes, 16));
@@ -149,11 +189,11 @@ const void* host_table(const void* data, size_t bytes) {
                   cudaGetErrorString(e));
         return nullptr;
     }
-    tab.push_back({dev, h, std::vector<unsigned char>(p, p + bytes), d});
+    tab.push_back({dev, h, std::vector<unsigned char>(p, p + bytes), d, pin});
     return d;
 }
-const int32_t* lag_table(const int32_t* lags, int64_t n) {
-    return (const int32_t*)host_table(lags, sizeof(int32_t) * (size_t)n);
+const int32_t* lag_table(const int32_t* lags, int64_t n, cudaStream_t s) {
+    return (const int32_t*)host_table(lags, sizeof(int32_t) * (size_t)n, s);
 }
 
 // ---------------------------------------------------------------- profiling

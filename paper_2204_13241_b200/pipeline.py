@@ -73,6 +73,9 @@ class Pipeline:
         # GPU alone: they run concurrently on two side streams and the caller's stream, joined before returning
         self.s_red = [torch.cuda.Stream(self.device), torch.cuda.Stream(self.device)] if self.device.type == "cuda" else None
         self.serial_reductions = False      # True: all reductions on the caller's stream (per-kernel timing)
+        # own library scratch (xpcs_opts.workspace): pipelines replayed concurrently never share buffers, even when
+        # torch hands out recycled pool streams
+        self.ws = X.new_workspace()
 
     def close(self):
         """Free the registered ring plan (the bins tensor dies with the pipeline; a stale plan must not outlive it)."""
@@ -91,6 +94,10 @@ class Pipeline:
         return int(self.wl.N) * int(self.n_q) * int(self.wl.T)
 
     def run(self, positions: torch.Tensor, form_factors: torch.Tensor | None, profile=False) -> dict:
+        with X.workspace(self.ws):
+            return self._run(positions, form_factors, profile)
+
+    def _run(self, positions, form_factors, profile):
         wl, s = self.wl, self.stream
         if self.kind_fq is not None:
             X.xpcs_intensity_volume(positions, None, self.vol, species=wl.kinds, f_q=self.kind_fq, out=self.I,
@@ -177,6 +184,10 @@ class Pipeline:
         """End to end from pinned host memory: one `xpcs_step_host` call (the C ABI's host-buffer entry: frame-batched
         H2D / intensity / D2H overlap on internal copy streams, then g2, rings and XSVS and their D2H), enqueued on
         the current stream (lattice planes and explicit q lists)."""
+        with X.workspace(self.ws):
+            return self._run_host()
+
+    def _run_host(self):
         wl = self.wl
         main = torch.cuda.current_stream(self.device)
         h = self.h_out

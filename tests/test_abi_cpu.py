@@ -166,7 +166,7 @@ def test_species_engine_rule():
     assert se([500, 500], [1.0, 2.0]) == [500, 125]            # c3/c5: f = 1 half + a quarter of the f = 2 half
     assert se([300, 700], [2.0, 1.0]) == [75, 700]
     assert se([400, 400, 200], [1.0, 1.0, 1.0]) == [400, 400, 200]
-    assert se([10, 10], None) == [10, 10]                      # no hints: every kind
+    assert se([10, 10], None) == [0, 0]                        # no hints: every kind on split-FP16
     assert se([0, 100], [0.5, 1.0])[1] == 100                  # an empty kind does not set the reference weight
 
 
@@ -193,6 +193,17 @@ def test_step_host_validation_before_launch(lib):
     st.batches = 0
     assert lib.xpcs_step_host(ctypes.byref(st), ctypes.byref(o)) == _lib.XPCS_EINVAL
     st.batches = 2
+    # the limits of the calls inside the step are checked up front too (an error after the stream fork
+    # left the copy streams unjoined): a lag beyond the g2 kernel's 640, too many rings
+    st.frames = 1000
+    big, bp = _lib._i32_array([700])
+    st.lags, st.n_lags = bp, 1
+    assert lib.xpcs_step_host(ctypes.byref(st), ctypes.byref(o)) == _lib.XPCS_EUNSUPPORTED
+    st.n_lags = 0
+    st.n_bins = 20000
+    assert lib.xpcs_step_host(ctypes.byref(st), ctypes.byref(o)) == _lib.XPCS_EINVAL
+    st.n_bins = 4
+    st.frames = 10
     st.positions = None
     assert lib.xpcs_step_host(ctypes.byref(st), ctypes.byref(o)) == _lib.XPCS_EINVAL
     assert lib.xpcs_launch_count() == n0

@@ -149,3 +149,42 @@ def test_moments_empty_rings_are_nan():
     assert np.array_equal(np.isnan(beta), np.isnan(ref))
     ok = ~np.isnan(ref)
     np.testing.assert_allclose(beta[ok], ref[ok], rtol=1e-12)
+
+
+def test_graph_survives_scratch_growth_and_stream_reuse():
+    """a captured graph holds raw scratch pointers.  After the capture, a larger eager call on the SAME
+    stream and workspace grows the same scratch slots: the buffers the graph uses must be retired (kept until
+    xpcs_release), not freed, so replaying the graph still gives the eager result bit for bit.  A pipeline with its
+    own workspace on a (possibly recycled) stream must not disturb it either."""
+    cfg = _cfg(False)
+    pos = torch.from_numpy(xi.positions(cfg)).to(DEV)
+    grid = xp.lattice_plane(cfg.L, 96)
+    ws = xp.new_workspace()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with xp.workspace(ws), torch.cuda.stream(s):
+        ref = xp.xpcs_intensity_grid(pos, None, grid, stream=s).clone()       # sizes the scratch (eager)
+        g2ref = xp.xpcs_g2(ref, [1, 2, 3], stream=s).clone()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with xp.workspace(ws), torch.cuda.graph(g, stream=s):
+        out = xp.xpcs_intensity_grid(pos, None, grid, stream=s)
+        g2 = xp.xpcs_g2(out, [1, 2, 3], stream=s)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref) and torch.equal(g2, g2ref)
+    big = xi.scaled(cfg, N=9000, T=60)
+    pos_big = torch.from_numpy(xi.positions(big)).to(DEV)
+    with xp.workspace(ws), torch.cuda.stream(s):                            # same key: the slots grow
+        Ib = xp.xpcs_intensity_grid(pos_big, None, xp.lattice_plane(big.L, 200), stream=s)
+        xp.xpcs_g2(Ib, list(range(1, 40)), stream=s)
+    Q = pipeline.Pipeline(pipeline.workload_from_config(big))
+    Q.run(pos_big, None)
+    torch.cuda.synchronize()
+    out.zero_()
+    g2.zero_()
+    for _ in range(2):
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref) and torch.equal(g2, g2ref)
+    Q.close()

@@ -264,3 +264,38 @@ def test_end_to_end_host_path_matches_device_path():
                 np.testing.assert_array_equal(host[k].numpy(), first[k], err_msg=k)
     h2d, d2h = P.io_bytes()
     assert h2d == pos.nbytes + f.nbytes and d2h > pos.shape[0] * 128 * 128 * 4
+
+
+@pytest.mark.parametrize("out_dtype", [xp.F32, xp.F64])
+def test_step_host_mixed_dtypes_and_host_kinds(out_dtype):
+    """xpcs_step_host straight through the C ABI with f32 inputs, f32 or f64 outputs and per-atom HOST form factors
+    f in {1, 2} (no species): the library runs the two values as atom kinds (integer engine for the light kind) and
+    normalises S(q,t) by sum f^2 read at the INPUT dtype (it was read at the output dtype).  I against
+    the oracle at the per-pixel gate; S rings, g2 and beta against the oracle's reductions of the returned I."""
+    cfg = xi.scaled(xi.CONFIGS["c3"], N=6000, T=12)
+    pos = np.ascontiguousarray(xi.positions(cfg))
+    f = xi.form_factors(cfg).astype(np.float32)
+    n = 96
+    g = xp.lattice_plane(cfg.L, n)
+    bins_h = oracle.lattice_bins(n, 32 if n % 64 == 0 else 16)
+    nb = int(bins_h.max()) + 1
+    bins = _t(bins_h)
+    T, n_q = cfg.T, n * n
+    od = np.float64 if out_dtype == xp.F64 else np.float32
+    pos_p = torch.from_numpy(pos).pin_memory()
+    f_p = torch.from_numpy(f).pin_memory()
+    I = torch.empty((T, n_q), dtype=torch.float64 if out_dtype == xp.F64 else torch.float32).pin_memory()
+    S = torch.empty((T, nb), dtype=torch.float64).pin_memory()
+    g2 = torch.empty((3, n_q), dtype=I.dtype).pin_memory()
+    beta = torch.empty((3, nb), dtype=torch.float64).pin_memory()
+    keep = xp.xpcs_step_host(pos_p, f_p, g, bins, nb, lags=(1, 2, 5), windows=(1, 2, 4), I_out=I, g2_out=g2,
+                             S_rings=S, beta=beta, batches=3, out_dtype=out_dtype)
+    torch.cuda.synchronize()
+    del keep
+    Ih = I.numpy()
+    assert Ih.dtype == od
+    ref = oracle.intensity(pos, f.astype(np.float64), _grid_q(g), cfg.L)
+    assert_pixels(Ih, ref, cfg.N, "step_host host kinds")
+    assert_rel(S.numpy(), oracle.structure_factor_shells(Ih, f, cfg.N, bins_h, nb), 1e-10, "S rings (sum f^2 norm)")
+    assert_rel(g2.numpy(), oracle.g2(Ih, (1, 2, 5)).astype(od), 1e-6 if od == np.float32 else 1e-10, "g2")
+    assert_rel(beta.numpy(), oracle.xsvs_beta(Ih, bins_h, nb, (1, 2, 4)), 1e-10, "beta")
