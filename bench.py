@@ -9,8 +9,9 @@ pixel of every frame, g2 for all lags, ring-averaged S(q,t) and g2, XSVS contras
 Default workload = BASELINE.json configs[2] ("c3": N = 262144 atoms of two species, 1000 Brownian frames, 512 x 512
 lattice plane, g2 tau = 1..200), the largest configuration that fits one GPU (BASELINE.json quotes its metric on no
 config; c3 is 6.9e13 pairs per step, c2 2.1e11).  Metric: atom.q pairs/s for I(q,t) (whole job, all ranks).
-Multi-GPU = weak scaling: every rank processes its own independent trajectory (no data-path collective);
---qslab splits one trajectory's detector across the ranks instead.
+Multi-GPU (torchrun, N > 1): ONE trajectory with the detector split across the ranks and the ring / XSVS moments
+all-reduced once per step (SURVEY 8(e), strong scaling); --replicas runs independent trajectories instead (weak
+scaling, no data-path collective).
 """
 from __future__ import annotations
 
@@ -276,25 +277,32 @@ def cpu_baseline(cfg, budget_s):
             "sample": f"{cfg.name} frame 0, {len(pix)} seeded pixels x {cfg.N} atoms ({pairs:.3g} pairs, {dt:.1f} s)"}
 
 
-def run_qslab(args, cfg, ws, rank, dev, dist):
-    """--qslab: every rank holds the same trajectory and computes its slab of detector rows; one NCCL all-reduce of
-    the ring / XSVS moments per step; value = the whole detector's pairs / the max-over-ranks step time."""
+def run_qshard(args, cfg, ws, rank, dev, dist):
+    """N > 1 (default): ONE trajectory, the detector split across the ranks (pipeline.QShardPipeline: tile-aligned 2-D
+    q-blocks of a lattice plane, pixel ranges of an explicit q list); every rank computes I and g2 of its
+    block and the ring / XSVS moments, one NCCL all-reduce of the moments per step (the path's only exchange), ring
+    results from the sums.  Strong scaling: value = the whole detector's pairs / the max-over-ranks step time.
+    e2e: per rank, the pinned positions copied in, the step, and the block's I plus the ring results copied out."""
     import torch
     import paper_2204_13241_b200 as xp
     from paper_2204_13241_b200 import pipeline
     from paper_2204_13241_b200 import dist as xd
-    assert cfg.n_plane and not cfg.two_species, "--qslab: lattice configs with unit form factors (c2)"
     wl = pipeline.workload_from_config(cfg, device=dev)
     wl.engine = {"auto": xp.ENGINE_AUTO, "simt": xp.ENGINE_SIMT, "tensor": xp.ENGINE_TENSOR,
                  "i8": xp.ENGINE_TENSOR_I8}[args.engine]
-    Q = pipeline.QSlabPipeline(wl, rank, ws, device=dev)
-    pos_d = torch.from_numpy(xi.positions(cfg)).to(dev)
+    Q = pipeline.QShardPipeline(wl, rank, ws, device=dev)
+    pos_h = xi.positions(cfg)
+    f_h = xi.form_factors(cfg) if cfg.two_species else None
+    pos_d = torch.from_numpy(pos_h).to(dev)
+    f_d = torch.from_numpy(f_h).to(dev) if f_h is not None else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     for _ in range(args.warmup):
-        Q.run(pos_d, None)
+        Q.run(pos_d, f_d)
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
     t_ms = []
+    xp.profile_reset()
+    n0 = xp.launch_count()
     with ClockSampler(dev.index) as clk:
         for _ in range(args.steps):
             flush.zero_()
@@ -304,22 +312,61 @@ def run_qslab(args, cfg, ws, rank, dev, dist):
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            Q.run(pos_d, None)
+            Q.run(pos_d, f_d, profile=True)
             b.record(stream)
             torch.cuda.synchronize()
             t_ms.append(a.elapsed_time(b))
+    n_launch = xp.launch_count() - n0
+    prof = xp.profile_query()
     ms = xd.max_over_ranks(float(np.mean(t_ms)), dev)
-    pairs = int(cfg.N) * int(cfg.n_plane) ** 2 * int(cfg.T)
+    peaks, peak_src = _peaks()
+    sm_count, _ = xp.device_info()
+    roof, eng_name, dtype = _roofline(cfg, wl, wl.engine, f_h, prof, Q.pairs_per_step, args.steps, float(np.mean(t_ms)),
+                                      peaks, peak_src, sm_count, clk.summary(), xp)
+    roof["note"] = "rank 0's block: its own pairs and kernel time"
+    pairs = int(cfg.N) * int(Q.wl.q.shape[0] if cfg.n_plane == 0 else cfg.n_plane ** 2) * int(cfg.T)
+    # end to end: pinned positions in, the step, this rank's I block and the ring results out, every step
+    e2e = None
+    if not args.no_e2e:
+        h_pos = torch.from_numpy(pos_h).pin_memory()
+        h_f = torch.from_numpy(f_h).pin_memory() if f_h is not None else None
+        h_I = torch.empty(Q.I.shape, dtype=Q.I.dtype).pin_memory()
+        t_e = []
+        for _ in range(max(2, args.steps)):
+            if dist is not None:
+                dist.barrier()
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            pos_d.copy_(h_pos, non_blocking=True)
+            if h_f is not None:
+                f_d.copy_(h_f, non_blocking=True)
+            res = Q.run(pos_d, f_d)
+            h_I.copy_(Q.I, non_blocking=True)
+            small = {k: v.to("cpu", non_blocking=True) for k, v in res.items() if k in ("S_rings", "g2_rings", "beta")}
+            b.record(stream)
+            torch.cuda.synchronize()
+            t_e.append(a.elapsed_time(b))
+        e_ms = xd.max_over_ranks(float(np.mean(t_e)), dev)
+        d2h = h_I.numel() * h_I.element_size() + sum(v.numel() * v.element_size() for v in small.values())
+        e2e = {"value": pairs / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms,
+               "mode": "per rank: pinned positions in, the q-shard step, its I block and the ring results out",
+               "h2d_bytes_per_step": int(pos_h.nbytes + (f_h.nbytes if f_h is not None else 0)),
+               "d2h_bytes_per_step": int(d2h)}
     if rank == 0:
         line = {"metric": METRIC, "value": pairs / (ms / 1e3), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-                "vs_baseline": None, "dtype": "f32", "data": "synthetic", "mode": "qslab",
-                "config": {"workload": cfg.name, "N": cfg.N, "n_q": cfg.n_plane ** 2, "frames": cfg.T,
-                           "parallelism": f"q-slab x{ws} (one trajectory, detector rows split, moments all-reduced)",
-                           "rows_per_rank": [xd.qslab(cfg.n_plane, -cfg.n_plane // 2, r, ws)[1] for r in range(ws)],
-                           "allreduce_bytes": int(Q.mom.numel() * 8),
+                "vs_baseline": None, "dtype": dtype, "data": "synthetic", "mode": "qshard",
+                "config": {"workload": cfg.name, "N": cfg.N, "frames": cfg.T,
+                           "n_q": int(cfg.n_plane ** 2 if cfg.n_plane else Q.wl.q.shape[0]),
+                           "parallelism": f"q-shard x{ws} (one trajectory; detector blocks per rank; ring / XSVS "
+                                          f"moments all-reduced once per step)",
+                           "block_rank0": list(Q.block), "allreduce_bytes": int(Q.mom.numel() * 8),
                            "l2": "flushed between timed steps (256 MB write, untimed)"},
-                "e2e": None, "clocks": clk.summary(), "step_ms_all": t_ms}
+                "roofline": roof, "e2e": e2e, "gpu_launches": int(n_launch), "clocks": clk.summary(),
+                "step_ms_all": t_ms, "engine_used": eng_name,
+                "kernel_ms_rank0": {k: v[0] / max(args.steps, 1) for k, v in prof.items()}}
         print(json.dumps(line), flush=True)
     Q.close()
     if dist is not None:
@@ -378,9 +425,11 @@ def main():
                          "else 2)")
     ap.add_argument("--e2e-batches", type=int, default=4, help="frame batches per step in the end-to-end figure")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of replaying its CUDA graph")
-    ap.add_argument("--qslab", action="store_true",
-                    help="strong scaling: ONE trajectory, the detector split into row slabs across the ranks, ring "
-                         "moments all-reduced once per step (SURVEY 8(e)); lattice configs without species")
+    ap.add_argument("--qslab", "--qshard", dest="qshard", action="store_true",
+                    help="ONE trajectory, the detector split into blocks across the ranks, ring moments all-reduced "
+                         "once per step (SURVEY 8(e)); the default when more than one process runs")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent trajectories per rank instead (weak scaling, no data-path collective)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -395,8 +444,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     cfg = xi.CONFIGS[args.config]
-    if args.qslab:
-        return run_qslab(args, cfg, ws, rank, dev, dist)
+    if args.qshard or (ws > 1 and not args.replicas):
+        return run_qshard(args, cfg, ws, rank, dev, dist)
     # weak scaling: each rank its own independent trajectory
     from paper_2204_13241_b200 import dist as xd
     cfg_r = xi.scaled(cfg, seed=xd.trajectory_seed(cfg.seed, rank)) if rank else cfg

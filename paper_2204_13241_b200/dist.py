@@ -69,29 +69,39 @@ def qslab(n_h: int, h0: int, rank: int, world_size: int):
     return h0 + lo, hi - lo, lo
 
 
-def ring_moments(values, bins, n_bins):
-    """Per-row ring moments (count of finite values, their sum) of a [rows][n_pix] slab; the host-side form of
-    the combine step (the device reductions produce the same moments per rank)."""
-    v = np.asarray(values, dtype=np.float64)
-    if v.ndim == 1:
-        v = v[None]
-    cnt = np.zeros((v.shape[0], n_bins))
-    s = np.zeros((v.shape[0], n_bins))
-    for b in range(n_bins):
-        sel = v[:, bins == b]
-        ok = np.isfinite(sel)
-        cnt[:, b] = ok.sum(1)
-        s[:, b] = np.where(ok, sel, 0.0).sum(1)
-    return cnt, s
+# the tensor engines' pair tile (k_lattice_i8.cu / k_lattice_tc.cu): 256 rows h x 128 columns k
+TILE_H, TILE_K = 256, 128
 
 
-def ring_means_from_moments(cnt, s):
-    with np.errstate(invalid="ignore", divide="ignore"):
-        return np.where(cnt > 0, s / np.where(cnt > 0, cnt, 1), np.nan)
+def _split_aligned(n: int, parts: int, unit: int, idx: int):
+    """[lo, hi) of part idx when n is split into `parts` contiguous ranges: whole multiples of `unit` while there are
+    at least as many units as parts (balanced in units), else an even split."""
+    units = -(-n // unit)
+    if parts <= units:
+        ulo, uhi = shard(units, idx, parts)
+        return min(n, ulo * unit), min(n, uhi * unit)
+    return shard(n, idx, parts)
 
 
-def allreduce_ring_means(values, bins, n_bins, device=None):
-    """Ring averages over a detector split across ranks: all-reduce (count, sum), then divide."""
-    cnt, s = ring_moments(values, bins, n_bins)
-    both = sum_over_ranks(np.stack([cnt, s]), device)
-    return ring_means_from_moments(both[0], both[1])
+def qblocks(n_h: int, n_k: int, h0: int, k0: int, rank: int, world_size: int):
+    """2-D block of a lattice plane for rank: the factorisation world = ph x pk whose blocks need the fewest pair
+    tiles on the busiest rank (ties: the most even pixel split), rows and columns cut at tile boundaries where
+    possible.  Returns ((h0_r, n_h_r, k0_r, n_k_r), (row0, col0, ph, pk))."""
+    best = None
+    for ph in range(1, world_size + 1):
+        if world_size % ph:
+            continue
+        pk = world_size // ph
+        tiles, pix = [], []
+        for r in range(world_size):
+            hl, hh = _split_aligned(n_h, ph, TILE_H, r // pk)
+            kl, kh = _split_aligned(n_k, pk, TILE_K, r % pk)
+            tiles.append(-(-(hh - hl) // TILE_H) * -(-(kh - kl) // TILE_K))
+            pix.append((hh - hl) * (kh - kl))
+        key = (max(tiles), max(pix) - min(pix), ph)
+        if best is None or key < best[0]:
+            best = (key, ph, pk)
+    _, ph, pk = best
+    hl, hh = _split_aligned(n_h, ph, TILE_H, rank // pk)
+    kl, kh = _split_aligned(n_k, pk, TILE_K, rank % pk)
+    return (h0 + hl, hh - hl, k0 + kl, kh - kl), (hl, kl, ph, pk)

@@ -236,38 +236,71 @@ def workload_from_config(cfg, device="cuda", stream=None) -> Workload:
                     windows=tuple(cfg.windows), n_bins=cfg.n_bins, in_dtype=in_dtype)
 
 
-class QSlabPipeline:
-    """One trajectory on a detector split into slabs of rows across ranks ("partition by q ... each GPU
-    then owns complete time series, so g2 stays local; shell sums need one small all-reduce").  Rank r computes I and
-    g2 on its rows [h0 + lo, h0 + hi) of the lattice plane, the additive ring moments of I (S rings), of g2 (g2 rings)
-    and the XSVS moments on its pixels, all-reduces the moments once (one flat FP64 buffer: NCCL on GPUs), and forms
-    S_b(t), g2_b(tau) and beta_{W,b} from the sums -- equal to the single-device reductions up to summation order.
-    Orchestration only: every step is an ABI call; `allreduce(t)` sums a device tensor in place over the ranks
-    (torch.distributed.all_reduce when a process group exists)."""
+class MomentLayout:
+    """The q-sharded step's single FP64 all-reduce buffer: [S moments T x n_bins x 2 | g2 moments n_lags x n_bins x 2 |
+    XSVS moments n_slots x n_bins x 3] (the layouts of xpcs_ring_moments and xsvs_moments, include/xpcs.h).  Pure
+    indexing: the arithmetic is in the library."""
+
+    def __init__(self, T, n_lags, n_slots, n_bins):
+        self.T, self.n_lags, self.n_slots, self.n_bins = int(T), int(n_lags), int(n_slots), int(n_bins)
+        self.sizes = [self.T * self.n_bins * 2, self.n_lags * self.n_bins * 2, self.n_slots * self.n_bins * 3]
+        self.offsets = [0, self.sizes[0], self.sizes[0] + self.sizes[1]]
+        self.total = sum(self.sizes)
+
+    def views(self, m):
+        """(S [T][nb][2], g2 [n_lags][nb][2] or None, XSVS [n_slots][nb][3] or None) views of a flat buffer m."""
+        o, nb = self.offsets, self.n_bins
+        mS = m[o[0]:o[1]].view(self.T, nb, 2)
+        mG = m[o[1]:o[2]].view(self.n_lags, nb, 2) if self.n_lags else None
+        mX = m[o[2]:].view(self.n_slots, nb, 3) if self.n_slots else None
+        return mS, mG, mX
+
+
+class QShardPipeline:
+    """One trajectory on a detector split across ranks ("partition by q ... each GPU then owns complete
+    time series, so g2 stays local; shell sums need one small all-reduce"; the q vectors are
+    independent).  Lattice planes are split into 2-D blocks aligned to the tensor engines' 256 (h) x 128 (k) pair
+    tiles (dist.qblocks); explicit q lists (config 4's Ewald detector) into contiguous pixel ranges.  Rank r computes
+    I and g2 on its block (atom kinds included: the kinds' f_q rows cover the block), the additive ring moments of I
+    (S rings), of g2 (g2 rings) and the XSVS moments on its pixels, all-reduces the moments once (one flat FP64
+    buffer, MomentLayout: NCCL on GPUs), and forms S_b(t), g2_b(tau) and beta_{W,b} from the sums -- equal to the
+    single-device reductions up to summation order.  Orchestration only: every step is an ABI call; `allreduce(t)`
+    sums a device tensor in place over the ranks (torch.distributed.all_reduce when a process group exists)."""
 
     def __init__(self, wl: Workload, rank: int, world: int, device="cuda", allreduce=None):
         from . import dist as xd
-        assert wl.n_plane and wl.kinds is None, "q-slab mode: lattice plane, per-atom (or unit) form factors"
         self.wl, self.rank, self.world = wl, rank, world
         self.device = torch.device(device)
-        full = X.lattice_plane(wl.L, wl.n_plane, 0)
-        h0, n_h, self.row0 = xd.qslab(full.n_h, full.h0, rank, world)
-        self.full = full
-        self.grid = X.qgrid(wl.L, h0, n_h, full.k0, full.n_k, tuple(full.m0), tuple(full.ma), tuple(full.mb))
-        self.n_q = self.grid.n_q
-        self.bins = X.xpcs_lattice_bins(self.grid, wl.n_bins, wl.n_plane // (2 * wl.n_bins), self.device)
-        X.xpcs_rings_register(self.bins, wl.n_bins)
+        self.ws = X.new_workspace()
         odt = torch.float64 if wl.in_dtype == X.F64 else torch.float32
+        self.kind_fq = None
+        if wl.n_plane:
+            full = X.lattice_plane(wl.L, wl.n_plane, 0)
+            (h0, n_h, k0, n_k), self.block = xd.qblocks(full.n_h, full.n_k, full.h0, full.k0, rank, world)
+            self.full = full
+            self.grid = X.qgrid(wl.L, h0, n_h, k0, n_k, tuple(full.m0), tuple(full.ma), tuple(full.mb))
+            self.n_q = self.grid.n_q
+            self.q = None
+            self.bins = X.xpcs_lattice_bins(self.grid, wl.n_bins, wl.n_plane // (2 * wl.n_bins), self.device)
+            if wl.kinds is not None:
+                self.vol = X.qvolume(wl.L, h0, n_h, k0, n_k, 0, 1, m0=tuple(full.m0), ma=tuple(full.ma),
+                                     mb=tuple(full.mb))
+                kf = torch.tensor(list(wl.kind_f), dtype=odt, device=self.device)
+                self.kind_fq = kf[:, None].expand(len(wl.kind_f), self.n_q).contiguous()
+        else:
+            lo, hi = xd.shard(wl.q.shape[0], rank, world)
+            self.block = (lo, hi)
+            self.grid = None
+            self.q = wl.q[lo:hi].contiguous()
+            self.n_q = hi - lo
+            self.bins = X.xpcs_radial_bins(self.q, wl.q_max, wl.n_bins)
+        X.xpcs_rings_register(self.bins, wl.n_bins)
         self.I = torch.empty((wl.T, self.n_q), dtype=odt, device=self.device)
         self.g2 = torch.empty((len(wl.lags), self.n_q), dtype=torch.float32, device=self.device) if wl.lags else None
-        nb, T, nl = wl.n_bins, wl.T, len(wl.lags)
-        self.n_slots = X.xsvs_n_slots(T, wl.windows) if wl.windows else 0
-        sizes = [T * nb * 2, nl * nb * 2, self.n_slots * nb * 3]
-        self.mom = torch.zeros(sum(sizes), dtype=torch.float64, device=self.device)
-        o1, o2 = sizes[0], sizes[0] + sizes[1]
-        self.mS = self.mom[:o1].view(T, nb, 2)
-        self.mG = self.mom[o1:o2].view(nl, nb, 2) if nl else None
-        self.mX = self.mom[o2:].view(self.n_slots, nb, 3) if self.n_slots else None
+        self.n_slots = X.xsvs_n_slots(wl.T, wl.windows) if wl.windows else 0
+        self.layout = MomentLayout(wl.T, len(wl.lags), self.n_slots, wl.n_bins)
+        self.mom = torch.zeros(self.layout.total, dtype=torch.float64, device=self.device)
+        self.mS, self.mG, self.mX = self.layout.views(self.mom)
         self._allreduce = allreduce if allreduce is not None else self._default_allreduce
 
     @staticmethod
@@ -281,33 +314,39 @@ class QSlabPipeline:
         return int(self.wl.N) * int(self.n_q) * int(self.wl.T)
 
     def local(self, positions, form_factors, profile=False):
-        """This rank's slab: I, g2 and the ring / XSVS moments (before the all-reduce)."""
+        """This rank's block: I, g2 and the ring / XSVS moments (before the all-reduce)."""
         wl = self.wl
-        X.xpcs_intensity_grid(positions, form_factors, self.grid, out=self.I, engine=wl.engine, profile=profile)
-        X.xpcs_ring_moments(self.I, self.bins, wl.n_bins, out=self.mS, profile=profile)
-        if wl.lags:
-            X.xpcs_g2(self.I, wl.lags, out=self.g2, out_dtype=X.F32, profile=profile)
-            X.xpcs_ring_moments(self.g2, self.bins, wl.n_bins, out=self.mG, profile=profile)
-        if self.n_slots:
-            X.xsvs_moments(self.I, self.bins, wl.n_bins, wl.windows, out=self.mX, profile=profile)
+        with X.workspace(self.ws):
+            if self.kind_fq is not None:
+                X.xpcs_intensity_volume(positions, None, self.vol, species=wl.kinds, f_q=self.kind_fq, out=self.I,
+                                        engine=wl.engine, profile=profile, f_max=wl.kind_f)
+            elif self.grid is not None:
+                X.xpcs_intensity_grid(positions, form_factors, self.grid, out=self.I, engine=wl.engine, profile=profile)
+            else:
+                X.xpcs_intensity(positions, form_factors, self.q, wl.L, out=self.I, profile=profile)
+            X.xpcs_ring_moments(self.I, self.bins, wl.n_bins, out=self.mS, profile=profile)
+            if wl.lags:
+                X.xpcs_g2(self.I, wl.lags, out=self.g2, out_dtype=X.F32, profile=profile)
+                X.xpcs_ring_moments(self.g2, self.bins, wl.n_bins, out=self.mG, profile=profile)
+            if self.n_slots:
+                X.xsvs_moments(self.I, self.bins, wl.n_bins, wl.windows, out=self.mX, profile=profile)
         return self.mom
 
     def finish(self, form_factors, moments=None):
         """Ring results from (summed) moments."""
         wl = self.wl
-        m = self.mom if moments is None else moments
-        T, nb, nl = wl.T, wl.n_bins, len(wl.lags)
-        mS = m[:T * nb * 2].view(T, nb, 2)
+        mS, mG, mX = self.layout.views(self.mom if moments is None else moments)
         out = {"I": self.I}
-        if form_factors is not None:
-            out["S_rings"] = X.xpcs_ring_means_from_moments(mS, 1.0, form_factors, wl.N)
-        else:
-            out["S_rings"] = X.xpcs_ring_means_from_moments(mS, 1.0 / wl.N)
-        if nl:
-            out["g2"] = self.g2
-            out["g2_rings"] = X.xpcs_ring_means_from_moments(m[T * nb * 2:(T + nl) * nb * 2].view(nl, nb, 2))
-        if self.n_slots:
-            out["beta"] = X.xsvs_contrast_from_moments(m[(T + nl) * nb * 2:].view(self.n_slots, nb, 3), T, wl.windows)
+        with X.workspace(self.ws):
+            if form_factors is not None:
+                out["S_rings"] = X.xpcs_ring_means_from_moments(mS, 1.0, form_factors, wl.N)
+            else:
+                out["S_rings"] = X.xpcs_ring_means_from_moments(mS, 1.0 / wl.N)
+            if wl.lags:
+                out["g2"] = self.g2
+                out["g2_rings"] = X.xpcs_ring_means_from_moments(mG)
+            if self.n_slots:
+                out["beta"] = X.xsvs_contrast_from_moments(mX, wl.T, wl.windows)
         return out
 
     def run(self, positions, form_factors, profile=False):
@@ -320,3 +359,6 @@ class QSlabPipeline:
             X.xpcs_rings_unregister(self.bins)
         except Exception:
             pass
+
+
+QSlabPipeline = QShardPipeline   # round-1 name

@@ -1,6 +1,6 @@
-"""The q-sharded single-trajectory mode: a detector split into slabs of rows, each slab's I, g2 and
-additive ring / XSVS moments computed separately, the moments summed (the all-reduce), the ring results formed from
-the sums.  On one GPU the ranks run one after another (no rank waits on another) and the sum stands in for the
+"""The q-sharded single-trajectory mode: a detector split into tile-aligned blocks (lattice planes) or
+pixel ranges (explicit q), each block's I, g2 and additive ring / XSVS moments computed separately, the moments
+summed (the all-reduce), the ring results formed from the sums.  On one GPU the ranks run one after another (no rank waits on another) and the sum stands in for the
 NCCL all-reduce; the result must equal the single-detector reductions up to summation order, and each slab's I must
 equal the matching rows of the full-plane I within the per-pixel gate.  Also pins the moment entry points on their
 own: moments of the full detector reproduce xpcs_shell_mean / xsvs_contrast."""
@@ -13,6 +13,7 @@ pytestmark = pytest.mark.gpu
 import xpcs_inputs as xi  # noqa: E402
 import paper_2204_13241_b200 as xp  # noqa: E402
 from paper_2204_13241_b200 import pipeline  # noqa: E402
+from paper_2204_13241_b200 import dist as xd  # noqa: E402
 from _gates import assert_pixels, assert_rel  # noqa: E402
 
 DEV = "cuda"
@@ -53,33 +54,69 @@ def test_moment_entry_points_match_direct_reductions():
     P.close()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_qslab_split_equals_full_detector(world):
+def _shape(name):
+    """Reduced inputs with the structure of each config: c2 (uniform f), c3 / c5 (two kinds, AUTO's hybrid engine
+    split), c4 (explicit Ewald q list)."""
+    if name == "c4":
+        return xi.scaled(xi.CONFIGS["c4"], N=4000, T=6, detector=64, lags=(1, 2), windows=(1, 2), n_bins=8)
+    base = xi.CONFIGS[name]
+    return xi.scaled(base, N=3000, T=24, n_plane=96, lags=(1, 2, 3, 5), windows=(1, 2, 4, 7), n_bins=8)
+
+
+@pytest.mark.parametrize("name,world", [("c2", 2), ("c2", 3), ("c3", 2), ("c3", 4), ("c5", 3), ("c4", 2), ("c4", 3)])
+def test_qshard_split_equals_full_detector(name, world):
+    """One trajectory, the detector split across `world` ranks run one after another on this GPU (no rank waits on
+    another; the sum stands in for the NCCL all-reduce): ring results within the ring gate of the full detector,
+    every block's I within the per-pixel gate of the matching full-detector pixels, and the blocks tile it."""
+    cfg = _shape(name)
+    pos = torch.from_numpy(xi.positions(cfg)).to(DEV)
+    f = torch.from_numpy(xi.form_factors(cfg)).to(DEV) if cfg.two_species else None
+    wl = pipeline.workload_from_config(cfg, device=DEV)
+    P = pipeline.Pipeline(wl, device=DEV)
+    full = {k: v.clone() for k, v in P.run(pos, f).items() if torch.is_tensor(v)}
+    ranks = [pipeline.QShardPipeline(wl, r, world, device=DEV, allreduce=lambda t: None) for r in range(world)]
+    total = None
+    for Q in ranks:
+        m = Q.local(pos, f).clone()
+        total = m if total is None else total + m
+    torch.cuda.synchronize()
+    res = ranks[0].finish(f, moments=total)
+    for key in ("S_rings", "g2_rings", "beta"):
+        assert_rel(res[key].cpu().numpy(), full[key].cpu().numpy(), 1e-4, f"q-shard {key} ({name}, world {world})")
+    I_full = full["I"].cpu().numpy()
+    g2_full = full["g2"].cpu().numpy()
+    covered = np.zeros(I_full.shape[1], dtype=int)
+    for Q in ranks:
+        if Q.grid is not None:
+            n = cfg.n_plane
+            row0, col0, _, _ = Q.block
+            idx = ((np.arange(Q.grid.n_h)[:, None] + row0) * n + col0 + np.arange(Q.grid.n_k)[None, :]).ravel()
+        else:
+            idx = np.arange(*Q.block)
+        covered[idx] += 1
+        assert_pixels(Q.I.cpu().numpy(), I_full[:, idx], cfg.N, f"{name} block {Q.rank} I")
+        np.testing.assert_allclose(Q.g2.cpu().numpy(), g2_full[:, idx], rtol=1e-3)
+        Q.close()
+    assert np.all(covered == 1)
+    P.close()
+
+
+def test_qshard_decomposition_exact_on_identical_input():
+    """The decomposition itself is exact: the full detector's I split into the blocks, the blocks' moments summed,
+    reproduce the full-detector reductions to 1e-12 (only the summation order differs)."""
     cfg = _cfg()
     pos = torch.from_numpy(xi.positions(cfg)).to(DEV)
     wl = pipeline.workload_from_config(cfg, device=DEV)
     P = pipeline.Pipeline(wl, device=DEV)
     full = {k: v.clone() for k, v in P.run(pos, None).items() if torch.is_tensor(v)}
-    ranks = [pipeline.QSlabPipeline(wl, r, world, device=DEV, allreduce=lambda t: None) for r in range(world)]
-    total = None
-    for Q in ranks:
-        m = Q.local(pos, None).clone()
-        total = m if total is None else total + m
-    torch.cuda.synchronize()
-    res = ranks[0].finish(None, moments=total)
-    # each slab's I comes from its own engine launch (its own tiling and atom chunking), so the ring results agree
-    # with the full detector's within the ring gate (1e-4, north_star), not bitwise; the decomposition itself is
-    # pinned exactly below on identical input
-    for key in ("S_rings", "g2_rings", "beta"):
-        assert_rel(res[key].cpu().numpy(), full[key].cpu().numpy(), 1e-4, f"q-slab {key} (world {world})")
-    # exact decomposition: the full-detector I split into the same slabs, moments summed over slabs == full moments
     n = cfg.n_plane
     tot_S = tot_G = tot_X = None
-    for Q in ranks:
-        lo, hi = Q.row0 * n, (Q.row0 + Q.grid.n_h) * n
-        I_s = full["I"][:, lo:hi].contiguous()
-        g2_s = full["g2"][:, lo:hi].contiguous()
-        b_s = P.bins[lo:hi].contiguous()
+    for r in range(3):
+        (h0, n_h, k0, n_k), (row0, col0, _, _) = xd.qblocks(n, n, -n // 2, -n // 2, r, 3)
+        idx = torch.from_numpy(((np.arange(n_h)[:, None] + row0) * n + col0 + np.arange(n_k)[None, :]).ravel()).to(DEV)
+        I_s = full["I"][:, idx].contiguous()
+        g2_s = full["g2"][:, idx].contiguous()
+        b_s = P.bins[idx].contiguous()
         mS = xp.xpcs_ring_moments(I_s, b_s, wl.n_bins)
         mG = xp.xpcs_ring_moments(g2_s, b_s, wl.n_bins)
         mX = xp.xsvs_moments(I_s, b_s, wl.n_bins, wl.windows)
@@ -87,21 +124,9 @@ def test_qslab_split_equals_full_detector(world):
         tot_G = mG if tot_G is None else tot_G + mG
         tot_X = mX if tot_X is None else tot_X + mX
     assert_rel(xp.xpcs_ring_means_from_moments(tot_S, 1.0 / cfg.N).cpu().numpy(), full["S_rings"].cpu().numpy(),
-               1e-12, "slab-summed S rings")
+               1e-12, "block-summed S rings")
     assert_rel(xp.xpcs_ring_means_from_moments(tot_G).cpu().numpy(), full["g2_rings"].cpu().numpy(), 1e-12,
-               "slab-summed g2 rings")
+               "block-summed g2 rings")
     assert_rel(xp.xsvs_contrast_from_moments(tot_X, cfg.T, wl.windows).cpu().numpy(), full["beta"].cpu().numpy(),
-               1e-12, "slab-summed beta")
-    I_full = full["I"].cpu().numpy().reshape(cfg.T, cfg.n_plane, cfg.n_plane)
-    g2_full = full["g2"].cpu().numpy().reshape(len(cfg.lags), cfg.n_plane, cfg.n_plane)
-    rows = 0
-    for Q in ranks:
-        n_h = Q.grid.n_h
-        Ir = Q.I.cpu().numpy().reshape(cfg.T, n_h, cfg.n_plane)
-        assert_pixels(Ir, I_full[:, Q.row0:Q.row0 + n_h], cfg.N, f"slab {Q.rank} I")
-        g2r = Q.g2.cpu().numpy().reshape(len(cfg.lags), n_h, cfg.n_plane)
-        np.testing.assert_allclose(g2r, g2_full[:, Q.row0:Q.row0 + n_h], rtol=1e-3)
-        rows += n_h
-        Q.close()
-    assert rows == cfg.n_plane
+               1e-12, "block-summed beta")
     P.close()
