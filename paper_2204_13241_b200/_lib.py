@@ -633,7 +633,10 @@ def engine_resolved(engine, uniform_f=True) -> int:
 AUTO_I8 = True    # AUTO routes uniform-f lattice calls to the integer engine (mirrors api.cu)
 
 
-def species_engines(counts, f_max=None):
+I8_BUDGET = float(os.environ.get("XPCS_I8_BUDGET", "1.5"))   # mirror of api.cu's kI8BudgetDefault (env: experiments)
+
+
+def species_engines(counts, f_max=None, budget=None):
     """Mirror of api.cu's AUTO rule for species calls: kinds in increasing |f_max| go to the integer engine while
     sum (f_max / f_min)^2 N_s / N <= 1; the kind that crosses the budget is split (its first atoms on the integer
     engine up to the budget), the rest run on split-FP16.  Without f_max hints every kind runs on split-FP16.
@@ -645,10 +648,11 @@ def species_engines(counts, f_max=None):
     order = sorted(range(n), key=lambda k: abs(f_max[k]))
     fref = next((abs(f_max[k]) for k in order if counts[k] > 0 and abs(f_max[k]) > 0), 0.0)
     total = max(1, sum(counts))
+    cap = I8_BUDGET if budget is None else float(budget)
     out, budget = [0] * n, 0.0
     for k in order:
         w2 = (f_max[k] / fref) ** 2 if fref > 0 else 1.0
-        room = 1.0 + 1e-12 - budget
+        room = cap + 1e-12 - budget
         take = counts[k]
         if room <= 0:
             take = 0

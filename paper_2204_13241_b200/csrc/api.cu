@@ -433,10 +433,18 @@ static int validate_volume(const xpcs_qvolume* vol) {
     return XPCS_OK;
 }
 
+constexpr double kI8BudgetDefault = 1.5;   // tools/i8_budget_probe.py: worst 0.40 (c3, 9e4 samples) / 0.43 (c5, 6e4)
 static bool fixup_enabled() {
     static int on = -1;
     if (on < 0) { const char* e = getenv("XPCS_FIXUP"); on = (e && atoi(e) == 0) ? 0 : 1; }   // experiments only
     return on == 1;
+}
+
+// AUTO's error budget for the integer engine in species calls: kinds in increasing max |f_s| go to it while
+// sum_s (f_max_s / f_ref)^2 N_s / N <= budget (1 = the error level of a single f = 1 species on the engine)
+static double i8_budget() {
+    const char* e = getenv("XPCS_I8_BUDGET");   // experiments only (read per call: the precision probe varies it)
+    return e ? atof(e) : kI8BudgetDefault;
 }
 
 // ---- integer-engine grid planning (k_lattice_i8: clusters of 2 CTAs, one CTA per SM, 32-atom stages) ----
@@ -538,7 +546,7 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
     int ng = G.count();
     // engine per atom group.  AUTO with species: the integer engine's limb error grows with the kind's weight, so
     // kinds are taken in increasing max |f_s| (species->f_max, host hints; absent = all equal) while the integer
-    // share of the error budget, sum f_max^2 N_s / (f_ref^2 N) with f_ref the smallest weight, stays <= 1 -- the
+    // share of the error budget, sum f_max^2 N_s / (f_ref^2 N) with f_ref the smallest weight, stays <= the budget (1.5, i8_budget) -- near the
     // single-species f = 1 level validated against the gate; the heavier kinds run on the split-FP16 engine.
     std::vector<char> gi8((size_t)ng, i8 ? 1 : 0);
     // AUTO species call without f_max hints: the kinds' weights are unknown (f_q lives on the device), so the
@@ -555,9 +563,10 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
         for (int k : order) if (G.cnt[k] > 0 && std::fabs(species->f_max[k]) > 0.0) { fref = std::fabs(species->f_max[k]); break; }
         std::vector<int64_t> n_int((size_t)ng, 0);
         double budget = 0.0;
+        const double cap = i8_budget();
         for (int k : order) {
             const double w2 = fref > 0.0 ? (species->f_max[k] / fref) * (species->f_max[k] / fref) : 1.0;
-            const double room = 1.0 + 1e-12 - budget;
+            const double room = cap + 1e-12 - budget;
             int64_t take = G.cnt[k];
             if (room <= 0.0) take = 0;
             else if (w2 * (double)G.cnt[k] / (double)N > room) take = (int64_t)std::floor(room * (double)N / w2);

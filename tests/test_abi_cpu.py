@@ -161,13 +161,15 @@ def test_binding_argument_checks():
 def test_species_engine_rule():
     """AUTO's per-kind engine split (mirror of api.cu): kinds in increasing f_max on the integer engine while
     sum (f_max / f_min)^2 N_s / N <= 1, the crossing kind split at the budget."""
-    se = xp.species_engines
+    se = lambda c, f: xp.species_engines(c, f, budget=1.0)
     assert se([1000], [1.0]) == [1000]
-    assert se([500, 500], [1.0, 2.0]) == [500, 125]            # c3/c5: f = 1 half + a quarter of the f = 2 half
+    assert se([500, 500], [1.0, 2.0]) == [500, 125]            # budget 1: f = 1 half + a quarter of the f = 2 half
     assert se([300, 700], [2.0, 1.0]) == [75, 700]
     assert se([400, 400, 200], [1.0, 1.0, 1.0]) == [400, 400, 200]
     assert se([10, 10], None) == [0, 0]                        # no hints: every kind on split-FP16
     assert se([0, 100], [0.5, 1.0])[1] == 100                  # an empty kind does not set the reference weight
+    # the default budget (1.5, api.cu kI8BudgetDefault; tools/i8_budget_probe.py): half of the f = 2 kind
+    assert xp.species_engines([500, 500], [1.0, 2.0]) == [500, 250]
 
 
 def test_step_host_validation_before_launch(lib):
