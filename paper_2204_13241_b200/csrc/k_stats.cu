@@ -12,37 +12,44 @@
 namespace xpcs {
 
 // =====================================================================================================
-// K4: g2.  A warp owns 32 pixels (lanes) x 16 lags.  The pixels' time series are staged through shared memory
-// (fp32 for fp32 input: products of two fp32 are exact in FP64) in chunks of GC frames plus a halo of max_lag
-// frames (zero beyond T, so products with t + tau >= T vanish and each lag sums exactly over t < T - tau).
-// Consecutive lag groups (tau_l = tau_0 + l) use a register-blocked sliding window: per 16 frames 48 shared loads
-// feed 256 DFMA; other lag lists fall back to one shared load per DFMA.
+// K4: g2.  A warp owns 32 pixels (lanes) x LPW lags.  The pixels' time series are staged through shared memory (as
+// FP64: products of two fp32 are exact in FP64) in chunks of GC frames plus a halo of max_lag frames (zero beyond T,
+// so products with t + tau >= T vanish and each lag sums exactly over t < T - tau).  Consecutive lag groups
+// (tau_l = tau_0 + l) use a register-blocked sliding window: per 16 frames 16 + 16 + LPW - 1 shared loads feed
+// 16 LPW DFMA; other lag lists fall back to one shared load per DFMA.
 // =====================================================================================================
-#ifndef XPCS_G2_LPW
-#define XPCS_G2_LPW 8
-#endif
-namespace { constexpr int G2_LPW = XPCS_G2_LPW, G2_WARPS = 8, G2_LAGS_PER_BLOCK = G2_LPW * G2_WARPS, GC = 128; }
+namespace {
+constexpr int G2_WARPS = 8, GC = 128;
+constexpr int G2_LPW = 8, G2_LAGS_PER_BLOCK = G2_LPW * G2_WARPS;   // the ISF kernel's tiling (below)
+}
 
-template <typename In, typename Out, typename St>
+// LPW lags per warp (8: short lag lists such as config 2's 50; 16: long ones such as config 3's 200 -- per 16 rows
+// 16 + 16 + LPW shared loads feed 16 LPW DFMA, so 16 lags per warp keep the FP64 pipe, not shared memory, the bound).
+// A block's warps cover `lpb` consecutive entries of the lag list (balanced over the y-blocks); the series mean is
+// summed once per block (warp 0) and broadcast through shared memory.
+template <typename In, typename Out, typename St, int LPW>
 __global__ void __launch_bounds__(256)
 k_g2(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __restrict__ lags, int64_t n_lags,
-     int halo, Out* __restrict__ out) {
+     int halo, int lpb, Out* __restrict__ out) {
     extern __shared__ __align__(16) unsigned char g2_smem[];
     St* S = reinterpret_cast<St*>(g2_smem);              // [(GC + halo + 16)][32]
+    __shared__ double mean_sh[32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t px = (int64_t)blockIdx.x * 32 + lane;
-    const int64_t lbase = (int64_t)blockIdx.y * G2_LAGS_PER_BLOCK + warp * G2_LPW;
-    const bool active = lbase < n_lags;
-    int tau[G2_LPW];
+    const int64_t lblk = (int64_t)blockIdx.y * lpb;
+    const int64_t lbase = lblk + warp * LPW;
+    const int64_t lend = min(n_lags, lblk + lpb);
+    const bool active = lbase < lend;
+    int tau[LPW];
     bool consecutive = true;
 #pragma unroll
-    for (int l = 0; l < G2_LPW; ++l) {
-        tau[l] = (lbase + l < n_lags) ? lags[lbase + l] : (active ? lags[lbase] + l : 0);
+    for (int l = 0; l < LPW; ++l) {
+        tau[l] = (lbase + l < lend) ? lags[lbase + l] : (active ? lags[lbase] + l : 0);
         if (tau[l] != tau[0] + l) consecutive = false;
     }
-    double acc[G2_LPW];
+    double acc[LPW];
 #pragma unroll
-    for (int l = 0; l < G2_LPW; ++l) acc[l] = 0.0;
+    for (int l = 0; l < LPW; ++l) acc[l] = 0.0;
     double sum = 0.0;
     const int rows = GC + halo + 16;
     for (int64_t t0 = 0; t0 < T; t0 += GC) {
@@ -53,37 +60,42 @@ k_g2(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __restrict
         }
         __syncthreads();
         const int rmax = (int)min((int64_t)GC, T - t0);
-        for (int r = 0; r < rmax; ++r) sum += (double)S[r * 32 + lane];
+        if (warp == 0)
+            for (int r = 0; r < rmax; ++r) sum += (double)S[r * 32 + lane];
         if (!active) continue;
         if (consecutive) {
             const int t0l = tau[0];
             // rows t with t + tau_0 >= T only meet the zero halo: stop before them (the warp's smallest lag)
             const int rlim = (int)min((int64_t)rmax, max((int64_t)0, T - t0 - t0l));
             for (int r0 = 0; r0 < rlim; r0 += 16) {          // rows beyond rlim are zero-padded or ignored
-                double a[16], w[16 + G2_LPW];
+                double a[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i) a[i] = (r0 + i < rlim) ? (double)S[(r0 + i) * 32 + lane] : 0.0;
+                // sliding window: w_j = S[r0 + t0l + j] meets a[i] for lag l = j - i
 #pragma unroll
-                for (int j = 0; j < 16 + G2_LPW; ++j) w[j] = (double)S[(r0 + t0l + j) * 32 + lane];
+                for (int j = 0; j < 16 + LPW - 1; ++j) {
+                    const double w = (double)S[(r0 + t0l + j) * 32 + lane];
 #pragma unroll
-                for (int i = 0; i < 16; ++i)
-#pragma unroll
-                    for (int l = 0; l < G2_LPW; ++l) acc[l] = fma(a[i], w[i + l], acc[l]);
+                    for (int i = 0; i < 16; ++i)
+                        if (j - i >= 0 && j - i < LPW) acc[j - i] = fma(a[i], w, acc[j - i]);
+                }
             }
         } else {
             for (int r = 0; r < rmax; ++r) {
                 const double a = (double)S[r * 32 + lane];
 #pragma unroll
-                for (int l = 0; l < G2_LPW; ++l) acc[l] = fma(a, (double)S[(r + tau[l]) * 32 + lane], acc[l]);
+                for (int l = 0; l < LPW; ++l) acc[l] = fma(a, (double)S[(r + tau[l]) * 32 + lane], acc[l]);
             }
         }
     }
+    if (warp == 0) mean_sh[lane] = sum / (double)T;
+    __syncthreads();
     if (px >= n_q || !active) return;
-    const double mean = sum / (double)T;
+    const double mean = mean_sh[lane];
     const double den = mean * mean;
 #pragma unroll
-    for (int l = 0; l < G2_LPW; ++l) {
-        if (lbase + l >= n_lags) break;
+    for (int l = 0; l < LPW; ++l) {
+        if (lbase + l >= lend) break;
         const double num = acc[l] / (double)(T - tau[l]);
         out[(lbase + l) * n_q + px] = (Out)(den > 0.0 ? num / den : __longlong_as_double(0x7ff8000000000000ll));
     }
@@ -91,17 +103,19 @@ k_g2(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __restrict
 
 cudaError_t launch_g2(const void* I, int in_f64, int64_t T, int64_t n_q, const int32_t* lags_dev,
                       int64_t n_lags, int max_lag, void* out, int out_f64, cudaStream_t s) {
-    const int wpb = (int)std::min<int64_t>(G2_WARPS, (n_lags + G2_LPW - 1) / G2_LPW);   // drop idle warps
-    dim3 grid((unsigned)((n_q + 31) / 32), (unsigned)((n_lags + G2_LAGS_PER_BLOCK - 1) / G2_LAGS_PER_BLOCK));
     const size_t elem = sizeof(double);                    // the series is staged in FP64 for both input types
     const size_t smem = elem * 32 * (GC + max_lag + 16 + 16);
-    (void)wpb;
     note_launch();
-#define G2_CASE(IN, OUT, ST)                                                                          \
-    {                                                                                                 \
-        auto kern = k_g2<IN, OUT, ST>;                                                                \
+    // lags per warp, and the lag list split over y-blocks of at most 8 warps with balanced counts
+    const int lpw = n_lags >= 64 ? 16 : 8;
+    const int64_t ny = (n_lags + (int64_t)G2_WARPS * lpw - 1) / ((int64_t)G2_WARPS * lpw);
+    const int lpb = (int)(((n_lags + ny - 1) / ny + lpw - 1) / lpw * lpw);
+    dim3 grid((unsigned)((n_q + 31) / 32), (unsigned)ny);
+#define G2_CASE(IN, OUT, ST)                                                                                    \
+    {                                                                                                           \
+        auto kern = lpw == 16 ? k_g2<IN, OUT, ST, 16> : k_g2<IN, OUT, ST, 8>;                                   \
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-        kern<<<grid, 256, smem, s>>>((const IN*)I, T, n_q, lags_dev, n_lags, max_lag + 16, (OUT*)out); \
+        kern<<<grid, 256, smem, s>>>((const IN*)I, T, n_q, lags_dev, n_lags, max_lag + 16, lpb, (OUT*)out);    \
     }
     if (in_f64) { if (out_f64) G2_CASE(double, double, double) else G2_CASE(double, float, double) }
     else { if (out_f64) G2_CASE(float, double, double) else G2_CASE(float, float, double) }   // staged as FP64: one conversion per load, not per use
