@@ -38,6 +38,7 @@
 // conjugate-pair combination above with row-contiguous global writes of the partial amplitude or, with a single
 // atom chunk, the final I = |p|^2 (or p) itself.
 #include "common.cuh"
+#include <type_traits>
 
 namespace xpcs {
 
@@ -81,6 +82,9 @@ constexpr float MAGIC = 12582912.0f;                // 1.5 * 2^23
 // t = fma(v, QS, M + 128) holds y = x + 128 in its low 16 bits: byte 1 = hi, byte 0 = lo + 128 (= lo ^ 0x80)
 constexpr float QS = 32512.0f;
 constexpr float QMAGIC = MAGIC + 128.0f;
+#ifndef XPCS_I8_EXPERIMENTS
+#define XPCS_I8_EXPERIMENTS 0   // 1: honour XPCS_I8_DEBUG bit 1 (skip production) in the producers' hot loop
+#endif
 // Global rotation: W carries an extra phase GAMMA (turns x 2^32), so both rows of a pair hold q e^{i Gamma} (Gamma =
 // 2 pi GAMMA / 2^32) and the drain rotates it back (ROT_C, ROT_S = cos, sin Gamma).  Without it, X_d and W are exact
 // conjugates (or equals) at q = 0 (X_d = e^{i pi Th_a}, W = e^{-i pi Th_a}), so their limbs' rounding errors -- and
@@ -271,11 +275,11 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
         // every warp prefetches its own 16 atom records with cp.async into a private ring: no cross-warp barrier
         const uint32_t slot0 = su32(aslot) + (uint32_t)(warp * ASL * WSLOT * 16);
         const float invF = 1.0f / F;
-        // X rows: d = i + 1/2, i = 64 rank + mr + 8 r; phase d Th_a = (2i + 1) Th_a / 2 turns (33-bit product, the
-        // half unit truncated: <= 2^-32 turns).  W rows: k = bk0 + mr + 8 r; phase Th_0 + k Th_b + c Th_a with
-        // c Th_a = (2 H0 + 255) Th_a / 2 turns (the sum with the X phase is h Th_a to within one 2^-32 unit).
-        const uint64_t x_odd = (uint64_t)(2 * ((int)rank * HD + mr) + 1);
-        const uint64_t c_odd = (uint64_t)(2 * H0 + 2 * (PAIR_H / 2) - 1);
+        // X rows: d = i + 1/2, i = 64 rank + mr + 8 r; phase d Th_a = i Th_a + Th_a / 2 turns.  W rows: k = bk0 + mr + 8 r;
+        // phase Th_0 + k Th_b + c Th_a, c Th_a = (H0 + 127) Th_a + Th_a / 2.  Th_a / 2 is taken as Th_a >> 1 on both
+        // sides: the pair's phases sum to h Th_a exactly (row c - d) or to within one 2^-32 unit (row c + d).
+        const uint32_t i0 = (uint32_t)((int)rank * HD + mr);
+        const uint32_t cH = (uint32_t)(H0 + PAIR_H / 2 - 1);
         const uint32_t kk = (uint32_t)(g.k0 + bk0 + mr);
         const uint32_t pbase = (uint32_t)((is_x ? 0 : 2 * PLANE) + qh * 128 + mr * 16 + qq * 4);
         auto prefetch = [&](int li) {   // local stage li of this group -> slot li % ASL of this warp
@@ -290,72 +294,76 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
         };
 #pragma unroll
         for (int k = 0; k < ASL - 1; ++k) prefetch(k);
-        for (int li = 0;; ++li) {
-            const int i = grp + li * NGROUPS;
-            if (i >= n_stages) break;
-            const int s = i % STAGES;
-            asm volatile("cp.async.wait_group %0;" ::"n"(ti8::ASL - 2) : "memory");
-            __syncwarp();                 // the warp's records of stage i are visible to all its lanes; every lane has
-            prefetch(li + ASL - 1);       // finished reading slot (li - 1) % ASL, which is refilled now
-            unsigned long long v[4], st[4];
-            {
+        // the stage loop, specialised per warp role (no per-stage branch between the X and W paths)
+        auto produce = [&](auto role) {
+            constexpr bool X = decltype(role)::value;
+            for (int li = 0;; ++li) {
+                const int i = grp + li * NGROUPS;
+                if (i >= n_stages) break;
+                const int s = i % STAGES;
+                asm volatile("cp.async.wait_group %0;" ::"n"(ti8::ASL - 2) : "memory");
+                __syncwarp();                 // the warp's records of stage i are visible to all its lanes; every lane
+                prefetch(li + ASL - 1);       // has finished reading slot (li - 1) % ASL, which is refilled now
+                unsigned long long v[4], st[4];
                 const uint32_t ra = slot0 + (uint32_t)((li % ASL) * WSLOT * 16);
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const uint32_t a = ra + (uint32_t)((((4 * qq + u) ^ (qq & 2))) * 16);   // record 4 qq + u
-                    uint32_t tha, thb = 0u, th0 = 0u, fw = 0u;
-                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tha) : "r"(a));
-                    if (!is_x) {
-                        asm volatile("ld.shared.u32 %0, [%1+4];" : "=r"(thb) : "r"(a));
-                        asm volatile("ld.shared.u32 %0, [%1+8];" : "=r"(th0) : "r"(a));
-                        asm volatile("ld.shared.u32 %0, [%1+12];" : "=r"(fw) : "r"(a));
-                    }
                     float s0, c0, s1, c1;
-                    if (is_x) {
-                        __sincosf(turns_to_radians((uint32_t)((x_odd * tha) >> 1)), &s0, &c0);
+                    if (X) {
+                        uint32_t tha;
+                        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tha) : "r"(a));
+                        __sincosf(turns_to_radians(i0 * tha + (tha >> 1)), &s0, &c0);
                         __sincosf(turns_to_radians(8u * tha), &s1, &c1);
                         v[u] = pack2(c0, s0);
                     } else {
-                        const uint32_t tc = (uint32_t)((c_odd * tha) >> 1);
-                        __sincosf(turns_to_radians(th0 + kk * thb + tc + GAMMA), &s0, &c0);
+                        uint32_t tha, thb, th0, fw;
+                        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                     : "=r"(tha), "=r"(thb), "=r"(th0), "=r"(fw) : "r"(a));
+                        __sincosf(turns_to_radians(kk * thb + th0 + cH * tha + (tha >> 1) + GAMMA), &s0, &c0);
                         __sincosf(turns_to_radians(8u * thb), &s1, &c1);
                         const float fs = __uint_as_float(fw) * invF;
                         v[u] = pack2(fs * c0, fs * s0);
                     }
                     st[u] = pack2(c1, s1);
                 }
-            }
-            i8_mbar_wait(&empty[s], (uint32_t)(((i / STAGES) + 1) & 1));
-            if (!(dbg_flags & 2)) {
-                // rows m = mr + 8 r: real parts (a | wr) into rows m of the hi/lo planes, imaginary parts (b | wi) into
-                // rows 64 + m
-                const uint32_t a0 = su32(smem) + (uint32_t)(s * STAGE_BYTES) + pbase;
-                const unsigned long long QS2 = pack2(QS, QS), QM2 = pack2(QMAGIC, QMAGIC);
+                i8_mbar_wait(&empty[s], (uint32_t)(((i / STAGES) + 1) & 1));
+#if XPCS_I8_EXPERIMENTS
+                if (!(dbg_flags & 2))
+#endif
+                {
+                    // rows m = mr + 8 r: real parts (a | wr) into rows m of the hi/lo planes, imaginary parts (b | wi)
+                    // into rows 64 + m
+                    const uint32_t a0 = su32(smem) + (uint32_t)(s * STAGE_BYTES) + pbase;
+                    const unsigned long long QS2 = pack2(QS, QS), QM2 = pack2(QMAGIC, QMAGIC);
 #pragma unroll
-                for (int r = 0; r < 8; ++r) {
-                    uint32_t tc[4], ts[4];
+                    for (int r = 0; r < 8; ++r) {
+                        uint32_t tc[4], ts[4];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const unsigned long long tq = ffma2(v[u], QS2, QM2);
-                        tc[u] = (uint32_t)tq; ts[u] = (uint32_t)(tq >> 32);
-                        const unsigned long long cd = pack2(lo2(st[u]), lo2(st[u]));
-                        const unsigned long long sd = pack2(-hi2(st[u]), hi2(st[u]));
-                        v[u] = ffma2(swap2(v[u]), sd, f2mul(v[u], cd));
+                        for (int u = 0; u < 4; ++u) {
+                            const unsigned long long tq = ffma2(v[u], QS2, QM2);
+                            tc[u] = (uint32_t)tq; ts[u] = (uint32_t)(tq >> 32);
+                            const unsigned long long cd = pack2(lo2(st[u]), lo2(st[u]));
+                            const unsigned long long sd = pack2(-hi2(st[u]), hi2(st[u]));
+                            v[u] = ffma2(swap2(v[u]), sd, f2mul(v[u], cd));
+                        }
+                        uint32_t rh, rl, ih, il;
+                        q16_pack(tc[0], tc[1], tc[2], tc[3], rh, rl);
+                        q16_pack(ts[0], ts[1], ts[2], ts[3], ih, il);
+                        const uint32_t ad = a0 + (uint32_t)(r * 256);
+                        i8_sts<0>(ad, rh);
+                        i8_sts<PLANE>(ad, rl);
+                        i8_sts<HALF_ROWS>(ad, ih);
+                        i8_sts<PLANE + HALF_ROWS>(ad, il);
                     }
-                    uint32_t rh, rl, ih, il;
-                    q16_pack(tc[0], tc[1], tc[2], tc[3], rh, rl);
-                    q16_pack(ts[0], ts[1], ts[2], ts[3], ih, il);
-                    const uint32_t ad = a0 + (uint32_t)(r * 256);
-                    i8_sts<0>(ad, rh);
-                    i8_sts<PLANE>(ad, rl);
-                    i8_sts<HALF_ROWS>(ad, ih);
-                    i8_sts<PLANE + HALF_ROWS>(ad, il);
                 }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) i8_arrive_cluster(full0 + (uint32_t)(s * 8));
             }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) i8_arrive_cluster(full0 + (uint32_t)(s * 8));
-        }
+        };
+        if (is_x) produce(std::true_type{});
+        else produce(std::false_type{});
         asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     if (warp < 8) {

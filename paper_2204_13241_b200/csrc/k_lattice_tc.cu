@@ -27,6 +27,7 @@
 // drain -> MMA: tempty[b] (8 arrivals).
 #include "common.cuh"
 #include <cuda_fp16.h>
+#include <type_traits>
 
 namespace xpcs {
 
@@ -372,10 +373,11 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
         const bool is_x = wi < XWARPS;
         const uint32_t slot0 = smem_u32(aslot) + (uint32_t)(warp * ASLOTS * WSLOT * 16);
         const uint32_t full0 = mapa(smem_u32(full), 0);
-        // X rows: d = i + 1/2, i = 64 rank + mr + 8 r, phase d Th_a = (2i + 1) Th_a / 2 turns (33-bit product, the half
-        // unit truncated); W rows: k = bk0 + mr + 8 r, phase Th_0 + k Th_b + c Th_a, c Th_a = (2 H0 + 255) Th_a / 2
-        const uint64_t x_odd = (uint64_t)(2 * ((int)rank * HD + mr) + 1);
-        const uint64_t c_odd = (uint64_t)(2 * H0 + 2 * (PAIR_H / 2) - 1);
+        // X rows: d = i + 1/2, i = 64 rank + mr + 8 r, phase d Th_a = i Th_a + Th_a / 2 turns; W rows: k = bk0 + mr + 8 r,
+        // phase Th_0 + k Th_b + c Th_a, c Th_a = (H0 + 127) Th_a + Th_a / 2 (Th_a / 2 taken as Th_a >> 1 on both sides:
+        // the pair's phases sum to h Th_a exactly or to within one 2^-32 unit)
+        const uint32_t i0 = (uint32_t)((int)rank * HD + mr);
+        const uint32_t cH = (uint32_t)(H0 + PAIR_H / 2 - 1);
         const uint32_t kk = (uint32_t)(g.k0 + bk0 + mr);
         auto prefetch = [&](int li) {
             const int i = grp + li * NGROUPS;
@@ -390,33 +392,35 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
 #pragma unroll
         for (int k = 0; k < ASLOTS - 1; ++k) prefetch(k);
         const unsigned long long MX2 = pack2(12288.0f, 12288.0f);             // |X| <= 1: hi on the 2^-10 grid
-        for (int li = 0;; ++li) {
-            const int i = grp + li * NGROUPS;
-            if (i >= n_stages) break;
-            const int s = i % STAGES;
-            cp_async_wait<ASLOTS - 2>();
-            __syncwarp();
-            prefetch(li + ASLOTS - 1);
-            unsigned long long v[4], st[4], f2[4];
-            float fm = 0.f;
-            {
+        // byte offset of (row m, quad qq) in a plane: [m/8][qq/2][m%8][qq%2 * 8 B]
+        const uint32_t qoff = (uint32_t)((qq >> 1) * 128 + mr * 16 + (qq & 1) * 8);
+        // the stage loop, specialised per warp role (no per-stage branch between the X and W paths)
+        auto produce = [&](auto role) {
+            constexpr bool X = decltype(role)::value;
+            for (int li = 0;; ++li) {
+                const int i = grp + li * NGROUPS;
+                if (i >= n_stages) break;
+                const int s = i % STAGES;
+                cp_async_wait<ASLOTS - 2>();
+                __syncwarp();
+                prefetch(li + ASLOTS - 1);
+                unsigned long long v[4], st[4], f2[4];
+                float fm = 0.f;
                 const uint32_t ra = slot0 + (uint32_t)((li % ASLOTS) * WSLOT * 16);
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const uint32_t a = ra + (uint32_t)((((4 * qq + u) ^ (qq & 2))) * 16);   // record 4 qq + u
-                    uint32_t tha, thb = 0u, th0 = 0u, fw = 0u;
-                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tha) : "r"(a));
-                    if (!is_x) {
-                        asm volatile("ld.shared.u32 %0, [%1+4];" : "=r"(thb) : "r"(a));
-                        asm volatile("ld.shared.u32 %0, [%1+8];" : "=r"(th0) : "r"(a));
-                        asm volatile("ld.shared.u32 %0, [%1+12];" : "=r"(fw) : "r"(a));
-                    }
                     float s0, c0, s1, c1;
-                    if (is_x) {
-                        __sincosf(turns_to_radians((uint32_t)((x_odd * tha) >> 1)), &s0, &c0);
+                    if (X) {
+                        uint32_t tha;
+                        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tha) : "r"(a));
+                        __sincosf(turns_to_radians(i0 * tha + (tha >> 1)), &s0, &c0);
                         twiddle8(tha, s1, c1);
                     } else {
-                        __sincosf(turns_to_radians(th0 + kk * thb + (uint32_t)((c_odd * tha) >> 1)), &s0, &c0);
+                        uint32_t tha, thb, th0, fw;
+                        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                     : "=r"(tha), "=r"(thb), "=r"(th0), "=r"(fw) : "r"(a));
+                        __sincosf(turns_to_radians(kk * thb + th0 + cH * tha + (tha >> 1)), &s0, &c0);
                         twiddle8(thb, s1, c1);
                         const float fj = __uint_as_float(fw);             // padding atoms: f = 0 -> W = 0
                         f2[u] = pack2(fj, fj);
@@ -425,44 +429,44 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
                     v[u] = pack2(c0, s0);
                     st[u] = pack2(c1, s1);
                 }
-            }
-            mbar_wait(&empty[s], (uint32_t)(((i / STAGES) + 1) & 1));
-            const uint32_t sbase = smem_u32(smem) + (uint32_t)(s * STAGE_BYTES);
-            // byte offset of (row m, quad qq) in a plane: [m/8][qq/2][m%8][qq%2 * 8 B]
-            const uint32_t qoff = (uint32_t)((qq >> 1) * 128 + mr * 16 + (qq & 1) * 8);
-            if (!(dbg_flags & 2)) {
-                // rows m = mr + 8 r: real parts (a | wr) into rows m of the hi/lo planes, imaginary parts (b | wi) into
-                // rows 64 + m
-                const uint32_t a0 = sbase + (is_x ? 0u : (uint32_t)(2 * APLANE)) + qoff;
-                const unsigned long long M2 = is_x ? MX2 : pack2(split_magic(fm), split_magic(fm));
+                mbar_wait(&empty[s], (uint32_t)(((i / STAGES) + 1) & 1));
+                const uint32_t sbase = smem_u32(smem) + (uint32_t)(s * STAGE_BYTES);
+                {
+                    // rows m = mr + 8 r: real parts (a | wr) into rows m of the hi/lo planes, imaginary parts (b | wi)
+                    // into rows 64 + m
+                    const uint32_t a0 = sbase + (X ? 0u : (uint32_t)(2 * APLANE)) + qoff;
+                    const unsigned long long M2 = X ? MX2 : pack2(split_magic(fm), split_magic(fm));
 #pragma unroll
-                for (int r = 0; r < RPT; ++r) {
-                    unsigned long long hi[4], lo[4];
+                    for (int r = 0; r < RPT; ++r) {
+                        unsigned long long hi[4], lo[4];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        if (is_x) {
-                            hi[u] = fsub2(fadd2(v[u], M2), M2);               // (c_hi, s_hi), exact in fp16
-                            lo[u] = fsub2(v[u], hi[u]);                        // (c_lo, s_lo)
-                        } else {
-                            const unsigned long long tt = ffma2(f2[u], v[u], M2);
-                            hi[u] = fsub2(tt, M2);                             // f (c, s) hi
-                            lo[u] = ffma2(f2[u], v[u], fsub2(M2, tt));         // f (c, s) - hi, from the exact product
+                        for (int u = 0; u < 4; ++u) {
+                            if (X) {
+                                hi[u] = fsub2(fadd2(v[u], M2), M2);               // (c_hi, s_hi), exact in fp16
+                                lo[u] = fsub2(v[u], hi[u]);                        // (c_lo, s_lo)
+                            } else {
+                                const unsigned long long tt = ffma2(f2[u], v[u], M2);
+                                hi[u] = fsub2(tt, M2);                             // f (c, s) hi
+                                lo[u] = ffma2(f2[u], v[u], fsub2(M2, tt));         // f (c, s) - hi, from the exact product
+                            }
+                            const unsigned long long cd = pack2(lo2(st[u]), lo2(st[u]));
+                            const unsigned long long sd = pack2(-hi2(st[u]), hi2(st[u]));
+                            v[u] = ffma2(swap2(v[u]), sd, fmul2(v[u], cd));
                         }
-                        const unsigned long long cd = pack2(lo2(st[u]), lo2(st[u]));
-                        const unsigned long long sd = pack2(-hi2(st[u]), hi2(st[u]));
-                        v[u] = ffma2(swap2(v[u]), sd, fmul2(v[u], cd));
+                        const uint32_t ad = a0 + (uint32_t)(r * 256);
+                        sts64<0>(ad, pack_h2(lo2(hi[1]), lo2(hi[0])), pack_h2(lo2(hi[3]), lo2(hi[2])));                    // re hi
+                        sts64<APLANE>(ad, pack_h2(lo2(lo[1]), lo2(lo[0])), pack_h2(lo2(lo[3]), lo2(lo[2])));               // re lo
+                        sts64<HALF_ROWS>(ad, pack_h2(hi2(hi[1]), hi2(hi[0])), pack_h2(hi2(hi[3]), hi2(hi[2])));            // im hi
+                        sts64<APLANE + HALF_ROWS>(ad, pack_h2(hi2(lo[1]), hi2(lo[0])), pack_h2(hi2(lo[3]), hi2(lo[2])));   // im lo
                     }
-                    const uint32_t ad = a0 + (uint32_t)(r * 256);
-                    sts64<0>(ad, pack_h2(lo2(hi[1]), lo2(hi[0])), pack_h2(lo2(hi[3]), lo2(hi[2])));                    // re hi
-                    sts64<APLANE>(ad, pack_h2(lo2(lo[1]), lo2(lo[0])), pack_h2(lo2(lo[3]), lo2(lo[2])));               // re lo
-                    sts64<HALF_ROWS>(ad, pack_h2(hi2(hi[1]), hi2(hi[0])), pack_h2(hi2(hi[3]), hi2(hi[2])));            // im hi
-                    sts64<APLANE + HALF_ROWS>(ad, pack_h2(hi2(lo[1]), hi2(lo[0])), pack_h2(hi2(lo[3]), hi2(lo[2])));   // im lo
                 }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> async proxy
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(full0 + (uint32_t)(s * 8));   // the leader's full[s]
             }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> async proxy
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(full0 + (uint32_t)(s * 8));   // the leader's full[s]
-        }
+        };
+        if (is_x) produce(std::true_type{});
+        else produce(std::false_type{});
         cp_async_wait<0>();
     } else {
         // ================= drain warps: TMEM accumulator -> RN fp32 running sums (smem) -> tile =================
