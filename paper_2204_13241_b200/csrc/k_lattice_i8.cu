@@ -153,19 +153,27 @@ __device__ __forceinline__ uint64_t i8_desc(uint32_t saddr) {
 // kind::i8 instruction descriptor: D s32 (2), A/B signed int8 (1), K-major, N = 256, M = 256 (cta_group::2)
 constexpr uint32_t kIdescI8 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(ti8::MMA_N >> 3) << 17) |
                               ((uint32_t)(ti8::PAIR_M >> 4) << 24);
-__device__ __forceinline__ void umma2_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t acc) {
+// warp-uniform issue: the whole warp executes the stage's MMAs and commit, elect.sync picks the issuing lane (always
+// lane 0, so the commit tracks that lane's MMAs); operands stay warp-uniform (no per-instruction ELECT loops)
+__device__ __forceinline__ void umma2_i8_stage(uint32_t tmem, uint64_t a_h, uint64_t a_l, uint64_t b_h, uint64_t b_l,
+                                               uint32_t acc, uint32_t bar) {
     asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "l"(a), "l"(b), "r"(kIdescI8), "r"(acc));
-}
-__device__ __forceinline__ void i8_commit_both(uint64_t* bar) {
-    asm volatile(
-        "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
-        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
-            su32(bar))
+        "{\n\t.reg .pred p, e;\n\t.reg .b16 m;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %7, 0;\n\t"
+        "mov.b16 m, 3;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %2, %4, %6, p;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::i8 [%1], %2, %5, %6, p;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::i8 [%1], %3, %4, %6, 1;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%8], m;\n\t}"
+        ::"r"(tmem), "r"(tmem + 256u), "l"(a_h), "l"(a_l), "l"(b_h), "l"(b_l), "r"(kIdescI8), "r"(acc), "r"(bar)
         : "memory");
+}
+__device__ __forceinline__ void i8_commit_both_elect(uint32_t bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t.reg .b16 m;\n\telect.sync _|e, 0xffffffff;\n\tmov.b16 m, 3;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}"
+        ::"r"(bar) : "memory");
 }
 __device__ __forceinline__ void i8_cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
@@ -244,25 +252,23 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
     const uint32_t tmem = *tmem_slot;
 
     if (warp == MMA_WARP) {
-        // ================= MMA issuer: one lane of the leader CTA drives the pair =================
-        if (rank == 0 && lane == 0) {
-            const uint32_t base = su32(smem);
+        // ================= MMA issuer: the leader CTA's MMA warp drives the pair (one elected lane issues) ==========
+        if (rank == 0) {
+            // descriptors of stage slot 0; slot s adds s * STAGE_BYTES / 16 to the 14-bit address field (no carry:
+            // shared addresses < 2^18)
+            const uint64_t d0 = i8_desc(su32(smem));
+            constexpr uint64_t dP = (uint64_t)(PLANE >> 4), dS = (uint64_t)(STAGE_BYTES >> 4);
             for (int i = 0; i < n_stages; ++i) {
                 const int s = i % STAGES;
                 i8_mbar_wait(&full[s], (uint32_t)((i / STAGES) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t sb = base + s * STAGE_BYTES;
-                const uint64_t a_h = i8_desc(sb), a_l = i8_desc(sb + PLANE);
-                const uint64_t b_h = i8_desc(sb + 2 * PLANE), b_l = i8_desc(sb + 3 * PLANE);
-                const uint32_t acc = i > 0 ? 1u : 0u;
-                if (!(dbg_flags & 4)) {
-                    umma2_i8(tmem, a_h, b_h, acc);          // HH
-                    umma2_i8(tmem + 256, a_h, b_l, acc);    // X
-                    umma2_i8(tmem + 256, a_l, b_h, 1);
-                }
-                i8_commit_both(&empty[s]);
+                const uint64_t a_h = d0 + (uint64_t)s * dS;
+#if XPCS_I8_EXPERIMENTS
+                if (dbg_flags & 4) { i8_commit_both_elect(su32(&empty[s])); continue; }
+#endif
+                umma2_i8_stage(tmem, a_h, a_h + dP, a_h + 2 * dP, a_h + 3 * dP, i > 0 ? 1u : 0u, su32(&empty[s]));
             }
-            i8_commit_both(done);
+            i8_commit_both_elect(su32(done));
         }
         __syncwarp();
     } else if (warp < NPROD_WARPS) {

@@ -164,6 +164,29 @@ __device__ __forceinline__ void umma2_f16(uint32_t d_tmem, uint64_t a, uint64_t 
         "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
         "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
+// warp-uniform issue of one stage: the whole warp executes it, elect.sync picks the issuing lane (always lane 0, so
+// the commits track that lane's MMAs); D += A_hi.B_hi (+ A_hi.B_lo + A_lo.B_hi), commit to empty[s] (and to
+// tfull[b] when bar2 != 0); operands stay warp-uniform (no per-instruction ELECT loops)
+__device__ __forceinline__ void umma2_tc_stage(uint32_t d, uint64_t a_h, uint64_t a_l, uint64_t b_h, uint64_t b_l,
+                                               uint32_t idesc, uint32_t first, uint32_t mma_on, uint32_t lo_on,
+                                               uint32_t bar, uint32_t bar2) {
+    asm volatile(
+        "{\n\t.reg .pred p, e, q, l, t;\n\t.reg .b16 m;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "setp.ne.and.b32 q, %7, 0, e;\n\t"
+        "setp.ne.and.b32 l, %8, 0, q;\n\t"
+        "setp.ne.and.b32 t, %10, 0, e;\n\t"
+        "mov.b16 m, 3;\n\t"
+        "@q tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %3, %5, p;\n\t"
+        "@l tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %4, %5, 1;\n\t"
+        "@l tcgen05.mma.cta_group::2.kind::f16 [%0], %2, %3, %5, 1;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%9], m;\n\t"
+        "@t tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%10], m;\n\t}"
+        ::"r"(d), "l"(a_h), "l"(a_l), "l"(b_h), "l"(b_l), "r"(idesc), "r"(first), "r"(mma_on), "r"(lo_on), "r"(bar),
+          "r"(bar2)
+        : "memory");
+}
 // commit to the barrier at the same offset in both CTAs of the pair
 __device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {
     asm volatile(
@@ -332,11 +355,13 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
     const uint32_t tmem = *tmem_slot;
 
     if (warp == MMA_WARP) {
-        // ================= MMA issuer: one lane of the leader CTA drives the pair =================
-        if (rank == 0 && lane == 0) {
+        // ================= MMA issuer: the leader CTA's MMA warp drives the pair (one elected lane issues) ==========
+        if (rank == 0) {
             const uint32_t idesc = idesc_f16(false);
             const uint32_t lo_on = dbg_flags & 1 ? 0u : 1u;   // experiments: bit 0 drops the hi.lo / lo.hi products
-            const uint32_t base = smem_u32(smem);
+            // descriptors of stage slot 0; slot s adds s * STAGE_BYTES / 16 to the 14-bit address field
+            const uint64_t d0 = umma_desc(smem_u32(smem), 128, 256);
+            constexpr uint64_t dP = (uint64_t)(APLANE >> 4), dS = (uint64_t)(STAGE_BYTES >> 4);
             for (int i = 0; i < n_stages; ++i) {
                 const int s = i % STAGES;
                 const int u = i / SUB_STAGES, b = u & 1;
@@ -347,17 +372,13 @@ k_lattice_tc(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
                 }
                 mbar_wait_cluster(&full[s], (uint32_t)((i / STAGES) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t sb = base + s * STAGE_BYTES;
-                const uint64_t a_h = umma_desc(sb, 128, 256), a_l = umma_desc(sb + APLANE, 128, 256);
-                const uint64_t b_h = umma_desc(sb + 2 * APLANE, 128, 256), b_l = umma_desc(sb + 2 * APLANE + BPLANE, 128, 256);
+                const uint64_t a_h = d0 + (uint64_t)s * dS;
                 const uint32_t d = tmem + (uint32_t)(b * 256);
                 const uint32_t first = sub_first ? 0u : 1u;
-                if (!(dbg_flags & 4)) {   // experiments: bit 2 skips the MMAs (producer/drain cost alone)
-                    umma2_f16(d, a_h, b_h, idesc, first);
-                    if (lo_on) { umma2_f16(d, a_h, b_l, idesc, 1); umma2_f16(d, a_l, b_h, idesc, 1); }
-                }
-                umma2_commit_both(&empty[s]);                     // frees the stage in both CTAs
-                if ((i % SUB_STAGES) == SUB_STAGES - 1 || i == n_stages - 1) umma2_commit_both(&tfull[b]);
+                const bool last_sub = (i % SUB_STAGES) == SUB_STAGES - 1 || i == n_stages - 1;
+                // experiments: bit 2 skips the MMAs (producer/drain cost alone)
+                umma2_tc_stage(d, a_h, a_h + dP, a_h + 2 * dP, a_h + 3 * dP, idesc, first, (dbg_flags & 4) ? 0u : 1u,
+                               lo_on, smem_u32(&empty[s]), last_sub ? smem_u32(&tfull[b]) : 0u);
             }
         }
         __syncwarp();
