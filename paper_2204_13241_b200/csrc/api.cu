@@ -460,19 +460,21 @@ static int64_t i8_tiles(const LatticeGeom& g) { return ((g.n_h + 255) / 256) * (
 // accumulation) and stay <= kI8MaxChunk; cost = waves x (stages per CTA + kI8CtaCost), the smallest C wins ties
 static int64_t i8_plan_chunk(int64_t Ng, int64_t units, double* cost_out) {
     const int64_t wave = std::max<int64_t>(1, i8_cluster_slots());
+    const int64_t ks = i8_stage_atoms();
+    const double cta_cost = i8_cta_cost() * 32.0 / (double)ks;   // the fixed cost is calibrated in 32-atom stages
     const int64_t cmin = std::max<int64_t>(1, (Ng + kI8MaxChunk - 1) / kI8MaxChunk);
     const int64_t cmax = std::max<int64_t>(cmin, std::min<int64_t>((Ng + 1023) / 1024, 64));
     int64_t best = cmin;
     double best_cost = 1e300;
     for (int64_t c = cmin; c <= cmax; ++c) {
-        const int64_t ch = std::min<int64_t>(((Ng + c - 1) / c + 31) / 32 * 32, kI8MaxChunk);
+        const int64_t ch = std::min<int64_t>(((Ng + c - 1) / c + ks - 1) / ks * ks, kI8MaxChunk);
         const int64_t cc = (Ng + ch - 1) / ch;
         const double waves = std::ceil((double)(units * cc) / (double)wave);
-        const double cost = waves * ((double)(ch / 32) + i8_cta_cost());
+        const double cost = waves * ((double)(ch / ks) + cta_cost);
         if (cost < best_cost * (1.0 - 1e-9)) { best_cost = cost; best = c; }
     }
-    if (cost_out) *cost_out = best_cost;
-    return std::min<int64_t>(((Ng + best - 1) / best + 31) / 32 * 32, kI8MaxChunk);
+    if (cost_out) *cost_out = best_cost * (double)ks / 32.0;   // in 32-atom stage units (kI8BatchCost)
+    return std::min<int64_t>(((Ng + best - 1) / best + ks - 1) / ks * ks, kI8MaxChunk);
 }
 
 // split of V virtual frames into [V1 | V - V1] batches with their own chunking (V1 = 0: no split), memoised: the

@@ -181,6 +181,7 @@ bool lattice_tc_supported(const LatticeGeom& g);
 // uniform_f != 0: all f_j = 1 (no W scale); else F = max |f_j| is reduced into fmax_scratch (1 float) first.
 constexpr int64_t kI8MaxChunk = 32768;
 int i8_cluster_slots();   // k_lattice_i8 clusters resident at once (cudaOccupancyMaxActiveClusters)
+int i8_stage_atoms();     // k_lattice_i8 atoms per pipeline stage (chunks are multiples of it)
 cudaError_t launch_absmax_f(const uint4* staged, int64_t n, float* out, cudaStream_t s);   // max |f| of staged records
 // Bright pixels after the integer engine (k_fixup.cu): the epilogue that writes a batch's final I (or p) appends
 // every pixel with I > thr * F(q)^2 (F = *fmax or 1; species: max_s |f_s(q)|) to `list` (index v * n_q + pixel of the

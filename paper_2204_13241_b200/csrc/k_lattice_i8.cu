@@ -46,20 +46,26 @@ namespace ti8 {
 constexpr int HD = 64;                              // d values per CTA (the pair covers 128 d = 256 h rows)
 constexpr int TM = 2 * HD;                          // A rows per CTA: [a | b]
 constexpr int PAIR_H = 4 * HD;                      // 256 output rows h per pair tile
-constexpr int TN = 128, KS = 32;                    // pair tile cols (k), atoms per stage
+#ifndef XPCS_I8_KS
+#define XPCS_I8_KS 32
+#endif
+constexpr int TN = 128, KS = XPCS_I8_KS;            // pair tile cols (k), atoms per stage (32 or 64)
+static_assert(KS == 32 || KS == 64, "stage of 32 or 64 atoms");
+constexpr int KQ = KS / 16;                         // 16-atom K slices per stage (one X and one W warp each)
+constexpr int RG = 8 * KS;                          // bytes per 8-row core-matrix group of a plane (SBO)
 constexpr int BK = TN / 2;                          // k per CTA; B rows per CTA: [wr | wi] = 128
 constexpr int PAIR_M = 2 * TM;                      // MMA M = 256
-constexpr int PLANE = TM * KS;                      // int8 plane: 128 rows x 32 atoms = 4 KB (A and B alike)
-constexpr int HALF_ROWS = HD / 8 * 256;             // byte offset of row 64 in a plane (8-row core groups of 256 B)
-constexpr int STAGE_BYTES = 4 * PLANE;              // A_hi A_lo B_hi B_lo = 16 KB
+constexpr int PLANE = TM * KS;                      // int8 plane: 128 rows x KS atoms (A and B alike)
+constexpr int HALF_ROWS = HD / 8 * RG;              // byte offset of row 64 in a plane
+constexpr int STAGE_BYTES = 4 * PLANE;              // A_hi A_lo B_hi B_lo = 16 KB (KS = 32) / 32 KB (KS = 64)
 #ifndef XPCS_I8_STAGES
-#define XPCS_I8_STAGES 8
+#define XPCS_I8_STAGES (XPCS_I8_KS == 64 ? 6 : 8)
 #endif
 constexpr int STAGES = XPCS_I8_STAGES;
 #ifndef XPCS_I8_GROUPS
-#define XPCS_I8_GROUPS 5
+#define XPCS_I8_GROUPS (XPCS_I8_KS == 64 ? 3 : 5)
 #endif
-constexpr int NGROUPS = XPCS_I8_GROUPS, GROUP_WARPS = 4;   // per group: 2 X warps, 2 W warps (one per K half)
+constexpr int NGROUPS = XPCS_I8_GROUPS, GROUP_WARPS = 2 * KQ;   // per group: KQ X warps, KQ W warps (one per K slice)
 static_assert(NGROUPS <= STAGES, "mbarrier parity: producer groups must not exceed the stage count");
 constexpr int NPROD_WARPS = NGROUPS * GROUP_WARPS;
 constexpr int MMA_WARP = NPROD_WARPS;               // producer warps 0-7 (two per TMEM lane quarter) also drain the tile
@@ -146,7 +152,7 @@ __device__ __forceinline__ uint64_t i8_desc(uint32_t saddr) {
     uint64_t d = 0;
     d |= (uint64_t)((saddr >> 4) & 0x3FFF);
     d |= (uint64_t)((128u >> 4) & 0x3FFF) << 16;
-    d |= (uint64_t)((256u >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)(((uint32_t)ti8::RG >> 4) & 0x3FFF) << 32;
     d |= (uint64_t)1 << 46;
     return d;
 }
@@ -154,19 +160,18 @@ __device__ __forceinline__ uint64_t i8_desc(uint32_t saddr) {
 constexpr uint32_t kIdescI8 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(ti8::MMA_N >> 3) << 17) |
                               ((uint32_t)(ti8::PAIR_M >> 4) << 24);
 // warp-uniform issue: the whole warp executes the stage's MMAs and commit, elect.sync picks the issuing lane (always
-// lane 0, so the commit tracks that lane's MMAs); operands stay warp-uniform (no per-instruction ELECT loops)
-__device__ __forceinline__ void umma2_i8_stage(uint32_t tmem, uint64_t a_h, uint64_t a_l, uint64_t b_h, uint64_t b_l,
-                                               uint32_t acc, uint32_t bar) {
+// lane 0, so the commit tracks that lane's MMAs); operands stay warp-uniform (no per-instruction ELECT loops).
+// One K = 32 step: HH += A_hi.B_hi, X += A_hi.B_lo + A_lo.B_hi; `acc` = 0 overwrites the accumulators.
+__device__ __forceinline__ void umma2_i8_kstep(uint32_t tmem, uint64_t a_h, uint64_t a_l, uint64_t b_h, uint64_t b_l,
+                                               uint32_t acc) {
     asm volatile(
-        "{\n\t.reg .pred p, e;\n\t.reg .b16 m;\n\t"
+        "{\n\t.reg .pred p, e;\n\t"
         "elect.sync _|e, 0xffffffff;\n\t"
         "setp.ne.b32 p, %7, 0;\n\t"
-        "mov.b16 m, 3;\n\t"
         "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %2, %4, %6, p;\n\t"
         "@e tcgen05.mma.cta_group::2.kind::i8 [%1], %2, %5, %6, p;\n\t"
-        "@e tcgen05.mma.cta_group::2.kind::i8 [%1], %3, %4, %6, 1;\n\t"
-        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%8], m;\n\t}"
-        ::"r"(tmem), "r"(tmem + 256u), "l"(a_h), "l"(a_l), "l"(b_h), "l"(b_l), "r"(kIdescI8), "r"(acc), "r"(bar)
+        "@e tcgen05.mma.cta_group::2.kind::i8 [%1], %3, %4, %6, 1;\n\t}"
+        ::"r"(tmem), "r"(tmem + 256u), "l"(a_h), "l"(a_l), "l"(b_h), "l"(b_l), "r"(kIdescI8), "r"(acc)
         : "memory");
 }
 __device__ __forceinline__ void i8_commit_both_elect(uint32_t bar) {
@@ -266,7 +271,12 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
 #if XPCS_I8_EXPERIMENTS
                 if (dbg_flags & 4) { i8_commit_both_elect(su32(&empty[s])); continue; }
 #endif
-                umma2_i8_stage(tmem, a_h, a_h + dP, a_h + 2 * dP, a_h + 3 * dP, i > 0 ? 1u : 0u, su32(&empty[s]));
+#pragma unroll
+                for (int ks = 0; ks < KS / 32; ++ks) {       // K = 32 per MMA: the next 32 atoms are 2 core matrices on
+                    const uint64_t a = a_h + (uint64_t)(ks * 16);  // (256 B >> 4)
+                    umma2_i8_kstep(tmem, a, a + dP, a + 2 * dP, a + 3 * dP, (i > 0 || ks > 0) ? 1u : 0u);
+                }
+                i8_commit_both_elect(su32(&empty[s]));
             }
             i8_commit_both_elect(su32(done));
         }
@@ -275,8 +285,8 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
         // ================= producers: group g fills stages g, g + NGROUPS, g + 2 NGROUPS, ... =================
         const int grp = warp / GROUP_WARPS, wi = warp % GROUP_WARPS;
         const int qq = lane & 3, mr = lane >> 2;
-        const bool is_x = wi < 2;
-        const int qh = wi & 1;                                // K half of the stage (atoms 16 qh .. 16 qh + 15)
+        const bool is_x = wi < KQ;
+        const int qh = wi % KQ;                               // K slice of the stage (atoms 16 qh .. 16 qh + 15)
         const uint32_t full0 = i8_mapa(su32(full), 0);
         // every warp prefetches its own 16 atom records with cp.async into a private ring: no cross-warp barrier
         const uint32_t slot0 = su32(aslot) + (uint32_t)(warp * ASL * WSLOT * 16);
@@ -356,7 +366,7 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
                         uint32_t rh, rl, ih, il;
                         q16_pack(tc[0], tc[1], tc[2], tc[3], rh, rl);
                         q16_pack(ts[0], ts[1], ts[2], ts[3], ih, il);
-                        const uint32_t ad = a0 + (uint32_t)(r * 256);
+                        const uint32_t ad = a0 + (uint32_t)(r * RG);
                         i8_sts<0>(ad, rh);
                         i8_sts<PLANE>(ad, rl);
                         i8_sts<HALF_ROWS>(ad, ih);
@@ -471,6 +481,8 @@ cudaError_t launch_absmax_f(const uint4* staged, int64_t n, float* out, cudaStre
 }
 
 // clusters of k_lattice_i8 resident at once on the current device (one wave); sm_count / 2 if the query fails
+int i8_stage_atoms() { return ti8::KS; }
+
 int i8_cluster_slots() {
     using namespace ti8;
     static int cached[64];
