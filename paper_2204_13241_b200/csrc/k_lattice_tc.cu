@@ -38,7 +38,7 @@ constexpr int PAIR_M = 2 * TM;                    // MMA M = 256
 constexpr int PAIR_H = 4 * HD;                    // 256 output rows h per pair tile
 constexpr int BN = TN / 2;                        // k per CTA; B rows per CTA: [wr | wi] = 128
 #ifndef XPCS_TC_STAGES
-#define XPCS_TC_STAGES 5
+#define XPCS_TC_STAGES 4
 #endif
 constexpr int STAGES = XPCS_TC_STAGES;
 #ifndef XPCS_TC_SUB_STAGES
@@ -51,7 +51,7 @@ constexpr int HALF_ROWS = HD / 8 * 256;           // byte offset of row 64 in a 
 constexpr int STAGE_BYTES = 2 * APLANE + 2 * BPLANE;   // A_hi A_lo | B_hi B_lo = 16 KB
 constexpr int MMA_N = 2 * TN;                     // N = 256: [wr | wi] of 64 k per CTA half
 #ifndef XPCS_TC_GROUPS
-#define XPCS_TC_GROUPS 5
+#define XPCS_TC_GROUPS 4
 #endif
 constexpr int RPT = 8, XWARPS = 1, WWARPS = 1;    // rows per producer thread; X / W warps per group
 constexpr int NGROUPS = XPCS_TC_GROUPS, GROUP_WARPS = XWARPS + WWARPS;
