@@ -1051,10 +1051,16 @@ int xsvs_contrast(const void* I_series, int64_t frames, int64_t n_q, const int32
     ProfScope p(o.profile, KC_XSVS, o.s);
     PlanBufs pb;
     TRY(make_plan(bin_of_q, n_q, n_bins, o.s, pb));
-    double* mom = (double*)scratch(o.s, SS_XSVS, sizeof(double2) * (size_t)(pb.max_warps * max_slots));
+    // per-warp moments, then the per-(slot, ring) moments (summed over the ring's warps), then beta from those
+    int64_t all_slots = 0;
+    for (int64_t i = 0; i < n_windows; ++i) all_slots += frames / windows[i];
+    const size_t warp_bytes = sizeof(double2) * (size_t)(pb.max_warps * max_slots);
+    double* mom = (double*)scratch(o.s, SS_XSVS, warp_bytes + sizeof(double) * 3 * (size_t)(all_slots * n_bins));
     if (!mom) return XPCS_ENOMEM;
-    return cuda_fail(launch_xsvs(I_series, o.in_f64, frames, n_q, pb.plan, n_bins, windows, n_windows, pb.max_warps,
-                                 mom, nullptr, beta_out, o.s), "xsvs");
+    double* ring_mom = (double*)((char*)mom + warp_bytes);
+    TRY(cuda_fail(launch_xsvs(I_series, o.in_f64, frames, n_q, pb.plan, n_bins, windows, n_windows, pb.max_warps,
+                              mom, ring_mom, o.s), "xsvs"));
+    return cuda_fail(launch_xsvs_beta_from_moments(ring_mom, frames, windows, n_windows, n_bins, beta_out, o.s), "xsvs beta");
 }
 
 // ------------------------------------------------------------------------------------------- ring moments
@@ -1138,7 +1144,7 @@ int xsvs_moments(const void* I_series, int64_t frames, int64_t n_q, const int32_
     double* mom = (double*)scratch(o.s, SS_XSVS, sizeof(double2) * (size_t)(pb.max_warps * max_pass));
     if (!mom) return XPCS_ENOMEM;
     return cuda_fail(launch_xsvs(I_series, o.in_f64, frames, n_q, pb.plan, n_bins, windows, n_windows, pb.max_warps,
-                                 mom, moments_out, nullptr, o.s), "xsvs moments");
+                                 mom, moments_out, o.s), "xsvs moments");
 }
 
 int xsvs_contrast_from_moments(const double* moments, int64_t frames, const int32_t* windows, int64_t n_windows,

@@ -255,7 +255,7 @@ cudaError_t launch_speckle_hist(const void* I, int in_f64, int64_t T, int64_t n_
                                 double kappa_max, int64_t* counts, cudaStream_t s);
 cudaError_t launch_xsvs(const void* I, int in_f64, int64_t T, int64_t n_q, BinPlan plan, int32_t n_bins,
                         const int32_t* windows_host, int64_t n_windows, int64_t max_warps, double* warp_moments,
-                        double* mom_out, double* beta_out, cudaStream_t s);   // mom_out != NULL: moments, no beta
+                        double* mom_out, cudaStream_t s);   // per (slot, ring) moments; beta: launch_xsvs_beta_from_moments
 cudaError_t launch_xsvs_beta_from_moments(const double* mom, int64_t T, const int32_t* windows_host, int64_t n_windows,
                                           int32_t n_bins, double* beta_out, cudaStream_t s);
 cudaError_t launch_shell_moments(const void* v, int in_f64, int64_t rows, int64_t n_q, BinPlan plan, int32_t n_bins,

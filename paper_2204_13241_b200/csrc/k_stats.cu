@@ -477,7 +477,7 @@ k_xsvs_warp(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __r
                     if (sidx[k] < ws.S[w0 + k]) {
                         const double m1 = warp_sum_d(run[k]);
                         const double m2 = warp_sum_d(run[k] * run[k]);
-                        if (lane == 0) mom[gw * ws.total_slots + ws.base[w0 + k] + sidx[k]] = make_double2(m1, m2);
+                        if (lane == 0) mom[(int64_t)(ws.base[w0 + k] + sidx[k]) * total_warps + gw] = make_double2(m1, m2);
                         ++sidx[k];
                     }
                     run[k] = 0.0;
@@ -504,9 +504,18 @@ k_xsvs_warp(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __r
 #define XPCS_XSVS_WARPS 4
 #endif
 namespace { constexpr int XB = XPCS_XSVS_XB, XWARPS = XPCS_XSVS_WARPS, XFC = XPCS_XSVS_FC; }
+static_assert(XFC % 4 == 0, "the close-mask loop reads four frames per word");
+// per-frame close masks (bit k: window k of the pass closes after frame t) are built once per block in shared
+// memory, so a frame costs one byte test instead of a scan over the windows; the window state stays in registers
+constexpr int XMASK_MAX = 16384;   // frames a pass can cover with the shared-memory mask (longer series: k_xsvs_warp)
 template <typename In>
-__host__ __device__ constexpr size_t xsvs2_smem() {
-    return (size_t)XWARPS * ((size_t)XB * 33 * sizeof(double2) + (size_t)XB * sizeof(int) + 2 * XFC * 32 * sizeof(In));
+__host__ __device__ constexpr size_t xsvs2_warp_smem() {
+    return (size_t)XB * 33 * sizeof(double2) + (size_t)XB * sizeof(int) + 2 * XFC * 32 * sizeof(In);
+}
+__host__ __device__ constexpr size_t xsvs2_mask_bytes(int64_t tuse) { return (size_t)((tuse + 15) / 16) * 16; }
+template <typename In>
+__host__ __device__ constexpr size_t xsvs2_smem(int64_t tuse) {
+    return xsvs2_mask_bytes(tuse) + (size_t)XWARPS * xsvs2_warp_smem<In>();
 }
 template <typename In>
 __global__ void __launch_bounds__(32 * XWARPS)
@@ -515,10 +524,25 @@ k_xsvs_warp2(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __
              WinSet ws, double2* __restrict__ mom) {
     extern __shared__ __align__(16) unsigned char xs_smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    unsigned char* base = xs_smem + (size_t)wib * (XB * 33 * sizeof(double2) + XB * sizeof(int) + 2 * XFC * 32 * sizeof(In));
+    const int nw = ws.n;
+    int64_t Tuse = 0;
+#pragma unroll
+    for (int k = 0; k < XW; ++k)
+        if (k < nw) Tuse = max(Tuse, (int64_t)ws.S[k] * ws.W[k]);
+    uint32_t* cmask = reinterpret_cast<uint32_t*>(xs_smem);      // byte t: windows closing after frame t
+    unsigned char* base = xs_smem + xsvs2_mask_bytes(Tuse) + (size_t)wib * xsvs2_warp_smem<In>();
     double2 (*B)[33] = reinterpret_cast<double2 (*)[33]>(base);
     In* ser = reinterpret_cast<In*>(base + XB * 33 * sizeof(double2));          // [2][XFC][32]
     int* ids = reinterpret_cast<int*>(base + XB * 33 * sizeof(double2) + 2 * XFC * 32 * sizeof(In));
+    // close masks: thread k.. marks frames s W_k - 1 (windows aligned at t = 0, remainder dropped)
+    for (int i = threadIdx.x; i < (int)((Tuse + 3) / 4); i += blockDim.x) cmask[i] = 0u;
+    __syncthreads();
+    for (int k = 0; k < nw; ++k)
+        for (int sI = threadIdx.x; sI < ws.S[k]; sI += blockDim.x) {
+            const int t = (sI + 1) * ws.W[k] - 1;
+            atomicOr(&cmask[t >> 2], (1u << k) << (8 * (t & 3)));
+        }
+    __syncthreads();
     const int64_t gw = (int64_t)blockIdx.x * XWARPS + wib;
     if (gw >= total_warps || gw >= woff[n_bins]) return;
     int lo = 0, hi = n_bins;
@@ -530,33 +554,26 @@ k_xsvs_warp2(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __
     const int64_t idx = off[b] + (gw - woff[b]) * 32 + lane;
     const bool valid = idx < off[b + 1];
     const int64_t px = valid ? perm[idx] : 0;
-    const int nw = ws.n;
-    // running prefix sum P of the series; window k closes at frames t + 1 = W_k, 2 W_k, ... (aligned, non-overlapping)
-    // and its sum is P - (P at its previous close): per frame one DADD and one compare against the next close
+    // running prefix sum P of the series; window k's sum at a close is P - (P at its previous close)
     double P = 0.0, lastP[XW];
-    int nextc[XW], sidx[XW];
-    int nc = INT_MAX;
-    int64_t Tuse = 0;
+    int sidx[XW];
 #pragma unroll
-    for (int k = 0; k < XW; ++k) {
-        lastP[k] = 0.0;
-        sidx[k] = 0;
-        nextc[k] = (k < nw && ws.S[k] > 0) ? ws.W[k] : INT_MAX;
-        nc = min(nc, nextc[k]);
-        if (k < nw) Tuse = max(Tuse, (int64_t)ws.S[k] * ws.W[k]);
-    }
+    for (int k = 0; k < XW; ++k) { lastP[k] = 0.0; sidx[k] = 0; }
     const int n_chunks = (int)((Tuse + XFC - 1) / XFC);
+    const In* src0 = I + px;                                  // this lane's pixel column, frame 0
+    const uint32_t src_bytes = valid ? (uint32_t)sizeof(In) : 0u;
     auto prefetch = [&](int c) {
         if (c < n_chunks) {
             const uint32_t dst0 = (uint32_t)__cvta_generic_to_shared(ser + (size_t)(c & 1) * XFC * 32 + lane);
+            const int64_t t0 = (int64_t)c * XFC;
+            const In* src = src0 + t0 * n_q;
+            const int un = (int)min((int64_t)XFC, Tuse - t0);
 #pragma unroll 8
             for (int u = 0; u < XFC; ++u) {
-                const int64_t t = (int64_t)c * XFC + u;
-                const bool ok = valid && t < Tuse;
-                const In* src = I + (ok ? t * n_q + px : 0);
                 asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(dst0 + (uint32_t)(u * 32 * sizeof(In))),
-                             "l"(src), "n"(sizeof(In)), "r"(ok ? (uint32_t)sizeof(In) : 0u)
+                             "l"(u < un ? src : src0), "n"(sizeof(In)), "r"(u < un ? src_bytes : 0u)
                              : "memory");
+                src += n_q;
             }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
@@ -572,7 +589,7 @@ k_xsvs_warp2(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __
                 m1 += v.x;
                 m2 += v.y;
             }
-            mom[gw * ws.total_slots + ids[lane]] = make_double2(m1, m2);
+            mom[(int64_t)ids[lane] * total_warps + gw] = make_double2(m1, m2);   // slot-major: a ring's warps contiguous
         }
         __syncwarp();
         nb = 0;
@@ -583,25 +600,31 @@ k_xsvs_warp2(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __
         asm volatile("cp.async.wait_group 1;" ::: "memory");
         __syncwarp();
         const In* sc = ser + (size_t)(c & 1) * XFC * 32 + lane;
-        const int un = (int)min((int64_t)XFC, Tuse - (int64_t)c * XFC);
-        for (int u = 0; u < un; ++u) {
-            P += (double)sc[u * 32];
-            const int t1 = c * XFC + u + 1;           // frames consumed
-            if (t1 != nc) continue;                   // warp-uniform
-            nc = INT_MAX;
+        const int t0 = c * XFC;
+        const int un = (int)min((int64_t)XFC, Tuse - (int64_t)t0);
+        for (int u0 = 0; u0 < un; u0 += 4) {          // 4 frames per step: their loads and masks in flight at once
+            double v[4];
 #pragma unroll
-            for (int k = 0; k < XW; ++k) {
-                if (k >= nw) break;
-                if (nextc[k] == t1) {
-                    const double val = P - lastP[k];
-                    lastP[k] = P;
-                    B[nb][lane] = make_double2(val, val * val);
-                    if (lane == 0) ids[nb] = ws.base[k] + sidx[k];
-                    ++sidx[k];
-                    nextc[k] = sidx[k] < ws.S[k] ? nextc[k] + ws.W[k] : INT_MAX;
-                    if (++nb == XB) flush();
+            for (int i = 0; i < 4; ++i) v[i] = u0 + i < un ? (double)sc[(u0 + i) * 32] : 0.0;
+            const uint32_t m4 = cmask[(t0 + u0) >> 2];     // t0 and u0 are multiples of 4: one word, warp-uniform
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                P += v[i];
+                uint32_t m = (m4 >> (8 * i)) & 0xFFu;       // frames past un have no close bits
+                if (m == 0u) continue;
+#pragma unroll
+                for (int k = 0; k < XW; ++k) {
+                    if (m == 0u) break;                   // stop after the last closing window
+                    if (m & 1u) {
+                        const double val = P - lastP[k];
+                        lastP[k] = P;
+                        B[nb][lane] = make_double2(val, val * val);
+                        if (lane == 0) ids[nb] = ws.base[k] + sidx[k];
+                        ++sidx[k];
+                        if (++nb == XB) flush();
+                    }
+                    m >>= 1;
                 }
-                nc = min(nc, nextc[k]);
             }
         }
         __syncwarp();                             // chunk c's buffer is refilled by prefetch(c + 2)
@@ -610,85 +633,62 @@ k_xsvs_warp2(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __
     if (nb > 0) flush();
 }
 
-__global__ void __launch_bounds__(256)
-k_xsvs_final(const double2* __restrict__ mom, const int32_t* __restrict__ off, const int32_t* __restrict__ woff,
-             WinSet ws, int w_first, int32_t n_bins, double* __restrict__ beta_out) {
-    // block = (window, ring).  Snapshots s are spread over the threads; when there are fewer than 256 snapshots,
-    // tp = 256 / S (power of two) threads share one snapshot and split the ring's warps g (strided), their partial
-    // moments combined in a fixed order (deterministic), so long windows (few snapshots) are not one serial chain.
-    __shared__ double sh[256];
-    __shared__ double2 part[256];
-    const int w = blockIdx.x, b = blockIdx.y;
-    const int m0 = off[b + 1] - off[b];
-    const int S = ws.S[w];
-    const int g0 = woff[b], g1 = woff[b + 1];
-    int tp = 1;
-    while (tp * 2 * S <= 256 && tp < 64) tp *= 2;
-    const int j = threadIdx.x % tp, sl = threadIdx.x / tp, sstride = 256 / tp;
-    double acc = 0.0;
-    for (int s0 = 0; s0 < S; s0 += sstride) {
-        const int s = s0 + sl;
-        double m1 = 0.0, m2 = 0.0;
-        if (s < S) {
-#pragma unroll 4
-            for (int g = g0 + j; g < g1; g += tp) {
-                const double2 v = mom[(int64_t)g * ws.total_slots + ws.base[w] + s];
-                m1 += v.x;
-                m2 += v.y;
-            }
-        }
-        part[threadIdx.x] = make_double2(m1, m2);
-        __syncthreads();
-        if (j == 0 && s < S) {
-            double a1 = 0.0, a2 = 0.0;
-            for (int k = 0; k < tp; ++k) { a1 += part[threadIdx.x + k].x; a2 += part[threadIdx.x + k].y; }
-            const double mean = a1 / m0;
-            acc += (a2 / m0 - mean * mean) / (mean * mean);           // Eq.(17), population variance
-        }
-        __syncthreads();
-    }
-    const double tot = block_sum_d(acc, sh);
-    if (threadIdx.x == 0)
-        beta_out[(int64_t)(w_first + w) * n_bins + b] = m0 > 0 ? tot / S : __longlong_as_double(0x7ff8000000000000ll);
-}
-
 // per (slot, ring) moments (m0 = ring pixel count, m1, m2) summed over the ring's warps in warp order, for
 // xsvs_moments (a q-sharded detector adds these over ranks before forming beta)
 __global__ void __launch_bounds__(256)
 k_xsvs_final_moments(const double2* __restrict__ mom, const int32_t* __restrict__ off, const int32_t* __restrict__ woff,
-                     WinSet ws, int64_t slot_first, int32_t n_bins, double* __restrict__ out) {
+                     WinSet ws, int64_t slot_first, int32_t n_bins, int64_t total_warps, double* __restrict__ out) {
     const int w = blockIdx.x, b = blockIdx.y;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const double m0 = (double)(off[b + 1] - off[b]);
-    for (int s = threadIdx.x; s < ws.S[w]; s += blockDim.x) {
+    const int64_t g0 = woff[b], g1 = woff[b + 1];
+    const int sI = blockIdx.z * 8 + wid;                      // one warp per snapshot, fixed-order shuffle tree
+    if (sI < ws.S[w]) {
+        const double2* row = mom + (int64_t)(ws.base[w] + sI) * total_warps;
         double m1 = 0.0, m2 = 0.0;
-        for (int g = woff[b]; g < woff[b + 1]; ++g) {
-            const double2 v = mom[(int64_t)g * ws.total_slots + ws.base[w] + s];
+#pragma unroll 4
+        for (int64_t g = g0 + lane; g < g1; g += 32) {
+            const double2 v = row[g];
             m1 += v.x;
             m2 += v.y;
         }
-        double* o = out + ((slot_first + ws.base[w] + s) * n_bins + b) * 3;
-        o[0] = m0;
-        o[1] = m1;
-        o[2] = m2;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            m1 += __shfl_xor_sync(0xffffffffu, m1, o);
+            m2 += __shfl_xor_sync(0xffffffffu, m2, o);
+        }
+        if (lane == 0) {
+            double* o = out + ((slot_first + ws.base[w] + sI) * n_bins + b) * 3;
+            o[0] = m0;
+            o[1] = m1;
+            o[2] = m2;
+        }
     }
 }
 
-// beta_{W,b} from summed moments (Eq. 17 per snapshot, population variance, then the mean over snapshots)
-__global__ void __launch_bounds__(256)
+// beta_{W,b} from summed moments (Eq. 17 per snapshot, population variance, then the mean over snapshots); block =
+// (window, ring), threads over snapshots, a fixed-order tree (deterministic)
+__global__ void __launch_bounds__(128)
 k_xsvs_beta_from_moments(const double* __restrict__ mom, WinSet ws, int64_t slot_first, int w_first, int32_t n_bins,
                          double* __restrict__ beta_out) {
-    const int w = blockIdx.x;
-    for (int b = threadIdx.x; b < n_bins; b += blockDim.x) {
-        double acc = 0.0;
-        bool ok = ws.S[w] > 0;
-        for (int sI = 0; sI < ws.S[w]; ++sI) {
-            const double* o = mom + ((slot_first + ws.base[w] + sI) * n_bins + b) * 3;
-            if (!(o[0] > 0.0)) { ok = false; break; }
-            const double mean = o[1] / o[0];
-            acc += (o[2] / o[0] - mean * mean) / (mean * mean);
-        }
-        beta_out[(int64_t)(w_first + w) * n_bins + b] = ok ? acc / ws.S[w] : __longlong_as_double(0x7ff8000000000000ll);
+    __shared__ double sh[128];
+    const int w = blockIdx.x, b = blockIdx.y, S = ws.S[w];
+    double acc = 0.0;
+    int bad = S <= 0;
+    for (int sI = threadIdx.x; sI < S; sI += 128) {
+        const double* o = mom + ((slot_first + ws.base[w] + sI) * n_bins + b) * 3;
+        if (!(o[0] > 0.0)) { bad = 1; continue; }
+        const double mean = o[1] / o[0];
+        acc += (o[2] / o[0] - mean * mean) / (mean * mean);
     }
+    sh[threadIdx.x] = acc;
+    bad = __syncthreads_or(bad);
+    for (int h = 64; h > 0; h >>= 1) {
+        if (threadIdx.x < h) sh[threadIdx.x] += sh[threadIdx.x + h];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        beta_out[(int64_t)(w_first + w) * n_bins + b] = bad ? __longlong_as_double(0x7ff8000000000000ll) : sh[0] / S;
 }
 
 cudaError_t launch_xsvs_beta_from_moments(const double* mom, int64_t T, const int32_t* windows_host, int64_t n_windows,
@@ -706,7 +706,7 @@ cudaError_t launch_xsvs_beta_from_moments(const double* mom, int64_t T, const in
         }
         ws.total_slots = slots;
         note_launch();
-        k_xsvs_beta_from_moments<<<ws.n, 256, 0, s>>>(mom, ws, slot_first, (int)w0, n_bins, beta_out);
+        k_xsvs_beta_from_moments<<<dim3(ws.n, n_bins), 128, 0, s>>>(mom, ws, slot_first, (int)w0, n_bins, beta_out);
         slot_first += slots;
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
@@ -716,7 +716,7 @@ cudaError_t launch_xsvs_beta_from_moments(const double* mom, int64_t T, const in
 
 cudaError_t launch_xsvs(const void* I, int in_f64, int64_t T, int64_t n_q, BinPlan plan, int32_t n_bins,
                         const int32_t* windows_host, int64_t n_windows, int64_t max_warps, double* warp_moments,
-                        double* mom_out, double* beta_out, cudaStream_t s) {
+                        double* mom_out, cudaStream_t s) {
     int64_t slot_first = 0;
     for (int64_t w0 = 0; w0 < n_windows; w0 += XW) {
         WinSet ws{};
@@ -739,24 +739,30 @@ cudaError_t launch_xsvs(const void* I, int in_f64, int64_t T, int64_t n_q, BinPl
         }
 #else
         const unsigned blocks = (unsigned)((max_warps + XWARPS - 1) / XWARPS);
-        if (blocks > 0) {
+        int64_t tuse = 0;
+        for (int i = 0; i < ws.n; ++i) tuse = std::max<int64_t>(tuse, (int64_t)ws.S[i] * ws.W[i]);
+        if (tuse > XMASK_MAX) {   // very long series: one warp per window (no shared-memory close mask)
+            const dim3 gr((unsigned)((max_warps + 3) / 4), (unsigned)((ws.n + XWPW - 1) / XWPW));
+            if (blocks > 0) {
+                if (in_f64) k_xsvs_warp<double><<<gr, 128, 0, s>>>((const double*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, ws, (double2*)warp_moments);
+                else k_xsvs_warp<float><<<gr, 128, 0, s>>>((const float*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, ws, (double2*)warp_moments);
+            }
+        } else if (blocks > 0) {
+            const size_t sm = in_f64 ? xsvs2_smem<double>(tuse) : xsvs2_smem<float>(tuse);
             if (in_f64) {
-                static bool a = false;
-                if (!a) { cudaFuncSetAttribute(k_xsvs_warp2<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsvs2_smem<double>()); a = true; }
-                k_xsvs_warp2<double><<<blocks, 32 * XWARPS, xsvs2_smem<double>(), s>>>((const double*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, ws, (double2*)warp_moments);
+                cudaFuncSetAttribute(k_xsvs_warp2<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+                k_xsvs_warp2<double><<<blocks, 32 * XWARPS, sm, s>>>((const double*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, ws, (double2*)warp_moments);
             } else {
-                static bool a = false;
-                if (!a) { cudaFuncSetAttribute(k_xsvs_warp2<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsvs2_smem<float>()); a = true; }
-                k_xsvs_warp2<float><<<blocks, 32 * XWARPS, xsvs2_smem<float>(), s>>>((const float*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, ws, (double2*)warp_moments);
+                cudaFuncSetAttribute(k_xsvs_warp2<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+                k_xsvs_warp2<float><<<blocks, 32 * XWARPS, sm, s>>>((const float*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, ws, (double2*)warp_moments);
             }
         }
 #endif
-        if (mom_out)
-            k_xsvs_final_moments<<<dim3(ws.n, n_bins), 256, 0, s>>>((const double2*)warp_moments, plan.offsets,
-                                                                    plan.warp_off, ws, slot_first, n_bins, mom_out);
-        else
-            k_xsvs_final<<<dim3(ws.n, n_bins), 256, 0, s>>>((const double2*)warp_moments, plan.offsets, plan.warp_off,
-                                                            ws, (int)w0, n_bins, beta_out);
+        int max_s = 0;
+        for (int i = 0; i < ws.n; ++i) max_s = std::max(max_s, ws.S[i]);
+        if (max_s > 0)
+            k_xsvs_final_moments<<<dim3(ws.n, n_bins, (max_s + 7) / 8), 256, 0, s>>>(
+                (const double2*)warp_moments, plan.offsets, plan.warp_off, ws, slot_first, n_bins, max_warps, mom_out);
         slot_first += ws.total_slots;
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
@@ -773,12 +779,12 @@ cudaError_t launch_xsvs(const void* I, int in_f64, int64_t T, int64_t n_q, BinPl
 // =====================================================================================================
 __global__ void __launch_bounds__(256)
 k_ring_snapshot_mean(const double2* __restrict__ mom, const int32_t* __restrict__ off, const int32_t* __restrict__ woff,
-                     int S, int total_slots, int32_t n_bins, double* __restrict__ mean) {
+                     int S, int64_t total_warps, int32_t n_bins, double* __restrict__ mean) {
     const int b = blockIdx.x;
     const int m0 = off[b + 1] - off[b];
     for (int s = threadIdx.x; s < S; s += 256) {
         double m1 = 0.0;
-        for (int g = woff[b]; g < woff[b + 1]; ++g) m1 += mom[(int64_t)g * total_slots + s].x;
+        for (int g = woff[b]; g < woff[b + 1]; ++g) m1 += mom[(int64_t)s * total_warps + g].x;   // slot-major
         mean[(int64_t)s * n_bins + b] = m0 > 0 ? m1 / m0 : 0.0;
     }
 }
@@ -834,7 +840,7 @@ cudaError_t launch_speckle_hist(const void* I, int in_f64, int64_t T, int64_t n_
     note_launch(3);
     if (in_f64) k_xsvs_warp<double><<<blocks, 128, 0, s>>>((const double*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, ws, (double2*)warp_moments);
     else k_xsvs_warp<float><<<blocks, 128, 0, s>>>((const float*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, ws, (double2*)warp_moments);
-    k_ring_snapshot_mean<<<n_bins, 256, 0, s>>>((const double2*)warp_moments, plan.offsets, plan.warp_off, S, S, n_bins, means);
+    k_ring_snapshot_mean<<<n_bins, 256, 0, s>>>((const double2*)warp_moments, plan.offsets, plan.warp_off, S, max_warps, n_bins, means);
     if (in_f64) k_speckle_hist<double><<<blocks, 128, 0, s>>>((const double*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, M, S, means, n_hist, kappa_max, (unsigned long long*)counts);
     else k_speckle_hist<float><<<blocks, 128, 0, s>>>((const float*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, M, S, means, n_hist, kappa_max, (unsigned long long*)counts);
     return cudaGetLastError();
