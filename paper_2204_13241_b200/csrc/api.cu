@@ -148,7 +148,8 @@ int build_plan(const int32_t* bins, int64_t n_q, int32_t n_bins, cudaStream_t s,
     pb.plan.perm = (int32_t*)base;
     pb.plan.offsets = (int32_t*)(base + perm_b);
     pb.plan.warp_off = (int32_t*)(base + perm_b + off_b);
-    pb.plan.bcounts = (int32_t*)(base + perm_b + 2 * off_b);
+    pb.plan.sw_off = (int32_t*)(base + perm_b + 2 * off_b);
+    pb.plan.bcounts = (int32_t*)(base + perm_b + 3 * off_b);
     pb.max_warps = (n_q + 31) / 32 + n_bins;
     return cuda_fail(launch_binplan(bins, n_q, n_bins, pb.plan, s), "ring plan");
 }
@@ -157,7 +158,7 @@ size_t plan_bytes(int64_t n_q, int32_t n_bins) {
     const size_t perm_b = ((sizeof(int32_t) * (size_t)n_q + 255) / 256) * 256;
     const size_t off_b = ((sizeof(int32_t) * (size_t)(n_bins + 1) + 255) / 256) * 256;
     const size_t cnt_b = sizeof(int32_t) * (size_t)((n_q + 1023) / 1024) * (size_t)n_bins;
-    return perm_b + 2 * off_b + cnt_b + 256;
+    return perm_b + 3 * off_b + cnt_b + 256;
 }
 
 int make_plan(const int32_t* bins, int64_t n_q, int32_t n_bins, cudaStream_t s, PlanBufs& pb) {

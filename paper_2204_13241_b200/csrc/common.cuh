@@ -240,10 +240,15 @@ cudaError_t launch_isf(const void* A, int in_f64, int64_t T, int64_t n_q, const 
 // statistics
 cudaError_t launch_g2(const void* I, int in_f64, int64_t T, int64_t n_q, const int32_t* lags_dev,
                       int64_t n_lags, int max_lag, void* out, int out_f64, cudaStream_t s);
+#ifndef XPCS_XSVS_PX
+#define XPCS_XSVS_PX 4
+#endif
+constexpr int XSVS_PX = XPCS_XSVS_PX;   // pixels per lane of the XSVS kernel (when the grid still fills the GPU)
 struct BinPlan {
     int32_t* perm;        // [n_valid] pixel indices sorted by (bin, pixel)
     int32_t* offsets;     // [n_bins + 1]
     int32_t* warp_off;    // [n_bins + 1] prefix of ceil(count_b / 32)
+    int32_t* sw_off;      // [n_bins + 1] prefix of ceil(count_b / (32 XSVS_PX)): the XSVS kernel's warps (XSVS_PX pixels per lane)
     int32_t* bcounts;     // [ceil(n_q / 1024)][n_bins] scratch of the plan build
 };
 cudaError_t launch_binplan(const int32_t* bins, int64_t n_q, int32_t n_bins, BinPlan plan, cudaStream_t s);

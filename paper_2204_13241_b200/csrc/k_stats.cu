@@ -220,7 +220,8 @@ __global__ void __launch_bounds__(256) k_bin_count(const int32_t* __restrict__ b
 }
 
 __global__ void __launch_bounds__(256) k_bin_scan(int32_t* __restrict__ bcounts, int nblk, int32_t n_bins,
-                                                  int32_t* __restrict__ offsets, int32_t* __restrict__ warp_off) {
+                                                  int32_t* __restrict__ offsets, int32_t* __restrict__ warp_off,
+                                                  int32_t* __restrict__ sw_off) {
     // one thread per ring: in-place exclusive scan of its counts over blocks -> per-block start (relative)
     __shared__ int tot[1024];
     for (int b0 = 0; b0 < n_bins; b0 += 1024) {
@@ -235,15 +236,18 @@ __global__ void __launch_bounds__(256) k_bin_scan(int32_t* __restrict__ bcounts,
         }
         __syncthreads();
         if (threadIdx.x == 0) {
-            int o = b0 == 0 ? 0 : offsets[b0], w = b0 == 0 ? 0 : warp_off[b0];
+            int o = b0 == 0 ? 0 : offsets[b0], w = b0 == 0 ? 0 : warp_off[b0], x = b0 == 0 ? 0 : sw_off[b0];
             for (int b = b0; b < min(n_bins, b0 + 1024); ++b) {
                 offsets[b] = o;
                 warp_off[b] = w;
+                sw_off[b] = x;
                 o += tot[b - b0];
                 w += (tot[b - b0] + 31) / 32;
+                x += (tot[b - b0] + 32 * XSVS_PX - 1) / (32 * XSVS_PX);
             }
             offsets[min(n_bins, b0 + 1024)] = o;
             warp_off[min(n_bins, b0 + 1024)] = w;
+            sw_off[min(n_bins, b0 + 1024)] = x;
         }
         __syncthreads();
     }
@@ -279,7 +283,7 @@ cudaError_t launch_binplan(const int32_t* bins, int64_t n_q, int32_t n_bins, Bin
     const size_t sh = sizeof(int) * (size_t)n_bins;
     note_launch(3);
     k_bin_count<<<nblk, 256, sh, s>>>(bins, n_q, n_bins, plan.bcounts);
-    k_bin_scan<<<1, 256, 0, s>>>(plan.bcounts, nblk, n_bins, plan.offsets, plan.warp_off);
+    k_bin_scan<<<1, 256, 0, s>>>(plan.bcounts, nblk, n_bins, plan.offsets, plan.warp_off, plan.sw_off);
     k_bin_fill<<<nblk, 256, sh, s>>>(bins, n_q, n_bins, plan.bcounts, plan.offsets, plan.perm);
     return cudaGetLastError();
 }
@@ -497,31 +501,64 @@ k_xsvs_warp(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __r
 #ifndef XPCS_XSVS_XB
 #define XPCS_XSVS_XB 16
 #endif
-#ifndef XPCS_XSVS_FC
-#define XPCS_XSVS_FC 32
+#ifndef XPCS_XSVS_WIDE_MIN
+#define XPCS_XSVS_WIDE_MIN 2   // warps per SM the wide grid must reach
+#endif
+#ifndef XPCS_XSVS_STAGES
+#define XPCS_XSVS_STAGES 2   // staged chunks per warp (cp.async ring depth)
 #endif
 #ifndef XPCS_XSVS_WARPS
 #define XPCS_XSVS_WARPS 4
 #endif
-namespace { constexpr int XB = XPCS_XSVS_XB, XWARPS = XPCS_XSVS_WARPS, XFC = XPCS_XSVS_FC; }
-static_assert(XFC % 4 == 0, "the close-mask loop reads four frames per word");
+#ifndef XPCS_XSVS_UNROLL
+#define XPCS_XSVS_UNROLL 8   // 4-frame groups of a chunk unrolled
+#endif
+#ifndef XPCS_XSVS_FRAMES
+#define XPCS_XSVS_FRAMES 16   // pixel-frames staged per lane per chunk
+#endif
+namespace { constexpr int XB = XPCS_XSVS_XB, XWARPS = XPCS_XSVS_WARPS, XFRAMES = XPCS_XSVS_FRAMES, XST = XPCS_XSVS_STAGES, XUN = XPCS_XSVS_UNROLL; }
+// frames per staged chunk: 32 pixel-frames in flight per lane for XP pixels per lane
+template <int XP> __host__ __device__ constexpr int xsvs_fc() { return XFRAMES / XP; }
+static_assert(XB == 8 || XB == 16 || XB == 32, "the fold gives each buffered close 32 / XB lanes");
 // per-frame close masks (bit k: window k of the pass closes after frame t) are built once per block in shared
 // memory, so a frame costs one byte test instead of a scan over the windows; the window state stays in registers
 constexpr int XMASK_MAX = 16384;   // frames a pass can cover with the shared-memory mask (longer series: k_xsvs_warp)
-template <typename In>
+template <typename In, int XP>
 __host__ __device__ constexpr size_t xsvs2_warp_smem() {
-    return (size_t)XB * 33 * sizeof(double2) + (size_t)XB * sizeof(int) + 2 * XFC * 32 * sizeof(In);
+    return (size_t)XB * 33 * sizeof(double2) + (size_t)XB * sizeof(int) + XST * XFRAMES * 32 * sizeof(In);
 }
-__host__ __device__ constexpr size_t xsvs2_mask_bytes(int64_t tuse) { return (size_t)((tuse + 15) / 16) * 16; }
-template <typename In>
+// one byte per frame, rounded up to whole chunks (the loop reads the mask of every frame of its last chunk) and 16 B
+__host__ __device__ constexpr size_t xsvs2_mask_bytes(int64_t tuse) {
+    return (size_t)((tuse + 16 * XFRAMES - 1) / (16 * XFRAMES)) * (16 * XFRAMES);
+}
+template <typename In, int XP>
 __host__ __device__ constexpr size_t xsvs2_smem(int64_t tuse) {
-    return xsvs2_mask_bytes(tuse) + (size_t)XWARPS * xsvs2_warp_smem<In>();
+    return xsvs2_mask_bytes(tuse) + (size_t)XWARPS * xsvs2_warp_smem<In, XP>();
 }
-template <typename In>
-__global__ void __launch_bounds__(32 * XWARPS)
+// One warp per 32 XP consecutive ring-ordered pixels of one ring (plan.sw_off), XP per lane (pixel j of lane l is
+// entry 32 j + l), all windows of the pass.  Each lane keeps a running prefix sum P per pixel; window k's sum at
+// its close is P - (P at its previous close).  At a close the lane adds its XP pixels' (I_W, I_W^2) in pixel order
+// and writes one pair into a padded [slot][lane] shared buffer; every XB closes the warp folds the buffer (one lane
+// per slot, lane order) into mom[slot][warp].  The series is gathered by cp.async into a double-buffered
+// [XFC frames][XP][32] warp-private ring.
+#ifndef XPCS_XSVS_CARVE
+#define XPCS_XSVS_CARVE 0
+#endif
+#ifndef XPCS_XSVS_MINB
+#define XPCS_XSVS_MINB 0     // > 0: minimum resident blocks per SM for the register allocator (experiments)
+#endif
+#if XPCS_XSVS_MINB > 0
+#define XSVS2_BOUNDS __launch_bounds__(32 * XWARPS, XPCS_XSVS_MINB)
+#else
+#define XSVS2_BOUNDS __launch_bounds__(32 * XWARPS)
+#endif
+template <typename In, int XP>
+__global__ void XSVS2_BOUNDS
 k_xsvs_warp2(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __restrict__ perm,
-             const int32_t* __restrict__ off, const int32_t* __restrict__ woff, int32_t n_bins, int64_t total_warps,
+             const int32_t* __restrict__ off, const int32_t* __restrict__ swoff, int32_t n_bins, int64_t total_warps,
              WinSet ws, double2* __restrict__ mom) {
+    constexpr int XFC = xsvs_fc<XP>();
+    static_assert(XFC % 4 == 0, "the close-mask loop reads four frames per word");
     extern __shared__ __align__(16) unsigned char xs_smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int nw = ws.n;
@@ -530,95 +567,137 @@ k_xsvs_warp2(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __
     for (int k = 0; k < XW; ++k)
         if (k < nw) Tuse = max(Tuse, (int64_t)ws.S[k] * ws.W[k]);
     uint32_t* cmask = reinterpret_cast<uint32_t*>(xs_smem);      // byte t: windows closing after frame t
-    unsigned char* base = xs_smem + xsvs2_mask_bytes(Tuse) + (size_t)wib * xsvs2_warp_smem<In>();
+    unsigned char* base = xs_smem + xsvs2_mask_bytes(Tuse) + (size_t)wib * xsvs2_warp_smem<In, XP>();
     double2 (*B)[33] = reinterpret_cast<double2 (*)[33]>(base);
-    In* ser = reinterpret_cast<In*>(base + XB * 33 * sizeof(double2));          // [2][XFC][32]
-    int* ids = reinterpret_cast<int*>(base + XB * 33 * sizeof(double2) + 2 * XFC * 32 * sizeof(In));
-    // close masks: thread k.. marks frames s W_k - 1 (windows aligned at t = 0, remainder dropped)
-    for (int i = threadIdx.x; i < (int)((Tuse + 3) / 4); i += blockDim.x) cmask[i] = 0u;
+    In* ser = reinterpret_cast<In*>(base + XB * 33 * sizeof(double2));          // [XST][XFC][XP][32]
+    int* ids = reinterpret_cast<int*>(base + XB * 33 * sizeof(double2) + XST * XFC * XP * 32 * sizeof(In));
+    // close masks: frame s W_k - 1 closes window k's snapshot s (windows aligned at t = 0, remainder dropped)
+    for (int i = threadIdx.x; i < (int)(xsvs2_mask_bytes(Tuse) / 4); i += blockDim.x) cmask[i] = 0u;
     __syncthreads();
-    for (int k = 0; k < nw; ++k)
-        for (int sI = threadIdx.x; sI < ws.S[k]; sI += blockDim.x) {
-            const int t = (sI + 1) * ws.W[k] - 1;
-            atomicOr(&cmask[t >> 2], (1u << k) << (8 * (t & 3)));
-        }
+#pragma unroll
+    for (int k = 0; k < XW; ++k)   // static k: ws stays in the parameter bank (no local copy)
+        if (k < nw)
+            for (int sI = threadIdx.x; sI < ws.S[k]; sI += blockDim.x) {
+                const int t = (sI + 1) * ws.W[k] - 1;
+                atomicOr(&cmask[t >> 2], (1u << k) << (8 * (t & 3)));
+            }
     __syncthreads();
     const int64_t gw = (int64_t)blockIdx.x * XWARPS + wib;
-    if (gw >= total_warps || gw >= woff[n_bins]) return;
+    if (gw >= total_warps || gw >= swoff[n_bins]) return;
     int lo = 0, hi = n_bins;
     while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
-        if (woff[mid] <= gw) lo = mid; else hi = mid;
+        if (swoff[mid] <= gw) lo = mid; else hi = mid;
     }
     const int b = lo;
-    const int64_t idx = off[b] + (gw - woff[b]) * 32 + lane;
-    const bool valid = idx < off[b + 1];
-    const int64_t px = valid ? perm[idx] : 0;
-    // running prefix sum P of the series; window k's sum at a close is P - (P at its previous close)
-    double P = 0.0, lastP[XW];
+    const int64_t idx0 = off[b] + (gw - swoff[b]) * (32 * XP) + lane;
+    const In* src0[XP];
+    uint32_t src_bytes[XP];
+#pragma unroll
+    for (int j = 0; j < XP; ++j) {
+        const bool valid = idx0 + 32 * j < off[b + 1];
+        src0[j] = I + (valid ? perm[idx0 + 32 * j] : 0);
+        src_bytes[j] = valid ? (uint32_t)sizeof(In) : 0u;
+    }
+    double P[XP], lastP[XW][XP];
     int sidx[XW];
 #pragma unroll
-    for (int k = 0; k < XW; ++k) { lastP[k] = 0.0; sidx[k] = 0; }
+    for (int j = 0; j < XP; ++j) P[j] = 0.0;
+#pragma unroll
+    for (int k = 0; k < XW; ++k) {
+        sidx[k] = 0;
+#pragma unroll
+        for (int j = 0; j < XP; ++j) lastP[k][j] = 0.0;
+    }
     const int n_chunks = (int)((Tuse + XFC - 1) / XFC);
-    const In* src0 = I + px;                                  // this lane's pixel column, frame 0
-    const uint32_t src_bytes = valid ? (uint32_t)sizeof(In) : 0u;
     auto prefetch = [&](int c) {
         if (c < n_chunks) {
-            const uint32_t dst0 = (uint32_t)__cvta_generic_to_shared(ser + (size_t)(c & 1) * XFC * 32 + lane);
+            const uint32_t dst0 = (uint32_t)__cvta_generic_to_shared(ser + (size_t)(c % XST) * XFC * XP * 32 + lane);
             const int64_t t0 = (int64_t)c * XFC;
-            const In* src = src0 + t0 * n_q;
             const int un = (int)min((int64_t)XFC, Tuse - t0);
-#pragma unroll 8
-            for (int u = 0; u < XFC; ++u) {
-                asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(dst0 + (uint32_t)(u * 32 * sizeof(In))),
-                             "l"(u < un ? src : src0), "n"(sizeof(In)), "r"(u < un ? src_bytes : 0u)
-                             : "memory");
-                src += n_q;
+            if (un == XFC) {                      // whole chunk
+#pragma unroll
+                for (int j = 0; j < XP; ++j) {
+                    const In* src = src0[j] + t0 * n_q;
+#pragma unroll
+                    for (int u = 0; u < XFC; ++u) {
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;"
+                                     ::"r"(dst0 + (uint32_t)((u * XP + j) * 32 * sizeof(In))), "l"(src),
+                                     "n"(sizeof(In)), "r"(src_bytes[j])
+                                     : "memory");
+                        src += n_q;
+                    }
+                }
+            } else {                              // the last chunk: frames past Tuse zero-filled
+#pragma unroll
+                for (int j = 0; j < XP; ++j) {
+                    const In* src = src0[j] + t0 * n_q;
+                    for (int u = 0; u < XFC; ++u) {
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;"
+                                     ::"r"(dst0 + (uint32_t)((u * XP + j) * 32 * sizeof(In))),
+                                     "l"(u < un ? src : src0[j]), "n"(sizeof(In)), "r"(u < un ? src_bytes[j] : 0u)
+                                     : "memory");
+                        src += n_q;
+                    }
+                }
             }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     int nb = 0;                                   // buffered closes (warp-uniform)
-    auto flush = [&]() {
+    auto flush = [&]() {   // LPS lanes per buffered close, 32 / LPS lanes' pairs each, then a fixed-order tree
+        constexpr int LPS = 32 / XB;
         __syncwarp();
-        if (lane < nb) {
-            double m1 = 0.0, m2 = 0.0;
-#pragma unroll 8
-            for (int i = 0; i < 32; ++i) {
-                const double2 v = B[lane][i];
+        const int slot = lane / LPS, part = lane % LPS;
+        double m1 = 0.0, m2 = 0.0;
+        if (slot < nb) {
+#pragma unroll
+            for (int i = 0; i < 32 / LPS; ++i) {
+                const double2 v = B[slot][part * (32 / LPS) + i];
                 m1 += v.x;
                 m2 += v.y;
             }
-            mom[(int64_t)ids[lane] * total_warps + gw] = make_double2(m1, m2);   // slot-major: a ring's warps contiguous
         }
+#pragma unroll
+        for (int o = 1; o < LPS; o <<= 1) {
+            m1 += __shfl_xor_sync(0xffffffffu, m1, o);
+            m2 += __shfl_xor_sync(0xffffffffu, m2, o);
+        }
+        if (part == 0 && slot < nb)
+            mom[(int64_t)ids[slot] * total_warps + gw] = make_double2(m1, m2);   // slot-major: a ring's warps contiguous
         __syncwarp();
         nb = 0;
     };
-    prefetch(0);
-    for (int c = 0; c < n_chunks; ++c) {
-        prefetch(c + 1);
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
-        __syncwarp();
-        const In* sc = ser + (size_t)(c & 1) * XFC * 32 + lane;
-        const int t0 = c * XFC;
-        const int un = (int)min((int64_t)XFC, Tuse - (int64_t)t0);
-        for (int u0 = 0; u0 < un; u0 += 4) {          // 4 frames per step: their loads and masks in flight at once
-            double v[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) v[i] = u0 + i < un ? (double)sc[(u0 + i) * 32] : 0.0;
-            const uint32_t m4 = cmask[(t0 + u0) >> 2];     // t0 and u0 are multiples of 4: one word, warp-uniform
+    for (int c = 0; c < XST - 1; ++c) prefetch(c);
+    for (int c = 0; c < n_chunks; ++c) {
+        prefetch(c + XST - 1);
+        asm volatile("cp.async.wait_group %0;" ::"n"(XST - 1) : "memory");
+        __syncwarp();
+        const In* sc = ser + (size_t)(c % XST) * XFC * XP * 32 + lane;
+        const int t0 = c * XFC;
+#pragma unroll (XUN)
+        for (int u0 = 0; u0 < XFC; u0 += 4) {          // frames past Tuse are zero-filled and close nothing
+            const uint32_t m4 = cmask[(t0 + u0) >> 2];     // one word per 4 frames, warp-uniform
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                P += v[i];
-                uint32_t m = (m4 >> (8 * i)) & 0xFFu;       // frames past un have no close bits
+#pragma unroll
+                for (int j = 0; j < XP; ++j) P[j] += (double)sc[((u0 + i) * XP + j) * 32];
+                uint32_t m = (m4 >> (8 * i)) & 0xFFu;
                 if (m == 0u) continue;
 #pragma unroll
                 for (int k = 0; k < XW; ++k) {
                     if (m == 0u) break;                   // stop after the last closing window
                     if (m & 1u) {
-                        const double val = P - lastP[k];
-                        lastP[k] = P;
-                        B[nb][lane] = make_double2(val, val * val);
+                        double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+                        for (int j = 0; j < XP; ++j) {
+                            const double val = P[j] - lastP[k][j];
+                            lastP[k][j] = P[j];
+                            s1 += val;
+                            s2 = fma(val, val, s2);
+                        }
+                        B[nb][lane] = make_double2(s1, s2);
                         if (lane == 0) ids[nb] = ws.base[k] + sidx[k];
                         ++sidx[k];
                         if (++nb == XB) flush();
@@ -627,7 +706,7 @@ k_xsvs_warp2(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __
                 }
             }
         }
-        __syncwarp();                             // chunk c's buffer is refilled by prefetch(c + 2)
+        __syncwarp();                             // chunk c's buffer is refilled by prefetch(c + XST)
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     if (nb > 0) flush();
@@ -730,39 +809,45 @@ cudaError_t launch_xsvs(const void* I, int in_f64, int64_t T, int64_t n_q, BinPl
         }
         ws.total_slots = slots;
         note_launch(2);
-#if XPCS_XSVS_V1
-        const unsigned blocks = (unsigned)((max_warps + 3) / 4);
-        if (blocks > 0) {
-            const dim3 gr(blocks, (unsigned)((ws.n + XWPW - 1) / XWPW));
-            if (in_f64) k_xsvs_warp<double><<<gr, 128, 0, s>>>((const double*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, ws, (double2*)warp_moments);
-            else k_xsvs_warp<float><<<gr, 128, 0, s>>>((const float*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, ws, (double2*)warp_moments);
-        }
-#else
-        const unsigned blocks = (unsigned)((max_warps + XWARPS - 1) / XWARPS);
         int64_t tuse = 0;
         for (int i = 0; i < ws.n; ++i) tuse = std::max<int64_t>(tuse, (int64_t)ws.S[i] * ws.W[i]);
+        const int32_t* woff = plan.warp_off;
         if (tuse > XMASK_MAX) {   // very long series: one warp per window (no shared-memory close mask)
             const dim3 gr((unsigned)((max_warps + 3) / 4), (unsigned)((ws.n + XWPW - 1) / XWPW));
-            if (blocks > 0) {
+            if (max_warps > 0) {
                 if (in_f64) k_xsvs_warp<double><<<gr, 128, 0, s>>>((const double*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, ws, (double2*)warp_moments);
                 else k_xsvs_warp<float><<<gr, 128, 0, s>>>((const float*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, ws, (double2*)warp_moments);
             }
-        } else if (blocks > 0) {
-            const size_t sm = in_f64 ? xsvs2_smem<double>(tuse) : xsvs2_smem<float>(tuse);
-            if (in_f64) {
-                cudaFuncSetAttribute(k_xsvs_warp2<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-                k_xsvs_warp2<double><<<blocks, 32 * XWARPS, sm, s>>>((const double*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, ws, (double2*)warp_moments);
-            } else {
-                cudaFuncSetAttribute(k_xsvs_warp2<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-                k_xsvs_warp2<float><<<blocks, 32 * XWARPS, sm, s>>>((const float*)I, T, n_q, plan.perm, plan.offsets, plan.warp_off, n_bins, max_warps, ws, (double2*)warp_moments);
+        } else {
+            // XSVS_PX pixels per lane when that still fills the GPU, else one (plan.warp_off)
+            const int64_t max_sw = std::min<int64_t>(max_warps, (n_q + 32 * XSVS_PX - 1) / (32 * XSVS_PX) + n_bins);
+            const bool wide = XSVS_PX > 1 && max_sw >= (int64_t)sm_count() * XPCS_XSVS_WIDE_MIN;
+            const int64_t n_w = wide ? max_sw : max_warps;
+            const unsigned blocks = (unsigned)((n_w + XWARPS - 1) / XWARPS);
+            woff = wide ? plan.sw_off : plan.warp_off;
+            auto go = [&](auto kern, size_t sm, const auto* src) {
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+#if XPCS_XSVS_CARVE
+                cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+#endif
+                kern<<<blocks, 32 * XWARPS, sm, s>>>(src, T, n_q, plan.perm, plan.offsets, woff, n_bins, max_warps, ws,
+                                                     (double2*)warp_moments);
+            };
+            if (blocks > 0) {
+                if (in_f64) {
+                    if (wide) go(k_xsvs_warp2<double, XSVS_PX>, xsvs2_smem<double, XSVS_PX>(tuse), (const double*)I);
+                    else go(k_xsvs_warp2<double, 1>, xsvs2_smem<double, 1>(tuse), (const double*)I);
+                } else {
+                    if (wide) go(k_xsvs_warp2<float, XSVS_PX>, xsvs2_smem<float, XSVS_PX>(tuse), (const float*)I);
+                    else go(k_xsvs_warp2<float, 1>, xsvs2_smem<float, 1>(tuse), (const float*)I);
+                }
             }
         }
-#endif
         int max_s = 0;
         for (int i = 0; i < ws.n; ++i) max_s = std::max(max_s, ws.S[i]);
         if (max_s > 0)
             k_xsvs_final_moments<<<dim3(ws.n, n_bins, (max_s + 7) / 8), 256, 0, s>>>(
-                (const double2*)warp_moments, plan.offsets, plan.warp_off, ws, slot_first, n_bins, max_warps, mom_out);
+                (const double2*)warp_moments, plan.offsets, woff, ws, slot_first, n_bins, max_warps, mom_out);
         slot_first += ws.total_slots;
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
