@@ -219,6 +219,24 @@ def test_xsvs_reduction_parity(T, windows):
     assert_rel(beta, oracle.xsvs_beta(I, bins, 17, windows), 1e-10, "xsvs")
 
 
+@pytest.mark.parametrize("case", ["wide", "wide_f64", "long"])
+def test_xsvs_kernel_paths(case):
+    """The three XSVS gather paths (k_stats.cu launch_xsvs): four pixels per lane when the detector fills the GPU
+    (65536 pixels), one per lane below that (the test above), and the one-warp-per-window kernel for series longer
+    than the shared-memory close mask (17000 frames)."""
+    rng = np.random.default_rng(11)
+    if case == "long":
+        T, n, windows = 17000, 32, [1, 7, 1000, 16999]
+    else:
+        T, n, windows = 130, 256, [1, 2, 3, 4, 8, 16, 64, 129]
+    I = rng.exponential(2.0, (T, n * n)).astype(np.float64 if case == "wide_f64" else np.float32)
+    nb = n // 16 if case == "long" else 16          # ring width n / (2 nb) pixels
+    bins = oracle.lattice_bins(n, n_bins=nb)
+    bins[:37] = nb - 1  # a scattered ring with a ragged pixel count
+    beta = xp.xsvs_contrast(_t(I), _t(bins), nb + 1, windows).cpu().numpy()    # ring nb empty
+    assert_rel(beta, oracle.xsvs_beta(I, bins, nb + 1, windows), 1e-10, f"xsvs {case}")
+
+
 # ----------------------------------------------------------------------------------- config-size cases
 def test_config2_simt_engine_sampled():
     """The SIMT engine on config 2's size (first 10 frames) against the oracle."""
