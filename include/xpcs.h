@@ -217,6 +217,28 @@ XPCS_API int xpcs_isf(const void* A_series, int64_t frames, int64_t n_q, const i
 XPCS_API int xpcs_g2(const void* I_series, int64_t frames, int64_t n_q, const int32_t* lags, int64_t n_lags,
             void* g2_out, const xpcs_opts* opts);
 
+/* Block-streamed g2 (SURVEY 8(d) K4 "update in blocks of B frames"; Eq.(14)): for series longer
+ * than device memory (PAPER.md:476 uses 5000 frames) the frames arrive in blocks and only the FP64 state and the
+ * last max-lag frames stay resident.  Same estimator and FP64 arithmetic as xpcs_g2: after streaming frames
+ * 0 .. T-1 in any block sizes, xpcs_g2_finalize gives xpcs_g2 of the whole series (up to summation order).
+ * xpcs_g2_accumulate, for the block I_block [block_frames][n_q] in_dtype holding global frames t0 .. t0+B-1:
+ *     acc[l][px] += sum of I_t I_{t+tau_l} over the pairs whose LATER frame t + tau_l is in the block and t >= 0,
+ *     sum[px]    += sum of the block's frames,
+ *   the earlier frames before the block coming from `ring` DEVICE [ring_frames][n_q] in_dtype (frame g in slot
+ *   g mod ring_frames, ring_frames >= max lag; the library writes the block's last min(B, ring_frames) frames into it
+ *   after reading it: the caller allocates it and never writes it).  acc DEVICE [n_lags][n_q] and sum DEVICE [n_q]
+ *   double are zeroed by the caller before the first block (t0 = 0).  Blocks must arrive in order (t0 = frames
+ *   already streamed), all with the same lags and ring, on one stream (or ordered streams).
+ * xpcs_g2_finalize: g2_out [n_lags][n_q] out_dtype = (acc / (T - tau)) / (sum / T)^2 for the total frame count T
+ *   (NaN where the mean intensity is 0).
+ * Errors: EINVAL for null pointers, sizes <= 0, t0 < 0, a negative lag, ring_frames < max lag (or a NULL ring with
+ * ring_frames > 0), a lag >= frames in finalize; EUNSUPPORTED for lags > 640. */
+XPCS_API int xpcs_g2_accumulate(const void* I_block, int64_t block_frames, int64_t t0, int64_t n_q,
+                                const int32_t* lags, int64_t n_lags, void* ring, int64_t ring_frames, double* acc,
+                                double* sum, const xpcs_opts* opts);
+XPCS_API int xpcs_g2_finalize(const double* acc, const double* sum, int64_t frames, int64_t n_q, const int32_t* lags,
+                              int64_t n_lags, void* g2_out, const xpcs_opts* opts);
+
 /* ------------------------------------------------------------------------------------------------
  * XSVS optical contrast versus exposure.  Eq.(15), as a discrete unnormalised sum over
  * non-overlapping windows of W frames aligned at t = 0 (remainder dropped):

@@ -11,4 +11,5 @@ from ._lib import (  # noqa: F401
     xpcs_amplitude, xpcs_amplitude_grid, xpcs_g2, xpcs_intensity, xpcs_intensity_grid, xpcs_isf, xpcs_lattice_bins, xpcs_qgrid_ewald, xpcs_radial_bins,
     xpcs_shell_mean, xpcs_structure_factor_shells, xsvs_contrast, xpcs_step_host, xpcs_ring_moments,
     xpcs_ring_means_from_moments, xsvs_moments, xsvs_contrast_from_moments, xsvs_n_slots, new_workspace, workspace,
+    xpcs_g2_accumulate, xpcs_g2_finalize, G2Stream,
 )

@@ -32,7 +32,7 @@ EXPORTED = (
     "xpcs_intensity_volume", "xpcs_amplitude_volume", "xpcs_intensity_species", "xpcs_amplitude_species",
     "xpcs_form_factor_gaussian", "xpcs_speckle_histogram", "xpcs_intensity_fft", "xpcs_rings_register",
     "xpcs_rings_unregister", "xpcs_step_host", "xpcs_ring_moments", "xpcs_ring_means_from_moments", "xsvs_moments",
-    "xsvs_contrast_from_moments",
+    "xsvs_contrast_from_moments", "xpcs_g2_accumulate", "xpcs_g2_finalize",
 )
 
 
@@ -102,6 +102,8 @@ def load():
         "xpcs_intensity": [vp, i64, vp, vp, i64, i64, dbl, vp, op],
         "xpcs_intensity_grid": [vp, i64, vp, gp, i64, vp, op],
         "xpcs_g2": [vp, i64, i64, ip32, i64, vp, op],
+        "xpcs_g2_accumulate": [vp, i64, i64, i64, ip32, i64, vp, i64, vp, vp, op],
+        "xpcs_g2_finalize": [vp, vp, i64, i64, ip32, i64, vp, op],
         "xsvs_contrast": [vp, i64, i64, vp, i32, ip32, i64, vp, op],
         "xpcs_shell_mean": [vp, i64, i64, vp, i32, dbl, vp, op],
         "xpcs_structure_factor_shells": [vp, i64, i64, vp, i64, vp, i32, vp, op],
@@ -464,6 +466,54 @@ def xpcs_g2(I, lags, out=None, out_dtype=F64, stream=None, profile=False):
     o = make_opts(_dtype_code(I), out_dtype, stream, ENGINE_AUTO, profile)
     _check(load().xpcs_g2(_ptr(I), T, n_q, lag_p, len(lag_arr), _ptr(out), ctypes.byref(o)))
     return out
+
+
+def xpcs_g2_accumulate(I_block, t0, lags, ring, acc, sum_, stream=None, profile=False):
+    """Block-streamed g2 (include/xpcs.h): add the pairs whose later frame is in I_block [B][n_q] (global frames
+    t0 .. t0+B-1) to acc [n_lags][n_q] and the block's frames to sum_ [n_q] (float64); ring [R][n_q] (R >= max lag,
+    I_block's dtype) holds the last frames and is updated by the library."""
+    B, n_q = I_block.shape
+    lag_arr, lag_p = _i32_array(lags)
+    o = make_opts(_dtype_code(I_block), F64, stream, ENGINE_AUTO, profile)
+    _check(load().xpcs_g2_accumulate(_ptr(I_block), B, int(t0), n_q, lag_p, len(lag_arr), _ptr(ring),
+                                     ring.shape[0] if ring is not None else 0, _ptr(acc), _ptr(sum_), ctypes.byref(o)))
+
+
+def xpcs_g2_finalize(acc, sum_, frames, lags, out=None, out_dtype=F64, stream=None):
+    """g2 [n_lags][n_q] of the streamed series of `frames` frames from the accumulated state."""
+    import torch
+    n_q = sum_.shape[0]
+    lag_arr, lag_p = _i32_array(lags)
+    if out is None:
+        out = torch.empty((len(lag_arr), n_q), dtype=torch.float64 if out_dtype == F64 else torch.float32,
+                          device=acc.device)
+    o = make_opts(F64, out_dtype, stream)
+    _check(load().xpcs_g2_finalize(_ptr(acc), _ptr(sum_), int(frames), n_q, lag_p, len(lag_arr), _ptr(out),
+                                   ctypes.byref(o)))
+    return out
+
+
+class G2Stream:
+    """Owns the block-streamed g2 state (acc, sum, frame ring) for one detector: push(I_block) per block of frames in
+    order, result() = xpcs_g2 of everything pushed.  Buffers only; the arithmetic is in the library."""
+
+    def __init__(self, n_q, lags, dtype=None, device="cuda", stream=None):
+        import torch
+        self.lags = tuple(int(t) for t in lags)
+        self.n_q, self.t, self.stream = int(n_q), 0, stream
+        dtype = dtype or torch.float32
+        self.acc = torch.zeros((len(self.lags), self.n_q), dtype=torch.float64, device=device)
+        self.sum = torch.zeros((self.n_q,), dtype=torch.float64, device=device)
+        R = max(self.lags) if self.lags else 0
+        self.ring = torch.empty((R, self.n_q), dtype=dtype, device=device) if R > 0 else None
+
+    def push(self, I_block):
+        xpcs_g2_accumulate(I_block, self.t, self.lags, self.ring, self.acc, self.sum, stream=self.stream)
+        self.t += I_block.shape[0]
+
+    def result(self, out=None, out_dtype=F64):
+        return xpcs_g2_finalize(self.acc, self.sum, self.t, self.lags, out=out, out_dtype=out_dtype,
+                                stream=self.stream)
 
 
 def xsvs_contrast(I, bins, n_bins, windows, out=None, stream=None, profile=False):

@@ -1064,6 +1064,81 @@ int xsvs_contrast(const void* I_series, int64_t frames, int64_t n_q, const int32
     return cuda_fail(launch_xsvs_beta_from_moments(ring_mom, frames, windows, n_windows, n_bins, beta_out, o.s), "xsvs beta");
 }
 
+// ------------------------------------------------------------------------------------------- block-streamed g2
+static int g2_lag_check(const int32_t* lags, int64_t n_lags, int64_t frames, int& max_lag) {
+    max_lag = 0;
+    for (int64_t i = 0; i < n_lags; ++i) {
+        if (lags[i] < 0 || (frames > 0 && lags[i] >= frames)) {
+            set_error("xpcs: lag %d out of range [0, %lld)", lags[i], (long long)frames);
+            return XPCS_EINVAL;
+        }
+        max_lag = std::max(max_lag, (int)lags[i]);
+    }
+    if (max_lag > 640) {
+        set_error("xpcs: lags > 640 frames are not supported by this build");
+        return XPCS_EUNSUPPORTED;
+    }
+    return XPCS_OK;
+}
+
+int xpcs_g2_accumulate(const void* I_block, int64_t block_frames, int64_t t0, int64_t n_q, const int32_t* lags,
+                       int64_t n_lags, void* ring, int64_t ring_frames, double* acc, double* sum,
+                       const xpcs_opts* opts) {
+    clear_error();
+    Opts o;
+    TRY(parse_opts(opts, o));
+    NEED(I_block, "I_block");
+    NEED(lags, "lags");
+    NEED(acc, "acc");
+    NEED(sum, "sum");
+    POS(block_frames, "block_frames");
+    POS(n_q, "n_q");
+    POS(n_lags, "n_lags");
+    if (t0 < 0) {
+        set_error("xpcs: t0 must be >= 0");
+        return XPCS_EINVAL;
+    }
+    int max_lag = 0;
+    for (int64_t i = 0; i < n_lags; ++i)
+        if (lags[i] < 0) {
+            set_error("xpcs: lag %d out of range (negative)", lags[i]);
+            return XPCS_EINVAL;
+        }
+    TRY(g2_lag_check(lags, n_lags, 0, max_lag));
+    if (ring_frames < max_lag || (ring_frames > 0 && !ring)) {
+        set_error("xpcs: the frame ring must hold at least the largest lag (%d frames; got %lld)", max_lag,
+                  (long long)ring_frames);
+        return XPCS_EINVAL;
+    }
+    TRY(check_sticky());
+    const int32_t* dl = lag_table(lags, n_lags, o.s);
+    if (!dl) return XPCS_ECUDA;
+    ProfScope p(o.profile, KC_G2, o.s);
+    return cuda_fail(launch_g2_accumulate(I_block, o.in_f64, block_frames, ring, ring_frames, t0, n_q, dl, n_lags,
+                                          max_lag, acc, sum, o.s), "g2 accumulate");
+}
+
+int xpcs_g2_finalize(const double* acc, const double* sum, int64_t frames, int64_t n_q, const int32_t* lags,
+                     int64_t n_lags, void* g2_out, const xpcs_opts* opts) {
+    clear_error();
+    Opts o;
+    TRY(parse_opts(opts, o));
+    NEED(acc, "acc");
+    NEED(sum, "sum");
+    NEED(lags, "lags");
+    NEED(g2_out, "g2_out");
+    POS(frames, "frames");
+    POS(n_q, "n_q");
+    POS(n_lags, "n_lags");
+    int max_lag = 0;
+    TRY(g2_lag_check(lags, n_lags, frames, max_lag));
+    TRY(check_sticky());
+    const int32_t* dl = lag_table(lags, n_lags, o.s);
+    if (!dl) return XPCS_ECUDA;
+    ProfScope p(o.profile, KC_G2, o.s);
+    return cuda_fail(launch_g2_finalize(acc, sum, frames, n_q, dl, n_lags, g2_out, o.out_f64, o.s), "g2 finalize");
+}
+
 // ------------------------------------------------------------------------------------------- ring moments
 // (the additive form of the ring reductions: a detector split across devices adds these before forming the
 // means / beta)

@@ -240,6 +240,12 @@ cudaError_t launch_isf(const void* A, int in_f64, int64_t T, int64_t n_q, const 
 // statistics
 cudaError_t launch_g2(const void* I, int in_f64, int64_t T, int64_t n_q, const int32_t* lags_dev,
                       int64_t n_lags, int max_lag, void* out, int out_f64, cudaStream_t s);
+// block-streamed g2 (k_stats.cu): acc [n_lags][n_q] / sum [n_q] FP64 state, ring [R][n_q] of the last frames
+cudaError_t launch_g2_accumulate(const void* blk, int in_f64, int64_t B, void* ring, int64_t R, int64_t t0,
+                                 int64_t n_q, const int32_t* lags_dev, int64_t n_lags, int max_lag, double* acc,
+                                 double* sum, cudaStream_t s);
+cudaError_t launch_g2_finalize(const double* acc, const double* sum, int64_t T, int64_t n_q, const int32_t* lags_dev,
+                               int64_t n_lags, void* out, int out_f64, cudaStream_t s);
 #ifndef XPCS_XSVS_PX
 #define XPCS_XSVS_PX 4
 #endif

@@ -19,7 +19,10 @@ namespace xpcs {
 // 16 LPW DFMA; other lag lists fall back to one shared load per DFMA.
 // =====================================================================================================
 namespace {
-constexpr int G2_WARPS = 8, GC = 128;
+#ifndef XPCS_G2_BATCHED_STAGE
+#define XPCS_G2_BATCHED_STAGE 0
+#endif
+constexpr int G2_WARPS = 8, GC = 128, G2_STAGE_BATCH = 8;   // rows loaded per warp before storing
 constexpr int G2_LPW = 8, G2_LAGS_PER_BLOCK = G2_LPW * G2_WARPS;   // the ISF kernel's tiling (below)
 }
 
@@ -54,10 +57,25 @@ k_g2(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __restrict
     const int rows = GC + halo + 16;
     for (int64_t t0 = 0; t0 < T; t0 += GC) {
         __syncthreads();
+#if XPCS_G2_BATCHED_STAGE
+        for (int r0 = warp; r0 < rows; r0 += G2_STAGE_BATCH * G2_WARPS) {   // G2_STAGE_BATCH loads in flight
+            In v[G2_STAGE_BATCH];
+#pragma unroll
+            for (int k = 0; k < G2_STAGE_BATCH; ++k) {
+                const int r = r0 + k * G2_WARPS;
+                const int64_t t = t0 + r;
+                v[k] = (r < rows && t < T && px < n_q) ? I[t * n_q + px] : (In)0;
+            }
+#pragma unroll
+            for (int k = 0; k < G2_STAGE_BATCH; ++k)
+                if (r0 + k * G2_WARPS < rows) S[(r0 + k * G2_WARPS) * 32 + lane] = (St)v[k];
+        }
+#else
         for (int r = warp; r < rows; r += G2_WARPS) {
             const int64_t t = t0 + r;
             S[r * 32 + lane] = (t < T && px < n_q) ? (St)I[t * n_q + px] : (St)0;
         }
+#endif
         __syncthreads();
         const int rmax = (int)min((int64_t)GC, T - t0);
         if (warp == 0)
@@ -123,6 +141,172 @@ cudaError_t launch_g2(const void* I, int in_f64, int64_t T, int64_t n_q, const i
     return cudaGetLastError();
 }
 
+
+// =====================================================================================================
+// Block-streamed g2 ("update in blocks of B frames"; Eq.(14)): a series longer
+// than device memory arrives in blocks.  For a block of B frames starting at global frame t0, with the P =
+// min(max_lag, t0) frames before it held in a device ring (frame g in slot g mod R), the pairs (t, t + tau) whose
+// LATER frame lies in the block are added to acc[l][px]; the block's frames are added to sum[px]; then the block's
+// last min(B, R) frames replace the ring's oldest.  Reversing time, D_u = C_{P+B-1-u} over C = [ring frames | block],
+// the block's pairs are sum_{u < B} D_u D_{u+tau} with D = 0 past P + B (frames before the series): the k_g2 loop
+// with the "a" rows limited to the block.  FP64 products and sums, as k_g2.
+// =====================================================================================================
+// 16 "a" rows r0 .. r0 + 15 (TAIL: only those < rlim) against the sliding window of LPW consecutive lags from t0l
+template <int LPW, bool TAIL>
+__device__ __forceinline__ void g2_rows16(const double* __restrict__ S, int lane, int r0, int rlim, int t0l,
+                                          double (&acc)[LPW]) {
+    double a[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = (!TAIL || r0 + i < rlim) ? S[(r0 + i) * 32 + lane] : 0.0;
+#pragma unroll
+    for (int j = 0; j < 16 + LPW - 1; ++j) {
+        const double w = S[(r0 + t0l + j) * 32 + lane];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            if (j - i >= 0 && j - i < LPW) acc[j - i] = fma(a[i], w, acc[j - i]);
+    }
+}
+
+template <typename In, int LPW>
+__global__ void __launch_bounds__(256)
+k_g2_accum(const In* __restrict__ blk, int64_t B, const In* __restrict__ ring, int64_t R, int64_t ring0, int64_t P,
+           int64_t n_q, const int32_t* __restrict__ lags, int64_t n_lags, int halo, int lpb, double* __restrict__ acc_out,
+           double* __restrict__ sum_out) {
+    extern __shared__ __align__(16) unsigned char g2a_smem[];
+    double* S = reinterpret_cast<double*>(g2a_smem);      // [(GC + halo + 16)][32]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t px = (int64_t)blockIdx.x * 32 + lane;
+    const int64_t lblk = (int64_t)blockIdx.y * lpb;
+    const int64_t lbase = lblk + warp * LPW;
+    const int64_t lend = min(n_lags, lblk + lpb);
+    const bool active = lbase < lend;
+    int tau[LPW];
+    bool consecutive = true;
+#pragma unroll
+    for (int l = 0; l < LPW; ++l) {
+        tau[l] = (lbase + l < lend) ? lags[lbase + l] : (active ? lags[lbase] + l : 0);
+        if (tau[l] != tau[0] + l) consecutive = false;
+    }
+    double acc[LPW];
+#pragma unroll
+    for (int l = 0; l < LPW; ++l) acc[l] = 0.0;
+    double sum = 0.0;
+    const int64_t len = P + B;                             // combined series [ring frames | block]
+    const int rows = GC + halo + 16;
+    for (int64_t u0 = 0; u0 < B; u0 += GC) {
+        __syncthreads();
+        {
+            // row u = u0 + r of the combined series (index i = len - 1 - u): block frame B - 1 - u for u < B, frame
+            // t0 - P + i in ring slot (ring0 + i) mod R for B <= u < len (0 <= i < P <= R: one conditional
+            // subtraction), zero past len.  Three simple loops (so each unrolls and keeps its loads in flight).
+            const int rb = (int)max((int64_t)0, min((int64_t)rows, B - u0));
+            const int rl = (int)max((int64_t)rb, min((int64_t)rows, len - u0));
+            const int first = [&](int lo) { return lo + ((warp - lo) % G2_WARPS + G2_WARPS) % G2_WARPS; }(0);
+            const In* src = blk + (B - 1 - u0) * n_q + px;
+            for (int r = first; r < rb; r += G2_WARPS) S[r * 32 + lane] = px < n_q ? (double)src[-(int64_t)r * n_q] : 0.0;
+            int r = rb + ((warp - rb) % G2_WARPS + G2_WARPS) % G2_WARPS;
+            for (; r < rl; r += G2_WARPS) {
+                const int64_t sl = ring0 + (len - 1 - u0 - r);
+                S[r * 32 + lane] = px < n_q ? (double)ring[(sl >= R ? sl - R : sl) * n_q + px] : 0.0;
+            }
+            for (r = rl + ((warp - rl) % G2_WARPS + G2_WARPS) % G2_WARPS; r < rows; r += G2_WARPS) S[r * 32 + lane] = 0.0;
+        }
+        __syncthreads();
+        const int rmax = (int)min((int64_t)GC, B - u0);     // "a" rows: the block's frames only
+        if (warp == 0 && blockIdx.y == 0)
+            for (int r = 0; r < rmax; ++r) sum += S[r * 32 + lane];
+        if (!active) continue;
+        if (consecutive) {
+            const int t0l = tau[0];
+            const int rlim = (int)min((int64_t)rmax, max((int64_t)0, len - u0 - t0l));   // later rows meet zeros only
+            int r0 = 0;
+            for (; r0 + 16 <= rlim; r0 += 16) g2_rows16<LPW, false>(S, lane, r0, rlim, t0l, acc);   // whole groups
+            if (r0 < rlim) g2_rows16<LPW, true>(S, lane, r0, rlim, t0l, acc);                      // the tail
+        } else {
+            for (int r = 0; r < rmax; ++r) {
+                const double a = S[r * 32 + lane];
+#pragma unroll
+                for (int l = 0; l < LPW; ++l) acc[l] = fma(a, S[(r + tau[l]) * 32 + lane], acc[l]);
+            }
+        }
+    }
+    if (px >= n_q) return;
+    if (warp == 0 && blockIdx.y == 0) sum_out[px] += sum;
+    if (!active) return;
+#pragma unroll
+    for (int l = 0; l < LPW; ++l) {
+        if (lbase + l >= lend) break;
+        acc_out[(lbase + l) * n_q + px] += acc[l];
+    }
+}
+
+// the block's last min(B, R) frames into the ring (frame g -> slot g mod R), after k_g2_accum has read the ring
+template <typename In>
+__global__ void __launch_bounds__(256)
+k_g2_ring_update(const In* __restrict__ blk, int64_t B, In* __restrict__ ring, int64_t R, int64_t t0, int64_t n_q) {
+    const int64_t keep = min(B, R), first = B - keep;
+    for (int64_t f = first + blockIdx.y; f < B; f += gridDim.y) {       // y: frames, x: pixels
+        const int64_t slot = (t0 + f) % R;
+        for (int64_t px = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; px < n_q; px += (int64_t)gridDim.x * blockDim.x)
+            ring[slot * n_q + px] = blk[f * n_q + px];
+    }
+}
+
+// g2 = (acc / (T - tau)) / (sum / T)^2 (NaN where the mean is 0), as k_g2's epilogue
+template <typename Out>
+__global__ void __launch_bounds__(256)
+k_g2_finalize(const double* __restrict__ acc, const double* __restrict__ sum, int64_t T, int64_t n_q,
+              const int32_t* __restrict__ lags, int64_t n_lags, Out* __restrict__ out) {
+    for (int64_t l = blockIdx.y; l < n_lags; l += gridDim.y) {          // y: lags, x: pixels
+        const double w = 1.0 / (double)(T - lags[l]);
+        for (int64_t px = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; px < n_q; px += (int64_t)gridDim.x * blockDim.x) {
+            const double mean = sum[px] / (double)T;
+            const double den = mean * mean;
+            const double num = acc[l * n_q + px] * w;
+            out[l * n_q + px] = (Out)(den > 0.0 ? num / den : __longlong_as_double(0x7ff8000000000000ll));
+        }
+    }
+}
+
+static dim3 grid_rows(int64_t rows, int64_t n) {     // x: 256-wide pixel blocks, y: rows (strided)
+    const int64_t bx = std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 16));
+    const int64_t by = std::max<int64_t>(1, std::min<int64_t>({rows, (int64_t)sm_count() * 64 / bx + 1, (int64_t)65535}));
+    return dim3((unsigned)bx, (unsigned)by);
+}
+
+cudaError_t launch_g2_accumulate(const void* blk, int in_f64, int64_t B, void* ring, int64_t R, int64_t t0,
+                                 int64_t n_q, const int32_t* lags_dev, int64_t n_lags, int max_lag, double* acc,
+                                 double* sum, cudaStream_t s) {
+    const int64_t P = std::min<int64_t>(max_lag, t0);
+    const int64_t ring0 = R > 0 ? (t0 - P) % R : 0;          // slot of the first ring frame used
+    const size_t smem = sizeof(double) * 32 * (GC + max_lag + 16 + 16);
+    const int lpw = n_lags >= 64 ? 16 : 8;
+    const int64_t ny = (n_lags + (int64_t)G2_WARPS * lpw - 1) / ((int64_t)G2_WARPS * lpw);
+    const int lpb = (int)(((n_lags + ny - 1) / ny + lpw - 1) / lpw * lpw);
+    const dim3 grid((unsigned)((n_q + 31) / 32), (unsigned)ny);
+    note_launch(R > 0 ? 2 : 1);
+#define G2A_CASE(IN)                                                                                             \
+    {                                                                                                            \
+        auto kern = lpw == 16 ? k_g2_accum<IN, 16> : k_g2_accum<IN, 8>;                                          \
+        if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        kern<<<grid, 256, smem, s>>>((const IN*)blk, B, (const IN*)ring, R, ring0, P, n_q, lags_dev, n_lags,     \
+                                     max_lag + 16, lpb, acc, sum);                                               \
+        if (R > 0)                                                                                               \
+            k_g2_ring_update<IN><<<grid_rows(std::min(B, R), n_q), 256, 0, s>>>((const IN*)blk, B, (IN*)ring, R, t0, n_q); \
+    }
+    if (in_f64) G2A_CASE(double) else G2A_CASE(float)
+#undef G2A_CASE
+    return cudaGetLastError();
+}
+
+cudaError_t launch_g2_finalize(const double* acc, const double* sum, int64_t T, int64_t n_q, const int32_t* lags_dev,
+                               int64_t n_lags, void* out, int out_f64, cudaStream_t s) {
+    note_launch();
+    const dim3 gr = grid_rows(n_lags, n_q);
+    if (out_f64) k_g2_finalize<double><<<gr, 256, 0, s>>>(acc, sum, T, n_q, lags_dev, n_lags, (double*)out);
+    else k_g2_finalize<float><<<gr, 256, 0, s>>>(acc, sum, T, n_q, lags_dev, n_lags, (float*)out);
+    return cudaGetLastError();
+}
 
 // =====================================================================================================
 // Intermediate scattering function, Eq.(22), PAPER.md:218-223:

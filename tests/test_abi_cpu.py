@@ -74,6 +74,20 @@ def test_validation_rejects_before_any_launch(lib):
     assert rc == _lib.XPCS_EINVAL
     rc = lib.xpcs_profile_query(99, None, None, None)
     assert rc == _lib.XPCS_EINVAL
+    # block-streamed g2: the ring must hold the largest lag; t0 >= 0; finalize checks lags against the frame count
+    rc = lib.xpcs_g2_accumulate(dummy, 4, 0, 4, lp, 3, dummy, 8, dummy, dummy, ctypes.byref(o))
+    assert rc == _lib.XPCS_EINVAL and b"ring" in lib.xpcs_last_error()
+    rc = lib.xpcs_g2_accumulate(dummy, 4, -1, 4, lp, 3, dummy, 9, dummy, dummy, ctypes.byref(o))
+    assert rc == _lib.XPCS_EINVAL and b"t0" in lib.xpcs_last_error()
+    rc = lib.xpcs_g2_accumulate(dummy, 4, 0, 4, lp, 3, None, 9, dummy, dummy, ctypes.byref(o))
+    assert rc == _lib.XPCS_EINVAL and b"ring" in lib.xpcs_last_error()
+    big, bp = _lib._i32_array([1, 700])
+    rc = lib.xpcs_g2_accumulate(dummy, 4, 0, 4, bp, 2, dummy, 700, dummy, dummy, ctypes.byref(o))
+    assert rc == _lib.XPCS_EUNSUPPORTED
+    rc = lib.xpcs_g2_finalize(dummy, dummy, 9, 4, lp, 3, dummy, ctypes.byref(o))
+    assert rc == _lib.XPCS_EINVAL and b"lag 9" in lib.xpcs_last_error()
+    rc = lib.xpcs_g2_finalize(dummy, None, 10, 4, lp, 3, dummy, ctypes.byref(o))
+    assert rc == _lib.XPCS_EINVAL and b"must not be NULL" in lib.xpcs_last_error()
     assert lib.xpcs_launch_count() == n0
 
 

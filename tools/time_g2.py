@@ -50,4 +50,21 @@ for name in sys.argv[1:] or ["c2", "c3"]:
     res[name] = {"ms": round(ms, 4), "fp64_frac": round(dfma / (ms * 1e-3) / 17.1e12, 3),
                  "checksum": float(out.double().sum()),
                  "sm_mhz": sorted(clocks)[len(clocks) // 2] if clocks else None}
+    for B in (int(b) for b in os.environ.get("XPCS_G2_STREAM", "").split(",") if b):
+        # block-streamed g2 of the same series in blocks of B frames (state reset untimed)
+        S = xp.G2Stream(n_q, cfg.lags, dtype=torch.float32)
+        reps, tot = 3, 0.0
+        for rep in range(reps + 1):
+            S.acc.zero_(); S.sum.zero_(); S.t = 0
+            torch.cuda.synchronize()
+            a.record()
+            for t in range(0, cfg.T, B):
+                S.push(I[t:t + B])
+            S.result(out=out, out_dtype=xp.F32)
+            b.record()
+            torch.cuda.synchronize()
+            if rep:
+                tot += a.elapsed_time(b)
+        res[name][f"stream_{B}_ms"] = round(tot / reps, 4)
+        res[name][f"stream_{B}_checksum"] = float(out.double().sum())
 print(json.dumps(res))
