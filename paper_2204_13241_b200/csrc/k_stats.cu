@@ -19,10 +19,7 @@ namespace xpcs {
 // 16 LPW DFMA; other lag lists fall back to one shared load per DFMA.
 // =====================================================================================================
 namespace {
-#ifndef XPCS_G2_BATCHED_STAGE
-#define XPCS_G2_BATCHED_STAGE 0
-#endif
-constexpr int G2_WARPS = 8, GC = 128, G2_STAGE_BATCH = 8;   // rows loaded per warp before storing
+constexpr int G2_WARPS = 8, GC = 128;
 constexpr int G2_LPW = 8, G2_LAGS_PER_BLOCK = G2_LPW * G2_WARPS;   // the ISF kernel's tiling (below)
 }
 
@@ -57,25 +54,10 @@ k_g2(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __restrict
     const int rows = GC + halo + 16;
     for (int64_t t0 = 0; t0 < T; t0 += GC) {
         __syncthreads();
-#if XPCS_G2_BATCHED_STAGE
-        for (int r0 = warp; r0 < rows; r0 += G2_STAGE_BATCH * G2_WARPS) {   // G2_STAGE_BATCH loads in flight
-            In v[G2_STAGE_BATCH];
-#pragma unroll
-            for (int k = 0; k < G2_STAGE_BATCH; ++k) {
-                const int r = r0 + k * G2_WARPS;
-                const int64_t t = t0 + r;
-                v[k] = (r < rows && t < T && px < n_q) ? I[t * n_q + px] : (In)0;
-            }
-#pragma unroll
-            for (int k = 0; k < G2_STAGE_BATCH; ++k)
-                if (r0 + k * G2_WARPS < rows) S[(r0 + k * G2_WARPS) * 32 + lane] = (St)v[k];
-        }
-#else
         for (int r = warp; r < rows; r += G2_WARPS) {
             const int64_t t = t0 + r;
             S[r * 32 + lane] = (t < T && px < n_q) ? (St)I[t * n_q + px] : (St)0;
         }
-#endif
         __syncthreads();
         const int rmax = (int)min((int64_t)GC, T - t0);
         if (warp == 0)
