@@ -146,7 +146,7 @@ typedef struct {
     const int32_t* species;
     const void* f_q;
     const double* f_max;   /* HOST [n_species] or NULL: max_q |f_s(q)| per kind, a hint for AUTO's engine choice
-                              (lightest kinds on the integer engine while sum f_max^2 N_s / (f_min^2 N) <= 1.5, the kind
+                              (lightest kinds on the integer engine while sum f_max^2 N_s / (f_min^2 N) <= 2.5, the kind
                               crossing the budget split at it, the rest on the split-FP16 engine; NULL: AUTO runs
                               every kind on the split-FP16 engine, XPCS_ENGINE_TENSOR_I8 every kind on the integer
                               engine) */

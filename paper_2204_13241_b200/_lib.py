@@ -683,12 +683,12 @@ def engine_resolved(engine, uniform_f=True) -> int:
 AUTO_I8 = True    # AUTO routes uniform-f lattice calls to the integer engine (mirrors api.cu)
 
 
-I8_BUDGET = float(os.environ.get("XPCS_I8_BUDGET", "1.5"))   # mirror of api.cu's kI8BudgetDefault (env: experiments)
+I8_BUDGET = float(os.environ.get("XPCS_I8_BUDGET", "2.5"))   # mirror of api.cu's kI8BudgetDefault (env: experiments)
 
 
 def species_engines(counts, f_max=None, budget=None):
     """Mirror of api.cu's AUTO rule for species calls: kinds in increasing |f_max| go to the integer engine while
-    sum (f_max / f_min)^2 N_s / N <= 1; the kind that crosses the budget is split (its first atoms on the integer
+    sum (f_max / f_min)^2 N_s / N <= budget (default I8_BUDGET = 2.5); the kind that crosses the budget is split (its first atoms on the integer
     engine up to the budget), the rest run on split-FP16.  Without f_max hints every kind runs on split-FP16.
     Returns the number of atoms of each kind on the integer engine."""
     counts = [int(c) for c in counts]

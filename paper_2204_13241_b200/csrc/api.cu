@@ -434,7 +434,8 @@ static int validate_volume(const xpcs_qvolume* vol) {
     return XPCS_OK;
 }
 
-constexpr double kI8BudgetDefault = 1.5;   // tools/i8_budget_probe.py: worst 0.40 (c3, 9e4 samples) / 0.43 (c5, 6e4)
+constexpr double kI8BudgetDefault = 2.5;   // tools/i8_budget_probe.py (profiles/r02_i8_budget_probe*.log): f in {1, 2}
+                                           // all on the integer engine, worst 0.61 / 0.56 of the gate (c3 3e5 / c5 2e5 samples)
 static bool fixup_enabled() {
     static int on = -1;
     if (on < 0) { const char* e = getenv("XPCS_FIXUP"); on = (e && atoi(e) == 0) ? 0 : 1; }   // experiments only
@@ -549,7 +550,7 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
     int ng = G.count();
     // engine per atom group.  AUTO with species: the integer engine's limb error grows with the kind's weight, so
     // kinds are taken in increasing max |f_s| (species->f_max, host hints; absent = all equal) while the integer
-    // share of the error budget, sum f_max^2 N_s / (f_ref^2 N) with f_ref the smallest weight, stays <= the budget (1.5, i8_budget) -- near the
+    // share of the error budget, sum f_max^2 N_s / (f_ref^2 N) with f_ref the smallest weight, stays <= the budget (2.5, i8_budget) -- near the
     // single-species f = 1 level validated against the gate; the heavier kinds run on the split-FP16 engine.
     std::vector<char> gi8((size_t)ng, i8 ? 1 : 0);
     // AUTO species call without f_max hints: the kinds' weights are unknown (f_q lives on the device), so the

@@ -182,8 +182,10 @@ def test_species_engine_rule():
     assert se([400, 400, 200], [1.0, 1.0, 1.0]) == [400, 400, 200]
     assert se([10, 10], None) == [0, 0]                        # no hints: every kind on split-FP16
     assert se([0, 100], [0.5, 1.0])[1] == 100                  # an empty kind does not set the reference weight
-    # the default budget (1.5, api.cu kI8BudgetDefault; tools/i8_budget_probe.py): half of the f = 2 kind
-    assert xp.species_engines([500, 500], [1.0, 2.0]) == [500, 250]
+    # the default budget (2.5, api.cu kI8BudgetDefault; tools/i8_budget_probe.py): an f in {1, 2} half-half mix runs
+    # entirely on the integer engine, a heavier kind only in part
+    assert xp.species_engines([500, 500], [1.0, 2.0]) == [500, 500]
+    assert xp.species_engines([500, 500], [1.0, 8.0]) == [500, 31]
 
 
 def test_step_host_validation_before_launch(lib):
