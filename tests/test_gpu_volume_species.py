@@ -165,20 +165,26 @@ def test_table1_grid():
         assert_pixels(I[il], ref, t1["N"], f"table1 l-plane {il}")
 
 
-def test_species_hybrid_auto_parity():
-    """AUTO with f_max hints splits kinds between the integer and split-FP16 engines (heavy kind on FP16); parity at
-    the per-kind gate, and the amplitude of the mixed engines (both hold conj(p) partials)."""
+@pytest.mark.parametrize("f_heavy", [2.0, 4.0])
+def test_species_hybrid_auto_parity(f_heavy):
+    """AUTO with f_max hints: f in {1, 2} runs every kind on the integer engine (budget 2.5), f in {1, 4} splits the
+    heavy kind between the integer and split-FP16 engines; parity at the gate, and the amplitude of the mixed
+    engines (both hold conj(p) partials)."""
     cfg = xi.scaled(xi.CONFIGS["c3"], N=7001, T=2)
     pos = xi.positions(cfg)
     f = xi.form_factors(cfg)
     sp = (f > 1.5).astype(np.int32)
+    f = np.where(sp == 1, f_heavy, 1.0)
+    counts = np.bincount(sp, minlength=2)
+    split = xp.species_engines(counts, [1.0, f_heavy])
+    assert split[0] == counts[0] and (split[1] == counts[1]) == (f_heavy == 2.0)
     v = xp.qvolume(cfg.L, -60, 120, -40, 150, 0, 1)
     q = _vol_q(v)
-    fq = np.stack([np.full(q.shape[0], 1.0), np.full(q.shape[0], 2.0)]).astype(np.float32)
-    I = xp.xpcs_intensity_volume(_t(pos), None, v, species=sp, f_q=_t(fq), f_max=[1.0, 2.0]).cpu().numpy()
+    fq = np.stack([np.full(q.shape[0], 1.0), np.full(q.shape[0], f_heavy)]).astype(np.float32)
+    I = xp.xpcs_intensity_volume(_t(pos), None, v, species=sp, f_q=_t(fq), f_max=[1.0, f_heavy]).cpu().numpy()
     ref = oracle.intensity(pos, f.astype(np.float64), q, cfg.L)
-    assert_pixels(I, ref, cfg.N, "species hybrid")
-    A = xp.xpcs_intensity_volume(_t(pos), None, v, species=sp, f_q=_t(fq), f_max=[1.0, 2.0], amplitude=True)
+    assert_pixels(I, ref, cfg.N, f"species hybrid f_heavy {f_heavy}")
+    A = xp.xpcs_intensity_volume(_t(pos), None, v, species=sp, f_q=_t(fq), f_max=[1.0, f_heavy], amplitude=True)
     A = A.cpu().numpy().astype(np.float64)
     Aref = oracle.amplitudes(pos, f.astype(np.float64), q, cfg.L)
     err = np.abs(A[..., 0] + 1j * A[..., 1] - Aref)
