@@ -179,7 +179,7 @@ bool lattice_tc_supported(const LatticeGeom& g);
 // lattice contraction, tcgen05 kind::i8 with two int8 limbs and exact int32 accumulation (k_lattice_i8.cu):
 // partial [C][Tb][n_h*n_k] float2 (conj(p), like the split-FP16 engine); chunk_atoms <= kI8MaxChunk.
 // uniform_f != 0: all f_j = 1 (no W scale); else F = max |f_j| is reduced into fmax_scratch (1 float) first.
-constexpr int64_t kI8MaxChunk = 32768;
+constexpr int64_t kI8MaxChunk = 65536;   // int32 TMEM accumulators: |X| <= 65536 x 2 x 127 x 128 < 2^31
 int i8_cluster_slots();   // k_lattice_i8 clusters resident at once (cudaOccupancyMaxActiveClusters)
 int i8_stage_atoms();     // k_lattice_i8 atoms per pipeline stage (chunks are multiples of it)
 cudaError_t launch_absmax_f(const uint4* staged, int64_t n, float* out, cudaStream_t s);   // max |f| of staged records

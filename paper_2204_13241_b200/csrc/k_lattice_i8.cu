@@ -21,8 +21,9 @@
 //     v w ~ [65536 hi.hi' + 256 (hi.lo' + lo.hi')] / 32512^2      (the dropped lo.lo' term is <= 1.55e-5, zero-mean)
 // i.e. three int8 MMAs into two TMEM accumulators, HH = sum hi.hi' and X = sum (hi.lo' + lo.hi').  The integer
 // accumulation is EXACT (no TMEM rounding, unlike the FP32 accumulator of the split-FP16 engine), so
-// a chunk of up to 32768 atoms accumulates in TMEM and is drained once (int32 bound: the drain's integer differences
-// AR - BI etc. stay below 2 x 32768 x 2 x 127 x 128 < 2^31).
+// a chunk of up to 65536 atoms accumulates in TMEM and is drained once (int32 bound: |HH| <= 65536 x 127^2 and
+// |X| <= 65536 x 2 x 127 x 128 = 2130706432 < 2^31; the drain converts each accumulator to FP32 before the
+// conjugate-pair sums and differences).
 // The int8 tensor rate is twice the fp16 rate on sm_100a (measured 8192 vs 4096 MAC/clk/SM, tools/mma_rate.cu).
 //
 // CTA pair (cluster of 2, cta_group::2): M = 256 (each CTA: rows [a | b] of its 64 d), N = 256 (each CTA: B rows
