@@ -89,6 +89,9 @@ constexpr float MAGIC = 12582912.0f;                // 1.5 * 2^23
 // t = fma(v, QS, M + 128) holds y = x + 128 in its low 16 bits: byte 1 = hi, byte 0 = lo + 128 (= lo ^ 0x80)
 constexpr float QS = 32512.0f;
 constexpr float QMAGIC = MAGIC + 128.0f;
+#ifndef XPCS_I8_THREE_TERM
+#define XPCS_I8_THREE_TERM 1   // rows by the sign-alternating Chebyshev recurrence (0: complex multiply per row)
+#endif
 #ifndef XPCS_I8_EXPERIMENTS
 #define XPCS_I8_EXPERIMENTS 0   // 1: honour XPCS_I8_DEBUG bit 1 (skip production) in the producers' hot loop
 #endif
@@ -352,17 +355,47 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
                     // rows m = mr + 8 r: real parts (a | wr) into rows m of the hi/lo planes, imaginary parts (b | wi)
                     // into rows 64 + m
                     const uint32_t a0 = su32(smem) + (uint32_t)(s * STAGE_BYTES) + pbase;
-                    const unsigned long long QS2 = pack2(QS, QS), QM2 = pack2(QMAGIC, QMAGIC);
+                    const unsigned long long QM2 = pack2(QMAGIC, QMAGIC);
+#if XPCS_I8_THREE_TERM
+                    // rows 0, 1 from the start phasor and one complex step; rows r + 1 = 2 cos(8 Th) X_r - X_{r-1}
+                    // (Chebyshev, one packed FFMA per phasor; |U_k| <= k + 1 keeps the FP32 error < 4e-6, far below
+                    // the 1.5e-5 Q16 step).  The rows are carried with signs e_r = + + - - + + - -, so the update is
+                    // u_{r+1} = (e_{r+1} e_r) c2 u_r + u_{r-1} (no negation) and row r is quantised with e_r QS.
+                    unsigned long long up[4];
+                    float c2[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) c2[u] = 2.0f * lo2(st[u]);
+#endif
 #pragma unroll
                     for (int r = 0; r < 8; ++r) {
                         uint32_t tc[4], ts[4];
+#if XPCS_I8_THREE_TERM
+                        const float er = ((r >> 1) & 1) ? -QS : QS;                       // e_r QS
+                        const unsigned long long QS2 = pack2(er, er);
+#else
+                        const unsigned long long QS2 = pack2(QS, QS);
+#endif
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
                             const unsigned long long tq = ffma2(v[u], QS2, QM2);
                             tc[u] = (uint32_t)tq; ts[u] = (uint32_t)(tq >> 32);
+#if XPCS_I8_THREE_TERM
+                            if (r == 0) {
+                                const unsigned long long cd = pack2(lo2(st[u]), lo2(st[u]));
+                                const unsigned long long sd = pack2(-hi2(st[u]), hi2(st[u]));
+                                up[u] = v[u];
+                                v[u] = ffma2(swap2(v[u]), sd, f2mul(v[u], cd));
+                            } else if (r < 7) {
+                                const float k = (r & 1) ? -c2[u] : c2[u];                      // e_{r+1} e_r c2
+                                const unsigned long long nv = ffma2(pack2(k, k), v[u], up[u]);
+                                up[u] = v[u];
+                                v[u] = nv;
+                            }
+#else
                             const unsigned long long cd = pack2(lo2(st[u]), lo2(st[u]));
                             const unsigned long long sd = pack2(-hi2(st[u]), hi2(st[u]));
                             v[u] = ffma2(swap2(v[u]), sd, f2mul(v[u], cd));
+#endif
                         }
                         uint32_t rh, rl, ih, il;
                         q16_pack(tc[0], tc[1], tc[2], tc[3], rh, rl);
