@@ -23,68 +23,87 @@ constexpr int G2_WARPS = 8, GC = 128;
 constexpr int G2_LPW = 8, G2_LAGS_PER_BLOCK = G2_LPW * G2_WARPS;   // the ISF kernel's tiling (below)
 }
 
-// LPW lags per warp (8: short lag lists such as config 2's 50; 16: long ones such as config 3's 200 -- per 16 rows
-// 16 + 16 + LPW shared loads feed 16 LPW DFMA, so 16 lags per warp keep the FP64 pipe, not shared memory, the bound).
-// A block's warps cover `lpb` consecutive entries of the lag list (balanced over the y-blocks); the series mean is
-// summed once per block (warp 0) and broadcast through shared memory.
-template <typename In, typename Out, typename St, int LPW>
-__global__ void __launch_bounds__(256)
+// 16 "a" rows r0 .. r0 + 15 (TAIL: only those < rlim) against the sliding window of LPW consecutive lags from t0l:
+// per 16 rows 16 + 16 + LPW - 1 shared loads feed 16 LPW DFMA.  acc has room for the largest LPW (compile-time
+// indices only, so it stays in registers whichever LPW a warp runs).
+template <int LPW, bool TAIL, int CAP>
+__device__ __forceinline__ void g2_rows16(const double* __restrict__ S, int lane, int r0, int rlim, int t0l,
+                                          double (&acc)[CAP]) {
+    static_assert(LPW <= CAP, "accumulator too small");
+    double a[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = (!TAIL || r0 + i < rlim) ? S[(r0 + i) * 32 + lane] : 0.0;
+#pragma unroll
+    for (int j = 0; j < 16 + LPW - 1; ++j) {
+        const double w = S[(r0 + t0l + j) * 32 + lane];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            if (j - i >= 0 && j - i < LPW) acc[j - i] = fma(a[i], w, acc[j - i]);
+    }
+}
+
+template <int LPW, int CAP>
+__device__ __forceinline__ void g2_rows(const double* __restrict__ S, int lane, int rlim, int t0l, double (&acc)[CAP]) {
+    int r0 = 0;
+    for (; r0 + 16 <= rlim; r0 += 16) g2_rows16<LPW, false>(S, lane, r0, rlim, t0l, acc);   // whole groups
+    if (r0 < rlim) g2_rows16<LPW, true>(S, lane, r0, rlim, t0l, acc);                      // the tail
+}
+
+// A block owns 32 pixels (lanes) and up to G2_WARPS x G2_MAXLPW entries of the lag list (one block row for lists of
+// <= 256 lags, so the series is staged once per pixel block); the block's lags are dealt to its warps in groups of
+// 8, balanced (config 3's 200 lags: seven warps of 24 and one of 32), and each warp runs the register-blocked loop
+// of the smallest width in {8, 16, 24, 32} that holds its lags.  The series mean is summed by warp 0.
+constexpr int G2_MAXLPW = 32;
+template <typename In, typename Out>
+__global__ void __launch_bounds__(256, 2)
 k_g2(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __restrict__ lags, int64_t n_lags,
      int halo, int lpb, Out* __restrict__ out) {
     extern __shared__ __align__(16) unsigned char g2_smem[];
-    St* S = reinterpret_cast<St*>(g2_smem);              // [(GC + halo + 16)][32]
+    double* S = reinterpret_cast<double*>(g2_smem);       // [(GC + halo + 16)][32]
     __shared__ double mean_sh[32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t px = (int64_t)blockIdx.x * 32 + lane;
     const int64_t lblk = (int64_t)blockIdx.y * lpb;
-    const int64_t lbase = lblk + warp * LPW;
-    const int64_t lend = min(n_lags, lblk + lpb);
-    const bool active = lbase < lend;
-    int tau[LPW];
+    const int nlb = (int)max((int64_t)0, min((int64_t)lpb, n_lags - lblk));   // lags of this block
+    const int ng = (nlb + 7) / 8;                                              // groups of 8
+    const int g0 = warp * ng / G2_WARPS, g1 = (warp + 1) * ng / G2_WARPS;
+    const int64_t lbase = lblk + 8 * g0;
+    const int nl = min(8 * g1, nlb) - 8 * g0;                                 // this warp's lags
+    const bool active = nl > 0;
+    const int width = (nl + 7) / 8 * 8;                                       // 8, 16, 24 or 32
     bool consecutive = true;
+    for (int l = 1; l < nl; ++l)
+        if (lags[lbase + l] != lags[lbase] + l) consecutive = false;
+    const int t0l = active ? lags[lbase] : 0;
+    double acc[G2_MAXLPW];
 #pragma unroll
-    for (int l = 0; l < LPW; ++l) {
-        tau[l] = (lbase + l < lend) ? lags[lbase + l] : (active ? lags[lbase] + l : 0);
-        if (tau[l] != tau[0] + l) consecutive = false;
-    }
-    double acc[LPW];
-#pragma unroll
-    for (int l = 0; l < LPW; ++l) acc[l] = 0.0;
+    for (int l = 0; l < G2_MAXLPW; ++l) acc[l] = 0.0;
     double sum = 0.0;
     const int rows = GC + halo + 16;
     for (int64_t t0 = 0; t0 < T; t0 += GC) {
         __syncthreads();
-        for (int r = warp; r < rows; r += G2_WARPS) {
-            const int64_t t = t0 + r;
-            S[r * 32 + lane] = (t < T && px < n_q) ? (St)I[t * n_q + px] : (St)0;
-        }
+        const int rv = (int)min((int64_t)rows, T - t0);                      // rows inside the series
+#pragma unroll 4
+        for (int r = warp; r < rv; r += G2_WARPS) S[r * 32 + lane] = px < n_q ? (double)I[(t0 + r) * n_q + px] : 0.0;
+        for (int r = rv + ((warp - rv) % G2_WARPS + G2_WARPS) % G2_WARPS; r < rows; r += G2_WARPS) S[r * 32 + lane] = 0.0;
         __syncthreads();
         const int rmax = (int)min((int64_t)GC, T - t0);
         if (warp == 0)
-            for (int r = 0; r < rmax; ++r) sum += (double)S[r * 32 + lane];
+            for (int r = 0; r < rmax; ++r) sum += S[r * 32 + lane];
         if (!active) continue;
         if (consecutive) {
-            const int t0l = tau[0];
             // rows t with t + tau_0 >= T only meet the zero halo: stop before them (the warp's smallest lag)
             const int rlim = (int)min((int64_t)rmax, max((int64_t)0, T - t0 - t0l));
-            for (int r0 = 0; r0 < rlim; r0 += 16) {          // rows beyond rlim are zero-padded or ignored
-                double a[16];
-#pragma unroll
-                for (int i = 0; i < 16; ++i) a[i] = (r0 + i < rlim) ? (double)S[(r0 + i) * 32 + lane] : 0.0;
-                // sliding window: w_j = S[r0 + t0l + j] meets a[i] for lag l = j - i
-#pragma unroll
-                for (int j = 0; j < 16 + LPW - 1; ++j) {
-                    const double w = (double)S[(r0 + t0l + j) * 32 + lane];
-#pragma unroll
-                    for (int i = 0; i < 16; ++i)
-                        if (j - i >= 0 && j - i < LPW) acc[j - i] = fma(a[i], w, acc[j - i]);
-                }
-            }
+            if (width == 8) g2_rows<8>(S, lane, rlim, t0l, acc);
+            else if (width == 16) g2_rows<16>(S, lane, rlim, t0l, acc);
+            else if (width == 24) g2_rows<24>(S, lane, rlim, t0l, acc);
+            else g2_rows<32>(S, lane, rlim, t0l, acc);
         } else {
             for (int r = 0; r < rmax; ++r) {
-                const double a = (double)S[r * 32 + lane];
+                const double a = S[r * 32 + lane];
 #pragma unroll
-                for (int l = 0; l < LPW; ++l) acc[l] = fma(a, (double)S[(r + tau[l]) * 32 + lane], acc[l]);
+                for (int l = 0; l < G2_MAXLPW; ++l)
+                    if (l < nl) acc[l] = fma(a, S[(r + lags[lbase + l]) * 32 + lane], acc[l]);
             }
         }
     }
@@ -94,31 +113,30 @@ k_g2(const In* __restrict__ I, int64_t T, int64_t n_q, const int32_t* __restrict
     const double mean = mean_sh[lane];
     const double den = mean * mean;
 #pragma unroll
-    for (int l = 0; l < LPW; ++l) {
-        if (lbase + l >= lend) break;
-        const double num = acc[l] / (double)(T - tau[l]);
+    for (int l = 0; l < G2_MAXLPW; ++l) {
+        if (l >= nl) break;
+        const double num = acc[l] / (double)(T - lags[lbase + l]);
         out[(lbase + l) * n_q + px] = (Out)(den > 0.0 ? num / den : __longlong_as_double(0x7ff8000000000000ll));
     }
 }
 
 cudaError_t launch_g2(const void* I, int in_f64, int64_t T, int64_t n_q, const int32_t* lags_dev,
                       int64_t n_lags, int max_lag, void* out, int out_f64, cudaStream_t s) {
-    const size_t elem = sizeof(double);                    // the series is staged in FP64 for both input types
-    const size_t smem = elem * 32 * (GC + max_lag + 16 + 16);
+    const size_t smem = sizeof(double) * 32 * (GC + max_lag + 16 + 16);   // the series is staged in FP64
     note_launch();
-    // lags per warp, and the lag list split over y-blocks of at most 8 warps with balanced counts
-    const int lpw = n_lags >= 64 ? 16 : 8;
-    const int64_t ny = (n_lags + (int64_t)G2_WARPS * lpw - 1) / ((int64_t)G2_WARPS * lpw);
-    const int lpb = (int)(((n_lags + ny - 1) / ny + lpw - 1) / lpw * lpw);
+    // block rows of at most G2_WARPS x G2_MAXLPW lags, balanced in groups of 8
+    const int64_t cap = (int64_t)G2_WARPS * G2_MAXLPW;
+    const int64_t ny = (n_lags + cap - 1) / cap;
+    const int lpb = (int)(((n_lags + ny - 1) / ny + 7) / 8 * 8);
     dim3 grid((unsigned)((n_q + 31) / 32), (unsigned)ny);
-#define G2_CASE(IN, OUT, ST)                                                                                    \
+#define G2_CASE(IN, OUT)                                                                                        \
     {                                                                                                           \
-        auto kern = lpw == 16 ? k_g2<IN, OUT, ST, 16> : k_g2<IN, OUT, ST, 8>;                                   \
+        auto kern = k_g2<IN, OUT>;                                                                              \
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
         kern<<<grid, 256, smem, s>>>((const IN*)I, T, n_q, lags_dev, n_lags, max_lag + 16, lpb, (OUT*)out);    \
     }
-    if (in_f64) { if (out_f64) G2_CASE(double, double, double) else G2_CASE(double, float, double) }
-    else { if (out_f64) G2_CASE(float, double, double) else G2_CASE(float, float, double) }   // staged as FP64: one conversion per load, not per use
+    if (in_f64) { if (out_f64) G2_CASE(double, double) else G2_CASE(double, float) }
+    else { if (out_f64) G2_CASE(float, double) else G2_CASE(float, float) }
 #undef G2_CASE
     return cudaGetLastError();
 }
@@ -133,22 +151,6 @@ cudaError_t launch_g2(const void* I, int in_f64, int64_t T, int64_t n_q, const i
 // the block's pairs are sum_{u < B} D_u D_{u+tau} with D = 0 past P + B (frames before the series): the k_g2 loop
 // with the "a" rows limited to the block.  FP64 products and sums, as k_g2.
 // =====================================================================================================
-// 16 "a" rows r0 .. r0 + 15 (TAIL: only those < rlim) against the sliding window of LPW consecutive lags from t0l
-template <int LPW, bool TAIL>
-__device__ __forceinline__ void g2_rows16(const double* __restrict__ S, int lane, int r0, int rlim, int t0l,
-                                          double (&acc)[LPW]) {
-    double a[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) a[i] = (!TAIL || r0 + i < rlim) ? S[(r0 + i) * 32 + lane] : 0.0;
-#pragma unroll
-    for (int j = 0; j < 16 + LPW - 1; ++j) {
-        const double w = S[(r0 + t0l + j) * 32 + lane];
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-            if (j - i >= 0 && j - i < LPW) acc[j - i] = fma(a[i], w, acc[j - i]);
-    }
-}
-
 template <typename In, int LPW>
 __global__ void __launch_bounds__(256)
 k_g2_accum(const In* __restrict__ blk, int64_t B, const In* __restrict__ ring, int64_t R, int64_t ring0, int64_t P,

@@ -192,6 +192,18 @@ def test_g2_reduction_parity(dt):
     assert_rel(G, ref, 1e-10, "g2")
 
 
+@pytest.mark.parametrize("lags", [list(range(1, 201)),                       # config 3's list: 7 warps x 24 + 32
+                                  list(range(0, 301)),                       # two block rows (> 256 lags)
+                                  list(range(1, 51)),                        # config 2's list: 7 warps x 8 (ragged)
+                                  [3, 9, 10, 11, 40] + list(range(60, 101)) + [150, 151, 203]])  # mixed runs
+def test_g2_reduction_parity_long_lag_lists(lags):
+    rng = np.random.default_rng(41)
+    T, n_q = 419, 70                                     # ragged: 3 chunks + a tail, 3 pixel blocks (the last partial)
+    I = rng.exponential(1.0, (T, n_q)).astype(np.float32)
+    G = xp.xpcs_g2(_t(I), lags).cpu().numpy()
+    assert_rel(G, oracle.g2(I, lags), 1e-10, "g2")
+
+
 def test_rings_and_structure_factor_parity():
     rng = np.random.default_rng(5)
     T, n = 11, 256

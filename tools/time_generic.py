@@ -1,4 +1,5 @@
-"""Time the generic (explicit-q) kernel on a c4-like slice: 1 frame, N = 1M atoms, the first 262144 Ewald pixels."""
+"""Time the generic (explicit-q) kernel on a c4 slice: N = 1M atoms, FRAMES frames (env, default 1), the first PIXELS
+Ewald pixels (env, default 262144; 1048576 = the whole c4 detector)."""
 import os, sys, json
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -7,8 +8,10 @@ import torch
 import xpcs_inputs as xi
 import paper_2204_13241_b200 as xp
 cfg = xi.CONFIGS["c4"]
-pos = torch.from_numpy(xi.positions(cfg, frames=1)).cuda()
-q = xp.xpcs_qgrid_ewald(xi.EWALD_WAVELENGTH_SIGMA, cfg.detector, cfg.detector, xi.EWALD_PITCH_RAD)[: 262144].contiguous()
+FR = int(os.environ.get("FRAMES", "1"))
+PX = int(os.environ.get("PIXELS", "262144"))
+pos = torch.from_numpy(xi.positions(cfg, frames=FR)).cuda()
+q = xp.xpcs_qgrid_ewald(xi.EWALD_WAVELENGTH_SIGMA, cfg.detector, cfg.detector, xi.EWALD_PITCH_RAD)[:PX].contiguous()
 for _ in range(2):
     I = xp.xpcs_intensity(pos, None, q, cfg.L)
 torch.cuda.synchronize()
@@ -19,5 +22,5 @@ for _ in range(3):
 b.record()
 torch.cuda.synchronize()
 ms = a.elapsed_time(b) / 3
-pairs = cfg.N * q.shape[0]
-print(json.dumps({"lib": os.environ.get("XPCS_LIB", "main"), "ms": ms, "pairs_per_s": pairs / (ms / 1e3)}))
+pairs = cfg.N * q.shape[0] * FR
+print(json.dumps({"lib": os.environ.get("XPCS_LIB", "main"), "frames": FR, "pixels": PX, "ms": ms, "pairs_per_s": pairs / (ms / 1e3)}))
