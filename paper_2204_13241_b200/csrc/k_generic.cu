@@ -6,9 +6,9 @@
 // g_c = q_c L / 2 pi (per q, formed once in FP64) and u_c = r_c / L in [0, 1) (per atom, staged as 32-bit fixed
 // point Xi_c and as fp32 xi_c).  Writing g_c = n_c + phi_c (integer part, fraction in [0, 1)):
 //     turns = [ sum_c n_c Xi_c mod 2^32 ] * 2^-32  +  sum_c phi_c xi_c
-// the first term exact in integer arithmetic (3 IMAD), the second in fp32 FFMA (|error| <~ 2e-7 turns, and the
-// per-q rounding of phi_c only moves q by < 1e-7 of a reciprocal-lattice spacing).  No rounded 2 pi ever multiplies
-// a large argument.
+// the first term exact in integer arithmetic (3 IMAD; one I2FP rounds the signed turns to fp32, <= 2^-25 turns), the
+// second in fp32 FFMA (|error| <~ 2e-7 turns, and the per-q rounding of phi_c only moves q by < 1e-7 of a
+// reciprocal-lattice spacing).  No rounded 2 pi ever multiplies a large argument.
 // The angle then goes to the SFU: FFMA -> FMUL.RZ -> MUFU.SIN / MUFU.COS (2 XU ops per atom.q pair, the
 // pipe that bounds this kernel), and f_j cos / f_j sin accumulate in fp32 for at most SUB atoms before being
 // folded into FP64 registers.
@@ -18,6 +18,13 @@ namespace xpcs {
 
 #ifndef XPCS_GEN_QT
 #define XPCS_GEN_QT 2          // q per thread (c4: 2 q x 3 CTAs/SM 1.915e12 pairs/s vs 4 q x 2 CTAs/SM 1.881e12)
+#endif
+#ifndef XPCS_GEN_I2F
+#define XPCS_GEN_I2F 1         // integer turns -> fp32 by one I2FP (c4: 1.97e12 pairs/s) instead of the shift /
+                               // exponent-OR trick (0: SHF + LOP3 + FFMA, 1.89e12)
+#endif
+#ifndef XPCS_GEN_DERIVE
+#define XPCS_GEN_DERIVE 0      // 1: the fp32 fractions xi_c = Xi_c 2^-32 by I2FP in the thread (one shared record per atom)
 #endif
 #ifndef XPCS_GEN_MINB
 #define XPCS_GEN_MINB 3        // resident CTAs per SM the register budget is sized for
@@ -58,6 +65,11 @@ k_generic32(const uint4* __restrict__ staged, int64_t N, const Q* __restrict__ q
         q_split((double)q[3 * qq + 0], L_over_2pi, nx[i], px[i]);
         q_split((double)q[3 * qq + 1], L_over_2pi, ny[i], py[i]);
         q_split((double)q[3 * qq + 2], L_over_2pi, nz[i], pz[i]);
+#if XPCS_GEN_DERIVE
+        px[i] *= 2.3283064365386963e-10f;                     // 2^-32: exact
+        py[i] *= 2.3283064365386963e-10f;
+        pz[i] *= 2.3283064365386963e-10f;
+#endif
     }
     double dre[QT], dim[QT];
 #pragma unroll
@@ -66,26 +78,43 @@ k_generic32(const uint4* __restrict__ staged, int64_t N, const Q* __restrict__ q
     for (int64_t a0 = a_begin; a0 < a_end; a0 += SUB) {
         const int cnt = (int)min((int64_t)SUB, a_end - a0);
         __syncthreads();
+#if XPCS_GEN_DERIVE
+        for (int e = threadIdx.x; e < SUB; e += GT) As[e] = e < cnt ? S[2 * (a0 + e)] : make_uint4(0, 0, 0, 0);
+#else
         for (int e = threadIdx.x; e < 2 * SUB; e += GT) As[e] = (e >> 1) < cnt ? S[2 * a0 + e] : make_uint4(0, 0, 0, 0);
+#endif
         __syncthreads();
         float re[QT], im[QT];
 #pragma unroll
         for (int i = 0; i < QT; ++i) re[i] = im[i] = 0.f;
 #pragma unroll 4
         for (int a = 0; a < SUB; ++a) {
+#if XPCS_GEN_DERIVE
+            const uint4 at = As[a];                               // broadcast: exact fractions + f
+            const float fj = __uint_as_float(at.w);               // 0 for padding atoms
+            // xi_c 2^32 (the 2^-32 sits in px / py / pz)
+            const float xf = __uint2float_rn(at.x), yf = __uint2float_rn(at.y), zf = __uint2float_rn(at.z);
+#else
             const uint4 at = As[2 * a];                           // broadcast: exact fractions + f
             const uint4 af = As[2 * a + 1];                       // fp32 fractions
             const float fj = __uint_as_float(at.w);               // 0 for padding atoms
             const float xf = __uint_as_float(af.x), yf = __uint_as_float(af.y), zf = __uint_as_float(af.z);
+#endif
 #pragma unroll
             for (int i = 0; i < QT; ++i) {
                 uint32_t T = nx[i] * at.x;
                 T = ny[i] * at.y + T;
                 T = nz[i] * at.z + T;
+#if XPCS_GEN_I2F
+                // signed turns to fp32 by one I2FP (round to nearest), scaled inside the last FFMA
+                float th = fmaf(px[i], xf, fmaf(py[i], yf, pz[i] * zf));  // 2 pi sum_c phi_c xi_c
+                th = fmaf(__int2float_rn((int32_t)T), 1.46291807926715968e-9f, th);   // + 2 pi T 2^-32
+#else
                 float th = turns_to_radians(T);                   // integer part of the phase, in [-pi, pi)
                 th = fmaf(px[i], xf, th);                         // + 2 pi sum_c phi_c xi_c
                 th = fmaf(py[i], yf, th);
                 th = fmaf(pz[i], zf, th);
+#endif
                 float s, c;
                 __sincosf(th, &s, &c);
                 re[i] = fmaf(fj, c, re[i]);
