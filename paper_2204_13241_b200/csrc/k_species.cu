@@ -8,6 +8,7 @@
 // folds the engines' atom-chunk partials in FP64, weights them by f_s(q) and forms I = |p|^2 (Eq. 8) or p.
 // HBM-bound: reads sum_s C_s x 8-16 B and S x 4-8 B of f per output element.
 #include "common.cuh"
+#include <type_traits>
 
 namespace xpcs {
 
@@ -36,6 +37,57 @@ __global__ void __launch_bounds__(256) k_species_combine(SpeciesParts sp, int64_
         if (mode == 0) out[i] = (O)(re * re + im * im);
         else { out[2 * i] = (O)re; out[2 * i + 1] = (O)(mode == 2 ? -im : im); }
         bright_append(bs, re * re + im * im, F, i);
+    }
+}
+
+// The same combination for two consecutive outputs per thread (I only, fp32 partials, <= CMB_MAXP partial planes in
+// all, flattened in (species, chunk) order): every plane's two partials arrive by one 16-B load, all issued before
+// the first sum (the scalar loop above keeps one load in flight per thread), then the sums run in the scalar
+// kernel's order -- identical results.
+constexpr int CMB_MAXP = 8;
+struct CombPlanes {
+    const float4* p[CMB_MAXP];     // plane base (2 outputs per float4)
+    const void* f[CMB_MAXP];       // f_q table of the plane's species (read at its first plane)
+    int first[CMB_MAXP + 1];       // 1: the plane starts a species (first[n] = 1)
+    int n;
+};
+template <typename Fq, typename O>
+__global__ void __launch_bounds__(256) k_species_combine2(CombPlanes cp, int64_t total, int64_t n_q, int64_t v0,
+                                                          int64_t n_l, O* __restrict__ out, BrightSink bs) {
+    using Fq2 = typename std::conditional<std::is_same<Fq, double>::value, double2, float2>::type;
+    using O2 = typename std::conditional<std::is_same<O, double>::value, double2, float2>::type;
+    for (int64_t i = 2 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x); i < total;
+         i += 2 * (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = i / n_q, q = i - v * n_q;           // n_q even: i and i + 1 share the frame
+        const int64_t row = ((v0 + v) % n_l) * n_q + q;
+        float4 w[CMB_MAXP];
+        Fq2 fv[CMB_MAXP];
+#pragma unroll
+        for (int k = 0; k < CMB_MAXP; ++k)
+            if (k < cp.n) {
+                w[k] = __ldcs(cp.p[k] + i / 2);
+                if (cp.first[k]) fv[k] = *((const Fq2*)cp.f[k] + row / 2);
+            }
+        double re0 = 0.0, im0 = 0.0, re1 = 0.0, im1 = 0.0, F0 = 0.0, F1 = 0.0;
+        double pr0 = 0.0, pi0 = 0.0, pr1 = 0.0, pi1 = 0.0, fa = 0.0, fb = 0.0;
+#pragma unroll
+        for (int k = 0; k < CMB_MAXP; ++k)
+            if (k < cp.n) {
+                if (cp.first[k]) { fa = (double)fv[k].x; fb = (double)fv[k].y; pr0 = pi0 = pr1 = pi1 = 0.0; }
+                pr0 += (double)w[k].x; pi0 += (double)w[k].y;
+                pr1 += (double)w[k].z; pi1 += (double)w[k].w;
+                if (cp.first[k + 1] || k + 1 == cp.n) {         // the species' last plane
+                    re0 += fa * pr0; im0 += fa * pi0; F0 = fmax(F0, fabs(fa));
+                    re1 += fb * pr1; im1 += fb * pi1; F1 = fmax(F1, fabs(fb));
+                }
+            }
+        const double I0 = re0 * re0 + im0 * im0, I1 = re1 * re1 + im1 * im1;
+        O2 o;
+        o.x = (O)I0;
+        o.y = (O)I1;
+        *(O2*)(out + i) = o;
+        bright_append(bs, I0, F0, i);
+        bright_append(bs, I1, F1, i + 1);
     }
 }
 
@@ -89,6 +141,31 @@ cudaError_t launch_species_combine(const SpeciesParts& sp, int64_t frames, int64
     const dim3 gr = grid_n(total);
     const BrightSink bs = bright ? *bright : BrightSink{nullptr, nullptr, 0.0, nullptr};
     note_launch();
+    int64_t nplanes = 0;
+    bool aligned = true;
+    for (int k = 0; k < sp.n; ++k) {
+        nplanes += sp.C[k];
+        aligned = aligned && ((uintptr_t)sp.part[k] % 16 == 0);
+    }
+    const size_t fqe = fq_f64 ? 8 : 4, oe = out_f64 ? 8 : 4;
+    if (mode == 0 && !sp.part_f64 && nplanes <= CMB_MAXP && n_q % 2 == 0 && aligned &&
+        (uintptr_t)fq % (2 * fqe) == 0 && (uintptr_t)out % (2 * oe) == 0) {
+        CombPlanes cp{};
+        for (int k = 0; k < sp.n; ++k)
+            for (int64_t c = 0; c < sp.C[k]; ++c) {
+                cp.p[cp.n] = (const float4*)((const float2*)sp.part[k] + c * total);
+                cp.f[cp.n] = (const char*)fq + (size_t)sp.kind[k] * n_l * n_q * fqe;
+                cp.first[cp.n] = c == 0;
+                ++cp.n;
+            }
+        cp.first[cp.n] = 1;
+        const dim3 gr2 = grid_n(total / 2);
+#define XPCS_SPC2(F, O) k_species_combine2<F, O><<<gr2, 256, 0, s>>>(cp, total, n_q, v0, n_l, (O*)out, bs)
+        if (fq_f64) { if (out_f64) XPCS_SPC2(double, double); else XPCS_SPC2(double, float); }
+        else { if (out_f64) XPCS_SPC2(float, double); else XPCS_SPC2(float, float); }
+#undef XPCS_SPC2
+        return cudaGetLastError();
+    }
 #define XPCS_SPC(P, F, O) k_species_combine<P, F, O><<<gr, 256, 0, s>>>(sp, total, n_q, (const F*)fq, v0, n_l, (O*)out, mode, bs)
     if (sp.part_f64) {
         if (fq_f64) { if (out_f64) XPCS_SPC(double2, double, double); else XPCS_SPC(double2, double, float); }
