@@ -9,6 +9,7 @@
 // HBM-bound: reads sum_s C_s x 8-16 B and S x 4-8 B of f per output element.
 #include "common.cuh"
 #include <type_traits>
+#include <algorithm>
 
 namespace xpcs {
 
@@ -52,20 +53,21 @@ struct CombPlanes {
     int n;
 };
 template <typename Fq, typename O>
-__global__ void __launch_bounds__(256) k_species_combine2(CombPlanes cp, int64_t total, int64_t n_q, int64_t v0,
+__global__ void __launch_bounds__(256) k_species_combine2(CombPlanes cp, int64_t frames, int64_t n_q, int64_t v0,
                                                           int64_t n_l, O* __restrict__ out, BrightSink bs) {
     using Fq2 = typename std::conditional<std::is_same<Fq, double>::value, double2, float2>::type;
     using O2 = typename std::conditional<std::is_same<O, double>::value, double2, float2>::type;
-    for (int64_t i = 2 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x); i < total;
-         i += 2 * (int64_t)gridDim.x * blockDim.x) {
-        const int64_t v = i / n_q, q = i - v * n_q;           // n_q even: i and i + 1 share the frame
-        const int64_t row = ((v0 + v) % n_l) * n_q + q;
+    const int64_t q = 2 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);   // x: pixel pairs, y: frames (no division)
+    if (q >= n_q) return;
+    for (int64_t v = blockIdx.y; v < frames; v += gridDim.y) {
+        const int64_t i = v * n_q + q;                        // n_q even: i and i + 1 share the frame
+        const int64_t row = (n_l == 1 ? 0 : ((v0 + v) % n_l) * n_q) + q;
         float4 w[CMB_MAXP];
         Fq2 fv[CMB_MAXP];
 #pragma unroll
         for (int k = 0; k < CMB_MAXP; ++k)
             if (k < cp.n) {
-                w[k] = __ldcs(cp.p[k] + i / 2);
+                w[k] = __ldcs(cp.p[k] + i / 2);   // i even: a shift
                 if (cp.first[k]) fv[k] = *((const Fq2*)cp.f[k] + row / 2);
             }
         double re0 = 0.0, im0 = 0.0, re1 = 0.0, im1 = 0.0, F0 = 0.0, F1 = 0.0;
@@ -159,8 +161,10 @@ cudaError_t launch_species_combine(const SpeciesParts& sp, int64_t frames, int64
                 ++cp.n;
             }
         cp.first[cp.n] = 1;
-        const dim3 gr2 = grid_n(total / 2);
-#define XPCS_SPC2(F, O) k_species_combine2<F, O><<<gr2, 256, 0, s>>>(cp, total, n_q, v0, n_l, (O*)out, bs)
+        const int64_t bx = (n_q / 2 + 255) / 256;
+        const dim3 gr2((unsigned)bx, (unsigned)std::max<int64_t>(1, std::min<int64_t>(frames, std::min<int64_t>(
+                                                  65535, ((int64_t)sm_count() * 16 + bx - 1) / bx))));
+#define XPCS_SPC2(F, O) k_species_combine2<F, O><<<gr2, 256, 0, s>>>(cp, frames, n_q, v0, n_l, (O*)out, bs)
         if (fq_f64) { if (out_f64) XPCS_SPC2(double, double); else XPCS_SPC2(double, float); }
         else { if (out_f64) XPCS_SPC2(float, double); else XPCS_SPC2(float, float); }
 #undef XPCS_SPC2
