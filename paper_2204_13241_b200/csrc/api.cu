@@ -21,6 +21,7 @@ int profile_query(int cls, const char** name, double* ms, long long* n);
 using namespace xpcs;
 
 void release_host_resources();   // xpcs_step_host's copy streams and events (defined below)
+void release_overlap_resources();   // the frame-batch overlap's side streams and events (defined below)
 
 namespace {
 
@@ -192,6 +193,7 @@ int xpcs_release(void) {
     clear_error();
     fft_release_plan();
     release_host_resources();
+    release_overlap_resources();
     if (!registered().empty()) {
         cudaDeviceSynchronize();
         for (auto& r : registered()) cudaFree(r.mem);
@@ -507,6 +509,68 @@ static void i8_plan_split(int64_t Ng, int64_t tiles, int64_t V, int64_t& V1, int
     memo.push_back({{Ng, tiles, V, slots}, V1, ch1, ch2});
 }
 
+// Frame-batch overlap (lattice engines): batch b runs on the caller's stream (b even) or on a library side stream
+// (b odd) with its own staging / partial / bright-list buffers, so batch b + 1's staging and batch b's reduction and
+// bright-pixel recompute (HBM-bound, small CTAs) run beside the tensor engine of the neighbouring batch; the engines
+// themselves stay in batch order (each waits for the previous batch's engine).  One side stream and a few events
+// per (device, caller stream), created on first use outside a graph capture (inside one without them: serial).
+namespace {
+struct OverlapRes {
+    cudaStream_t side = nullptr;
+    std::vector<cudaEvent_t> ev;
+};
+std::mutex g_ovl_mu;
+std::map<std::pair<int, cudaStream_t>, OverlapRes> g_ovl;   // node-based: references stay valid
+OverlapRes* overlap_resources(cudaStream_t s, size_t n_events) {
+    std::lock_guard<std::mutex> lk(g_ovl_mu);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    auto it = g_ovl.find({dev, s});
+    OverlapRes* r = it == g_ovl.end() ? nullptr : &it->second;
+    if (r && r->ev.size() >= n_events) return r;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (!r) {
+        r = &g_ovl[{dev, s}];
+        if (cudaStreamCreateWithFlags(&r->side, cudaStreamNonBlocking) != cudaSuccess) {
+            cudaGetLastError();
+            r->side = nullptr;
+            return nullptr;
+        }
+    }
+    if (!r->side) return nullptr;
+    while (r->ev.size() < n_events) {
+        cudaEvent_t e;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        r->ev.push_back(e);
+    }
+    return r;
+}
+bool batch_overlap_enabled() {
+    static int on = -1;
+    if (on < 0) { const char* e = getenv("XPCS_BATCH_OVERLAP"); on = (e && atoi(e) == 0) ? 0 : 1; }
+    return on == 1;
+}
+}  // namespace
+void release_overlap_resources() {
+    std::lock_guard<std::mutex> lk(g_ovl_mu);
+    for (auto& kv : g_ovl) {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(kv.first.first);
+        if (kv.second.side) { cudaStreamSynchronize(kv.second.side); cudaStreamDestroy(kv.second.side); }
+        for (cudaEvent_t e : kv.second.ev) cudaEventDestroy(e);
+        cudaSetDevice(cur);
+    }
+    g_ovl.clear();
+}
+
 static int run_volume(const void* positions, int64_t N, const void* form_factors, const xpcs_species* species,
                       const xpcs_qvolume* vol, int64_t frames, void* I_out, const xpcs_opts* opts, int amp) {
     clear_error();
@@ -695,7 +759,10 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
         sumC += C[gi];
     }
     sp.part_f64 = 0;
-    const int64_t Tb = std::max<int64_t>(1, std::min<int64_t>(V, (int64_t)(kBatchBytes / std::max<int64_t>(16 * N, 8 * sumC * n_q))));
+    // XPCS_BATCH_BYTES (tests and experiments): a smaller cap forces many frame batches (results do not depend on it)
+    const char* bb_env = getenv("XPCS_BATCH_BYTES");
+    const int64_t batch_bytes = bb_env ? std::max<int64_t>(1, atoll(bb_env)) : (int64_t)kBatchBytes;
+    const int64_t Tb = std::max<int64_t>(1, std::min<int64_t>(V, batch_bytes / std::max<int64_t>(16 * N, 8 * sumC * n_q)));
     // frame batches: memory-bounded (Tb).  A single integer-engine group in one batch is split in two when that
     // shortens the last, partly filled wave of clusters: the leading frames fill whole waves with unsplit atom
     // ranges, the remaining frames get their own atom chunking (cost model of i8_plan_chunk), e.g. c2: 100 frames x
@@ -717,25 +784,54 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
             for (int64_t v0 = 0; v0 < V; v0 += Tb) batches.push_back({v0, std::min(Tb, V - v0), 0});
         }
     }
-    uint4* st = (uint4*)scratch(o.s, SS_STAGE, sizeof(uint4) * (size_t)(N * Tb));
-    float2* part = (float2*)scratch(o.s, SS_PARTIAL, sizeof(float2) * (size_t)part_elems);
-    if (!st || !part) return XPCS_ENOMEM;
-    float* fmax = nullptr;
+    // two buffer sets and the side stream when the frames run in several batches (see overlap_resources)
+    OverlapRes* ovl = (batches.size() > 1 && batch_overlap_enabled()) ? overlap_resources(o.s, batches.size() + 2) : nullptr;
+    uint4* stb[2] = {(uint4*)scratch(o.s, SS_STAGE, sizeof(uint4) * (size_t)(N * Tb)), nullptr};
+    float2* partb[2] = {(float2*)scratch(o.s, SS_PARTIAL, sizeof(float2) * (size_t)part_elems), nullptr};
+    if (!stb[0] || !partb[0]) return XPCS_ENOMEM;
+    if (ovl) {
+        stb[1] = (uint4*)scratch(o.s, SS_STAGE2, sizeof(uint4) * (size_t)(N * Tb));
+        partb[1] = (float2*)scratch(o.s, SS_PARTIAL2, sizeof(float2) * (size_t)part_elems);
+        if (!stb[1] || !partb[1]) return XPCS_ENOMEM;
+    }
+    float* fmax0 = nullptr;   // max |f| per buffer set (written by the engine launch, read by its batch's fix-up)
     if ((i8 || tc) && form_factors) {
-        fmax = (float*)scratch(o.s, SS_SMALL, 64);
-        if (!fmax) return XPCS_ENOMEM;
+        fmax0 = (float*)scratch(o.s, SS_SMALL, 128);
+        if (!fmax0) return XPCS_ENOMEM;
     }
     // the tensor engines' partials hold conj(p) (R1)
     const int mode = amp ? ((tc || i8) ? 2 : 1) : 0;
-    void* fbuf = nullptr;
+    void* fbufb[2] = {nullptr, nullptr};
     if ((i8 || tc) && fixup_enabled()) {
         int64_t vb_max = 0;
         for (const FrameBatch& fb : batches) vb_max = std::max(vb_max, fb.vb);
-        fbuf = scratch(o.s, SS_FIX, fixup_scratch_bytes(vb_max, n_q, N));
-        if (!fbuf) return XPCS_ENOMEM;
+        fbufb[0] = scratch(o.s, SS_FIX, fixup_scratch_bytes(vb_max, n_q, N));
+        if (!fbufb[0]) return XPCS_ENOMEM;
+        if (ovl) {
+            fbufb[1] = scratch(o.s, SS_FIX2, fixup_scratch_bytes(vb_max, n_q, N));
+            if (!fbufb[1]) return XPCS_ENOMEM;
+        }
     }
-    for (const FrameBatch& fb : batches) {
+    // the side stream joins the caller's stream (fork) and is joined back before returning, also on errors
+    cudaEvent_t ev_join = nullptr;
+    if (ovl) {
+        TRY(cuda_fail(cudaEventRecord(ovl->ev[0], o.s), "fork"));
+        TRY(cuda_fail(cudaStreamWaitEvent(ovl->side, ovl->ev[0], 0), "fork"));
+        ev_join = ovl->ev[1];
+    }
+    struct Join {
+        OverlapRes* r; cudaEvent_t e; cudaStream_t s;
+        ~Join() { if (r) { cudaEventRecord(e, r->side); cudaStreamWaitEvent(s, e, 0); } }
+    } join{ovl, ev_join, o.s};
+    for (size_t bi = 0; bi < batches.size(); ++bi) {
+        const FrameBatch& fb = batches[bi];
         const int64_t v0 = fb.v0, vb = fb.vb;
+        const int par = ovl ? (int)(bi & 1) : 0;
+        const cudaStream_t sb = par ? ovl->side : o.s;
+        uint4* st = stb[par];
+        float2* part = partb[par];
+        void* fbuf = fbufb[par];
+        float* fmax = fmax0 ? fmax0 + 16 * par : nullptr;
         if (fb.chunk > 0) { chunk[0] = fb.chunk; C[0] = (G.cnt[0] + fb.chunk - 1) / fb.chunk; }
         void* dst = (char*)I_out + isz * n_q * v0;
         // one integer-engine group in a single atom chunk: the kernel writes the result itself (no partial planes)
@@ -746,36 +842,42 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
         // epilogue lists the brightest pixels and k_fixup.cu recomputes them exactly
         const bool fix = (i8 || tc) && fbuf;
         BrightSink bs{nullptr, nullptr, 0.0, nullptr};
-        if (fix) TRY(cuda_fail(fixup_prepare(fbuf, N, form_factors ? fmax : nullptr, bs, o.s), "bright-pixel list"));
+        if (fix) TRY(cuda_fail(fixup_prepare(fbuf, N, form_factors ? fmax : nullptr, bs, sb), "bright-pixel list"));
         int64_t stoff = 0, poff = 0;
+        bool waited = false;
         for (int gi = 0; gi < ng; ++gi) {
             const int64_t Ng = G.cnt[gi];
             sp.part[gi] = part + poff;
             sp.C[gi] = C[gi];
             if (Ng == 0) continue;
             const StageMap m = stage_map(G, gi, N, v0, n_l, l0, vol->mc);
-            { ProfScope p(o.profile, KC_STAGE, o.s);
-              TRY(cuda_fail(launch_stage_lattice32(positions, 0, form_factors, 0, Ng, vb, g, m, st + stoff, o.s), "stage")); }
-            { ProfScope p(o.profile, KC_MAIN, o.s);
+            { ProfScope p(o.profile, KC_STAGE, sb);
+              TRY(cuda_fail(launch_stage_lattice32(positions, 0, form_factors, 0, Ng, vb, g, m, st + stoff, sb), "stage")); }
+            if (ovl && bi > 0 && !waited) {   // engines in batch order
+                TRY(cuda_fail(cudaStreamWaitEvent(sb, ovl->ev[2 + bi - 1], 0), "batch order"));
+                waited = true;
+            }
+            { ProfScope p(o.profile, KC_MAIN, sb);
               const bool g_i8 = i8 && gi8[(size_t)gi], g_tc = (i8 || tc) && !g_i8;
-              ProfScope pe(o.profile && (g_i8 || g_tc), g_i8 ? KC_I8 : KC_TC, o.s);
+              ProfScope pe(o.profile && (g_i8 || g_tc), g_i8 ? KC_I8 : KC_TC, sb);
               if (g_i8) TRY(cuda_fail(launch_lattice_i8(st + stoff, Ng, vb, g, chunk[gi], C[gi], fmax, form_factors == nullptr,
-                                                      part + poff, o.s, direct ? dst : nullptr, o.out_f64, mode,
+                                                      part + poff, sb, direct ? dst : nullptr, o.out_f64, mode,
                                                       (fix && direct) ? &bs : nullptr),
                                     "lattice tcgen05 i8"));
               else if (g_tc) {
-                  if (fmax) TRY(cuda_fail(launch_absmax_f(st + stoff, Ng, fmax, o.s), "max |f|"));   // the fix-up threshold
-                  TRY(cuda_fail(launch_lattice_tc(st + stoff, Ng, vb, g, chunk[gi], C[gi], part + poff, o.s), "lattice tcgen05"));
+                  if (fmax) TRY(cuda_fail(launch_absmax_f(st + stoff, Ng, fmax, sb), "max |f|"));   // the fix-up threshold
+                  TRY(cuda_fail(launch_lattice_tc(st + stoff, Ng, vb, g, chunk[gi], C[gi], part + poff, sb), "lattice tcgen05"));
               }
-              else TRY(cuda_fail(launch_lattice_simt(st + stoff, Ng, vb, g, chunk[gi], C[gi], part + poff, o.s), "lattice simt")); }
+              else TRY(cuda_fail(launch_lattice_simt(st + stoff, Ng, vb, g, chunk[gi], C[gi], part + poff, sb), "lattice simt")); }
             stoff += Ng * vb;
             poff += C[gi] * n_q * vb;
         }
+        if (ovl) TRY(cuda_fail(cudaEventRecord(ovl->ev[2 + bi], sb), "batch order"));   // this batch's engines done
         if (!direct) {
-            ProfScope p(o.profile, KC_REDUCE, o.s);
-            if (G.n_species) TRY(cuda_fail(launch_species_combine(sp, vb, n_q, G.fq, 0, v0, n_l, dst, o.out_f64, mode, o.s,
+            ProfScope p(o.profile, KC_REDUCE, sb);
+            if (G.n_species) TRY(cuda_fail(launch_species_combine(sp, vb, n_q, G.fq, 0, v0, n_l, dst, o.out_f64, mode, sb,
                                                                   fix ? &bs : nullptr), "species combine"));
-            else TRY(cuda_fail(launch_amp_reduce_f(part, C[0], vb, n_q, dst, o.out_f64, mode, o.s, fix ? &bs : nullptr), "reduce"));
+            else TRY(cuda_fail(launch_amp_reduce_f(part, C[0], vb, n_q, dst, o.out_f64, mode, sb, fix ? &bs : nullptr), "reduce"));
         }
         if (fix) {
             FixGroups fg{};
@@ -793,8 +895,8 @@ static int run_volume(const void* positions, int64_t N, const void* form_factors
             fg.fq_f64 = 0;
             fg.v0 = v0;
             fg.n_l = n_l;
-            ProfScope p(o.profile, KC_FIXUP, o.s);
-            TRY(cuda_fail(launch_fixup(fg, g, vb, dst, o.out_f64, amp ? 1 : 0, fbuf, o.s), "bright-pixel recompute"));
+            ProfScope p(o.profile, KC_FIXUP, sb);
+            TRY(cuda_fail(launch_fixup(fg, g, vb, dst, o.out_f64, amp ? 1 : 0, fbuf, sb), "bright-pixel recompute"));
         }
     }
     return XPCS_OK;

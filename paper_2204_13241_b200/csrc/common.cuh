@@ -18,7 +18,7 @@ void note_launch(int n = 1);
 // Scratch cached per (stream, slot); grown on demand (the grow synchronises the device).
 enum ScratchSlot {
     SS_STAGE = 0, SS_PARTIAL, SS_PLAN, SS_PLAN2, SS_XSVS, SS_SMALL, SS_LAGS, SS_TC, SS_IDX, SS_FFT,
-    SS_H_POS, SS_H_FF, SS_H_I, SS_H_G2, SS_H_RED, SS_FIX, SS_H_FQ, SS_COUNT
+    SS_H_POS, SS_H_FF, SS_H_I, SS_H_G2, SS_H_RED, SS_FIX, SS_H_FQ, SS_STAGE2, SS_PARTIAL2, SS_FIX2, SS_COUNT
 };
 void* scratch(cudaStream_t s, int slot, size_t bytes);   // nullptr on failure (error already set)
 // workspace id of the calling thread's current API call (xpcs_opts.workspace): scratch is keyed by (device, workspace,

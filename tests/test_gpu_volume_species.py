@@ -189,3 +189,35 @@ def test_species_hybrid_auto_parity(f_heavy):
     Aref = oracle.amplitudes(pos, f.astype(np.float64), q, cfg.L)
     err = np.abs(A[..., 0] + 1j * A[..., 1] - Aref)
     assert np.max(err / (1e-3 * np.sqrt(cfg.N) + 1e-5 * np.abs(Aref))) <= 1.0
+
+
+@pytest.mark.parametrize("case", ["species_hybrid", "per_atom_f", "uniform_i8"])
+def test_frame_batches_overlapped(case, monkeypatch):
+    """Frames split into many batches (XPCS_BATCH_BYTES) run on two alternating streams with their own buffers
+    (a batch's staging and reduction beside the neighbouring batch's tensor engine): the same intensities as one
+    batch -- bit-identical where the atom chunking does not change (species calls) -- and the per-pixel gate."""
+    cfg = xi.scaled(xi.CONFIGS["c3"], N=5003, T=7)
+    pos = xi.positions(cfg)
+    v = xp.qvolume(cfg.L, -70, 140, -64, 256, 0, 1)
+    q = _vol_q(v)
+    kw, f64 = {}, None
+    if case == "species_hybrid":
+        f = xi.form_factors(cfg)
+        sp = (f > 1.5).astype(np.int32)
+        f64 = np.where(sp == 1, 4.0, 1.0)
+        fq = np.stack([np.full(q.shape[0], 1.0), np.full(q.shape[0], 4.0)]).astype(np.float32)
+        kw = dict(species=sp, f_q=_t(fq), f_max=[1.0, 4.0])
+        ff = None
+    elif case == "per_atom_f":
+        f64 = 1.0 + np.random.default_rng(3).random(cfg.N)
+        ff = _t(f64.astype(np.float32))
+    else:
+        ff = None
+    one = xp.xpcs_intensity_volume(_t(pos), ff, v, **kw).cpu().numpy()
+    monkeypatch.setenv("XPCS_BATCH_BYTES", str(16 * cfg.N * 2))    # two frames per batch: 4 batches
+    many = xp.xpcs_intensity_volume(_t(pos), ff, v, **kw).cpu().numpy()
+    torch.cuda.synchronize()
+    if case == "species_hybrid":
+        np.testing.assert_array_equal(many, one)
+    ref = oracle.intensity(pos, f64, q, cfg.L)
+    assert_pixels(many, ref, cfg.N if f64 is None else float((f64 ** 2).sum()), f"batched {case}")
