@@ -627,7 +627,10 @@ def main():
                 "kernel_ms": {k: v[0] / max(args.steps, 1) for k, v in prof.items()},
                 "secondary_rooflines": secondary,
                 "secondary_note": f"reductions timed alone (serialised, {n_iso} eager steps after the timed region); "
-                                  "kernel_ms are from the timed graph replays, where they run concurrently"}
+                                  "kernel_ms are event intervals per kernel class from the timed graph replays, where "
+                                  "classes run concurrently (consecutive frame batches on two streams: a batch's "
+                                  "staging / reduction / fix-up interval includes time spent beside the neighbouring "
+                                  "batch's tensor engine), so they overlap and do not add up to ms_per_step"}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
