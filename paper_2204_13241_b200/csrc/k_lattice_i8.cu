@@ -64,7 +64,7 @@ constexpr int STAGE_BYTES = 4 * PLANE;              // A_hi A_lo B_hi B_lo = 16 
 #endif
 constexpr int STAGES = XPCS_I8_STAGES;
 #ifndef XPCS_I8_GROUPS
-#define XPCS_I8_GROUPS (XPCS_I8_KS == 64 ? 3 : 5)
+#define XPCS_I8_GROUPS (XPCS_I8_KS == 64 ? 3 : 4)   // c3 4 x 8: 2.346e14 vs 5 x 8 2.283e14; c2 0.992 vs 1.013 ms
 #endif
 constexpr int NGROUPS = XPCS_I8_GROUPS, GROUP_WARPS = 2 * KQ;   // per group: KQ X warps, KQ W warps (one per K slice)
 static_assert(NGROUPS <= STAGES, "mbarrier parity: producer groups must not exceed the stage count");

@@ -1,0 +1,8 @@
+# integer engine producer groups x stages: c3 (power-capped) and c2 (full clock) bench steps
+mkdir -p gpurun_out/gs2
+for v in main g4s8 g3s8 g4s10 g3s6 g4s7 g4s6; do
+  if [ $v = main ]; then unset XPCS_LIB; else export XPCS_LIB=$PWD/build/libxpcs_$v.so; fi
+  timeout 600 python bench.py --no-e2e --no-cpu-baseline --steps 5 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.readlines()[-1]); print('c3 $v', d['value'], round(d['ms_per_step'],3), round(d['kernel_ms']['intensity_i8'],3), d['clocks']['sm_mhz'])" >> gpurun_out/gs2/sweep.log 2>&1
+  timeout 600 python bench.py --config c2 --no-e2e --no-cpu-baseline --steps 20 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.readlines()[-1]); print('c2 $v', d['value'], round(d['ms_per_step'],4), round(d['kernel_ms']['intensity_i8'],4), d['clocks']['sm_mhz'])" >> gpurun_out/gs2/sweep.log 2>&1
+done
+unset XPCS_LIB; cat gpurun_out/gs2/sweep.log
