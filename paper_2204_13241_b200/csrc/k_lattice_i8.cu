@@ -29,12 +29,13 @@
 // CTA pair (cluster of 2, cta_group::2): M = 256 (each CTA: rows [a | b] of its 64 d), N = 256 (each CTA: B rows
 // [wr | wi] of its 64 k), K = 32 atoms per stage, 3 MMAs per stage:  HH += A_hi.B_hi,  X += A_hi.B_lo + A_lo.B_hi.
 //
-// Producers: NGROUPS groups of 4 warps (2 X warps, 2 W warps: one per 16-atom K half); group g fills stages
-// i = g mod NGROUPS of a STAGES-deep ring (16 KB per stage; the group count must not exceed the stage count, see the
-// empty-barrier parity note in DESIGN.md 6.1).  A warp thread owns 4 consecutive atoms (one 32-bit word per row and
-// limb plane) and 8 rows spaced 8 apart, walks the rows with the angle-addition recurrence X_{m+8} = X_m X_8
-// (packed FP32x2, 2 ops per phasor; 2 SFU sincos per atom per thread), quantises with one packed magic-number FFMA
-// per phasor and packs limb bytes with PRMT.  After the last stage, warps 0-7 drain both accumulators through a
+// Producers: NGROUPS groups of one X warp and one W warp, each covering the stage's 32 atoms (XPCS_I8_OCT = 0: 2 + 2
+// warps, one per 16-atom K half); group g fills stages i = g mod NGROUPS of a STAGES-deep ring (16 KB per stage; the
+// group count must not exceed the stage count, see the empty-barrier parity note in DESIGN.md 6.1).  A warp thread
+// owns 8 consecutive atoms (two 32-bit words per row and limb plane, one STS.64) and 8 rows spaced 8 apart: rows 0
+// and 1 from a start phasor and one angle-addition step X_{m+8} = X_m X_8 (2 SFU sincos per atom per thread), the
+// rest by the sign-alternating Chebyshev recurrence (one packed FFMA per phasor-row); it quantises with one packed
+// magic-number FFMA per phasor and packs limb bytes with PRMT.  After the last stage, warps 0-7 drain both accumulators through a
 // shared-memory tile in 4 rounds of 32 k: p-components v = (65536 HH + 256 X) F / 32512^2 in FP32, then the
 // conjugate-pair combination above with row-contiguous global writes of the partial amplitude or, with a single
 // atom chunk, the final I = |p|^2 (or p) itself.
@@ -63,10 +64,17 @@ constexpr int STAGE_BYTES = 4 * PLANE;              // A_hi A_lo B_hi B_lo = 16 
 #define XPCS_I8_STAGES (XPCS_I8_KS == 64 ? 6 : 8)
 #endif
 constexpr int STAGES = XPCS_I8_STAGES;
-#ifndef XPCS_I8_GROUPS
-#define XPCS_I8_GROUPS (XPCS_I8_KS == 64 ? 3 : 4)   // c3 4 x 8: 2.346e14 vs 5 x 8 2.283e14; c2 0.992 vs 1.013 ms
+#ifndef XPCS_I8_OCT
+#define XPCS_I8_OCT 1   // 1: a producer thread owns 8 consecutive atoms (STS.64; one X and one W warp per group cover
+                        // K = 32); 0: 4 atoms (one X and one W warp per 16-atom K slice)
 #endif
-constexpr int NGROUPS = XPCS_I8_GROUPS, GROUP_WARPS = 2 * KQ;   // per group: KQ X warps, KQ W warps (one per K slice)
+#ifndef XPCS_I8_GROUPS
+#define XPCS_I8_GROUPS (XPCS_I8_KS == 64 ? 3 : (XPCS_I8_OCT ? 6 : 4))   // DESIGN.md 6.2 sweeps
+#endif
+constexpr int AT = XPCS_I8_OCT ? 8 : 4;             // atoms per producer thread
+static_assert(AT == 4 || KS == 32, "8 atoms per thread: 32-atom stages");
+constexpr int NGROUPS = XPCS_I8_GROUPS;
+constexpr int GROUP_WARPS = AT == 8 ? 2 : 2 * KQ;   // per group: X and W warps (AT = 4: one per 16-atom K slice)
 static_assert(NGROUPS <= STAGES, "mbarrier parity: producer groups must not exceed the stage count");
 constexpr int NPROD_WARPS = NGROUPS * GROUP_WARPS;
 constexpr int MMA_WARP = NPROD_WARPS;               // producer warps 0-7 (two per TMEM lane quarter) also drain the tile
@@ -75,7 +83,7 @@ constexpr int NTHREADS = (MMA_WARP + 1) * 32;
 constexpr int MMA_N = 2 * TN;                       // 256
 constexpr int TMEM_COLS = 512;                      // HH cols [0, 256), X cols [256, 512)
 constexpr int ASL = 4;                              // atom-record slots per warp (cp.async prefetch distance ASL - 1)
-constexpr int WREC = 16;                            // records a producer warp needs per stage (its 4 atom quads)
+constexpr int WREC = AT == 8 ? KS : 16;             // records a producer warp needs per stage
 // record r of a warp's stage sits in 16-B unit r ^ ((r & 8) >> 2) of its slot: the cp.async writes (8 lanes per
 // phase, records 0-7 / 8-15) and the per-field 32-bit reads of records {u, 4 + u, 8 + u, 12 + u} (one per quad)
 // both hit distinct banks, one wavefront per instruction
@@ -204,6 +212,10 @@ template <int OFF>
 __device__ __forceinline__ void i8_sts(uint32_t addr, uint32_t v) {
     asm volatile("st.shared.b32 [%0+%2], %1;" ::"r"(addr), "r"(v), "n"(OFF));
 }
+template <int OFF>
+__device__ __forceinline__ void i8_sts64(uint32_t addr, uint32_t v0, uint32_t v1) {
+    asm volatile("st.shared.v2.b32 [%0+%3], {%1, %2};" ::"r"(addr), "r"(v0), "r"(v1), "n"(OFF));
+}
 
 #define I8_TMEM_LD8(taddr, r)                                                                                      \
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"                            \
@@ -289,8 +301,10 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
         // ================= producers: group g fills stages g, g + NGROUPS, g + 2 NGROUPS, ... =================
         const int grp = warp / GROUP_WARPS, wi = warp % GROUP_WARPS;
         const int qq = lane & 3, mr = lane >> 2;
-        const bool is_x = wi < KQ;
-        const int qh = wi % KQ;                               // K slice of the stage (atoms 16 qh .. 16 qh + 15)
+        const bool is_x = wi < GROUP_WARPS / 2;
+        // AT = 4: K slice qh of the stage (atoms 16 qh + 4 qq + u); AT = 8: the warp covers the stage, the thread
+        // owns atoms 8 qq + u (K half qq >> 1, octet qq & 1)
+        const int qh = AT == 8 ? 0 : wi % KQ;
         const uint32_t full0 = i8_mapa(su32(full), 0);
         // every warp prefetches its own 16 atom records with cp.async into a private ring: no cross-warp barrier
         const uint32_t slot0 = su32(aslot) + (uint32_t)(warp * ASL * WSLOT * 16);
@@ -301,14 +315,15 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
         const uint32_t i0 = (uint32_t)((int)rank * HD + mr);
         const uint32_t cH = (uint32_t)(H0 + PAIR_H / 2 - 1);
         const uint32_t kk = (uint32_t)(g.k0 + bk0 + mr);
-        const uint32_t pbase = (uint32_t)((is_x ? 0 : 2 * PLANE) + qh * 128 + mr * 16 + qq * 4);
+        const uint32_t pbase = AT == 8 ? (uint32_t)((is_x ? 0 : 2 * PLANE) + (qq >> 1) * 128 + mr * 16 + (qq & 1) * 8)
+                                       : (uint32_t)((is_x ? 0 : 2 * PLANE) + qh * 128 + mr * 16 + qq * 4);
         auto prefetch = [&](int li) {   // local stage li of this group -> slot li % ASL of this warp
             const int i = grp + li * NGROUPS;
             if (i < n_stages && lane < WREC) {
                 const int64_t j = a_begin + (int64_t)i * KS + WREC * qh + lane;
                 const bool ok = j < a_end;
-                i8_cp_async16(slot0 + (uint32_t)(((li % ASL) * WSLOT + (lane ^ ((lane & 8) >> 2))) * 16), S + (ok ? j : 0),
-                              ok ? 16u : 0u);
+                const int unit = AT == 8 ? (lane ^ ((lane >> 3) & 3)) : (lane ^ ((lane & 8) >> 2));
+                i8_cp_async16(slot0 + (uint32_t)(((li % ASL) * WSLOT + unit) * 16), S + (ok ? j : 0), ok ? 16u : 0u);
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
         };
@@ -324,11 +339,12 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
                 asm volatile("cp.async.wait_group %0;" ::"n"(ti8::ASL - 2) : "memory");
                 __syncwarp();                 // the warp's records of stage i are visible to all its lanes; every lane
                 prefetch(li + ASL - 1);       // has finished reading slot (li - 1) % ASL, which is refilled now
-                unsigned long long v[4], st[4];
+                unsigned long long v[AT], st[AT];
                 const uint32_t ra = slot0 + (uint32_t)((li % ASL) * WSLOT * 16);
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const uint32_t a = ra + (uint32_t)((((4 * qq + u) ^ (qq & 2))) * 16);   // record 4 qq + u
+                for (int u = 0; u < AT; ++u) {
+                    // record AT qq + u of the warp's slot (swizzled 16-B units: conflict-free reads)
+                    const uint32_t a = ra + (uint32_t)((AT == 8 ? ((8 * qq + u) ^ qq) : ((4 * qq + u) ^ (qq & 2))) * 16);
                     float s0, c0, s1, c1;
                     if (X) {
                         uint32_t tha;
@@ -361,14 +377,14 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
                     // (Chebyshev, one packed FFMA per phasor; |U_k| <= k + 1 keeps the FP32 error < 4e-6, far below
                     // the 1.5e-5 Q16 step).  The rows are carried with signs e_r = + + - - + + - -, so the update is
                     // u_{r+1} = (e_{r+1} e_r) c2 u_r + u_{r-1} (no negation) and row r is quantised with e_r QS.
-                    unsigned long long up[4];
-                    float c2[4];
+                    unsigned long long up[AT];
+                    float c2[AT];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) c2[u] = 2.0f * lo2(st[u]);
+                    for (int u = 0; u < AT; ++u) c2[u] = 2.0f * lo2(st[u]);
 #endif
 #pragma unroll
                     for (int r = 0; r < 8; ++r) {
-                        uint32_t tc[4], ts[4];
+                        uint32_t tc[AT], ts[AT];
 #if XPCS_I8_THREE_TERM
                         const float er = ((r >> 1) & 1) ? -QS : QS;                       // e_r QS
                         const unsigned long long QS2 = pack2(er, er);
@@ -376,7 +392,7 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
                         const unsigned long long QS2 = pack2(QS, QS);
 #endif
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
+                        for (int u = 0; u < AT; ++u) {
                             const unsigned long long tq = ffma2(v[u], QS2, QM2);
                             tc[u] = (uint32_t)tq; ts[u] = (uint32_t)(tq >> 32);
 #if XPCS_I8_THREE_TERM
@@ -401,10 +417,20 @@ k_lattice_i8(const uint4* __restrict__ staged, int64_t N, LatticeGeom g, int64_t
                         q16_pack(tc[0], tc[1], tc[2], tc[3], rh, rl);
                         q16_pack(ts[0], ts[1], ts[2], ts[3], ih, il);
                         const uint32_t ad = a0 + (uint32_t)(r * RG);
-                        i8_sts<0>(ad, rh);
-                        i8_sts<PLANE>(ad, rl);
-                        i8_sts<HALF_ROWS>(ad, ih);
-                        i8_sts<PLANE + HALF_ROWS>(ad, il);
+                        if (AT == 8) {                        // atoms 4-7: the next word of each row, one STS.64 each
+                            uint32_t rh1, rl1, ih1, il1;
+                            q16_pack(tc[AT - 4], tc[AT - 3], tc[AT - 2], tc[AT - 1], rh1, rl1);
+                            q16_pack(ts[AT - 4], ts[AT - 3], ts[AT - 2], ts[AT - 1], ih1, il1);
+                            i8_sts64<0>(ad, rh, rh1);
+                            i8_sts64<PLANE>(ad, rl, rl1);
+                            i8_sts64<HALF_ROWS>(ad, ih, ih1);
+                            i8_sts64<PLANE + HALF_ROWS>(ad, il, il1);
+                        } else {
+                            i8_sts<0>(ad, rh);
+                            i8_sts<PLANE>(ad, rl);
+                            i8_sts<HALF_ROWS>(ad, ih);
+                            i8_sts<PLANE + HALF_ROWS>(ad, il);
+                        }
                     }
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
