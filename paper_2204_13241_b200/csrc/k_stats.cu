@@ -19,7 +19,10 @@ namespace xpcs {
 // 16 LPW DFMA; other lag lists fall back to one shared load per DFMA.
 // =====================================================================================================
 namespace {
-constexpr int G2_WARPS = 8, GC = 128;
+#ifndef XPCS_G2_GC
+#define XPCS_G2_GC 128
+#endif
+constexpr int G2_WARPS = 8, GC = XPCS_G2_GC;   // frames per staged chunk (each chunk also stages the max-lag halo)
 constexpr int G2_LPW = 8, G2_LAGS_PER_BLOCK = G2_LPW * G2_WARPS;   // the ISF kernel's tiling (below)
 }
 
