@@ -568,3 +568,21 @@ def test_golden_amplitude_sign_quarter_box():
         A = oracle.amplitude(np.array(c["pos"]), np.array(c["f"]), _hkl_q(L, c["hkl"]), L)
         np.testing.assert_allclose(A.real, c["re"], atol=1e-12)
         np.testing.assert_allclose(A.imag, c["im"], atol=1e-12)
+
+
+def test_golden_isf_order_and_pair_count():
+    """Eq.(22)-(23), PAPER.md:212-223: p(t) p*(t + tau) (not p*(t) p(t + tau)), averaged over the T - tau pairs;
+    hand-computed 3-frame, 2-pixel series."""
+    g = _gold("estimators.json")["isf_order_and_pair_count"]
+    A = np.array(g["A_re"]) + 1j * np.array(g["A_im"])
+    F = oracle.isf(A, g["lags"], g["S2"])
+    np.testing.assert_allclose(F.real, g["F_re"], atol=1e-15)
+    np.testing.assert_allclose(F.imag, g["F_im"], atol=1e-15)
+
+
+def test_golden_ewald_orientation():
+    """Eq.(1), PAPER.md:74-77 with reading R4: hand-computed q of off-axis pixels of a 3 x 3 detector (fixes which
+    pixel index runs along x and y, and the sign of each component)."""
+    g = _gold("estimators.json")["ewald_orientation"]
+    q = oracle.ewald_q(g["wavelength"], g["npx"], g["npy"], g["pitch"])
+    np.testing.assert_allclose(q[g["pixels"]], g["q"], atol=1e-15)
