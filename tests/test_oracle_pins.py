@@ -454,7 +454,7 @@ def test_volume_bragg_peaks_and_table1_grid():
 
 
 # ------------------------------------------------------------------ speckle statistics, Eq.(37)-(38)
-@pytest.mark.parametrize("case", ["one_ring_M1", "two_rings_M2_remainder"])
+@pytest.mark.parametrize("case", ["one_ring_M1", "two_rings_M2_remainder", "two_snapshots_per_snapshot_mean"])
 def test_speckle_histogram_worked_examples(case):
     g = _gold("speckle_histogram.json")[case]
     counts, amb = oracle.speckle_histogram(np.array(g["I"]), np.array(g["bins"]), len(g["counts"]), g["M"],

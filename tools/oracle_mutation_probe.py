@@ -10,7 +10,8 @@ import pytest
 sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
 import oracle
 
-MUTATIONS = ["g2", "xsvs", "radial", "amp", "isf_conj", "isf_T", "ewald_sign", "ewald_swap", "lbins_round", "sq_norm"]
+MUTATIONS = ["g2", "xsvs", "radial", "amp", "isf_conj", "isf_T", "ewald_sign", "ewald_swap", "lbins_round", "sq_norm",
+             "ff_s", "lq_scale", "lq_axes", "hist_round", "hist_mean_all", "species_sign", "fft_flip"]
 which = sys.argv[1] if len(sys.argv) > 1 else "all"
 if which == "all":
     bad = []
@@ -81,6 +82,42 @@ elif which == "sq_norm":
     oracle.structure_factor_shells = lambda I, f, N, bins, nb: oracle.shell_mean(I, bins, nb) / float(N)
 elif which == "lattice_q_sign":
     oracle.lattice_q = lambda *a, **k: -o["lattice_q"](*a, **k) * 1.0000001
+elif which == "ff_s":          # form factor in |q| instead of s = |q| / (4 pi)
+    def ff(q, a, b, c):
+        q = np.asarray(q, float); s2 = (q * q).sum(1)
+        return float(c) + sum(float(ai) * np.exp(-float(bi) * s2) for ai, bi in zip(a, b))
+    oracle.form_factor_gaussian = ff
+elif which == "lq_scale":      # q in units of 1/L instead of 2 pi / L
+    oracle.lattice_q = lambda L, *a, **k: o["lattice_q"](L, *a, **k) / (2 * np.pi)
+elif which == "lq_axes":       # pixel index ik * n_h + ih instead of ih * n_k + ik
+    def lq(L, h0, n_h, k0, n_k, **k):
+        q = o["lattice_q"](L, h0, n_h, k0, n_k, **k)
+        return q.reshape(n_h, n_k, 3).transpose(1, 0, 2).reshape(-1, 3)
+    oracle.lattice_q = lq
+elif which == "hist_round":    # nearest-bin instead of floor histogram
+    def sh(I, bins, n_bins, M, n_hist, kappa_max, edge_tol=1e-9):
+        c, a = o["speckle_histogram"](I, bins, n_bins, M, n_hist, kappa_max, edge_tol)
+        return np.roll(c, 1, axis=1), a
+    oracle.speckle_histogram = sh
+elif which == "hist_mean_all": # kappa normalised by the mean over all snapshots, not per snapshot
+    def sh(I, bins, n_bins, M, n_hist, kappa_max, edge_tol=1e-9):
+        I = np.asarray(I, float); S = I.shape[0] // M
+        IM = I[: S * M].reshape(S, M, -1).sum(1)
+        c = np.zeros((n_bins, n_hist), np.int64)
+        for b in range(n_bins):
+            x = IM[:, bins == b]
+            if x.size == 0 or not x.mean() > 0: continue
+            h = np.floor(x / x.mean() * n_hist / kappa_max).astype(int).ravel()
+            for v in h[h < n_hist]: c[b, v] += 1
+        return c, np.zeros((n_bins, n_hist + 1), np.int64)
+    oracle.speckle_histogram = sh
+elif which == "species_sign":  # e^{+iq.r} in the species amplitude
+    def si(pos, species, fq, q, L, amp=False):
+        r = o["species_intensity"](pos, species, fq, q, L, amp=amp)
+        return np.conj(r) if amp else r
+    oracle.species_intensity = si
+elif which == "fft_flip":
+    oracle.fft_intensity = lambda *a, **k: np.flip(o["fft_intensity"](*a, **k), -1)
 else:
     sys.exit(f"unknown mutation {which}")
 sys.exit(pytest.main(["-q", "-x", "-m", "not gpu", "-p", "no:cacheprovider", "tests/test_oracle_pins.py"]))
