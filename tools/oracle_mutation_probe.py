@@ -11,7 +11,8 @@ sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(_
 import oracle
 
 MUTATIONS = ["g2", "xsvs", "radial", "amp", "isf_conj", "isf_T", "ewald_sign", "ewald_swap", "lbins_round", "sq_norm",
-             "ff_s", "lq_scale", "lq_axes", "hist_round", "hist_mean_all", "species_sign", "fft_flip"]
+             "ff_s", "lq_scale", "lq_axes", "hist_round", "hist_mean_all", "species_sign", "fft_flip",
+             "f_squared", "isf_norm"]
 which = sys.argv[1] if len(sys.argv) > 1 else "all"
 if which == "all":
     bad = []
@@ -118,6 +119,14 @@ elif which == "species_sign":  # e^{+iq.r} in the species amplitude
     oracle.species_intensity = si
 elif which == "fft_flip":
     oracle.fft_intensity = lambda *a, **k: np.flip(o["fft_intensity"](*a, **k), -1)
+elif which == "f_squared":     # f_j^2 instead of f_j inside the amplitude (Eq. 7)
+    def amp(pos, f, q, L):
+        return o["amplitude"](pos, None if f is None else np.asarray(f, float) ** 2, q, L)
+    def inten(pos, f, q, L):
+        return o["intensity"](pos, None if f is None else np.asarray(f, float) ** 2, q, L)
+    oracle.amplitude, oracle.intensity = amp, inten
+elif which == "isf_norm":      # ISF normalised by (sum f)^2 instead of sum f^2
+    oracle.isf = lambda A, lags, S2: o["isf"](A, lags, S2 * 2.0)
 else:
     sys.exit(f"unknown mutation {which}")
 sys.exit(pytest.main(["-q", "-x", "-m", "not gpu", "-p", "no:cacheprovider", "tests/test_oracle_pins.py"]))
