@@ -87,3 +87,30 @@ def test_gpu_amplitude_sign_lattice_engines(engine):
     tol = 2e-4 if engine in (xp.ENGINE_TENSOR_I8, xp.ENGINE_AUTO) else 1e-5
     np.testing.assert_allclose(A[:, 0], expect.real, atol=tol)
     np.testing.assert_allclose(A[:, 1], expect.imag, atol=tol)
+
+
+def test_gpu_isf_order_and_pair_count():
+    """Eq.(22)-(23): p(t) p*(t + tau) over the T - tau pairs, hand-computed (estimators.json)."""
+    g = _g("isf_order_and_pair_count")
+    A = torch.stack([torch.tensor(g["A_re"], dtype=torch.float64), torch.tensor(g["A_im"], dtype=torch.float64)], -1)
+    F = xp.xpcs_isf(A.to(DEV).contiguous(), g["lags"], None, N=int(g["S2"])).cpu().numpy()   # f = 1: sum f^2 = N
+    np.testing.assert_allclose(F[..., 0], g["F_re"], atol=1e-15)
+    np.testing.assert_allclose(F[..., 1], g["F_im"], atol=1e-15)
+
+
+def test_gpu_ewald_orientation():
+    """Eq.(1), PAPER.md:74-77 with reading R4: hand-computed q of off-axis pixels of a 3 x 3 detector."""
+    g = _g("ewald_orientation")
+    q = xp.xpcs_qgrid_ewald(g["wavelength"], g["npx"], g["npy"], g["pitch"], out_dtype=xp.F64, device=DEV)
+    np.testing.assert_allclose(q.cpu().numpy()[g["pixels"]], g["q"], atol=1e-14)
+
+
+@pytest.mark.parametrize("case", ["one_ring_M1", "two_rings_M2_remainder", "two_snapshots_per_snapshot_mean"])
+def test_gpu_speckle_histogram_worked_examples(case):
+    """Eq.(37)-(38) statistics: hand-computed histograms (speckle_histogram.json)."""
+    with open(os.path.join(os.path.dirname(__file__), "golden", "speckle_histogram.json")) as fh:
+        g = json.load(fh)[case]
+    I = torch.tensor(g["I"], dtype=torch.float64, device=DEV)
+    bins = torch.tensor(g["bins"], dtype=torch.int32, device=DEV)
+    out = xp.xpcs_speckle_histogram(I, bins, len(g["counts"]), g["M"], g["n_hist"], g["kappa_max"]).cpu().numpy()
+    np.testing.assert_array_equal(out, g["counts"])
