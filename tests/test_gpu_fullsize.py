@@ -43,15 +43,27 @@ def _t(a):
     return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
 
 
-def _run(cfg):
-    """Generate the config's inputs, run the whole pipeline, return (outputs as numpy, positions, f, q, bins)."""
+def _run(cfg, repeat=False):
+    """Generate the config's inputs, run the whole pipeline, return (outputs as numpy, positions, f, q, bins).
+    repeat: run the step a second time on the same inputs and require bit-identical outputs (the deterministic
+    engines, folds and reductions at full size: many frame batches on two streams, every reduction)."""
     pos = xi.positions(cfg)
     f = xi.form_factors(cfg)
     wl = pipeline.workload_from_config(cfg)
     P = pipeline.Pipeline(wl)
     pos_d = _t(pos)
-    out = P.run(pos_d, _t(f) if cfg.two_species else None)
+    f_d = _t(f) if cfg.two_species else None
+    out = P.run(pos_d, f_d)
     torch.cuda.synchronize()
+    if repeat:
+        first = {k: v.clone() for k, v in out.items()}
+        out = P.run(pos_d, f_d)
+        torch.cuda.synchronize()
+        for k, v in out.items():
+            a, b = v, first[k]
+            same = (a == b) | (torch.isnan(a) & torch.isnan(b))
+            assert bool(same.all()), f"{cfg.name}: {k} differs between two runs of the same step"
+        del first
     res = {k: v.cpu().numpy() for k, v in out.items()}
     res["bins"] = P.bins.cpu().numpy()
     del pos_d
@@ -139,7 +151,7 @@ def _g2_numerator_pin(cfg, res, q, lags, shells):
 # ------------------------------------------------------------------------------------------------ configs
 def test_config2_full_size():
     cfg = xi.CONFIGS["c2"]
-    res, pos, f, q, inc = _run(cfg)
+    res, pos, f, q, inc = _run(cfg, repeat=True)
     bins = res["bins"]
     # full plane at frames {0, 49, 99}: per-pixel gate on every pixel and S_b(t) end to end (SURVEY 8(d) subset)
     frames = [0, 49, 99]
@@ -166,7 +178,7 @@ def test_config3_full_size():
     oracle's I on shell 0 (~200 pixels) x all 1000 frames (5e10 pairs, ~2 min on 16 cores): per-pixel gate on 2e5
     pixel-frames, ring g2 and S_b(t) of shell 0 within 1e-4."""
     cfg = xi.CONFIGS["c3"]
-    res, pos, f, q, inc = _run(cfg)
+    res, pos, f, q, inc = _run(cfg, repeat=True)
     bins = res["bins"]
     pix0 = _shell_pixels(bins, [0])
     Ir = _oracle_I(cfg, pos, f, q[pix0])
@@ -212,7 +224,7 @@ def test_config5_full_size():
     discrete Eq.(28) law beta_W = beta0 mean[(W + 2 S_W(x)) / W^2] (1 - 2/n_eff), x = exp(-2 D q^2 dt), on the
     rings with 2 D q^2 dt T >= 20 for W <= 64 (SURVEY 8(c) XSVS pin, A.11)."""
     cfg = xi.CONFIGS["c5"]
-    res, pos, f, q, inc = _run(cfg)
+    res, pos, f, q, inc = _run(cfg, repeat=True)
     bins = res["bins"]
     # end to end: the oracle's I on shells {0, 1} (~800 pixels) x 200 frames (8e10 pairs, ~3 min on 16 cores):
     # per-pixel gate on 1.6e5 pixel-frames and beta of both shells for every window within 1e-4
